@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: RF spectra/sec (fwd+bwd) at 100k Gaussians on B200 (BASELINE.json).
+
+Workload (config 2 of BASELINE.json): the reference perf
+scene cli._bench_scene(default_rng(0), 100_000, 360, 180) rounded to fp32,
+a batch of 64 TX per GPU from the default tx box (cli.py:90), and a fixed
+synthetic upstream lambda (L1 pattern of gradcheck.py:187).
+One step = project + bin + sort + hit lists + psi + composite + backward +
+epilogue (+ NCCL all-reduce of the gradient buffer when N > 1); the loss is
+not part of the step.  Data: synthetic, random-init scene.
+
+  python bench.py [--gpus N --steps K --warmup W]           # this framework
+  python bench.py --impl reference [...]                    # CPU reference arm
+
+The reference arm times the oracle port (oracle/, a C restatement of the
+reference's numba/numpy path) on the host cores: the reference package is
+pure Python, so there is no compiled `oracle/_ref` to run.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "RF spectra/sec (fwd+bwd) at 100k Gaussians, 1/2/4/8 B200; frac of HBM roofline"
+UNIT = "spectra/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--gaussians", type=int, default=100_000)
+    p.add_argument("--batch", type=int, default=64, help="TX per GPU")
+    p.add_argument("--sort", default="hand", choices=["hand", "cub"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=4, help="TX in the bounded CPU-baseline sample")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(n: int, b: int, rank: int, world: int):
+    from paper_2502_01826_b200.scene import bench_scene, default_txs, round_to_f32
+
+    scene = round_to_f32(bench_scene(np.random.default_rng(0), n, 360, 180))
+    txs = default_txs(b * world, seed=1)[rank * b:(rank + 1) * b]
+    return scene, txs
+
+
+# ------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------- algorithmic bytes
+def algo_bytes(n: int, m: int, r: int, b: int) -> dict:
+    """Per-step algorithmic bytes of SURVEY.md §8(d) (fp32/c64 storage)."""
+    return {
+        "project": n * (48 + 96),
+        "bin": n * 32 + m * 12,
+        "sort": m * 24,
+        "ranges": m * 8,
+        "psi": n * 140 + n * b * 8,
+        "forward": m * 68 + n * b * 8 + r * b * 8,
+        "backward": r * b * 8 + m * 68 + n * b * 8 + n * (56 + 8 * b),
+        "epilogue": n * (8 * b + 56 + 168) + n * 176,
+    }
+
+
+def peaks() -> dict:
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_01826_b200 import _native, api, raster
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    scene, txs = workload(args.gaussians, args.batch, rank, world)
+    ds = raster.DeviceScene.from_host(scene, dev)
+    tx = torch.as_tensor(txs, dtype=torch.float32, device=dev)
+    B = tx.shape[0]
+
+    def allreduce(g):
+        if world > 1:
+            flat = torch.cat([g[k].reshape(-1).view(torch.float32) for k in raster.GRAD_FIELDS])
+            dist.all_reduce(flat)
+            o = 0
+            for k in raster.GRAD_FIELDS:
+                v = g[k].reshape(-1).view(torch.float32)
+                v.copy_(flat[o:o + v.numel()])
+                o += v.numel()
+
+    # fixed synthetic upstream: lambda = upstream_to_ray(dL1/dP, S), target 1.3 P + 0.05
+    geo = raster.build_geometry(ds, sort_backend=args.sort)
+    S0 = raster.forward(geo, raster.compute_psi(ds, tx))
+    P0 = S0.abs() ** 2
+    lam = (2.0 * torch.sign(P0 - (1.3 * P0 + 0.05)) / P0[0].numel() * S0).to(torch.complex64).contiguous()
+    M, H = geo.m, geo.total_hits
+    R = geo.n_rays
+    del S0, P0
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(marks=None):
+        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks)
+        psi = raster.compute_psi(ds, tx)
+        raster._mark(marks, "psi")
+        S = raster.forward(g0, psi)
+        raster._mark(marks, "forward")
+        g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks)
+        allreduce(g)
+        raster._mark(marks, "allreduce")
+        return S, g
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    per_step, phases = [], {}
+    launches0 = _native.launch_counter["kernels"]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for _ in range(args.steps):
+        flush.fill_(1)  # evict L2 between steps (outside the timed events)
+        marks = []
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        marks.append(("start", e0))
+        step(marks)
+        torch.cuda.synchronize()
+        per_step.append(marks[0][1].elapsed_time(marks[-1][1]))
+        for (_, a), (name, bb) in zip(marks[:-1], marks[1:]):
+            phases.setdefault(name, []).append(a.elapsed_time(bb))
+    torch.cuda.synchronize()
+    launches = (_native.launch_counter["kernels"] - launches0) // args.steps
+    clk = clocks.stop()
+    t_ms = float(np.sum(per_step))
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    ms_per_step = t_ms / args.steps
+    value = world * B * args.steps / (t_ms / 1e3)
+
+    # roofline of the compositing kernels (SURVEY.md §8(d) bytes / measured time)
+    pk = peaks()
+    ab = algo_bytes(ds.n, M, R, B)
+    ph_ms = {k: float(np.mean(v)) for k, v in phases.items()}
+    kern = {
+        "forward": (ab["forward"], ph_ms.get("forward")),
+        "backward": (ab["backward"], ph_ms.get("backward_rays", 0) + ph_ms.get("backward_hits", 0)),
+    }
+    roof = {}
+    for k, (byts, ms) in kern.items():
+        ach = byts / (ms / 1e3) / 1e9
+        roof[k] = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                   "frac": round(ach / pk["hbm_gbs"], 4), "algo_bytes": byts, "ms": round(ms, 4)}
+    dom = max(kern, key=lambda k: kern[k][1])
+    rl = dict(roof[dom])
+    rl["kernel"] = dom
+    rl["traffic"] = None
+    rl["peak_source"] = pk["source"]
+
+    # ---- end to end through the host-buffer API (pinned H2D / D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hs = api.pinned_host_scene(scene)
+        txh = torch.as_tensor(txs, dtype=torch.float32).pin_memory()
+        lamh = lam.cpu().pin_memory()
+        out = api.alloc_host_outputs(ds.n, ds.coeffs.shape[1], B, 360, 180)
+        red = allreduce if world > 1 else None
+        for _ in range(max(1, args.warmup)):
+            api.fwd_bwd_host(hs, txh, lamh, out, ds.rx, ds.ress_radius, 360, 180, 3, True, args.sort, red)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        es = torch.cuda.Event(enable_timing=True)
+        ee = torch.cuda.Event(enable_timing=True)
+        es.record()
+        for _ in range(args.steps):
+            h2d, d2h = api.fwd_bwd_host(hs, txh, lamh, out, ds.rx, ds.ress_radius, 360, 180, 3, True, args.sort, red)
+        ee.record()
+        torch.cuda.synchronize()
+        te = es.elapsed_time(ee)
+        if world > 1:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": round(world * B * args.steps / (te / 1e3), 2), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(te / args.steps, 4)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(scene, txs[: args.cpu_sample])
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 geometry)", "data": "synthetic",
+            "config": {"workload": "config 2: 100k Gaussians (cli._bench_scene seed 0), 360x180 grid, "
+                                   f"{B} TX per GPU, fwd+bwd step", "gaussians": ds.n, "tx_per_gpu": B,
+                       "global_tx": B * world, "grid": "360x180", "incidences_M": M, "live_hits_H": H,
+                       "sort": args.sort, "parallelism": f"dp{world} (TX-sharded, grads all-reduced)",
+                       "l2": "flushed between steps (256 MB write)"},
+            "roofline": rl, "kernels_roofline": roof, "phase_ms": {k: round(v, 4) for k, v in ph_ms.items()},
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_baseline(scene, txs) -> dict:
+    """The oracle port (C, OpenMP) on the host cores: per TX the reference's
+    behaviour -- rebuild the context (train.py:268), render, backward."""
+    import oracle
+
+    threads = os.cpu_count() or 1
+    oracle.lib()
+    # one warm-up TX (page-in), then the timed sample
+    ctx = oracle.OracleContext(scene, threads)
+    ctx.set_tx(txs[0])
+    t0 = time.perf_counter()
+    for t in txs:
+        ctx = oracle.OracleContext(scene, threads)
+        ctx.set_tx(t)
+        S = ctx.forward()
+        ctx.backward(oracle.l1_upstream(S))
+    dt = time.perf_counter() - t0
+    return {"value": round(len(txs) / dt, 4), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(txs)} TX of config 2 (100k Gaussians, 360x180), context rebuilt per TX, {dt:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+
+    scene, txs = workload(args.gaussians, args.batch, 0, 1)
+    threads = os.cpu_count() or 1
+    oracle.lib()
+
+    def one(t):
+        ctx = oracle.OracleContext(scene, threads)
+        ctx.set_tx(t)
+        S = ctx.forward()
+        ctx.backward(oracle.l1_upstream(S))
+
+    for i in range(args.warmup):
+        one(txs[i % len(txs)])
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        one(txs[i % len(txs)])
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config 2: 100k Gaussians (cli._bench_scene seed 0), 360x180 grid, fwd+bwd, "
+                               "1 TX per step (bounded sample of the 64-TX batch)", "gaussians": args.gaussians,
+                   "grid": "360x180"},
+        "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} TX, context rebuilt per TX (train.py:268)"},
+        "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,148 @@
+/*
+ * rfsplat_b200.h -- C ABI of the B200 (sm_100a) RF-splatting rasterizer.
+ *
+ * Drop-in boundary for the reference package `rfsplat` (pkg/src/rfsplat/).
+ * The reference has no native library: its hot path is numba-compiled Python
+ * called through plain functions over caller-allocated numpy arrays
+ * (_kernels.py:140-559).  The FFI a maintainer would bind (ctypes, see
+ * INTEGRATION.md) is this header: plain device pointers, sizes and a
+ * cudaStream_t passed as void*, integer status codes, no torch types.
+ *
+ * Ownership: the caller allocates every buffer (the Python host layer uses
+ * the torch caching allocator); the library never frees caller memory.
+ * All entry points are stream-ordered and asynchronous unless noted.
+ *
+ * Status codes map onto rfsplat.errors (errors.py:4-40):
+ *   0 OK, 1 GeometryError, 2 ShapeError, 3 ContractViolationError,
+ *   4 NonFiniteGradientError, 5 CUDA failure, 6 capacity exceeded (retry
+ *   with larger scratch).
+ *
+ * Layouts (N Gaussians, B transmitters, R = n_az * n_el rays, r = u*n_el+v):
+ *   means f32[N*3], quats f32[N*4] (w,x,y,z), log_scales f32[N*3],
+ *   trans_mag_raw f32[N], trans_phase f32[N], coeffs complex64[N*K]
+ *   (K = (L+1)^2, index l*l+l+m), rx f64[3], tx f32[B*3],
+ *   S / grad_S complex64[B*R], psi / P complex64[N*B].
+ * Opaque records (sizes below): geom 128 B/Gaussian, sph 16 B/Gaussian,
+ *   rects 16 B/Gaussian, rho32 16 B/Gaussian, hit slab 16 B/(ray*hcap),
+ *   gslab 16 B/(ray*hcap), gacc 64 B/Gaussian.
+ */
+#ifndef RFSPLAT_B200_H
+#define RFSPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RFS_GEOM_BYTES 128
+#define RFS_SPH_BYTES 16
+#define RFS_RECT_BYTES 16
+#define RFS_RHO_BYTES 16
+#define RFS_HIT_BYTES 16
+#define RFS_GSLAB_BYTES 16
+#define RFS_GACC_FLOATS 16
+
+/* K1: per-Gaussian shape, transmittance, projection and tile counts.
+ * Replaces scene.covariances (scene.py:157-161), prepare_context's inverse /
+ * normalizer / rho (render.py:220-227), project_scene (splat.py:212-268),
+ * the rectangle math of _tiles_from_arrays (splat.py:308-328) and the count
+ * pass of expand_tile_rects (_kernels.py:532-541).  proj_out (nullable,
+ * f64[N*6]) receives SceneProjection (center_u, center_v, radius_px,
+ * tile_radius, depth, active).  err_flags bit 1 set => GeometryError. */
+int rfs_project(int n, const float* means, const float* quats, const float* log_scales, const float* trans_mag_raw,
+                const float* trans_phase, const double* rx /* host f64[3] */, double ress_radius, int n_az, int n_el,
+                void* geom, void* sph, uint32_t* depth_code, void* rects, uint32_t* counts, void* rho32,
+                double* proj_out, int* err_flags, void* stream);
+
+/* K2: exclusive warp-shuffle scan of per-Gaussian splat counts -> offsets;
+ * *total (device) = M.  Replaces the implicit cumulative positions of
+ * expand_tile_rects (_kernels.py:533-545).  temp: rfs_scan_temp_elems(n) u32. */
+size_t rfs_scan_temp_elems(int n);
+int rfs_exclusive_scan_u32(const uint32_t* in, int n, uint32_t* out, uint32_t* total, uint32_t* temp, void* stream);
+
+/* K2b: fill (compact key, Gaussian id) pairs in the reference expansion
+ * order (_kernels.py:545-558).  Compact key = tile << 31 | float32 depth
+ * bits; rfs_expand_keys restores the reference key tile << 32 | bits. */
+int rfs_bin_fill(int n, const void* rects, const uint32_t* depth_code, const uint32_t* offsets, int n_az,
+                 uint64_t* ckeys, uint32_t* vals, void* stream);
+int rfs_expand_keys(const uint64_t* ckeys, int m, uint64_t* keys, void* stream);
+
+/* K3: stable LSD radix sort of (u64 key, u32 value) on bits [0, end_bit).
+ * Replaces np.argsort(keys, kind="stable") (splat.py:337).  Hand-written
+ * onesweep passes; the _cub variant calls cub::DeviceRadixSort::SortPairs for
+ * comparison.  *result_in_alt (host) = 1 if the sorted data is in *_alt. */
+size_t rfs_sort_temp_bytes(int m, int end_bit);
+int rfs_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int m, int end_bit,
+                       void* temp, size_t temp_bytes, int* result_in_alt, void* stream);
+size_t rfs_sort_cub_temp_bytes(int m, int end_bit);
+int rfs_sort_pairs_u64_cub(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int m, int end_bit,
+                           void* temp, size_t temp_bytes, int* result_in_alt, void* stream);
+
+/* K4: per-tile [start, end) ranges = searchsorted left/right of each tile id
+ * (splat.py:340-343); ranges is int32[n_tiles*2]. */
+int rfs_tile_ranges(const uint64_t* ckeys, int m, int n_tiles, int* ranges, void* stream);
+
+/* K4b: per-incidence emission bound for the exact streaming re-sort:
+ * lb[i] = min_{j >= i, same tile} (depth_j - r3_j). */
+int rfs_lower_bounds(const int* ranges, int n_tiles, const uint32_t* vals, const void* geom, double* lb, void* stream);
+
+/* K6: TX-independent live hit lists.  Replaces _collect_hits + the live walk
+ * of forward_tiled / count_hits_tiled (_kernels.py:27-112, 140-192, 237-292).
+ * Writes hits of ray r to slab[r*hcap ...], counts[r] = live count.
+ * stats (device int[8]): [0] rays needing rfs_hits_slow (listed in
+ * slow_list), [1] rays with live > hcap (caller must retry with larger
+ * hcap), [2] max live, [3] total live hits, [4] longest tile list. */
+int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* geom,
+             const double* rx /* host */, double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts,
+             int* slow_list, int* stats, void* stream);
+int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
+                  const void* sph, const void* geom, const double* rx, double ress_radius, int n_az, int n_el,
+                  int hcap, void* slab, int* counts, double* pend_t, uint32_t* pend_g, float* pend_w, int pcap,
+                  int* stats, void* stream);
+
+/* K5: psi[g][b] = sum_k coeffs[g][k] * basis_k(bearing of tx_b from mu_g).
+ * Replaces render.py:229-238 + fle.fle_basis_with_derivs (fle.py:153-212). */
+int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, void* psi,
+            void* stream);
+
+/* K7: S[b][r] = sum over live hits of w * T * psi[g][b].  Replaces the
+ * composite of forward_tiled (_kernels.py:184-192) for a TX batch. */
+int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, int n_tx, int n_rays, void* S,
+                void* stream);
+
+/* K8a: TX-batched reverse sweep (_ray_backward's complex part,
+ * _kernels.py:369-387, 522).  Accumulates P[g][b] += conj(lam) w T (the
+ * reference's inc_pg bincount, grad.py:252-254) and per-hit TX-reduced
+ * scalars into gslab (+=).  n_tx <= 256 per call; P and gslab must be zeroed
+ * before the first call of a step. */
+int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam,
+                      const void* rho32, int n_tx, int n_rays, void* P, void* gslab, void* stream);
+
+/* K8b: per-hit mean / covariance chains in fp64 (_kernels.py:389-520),
+ * reduced per Gaussian into gacc[g][16] = {dmu[3], d|rho|, dcov[9], dphase}.
+ * gacc must be zeroed before the call. */
+int rfs_backward_hits(const void* slab, const int* counts, int hcap, const void* gslab, const void* geom,
+                      const double* rx /* host */, double ress_radius, int n_az, int n_el, float* gacc, void* stream);
+
+/* K9: per-Gaussian epilogue: d_coeffs = conj(P) conj(basis) (grad.py:255),
+ * bearing chain into d_mean (grad.py:167-189), chain_cov_to_shape
+ * (grad.py:134-164) and d_trans_mag_raw = d|rho| sigma(1-sigma)
+ * (train.py:161-162).  d_cov is nullable.  accumulate = 0 writes every output
+ * (first TX chunk of a step); accumulate = 1 adds only the TX-dependent
+ * terms (d_coeffs, bearing chain) of a further chunk. */
+int rfs_grad_epilogue(int n, int n_tx, int degree, const float* means, const float* quats, const float* log_scales,
+                      const float* trans_mag_raw, const void* coeffs, const float* tx, const void* P, const float* gacc,
+                      int include_direction_chain, int accumulate, float* d_mean, float* d_quat, float* d_log_scale,
+                      float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, void* d_coeffs, float* d_cov,
+                      void* stream);
+
+/* Library / build identification. */
+int rfs_version(void);
+int rfs_device_arch(void); /* compute capability the library was built for, e.g. 100 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RFSPLAT_B200_H */

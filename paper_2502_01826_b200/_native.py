@@ -1,0 +1,91 @@
+"""ctypes binding of the sm_100a library (include/rfsplat_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every entry point raises NativeLibraryError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import NativeLibraryError, raise_for_status
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "librfsplat_b200.so")
+_lock = threading.Lock()
+_lib = None
+
+vp = C.c_void_p
+i32 = C.c_int
+f64 = C.c_double
+sz = C.c_size_t
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "rfs_project": (i32, [i32, vp, vp, vp, vp, vp, vp, f64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "rfs_scan_temp_elems": (sz, [i32]),
+    "rfs_exclusive_scan_u32": (i32, [vp, i32, vp, vp, vp, vp]),
+    "rfs_bin_fill": (i32, [i32, vp, vp, vp, i32, vp, vp, vp]),
+    "rfs_expand_keys": (i32, [vp, i32, vp, vp]),
+    "rfs_sort_temp_bytes": (sz, [i32, i32]),
+    "rfs_sort_pairs_u64": (i32, [vp, vp, vp, vp, i32, i32, vp, sz, C.POINTER(i32), vp]),
+    "rfs_sort_cub_temp_bytes": (sz, [i32, i32]),
+    "rfs_sort_pairs_u64_cub": (i32, [vp, vp, vp, vp, i32, i32, vp, sz, C.POINTER(i32), vp]),
+    "rfs_tile_ranges": (i32, [vp, i32, i32, vp, vp]),
+    "rfs_lower_bounds": (i32, [vp, i32, vp, vp, vp, vp]),
+    "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, f64, i32, i32, i32, vp, vp, vp, vp, vp]),
+    "rfs_hits_slow": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp]),
+    "rfs_psi": (i32, [i32, i32, i32, vp, vp, vp, vp, vp]),
+    "rfs_forward": (i32, [vp, vp, i32, vp, i32, i32, vp, vp]),
+    "rfs_backward_rays": (i32, [vp, vp, i32, vp, vp, vp, i32, i32, vp, vp, vp]),
+    "rfs_backward_hits": (i32, [vp, vp, i32, vp, vp, vp, f64, i32, i32, vp, vp]),
+    "rfs_grad_epilogue": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32,
+                                vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "rfs_version": (i32, []),
+    "rfs_device_arch": (i32, []),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def load(require_cuda: bool = True):
+    """Load (once) and return the ctypes library handle."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeLibraryError(
+                    f"{LIB_PATH} is missing; run `python -m paper_2502_01826_b200.build` (no CPU fallback)"
+                )
+            try:
+                lib = C.CDLL(LIB_PATH)
+            except OSError as e:  # pragma: no cover - environment specific
+                raise NativeLibraryError(f"cannot load {LIB_PATH}: {e}") from e
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    if require_cuda:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise NativeLibraryError("no CUDA device visible: the rasterizer runs only on sm_100a GPUs")
+    return _lib
+
+
+# kernels launched per entry-point call (sort: 2 + passes, added by raster.sort_pairs)
+KERNELS_PER_CALL = {
+    "rfs_project": 1, "rfs_exclusive_scan_u32": 3, "rfs_bin_fill": 1, "rfs_expand_keys": 1,
+    "rfs_tile_ranges": 1, "rfs_lower_bounds": 1, "rfs_hits": 2, "rfs_hits_slow": 1, "rfs_psi": 1,
+    "rfs_forward": 1, "rfs_backward_rays": 1, "rfs_backward_hits": 1, "rfs_grad_epilogue": 1,
+}
+launch_counter = {"kernels": 0}
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(load(), name)(*args)
+    raise_for_status(int(rc), name)
+    launch_counter["kernels"] += KERNELS_PER_CALL.get(name, 0)

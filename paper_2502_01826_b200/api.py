@@ -1,0 +1,251 @@
+"""Reference-shaped entry points (drop-in for rfsplat's render / grad / splat).
+
+These mirror the reference's plain-function API over host numpy scenes so a
+caller of `rfsplat` can switch by changing the import:
+
+    render.render_complex_frame(scene, tx, workers, tiled, ctx)  render.py:282-289
+    render.render_spectrum / render_scalar                        render.py:292-307
+    grad.backward_frame(scene, tx, upstream, workers, include_direction_chain, ctx)
+                                                                  grad.py:192-259
+    splat.build_tiles_for_render(scene, proj) -> TileIndex        splat.py:374-380
+    splat.project_scene(scene) -> SceneProjection                 splat.py:212-268
+
+`workers` and `tiled` are accepted and ignored (the GPU path is always
+tiled and stream-ordered).  Batched variants take a TX batch [B, 3] and share
+the transmitter-independent geometry across it.
+Results come back as float64 / complex128 numpy arrays in the reference
+layouts; the arithmetic is fp32 (geometry fp64).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import raster
+from .errors import ContractViolationError, ShapeError
+from .scene import HostScene
+
+__all__ = [
+    "GradientBuffer", "TileIndex", "SceneProjection", "RenderContextGPU",
+    "prepare_context", "render_complex_frame", "render_complex_frames", "render_spectrum", "render_scalar",
+    "backward_frame", "backward_frames", "upstream_to_ray", "build_tiles_for_render", "project_scene",
+]
+
+
+@dataclass
+class TileIndex:
+    """splat.TileIndex (splat.py:82-101)."""
+
+    n_az: int
+    n_el: int
+    tiles_u: int
+    tiles_v: int
+    keys: np.ndarray
+    indices: np.ndarray
+    ranges: np.ndarray
+
+    @property
+    def n_tiles(self) -> int:
+        return self.tiles_u * self.tiles_v
+
+
+@dataclass
+class SceneProjection:
+    """splat.SceneProjection (splat.py:104-118)."""
+
+    active: np.ndarray
+    center_u: np.ndarray
+    center_v: np.ndarray
+    radius_px: np.ndarray
+    tile_radius: np.ndarray
+    depth: np.ndarray
+
+
+@dataclass
+class GradientBuffer:
+    """grad.GradientBuffer (grad.py:55-101) with float64 host arrays."""
+
+    d_mean: np.ndarray
+    d_quat: np.ndarray
+    d_log_scale: np.ndarray
+    d_trans_mag: np.ndarray
+    d_trans_phase: np.ndarray
+    d_coeffs: np.ndarray
+    d_cov: np.ndarray
+
+    def add(self, other: "GradientBuffer") -> None:
+        for k in ("d_mean", "d_quat", "d_log_scale", "d_trans_mag", "d_trans_phase", "d_coeffs", "d_cov"):
+            setattr(self, k, getattr(self, k) + getattr(other, k))
+
+    def all_finite(self) -> bool:
+        return all(np.all(np.isfinite(getattr(self, k))) for k in
+                   ("d_mean", "d_quat", "d_log_scale", "d_trans_mag", "d_trans_phase", "d_coeffs", "d_cov"))
+
+    @classmethod
+    def from_device(cls, g: dict) -> "GradientBuffer":
+        h = lambda t: t.detach().cpu().numpy()
+        return cls(
+            h(g["d_mean"]).astype(np.float64), h(g["d_quat"]).astype(np.float64),
+            h(g["d_log_scale"]).astype(np.float64), h(g["d_trans_mag"]).astype(np.float64),
+            h(g["d_trans_phase"]).astype(np.float64), h(g["d_coeffs"]).astype(np.complex128),
+            h(g["d_cov"]).astype(np.float64),
+        )
+
+
+@dataclass
+class RenderContextGPU:
+    """Device analogue of render.RenderContext (render.py:191-214): the
+    transmitter-independent geometry of a scene, reusable across TX."""
+
+    scene: raster.DeviceScene
+    geometry: raster.Geometry
+
+
+def _device_scene(scene) -> raster.DeviceScene:
+    if isinstance(scene, raster.DeviceScene):
+        return scene
+    return raster.DeviceScene.from_host(HostScene.from_any(scene))
+
+
+def prepare_context(scene, tx=None, want_proj: bool = False, sort_backend: str = "hand") -> RenderContextGPU:
+    ds = _device_scene(scene)
+    return RenderContextGPU(ds, raster.build_geometry(ds, sort_backend=sort_backend, want_proj=want_proj))
+
+
+def _tx_tensor(tx, dev) -> torch.Tensor:
+    t = torch.as_tensor(np.asarray(tx, dtype=np.float32), device=dev)
+    return t.reshape(-1, 3)
+
+
+def render_complex_frames(scene, txs, ctx: RenderContextGPU | None = None) -> np.ndarray:
+    """Complex frames for a TX batch, shape (B, n_az, n_el)."""
+    ctx = ctx or prepare_context(scene)
+    tx = _tx_tensor(txs, ctx.scene.means.device)
+    psi = raster.compute_psi(ctx.scene, tx)
+    return raster.forward(ctx.geometry, psi).cpu().numpy().astype(np.complex128)
+
+
+def render_complex_frame(scene, tx, workers: int = 1, tiled: bool = True,
+                         ctx: RenderContextGPU | None = None) -> np.ndarray:
+    """render.render_complex_frame (render.py:282-289)."""
+    return render_complex_frames(scene, np.asarray(tx, dtype=np.float64).reshape(1, 3), ctx)[0]
+
+
+def render_spectrum(scene, tx, workers: int = 1, ctx: RenderContextGPU | None = None) -> np.ndarray:
+    """render.render_spectrum (render.py:292-298): |S|^2."""
+    return np.abs(render_complex_frame(scene, tx, workers, ctx=ctx)) ** 2
+
+
+def render_scalar(scene, tx, workers: int = 1, ctx: RenderContextGPU | None = None) -> complex:
+    """render.render_scalar (render.py:301-307): coherent sum over rays."""
+    return complex(render_complex_frame(scene, tx, workers, ctx=ctx).sum())
+
+
+def upstream_to_ray(dL_dpower, s_frame) -> np.ndarray:
+    """grad.upstream_to_ray (grad.py:104-120)."""
+    if s_frame is None:
+        raise ContractViolationError("forward complex frame was not cached")
+    dL_dpower = np.asarray(dL_dpower, dtype=np.float64)
+    s_frame = np.asarray(s_frame, dtype=np.complex128)
+    if dL_dpower.shape != s_frame.shape:
+        raise ContractViolationError("gradient frame and forward frame shapes differ")
+    return 2.0 * dL_dpower * s_frame
+
+
+def backward_frames(scene, txs, upstreams, include_direction_chain: bool = True,
+                    ctx: RenderContextGPU | None = None) -> GradientBuffer:
+    """Gradients summed over a TX batch (GradientBuffer.add semantics, grad.py:85-92)."""
+    ctx = ctx or prepare_context(scene)
+    dev = ctx.scene.means.device
+    tx = _tx_tensor(txs, dev)
+    up = np.asarray(upstreams, dtype=np.complex64)
+    if up.ndim == 2:
+        up = up[None]
+    if up.shape != (tx.shape[0], ctx.geometry.n_az, ctx.geometry.n_el):
+        raise ShapeError("upstream frame shape does not match the scene grid")
+    g = raster.backward(ctx.scene, ctx.geometry, tx, torch.as_tensor(up, device=dev), include_direction_chain)
+    return GradientBuffer.from_device(g)
+
+
+def backward_frame(scene, tx, upstream, workers: int = 1, include_direction_chain: bool = True,
+                   ctx: RenderContextGPU | None = None) -> GradientBuffer:
+    """grad.backward_frame (grad.py:192-259)."""
+    upstream = np.asarray(upstream)
+    if upstream.ndim != 2:
+        raise ShapeError("upstream frame shape does not match the scene grid")
+    return backward_frames(scene, np.asarray(tx, dtype=np.float64).reshape(1, 3), upstream[None],
+                           include_direction_chain, ctx)
+
+
+SCENE_FIELDS = ("means", "quats", "log_scales", "trans_mag_raw", "trans_phase", "coeffs")
+OUT_GRADS = ("d_mean", "d_quat", "d_log_scale", "d_trans_mag", "d_trans_mag_raw", "d_trans_phase", "d_coeffs",
+             "d_cov")
+
+
+def pinned_host_scene(scene) -> dict:
+    """fp32 / complex64 pinned host copies of a scene's parameters."""
+    s = HostScene.from_any(scene)
+    f = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()
+    return {"means": f(s.means, np.float32), "quats": f(s.quats, np.float32), "log_scales": f(s.log_scales, np.float32),
+            "trans_mag_raw": f(s.trans_mag_raw, np.float32), "trans_phase": f(s.trans_phase, np.float32),
+            "coeffs": f(s.coeffs, np.complex64)}
+
+
+def alloc_host_outputs(n: int, k: int, b: int, n_az: int, n_el: int) -> dict:
+    z = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory()
+    return {"S": z((b, n_az, n_el), torch.complex64), "d_mean": z((n, 3), torch.float32),
+            "d_quat": z((n, 4), torch.float32), "d_log_scale": z((n, 3), torch.float32),
+            "d_trans_mag": z((n,), torch.float32), "d_trans_mag_raw": z((n,), torch.float32),
+            "d_trans_phase": z((n,), torch.float32), "d_coeffs": z((n, k), torch.complex64),
+            "d_cov": z((n, 3, 3), torch.float32)}
+
+
+def fwd_bwd_host(host_scene: dict, tx_host: torch.Tensor, lam_host: torch.Tensor, out: dict, rx, ress_radius: float,
+                 n_az: int, n_el: int, fle_degree: int = 3, include_direction_chain: bool = True,
+                 sort_backend: str = "hand", reduce_fn=None) -> tuple:
+    """One fwd+bwd step from HOST (pinned) buffers to HOST buffers.
+
+    The drop-in for a caller holding the scene and upstream frames on the
+    host, i.e. render_complex_frame + backward_frame of the reference
+    (render.py:282-289, grad.py:192-259) for a TX batch.  Copies are
+    stream-ordered (non_blocking); the caller synchronizes.  `reduce_fn`
+    (optional) all-reduces the device gradient dict before the D2H copy.
+    Returns (h2d_bytes, d2h_bytes).
+    """
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d = {k: host_scene[k].to(dev, non_blocking=True) for k in SCENE_FIELDS}
+    ds = raster.DeviceScene(d["means"], d["quats"], d["log_scales"], d["trans_mag_raw"], d["trans_phase"],
+                            d["coeffs"], tuple(float(x) for x in rx), float(ress_radius), n_az, n_el, fle_degree)
+    tx = tx_host.to(dev, non_blocking=True)
+    lam = lam_host.to(dev, non_blocking=True)
+    geo = raster.build_geometry(ds, sort_backend=sort_backend)
+    psi = raster.compute_psi(ds, tx)
+    S = raster.forward(geo, psi)
+    g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=psi)
+    if reduce_fn is not None:
+        reduce_fn(g)
+    out["S"].copy_(S, non_blocking=True)
+    for k in OUT_GRADS:
+        out[k].copy_(g[k], non_blocking=True)
+    h2d = sum(host_scene[k].numel() * host_scene[k].element_size() for k in SCENE_FIELDS)
+    h2d += tx_host.numel() * tx_host.element_size() + lam_host.numel() * lam_host.element_size()
+    d2h = sum(out[k].numel() * out[k].element_size() for k in ("S",) + OUT_GRADS)
+    return h2d, d2h
+
+
+def build_tiles_for_render(scene, proj=None, sort_backend: str = "hand") -> TileIndex:
+    """splat.build_tiles_for_render (splat.py:374-380), bit-exact TileIndex."""
+    ctx = prepare_context(scene, sort_backend=sort_backend)
+    g = ctx.geometry
+    keys, idx, rg = raster.tile_index_host(g)
+    return TileIndex(g.n_az, g.n_el, g.tiles_u, g.tiles_v, keys, idx, rg)
+
+
+def project_scene(scene) -> SceneProjection:
+    """splat.project_scene (splat.py:212-268)."""
+    ctx = prepare_context(scene, want_proj=True)
+    p = ctx.geometry.proj.cpu().numpy()[: ctx.scene.n]
+    return SceneProjection(p[:, 5] > 0.5, p[:, 0], p[:, 1], p[:, 2], p[:, 3], p[:, 4])

@@ -1,0 +1,451 @@
+// project.cu -- K1 projection, K2 tile binning (count, warp-scan, fill),
+// K4 tile ranges and the per-incidence emission bound.
+//
+// Compiled with -fmad=false: the tile index must be bit-exact with the
+// reference, so every fp64 expression that feeds a floor() or the depth key
+// is evaluated with the same roundings as numpy (no FMA contraction).
+#include "rfs_common.cuh"
+
+namespace {
+
+struct __align__(16) Rect {
+    short s1_lo, s1_hi, s2_hi, tv_lo, tv_hi, pad0, pad1, pad2;
+};
+
+__device__ __forceinline__ long long floordiv_ll(long long a, long long b) {
+    long long q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) q -= 1;
+    return q;
+}
+__device__ __forceinline__ double clampd(double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); }
+// numpy float remainder: sign follows the divisor (npy_divmod)
+__device__ __forceinline__ double py_fmod(double a, double b) {
+    double m = fmod(a, b);
+    if (m != 0.0) {
+        if ((b < 0.0) != (m < 0.0)) m += b;
+    } else {
+        m = copysign(0.0, b);
+    }
+    return m;
+}
+
+// Tile rectangle of one splat: splat.py:308-328 (integer logic restated).
+__device__ Rect splat_rect(double cu, double cv, double radius, int n_az, int n_el, int tiles_u) {
+    Rect r;
+    double flo = floor(cv - radius), fhi = floor(cv + radius);
+    long long v_lo = (long long)flo, v_hi = (long long)fhi;
+    v_lo = v_lo < 0 ? 0 : (v_lo > n_el - 1 ? n_el - 1 : v_lo);
+    v_hi = v_hi < -1 ? -1 : (v_hi > n_el - 1 ? n_el - 1 : v_hi);
+    bool off_grid = (fhi < 0.0) || (flo > (double)(n_el - 1));
+    long long tv_lo = floordiv_ll(v_lo, RFS_TILE);
+    long long tv_hi = off_grid ? -1 : floordiv_ll(v_hi, RFS_TILE);
+    long long u_lo = (long long)floor(cu - radius), u_hi = (long long)floor(cu + radius);
+    bool span_all = (u_hi - u_lo + 1) >= n_az;
+    long long a = u_lo - floordiv_ll(u_lo, n_az) * n_az;
+    long long b = a + (u_hi - u_lo);
+    bool wrap = b > n_az - 1;
+    long long s1_lo = floordiv_ll(a, RFS_TILE);
+    long long s1_hi = wrap ? tiles_u - 1 : floordiv_ll(b < n_az - 1 ? b : n_az - 1, RFS_TILE);
+    long long s2_hi = wrap ? floordiv_ll(b - n_az, RFS_TILE) : -1;
+    bool full = span_all || (wrap && (s2_hi >= s1_lo));
+    if (full) { s1_lo = 0; s1_hi = tiles_u - 1; s2_hi = -1; }
+    r.s1_lo = (short)s1_lo; r.s1_hi = (short)s1_hi; r.s2_hi = (short)s2_hi;
+    r.tv_lo = (short)tv_lo; r.tv_hi = (short)tv_hi;
+    r.pad0 = r.pad1 = r.pad2 = 0;
+    return r;
+}
+
+// K1: one thread per Gaussian.  prepare_context's shape part (render.py:220-227,
+// scene.py:118-161), project_scene (splat.py:212-268) and the count pass of
+// expand_tile_rects (_kernels.py:532-541), all fp64.
+__global__ void __launch_bounds__(256) k_project(
+    int n, const float* __restrict__ means, const float* __restrict__ quats,
+    const float* __restrict__ log_scales, const float* __restrict__ raw, const float* __restrict__ phase,
+    double rx0, double rx1, double rx2, double ress, int n_az, int n_el, int tiles_u,
+    RfsGeom* __restrict__ geom, float4* __restrict__ sph, uint32_t* __restrict__ code,
+    Rect* __restrict__ rects, uint32_t* __restrict__ counts, float4* __restrict__ rho32,
+    double* __restrict__ proj, int* __restrict__ err) {
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    double mx = (double)means[3 * g], my = (double)means[3 * g + 1], mz = (double)means[3 * g + 2];
+    double qw = quats[4 * g], qx = quats[4 * g + 1], qy = quats[4 * g + 2], qz = quats[4 * g + 3];
+    double s0 = log_scales[3 * g], s1 = log_scales[3 * g + 1], s2 = log_scales[3 * g + 2];
+
+    // rotation from the normalized quaternion (scene.py:118-142)
+    double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    double w = qw / qn, x = qx / qn, y = qy / qn, z = qz / qn;
+    double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                   2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                   2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    double e0 = exp(2.0 * s0), e1 = exp(2.0 * s1), e2 = exp(2.0 * s2);
+    double ie[3] = {1.0 / e0, 1.0 / e1, 1.0 / e2};
+    // Sigma^-1 = R diag(e^{-2s}) R^T: symmetric by construction (reference
+    // inverts then symmetrizes, render.py:221-222; agreement ~1e-16 rel)
+    double I[6];
+    {
+        int ij[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            int i = ij[k][0], j = ij[k][1];
+            I[k] = R[3 * i] * ie[0] * R[3 * j] + R[3 * i + 1] * ie[1] * R[3 * j + 1] + R[3 * i + 2] * ie[2] * R[3 * j + 2];
+        }
+    }
+    RfsGeom G;
+    G.mu[0] = mx; G.mu[1] = my; G.mu[2] = mz;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) G.inv[k] = I[k];
+    G.norm = RFS_GAUSS_NORM * exp(-(s0 + s1 + s2)); // (2pi)^-1.5 / sqrt(det Sigma)
+    double mag = 1.0 / (1.0 + exp(-(double)raw[g]));
+    double ph = (double)phase[g];
+    double sp, cp;
+    sincos(ph, &sp, &cp);
+    G.rho_re = mag * cp;
+    G.rho_im = mag * sp;
+    rho32[g] = make_float4((float)G.rho_re, (float)G.rho_im, (float)cp, (float)sp);
+
+    // projection onto the grid (splat.py:223-234)
+    double ox = mx - rx0, oy = my - rx1, oz = mz - rx2;
+    double depth = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(ox, ox), __dmul_rn(oy, oy)), __dmul_rn(oz, oz)));
+    if (depth < 1e-9) atomicOr(err, 1 << RFS_ERR_GEOMETRY);
+    bool active = depth >= ress;
+    double cell = 360.0 / (double)n_az;
+    double cover_all = (double)(n_az + n_el);
+    double alpha = py_fmod(atan2(oy, ox), RFS_TWO_PI);
+    double beta = RFS_PI / 2.0 - acos(clampd(oz / depth, -1.0, 1.0));
+    double cu = alpha * RFS_RAD2DEG / cell;
+    double cv = (beta * RFS_RAD2DEG + 90.0) / cell;
+    G.cu = cu;
+    G.cv = cv;
+
+    // conservative incidence radius (splat.py:256-267); lambda_max = max e^{2s}
+    double lam3 = fmax(fmax(e0, e1), e2);
+    double r3 = 3.0 * sqrt(lam3);
+    bool inside = depth <= r3;
+    double rho2 = ox * ox + oy * oy;
+    double pd = 1e-12 * depth;
+    bool polar = rho2 <= pd * pd;
+    double theta = asin(clampd(r3 / depth, 0.0, 1.0));
+    double ca = cos(beta - theta), cb = cos(beta + theta);
+    double cos_lo = ca < cb ? ca : cb;
+    double st = sin(theta);
+    bool pole_touch = cos_lo <= st;
+    double az_extent = asin(clampd(st / (pole_touch ? 1.0 : cos_lo), 0.0, 1.0));
+    double extent = pole_touch ? RFS_PI : (theta > az_extent ? theta : az_extent);
+    double tr = extent * RFS_RAD2DEG / cell + 2.0;
+    if (tr > cover_all) tr = cover_all;
+    if (inside || polar) tr = cover_all;
+    G.r2 = active ? tr * tr : -1.0;
+    // any hit's chord midpoint lies inside the 3-sigma ball, so
+    // t_mid >= depth - r3; widen by 1e-9 relative to absorb round-off
+    G.lbv = (depth - r3) - 1e-9 * (depth + r3);
+    geom[g] = G;
+
+    // fp32 bounding-sphere prefilter: accept if |(mu-rx) x d|^2 <= thr.
+    // Margin 1e-6 |mu-rx| + 1e-6 relative covers fp32 rounding of the cross
+    // product (~6 ulp) with a 2x safety factor; see DESIGN.md §4 (K6).
+    double om = depth;
+    double thr = (r3 + 1e-6 * om) * (1.0 + 1e-6);
+    thr = thr * thr;
+    sph[g] = make_float4((float)ox, (float)oy, (float)oz, __double2float_ru(thr));
+
+    float fd = __double2float_rn(depth);
+    code[g] = __float_as_uint(fd);
+
+    Rect rc = splat_rect(cu, cv, tr, n_az, n_el, tiles_u);
+    uint32_t cnt = 0;
+    if (active) {
+        long long nv = (long long)rc.tv_hi - rc.tv_lo + 1;
+        if (nv > 0) {
+            long long nu = (long long)rc.s1_hi - rc.s1_lo + 1;
+            if (rc.s2_hi >= 0) nu += rc.s2_hi + 1;
+            cnt = (uint32_t)(nv * nu);
+        }
+    }
+    if (!active) rc.tv_hi = -1;
+    rects[g] = rc;
+    counts[g] = cnt;
+
+    if (proj) {
+        // linearized radius of J Sigma J^T (splat.py:236-254), API parity only
+        double Sg[9];
+        double ev[3] = {e0, e1, e2};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                Sg[3 * i + k] = R[3 * i] * ev[0] * R[3 * k] + R[3 * i + 1] * ev[1] * R[3 * k + 1] + R[3 * i + 2] * ev[2] * R[3 * k + 2];
+        double r2s = rho2 + oz * oz;
+        double rho_s = sqrt(polar ? 1.0 : rho2);
+        double scale = RFS_RAD2DEG / cell;
+        double rc2 = rho2 < 1e-300 ? 1e-300 : rho2;
+        double J[6] = {-oy / rc2 * scale, ox / rc2 * scale, 0.0,
+                       -oz * ox / (rho_s * r2s) * scale, -oz * oy / (rho_s * r2s) * scale, rho_s / r2s * scale};
+        double c2[4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int l = 0; l < 2; ++l) {
+                double acc = 0.0;
+                for (int j = 0; j < 3; ++j)
+                    for (int k = 0; k < 3; ++k) acc += J[3 * i + j] * Sg[3 * j + k] * J[3 * l + k];
+                c2[2 * i + l] = acc;
+            }
+        double half_tr = 0.5 * (c2[0] + c2[3]);
+        double det2 = c2[0] * c2[3] - c2[1] * c2[2];
+        double dsc = half_tr * half_tr - det2;
+        double lmax = half_tr + sqrt(dsc > 0.0 ? dsc : 0.0);
+        double rpx = polar ? cover_all : 3.0 * sqrt(lmax > 0.0 ? lmax : 0.0);
+        proj[6 * g + 0] = cu;
+        proj[6 * g + 1] = cv;
+        proj[6 * g + 2] = rpx;
+        proj[6 * g + 3] = tr;
+        proj[6 * g + 4] = depth;
+        proj[6 * g + 5] = active ? 1.0 : 0.0;
+    }
+}
+
+// ---- K2: exclusive scan of per-Gaussian splat counts (warp-shuffle scan) ----
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+    int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// block-wide exclusive scan of one value per thread; returns the block total
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t& excl) {
+    __shared__ uint32_t warp_tot[32];
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t inc = warp_incl_scan(v);
+    if (lane == 31) warp_tot[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int nw = blockDim.x >> 5;
+        uint32_t t = lane < nw ? warp_tot[lane] : 0;
+        uint32_t ti = warp_incl_scan(t);
+        if (lane < nw) warp_tot[lane] = ti - t;
+        if (lane == nw - 1) warp_tot[31] = ti;
+    }
+    __syncthreads();
+    excl = warp_tot[wid] + inc - v;
+    uint32_t total = warp_tot[31];
+    __syncthreads();
+    return total;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(const uint32_t* __restrict__ in, int n, uint32_t* __restrict__ part) {
+    long long base = (long long)blockIdx.x * SCAN_TILE;
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        long long j = base + (long long)i * SCAN_THREADS + threadIdx.x;
+        if (j < n) s += in[j];
+    }
+    uint32_t ex;
+    uint32_t tot = block_excl_scan(s, ex);
+    if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_top(uint32_t* __restrict__ part, int nparts, uint32_t* __restrict__ total_out) {
+    // single block; nparts <= SCAN_THREADS * SCAN_ITEMS
+    uint32_t v[SCAN_ITEMS];
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        int j = threadIdx.x * SCAN_ITEMS + i;
+        v[i] = j < nparts ? part[j] : 0;
+        s += v[i];
+    }
+    uint32_t ex;
+    uint32_t tot = block_excl_scan(s, ex);
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        int j = threadIdx.x * SCAN_ITEMS + i;
+        if (j < nparts) part[j] = ex;
+        ex += v[i];
+    }
+    if (threadIdx.x == 0) *total_out = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const uint32_t* __restrict__ in, int n, const uint32_t* __restrict__ part,
+                                                             uint32_t* __restrict__ out) {
+    // blocked arrangement: thread t owns SCAN_ITEMS consecutive elements
+    long long base = (long long)blockIdx.x * SCAN_TILE + (long long)threadIdx.x * SCAN_ITEMS;
+    uint32_t v[SCAN_ITEMS];
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        long long j = base + i;
+        v[i] = j < n ? in[j] : 0;
+        s += v[i];
+    }
+    uint32_t ex;
+    block_excl_scan(s, ex);
+    ex += part[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        long long j = base + i;
+        if (j < n) out[j] = ex;
+        ex += v[i];
+    }
+}
+
+// K2b: fill (compact key, Gaussian id) pairs in expand_tile_rects order
+// (_kernels.py:545-558): per splat, tv ascending, s1 tiles then s2 tiles.
+// Compact key = tile << 31 | depth_code (the code's sign bit is always 0),
+// so the radix sort needs 31 + ceil(log2 tiles) bits.
+__global__ void __launch_bounds__(256) k_fill(int n, const Rect* __restrict__ rects, const uint32_t* __restrict__ code,
+                                              const uint32_t* __restrict__ offs, int tiles_u,
+                                              uint64_t* __restrict__ ckeys, uint32_t* __restrict__ vals) {
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    Rect r = rects[g];
+    if (r.tv_hi < r.tv_lo) return;
+    uint32_t pos = offs[g];
+    uint64_t c = code[g];
+    for (int tv = r.tv_lo; tv <= r.tv_hi; ++tv) {
+        int row = tv * tiles_u;
+        for (int tu = r.s1_lo; tu <= r.s1_hi; ++tu) {
+            ckeys[pos] = ((uint64_t)(row + tu) << 31) | c;
+            vals[pos] = (uint32_t)g;
+            ++pos;
+        }
+        for (int tu = 0; tu <= r.s2_hi; ++tu) {
+            ckeys[pos] = ((uint64_t)(row + tu) << 31) | c;
+            vals[pos] = (uint32_t)g;
+            ++pos;
+        }
+    }
+}
+
+// K4: per-tile [start, end) = searchsorted left/right (splat.py:340-343)
+__global__ void k_ranges(const uint64_t* __restrict__ ckeys, int m, int n_tiles, int2* __restrict__ ranges) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    int lo = 0, hi = m;
+    while (lo < hi) {  // lower bound of tile t
+        int mid = (lo + hi) >> 1;
+        if ((long long)(ckeys[mid] >> 31) < t) lo = mid + 1; else hi = mid;
+    }
+    int a = lo;
+    hi = m;
+    while (lo < hi) {  // upper bound
+        int mid = (lo + hi) >> 1;
+        if ((long long)(ckeys[mid] >> 31) <= t) lo = mid + 1; else hi = mid;
+    }
+    ranges[t] = make_int2(a, lo);
+}
+
+// Restore reference keys (tile << 32 | code) for TileIndex.keys.
+__global__ void k_expand_keys(const uint64_t* __restrict__ ckeys, int m, uint64_t* __restrict__ keys) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    uint64_t c = ckeys[i];
+    keys[i] = ((c >> 31) << 32) | (c & 0x7fffffffull);
+}
+
+// K4b: emission bound lb[i] = min_{j >= i in tile} lbv[g_j] (reverse
+// segmented min-scan, one block per tile).  Used by the exact streaming
+// re-sort in K6: a pending hit with t_mid < lb[i] precedes every hit that
+// candidates i.. can still produce.
+constexpr int LB_THREADS = 256;
+__global__ void __launch_bounds__(LB_THREADS) k_lower_bounds(const int2* __restrict__ ranges, const uint32_t* __restrict__ vals,
+                                                              const RfsGeom* __restrict__ geom, double* __restrict__ lb) {
+    __shared__ double s[LB_THREADS];
+    int2 rg = ranges[blockIdx.x];
+    double carry = INFINITY;
+    for (int end = rg.y; end > rg.x; end -= LB_THREADS) {
+        int i = end - 1 - (int)threadIdx.x;  // thread 0 handles the last element
+        double v = i >= rg.x ? geom[vals[i]].lbv : INFINITY;
+        s[threadIdx.x] = v;
+        __syncthreads();
+        // inclusive min-scan over increasing thread index (= decreasing i)
+        for (int o = 1; o < LB_THREADS; o <<= 1) {
+            double t = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : INFINITY;
+            __syncthreads();
+            v = fmin(v, t);
+            s[threadIdx.x] = v;
+            __syncthreads();
+        }
+        v = fmin(v, carry);
+        if (i >= rg.x) lb[i] = v;
+        carry = fmin(carry, s[LB_THREADS - 1]);
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int rfs_project(int n, const float* means, const float* quats, const float* log_scales, const float* trans_mag_raw,
+                const float* trans_phase, const double* rx, double ress_radius, int n_az, int n_el,
+                void* geom, void* sph, uint32_t* depth_code, void* rects, uint32_t* counts, void* rho32,
+                double* proj_out, int* err_flags, void* stream) {
+    if (n < 0 || n_az < 1 || n_az > 360 || n_el < 1 || n_el > 180) return RFS_ERR_SHAPE;
+    if (n == 0) return RFS_OK;
+    int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_project<<<rfs_ceil_div(n, 256), 256, 0, st>>>(
+        n, means, quats, log_scales, trans_mag_raw, trans_phase, rx[0], rx[1], rx[2], ress_radius, n_az, n_el,
+        tiles_u, (RfsGeom*)geom, (float4*)sph, depth_code, (Rect*)rects, counts, (float4*)rho32, proj_out, err_flags);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+size_t rfs_scan_temp_elems(int n) { return (size_t)rfs_ceil_div(n > 0 ? n : 1, SCAN_TILE) + 1; }
+
+int rfs_exclusive_scan_u32(const uint32_t* in, int n, uint32_t* out, uint32_t* total, uint32_t* temp, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) {
+        RFS_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(uint32_t), st));
+        return RFS_OK;
+    }
+    int nb = rfs_ceil_div(n, SCAN_TILE);
+    if (nb > SCAN_THREADS * SCAN_ITEMS) return RFS_ERR_CAPACITY;
+    k_scan_partials<<<nb, SCAN_THREADS, 0, st>>>(in, n, temp);
+    k_scan_top<<<1, SCAN_THREADS, 0, st>>>(temp, nb, total);
+    k_scan_final<<<nb, SCAN_THREADS, 0, st>>>(in, n, temp, out);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+int rfs_bin_fill(int n, const void* rects, const uint32_t* depth_code, const uint32_t* offsets, int n_az,
+                 uint64_t* ckeys, uint32_t* vals, void* stream) {
+    if (n <= 0) return RFS_OK;
+    int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
+    k_fill<<<rfs_ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(n, (const Rect*)rects, depth_code, offsets, tiles_u,
+                                                                    ckeys, vals);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+int rfs_tile_ranges(const uint64_t* ckeys, int m, int n_tiles, int* ranges, void* stream) {
+    k_ranges<<<rfs_ceil_div(n_tiles, 128), 128, 0, (cudaStream_t)stream>>>(ckeys, m, n_tiles, (int2*)ranges);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+int rfs_expand_keys(const uint64_t* ckeys, int m, uint64_t* keys, void* stream) {
+    if (m <= 0) return RFS_OK;
+    k_expand_keys<<<rfs_ceil_div(m, 256), 256, 0, (cudaStream_t)stream>>>(ckeys, m, keys);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+int rfs_lower_bounds(const int* ranges, int n_tiles, const uint32_t* vals, const void* geom, double* lb, void* stream) {
+    if (n_tiles <= 0) return RFS_OK;
+    k_lower_bounds<<<n_tiles, LB_THREADS, 0, (cudaStream_t)stream>>>((const int2*)ranges, vals, (const RfsGeom*)geom, lb);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+"""GPU parity: the sm_100a path against the reference-pinned oracle / golden vectors.
+
+Bars (BASELINE.json north_star):
+- tile index (keys, indices, ranges): bit-exact;
+- live hit counts per ray: exact (fp64 geometry reproduces the hit sets);
+- spectra P = |S|^2: normwise rel <= 1e-4 and per-ray |dP| <= 1e-4 * max(P, 1e-3 max P);
+- gradients: per class |a-r| / max(|a|, |r|, 1e-3 class_max) <= 1e-3.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+from helpers import GRAD_KEYS, class_rel, config1_scene, l1_upstream, load, rel_err, scene_from, sha
+
+from paper_2502_01826_b200 import api, raster
+from paper_2502_01826_b200.scene import bench_scene, default_txs, random_scene, round_to_f32
+
+pytestmark = pytest.mark.gpu
+
+SPEC_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+def _spectrum_ok(S, ref):
+    P, Pr = np.abs(S) ** 2, np.abs(ref) ** 2
+    assert rel_err(P, Pr) <= SPEC_TOL, rel_err(P, Pr)
+    floor = 1e-3 * Pr.max() if Pr.size else 0.0
+    bad = np.abs(P - Pr) > SPEC_TOL * np.maximum(Pr, floor) + 1e-30
+    assert not bad.any(), f"{bad.sum()} rays outside tolerance"
+
+
+def _grads_ok(g: api.GradientBuffer, z, prefix, sel=None):
+    sel = z[prefix + "grad_sel"] if sel is None else sel
+    for k in GRAD_KEYS:
+        a = getattr(g, k)[sel]
+        r = z[prefix + k]
+        e = class_rel(a, r)
+        assert e <= GRAD_TOL, (k, e)
+
+
+# ---------------------------------------------------------------- binning
+@pytest.mark.parametrize("backend", ["hand", "cub"])
+def test_tile_index_config1_bit_exact(backend):
+    z = load("config1_10k.npz")
+    t = api.build_tiles_for_render(config1_scene(), sort_backend=backend)
+    np.testing.assert_array_equal(t.keys, z["keys"])
+    np.testing.assert_array_equal(t.indices, z["indices"])
+    np.testing.assert_array_equal(t.ranges, z["ranges"])
+
+
+@pytest.mark.parametrize("n", [100_000, 500_000])
+def test_tile_index_large_bit_exact(n):
+    z = load("tile_hashes.npz")
+    s = round_to_f32(bench_scene(np.random.default_rng(0), n, 360, 180))
+    t = api.build_tiles_for_render(s)
+    assert t.keys.size == int(z[f"n{n}_m"])
+    assert sha(t.keys) == str(z[f"n{n}_sha_keys"])
+    assert sha(t.indices) == str(z[f"n{n}_sha_indices"])
+    assert sha(t.ranges) == str(z[f"n{n}_sha_ranges"])
+
+
+@pytest.mark.parametrize("prefix", ["cube_", "special_", "hemi_"])
+def test_tile_index_edge_scenes(prefix):
+    z = load("edge_scenes.npz")
+    t = api.build_tiles_for_render(scene_from(z, prefix))
+    np.testing.assert_array_equal(t.keys, z[prefix + "keys"])
+    np.testing.assert_array_equal(t.indices, z[prefix + "indices"])
+    np.testing.assert_array_equal(t.ranges, z[prefix + "ranges"])
+
+
+def test_projection_matches_reference():
+    z = load("config1_10k.npz")
+    p = api.project_scene(config1_scene())
+    got = np.stack([p.center_u, p.center_v, p.radius_px, p.tile_radius, p.depth, p.active.astype(float)], 1)
+    np.testing.assert_allclose(got[:, [0, 1, 3, 4, 5]], z["proj"][:, [0, 1, 3, 4, 5]], rtol=1e-12, atol=1e-11)
+    np.testing.assert_allclose(got[:, 2], z["proj"][:, 2], rtol=1e-9)
+
+
+def test_sort_hand_vs_cub_random_keys():
+    dev = "cuda"
+    rng = np.random.default_rng(3)
+    for m in (1, 2, 1000, 4097, 300_000):
+        k = rng.integers(0, 1 << 40, m, dtype=np.int64)
+        k[rng.integers(0, m, m // 3)] = k[0]  # many ties
+        v = np.arange(m, dtype=np.int32)
+        kt, vt = torch.as_tensor(k, device=dev), torch.as_tensor(v, device=dev)
+        a = raster.sort_pairs(kt.clone(), vt.clone(), 40, "hand")
+        b = raster.sort_pairs(kt.clone(), vt.clone(), 40, "cub")
+        order = np.argsort(k, kind="stable")
+        np.testing.assert_array_equal(a[0].cpu().numpy(), k[order])
+        np.testing.assert_array_equal(a[1].cpu().numpy(), v[order])
+        np.testing.assert_array_equal(b[1].cpu().numpy(), v[order])
+
+
+# ---------------------------------------------------------------- hit lists
+def test_live_counts_config1_exact():
+    z = load("config1_10k.npz")
+    ctx = api.prepare_context(config1_scene())
+    np.testing.assert_array_equal(ctx.geometry.ray_counts.cpu().numpy(), z["live"])
+
+
+@pytest.mark.parametrize("n", [100_000])
+def test_live_counts_large_vs_oracle(n):
+    s = round_to_f32(bench_scene(np.random.default_rng(0), n, 360, 180))
+    ctx = api.prepare_context(s)
+    oc = oracle.OracleContext(s)
+    np.testing.assert_array_equal(ctx.geometry.ray_counts.cpu().numpy(), oc.live_counts().ravel())
+
+
+# ---------------------------------------------------------------- forward
+def test_forward_config1():
+    z = load("config1_10k.npz")
+    S = api.render_complex_frame(config1_scene(), z["tx"])
+    _spectrum_ok(S, z["frame"])
+
+
+@pytest.mark.parametrize("i", range(20))
+def test_forward_gradcheck_scenes(i):
+    z = load("gradcheck_scenes.npz")
+    S = api.render_complex_frame(scene_from(z, f"s{i}_"), z[f"s{i}_tx"])
+    _spectrum_ok(S, z[f"s{i}_frame"])
+
+
+@pytest.mark.parametrize("prefix", ["cube_", "special_", "hemi_"])
+def test_forward_edge_scenes(prefix):
+    z = load("edge_scenes.npz")
+    S = api.render_complex_frame(scene_from(z, prefix), z[prefix + "tx"])
+    _spectrum_ok(S, z[prefix + "frame"])
+
+
+def test_forward_tx_batch_vs_oracle():
+    s = round_to_f32(bench_scene(np.random.default_rng(2), 20_000, 360, 180))
+    txs = default_txs(70, seed=5)  # > 64: exercises the second TX block
+    S = api.render_complex_frames(s, txs)
+    oc = oracle.OracleContext(s)
+    for b in (0, 33, 64, 69):
+        oc.set_tx(txs[b])
+        _spectrum_ok(S[b], oc.forward())
+
+
+# ---------------------------------------------------------------- backward
+def test_backward_config1():
+    z = load("config1_10k.npz")
+    lam = l1_upstream(z["frame"])
+    g = api.backward_frame(config1_scene(), z["tx"], lam)
+    _grads_ok(g, z, "")
+
+
+@pytest.mark.parametrize("i", range(20))
+def test_backward_gradcheck_scenes(i):
+    z = load("gradcheck_scenes.npz")
+    p = f"s{i}_"
+    g = api.backward_frame(scene_from(z, p), z[p + "tx"], l1_upstream(z[p + "frame"]))
+    _grads_ok(g, z, p)
+
+
+@pytest.mark.parametrize("prefix", ["cube_", "special_", "hemi_"])
+def test_backward_edge_scenes(prefix):
+    z = load("edge_scenes.npz")
+    g = api.backward_frame(scene_from(z, prefix), z[prefix + "tx"], l1_upstream(z[prefix + "frame"]))
+    _grads_ok(g, z, prefix)
+
+
+def test_backward_tx_batch_is_sum_of_singles():
+    """Batch semantics = sum over TX (GradientBuffer.add, grad.py:85-92) vs the oracle."""
+    s = round_to_f32(bench_scene(np.random.default_rng(8), 5_000, 180, 90))
+    txs = default_txs(5, seed=9)
+    oc = oracle.OracleContext(s)
+    ups, ref = [], None
+    for t in txs:
+        oc.set_tx(t)
+        lam = l1_upstream(oc.forward())
+        ups.append(lam)
+        g = oc.backward(lam)
+        ref = g if ref is None else {k: ref[k] + g[k] for k in ref}
+    got = api.backward_frames(s, txs, np.stack(ups))
+    for k in GRAD_KEYS:
+        assert class_rel(getattr(got, k), ref[k]) <= GRAD_TOL, k
+
+
+def test_autograd_matches_backward_frame():
+    from paper_2502_01826_b200 import RFSplat
+
+    z = load("gradcheck_scenes.npz")
+    s = scene_from(z, "s3_")
+    ds = raster.DeviceScene.from_host(s)
+    leaves = [t.clone().requires_grad_(True) for t in
+              (ds.means, ds.quats, ds.log_scales, ds.trans_mag_raw, ds.trans_phase, ds.coeffs)]
+    tx = torch.as_tensor(z["s3_tx"], dtype=torch.float32, device="cuda").reshape(1, 3)
+    S = RFSplat.apply(*leaves, torch.tensor(s.rx), tx, s.n_az, s.n_el, s.ress_radius, True)
+    P = (S.abs() ** 2)
+    loss = (P - (1.3 * P.detach() + 0.05)).abs().mean()
+    loss.backward()
+    lam = l1_upstream(S.detach().cpu().numpy()[0].astype(np.complex128))
+    ref = oracle.backward_frame(s, z["s3_tx"], lam)
+    assert class_rel(leaves[0].grad.cpu().numpy(), ref["d_mean"]) <= GRAD_TOL
+    assert class_rel(leaves[1].grad.cpu().numpy(), ref["d_quat"]) <= GRAD_TOL
+    assert class_rel(leaves[2].grad.cpu().numpy(), ref["d_log_scale"]) <= GRAD_TOL
+    sg = 1 / (1 + np.exp(-s.trans_mag_raw))
+    assert class_rel(leaves[3].grad.cpu().numpy(), ref["d_trans_mag"] * sg * (1 - sg)) <= GRAD_TOL
+    assert class_rel(leaves[4].grad.cpu().numpy(), ref["d_trans_phase"]) <= GRAD_TOL
+    assert class_rel(leaves[5].grad.cpu().numpy(), ref["d_coeffs"]) <= GRAD_TOL
+
+
+def test_geometry_error_raised():
+    from paper_2502_01826_b200.errors import GeometryError
+
+    s = round_to_f32(random_scene(np.random.default_rng(0), 5))
+    s.means[2] = 0.0
+    with pytest.raises(GeometryError):
+        api.build_tiles_for_render(s)
+
+
+def test_empty_scene_renders_zero():
+    s = round_to_f32(random_scene(np.random.default_rng(0), 5))
+    s.means[:] = [[0.2, 0.1, 0.0]] * 5  # all inside the RESS -> inactive
+    S = api.render_complex_frame(s, [1.0, 2.0, 3.0])
+    assert np.all(S == 0)
+    t = api.build_tiles_for_render(s)
+    assert t.keys.size == 0 and np.all(t.ranges == 0)
