@@ -74,6 +74,8 @@ def lib():
             L.orc_forward_naive.argtypes = [P, _dp, C.c_int]
             L.orc_live_counts.argtypes = [P, _i64p, C.c_int]
             L.orc_backward.argtypes = [P, _dp, C.c_int] + [_dp] * 7 + [C.c_int]
+            L.orc_ray_hits.argtypes = [P, C.c_int64, C.c_int64, _i64p, _dp, _dp, _dp, _dp, _u8p]
+            L.orc_ray_hits.restype = C.c_int64
             _lib = L
     return _lib
 
@@ -173,6 +175,16 @@ class OracleContext:
         out = np.zeros(self.n_az * self.n_el, np.int64)
         lib().orc_live_counts(C.byref(self._c), _p(out, _i64p), self.threads)
         return out.reshape(self.n_az, self.n_el)
+
+    def ray_hits(self, r: int) -> dict:
+        """All hits of ray r sorted by (t_mid, g) (_collect_hits, _kernels.py:27-112)."""
+        cap = max(self.m, 1)
+        g = np.zeros(cap, np.int64)
+        t, w, d1, d2 = (np.zeros(cap) for _ in range(4))
+        cl = np.zeros(cap, np.uint8)
+        n = int(lib().orc_ray_hits(C.byref(self._c), int(r), cap, _p(g, _i64p), _p(t), _p(w), _p(d1), _p(d2),
+                                   _p(cl, _u8p)))
+        return {"g": g[:n], "t_mid": t[:n], "w": w[:n], "d1": d1[:n], "d2": d2[:n], "clamped": cl[:n].astype(bool)}
 
     def backward(self, upstream, include_direction_chain: bool = True) -> dict:
         up = np.ascontiguousarray(np.asarray(upstream, dtype=np.complex128).reshape(-1))

@@ -892,4 +892,25 @@ int orc_live_counts(orc_ctx *c, int64_t *counts, int threads) {
     return 0;
 }
 
+/* Sorted hit list of one ray (all hits, not only live), for tests and
+ * diagnostics: returns the hit count, fills up to cap entries. */
+int64_t orc_ray_hits(orc_ctx *c, int64_t r, int64_t cap, int64_t *g, double *tmid, double *w, double *d1,
+                     double *d2, uint8_t *clamped) {
+    int64_t u = r / c->n_el, v = r % c->n_el;
+    int64_t t = (v / TILE) * c->tiles_u + (u / TILE);
+    int64_t lo = c->ranges[2 * t], hi = c->ranges[2 * t + 1];
+    if (hi == lo) return 0;
+    tile_cand_t tc;
+    gather_tile(c, lo, hi, &tc);
+    hits_t h;
+    hits_alloc(&h, tc.m);
+    int64_t cnt = collect_hits((double)u, (double)v, c->ray_dirs + 3 * r, &tc, c->rx, c->ress_radius, (double)c->n_az, 1, &h);
+    for (int64_t k = 0; k < cnt && k < cap; ++k) {
+        g[k] = h.g[k]; tmid[k] = h.tmid[k]; w[k] = h.w[k]; d1[k] = h.d1[k]; d2[k] = h.d2[k]; clamped[k] = h.clamped[k];
+    }
+    hits_free(&h);
+    free_tile(&tc);
+    return cnt;
+}
+
 int orc_version(void) { return 1; }

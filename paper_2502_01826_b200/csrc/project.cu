@@ -222,6 +222,7 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
 // block-wide exclusive scan of one value per thread; returns the block total
 __device__ uint32_t block_excl_scan(uint32_t v, uint32_t& excl) {
     __shared__ uint32_t warp_tot[32];
+    __shared__ uint32_t block_tot;
     int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t inc = warp_incl_scan(v);
     if (lane == 31) warp_tot[wid] = inc;
@@ -231,11 +232,11 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t& excl) {
         uint32_t t = lane < nw ? warp_tot[lane] : 0;
         uint32_t ti = warp_incl_scan(t);
         if (lane < nw) warp_tot[lane] = ti - t;
-        if (lane == nw - 1) warp_tot[31] = ti;
+        if (lane == nw - 1) block_tot = ti;
     }
     __syncthreads();
     excl = warp_tot[wid] + inc - v;
-    uint32_t total = warp_tot[31];
+    uint32_t total = block_tot;
     __syncthreads();
     return total;
 }
