@@ -226,7 +226,8 @@ def run_ours(args):
     ph_ms = {k: float(np.mean(v)) for k, v in phases.items()}
     kern = {
         "forward": (ab["forward"], ph_ms.get("forward")),
-        "backward": (ab["backward"], ph_ms.get("backward_rays", 0) + ph_ms.get("backward_hits", 0)),
+        "backward": (ab["backward"] + ab["epilogue"],
+                     ph_ms.get("backward_rays", 0) + ph_ms.get("gauss_index", 0) + ph_ms.get("grad_gauss", 0)),
     }
     roof = {}
     for k, (byts, ms) in kern.items():

@@ -20,11 +20,11 @@
  * Layouts (N Gaussians, B transmitters, R = n_az * n_el rays, r = u*n_el+v):
  *   means f32[N*3], quats f32[N*4] (w,x,y,z), log_scales f32[N*3],
  *   trans_mag_raw f32[N], trans_phase f32[N], coeffs complex64[N*K]
- *   (K = (L+1)^2, index l*l+l+m), rx f64[3], tx f32[B*3],
- *   S / grad_S complex64[B*R], psi / P complex64[N*B].
- * Opaque records (sizes below): geom 128 B/Gaussian, sph 16 B/Gaussian,
+ *   (K = (L+1)^2, index l*l+l+m), rx f64[3] (host), tx f32[B*3],
+ *   S / grad_S complex64[B*R], psi complex64[N*B], dirs f64[R*3].
+ * Opaque records: geom 128 B/Gaussian, sph 16 B/Gaussian, whit 64 B/Gaussian,
  *   rects 16 B/Gaussian, rho32 16 B/Gaussian, hit slab 16 B/(ray*hcap),
- *   gslab 16 B/(ray*hcap), gacc 64 B/Gaussian.
+ *   gslab 16 B/(ray*hcap).
  */
 #ifndef RFSPLAT_B200_H
 #define RFSPLAT_B200_H
@@ -38,11 +38,11 @@ extern "C" {
 
 #define RFS_GEOM_BYTES 128
 #define RFS_SPH_BYTES 16
+#define RFS_WHIT_BYTES 64
 #define RFS_RECT_BYTES 16
 #define RFS_RHO_BYTES 16
 #define RFS_HIT_BYTES 16
 #define RFS_GSLAB_BYTES 16
-#define RFS_GACC_FLOATS 16
 
 /* K1: per-Gaussian shape, transmittance, projection and tile counts.
  * Replaces scene.covariances (scene.py:157-161), prepare_context's inverse /
@@ -52,8 +52,8 @@ extern "C" {
  * f64[N*6]) receives SceneProjection (center_u, center_v, radius_px,
  * tile_radius, depth, active).  err_flags bit 1 set => GeometryError. */
 int rfs_project(int n, const float* means, const float* quats, const float* log_scales, const float* trans_mag_raw,
-                const float* trans_phase, const double* rx /* host f64[3] */, double ress_radius, int n_az, int n_el,
-                void* geom, void* sph, uint32_t* depth_code, void* rects, uint32_t* counts, void* rho32,
+                const float* trans_phase, const double* rx, double ress_radius, int n_az, int n_el, void* geom,
+                void* sph, void* whit, uint32_t* depth_code, void* rects, uint32_t* counts, void* rho32,
                 double* proj_out, int* err_flags, void* stream);
 
 /* K2: exclusive warp-shuffle scan of per-Gaussian splat counts -> offsets;
@@ -88,19 +88,24 @@ int rfs_tile_ranges(const uint64_t* ckeys, int m, int n_tiles, int* ranges, void
  * lb[i] = min_{j >= i, same tile} (depth_j - r3_j). */
 int rfs_lower_bounds(const int* ranges, int n_tiles, const uint32_t* vals, const void* geom, double* lb, void* stream);
 
+/* Ray directions through the cell centres (render.py:103-117); the Python
+ * host layer uploads a numpy-built table instead (bitwise the reference's). */
+int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream);
+
 /* K6: TX-independent live hit lists.  Replaces _collect_hits + the live walk
  * of forward_tiled / count_hits_tiled (_kernels.py:27-112, 140-192, 237-292).
- * Writes hits of ray r to slab[r*hcap ...], counts[r] = live count.
- * stats (device int[8]): [0] rays needing rfs_hits_slow (listed in
- * slow_list), [1] rays with live > hcap (caller must retry with larger
- * hcap), [2] max live, [3] total live hits, [4] longest tile list. */
-int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* geom,
-             const double* rx /* host */, double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts,
-             int* slow_list, int* stats, void* stream);
+ * Writes hits of ray r to slab[r*hcap ...], counts[r] = live count.  pcap
+ * selects the pending ring (32 or 64 entries per ray).  stats (device
+ * int[8]): [0] rays needing rfs_hits_slow (listed in slow_list), [1] rays
+ * with live > hcap (caller must retry with larger hcap), [2] max live,
+ * [3] total live hits, [4] longest tile list, [5] largest pending set. */
+int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
+             const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, void* stream);
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
-                  const void* sph, const void* geom, const double* rx, double ress_radius, int n_az, int n_el,
-                  int hcap, void* slab, int* counts, double* pend_t, uint32_t* pend_g, float* pend_w, int pcap,
-                  int* stats, void* stream);
+                  const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
+                  double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
+                  uint32_t* pend_g, int pcap, int* stats, void* stream);
 
 /* K5: psi[g][b] = sum_k coeffs[g][k] * basis_k(bearing of tx_b from mu_g).
  * Replaces render.py:229-238 + fle.fle_basis_with_derivs (fle.py:153-212). */
@@ -113,30 +118,35 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
                 void* stream);
 
 /* K8a: TX-batched reverse sweep (_ray_backward's complex part,
- * _kernels.py:369-387, 522).  Accumulates P[g][b] += conj(lam) w T (the
- * reference's inc_pg bincount, grad.py:252-254) and per-hit TX-reduced
- * scalars into gslab (+=).  n_tx <= 256 per call; P and gslab must be zeroed
- * before the first call of a step. */
+ * _kernels.py:369-387, 522): per hit, accumulates (+=) the TX-reduced
+ * scalars {Re(T C), d|rho|, d(phase)} into gslab and writes lambda
+ * transposed (lamT complex64[R*n_tx]).  n_tx <= 256 per call; gslab must be
+ * zeroed before the first call of a step. */
 int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam,
-                      const void* rho32, int n_tx, int n_rays, void* P, void* gslab, void* stream);
+                      const void* rho32, int n_tx, int n_rays, void* gslab, void* lamT, void* stream);
 
-/* K8b: per-hit mean / covariance chains in fp64 (_kernels.py:389-520),
- * reduced per Gaussian into gacc[g][16] = {dmu[3], d|rho|, dcov[9], dphase}.
- * gacc must be zeroed before the call. */
-int rfs_backward_hits(const void* slab, const int* counts, int hcap, const void* gslab, const void* geom,
-                      const double* rx /* host */, double ress_radius, int n_az, int n_el, float* gacc, void* stream);
+/* K8i: by-Gaussian index of the live hit slots (TX independent):
+ * keys[ray_off[r]+k] = Gaussian id, slots[...] = r*hcap + k; sort the pairs
+ * with rfs_sort_pairs_u64 and take g_off = rfs_gauss_offsets (int32[N+1]). */
+int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays, uint64_t* keys,
+                 uint32_t* slots, void* stream);
+int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream);
 
-/* K9: per-Gaussian epilogue: d_coeffs = conj(P) conj(basis) (grad.py:255),
- * bearing chain into d_mean (grad.py:167-189), chain_cov_to_shape
- * (grad.py:134-164) and d_trans_mag_raw = d|rho| sigma(1-sigma)
- * (train.py:161-162).  d_cov is nullable.  accumulate = 0 writes every output
- * (first TX chunk of a step); accumulate = 1 adds only the TX-dependent
- * terms (d_coeffs, bearing chain) of a further chunk. */
-int rfs_grad_epilogue(int n, int n_tx, int degree, const float* means, const float* quats, const float* log_scales,
-                      const float* trans_mag_raw, const void* coeffs, const float* tx, const void* P, const float* gacc,
-                      int include_direction_chain, int accumulate, float* d_mean, float* d_quat, float* d_log_scale,
-                      float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, void* d_coeffs, float* d_cov,
-                      void* stream);
+/* K9: per-Gaussian backward, one warp per Gaussian over its hits, no
+ * atomics: mean / covariance chains in fp64 (_kernels.py:387-520, summed in
+ * the fixed slot order like the reference's bincount, grad.py:243-254),
+ * p_acc and d_coeffs = conj(p_acc) conj(basis) (grad.py:252-255), bearing
+ * chain (grad.py:167-189), chain_cov_to_shape (grad.py:134-164) and
+ * d_trans_mag_raw = d|rho| sigma(1-sigma) (train.py:161-162).
+ * accumulate = 0 writes every output (first TX chunk of a step);
+ * accumulate = 1 adds only the TX-dependent terms of a further chunk.
+ * d_cov is nullable. */
+int rfs_grad_gauss(int n, int n_tx, int degree, const float* means, const float* quats, const float* log_scales,
+                   const float* trans_mag_raw, const void* coeffs, const float* tx, const void* geom, const void* slab,
+                   int hcap, const void* gslab, const void* lamT, const int* g_off, const uint32_t* g_slots,
+                   const double* dirs, const double* rx, double ress_radius, int include_direction_chain, int accumulate,
+                   float* d_mean, float* d_quat, float* d_log_scale, float* d_trans_mag, float* d_trans_mag_raw,
+                   float* d_trans_phase, void* d_coeffs, float* d_cov, void* stream);
 
 /* Library / build identification. */
 int rfs_version(void);

@@ -1,37 +1,39 @@
 // composite.cu -- TX-batched kernels on top of the shared hit lists.
 //
-//   K5  k_psi            psi[g][b] = sum_k c_gk basis_k(bearing mu_g -> tx_b)
-//   K7  k_forward        S[b][r]  = sum_k w_k T_k psi[g_k][b]          (SpMM)
-//   K8a k_backward_rays  per ray, back to front: C_k = sum_b conj(lam_b) psi[g_k][b],
-//                        suffix recursion for the transmittance chain, and
-//                        P[g][b] += conj(lam_b) w_k T_k (vector atomics)
-//   K8b k_backward_hits  per hit: fp64 mean/covariance chain (_kernels.py:387-520)
-//                        scaled by the TX-reduced weight gradient, reduced
-//                        per Gaussian with vector atomics
-//   K9  k_epilogue       per Gaussian: d_coeffs, bearing chain, Sigma -> (q, s)
-//
-// Reference: forward_tiled _kernels.py:184-192, _ray_backward _kernels.py:360-522,
-// backward_frame grad.py:243-258, _direction_chain grad.py:167-189,
-// chain_cov_to_shape grad.py:134-164, fle_basis_with_derivs fle.py:153-212.
+//   K5  k_psi          psi[g][b] = sum_k c_gk basis_k(bearing mu_g -> tx_b)
+//   K7  k_forward      S[b][r]  = sum_k w_k T_k psi[g_k][b]                 (SpMM)
+//   K8a k_backward_rays per ray, back to front, lanes over TX:
+//                      C_k = sum_b conj(lam_b) psi[g_k][b]                  (SDDMM)
+//                      A_k = w_{k+1} C_{k+1} + rho_{k+1} A_{k+1}  (suffix recursion)
+//                      -> per-hit scalars GW_k = Re(T_k C_k), d|rho|_k, d(phase)_k
+//                      and lamT[r][b] (lambda transposed for K9)
+//   K8i k_hit_keys     by-Gaussian index of the hit slots (TX independent)
+//   K9  k_grad_gauss   one warp per Gaussian over its hits:
+//                      fp64 mean / covariance chains (_kernels.py:387-520)
+//                      summed in fp64; P[b] = sum_hits conj(lam_b) w T (lanes
+//                      over TX); d_coeffs = conj(P) conj(basis) (grad.py:255);
+//                      bearing chain (grad.py:167-189); Sigma -> (q, s)
+//                      (grad.py:134-164).  No atomics, fixed summation order.
 //
 // Because the backward is linear in the upstream lambda, every sum over the
-// TX batch can be taken before the TX-independent geometry: per hit only the
-// scalars GW_k = Re(T_k C_k) and A_k = sum_b conj(lam_b) suffix_{k,b} are needed,
-// and A_k obeys the same recursion as the reference's suffix with psi -> C.
+// TX batch is taken before the TX-independent geometry: per hit only GW_k
+// and A_k are needed, and A_k obeys the reference's suffix recursion
+// (_kernels.py:382, 522) with psi replaced by C.
 #include "rfs_common.cuh"
 
 namespace {
 
 // ---------------------------------------------------------------- FLE basis
-// Fourier-Legendre basis e^{i m alpha} P_l^m(cos beta) with Condon-Shortley
-// phase, and its alpha / beta derivatives (fle.py:153-212), evaluated from the
-// bearing vector r = tx - mu without trigonometry: cos(beta) = rho / |r|,
-// sin(beta) = z / |r|, e^{i alpha} = (x + i y) / rho.
+// e^{i m alpha} P_l^m(cos beta) with Condon-Shortley phase and its alpha /
+// beta derivatives (fle.py:153-212), from the bearing vector r = tx - mu
+// without trigonometry: cos(beta) = rho/|r|, sin(beta) = z/|r|,
+// e^{i alpha} = (x + i y)/rho.
 template <int L>
 struct Fle {
     static constexpr int K = (L + 1) * (L + 1);
 
-    __device__ static __forceinline__ void eval(float rx, float ry, float rz, float2* B, float2* DA, float2* DB) {
+    __device__ static __forceinline__ void eval_full(float rx, float ry, float rz, float2* B, float2* DA, float2* DB,
+                                                     const float2* co, float2* dpa, float2* dpb) {
         float d = sqrtf(rx * rx + ry * ry + rz * rz);
         bool valid = d > 1e-12f;
         float rho = sqrtf(rx * rx + ry * ry);
@@ -101,8 +103,29 @@ struct Fle {
                     float dv = ratio * dp[l][ma];
                     DB[idx] = make_float2(az.x * dv, az.y * dv);
                 }
+                if (co) {
+                    // dpsi/dalpha = sum c (i m) basis, dpsi/dbeta = sum c e^{i m a} dP
+                    float2 cb = cmulf(co[idx], make_float2(az.x * pv, az.y * pv));
+                    dpa->x += -(float)m * cb.y;
+                    dpa->y += (float)m * cb.x;
+                    float dv = ratio * dp[l][ma];
+                    float2 cd = cmulf(co[idx], make_float2(az.x * dv, az.y * dv));
+                    dpb->x += cd.x;
+                    dpb->y += cd.y;
+                }
             }
         }
+    }
+
+    __device__ static __forceinline__ void eval(float rx, float ry, float rz, float2* B, float2* DA, float2* DB) {
+        eval_full(rx, ry, rz, B, DA, DB, nullptr, nullptr, nullptr);
+    }
+    // basis plus the bearing derivatives of psi = sum_k co_k basis_k
+    __device__ static __forceinline__ void eval_psi_derivs(float rx, float ry, float rz, float2* B, const float2* co,
+                                                           float2& dpa, float2& dpb) {
+        dpa = make_float2(0.f, 0.f);
+        dpb = make_float2(0.f, 0.f);
+        eval_full(rx, ry, rz, B, nullptr, nullptr, co, &dpa, &dpb);
     }
 };
 
@@ -171,8 +194,8 @@ constexpr int BR_MAXJ = 8;  // up to 256 TX per launch (lane owns b = lane + 32 
 
 __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
     const RfsHit* __restrict__ slab, const int* __restrict__ counts, int hcap, const float2* __restrict__ psi,
-    const float2* __restrict__ lam, const float4* __restrict__ rho32, int nb, int R, float2* __restrict__ P,
-    float4* __restrict__ gslab) {
+    const float2* __restrict__ lam, const float4* __restrict__ rho32, int nb, int R, float4* __restrict__ gslab,
+    float2* __restrict__ lamT) {
     extern __shared__ __align__(16) float2 s_lam[];  // [nb][BR_RAYS + 1]
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int r0 = blockIdx.x * BR_RAYS;
@@ -181,6 +204,11 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
         s_lam[b * (BR_RAYS + 1) + rl] = r < R ? lam[(size_t)b * R + r] : make_float2(0.f, 0.f);
     }
     __syncthreads();
+    // lambda transposed to [R][nb] rows for the per-Gaussian gather of K9
+    for (int i = threadIdx.x; i < nb * BR_RAYS; i += BR_THREADS) {
+        int rl = i / nb, b = i % nb, r = r0 + rl;
+        if (r < R) lamT[(size_t)r * nb + b] = s_lam[b * (BR_RAYS + 1) + rl];
+    }
     const int nj = (nb + 31) >> 5;
     for (int rl = wid; rl < BR_RAYS; rl += BR_THREADS / 32) {
         const int r = r0 + rl;
@@ -196,35 +224,29 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
         }
         const RfsHit* h = slab + (size_t)r * hcap;
         float4* gs = gslab + (size_t)r * hcap;
-        // A: running sum_b conj(lam_b) suffix_{k,b}; (wn, rn, cn) = w, rho, C of hit k+1
+        // A: sum_b conj(lam_b) suffix_{k,b}; (wn, rn, cn) = w, rho, C of hit k+1
         float2 A = make_float2(0.f, 0.f);
         float wn = 0.f;
         float2 rn = make_float2(0.f, 0.f), cn = make_float2(0.f, 0.f);
         for (int k = cnt - 1; k >= 0; --k) {
             RfsHit hk = h[k];
-            float4 rq = __ldg(&rho32[hk.g]);
             const float2* row = psi + (size_t)hk.g * nb;
-            float2* prow = P + (size_t)hk.g * nb;
-            float2 wt = make_float2(hk.w * hk.t_re, hk.w * hk.t_im);
             float2 c = make_float2(0.f, 0.f);
 #pragma unroll
             for (int j = 0; j < BR_MAXJ; ++j) {
                 int b = lane + 32 * j;
-                if (j < nj && b < nb) {
-                    c = caddf(c, cmulf(cl[j], __ldg(&row[b])));
-                    atomicAdd(&prow[b], cmulf(cl[j], wt));  // P[g][b] += conj(lam_b) w T
-                }
+                if (j < nj && b < nb) c = caddf(c, cmulf(cl[j], __ldg(&row[b])));
             }
             c.x = warp_sum(c.x);
             c.y = warp_sum(c.y);
-            // A_k = w_{k+1} C_{k+1} + rho_{k+1} A_{k+1}   (A_{last} = 0)
             A = caddf(make_float2(wn * cn.x, wn * cn.y), cmulf(rn, A));
+            float4 rq = __ldg(&rho32[hk.g]);
             if (lane == 0) {
                 float2 t = make_float2(hk.t_re, hk.t_im);
-                float gw = t.x * c.x - t.y * c.y;                    // Re(T C)
+                float gw = t.x * c.x - t.y * c.y;            // Re(T C)        (_kernels.py:387-388)
                 float2 ta = cmulf(t, A);
-                float dmag = ta.x * rq.z - ta.y * rq.w;              // Re(T e^{j phi} A)
-                float dph = -(ta.x * rq.y + ta.y * rq.x);            // -Im(T rho A)
+                float dmag = ta.x * rq.z - ta.y * rq.w;      // Re(T e^{jphi} A) (_kernels.py:382-383)
+                float dph = -(ta.x * rq.y + ta.y * rq.x);    // -Im(T rho A)     (_kernels.py:384-385)
                 float4 o = gs[k];
                 gs[k] = make_float4(o.x + gw, o.y + dmag, o.z + dph, 0.f);
             }
@@ -235,101 +257,33 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
     }
 }
 
-// ------------------------------------------------------- K8b backward hits
-__device__ __forceinline__ void ray_dir64(int u, int v, int n_az, double d[3]) {
-    double cell = 360.0 / (double)n_az;
-    double al = ((double)u + 0.5) * cell * (RFS_PI / 180.0);
-    double be = (((double)v + 0.5) * cell - 90.0) * (RFS_PI / 180.0);
-    double sa, ca, sb, cb;
-    sincos(al, &sa, &ca);
-    sincos(be, &sb, &cb);
-    d[0] = cb * ca;
-    d[1] = cb * sa;
-    d[2] = sb;
-}
-
-constexpr int BH_THREADS = 256;
-
-// one warp per ray, one lane per hit
-__global__ void __launch_bounds__(BH_THREADS) k_backward_hits(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
-                                                              int hcap, const float4* __restrict__ gslab,
-                                                              const RfsGeom* __restrict__ geom, double rx0, double rx1,
-                                                              double rx2, double min_t, int n_az, int n_el, int R,
-                                                              float* __restrict__ gacc) {
+// ------------------------------------------- K8i by-Gaussian hit-slot index
+__global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restrict__ counts, const uint32_t* __restrict__ ray_off,
+                           int hcap, int R, uint64_t* __restrict__ keys, uint32_t* __restrict__ slots) {
     const int lane = threadIdx.x & 31;
-    const int r = (blockIdx.x * BH_THREADS + threadIdx.x) >> 5;
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= R) return;
     const int cnt = min(counts[r], hcap);
-    if (cnt == 0) return;
-    const int u = r / n_el, v = r % n_el;
-    double d[3];
-    ray_dir64(u, v, n_az, d);
-    const double dx = d[0], dy = d[1], dz = d[2];
+    const uint32_t base = ray_off[r];
     for (int k = lane; k < cnt; k += 32) {
-        RfsHit hk = slab[(size_t)r * hcap + k];
-        float4 gsk = gslab[(size_t)r * hcap + k];
-        const RfsGeom* G = geom + hk.g;
-        const double gw = gsk.x, w = hk.w;
-        double mx = rx0 - G->mu[0], my = rx1 - G->mu[1], mz = rx2 - G->mu[2];
-        double i00 = G->inv[0], i01 = G->inv[1], i02 = G->inv[2], i11 = G->inv[3], i12 = G->inv[4], i22 = G->inv[5];
-        double p0 = i00 * dx + i01 * dy + i02 * dz, p1 = i01 * dx + i11 * dy + i12 * dz, p2 = i02 * dx + i12 * dy + i22 * dz;
-        double e0 = i00 * mx + i01 * my + i02 * mz, e1 = i01 * mx + i11 * my + i12 * mz, e2 = i02 * mx + i12 * my + i22 * mz;
-        double a = p0 * dx + p1 * dy + p2 * dz;
-        double b = p0 * mx + p1 * my + p2 * mz;
-        double c = e0 * mx + e1 * my + e2 * mz;
-        double disc = b * b - a * (c - 9.0);
-        double sq = sqrt(fmax(disc, 0.0));
-        double d2 = (-b + sq) / a, d1 = (-b - sq) / a;
-        bool clamped = d1 < min_t;
-        double t_in = clamped ? min_t : d1;
-        double t_mid = 0.5 * (t_in + d2);
-        double ddx = t_mid * dx + mx, ddy = t_mid * dy + my, ddz = t_mid * dz + mz;  // x_mid - mu
-        double q0 = i00 * ddx + i01 * ddy + i02 * ddz;
-        double q1 = i01 * ddx + i11 * ddy + i12 * ddz;
-        double q2 = i02 * ddx + i12 * ddy + i22 * ddz;
-        double gmu[3] = {gw * w * q0, gw * w * q1, gw * w * q2};
-        double f = gw * w * 0.5;
-        double qv[3] = {q0, q1, q2};
-        double Iv[9] = {i00, i01, i02, i01, i11, i12, i02, i12, i22};
-        double cv9[9];
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < 3; ++j) cv9[3 * i + j] = f * (qv[i] * qv[j] - Iv[3 * i + j]);
-        if (disc >= RFS_TANGENT_EPS) {
-            double pv[3] = {p0, p1, p2}, ev[3] = {e0, e1, e2};
-            double s_dv = q0 * dx + q1 * dy + q2 * dz;
-            double half = 0.5 * (gw * (-w) * s_dv);
-            double inv2sq = 0.5 / sq;
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-                double bmu = -pv[ax], cmu = -2.0 * ev[ax];
-                double dd = (2.0 * b * bmu - a * cmu) * inv2sq;
-                double dsum = (-bmu + dd) / a;
-                if (!clamped) dsum += (-bmu - dd) / a;
-                gmu[ax] += half * dsum;
-            }
-            double cm9 = c - 9.0;
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int j = 0; j < 3; ++j) {
-                    double da = -pv[i] * pv[j], db = -pv[i] * ev[j], dc = -ev[i] * ev[j];
-                    double ddisc = 2.0 * b * db - cm9 * da - a * dc;
-                    double dsum = (-db + ddisc * inv2sq) / a - d2 * da / a;
-                    if (!clamped) dsum += (-db - ddisc * inv2sq) / a - d1 * da / a;
-                    cv9[3 * i + j] += half * dsum;
-                }
-        }
-        float4* acc = reinterpret_cast<float4*>(gacc + (size_t)hk.g * RFS_GACC);
-        atomicAdd(acc + 0, make_float4((float)gmu[0], (float)gmu[1], (float)gmu[2], gsk.y));
-        atomicAdd(acc + 1, make_float4((float)cv9[0], (float)cv9[1], (float)cv9[2], (float)cv9[3]));
-        atomicAdd(acc + 2, make_float4((float)cv9[4], (float)cv9[5], (float)cv9[6], (float)cv9[7]));
-        atomicAdd(acc + 3, make_float4((float)cv9[8], gsk.z, 0.f, 0.f));
+        keys[base + k] = slab[(size_t)r * hcap + k].g;
+        slots[base + k] = (uint32_t)((size_t)r * hcap + k);
     }
 }
 
-// --------------------------------------------------------------- K9 epilogue
+// g_off[g] = lower_bound(g) over the sorted Gaussian keys, g in [0, n]
+__global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, int n, int* __restrict__ g_off) {
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g > n) return;
+    int lo = 0, hi = h;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if ((long long)keys[mid] < g) lo = mid + 1; else hi = mid;
+    }
+    g_off[g] = lo;
+}
+
+// ---------------------------------------------------------------- K9
 __device__ void rot_from_quat(const double q[4], double R[9]) {
     double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
     double w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
@@ -338,86 +292,201 @@ __device__ void rot_from_quat(const double q[4], double R[9]) {
     R[6] = 2 * (x * z - w * y); R[7] = 2 * (y * z + w * x); R[8] = 1 - 2 * (x * x + y * y);
 }
 
+// Sum of 32 per-lane values of 32 lanes; afterwards lane l holds the total of value l (31 shuffles).
+__device__ __forceinline__ float transpose_reduce32(float v[32], int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const bool upper = (lane & s) != 0;
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
+            float send = upper ? v[j] : v[j + s];
+            float keep = upper ? v[j + s] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+    }
+    return v[0];
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+constexpr int GG_THREADS = 256;
+
+// One warp per Gaussian.
 template <int L>
-__global__ void __launch_bounds__(128) k_epilogue(
+__global__ void __launch_bounds__(GG_THREADS) k_grad_gauss(
     int n, int nb, const float* __restrict__ means, const float* __restrict__ quats, const float* __restrict__ log_scales,
     const float* __restrict__ raw, const float2* __restrict__ coeffs, const float* __restrict__ tx,
-    const float2* __restrict__ P, const float* __restrict__ gacc, int include_dir, int accumulate,
+    const RfsGeom* __restrict__ geom, const RfsHit* __restrict__ slab, int hcap, const float4* __restrict__ gslab,
+    const float2* __restrict__ lamT, const int* __restrict__ g_off, const uint32_t* __restrict__ g_slots,
+    const double* __restrict__ dirs, double rx0, double rx1, double rx2, double min_t, int include_dir, int accumulate,
     float* __restrict__ d_mean, float* __restrict__ d_quat, float* __restrict__ d_log_scale, float* __restrict__ d_mag,
     float* __restrict__ d_mag_raw, float* __restrict__ d_phase, float2* __restrict__ d_coeffs, float* __restrict__ d_cov) {
     constexpr int K = Fle<L>::K;
-    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int NV = 2 * K;                  // real values of d_coeffs
+    constexpr int NG = (NV + 31) / 32;         // transpose-reduce groups
+    const int lane = threadIdx.x & 31;
+    const int g = (blockIdx.x * GG_THREADS + threadIdx.x) >> 5;
     if (g >= n) return;
-    const float mx = means[3 * g], my = means[3 * g + 1], mz = means[3 * g + 2];
-    float2 co[K];
+    const int h0 = g_off[g], h1 = g_off[g + 1];
+
+    // ---- phase A: TX-independent geometry chains, fp64, lanes over hits
+    double acc[14];
 #pragma unroll
-    for (int k = 0; k < K; ++k) co[k] = coeffs[(size_t)g * K + k];
-    float2 dc[K];
+    for (int i = 0; i < 14; ++i) acc[i] = 0.0;
+    if (!accumulate && h1 > h0) {
+        const RfsGeom* G = geom + g;
+        const double mx = rx0 - G->mu[0], my = rx1 - G->mu[1], mz = rx2 - G->mu[2];
+        const double i00 = G->inv[0], i01 = G->inv[1], i02 = G->inv[2], i11 = G->inv[3], i12 = G->inv[4],
+                     i22 = G->inv[5];
+        const double e0 = i00 * mx + i01 * my + i02 * mz, e1 = i01 * mx + i11 * my + i12 * mz,
+                     e2 = i02 * mx + i12 * my + i22 * mz;
+        const double c = e0 * mx + e1 * my + e2 * mz;
+        for (int h = h0 + lane; h < h1; h += 32) {
+            const uint32_t s = g_slots[h];
+            const int r = (int)(s / (uint32_t)hcap);
+            const float w = slab[s].w;
+            const float4 gs = gslab[s];
+            const double dx = dirs[3 * r], dy = dirs[3 * r + 1], dz = dirs[3 * r + 2];
+            const double p0 = i00 * dx + i01 * dy + i02 * dz, p1 = i01 * dx + i11 * dy + i12 * dz,
+                         p2 = i02 * dx + i12 * dy + i22 * dz;
+            const double a = p0 * dx + p1 * dy + p2 * dz;
+            const double b = p0 * mx + p1 * my + p2 * mz;
+            const double disc = b * b - a * (c - 9.0);
+            const double sq = sqrt(fmax(disc, 0.0));
+            const double d2 = (-b + sq) / a, d1 = (-b - sq) / a;
+            const bool clamped = d1 < min_t;
+            const double t_mid = 0.5 * ((clamped ? min_t : d1) + d2);
+            // q = Sigma^-1 (x_mid - mu) = t_mid p + e
+            const double q0 = t_mid * p0 + e0, q1 = t_mid * p1 + e1, q2 = t_mid * p2 + e2;
+            const double gww = (double)gs.x * (double)w;
+            double gmu[3] = {gww * q0, gww * q1, gww * q2};
+            const double f = 0.5 * gww;
+            const double qv[3] = {q0, q1, q2};
+            const double Iv[9] = {i00, i01, i02, i01, i11, i12, i02, i12, i22};
+            double cv9[9];
 #pragma unroll
-    for (int k = 0; k < K; ++k) dc[k] = make_float2(0.f, 0.f);
-    float dm0 = 0.f, dm1 = 0.f, dm2 = 0.f;
-    const float2* prow = P + (size_t)g * nb;
-    for (int b = 0; b < nb; ++b) {
-        float2 p = prow[b];
-        if (p.x == 0.f && p.y == 0.f) continue;  // Gaussian not hit under this TX
-        float rx = tx[3 * b] - mx, ry = tx[3 * b + 1] - my, rz = tx[3 * b + 2] - mz;
-        float2 B[K], DA[K], DB[K];
-        Fle<L>::eval(rx, ry, rz, B, DA, DB);
-        // d_coeffs = conj(p_acc) * conj(basis)   (grad.py:255)
+            for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            dc[k].x += p.x * B[k].x - p.y * B[k].y;
-            dc[k].y += -(p.x * B[k].y + p.y * B[k].x);
-        }
-        if (include_dir) {
-            // _direction_chain (grad.py:167-189)
-            float zeta2 = rx * rx + ry * ry + rz * rz;
-            float rho2 = rx * rx + ry * ry;
-            bool ok = (sqrtf(zeta2) > 1e-12f) && (rho2 > 1e-18f * zeta2);
-            if (ok) {
-                float rho = sqrtf(rho2);
-                float2 dpa = make_float2(0.f, 0.f), dpb = make_float2(0.f, 0.f);
+                for (int j = 0; j < 3; ++j) cv9[3 * i + j] = f * (qv[i] * qv[j] - Iv[3 * i + j]);
+            // Midpoint chain (_kernels.py:432-507).  For an unclamped chord the
+            // midpoint minimises the quadratic form along the ray, so
+            // q.d = t_mid a + b = 0 and the whole chain vanishes; only clamped
+            // hits carry it.
+            if (clamped && disc >= RFS_TANGENT_EPS) {
+                const double pv[3] = {p0, p1, p2}, ev[3] = {e0, e1, e2};
+                const double s_dv = q0 * dx + q1 * dy + q2 * dz;
+                const double half = -0.5 * gww * s_dv;
+                const double inv2sq = 0.5 / sq;
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    dpa = caddf(dpa, cmulf(co[k], DA[k]));
-                    dpb = caddf(dpb, cmulf(co[k], DB[k]));
+                for (int ax = 0; ax < 3; ++ax) {
+                    double bmu = -pv[ax], cmu = -2.0 * ev[ax];
+                    double dd = (2.0 * b * bmu - a * cmu) * inv2sq;
+                    gmu[ax] += half * ((-bmu + dd) / a);
                 }
-                float ga = p.x * dpa.x - p.y * dpa.y;  // Re(p * dpsi/dalpha)
-                float gb = p.x * dpb.x - p.y * dpb.y;
-                dm0 -= ga * (-ry / rho2) + gb * (-rz * rx / (rho * zeta2));
-                dm1 -= ga * (rx / rho2) + gb * (-rz * ry / (rho * zeta2));
-                dm2 -= gb * (rho / zeta2);
+                const double cm9 = c - 9.0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        double da = -pv[i] * pv[j], db = -pv[i] * ev[j], dc = -ev[i] * ev[j];
+                        double ddisc = 2.0 * b * db - cm9 * da - a * dc;
+                        cv9[3 * i + j] += half * ((-db + ddisc * inv2sq) / a - d2 * da / a);
+                    }
+            }
+            acc[0] += gmu[0];
+            acc[1] += gmu[1];
+            acc[2] += gmu[2];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) acc[3 + i] += cv9[i];
+            acc[12] += (double)gs.y;
+            acc[13] += (double)gs.z;
+        }
+#pragma unroll
+        for (int i = 0; i < 14; ++i) acc[i] = warp_sum_d(acc[i]);
+    }
+
+    // ---- phase B: TX-dependent terms, lanes over TX
+    float vals[NG * 32];
+#pragma unroll
+    for (int i = 0; i < NG * 32; ++i) vals[i] = 0.f;
+    float dm0 = 0.f, dm1 = 0.f, dm2 = 0.f;
+    if (h1 > h0) {
+        const float mxf = means[3 * g], myf = means[3 * g + 1], mzf = means[3 * g + 2];
+        float2 co[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) co[k] = __ldg(&coeffs[(size_t)g * K + k]);
+        for (int b0 = 0; b0 < nb; b0 += 32) {
+            const int b = b0 + lane;
+            if (b >= nb) break;
+            // P[g][b] = sum over hits of conj(lam_b) w T  (grad.py:252-254 bincount of inc_pg)
+            float2 P = make_float2(0.f, 0.f);
+            for (int h = h0; h < h1; ++h) {
+                const uint32_t s = g_slots[h];
+                const int r = (int)(s / (uint32_t)hcap);
+                const RfsHit hk = slab[s];
+                const float2 wt = make_float2(hk.w * hk.t_re, hk.w * hk.t_im);
+                const float2 l = lamT[(size_t)r * nb + b];
+                P = caddf(P, cmulf(make_float2(l.x, -l.y), wt));
+            }
+            const float rx = tx[3 * b] - mxf, ry = tx[3 * b + 1] - myf, rz = tx[3 * b + 2] - mzf;
+            float2 B[K], dpa, dpb;
+            Fle<L>::eval_psi_derivs(rx, ry, rz, B, co, dpa, dpb);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {  // conj(P) conj(basis)
+                vals[2 * k] += P.x * B[k].x - P.y * B[k].y;
+                vals[2 * k + 1] += -(P.x * B[k].y + P.y * B[k].x);
+            }
+            if (include_dir) {
+                const float zeta2 = rx * rx + ry * ry + rz * rz;
+                const float rho2 = rx * rx + ry * ry;
+                if (sqrtf(zeta2) > 1e-12f && rho2 > 1e-18f * zeta2) {
+                    const float rho = sqrtf(rho2);
+                    const float ga = P.x * dpa.x - P.y * dpa.y;  // Re(p dpsi/dalpha)
+                    const float gb = P.x * dpb.x - P.y * dpb.y;
+                    dm0 -= ga * (-ry / rho2) + gb * (-rz * rx / (rho * zeta2));
+                    dm1 -= ga * (rx / rho2) + gb * (-rz * ry / (rho * zeta2));
+                    dm2 -= gb * (rho / zeta2);
+                }
             }
         }
     }
-    if (accumulate) {
-        // a later TX chunk of the same step: only the TX-dependent terms
+    float mine[NG];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            float2 o = d_coeffs[(size_t)g * K + k];
-            d_coeffs[(size_t)g * K + k] = make_float2(o.x + dc[k].x, o.y + dc[k].y);
+    for (int q = 0; q < NG; ++q) mine[q] = transpose_reduce32(vals + 32 * q, lane);
+    dm0 = warp_sum(dm0);
+    dm1 = warp_sum(dm1);
+    dm2 = warp_sum(dm2);
+
+    float* dcf = reinterpret_cast<float*>(d_coeffs + (size_t)g * K);
+#pragma unroll
+    for (int q = 0; q < NG; ++q) {
+        const int i = 32 * q + lane;
+        if (i < NV) dcf[i] = accumulate ? dcf[i] + mine[q] : mine[q];
+    }
+    if (accumulate) {
+        if (lane == 0) {
+            d_mean[3 * g + 0] += dm0;
+            d_mean[3 * g + 1] += dm1;
+            d_mean[3 * g + 2] += dm2;
         }
-        d_mean[3 * g + 0] += dm0;
-        d_mean[3 * g + 1] += dm1;
-        d_mean[3 * g + 2] += dm2;
         return;
     }
+    if (lane != 0) return;
+    d_mean[3 * g + 0] = (float)acc[0] + dm0;
+    d_mean[3 * g + 1] = (float)acc[1] + dm1;
+    d_mean[3 * g + 2] = (float)acc[2] + dm2;
+    d_mag[g] = (float)acc[12];
+    const float sg = 1.f / (1.f + expf(-raw[g]));
+    d_mag_raw[g] = (float)acc[12] * sg * (1.f - sg);
+    d_phase[g] = (float)acc[13];
+    const double* dcv = acc + 3;
+    if (d_cov) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) d_coeffs[(size_t)g * K + k] = dc[k];
-    const float* ga = gacc + (size_t)g * RFS_GACC;
-    d_mean[3 * g + 0] = ga[0] + dm0;
-    d_mean[3 * g + 1] = ga[1] + dm1;
-    d_mean[3 * g + 2] = ga[2] + dm2;
-    float dmag = ga[3];
-    d_mag[g] = dmag;
-    float sg = 1.f / (1.f + expf(-raw[g]));
-    d_mag_raw[g] = dmag * sg * (1.f - sg);
-    d_phase[g] = ga[13];
-    double dcv[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-        dcv[i] = ga[4 + i];
-        if (d_cov) d_cov[9 * g + i] = ga[4 + i];
+        for (int i = 0; i < 9; ++i) d_cov[9 * g + i] = (float)dcv[i];
     }
     // chain_cov_to_shape (grad.py:134-164), fp64
     double q[4] = {quats[4 * g], quats[4 * g + 1], quats[4 * g + 2], quats[4 * g + 3]};
@@ -429,12 +498,12 @@ __global__ void __launch_bounds__(128) k_epilogue(
                     exp(2.0 * (double)log_scales[3 * g + 2])};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        double acc = 0.0;
+        double s = 0.0;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) acc += R[3 * i + a] * dcv[3 * i + j] * R[3 * j + a];
-        d_log_scale[3 * g + a] = (float)(2.0 * dv[a] * acc);
+            for (int j = 0; j < 3; ++j) s += R[3 * i + a] * dcv[3 * i + j] * R[3 * j + a];
+        d_log_scale[3 * g + a] = (float)(2.0 * dv[a] * s);
     }
     const double w = qu[0], x = qu[1], y = qu[2], z = qu[3];
     const double dr[4][9] = {{0, -2 * z, 2 * y, 2 * z, 0, -2 * x, -2 * y, 2 * x, 0},
@@ -444,7 +513,7 @@ __global__ void __launch_bounds__(128) k_epilogue(
     double gq[4];
 #pragma unroll
     for (int qi = 0; qi < 4; ++qi) {
-        double acc = 0.0;
+        double s = 0.0;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -455,9 +524,9 @@ __global__ void __launch_bounds__(128) k_epilogue(
                     s1 += dr[qi][3 * i + j] * dv[j] * R[3 * k + j];
                     s2 += R[3 * i + j] * dv[j] * dr[qi][3 * k + j];
                 }
-                acc += dcv[3 * i + k] * (s1 + s2);
+                s += dcv[3 * i + k] * (s1 + s2);
             }
-        gq[qi] = acc;
+        gq[qi] = s;
     }
     double dot = gq[0] * qu[0] + gq[1] * qu[1] + gq[2] * qu[2] + gq[3] * qu[3];
 #pragma unroll
@@ -465,21 +534,9 @@ __global__ void __launch_bounds__(128) k_epilogue(
 }
 
 template <int L>
-int launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, float2* psi, cudaStream_t st) {
+void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, float2* psi, cudaStream_t st) {
     long long tot = (long long)n * nb;
     k_psi<L><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, nb, means, coeffs, tx, psi);
-    return RFS_OK;
-}
-
-template <int L>
-int launch_epi(int n, int nb, const float* means, const float* quats, const float* log_scales, const float* raw,
-               const float2* coeffs, const float* tx, const float2* P, const float* gacc, int include_dir,
-               int accumulate, float* d_mean, float* d_quat, float* d_log_scale, float* d_mag, float* d_mag_raw, float* d_phase,
-               float2* d_coeffs, float* d_cov, cudaStream_t st) {
-    k_epilogue<L><<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, nb, means, quats, log_scales, raw, coeffs, tx, P, gacc,
-                                                       include_dir, accumulate, d_mean, d_quat, d_log_scale, d_mag, d_mag_raw,
-                                                       d_phase, d_coeffs, d_cov);
-    return RFS_OK;
 }
 
 }  // namespace
@@ -515,7 +572,7 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
 }
 
 int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam, const void* rho32,
-                      int n_tx, int n_rays, void* P, void* gslab, void* stream) {
+                      int n_tx, int n_rays, void* gslab, void* lamT, void* stream) {
     if (n_rays <= 0 || n_tx <= 0) return RFS_OK;
     if (n_tx > 32 * BR_MAXJ) return RFS_ERR_SHAPE;
     size_t smem = (size_t)n_tx * (BR_RAYS + 1) * sizeof(float2);
@@ -526,42 +583,50 @@ int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void*
     }
     k_backward_rays<<<rfs_ceil_div(n_rays, BR_RAYS), BR_THREADS, smem, (cudaStream_t)stream>>>(
         (const RfsHit*)slab, counts, hcap, (const float2*)psi, (const float2*)lam, (const float4*)rho32, n_tx, n_rays,
-        (float2*)P, (float4*)gslab);
+        (float4*)gslab, (float2*)lamT);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
-int rfs_backward_hits(const void* slab, const int* counts, int hcap, const void* gslab, const void* geom, const double* rx,
-                      double ress_radius, int n_az, int n_el, float* gacc, void* stream) {
-    int R = n_az * n_el;
-    if (R <= 0) return RFS_OK;
-    k_backward_hits<<<rfs_ceil_div((long long)R * 32, BH_THREADS), BH_THREADS, 0, (cudaStream_t)stream>>>(
-        (const RfsHit*)slab, counts, hcap, (const float4*)gslab, (const RfsGeom*)geom, rx[0], rx[1], rx[2], ress_radius,
-        n_az, n_el, R, gacc);
+int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays, uint64_t* keys,
+                 uint32_t* slots, void* stream) {
+    if (n_rays <= 0) return RFS_OK;
+    k_hit_keys<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const RfsHit*)slab, counts, ray_off, hcap, n_rays, keys, slots);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
-int rfs_grad_epilogue(int n, int n_tx, int degree, const float* means, const float* quats, const float* log_scales,
-                      const float* trans_mag_raw, const void* coeffs, const float* tx, const void* P, const float* gacc,
-                      int include_direction_chain, int accumulate, float* d_mean, float* d_quat, float* d_log_scale,
-                      float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, void* d_coeffs, float* d_cov,
-                      void* stream) {
+int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream) {
+    k_gauss_offsets<<<rfs_ceil_div(n + 1, 256), 256, 0, (cudaStream_t)stream>>>(keys, n_hits, n, g_off);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+int rfs_grad_gauss(int n, int n_tx, int degree, const float* means, const float* quats, const float* log_scales,
+                   const float* trans_mag_raw, const void* coeffs, const float* tx, const void* geom, const void* slab,
+                   int hcap, const void* gslab, const void* lamT, const int* g_off, const uint32_t* g_slots,
+                   const double* dirs, const double* rx, double ress_radius, int include_direction_chain, int accumulate,
+                   float* d_mean, float* d_quat, float* d_log_scale, float* d_trans_mag, float* d_trans_mag_raw,
+                   float* d_trans_phase, void* d_coeffs, float* d_cov, void* stream) {
     if (n <= 0) return RFS_OK;
     cudaStream_t st = (cudaStream_t)stream;
-#define RFS_EPI(LL)                                                                                                   \
-    launch_epi<LL>(n, n_tx, means, quats, log_scales, trans_mag_raw, (const float2*)coeffs, tx, (const float2*)P, gacc, \
-                   include_direction_chain, accumulate, d_mean, d_quat, d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase,  \
-                   (float2*)d_coeffs, d_cov, st)
+    unsigned grid = (unsigned)rfs_ceil_div((long long)n * 32, GG_THREADS);
+#define RFS_GG(LL)                                                                                                  \
+    k_grad_gauss<LL><<<grid, GG_THREADS, 0, st>>>(                                                                  \
+        n, n_tx, means, quats, log_scales, trans_mag_raw, (const float2*)coeffs, tx, (const RfsGeom*)geom,          \
+        (const RfsHit*)slab, hcap, (const float4*)gslab, (const float2*)lamT, g_off, g_slots, dirs, rx[0], rx[1],    \
+        rx[2], ress_radius, include_direction_chain, accumulate, d_mean, d_quat, d_log_scale, d_trans_mag,           \
+        d_trans_mag_raw, d_trans_phase, (float2*)d_coeffs, d_cov)
     switch (degree) {
-        case 0: RFS_EPI(0); break;
-        case 1: RFS_EPI(1); break;
-        case 2: RFS_EPI(2); break;
-        case 3: RFS_EPI(3); break;
-        case 4: RFS_EPI(4); break;
+        case 0: RFS_GG(0); break;
+        case 1: RFS_GG(1); break;
+        case 2: RFS_GG(2); break;
+        case 3: RFS_GG(3); break;
+        case 4: RFS_GG(4); break;
         default: return RFS_ERR_SHAPE;
     }
-#undef RFS_EPI
+#undef RFS_GG
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -9,300 +9,323 @@
 // runs once per step and the TX batch composites from its output.
 //
 // Exact streaming re-sort: candidates arrive in tile-key
-// (depth) order; a hit's t_mid is >= depth - r3 of its Gaussian, so a pending
-// hit whose t_mid is below lb[i] = min_{j>=i} (depth_j - r3_j) precedes every
-// hit the remaining candidates can produce and is emitted immediately.  The
-// emitted sequence equals the reference's sorted list, so rays stop scanning
-// as soon as they terminate.  Pending hits live in a per-thread ring buffer in
-// shared memory; a ray that overflows it is redone by k_hits_slow with a
-// global-memory buffer sized to its tile.
+// (depth) order; a hit's chord midpoint lies in the Gaussian's 3-sigma ball,
+// so t_mid >= depth - r3, and a pending hit whose t_mid is below
+// lb[i] = min_{j>=i} (depth_j - r3_j) precedes every hit the remaining
+// candidates can produce: it is emitted at once, and a ray stops scanning as
+// soon as it terminates.  Pending (t_mid, g) pairs live in a per-thread ring
+// in shared memory; a ray that overflows it is redone by k_hits_slow with a
+// global buffer sized to its tile (exact, rarely taken).
 //
-// Arithmetic: an fp32 bounding-sphere test rejects most candidates; survivors
-// get the reference's fp64 disc prefilter and fp64 quadratic, so hit sets and
-// orderings match the fp64 oracle.  T is carried in fp64.
+// Arithmetic: fp32 bounding-sphere and whitened-ellipsoid tests with proven
+// margins reject most candidates; survivors run the reference's fp64 disc
+// prefilter and quadratic with the reference's operation order and no FMA
+// contraction (explicit __d*_rn), so exact ties order like the reference.
+// Ray directions come from a table built with the reference's formula
+// (render.py:103-117).  T is carried in fp64.
 #include "rfs_common.cuh"
 
 namespace {
 
-constexpr int HT_THREADS = 128;  // half a 16x16 tile: 8 u-columns x 16 v-rows
-constexpr int HT_BATCH = 128;    // candidates staged per iteration
-constexpr int HT_PCAP = 32;      // pending ring capacity per ray (power of 2)
+constexpr int HB = 64;  // candidates staged per batch
+constexpr double DINF = 1.0e300;
 
-struct RayState {
-    double d[3];
-    float d32[3];
-    double tre, tim;
-    int live;
-    bool done;
-};
+#define DM(a, b) __dmul_rn((a), (b))
+#define DA(a, b) __dadd_rn((a), (b))
+#define DS(a, b) __dsub_rn((a), (b))
 
-// Exact hit test of candidate geometry G against a ray; returns true and
-// (t_mid, w) on a hit.  Same expressions as _kernels.py:45-91.
-__device__ __forceinline__ bool exact_hit(const RfsGeom* __restrict__ Gp, const double d[3], double u, double v,
-                                          double n_az, double rx0, double rx1, double rx2, double min_t,
-                                          double& t_mid, float& w_out) {
-    double r2 = __ldg(&Gp->r2);
+// Reference quadratic (_kernels.py:45-81): returns true and t_mid on a hit.
+__device__ __forceinline__ bool exact_hit(const RfsGeom* __restrict__ G, double dx, double dy, double dz, double u,
+                                          double v, double n_az, double rx0, double rx1, double rx2, double min_t,
+                                          double& t_mid) {
+    double r2 = __ldg(&G->r2);
     if (r2 < 0.0) return false;
-    double du = fabs(u - __ldg(&Gp->cu));
-    if (n_az - du < du) du = n_az - du;
-    double dv = v - __ldg(&Gp->cv);
-    if (du * du + dv * dv > r2) return false;
-    double mx = rx0 - __ldg(&Gp->mu[0]), my = rx1 - __ldg(&Gp->mu[1]), mz = rx2 - __ldg(&Gp->mu[2]);
-    double i00 = __ldg(&Gp->inv[0]), i01 = __ldg(&Gp->inv[1]), i02 = __ldg(&Gp->inv[2]);
-    double i11 = __ldg(&Gp->inv[3]), i12 = __ldg(&Gp->inv[4]), i22 = __ldg(&Gp->inv[5]);
-    double dx = d[0], dy = d[1], dz = d[2];
-    double sx = i00 * dx + i01 * dy + i02 * dz;
-    double sy = i01 * dx + i11 * dy + i12 * dz;
-    double sz = i02 * dx + i12 * dy + i22 * dz;
-    double a = sx * dx + sy * dy + sz * dz;
-    double b = sx * mx + sy * my + sz * mz;
-    double c = (i00 * mx + i01 * my + i02 * mz) * mx + (i01 * mx + i11 * my + i12 * mz) * my +
-               (i02 * mx + i12 * my + i22 * mz) * mz;
-    double disc = b * b - a * (c - 9.0);
+    double du = fabs(DS(u, __ldg(&G->cu)));
+    if (DS(n_az, du) < du) du = DS(n_az, du);
+    double dv = DS(v, __ldg(&G->cv));
+    if (DA(DM(du, du), DM(dv, dv)) > r2) return false;
+    double mx = DS(rx0, __ldg(&G->mu[0])), my = DS(rx1, __ldg(&G->mu[1])), mz = DS(rx2, __ldg(&G->mu[2]));
+    double i00 = __ldg(&G->inv[0]), i01 = __ldg(&G->inv[1]), i02 = __ldg(&G->inv[2]);
+    double i11 = __ldg(&G->inv[3]), i12 = __ldg(&G->inv[4]), i22 = __ldg(&G->inv[5]);
+    double sx = DA(DA(DM(i00, dx), DM(i01, dy)), DM(i02, dz));
+    double sy = DA(DA(DM(i01, dx), DM(i11, dy)), DM(i12, dz));
+    double sz = DA(DA(DM(i02, dx), DM(i12, dy)), DM(i22, dz));
+    double a = DA(DA(DM(sx, dx), DM(sy, dy)), DM(sz, dz));
+    double b = DA(DA(DM(sx, mx), DM(sy, my)), DM(sz, mz));
+    double c = DA(DA(DM(DA(DA(DM(i00, mx), DM(i01, my)), DM(i02, mz)), mx),
+                     DM(DA(DA(DM(i01, mx), DM(i11, my)), DM(i12, mz)), my)),
+                  DM(DA(DA(DM(i02, mx), DM(i12, my)), DM(i22, mz)), mz));
+    double disc = DS(DM(b, b), DM(a, DS(c, 9.0)));
     if (disc < 0.0) return false;
-    double sq = sqrt(disc);
-    double d2 = (-b + sq) / a;
+    double sq = __dsqrt_rn(disc);
+    double d2 = __ddiv_rn(DA(-b, sq), a);
     if (d2 < min_t) return false;
-    double d1 = (-b - sq) / a;
+    double d1 = __ddiv_rn(DS(-b, sq), a);
     double t_in = d1 < min_t ? min_t : d1;
-    t_mid = 0.5 * (t_in + d2);
-    double ex = t_mid * dx + mx, ey = t_mid * dy + my, ez = t_mid * dz + mz;
-    double qf = (i00 * ex + i01 * ey + i02 * ez) * ex + (i01 * ex + i11 * ey + i12 * ez) * ey +
-                (i02 * ex + i12 * ey + i22 * ez) * ez;
-    w_out = (float)(__ldg(&Gp->norm) * exp(-0.5 * qf));
+    t_mid = DM(0.5, DA(t_in, d2));
     return true;
 }
 
-__device__ __forceinline__ bool sphere_pass(float4 s, const float d[3]) {
-    float cx = s.y * d[2] - s.z * d[1];
-    float cy = s.z * d[0] - s.x * d[2];
-    float cz = s.x * d[1] - s.y * d[0];
+// Midpoint density w = norm * exp(-q(x_mid)/2), _kernels.py:82-91.
+__device__ __forceinline__ double hit_weight(const RfsGeom* __restrict__ G, double dx, double dy, double dz,
+                                             double rx0, double rx1, double rx2, double t_mid) {
+    double mx = DS(rx0, __ldg(&G->mu[0])), my = DS(rx1, __ldg(&G->mu[1])), mz = DS(rx2, __ldg(&G->mu[2]));
+    double i00 = __ldg(&G->inv[0]), i01 = __ldg(&G->inv[1]), i02 = __ldg(&G->inv[2]);
+    double i11 = __ldg(&G->inv[3]), i12 = __ldg(&G->inv[4]), i22 = __ldg(&G->inv[5]);
+    double ex = DA(DM(t_mid, dx), mx), ey = DA(DM(t_mid, dy), my), ez = DA(DM(t_mid, dz), mz);
+    double qf = DA(DA(DM(DA(DA(DM(i00, ex), DM(i01, ey)), DM(i02, ez)), ex),
+                      DM(DA(DA(DM(i01, ex), DM(i11, ey)), DM(i12, ez)), ey)),
+                   DM(DA(DA(DM(i02, ex), DM(i12, ey)), DM(i22, ez)), ez));
+    return DM(__ldg(&G->norm), exp(DM(-0.5, qf)));
+}
+
+__device__ __forceinline__ bool sphere_pass(float4 s, float d0, float d1, float d2) {
+    float cx = s.y * d2 - s.z * d1;
+    float cy = s.z * d0 - s.x * d2;
+    float cz = s.x * d1 - s.y * d0;
     return cx * cx + cy * cy + cz * cz <= s.w;
 }
 
+__device__ __forceinline__ bool whitened_pass(float4 a, float4 b, float4 c, float thr, float d0, float d1, float d2) {
+    // L rows: (a.x a.y a.z) (a.w b.x b.y) (b.z b.w c.x); p = (c.y c.z c.w)
+    float q0 = a.x * d0 + a.y * d1 + a.z * d2;
+    float q1 = a.w * d0 + b.x * d1 + b.y * d2;
+    float q2 = b.z * d0 + b.w * d1 + c.x * d2;
+    float x0 = q1 * c.w - q2 * c.z;
+    float x1 = q2 * c.y - q0 * c.w;
+    float x2 = q0 * c.z - q1 * c.y;
+    return x0 * x0 + x1 * x1 + x2 * x2 <= thr * (q0 * q0 + q1 * q1 + q2 * q2);
+}
+
+struct Ray {
+    double dx, dy, dz;
+    float fx, fy, fz;
+    double tre, tim;
+    int live;
+    bool done;
+    bool hcap_over;
+};
+
 // Emit one hit in sorted order: terminate, record, advance T (_kernels.py:186-191).
-__device__ __forceinline__ void emit_hit(RayState& st, uint32_t g, float w, const RfsGeom* __restrict__ geom,
-                                         RfsHit* __restrict__ slab_ray, int hcap, bool& hcap_over) {
+__device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, double t_mid, const RfsGeom* __restrict__ geom, double rx0,
+                                         double rx1, double rx2, RfsHit* __restrict__ slab_ray, int hcap) {
     if (st.tre * st.tre + st.tim * st.tim < RFS_TERM_EPS2) {
         st.done = true;
         return;
     }
+    const RfsGeom* G = geom + g;
     if (st.live < hcap) {
         RfsHit h;
         h.g = g;
-        h.w = w;
+        h.w = (float)hit_weight(G, st.dx, st.dy, st.dz, rx0, rx1, rx2, t_mid);
         h.t_re = (float)st.tre;
         h.t_im = (float)st.tim;
         slab_ray[st.live] = h;
     } else {
-        hcap_over = true;
+        st.hcap_over = true;
     }
     st.live += 1;
-    double rr = __ldg(&geom[g].rho_re), ri = __ldg(&geom[g].rho_im);
+    double rr = __ldg(&G->rho_re), ri = __ldg(&G->rho_im);
     double nr = st.tre * rr - st.tim * ri;
     double ni = st.tre * ri + st.tim * rr;
     st.tre = nr;
     st.tim = ni;
 }
 
-__device__ __forceinline__ void ray_dir(int u, int v, int n_az, double d[3]) {
-    double cell = 360.0 / (double)n_az;
-    double al = ((double)u + 0.5) * cell * (RFS_PI / 180.0);
-    double be = (((double)v + 0.5) * cell - 90.0) * (RFS_PI / 180.0);
-    double sa, ca, sb, cb;
-    sincos(al, &sa, &ca);
-    sincos(be, &sb, &cb);
-    d[0] = cb * ca;
-    d[1] = cb * sa;
-    d[2] = sb;
-}
-
+template <int PCAP, int NT>
 struct HitsSmem {
-    double pt[HT_PCAP][HT_THREADS];
-    uint32_t pg[HT_PCAP][HT_THREADS];
-    float pw[HT_PCAP][HT_THREADS];
-    float4 sph[HT_BATCH];
-    double lb[HT_BATCH];
-    uint32_t g[HT_BATCH];
+    double pt[PCAP][NT];
+    uint32_t pg[PCAP][NT];
+    float4 sph[HB];
+    float4 wh[HB][4];
+    double lb[HB];
+    uint32_t g[HB];
 };
 
-__global__ void __launch_bounds__(HT_THREADS) k_hits(
+// One block = NT rays of one tile (NT/16 u-columns x 16 v-rows); one thread per ray.
+template <int PCAP, int NT>
+__global__ void __launch_bounds__(NT) k_hits(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ vals, const double* __restrict__ lb,
-    const float4* __restrict__ sph, const RfsGeom* __restrict__ geom, double rx0, double rx1, double rx2,
-    double min_t, int n_az, int n_el, int tiles_u, int hcap, RfsHit* __restrict__ slab, int* __restrict__ counts,
-    int* __restrict__ slow_list, int* __restrict__ stats) {
+    const float4* __restrict__ sph, const float4* __restrict__ whit, const RfsGeom* __restrict__ geom,
+    const double* __restrict__ dirs, double rx0, double rx1, double rx2, double min_t, int n_az, int n_el,
+    int tiles_u, int hcap, RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ slow_list,
+    int* __restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    HitsSmem& S = *reinterpret_cast<HitsSmem*>(smem_raw);
-    const int tile = blockIdx.x >> 1, half = blockIdx.x & 1;
+    HitsSmem<PCAP, NT>& S = *reinterpret_cast<HitsSmem<PCAP, NT>*>(smem_raw);
+    constexpr int PARTS = 256 / NT;
+    const int tile = blockIdx.x / PARTS, part = blockIdx.x % PARTS;
     const int tid = threadIdx.x;
-    const int u = (tile % tiles_u) * RFS_TILE + half * 8 + (tid >> 4);
+    const int u = (tile % tiles_u) * RFS_TILE + part * (NT / 16) + (tid >> 4);
     const int v = (tile / tiles_u) * RFS_TILE + (tid & 15);
     const bool valid = u < n_az && v < n_el;
     const int r = valid ? u * n_el + v : 0;
-    RayState st;
+    Ray st;
+    st.dx = dirs[3 * r];
+    st.dy = dirs[3 * r + 1];
+    st.dz = dirs[3 * r + 2];
+    st.fx = (float)st.dx;
+    st.fy = (float)st.dy;
+    st.fz = (float)st.dz;
     st.tre = 1.0;
     st.tim = 0.0;
     st.live = 0;
     st.done = !valid;
-    ray_dir(valid ? u : 0, valid ? v : 0, n_az, st.d);
-    st.d32[0] = (float)st.d[0];
-    st.d32[1] = (float)st.d[1];
-    st.d32[2] = (float)st.d[2];
-    const double du_f = (double)u, dv_f = (double)v, naz = (double)n_az;
+    st.hcap_over = false;
+    const double uf = (double)u, vf = (double)v, naz = (double)n_az;
     RfsHit* slab_ray = slab + (size_t)r * hcap;
-    bool hcap_over = false, pend_over = false;
-    int head = 0, npend = 0;
+    bool pend_over = false;
+    int head = 0, npend = 0, max_pend = 0;
+    double head_t = DINF;
     const int2 rg = ranges[tile];
 
-    for (int base = rg.x; base < rg.y; base += HT_BATCH) {
-        const int nb = min(HT_BATCH, rg.y - base);
+    for (int base = rg.x; base < rg.y; base += HB) {
+        const int nb = min(HB, rg.y - base);
         __syncthreads();
-        for (int j = tid; j < nb; j += HT_THREADS) {
+        for (int j = tid; j < nb; j += NT) {
             uint32_t g = vals[base + j];
             S.g[j] = g;
             S.sph[j] = __ldg(&sph[g]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) S.wh[j][q] = __ldg(&whit[4 * g + q]);
             S.lb[j] = lb[base + j];
         }
         __syncthreads();
         if (!st.done) {
             for (int j = 0; j < nb; ++j) {
-                const double lbj = S.lb[j];
-                while (npend > 0) {
-                    int hslot = head & (HT_PCAP - 1);
-                    if (!(S.pt[hslot][tid] < lbj)) break;
-                    emit_hit(st, S.pg[hslot][tid], S.pw[hslot][tid], geom, slab_ray, hcap, hcap_over);
-                    ++head;
-                    --npend;
+                if (head_t < S.lb[j]) {
+                    // every pending hit with t_mid < lb[j] is final: emit in order
+                    do {
+                        int hs = head % PCAP;
+                        emit_hit(st, S.pg[hs][tid], head_t, geom, rx0, rx1, rx2, slab_ray, hcap);
+                        ++head;
+                        --npend;
+                        head_t = npend > 0 ? S.pt[head % PCAP][tid] : DINF;
+                    } while (!st.done && head_t < S.lb[j]);
                     if (st.done) break;
                 }
-                if (st.done) break;
-                if (!sphere_pass(S.sph[j], st.d32)) continue;
+                if (!sphere_pass(S.sph[j], st.fx, st.fy, st.fz)) continue;
+                if (!whitened_pass(S.wh[j][0], S.wh[j][1], S.wh[j][2], S.wh[j][3].x, st.fx, st.fy, st.fz)) continue;
                 const uint32_t g = S.g[j];
                 double t_mid;
-                float w;
-                if (!exact_hit(geom + g, st.d, du_f, dv_f, naz, rx0, rx1, rx2, min_t, t_mid, w)) continue;
-                if (npend == HT_PCAP) {
+                if (!exact_hit(geom + g, st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid)) continue;
+                if (npend == PCAP) {
                     pend_over = true;
                     st.done = true;
                     break;
                 }
-                // sorted insertion by (t_mid, g) into the ring
+                // sorted insertion by (t_mid, g)
                 int k = npend;
                 while (k > 0) {
-                    int ps = (head + k - 1) & (HT_PCAP - 1);
+                    int ps = (head + k - 1) % PCAP;
                     double pt = S.pt[ps][tid];
                     if (pt > t_mid || (pt == t_mid && S.pg[ps][tid] > g)) {
-                        int qs = (head + k) & (HT_PCAP - 1);
+                        int qs = (head + k) % PCAP;
                         S.pt[qs][tid] = pt;
                         S.pg[qs][tid] = S.pg[ps][tid];
-                        S.pw[qs][tid] = S.pw[ps][tid];
                         --k;
                     } else {
                         break;
                     }
                 }
-                int qs = (head + k) & (HT_PCAP - 1);
+                int qs = (head + k) % PCAP;
                 S.pt[qs][tid] = t_mid;
                 S.pg[qs][tid] = g;
-                S.pw[qs][tid] = w;
                 ++npend;
+                max_pend = max(max_pend, npend);
+                head_t = fmin(head_t, t_mid);
             }
         }
         if (__syncthreads_and(st.done)) break;
     }
-    // drain: every candidate seen, pending hits are final
+    // drain: every candidate was seen, the pending hits are final
     while (!st.done && npend > 0) {
-        int hslot = head & (HT_PCAP - 1);
-        emit_hit(st, S.pg[hslot][tid], S.pw[hslot][tid], geom, slab_ray, hcap, hcap_over);
+        emit_hit(st, S.pg[head % PCAP][tid], S.pt[head % PCAP][tid], geom, rx0, rx1, rx2, slab_ray, hcap);
         ++head;
         --npend;
     }
     if (!valid) return;
+    atomicMax(&stats[5], max_pend);
     if (pend_over) {
         int idx = atomicAdd(&stats[0], 1);
         slow_list[idx] = r;
         return;
     }
     counts[r] = st.live;
-    if (hcap_over) atomicAdd(&stats[1], 1);
+    if (st.hcap_over) atomicAdd(&stats[1], 1);
     atomicMax(&stats[2], st.live);
-    atomicAdd(&stats[3], st.live);
+    atomicAdd(&stats[3], min(st.live, hcap));
 }
 
-// Slow path for rays whose pending buffer overflowed: one thread per ray,
+// Slow path for rays whose pending ring overflowed: one thread per ray,
 // pending list in global scratch of capacity `pcap` (>= the largest tile
 // list, so it cannot overflow).  Same emission rule and arithmetic.
 __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2* __restrict__ ranges,
                             const uint32_t* __restrict__ vals, const double* __restrict__ lb,
-                            const float4* __restrict__ sph, const RfsGeom* __restrict__ geom, double rx0, double rx1,
+                            const float4* __restrict__ sph, const float4* __restrict__ whit,
+                            const RfsGeom* __restrict__ geom, const double* __restrict__ dirs, double rx0, double rx1,
                             double rx2, double min_t, int n_az, int n_el, int tiles_u, int hcap,
                             RfsHit* __restrict__ slab, int* __restrict__ counts, double* __restrict__ pt,
-                            uint32_t* __restrict__ pg, float* __restrict__ pw, int pcap, int* __restrict__ stats) {
+                            uint32_t* __restrict__ pg, int pcap, int* __restrict__ stats) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_rays) return;
     const int r = rays[i];
     const int u = r / n_el, v = r % n_el;
     const int tile = (v / RFS_TILE) * tiles_u + (u / RFS_TILE);
-    RayState st;
+    Ray st;
+    st.dx = dirs[3 * r];
+    st.dy = dirs[3 * r + 1];
+    st.dz = dirs[3 * r + 2];
+    st.fx = (float)st.dx;
+    st.fy = (float)st.dy;
+    st.fz = (float)st.dz;
     st.tre = 1.0;
     st.tim = 0.0;
     st.live = 0;
     st.done = false;
-    ray_dir(u, v, n_az, st.d);
-    st.d32[0] = (float)st.d[0];
-    st.d32[1] = (float)st.d[1];
-    st.d32[2] = (float)st.d[2];
+    st.hcap_over = false;
     RfsHit* slab_ray = slab + (size_t)r * hcap;
     double* my_t = pt + (size_t)i * pcap;
     uint32_t* my_g = pg + (size_t)i * pcap;
-    float* my_w = pw + (size_t)i * pcap;
-    bool hcap_over = false;
     int head = 0, npend = 0;
     const int2 rg = ranges[tile];
     for (int j = rg.x; j < rg.y && !st.done; ++j) {
         const double lbj = lb[j];
         while (npend > 0 && my_t[head] < lbj) {
-            emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap, hcap_over);
+            emit_hit(st, my_g[head], my_t[head], geom, rx0, rx1, rx2, slab_ray, hcap);
             ++head;
             --npend;
             if (st.done) break;
         }
         if (st.done) break;
         const uint32_t g = vals[j];
-        if (!sphere_pass(__ldg(&sph[g]), st.d32)) continue;
+        if (!sphere_pass(__ldg(&sph[g]), st.fx, st.fy, st.fz)) continue;
+        if (!whitened_pass(__ldg(&whit[4 * g]), __ldg(&whit[4 * g + 1]), __ldg(&whit[4 * g + 2]),
+                           __ldg(&whit[4 * g + 3]).x, st.fx, st.fy, st.fz))
+            continue;
         double t_mid;
-        float w;
-        if (!exact_hit(geom + g, st.d, (double)u, (double)v, (double)n_az, rx0, rx1, rx2, min_t, t_mid, w)) continue;
-        // linear layout [head, head + npend); compact when the tail hits pcap
-        if (head + npend == pcap) {
-            for (int k = 0; k < npend; ++k) {
-                my_t[k] = my_t[head + k];
-                my_g[k] = my_g[head + k];
-                my_w[k] = my_w[head + k];
-            }
-            head = 0;
-        }
+        if (!exact_hit(geom + g, st.dx, st.dy, st.dz, (double)u, (double)v, (double)n_az, rx0, rx1, rx2, min_t,
+                       t_mid))
+            continue;
+        // linear layout [head, head + npend): total inserts <= tile length <= pcap
         int k = head + npend;
         while (k > head && (my_t[k - 1] > t_mid || (my_t[k - 1] == t_mid && my_g[k - 1] > g))) {
             my_t[k] = my_t[k - 1];
             my_g[k] = my_g[k - 1];
-            my_w[k] = my_w[k - 1];
             --k;
         }
         my_t[k] = t_mid;
         my_g[k] = g;
-        my_w[k] = w;
         ++npend;
     }
     while (!st.done && npend > 0) {
-        emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap, hcap_over);
+        emit_hit(st, my_g[head], my_t[head], geom, rx0, rx1, rx2, slab_ray, hcap);
         ++head;
         --npend;
     }
     counts[r] = st.live;
-    if (hcap_over) atomicAdd(&stats[1], 1);
+    if (st.hcap_over) atomicAdd(&stats[1], 1);
     atomicMax(&stats[2], st.live);
-    atomicAdd(&stats[3], st.live);
+    atomicAdd(&stats[3], min(st.live, hcap));
 }
 
 __global__ void k_max_range(const int2* __restrict__ ranges, int n_tiles, int* __restrict__ out) {
@@ -310,43 +333,82 @@ __global__ void k_max_range(const int2* __restrict__ ranges, int n_tiles, int* _
     if (t < n_tiles) atomicMax(out, ranges[t].y - ranges[t].x);
 }
 
+// Ray directions through cell centres, render.py:103-117, same operation
+// order as numpy (deg2rad(x) = x * (pi/180)); used only when the host does
+// not supply the table.
+__global__ void k_ray_dirs(int n_az, int n_el, double* __restrict__ dirs) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_az * n_el) return;
+    int u = r / n_el, v = r % n_el;
+    double cell = 360.0 / (double)n_az;
+    double al = DM(DM(DA((double)u, 0.5), cell), RFS_PI / 180.0);
+    double be = DM(DS(DM(DA((double)v, 0.5), cell), 90.0), RFS_PI / 180.0);
+    dirs[3 * r] = DM(cos(be), cos(al));
+    dirs[3 * r + 1] = DM(cos(be), sin(al));
+    dirs[3 * r + 2] = sin(be);
+}
+
+template <int PCAP, int NT>
+int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const double* lb, const void* sph,
+                const void* whit, const void* geom, const double* dirs, const double* rx, double min_t, int n_az,
+                int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, cudaStream_t st) {
+    static bool attr = false;
+    size_t smem = sizeof(HitsSmem<PCAP, NT>);
+    if (!attr) {
+        RFS_CUDA_TRY(cudaFuncSetAttribute(k_hits<PCAP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    k_hits<PCAP, NT><<<n_tiles * (256 / NT), NT, smem, st>>>(
+        (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom, dirs, rx[0],
+        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats);
+    return RFS_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-// stats: [0] rays sent to the slow path, [1] rays whose live count exceeded
-// hcap, [2] max live count, [3] total live hits, [4] largest tile list.
-int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* geom,
-             const double* rx, double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts,
-             int* slow_list, int* stats, void* stream) {
+int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
+    int R = n_az * n_el;
+    if (R <= 0) return RFS_OK;
+    k_ray_dirs<<<rfs_ceil_div(R, 256), 256, 0, (cudaStream_t)stream>>>(n_az, n_el, dirs);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+// pcap selects the pending-ring template: 32 (128-thread blocks) or 64
+// (64-thread blocks); both use 48 KB of pending storage per block.
+int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
+             const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
-    static bool attr = false;
-    size_t smem = sizeof(HitsSmem);
-    if (!attr) {
-        RFS_CUDA_TRY(cudaFuncSetAttribute(k_hits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
     RFS_CUDA_TRY(cudaMemsetAsync(stats, 0, 8 * sizeof(int), st));
     RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)n_az * n_el, st));
     if (n_tiles <= 0) return RFS_OK;
-    k_hits<<<n_tiles * 2, HT_THREADS, smem, st>>>((const int2*)ranges, vals, lb, (const float4*)sph,
-                                                   (const RfsGeom*)geom, rx[0], rx[1], rx[2], ress_radius, n_az, n_el,
-                                                   tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats);
+    int rc;
+    if (pcap <= 32)
+        rc = launch_hits<32, 128>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
+                                  tiles_u, hcap, slab, counts, slow_list, stats, st);
+    else
+        rc = launch_hits<64, 64>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
+                                 tiles_u, hcap, slab, counts, slow_list, stats, st);
+    if (rc != RFS_OK) return rc;
     k_max_range<<<rfs_ceil_div(n_tiles, 256), 256, 0, st>>>((const int2*)ranges, n_tiles, stats + 4);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
-                  const void* sph, const void* geom, const double* rx, double ress_radius, int n_az, int n_el,
-                  int hcap, void* slab, int* counts, double* pend_t, uint32_t* pend_g, float* pend_w, int pcap,
-                  int* stats, void* stream) {
+                  const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
+                  double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
+                  uint32_t* pend_g, int pcap, int* stats, void* stream) {
     if (n_rays <= 0) return RFS_OK;
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     k_hits_slow<<<rfs_ceil_div(n_rays, 64), 64, 0, (cudaStream_t)stream>>>(
-        rays, n_rays, (const int2*)ranges, vals, lb, (const float4*)sph, (const RfsGeom*)geom, rx[0], rx[1], rx[2],
-        ress_radius, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, pend_t, pend_g, pend_w, pcap, stats);
+        rays, n_rays, (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom,
+        dirs, rx[0], rx[1], rx[2], ress_radius, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, pend_t, pend_g,
+        pcap, stats);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

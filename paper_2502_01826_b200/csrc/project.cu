@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_project(
     int n, const float* __restrict__ means, const float* __restrict__ quats,
     const float* __restrict__ log_scales, const float* __restrict__ raw, const float* __restrict__ phase,
     double rx0, double rx1, double rx2, double ress, int n_az, int n_el, int tiles_u,
-    RfsGeom* __restrict__ geom, float4* __restrict__ sph, uint32_t* __restrict__ code,
+    RfsGeom* __restrict__ geom, float4* __restrict__ sph, float4* __restrict__ whit, uint32_t* __restrict__ code,
     Rect* __restrict__ rects, uint32_t* __restrict__ counts, float4* __restrict__ rho32,
     double* __restrict__ proj, int* __restrict__ err) {
     int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -147,6 +147,34 @@ __global__ void __launch_bounds__(256) k_project(
     double thr = (r3 + 1e-6 * om) * (1.0 + 1e-6);
     thr = thr * thr;
     sph[g] = make_float4((float)ox, (float)oy, (float)oz, __double2float_ru(thr));
+
+    // fp32 whitened ellipsoid prefilter (K6).  With L = diag(e^-s) R^T
+    // (L^T L = Sigma^-1), q = L d and p = L (rx - mu), the reference
+    // discriminant is disc = 9|q|^2 - |q x p|^2, so a hit needs
+    // |q x p| <= 3|q|.  The fp32 error of |q x p| is bounded by
+    // ~10 aniso u |q||p| (u = 2^-24, aniso = e^{smax-smin}); the margin below
+    // is 4x that plus slack, so the test never rejects an fp64 hit.
+    {
+        double es[3] = {exp(-s0), exp(-s1), exp(-s2)};
+        double L[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) L[3 * a + j] = es[a] * R[3 * j + a];
+        double mm[3] = {rx0 - mx, rx1 - my, rx2 - mz};
+        double p[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) p[a] = L[3 * a] * mm[0] + L[3 * a + 1] * mm[1] + L[3 * a + 2] * mm[2];
+        double pn = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+        double smax = fmax(fmax(s0, s1), s2), smin = fmin(fmin(s0, s1), s2);
+        double aniso = exp(smax - smin);
+        double margin = 4e-6 * aniso * (pn + 1.0) + 1e-5;
+        double thw = (3.0 + margin) * (3.0 + margin);
+        whit[4 * g + 0] = make_float4((float)L[0], (float)L[1], (float)L[2], (float)L[3]);
+        whit[4 * g + 1] = make_float4((float)L[4], (float)L[5], (float)L[6], (float)L[7]);
+        whit[4 * g + 2] = make_float4((float)L[8], (float)p[0], (float)p[1], (float)p[2]);
+        whit[4 * g + 3] = make_float4(__double2float_ru(thw), 0.f, 0.f, 0.f);
+    }
 
     float fd = __double2float_rn(depth);
     code[g] = __float_as_uint(fd);
@@ -389,7 +417,7 @@ extern "C" {
 
 int rfs_project(int n, const float* means, const float* quats, const float* log_scales, const float* trans_mag_raw,
                 const float* trans_phase, const double* rx, double ress_radius, int n_az, int n_el,
-                void* geom, void* sph, uint32_t* depth_code, void* rects, uint32_t* counts, void* rho32,
+                void* geom, void* sph, void* whit, uint32_t* depth_code, void* rects, uint32_t* counts, void* rho32,
                 double* proj_out, int* err_flags, void* stream) {
     if (n < 0 || n_az < 1 || n_az > 360 || n_el < 1 || n_el > 180) return RFS_ERR_SHAPE;
     if (n == 0) return RFS_OK;
@@ -397,7 +425,7 @@ int rfs_project(int n, const float* means, const float* quats, const float* log_
     cudaStream_t st = (cudaStream_t)stream;
     k_project<<<rfs_ceil_div(n, 256), 256, 0, st>>>(
         n, means, quats, log_scales, trans_mag_raw, trans_phase, rx[0], rx[1], rx[2], ress_radius, n_az, n_el,
-        tiles_u, (RfsGeom*)geom, (float4*)sph, depth_code, (Rect*)rects, counts, (float4*)rho32, proj_out, err_flags);
+        tiles_u, (RfsGeom*)geom, (float4*)sph, (float4*)whit, depth_code, (Rect*)rects, counts, (float4*)rho32, proj_out, err_flags);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -1,14 +1,14 @@
 """Host orchestration of the sm_100a rasterizer (torch tensors + the C ABI).
 
 One step = `build_geometry` (K1-K6, transmitter independent) followed by the
-TX-batched `compute_psi` (K5), `forward` (K7) and `backward` (K8a, K8b, K9).
+TX-batched `compute_psi` (K5), `forward` (K7) and `backward` (K8a, K8i, K9).
 PyTorch supplies device memory (caching allocator) and the current CUDA
 stream; every kernel is launched through include/rfsplat_b200.h.
 
 Host synchronisations per step: one 8-byte read of M (the incidence count
 sizes the sort buffers) and one read of the hit-list statistics (slow-path
-rays, hit-capacity overflow).  Both are the analogue of the reference
-allocating its arrays from counts (_kernels.py:542-543, grad.py:224-231).
+rays, hit-capacity overflow).  Both mirror the reference allocating its
+arrays from counts (_kernels.py:542-543, grad.py:224-231).
 """
 
 from __future__ import annotations
@@ -22,11 +22,13 @@ import torch
 from . import _native
 from .errors import GeometryError, ShapeError
 
-__all__ = ["DeviceScene", "Geometry", "build_geometry", "compute_psi", "forward", "backward", "GRAD_FIELDS"]
+__all__ = ["DeviceScene", "Geometry", "build_geometry", "compute_psi", "forward", "backward", "GRAD_FIELDS",
+           "ray_directions"]
 
 TILE = 16
 MAX_TX_PER_LAUNCH = 256
-GRAD_FIELDS = ("d_mean", "d_quat", "d_log_scale", "d_trans_mag", "d_trans_mag_raw", "d_trans_phase", "d_coeffs", "d_cov")
+GRAD_FIELDS = ("d_mean", "d_quat", "d_log_scale", "d_trans_mag", "d_trans_mag_raw", "d_trans_phase", "d_coeffs",
+               "d_cov")
 
 
 def _ptr(t: torch.Tensor | None):
@@ -37,16 +39,23 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+def _mark(marks, name):
+    if marks is not None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        marks.append((name, ev))
+
+
 @dataclass
 class DeviceScene:
     """fp32 device copy of a scene's SoA parameters (the boundary's inputs)."""
 
-    means: torch.Tensor        # f32 [N,3]
-    quats: torch.Tensor        # f32 [N,4]
-    log_scales: torch.Tensor   # f32 [N,3]
+    means: torch.Tensor          # f32 [N,3]
+    quats: torch.Tensor          # f32 [N,4]
+    log_scales: torch.Tensor     # f32 [N,3]
     trans_mag_raw: torch.Tensor  # f32 [N]
-    trans_phase: torch.Tensor  # f32 [N]
-    coeffs: torch.Tensor       # c64 [N,K]
+    trans_phase: torch.Tensor    # f32 [N]
+    coeffs: torch.Tensor         # c64 [N,K]
     rx: tuple = (0.0, 0.0, 0.0)
     ress_radius: float = 1.0
     n_az: int = 360
@@ -78,7 +87,8 @@ class DeviceScene:
         ]
         for t, shape, dt in checks:
             if tuple(t.shape) != shape or t.dtype != dt or not t.is_cuda or not t.is_contiguous():
-                raise ShapeError(f"scene tensor must be contiguous CUDA {dt} of shape {shape}, got {tuple(t.shape)} {t.dtype}")
+                raise ShapeError(f"scene tensor must be contiguous CUDA {dt} of shape {shape}, "
+                                 f"got {tuple(t.shape)} {t.dtype}")
         if not (1 <= self.n_az <= 360 and 1 <= self.n_el <= 180):
             raise ShapeError("grid must satisfy 1 <= n_az <= 360, 1 <= n_el <= 180")
         if not (0 <= self.fle_degree <= 4):
@@ -96,18 +106,21 @@ class Geometry:
     tiles_v: int
     m: int
     geom: torch.Tensor
-    sph: torch.Tensor
     rho32: torch.Tensor
+    dirs: torch.Tensor
     ckeys: torch.Tensor
     vals: torch.Tensor
     ranges: torch.Tensor
-    lb: torch.Tensor
     hcap: int
     slab: torch.Tensor
     ray_counts: torch.Tensor
     stats: list = field(default_factory=list)
     proj: torch.Tensor | None = None
     sort_backend: str = "hand"
+    rx: tuple = (0.0, 0.0, 0.0)
+    ress_radius: float = 1.0
+    g_off: torch.Tensor | None = None    # by-Gaussian hit index (built on first backward)
+    g_slots: torch.Tensor | None = None
 
     @property
     def n_tiles(self) -> int:
@@ -122,7 +135,28 @@ class Geometry:
         return int(self.stats[3])
 
 
-_HCAP = {"value": 64}
+# adaptive capacities, remembered across steps
+_CAPS = {"hcap": 64, "pcap": 32}
+_DIRS: dict = {}
+
+
+def ray_directions(n_az: int, n_el: int) -> np.ndarray:
+    """render.ray_directions (render.py:103-117) with numpy, as the reference."""
+    cell = 360.0 / n_az
+    u = np.repeat(np.arange(n_az), n_el)
+    v = np.tile(np.arange(n_el), n_az)
+    alpha = np.deg2rad((u + 0.5) * cell)
+    beta = np.deg2rad((v + 0.5) * cell - 90.0)
+    return np.stack([np.cos(beta) * np.cos(alpha), np.cos(beta) * np.sin(alpha), np.sin(beta)], axis=1)
+
+
+def _dirs_table(n_az: int, n_el: int, dev) -> torch.Tensor:
+    key = (n_az, n_el, str(dev))
+    t = _DIRS.get(key)
+    if t is None:
+        t = torch.as_tensor(np.ascontiguousarray(ray_directions(n_az, n_el)), dtype=torch.float64, device=dev)
+        _DIRS[key] = t
+    return t
 
 
 def sort_end_bit(n_tiles: int) -> int:
@@ -130,38 +164,30 @@ def sort_end_bit(n_tiles: int) -> int:
 
 
 def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand"):
-    """K3: stable sort of compact keys with u32 payload; returns sorted (ckeys, vals)."""
+    """K3: stable sort of u64 keys with u32 payload; returns sorted (keys, vals)."""
     m = int(ckeys.numel())
     dev = ckeys.device
     if m <= 1:
         return ckeys, vals
-    raise_end = int(end_bit)
+    end_bit = int(end_bit)
     kalt = torch.empty_like(ckeys)
     valt = torch.empty_like(vals)
     lib = _native.load()
     res = _native.C.c_int(0)
     if backend == "hand":
-        tb = int(lib.rfs_sort_temp_bytes(m, raise_end))
+        tb = int(lib.rfs_sort_temp_bytes(m, end_bit))
         temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
-        _native.call("rfs_sort_pairs_u64", _ptr(ckeys), _ptr(vals), _ptr(kalt), _ptr(valt), m, raise_end,
+        _native.call("rfs_sort_pairs_u64", _ptr(ckeys), _ptr(vals), _ptr(kalt), _ptr(valt), m, end_bit,
                      _ptr(temp), tb, _native.C.byref(res), _stream())
-        _native.launch_counter["kernels"] += 2 + (raise_end + 7) // 8
+        _native.launch_counter["kernels"] += 2 + (end_bit + 7) // 8
     elif backend == "cub":
-        tb = int(lib.rfs_sort_cub_temp_bytes(m, raise_end))
+        tb = int(lib.rfs_sort_cub_temp_bytes(m, end_bit))
         temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
-        _native.call("rfs_sort_pairs_u64_cub", _ptr(ckeys), _ptr(vals), _ptr(kalt), _ptr(valt), m, raise_end,
+        _native.call("rfs_sort_pairs_u64_cub", _ptr(ckeys), _ptr(vals), _ptr(kalt), _ptr(valt), m, end_bit,
                      _ptr(temp), tb, _native.C.byref(res), _stream())
     else:
         raise ValueError(f"unknown sort backend {backend!r}")
     return (kalt, valt) if res.value else (ckeys, vals)
-
-
-
-def _mark(marks, name):
-    if marks is not None:
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record()
-        marks.append((name, ev))
 
 
 def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bool = False,
@@ -181,21 +207,24 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     R = n_az * n_el
     st = _stream()
     rx = (_native.C.c_double * 3)(*scene.rx)
+    dirs = _dirs_table(n_az, n_el, dev)
+    nn = max(n, 1)
 
-    geom = torch.empty(max(n, 1) * 128, dtype=torch.uint8, device=dev)
-    sph = torch.empty((max(n, 1), 4), dtype=torch.float32, device=dev)
-    code = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    rects = torch.empty(max(n, 1) * 16, dtype=torch.uint8, device=dev)
-    counts = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
-    rho32 = torch.empty((max(n, 1), 4), dtype=torch.float32, device=dev)
-    proj = torch.empty((max(n, 1), 6), dtype=torch.float64, device=dev) if want_proj else None
+    geom = torch.empty(nn * 128, dtype=torch.uint8, device=dev)
+    sph = torch.empty((nn, 4), dtype=torch.float32, device=dev)
+    whit = torch.empty((nn, 16), dtype=torch.float32, device=dev)
+    code = torch.empty(nn, dtype=torch.int32, device=dev)
+    rects = torch.empty(nn * 16, dtype=torch.uint8, device=dev)
+    counts = torch.zeros(nn, dtype=torch.int32, device=dev)
+    rho32 = torch.empty((nn, 4), dtype=torch.float32, device=dev)
+    proj = torch.empty((nn, 6), dtype=torch.float64, device=dev) if want_proj else None
     status = torch.zeros(8, dtype=torch.int32, device=dev)  # [0] error bits, [1] M
     _native.call("rfs_project", n, _ptr(scene.means), _ptr(scene.quats), _ptr(scene.log_scales),
                  _ptr(scene.trans_mag_raw), _ptr(scene.trans_phase), rx, float(scene.ress_radius), n_az, n_el,
-                 _ptr(geom), _ptr(sph), _ptr(code), _ptr(rects), _ptr(counts), _ptr(rho32), _ptr(proj),
+                 _ptr(geom), _ptr(sph), _ptr(whit), _ptr(code), _ptr(rects), _ptr(counts), _ptr(rho32), _ptr(proj),
                  _ptr(status), st)
-    offsets = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    temp = torch.empty(int(lib.rfs_scan_temp_elems(max(n, 1))), dtype=torch.int32, device=dev)
+    offsets = torch.empty(nn, dtype=torch.int32, device=dev)
+    temp = torch.empty(int(lib.rfs_scan_temp_elems(nn)), dtype=torch.int32, device=dev)
     _native.call("rfs_exclusive_scan_u32", _ptr(counts), n, _ptr(offsets), status.data_ptr() + 4, _ptr(temp), st)
     _mark(marks, "project+scan")
     host = status.cpu()  # sync #1: error flags and M
@@ -215,36 +244,39 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     _native.call("rfs_lower_bounds", _ptr(ranges), n_tiles, _ptr(vals), _ptr(geom), _ptr(lb), st)
     _mark(marks, "ranges+lb")
 
-    hc = int(hcap or _HCAP["value"])
+    hc = int(hcap or _CAPS["hcap"])
+    pc = _CAPS["pcap"]
     ray_counts = torch.empty(R, dtype=torch.int32, device=dev)
     slow = torch.empty(R, dtype=torch.int32, device=dev)
     stats = torch.zeros(8, dtype=torch.int32, device=dev)
     while True:
         slab = torch.empty(R * hc * 16, dtype=torch.uint8, device=dev)
-        _native.call("rfs_hits", _ptr(ranges), n_tiles, _ptr(vals), _ptr(lb), _ptr(sph), _ptr(geom), rx,
-                     float(scene.ress_radius), n_az, n_el, hc, _ptr(slab), _ptr(ray_counts), _ptr(slow),
-                     _ptr(stats), st)
+        _native.call("rfs_hits", _ptr(ranges), n_tiles, _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit), _ptr(geom),
+                     _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, pc, _ptr(slab), _ptr(ray_counts),
+                     _ptr(slow), _ptr(stats), st)
         _mark(marks, "hits")
         s = stats.cpu().tolist()  # sync #2
         if s[0] > 0:
-            # rays whose pending buffer overflowed: exact slow path
+            # rays whose pending ring overflowed: exact slow path, and a larger
+            # ring for the next steps if it happens often
+            if s[0] > R // 1000 and pc < 64:
+                _CAPS["pcap"] = 64
             pcap = max(int(s[4]), 1)
             nr = int(s[0])
             pt = torch.empty(nr * pcap, dtype=torch.float64, device=dev)
             pg = torch.empty(nr * pcap, dtype=torch.int32, device=dev)
-            pw = torch.empty(nr * pcap, dtype=torch.float32, device=dev)
-            _native.call("rfs_hits_slow", _ptr(slow), nr, _ptr(ranges), _ptr(vals), _ptr(lb), _ptr(sph),
-                         _ptr(geom), rx, float(scene.ress_radius), n_az, n_el, hc, _ptr(slab), _ptr(ray_counts),
-                         _ptr(pt), _ptr(pg), _ptr(pw), pcap, _ptr(stats), st)
+            _native.call("rfs_hits_slow", _ptr(slow), nr, _ptr(ranges), _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit),
+                         _ptr(geom), _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, _ptr(slab),
+                         _ptr(ray_counts), _ptr(pt), _ptr(pg), pcap, _ptr(stats), st)
             s2 = stats.cpu().tolist()
             s[1], s[2], s[3] = s2[1], s2[2], s2[3]
         if s[1] > 0:
             hc = 1 << max(6, math.ceil(math.log2(max(s[2], 1))))
-            _HCAP["value"] = max(_HCAP["value"], hc)
+            _CAPS["hcap"] = max(_CAPS["hcap"], hc)
             continue
         break
-    return Geometry(n, n_az, n_el, tiles_u, tiles_v, m, geom, sph, rho32, ckeys[:max(m, 0)], vals[:max(m, 0)],
-                    ranges, lb, hc, slab, ray_counts, s, proj, sort_backend)
+    return Geometry(n, n_az, n_el, tiles_u, tiles_v, m, geom, rho32, dirs, ckeys[:max(m, 0)], vals[:max(m, 0)],
+                    ranges, hc, slab, ray_counts, s, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
 
 
 def _check_tx(tx: torch.Tensor) -> torch.Tensor:
@@ -274,10 +306,34 @@ def forward(geo: Geometry, psi: torch.Tensor) -> torch.Tensor:
     return S
 
 
+def gauss_index(geo: Geometry) -> None:
+    """K8i: by-Gaussian index of the live hit slots (TX independent, cached)."""
+    if geo.g_off is not None:
+        return
+    lib = _native.load()
+    dev = geo.slab.device
+    st = _stream()
+    R = geo.n_rays
+    ray_off = torch.empty(R, dtype=torch.int32, device=dev)
+    tot = torch.empty(1, dtype=torch.int32, device=dev)
+    temp = torch.empty(int(lib.rfs_scan_temp_elems(R)), dtype=torch.int32, device=dev)
+    _native.call("rfs_exclusive_scan_u32", _ptr(geo.ray_counts), R, _ptr(ray_off), _ptr(tot), _ptr(temp), st)
+    h = geo.total_hits  # counts <= hcap here (hit-capacity overflow was resolved in build_geometry)
+    keys = torch.empty(max(h, 1), dtype=torch.int64, device=dev)
+    slots = torch.empty(max(h, 1), dtype=torch.int32, device=dev)
+    _native.call("rfs_hit_keys", _ptr(geo.slab), _ptr(geo.ray_counts), _ptr(ray_off), geo.hcap, R, _ptr(keys),
+                 _ptr(slots), st)
+    bits = max(1, math.ceil(math.log2(max(geo.n, 2))))
+    keys, slots = sort_pairs(keys[:h], slots[:h], bits, geo.sort_backend)
+    g_off = torch.empty(geo.n + 1, dtype=torch.int32, device=dev)
+    _native.call("rfs_gauss_offsets", _ptr(keys), h, geo.n, _ptr(g_off), st)
+    geo.g_off, geo.g_slots = g_off, slots
+
+
 def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.Tensor,
              include_direction_chain: bool = True, psi: torch.Tensor | None = None,
              marks: list | None = None) -> dict:
-    """K8a/K8b/K9: gradients summed over the TX batch (GradientBuffer.add, grad.py:85-92).
+    """K8a/K8i/K9: gradients summed over the TX batch (GradientBuffer.add, grad.py:85-92).
 
     grad_S is the complex-packed upstream lambda = dL/dRe S + i dL/dIm S
     (grad.py:4-8), which is also PyTorch's gradient convention for complex
@@ -293,46 +349,44 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     grad_S = grad_S.to(torch.complex64).contiguous()
     st = _stream()
     out = {
-        "d_mean": torch.zeros((n, 3), dtype=torch.float32, device=dev),
-        "d_quat": torch.zeros((n, 4), dtype=torch.float32, device=dev),
-        "d_log_scale": torch.zeros((n, 3), dtype=torch.float32, device=dev),
-        "d_trans_mag": torch.zeros(n, dtype=torch.float32, device=dev),
-        "d_trans_mag_raw": torch.zeros(n, dtype=torch.float32, device=dev),
-        "d_trans_phase": torch.zeros(n, dtype=torch.float32, device=dev),
-        "d_coeffs": torch.zeros((n, K), dtype=torch.complex64, device=dev),
-        "d_cov": torch.zeros((n, 3, 3), dtype=torch.float32, device=dev),
+        "d_mean": torch.empty((n, 3), dtype=torch.float32, device=dev),
+        "d_quat": torch.empty((n, 4), dtype=torch.float32, device=dev),
+        "d_log_scale": torch.empty((n, 3), dtype=torch.float32, device=dev),
+        "d_trans_mag": torch.empty(n, dtype=torch.float32, device=dev),
+        "d_trans_mag_raw": torch.empty(n, dtype=torch.float32, device=dev),
+        "d_trans_phase": torch.empty(n, dtype=torch.float32, device=dev),
+        "d_coeffs": torch.empty((n, K), dtype=torch.complex64, device=dev),
+        "d_cov": torch.empty((n, 3, 3), dtype=torch.float32, device=dev),
     }
     if n == 0 or b == 0:
+        for v in out.values():
+            v.zero_()
         return out
     R = geo.n_rays
     gslab = torch.zeros(R * geo.hcap * 4, dtype=torch.float32, device=dev)
-    gacc = torch.zeros(n * 16, dtype=torch.float32, device=dev)
     chunks = []
     for c0 in range(0, b, MAX_TX_PER_LAUNCH):
         c1 = min(b, c0 + MAX_TX_PER_LAUNCH)
         txc = tx[c0:c1].contiguous()
-        if psi is not None and c0 == 0 and c1 == b:
-            psic = psi
-        else:
-            psic = compute_psi(scene, txc)
-        P = torch.zeros((n, c1 - c0), dtype=torch.complex64, device=dev)
+        psic = psi if (psi is not None and c0 == 0 and c1 == b) else compute_psi(scene, txc)
         lam = grad_S[c0:c1].contiguous()
+        lamT = torch.empty((R, c1 - c0), dtype=torch.complex64, device=dev)
         _native.call("rfs_backward_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, _ptr(psic), _ptr(lam),
-                     _ptr(geo.rho32), c1 - c0, R, _ptr(P), _ptr(gslab), st)
-        chunks.append((txc, P))
+                     _ptr(geo.rho32), c1 - c0, R, _ptr(gslab), _ptr(lamT), st)
+        chunks.append((txc, lamT))
     _mark(marks, "backward_rays")
-    rx = (_native.C.c_double * 3)(*scene.rx)
-    _native.call("rfs_backward_hits", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, _ptr(gslab), _ptr(geo.geom),
-                 rx, float(scene.ress_radius), geo.n_az, geo.n_el, _ptr(gacc), st)
-    _mark(marks, "backward_hits")
-    for i, (txc, P) in enumerate(chunks):
-        _native.call("rfs_grad_epilogue", n, int(txc.shape[0]), scene.fle_degree, _ptr(scene.means),
-                     _ptr(scene.quats), _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(scene.coeffs),
-                     _ptr(txc), _ptr(P), _ptr(gacc), int(bool(include_direction_chain)), int(i > 0),
+    gauss_index(geo)
+    _mark(marks, "gauss_index")
+    rx = (_native.C.c_double * 3)(*geo.rx)
+    for i, (txc, lamT) in enumerate(chunks):
+        _native.call("rfs_grad_gauss", n, int(txc.shape[0]), scene.fle_degree, _ptr(scene.means), _ptr(scene.quats),
+                     _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(scene.coeffs), _ptr(txc), _ptr(geo.geom),
+                     _ptr(geo.slab), geo.hcap, _ptr(gslab), _ptr(lamT), _ptr(geo.g_off), _ptr(geo.g_slots),
+                     _ptr(geo.dirs), rx, float(geo.ress_radius), int(bool(include_direction_chain)), int(i > 0),
                      _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]), _ptr(out["d_trans_mag"]),
                      _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]), _ptr(out["d_coeffs"]),
                      _ptr(out["d_cov"]), st)
-    _mark(marks, "epilogue")
+    _mark(marks, "grad_gauss")
     return out
 
 
@@ -349,7 +403,7 @@ def tile_index_host(geo: Geometry):
 
 
 def hit_lists_host(geo: Geometry):
-    """(counts [R], hits [R, hcap] structured g/w/T) copied to the host, for tests."""
+    """(counts [R], g [R,hcap], w [R,hcap], T [R,hcap]) copied to the host, for tests."""
     counts = geo.ray_counts.cpu().numpy()
     raw = geo.slab.view(torch.int32).reshape(geo.n_rays, geo.hcap, 4).cpu().numpy()
     g = raw[..., 0].astype(np.int64)
