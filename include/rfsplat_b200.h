@@ -95,7 +95,8 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream);
 /* K6: TX-independent live hit lists.  Replaces _collect_hits + the live walk
  * of forward_tiled / count_hits_tiled (_kernels.py:27-112, 140-192, 237-292).
  * Writes hits of ray r to slab[r*hcap ...], counts[r] = live count.  pcap
- * selects the pending ring (32 or 64 entries per ray).  stats (device
+ * selects the pending ring (<= 24 -> 24 entries per ray, 128-thread blocks;
+ * else 48 entries, 64-thread blocks).  stats (device
  * int[8]): [0] rays needing rfs_hits_slow (listed in slow_list), [1] rays
  * with live > hcap (caller must retry with larger hcap), [2] max live,
  * [3] total live hits, [4] longest tile list, [5] largest pending set. */
@@ -105,7 +106,7 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
-                  uint32_t* pend_g, int pcap, int* stats, void* stream);
+                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, void* stream);
 
 /* K5: psi[g][b] = sum_k coeffs[g][k] * basis_k(bearing of tx_b from mu_g).
  * Replaces render.py:229-238 + fle.fle_basis_with_derivs (fle.py:153-212). */

@@ -37,8 +37,8 @@ _SIGS = {
     "rfs_lower_bounds": (i32, [vp, i32, vp, vp, vp, vp]),
     "rfs_ray_dirs": (i32, [i32, i32, vp, vp]),
     "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp]),
-    "rfs_hits_slow": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, vp, vp, vp, vp, i32, vp,
-                            vp]),
+    "rfs_hits_slow": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, vp, vp, vp, vp, vp, i32,
+                            vp, vp]),
     "rfs_psi": (i32, [i32, i32, i32, vp, vp, vp, vp, vp]),
     "rfs_forward": (i32, [vp, vp, i32, vp, i32, i32, vp, vp]),
     "rfs_backward_rays": (i32, [vp, vp, i32, vp, vp, vp, i32, i32, vp, vp, vp]),

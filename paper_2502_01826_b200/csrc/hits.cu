@@ -13,9 +13,16 @@
 // so t_mid >= depth - r3, and a pending hit whose t_mid is below
 // lb[i] = min_{j>=i} (depth_j - r3_j) precedes every hit the remaining
 // candidates can produce: it is emitted at once, and a ray stops scanning as
-// soon as it terminates.  Pending (t_mid, g) pairs live in a per-thread ring
-// in shared memory; a ray that overflows it is redone by k_hits_slow with a
-// global buffer sized to its tile (exact, rarely taken).
+// soon as it terminates.  Pending (t_mid, g, w) entries live in a per-thread
+// ring in shared memory; a ray that overflows it is redone by k_hits_slow with
+// a global buffer sized to its tile (exact, rarely taken).
+//
+// Execution: one thread per ray, one block per half tile (8 x 16 rays).  Each
+// warp streams the tile's candidate list on its own (warp-private staging,
+// __syncwarp only, warp-level early exit), testing candidates in groups of 4
+// for instruction-level parallelism; the emission check runs once per group
+// with the bound of the group's first candidate (hits of the group are all
+// >= that bound, so the emitted order is unchanged).
 //
 // Arithmetic: fp32 bounding-sphere and whitened-ellipsoid tests with proven
 // margins reject most candidates; survivors run the reference's fp64 disc
@@ -27,17 +34,17 @@
 
 namespace {
 
-constexpr int HB = 64;  // candidates staged per batch
+constexpr int GRP = 4;  // candidates per ILP group
 constexpr double DINF = 1.0e300;
 
 #define DM(a, b) __dmul_rn((a), (b))
 #define DA(a, b) __dadd_rn((a), (b))
 #define DS(a, b) __dsub_rn((a), (b))
 
-// Reference quadratic (_kernels.py:45-81): returns true and t_mid on a hit.
+// Reference quadratic + midpoint density (_kernels.py:45-91): true, t_mid, w on a hit.
 __device__ __forceinline__ bool exact_hit(const RfsGeom* __restrict__ G, double dx, double dy, double dz, double u,
                                           double v, double n_az, double rx0, double rx1, double rx2, double min_t,
-                                          double& t_mid) {
+                                          double& t_mid, float& w_out) {
     double r2 = __ldg(&G->r2);
     if (r2 < 0.0) return false;
     double du = fabs(DS(u, __ldg(&G->cu)));
@@ -63,20 +70,12 @@ __device__ __forceinline__ bool exact_hit(const RfsGeom* __restrict__ G, double 
     double d1 = __ddiv_rn(DS(-b, sq), a);
     double t_in = d1 < min_t ? min_t : d1;
     t_mid = DM(0.5, DA(t_in, d2));
-    return true;
-}
-
-// Midpoint density w = norm * exp(-q(x_mid)/2), _kernels.py:82-91.
-__device__ __forceinline__ double hit_weight(const RfsGeom* __restrict__ G, double dx, double dy, double dz,
-                                             double rx0, double rx1, double rx2, double t_mid) {
-    double mx = DS(rx0, __ldg(&G->mu[0])), my = DS(rx1, __ldg(&G->mu[1])), mz = DS(rx2, __ldg(&G->mu[2]));
-    double i00 = __ldg(&G->inv[0]), i01 = __ldg(&G->inv[1]), i02 = __ldg(&G->inv[2]);
-    double i11 = __ldg(&G->inv[3]), i12 = __ldg(&G->inv[4]), i22 = __ldg(&G->inv[5]);
     double ex = DA(DM(t_mid, dx), mx), ey = DA(DM(t_mid, dy), my), ez = DA(DM(t_mid, dz), mz);
     double qf = DA(DA(DM(DA(DA(DM(i00, ex), DM(i01, ey)), DM(i02, ez)), ex),
                       DM(DA(DA(DM(i01, ex), DM(i11, ey)), DM(i12, ez)), ey)),
                    DM(DA(DA(DM(i02, ex), DM(i12, ey)), DM(i22, ez)), ez));
-    return DM(__ldg(&G->norm), exp(DM(-0.5, qf)));
+    w_out = (float)DM(__ldg(&G->norm), exp(DM(-0.5, qf)));
+    return true;
 }
 
 __device__ __forceinline__ bool sphere_pass(float4 s, float d0, float d1, float d2) {
@@ -86,8 +85,10 @@ __device__ __forceinline__ bool sphere_pass(float4 s, float d0, float d1, float 
     return cx * cx + cy * cy + cz * cz <= s.w;
 }
 
-__device__ __forceinline__ bool whitened_pass(float4 a, float4 b, float4 c, float thr, float d0, float d1, float d2) {
-    // L rows: (a.x a.y a.z) (a.w b.x b.y) (b.z b.w c.x); p = (c.y c.z c.w)
+__device__ __forceinline__ bool whitened_pass(const float4* __restrict__ wp, float d0, float d1, float d2) {
+    // L rows: (a.x a.y a.z) (a.w b.x b.y) (b.z b.w c.x); p = (c.y c.z c.w); threshold e.x
+    const float4 a = __ldg(wp), b = __ldg(wp + 1), c = __ldg(wp + 2);
+    const float thr = __ldg(wp + 3).x;
     float q0 = a.x * d0 + a.y * d1 + a.z * d2;
     float q1 = a.w * d0 + b.x * d1 + b.y * d2;
     float q2 = b.z * d0 + b.w * d1 + c.x * d2;
@@ -107,17 +108,16 @@ struct Ray {
 };
 
 // Emit one hit in sorted order: terminate, record, advance T (_kernels.py:186-191).
-__device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, double t_mid, const RfsGeom* __restrict__ geom, double rx0,
-                                         double rx1, double rx2, RfsHit* __restrict__ slab_ray, int hcap) {
+__device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, float w, const RfsGeom* __restrict__ geom,
+                                         RfsHit* __restrict__ slab_ray, int hcap) {
     if (st.tre * st.tre + st.tim * st.tim < RFS_TERM_EPS2) {
         st.done = true;
         return;
     }
-    const RfsGeom* G = geom + g;
     if (st.live < hcap) {
         RfsHit h;
         h.g = g;
-        h.w = (float)hit_weight(G, st.dx, st.dy, st.dz, rx0, rx1, rx2, t_mid);
+        h.w = w;
         h.t_re = (float)st.tre;
         h.t_im = (float)st.tim;
         slab_ray[st.live] = h;
@@ -125,6 +125,7 @@ __device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, double t_mid, cons
         st.hcap_over = true;
     }
     st.live += 1;
+    const RfsGeom* G = geom + g;
     double rr = __ldg(&G->rho_re), ri = __ldg(&G->rho_im);
     double nr = st.tre * rr - st.tim * ri;
     double ni = st.tre * ri + st.tim * rr;
@@ -132,17 +133,21 @@ __device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, double t_mid, cons
     st.tim = ni;
 }
 
+struct __align__(16) Cand {
+    float4 sph;
+    double lb;
+    uint32_t g;
+    uint32_t pad;
+};
+
 template <int PCAP, int NT>
 struct HitsSmem {
     double pt[PCAP][NT];
     uint32_t pg[PCAP][NT];
-    float4 sph[HB];
-    float4 wh[HB][4];
-    double lb[HB];
-    uint32_t g[HB];
+    float pw[PCAP][NT];
+    Cand cand[NT / 32][32];
 };
 
-// One block = NT rays of one tile (NT/16 u-columns x 16 v-rows); one thread per ray.
 template <int PCAP, int NT>
 __global__ void __launch_bounds__(NT) k_hits(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ vals, const double* __restrict__ lb,
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(NT) k_hits(
     HitsSmem<PCAP, NT>& S = *reinterpret_cast<HitsSmem<PCAP, NT>*>(smem_raw);
     constexpr int PARTS = 256 / NT;
     const int tile = blockIdx.x / PARTS, part = blockIdx.x % PARTS;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int u = (tile % tiles_u) * RFS_TILE + part * (NT / 16) + (tid >> 4);
     const int v = (tile / tiles_u) * RFS_TILE + (tid & 15);
     const bool valid = u < n_az && v < n_el;
@@ -177,70 +182,81 @@ __global__ void __launch_bounds__(NT) k_hits(
     int head = 0, npend = 0, max_pend = 0;
     double head_t = DINF;
     const int2 rg = ranges[tile];
+    Cand* W = S.cand[wid];
 
-    for (int base = rg.x; base < rg.y; base += HB) {
-        const int nb = min(HB, rg.y - base);
-        __syncthreads();
-        for (int j = tid; j < nb; j += NT) {
-            uint32_t g = vals[base + j];
-            S.g[j] = g;
-            S.sph[j] = __ldg(&sph[g]);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) S.wh[j][q] = __ldg(&whit[4 * g + q]);
-            S.lb[j] = lb[base + j];
+    for (int base = rg.x; base < rg.y; base += 32) {
+        if (__all_sync(0xffffffffu, st.done)) break;
+        const int nb = min(32, rg.y - base);
+        if (lane < nb) {
+            Cand c;
+            c.g = vals[base + lane];
+            c.sph = __ldg(&sph[c.g]);
+            c.lb = lb[base + lane];
+            c.pad = 0;
+            W[lane] = c;
         }
-        __syncthreads();
+        __syncwarp();
         if (!st.done) {
-            for (int j = 0; j < nb; ++j) {
-                if (head_t < S.lb[j]) {
-                    // every pending hit with t_mid < lb[j] is final: emit in order
-                    do {
-                        int hs = head % PCAP;
-                        emit_hit(st, S.pg[hs][tid], head_t, geom, rx0, rx1, rx2, slab_ray, hcap);
-                        ++head;
-                        --npend;
-                        head_t = npend > 0 ? S.pt[head % PCAP][tid] : DINF;
-                    } while (!st.done && head_t < S.lb[j]);
+            for (int j = 0; j < nb; j += GRP) {
+                // emit every pending hit that precedes all candidates >= j
+                const double lbj = W[j].lb;
+                while (head_t < lbj) {
+                    emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap);
+                    if (++head == PCAP) head = 0;
+                    --npend;
+                    head_t = npend > 0 ? S.pt[head][tid] : DINF;
                     if (st.done) break;
                 }
-                if (!sphere_pass(S.sph[j], st.fx, st.fy, st.fz)) continue;
-                if (!whitened_pass(S.wh[j][0], S.wh[j][1], S.wh[j][2], S.wh[j][3].x, st.fx, st.fy, st.fz)) continue;
-                const uint32_t g = S.g[j];
-                double t_mid;
-                if (!exact_hit(geom + g, st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid)) continue;
-                if (npend == PCAP) {
-                    pend_over = true;
-                    st.done = true;
-                    break;
-                }
-                // sorted insertion by (t_mid, g)
-                int k = npend;
-                while (k > 0) {
-                    int ps = (head + k - 1) % PCAP;
-                    double pt = S.pt[ps][tid];
-                    if (pt > t_mid || (pt == t_mid && S.pg[ps][tid] > g)) {
-                        int qs = (head + k) % PCAP;
-                        S.pt[qs][tid] = pt;
-                        S.pg[qs][tid] = S.pg[ps][tid];
-                        --k;
-                    } else {
+                if (st.done) break;
+                unsigned pass = 0;
+#pragma unroll
+                for (int q = 0; q < GRP; ++q)
+                    if (j + q < nb && sphere_pass(W[j + q].sph, st.fx, st.fy, st.fz)) pass |= 1u << q;
+                while (pass) {
+                    const int q = __ffs(pass) - 1;
+                    pass &= pass - 1;
+                    const uint32_t g = W[j + q].g;
+                    if (!whitened_pass(whit + 4 * g, st.fx, st.fy, st.fz)) continue;
+                    double t_mid;
+                    float w;
+                    if (!exact_hit(geom + g, st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid, w))
+                        continue;
+                    if (npend == PCAP) {
+                        pend_over = true;
+                        st.done = true;
                         break;
                     }
+                    // sorted insertion by (t_mid, g) into the ring [head, head + npend)
+                    int k = npend;
+                    int ps = head + k - 1;
+                    if (ps >= PCAP) ps -= PCAP;
+                    while (k > 0) {
+                        const double pt = S.pt[ps][tid];
+                        if (!(pt > t_mid || (pt == t_mid && S.pg[ps][tid] > g))) break;
+                        int qs = ps + 1 == PCAP ? 0 : ps + 1;
+                        S.pt[qs][tid] = pt;
+                        S.pg[qs][tid] = S.pg[ps][tid];
+                        S.pw[qs][tid] = S.pw[ps][tid];
+                        --k;
+                        ps = ps == 0 ? PCAP - 1 : ps - 1;
+                    }
+                    int qs = ps + 1 == PCAP ? 0 : ps + 1;
+                    S.pt[qs][tid] = t_mid;
+                    S.pg[qs][tid] = g;
+                    S.pw[qs][tid] = w;
+                    ++npend;
+                    max_pend = max(max_pend, npend);
+                    head_t = fmin(head_t, t_mid);
                 }
-                int qs = (head + k) % PCAP;
-                S.pt[qs][tid] = t_mid;
-                S.pg[qs][tid] = g;
-                ++npend;
-                max_pend = max(max_pend, npend);
-                head_t = fmin(head_t, t_mid);
+                if (st.done) break;
             }
         }
-        if (__syncthreads_and(st.done)) break;
+        __syncwarp();
     }
     // drain: every candidate was seen, the pending hits are final
     while (!st.done && npend > 0) {
-        emit_hit(st, S.pg[head % PCAP][tid], S.pt[head % PCAP][tid], geom, rx0, rx1, rx2, slab_ray, hcap);
-        ++head;
+        emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap);
+        if (++head == PCAP) head = 0;
         --npend;
     }
     if (!valid) return;
@@ -265,7 +281,7 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
                             const RfsGeom* __restrict__ geom, const double* __restrict__ dirs, double rx0, double rx1,
                             double rx2, double min_t, int n_az, int n_el, int tiles_u, int hcap,
                             RfsHit* __restrict__ slab, int* __restrict__ counts, double* __restrict__ pt,
-                            uint32_t* __restrict__ pg, int pcap, int* __restrict__ stats) {
+                            uint32_t* __restrict__ pg, float* __restrict__ pw, int pcap, int* __restrict__ stats) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_rays) return;
     const int r = rays[i];
@@ -286,12 +302,13 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
     RfsHit* slab_ray = slab + (size_t)r * hcap;
     double* my_t = pt + (size_t)i * pcap;
     uint32_t* my_g = pg + (size_t)i * pcap;
+    float* my_w = pw + (size_t)i * pcap;
     int head = 0, npend = 0;
     const int2 rg = ranges[tile];
     for (int j = rg.x; j < rg.y && !st.done; ++j) {
         const double lbj = lb[j];
         while (npend > 0 && my_t[head] < lbj) {
-            emit_hit(st, my_g[head], my_t[head], geom, rx0, rx1, rx2, slab_ray, hcap);
+            emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap);
             ++head;
             --npend;
             if (st.done) break;
@@ -299,26 +316,27 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
         if (st.done) break;
         const uint32_t g = vals[j];
         if (!sphere_pass(__ldg(&sph[g]), st.fx, st.fy, st.fz)) continue;
-        if (!whitened_pass(__ldg(&whit[4 * g]), __ldg(&whit[4 * g + 1]), __ldg(&whit[4 * g + 2]),
-                           __ldg(&whit[4 * g + 3]).x, st.fx, st.fy, st.fz))
-            continue;
+        if (!whitened_pass(whit + 4 * g, st.fx, st.fy, st.fz)) continue;
         double t_mid;
+        float w;
         if (!exact_hit(geom + g, st.dx, st.dy, st.dz, (double)u, (double)v, (double)n_az, rx0, rx1, rx2, min_t,
-                       t_mid))
+                       t_mid, w))
             continue;
         // linear layout [head, head + npend): total inserts <= tile length <= pcap
         int k = head + npend;
         while (k > head && (my_t[k - 1] > t_mid || (my_t[k - 1] == t_mid && my_g[k - 1] > g))) {
             my_t[k] = my_t[k - 1];
             my_g[k] = my_g[k - 1];
+            my_w[k] = my_w[k - 1];
             --k;
         }
         my_t[k] = t_mid;
         my_g[k] = g;
+        my_w[k] = w;
         ++npend;
     }
     while (!st.done && npend > 0) {
-        emit_hit(st, my_g[head], my_t[head], geom, rx0, rx1, rx2, slab_ray, hcap);
+        emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap);
         ++head;
         --npend;
     }
@@ -376,8 +394,8 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
     return RFS_OK;
 }
 
-// pcap selects the pending-ring template: 32 (128-thread blocks) or 64
-// (64-thread blocks); both use 48 KB of pending storage per block.
+// pcap selects the pending-ring template: 24 entries (128-thread blocks,
+// 4 blocks/SM) or 48 entries (64-thread blocks) for dense scenes.
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
              int pcap, void* slab, int* counts, int* slow_list, int* stats, void* stream) {
@@ -387,11 +405,11 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
     RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)n_az * n_el, st));
     if (n_tiles <= 0) return RFS_OK;
     int rc;
-    if (pcap <= 32)
-        rc = launch_hits<32, 128>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
+    if (pcap <= 24)
+        rc = launch_hits<24, 128>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
                                   tiles_u, hcap, slab, counts, slow_list, stats, st);
     else
-        rc = launch_hits<64, 64>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
+        rc = launch_hits<48, 64>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
                                  tiles_u, hcap, slab, counts, slow_list, stats, st);
     if (rc != RFS_OK) return rc;
     k_max_range<<<rfs_ceil_div(n_tiles, 256), 256, 0, st>>>((const int2*)ranges, n_tiles, stats + 4);
@@ -402,13 +420,13 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
-                  uint32_t* pend_g, int pcap, int* stats, void* stream) {
+                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, void* stream) {
     if (n_rays <= 0) return RFS_OK;
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     k_hits_slow<<<rfs_ceil_div(n_rays, 64), 64, 0, (cudaStream_t)stream>>>(
         rays, n_rays, (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom,
         dirs, rx[0], rx[1], rx[2], ress_radius, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, pend_t, pend_g,
-        pcap, stats);
+        pend_w, pcap, stats);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -136,7 +136,7 @@ class Geometry:
 
 
 # adaptive capacities, remembered across steps
-_CAPS = {"hcap": 64, "pcap": 32}
+_CAPS = {"hcap": 64, "pcap": 24}
 _DIRS: dict = {}
 
 
@@ -259,15 +259,16 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         if s[0] > 0:
             # rays whose pending ring overflowed: exact slow path, and a larger
             # ring for the next steps if it happens often
-            if s[0] > R // 1000 and pc < 64:
-                _CAPS["pcap"] = 64
+            if s[0] > R // 1000 and pc < 48:
+                _CAPS["pcap"] = 48
             pcap = max(int(s[4]), 1)
             nr = int(s[0])
             pt = torch.empty(nr * pcap, dtype=torch.float64, device=dev)
             pg = torch.empty(nr * pcap, dtype=torch.int32, device=dev)
+            pw = torch.empty(nr * pcap, dtype=torch.float32, device=dev)
             _native.call("rfs_hits_slow", _ptr(slow), nr, _ptr(ranges), _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit),
                          _ptr(geom), _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, _ptr(slab),
-                         _ptr(ray_counts), _ptr(pt), _ptr(pg), pcap, _ptr(stats), st)
+                         _ptr(ray_counts), _ptr(pt), _ptr(pg), _ptr(pw), pcap, _ptr(stats), st)
             s2 = stats.cpu().tolist()
             s[1], s[2], s[3] = s2[1], s2[2], s2[3]
         if s[1] > 0:
