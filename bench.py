@@ -227,7 +227,7 @@ def run_ours(args):
     kern = {
         "forward": (ab["forward"], ph_ms.get("forward")),
         "backward": (ab["backward"] + ab["epilogue"],
-                     ph_ms.get("backward_rays", 0) + ph_ms.get("gauss_index", 0) + ph_ms.get("grad_gauss", 0)),
+                     sum(ph_ms.get(k, 0) for k in ("backward_rays", "gauss_index", "grad_geom", "grad_tx"))),
     }
     roof = {}
     for k, (byts, ms) in kern.items():

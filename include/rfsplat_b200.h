@@ -120,11 +120,13 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
 
 /* K8a: TX-batched reverse sweep (_ray_backward's complex part,
  * _kernels.py:369-387, 522): per hit, accumulates (+=) the TX-reduced
- * scalars {Re(T C), d|rho|, d(phase)} into gslab and writes lambda
- * transposed (lamT complex64[R*n_tx]).  n_tx <= 256 per call; gslab must be
- * zeroed before the first call of a step. */
+ * scalars {Re(T C), d|rho|, d(phase)} into gslab.  Optionally writes lambda
+ * transposed (lamT complex64[R*n_tx], for the deterministic p_acc gather)
+ * and/or adds p_acc[g][b] += conj(lam_b) w T with vector atomics into P
+ * (complex64[N*n_tx], zeroed by the caller).  Both are nullable.
+ * n_tx <= 256 per call; gslab must be zeroed before the first call. */
 int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam,
-                      const void* rho32, int n_tx, int n_rays, void* gslab, void* lamT, void* stream);
+                      const void* rho32, int n_tx, int n_rays, void* gslab, void* lamT, void* P, void* stream);
 
 /* K8i: by-Gaussian index of the live hit slots (TX independent):
  * keys[ray_off[r]+k] = Gaussian id, slots[...] = r*hcap + k; sort the pairs
@@ -133,21 +135,27 @@ int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, i
                  uint32_t* slots, void* stream);
 int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream);
 
-/* K9: per-Gaussian backward, one warp per Gaussian over its hits, no
- * atomics: mean / covariance chains in fp64 (_kernels.py:387-520, summed in
- * the fixed slot order like the reference's bincount, grad.py:243-254),
- * p_acc and d_coeffs = conj(p_acc) conj(basis) (grad.py:252-255), bearing
- * chain (grad.py:167-189), chain_cov_to_shape (grad.py:134-164) and
- * d_trans_mag_raw = d|rho| sigma(1-sigma) (train.py:161-162).
- * accumulate = 0 writes every output (first TX chunk of a step);
- * accumulate = 1 adds only the TX-dependent terms of a further chunk.
- * d_cov is nullable. */
-int rfs_grad_gauss(int n, int n_tx, int degree, const float* means, const float* quats, const float* log_scales,
-                   const float* trans_mag_raw, const void* coeffs, const float* tx, const void* geom, const void* slab,
-                   int hcap, const void* gslab, const void* lamT, const int* g_off, const uint32_t* g_slots,
-                   const double* dirs, const double* rx, double ress_radius, int include_direction_chain, int accumulate,
-                   float* d_mean, float* d_quat, float* d_log_scale, float* d_trans_mag, float* d_trans_mag_raw,
-                   float* d_trans_phase, void* d_coeffs, float* d_cov, void* stream);
+/* K9a: per-Gaussian TX-independent chains, one warp per Gaussian over its
+ * hits, fp64, fixed slot order (the reference's bincount, grad.py:243-254):
+ * mean / covariance (_kernels.py:387-520), d|rho|, d(phase); then
+ * chain_cov_to_shape (grad.py:134-164) and d_trans_mag_raw =
+ * d|rho| sigma(1-sigma) (train.py:161-162).  Writes d_mean (direct term),
+ * d_quat, d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov
+ * (nullable).  Deterministic. */
+int rfs_grad_geom(int n, const float* quats, const float* log_scales, const float* trans_mag_raw, const void* geom,
+                  const void* slab, int hcap, const void* gslab, const int* g_off, const uint32_t* g_slots,
+                  const double* dirs, const double* rx, double ress_radius, float* d_mean, float* d_quat,
+                  float* d_log_scale, float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov,
+                  void* stream);
+
+/* K9b: per-Gaussian TX-dependent terms: d_coeffs = conj(p_acc) conj(basis)
+ * (grad.py:255) and the bearing chain added to d_mean (grad.py:167-189).
+ * p_acc is read from P (atomic mode) or, when P is NULL, gathered from lamT
+ * over the by-Gaussian index in fixed order (deterministic mode).
+ * accumulate = 1 adds a further TX chunk's terms.  Run after rfs_grad_geom. */
+int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
+                const void* slab, int hcap, const void* lamT, const int* g_off, const uint32_t* g_slots,
+                int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs, void* stream);
 
 /* Library / build identification. */
 int rfs_version(void);

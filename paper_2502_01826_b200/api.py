@@ -156,8 +156,11 @@ def upstream_to_ray(dL_dpower, s_frame) -> np.ndarray:
 
 
 def backward_frames(scene, txs, upstreams, include_direction_chain: bool = True,
-                    ctx: RenderContextGPU | None = None) -> GradientBuffer:
-    """Gradients summed over a TX batch (GradientBuffer.add semantics, grad.py:85-92)."""
+                    ctx: RenderContextGPU | None = None, deterministic: bool = False) -> GradientBuffer:
+    """Gradients summed over a TX batch (GradientBuffer.add semantics, grad.py:85-92).
+
+    deterministic=True makes the buffer bitwise reproducible (the reference's
+    fixed-order reduction) at some cost in speed."""
     ctx = ctx or prepare_context(scene)
     dev = ctx.scene.means.device
     tx = _tx_tensor(txs, dev)
@@ -166,18 +169,19 @@ def backward_frames(scene, txs, upstreams, include_direction_chain: bool = True,
         up = up[None]
     if up.shape != (tx.shape[0], ctx.geometry.n_az, ctx.geometry.n_el):
         raise ShapeError("upstream frame shape does not match the scene grid")
-    g = raster.backward(ctx.scene, ctx.geometry, tx, torch.as_tensor(up, device=dev), include_direction_chain)
+    g = raster.backward(ctx.scene, ctx.geometry, tx, torch.as_tensor(up, device=dev), include_direction_chain,
+                        deterministic=deterministic)
     return GradientBuffer.from_device(g)
 
 
 def backward_frame(scene, tx, upstream, workers: int = 1, include_direction_chain: bool = True,
-                   ctx: RenderContextGPU | None = None) -> GradientBuffer:
+                   ctx: RenderContextGPU | None = None, deterministic: bool = False) -> GradientBuffer:
     """grad.backward_frame (grad.py:192-259)."""
     upstream = np.asarray(upstream)
     if upstream.ndim != 2:
         raise ShapeError("upstream frame shape does not match the scene grid")
     return backward_frames(scene, np.asarray(tx, dtype=np.float64).reshape(1, 3), upstream[None],
-                           include_direction_chain, ctx)
+                           include_direction_chain, ctx, deterministic)
 
 
 SCENE_FIELDS = ("means", "quats", "log_scales", "trans_mag_raw", "trans_phase", "coeffs")

@@ -77,7 +77,7 @@ constexpr int BR_MAXJ = 8;  // up to 256 TX per launch (lane owns b = lane + 32 
 __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
     const RfsHit* __restrict__ slab, const int* __restrict__ counts, int hcap, const float2* __restrict__ psi,
     const float2* __restrict__ lam, const float4* __restrict__ rho32, int nb, int R, float4* __restrict__ gslab,
-    float2* __restrict__ lamT) {
+    float2* __restrict__ lamT, float2* __restrict__ P) {
     extern __shared__ __align__(16) float2 s_lam[];  // [nb][BR_RAYS + 1]
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int r0 = blockIdx.x * BR_RAYS;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
     // lambda transposed to [R][nb] rows for the per-Gaussian gather of K9
     for (int i = threadIdx.x; i < nb * BR_RAYS; i += BR_THREADS) {
         int rl = i / nb, b = i % nb, r = r0 + rl;
-        if (r < R) lamT[(size_t)r * nb + b] = s_lam[b * (BR_RAYS + 1) + rl];
+        if (lamT && r < R) lamT[(size_t)r * nb + b] = s_lam[b * (BR_RAYS + 1) + rl];
     }
     const int nj = (nb + 31) >> 5;
     for (int rl = wid; rl < BR_RAYS; rl += BR_THREADS / 32) {
@@ -115,10 +115,16 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
             RfsHit hk = h[k];
             const float2* row = psi + (size_t)hk.g * nb;
             float2 c = make_float2(0.f, 0.f);
+            const float2 wt = make_float2(hk.w * hk.t_re, hk.w * hk.t_im);
 #pragma unroll
             for (int j = 0; j < BR_MAXJ; ++j) {
                 int b = lane + 32 * j;
-                if (j < nj && b < nb) c = caddf(c, cmulf(cl[j], __ldg(&row[b])));
+                if (j < nj && b < nb) {
+                    c = caddf(c, cmulf(cl[j], __ldg(&row[b])));
+                    // p_acc[g][b] += conj(lam_b) w T (inc_pg + bincount, grad.py:252-254):
+                    // one 8-byte vector reduction per lane, coalesced over the row
+                    if (P) atomicAdd(&P[(size_t)hk.g * nb + b], cmulf(cl[j], wt));
+                }
             }
             double cr = (double)c.x, ci = (double)c.y;
 #pragma unroll
@@ -216,7 +222,7 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
 }
 
 int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam, const void* rho32,
-                      int n_tx, int n_rays, void* gslab, void* lamT, void* stream) {
+                      int n_tx, int n_rays, void* gslab, void* lamT, void* P, void* stream) {
     if (n_rays <= 0 || n_tx <= 0) return RFS_OK;
     if (n_tx > 32 * BR_MAXJ) return RFS_ERR_SHAPE;
     size_t smem = (size_t)n_tx * (BR_RAYS + 1) * sizeof(float2);
@@ -227,7 +233,7 @@ int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void*
     }
     k_backward_rays<<<rfs_ceil_div(n_rays, BR_RAYS), BR_THREADS, smem, (cudaStream_t)stream>>>(
         (const RfsHit*)slab, counts, hcap, (const float2*)psi, (const float2*)lam, (const float4*)rho32, n_tx, n_rays,
-        (float4*)gslab, (float2*)lamT);
+        (float4*)gslab, (float2*)lamT, (float2*)P);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -333,13 +333,18 @@ def gauss_index(geo: Geometry) -> None:
 
 def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.Tensor,
              include_direction_chain: bool = True, psi: torch.Tensor | None = None,
-             marks: list | None = None) -> dict:
+             marks: list | None = None, deterministic: bool = False) -> dict:
     """K8a/K8i/K9: gradients summed over the TX batch (GradientBuffer.add, grad.py:85-92).
 
     grad_S is the complex-packed upstream lambda = dL/dRe S + i dL/dIm S
     (grad.py:4-8), which is also PyTorch's gradient convention for complex
     tensors.  Returns fp32 tensors with the GradientBuffer meaning plus
     d_trans_mag_raw (the logit chain of train.py:161-162).
+
+    Every per-Gaussian sum is taken in a fixed order except p_acc (the
+    TX-dependent sum behind d_coeffs and the bearing chain), which by default
+    uses fp32 vector atomics; `deterministic=True` gathers it in fixed order
+    instead, making the whole buffer bitwise reproducible.
     """
     tx = _check_tx(tx)
     b = int(tx.shape[0])
@@ -371,23 +376,30 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         txc = tx[c0:c1].contiguous()
         psic = psi if (psi is not None and c0 == 0 and c1 == b) else compute_psi(scene, txc)
         lam = grad_S[c0:c1].contiguous()
-        lamT = torch.empty((R, c1 - c0), dtype=torch.complex64, device=dev)
+        if deterministic:
+            lamT = torch.empty((R, c1 - c0), dtype=torch.complex64, device=dev)
+            P = None
+        else:
+            lamT = None
+            P = torch.zeros((n, c1 - c0), dtype=torch.complex64, device=dev)
         _native.call("rfs_backward_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, _ptr(psic), _ptr(lam),
-                     _ptr(geo.rho32), c1 - c0, R, _ptr(gslab), _ptr(lamT), st)
-        chunks.append((txc, lamT))
+                     _ptr(geo.rho32), c1 - c0, R, _ptr(gslab), _ptr(lamT), _ptr(P), st)
+        chunks.append((txc, lamT, P))
     _mark(marks, "backward_rays")
     gauss_index(geo)
     _mark(marks, "gauss_index")
     rx = (_native.C.c_double * 3)(*geo.rx)
-    for i, (txc, lamT) in enumerate(chunks):
-        _native.call("rfs_grad_gauss", n, int(txc.shape[0]), scene.fle_degree, _ptr(scene.means), _ptr(scene.quats),
-                     _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(scene.coeffs), _ptr(txc), _ptr(geo.geom),
-                     _ptr(geo.slab), geo.hcap, _ptr(gslab), _ptr(lamT), _ptr(geo.g_off), _ptr(geo.g_slots),
-                     _ptr(geo.dirs), rx, float(geo.ress_radius), int(bool(include_direction_chain)), int(i > 0),
-                     _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]), _ptr(out["d_trans_mag"]),
-                     _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]), _ptr(out["d_coeffs"]),
-                     _ptr(out["d_cov"]), st)
-    _mark(marks, "grad_gauss")
+    _native.call("rfs_grad_geom", n, _ptr(scene.quats), _ptr(scene.log_scales), _ptr(scene.trans_mag_raw),
+                 _ptr(geo.geom), _ptr(geo.slab), geo.hcap, _ptr(gslab), _ptr(geo.g_off), _ptr(geo.g_slots),
+                 _ptr(geo.dirs), rx, float(geo.ress_radius), _ptr(out["d_mean"]), _ptr(out["d_quat"]),
+                 _ptr(out["d_log_scale"]), _ptr(out["d_trans_mag"]), _ptr(out["d_trans_mag_raw"]),
+                 _ptr(out["d_trans_phase"]), _ptr(out["d_cov"]), st)
+    _mark(marks, "grad_geom")
+    for i, (txc, lamT, P) in enumerate(chunks):
+        _native.call("rfs_grad_tx", n, int(txc.shape[0]), scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs),
+                     _ptr(txc), _ptr(P), _ptr(geo.slab), geo.hcap, _ptr(lamT), _ptr(geo.g_off), _ptr(geo.g_slots),
+                     int(bool(include_direction_chain)), int(i > 0), _ptr(out["d_mean"]), _ptr(out["d_coeffs"]), st)
+    _mark(marks, "grad_tx")
     return out
 
 

@@ -164,6 +164,29 @@ def test_backward_edge_scenes(prefix):
     _grads_ok(g, z, prefix)
 
 
+def test_backward_deterministic_mode_config1():
+    """Fixed-order p_acc: parity, and bitwise identical buffers across runs."""
+    z = load("config1_10k.npz")
+    lam = l1_upstream(z["frame"])
+    s = config1_scene()
+    g1 = api.backward_frame(s, z["tx"], lam, deterministic=True)
+    _grads_ok(g1, z, "")
+    g2 = api.backward_frame(s, z["tx"], lam, deterministic=True)
+    for k in GRAD_KEYS:
+        np.testing.assert_array_equal(getattr(g1, k), getattr(g2, k))
+
+
+def test_backward_deterministic_matches_atomic_batch():
+    s = round_to_f32(bench_scene(np.random.default_rng(12), 8_000, 180, 90))
+    txs = default_txs(40, seed=3)
+    rng = np.random.default_rng(0)
+    up = (rng.normal(size=(40, 180, 90)) + 1j * rng.normal(size=(40, 180, 90))) * 1e-3
+    a = api.backward_frames(s, txs, up, deterministic=False)
+    d = api.backward_frames(s, txs, up, deterministic=True)
+    for k in GRAD_KEYS:
+        assert class_rel(getattr(a, k), getattr(d, k)) <= 1e-4, k
+
+
 def test_backward_tx_batch_is_sum_of_singles():
     """Batch semantics = sum over TX (GradientBuffer.add, grad.py:85-92) vs the oracle."""
     s = round_to_f32(bench_scene(np.random.default_rng(8), 5_000, 180, 90))
