@@ -169,6 +169,8 @@ def run_ours(args):
     P0 = S0.abs() ** 2
     lam = (2.0 * torch.sign(P0 - (1.3 * P0 + 0.05)) / P0[0].numel() * S0).to(torch.complex64).contiguous()
     M, H = geo.m, geo.total_hits
+    hit_stats = {"max_live": geo.stats[2], "max_tile_list": geo.stats[4], "max_pending": geo.stats[5],
+                 "sphere_pass": geo.stats[6], "whitened_pass": geo.stats[7], "slow_rays": geo.stats[0]}
     R = geo.n_rays
     del S0, P0
 
@@ -280,7 +282,8 @@ def run_ours(args):
             "config": {"workload": "config 2: 100k Gaussians (cli._bench_scene seed 0), 360x180 grid, "
                                    f"{B} TX per GPU, fwd+bwd step", "gaussians": ds.n, "tx_per_gpu": B,
                        "global_tx": B * world, "grid": "360x180", "incidences_M": M, "live_hits_H": H,
-                       "sort": args.sort, "parallelism": f"dp{world} (TX-sharded, grads all-reduced)",
+                       "sort": args.sort, "hit_stats": hit_stats,
+                       "parallelism": f"dp{world} (TX-sharded, grads all-reduced)",
                        "l2": "flushed between steps (256 MB write)"},
             "roofline": rl, "kernels_roofline": roof, "phase_ms": {k: round(v, 4) for k, v in ph_ms.items()},
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clk,

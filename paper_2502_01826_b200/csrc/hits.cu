@@ -12,29 +12,33 @@
 // (depth) order; a hit's chord midpoint lies in the Gaussian's 3-sigma ball,
 // so t_mid >= depth - r3, and a pending hit whose t_mid is below
 // lb[i] = min_{j>=i} (depth_j - r3_j) precedes every hit the remaining
-// candidates can produce: it is emitted at once, and a ray stops scanning as
-// soon as it terminates.  Pending (t_mid, g, w) entries live in a per-thread
-// ring in shared memory; a ray that overflows it is redone by k_hits_slow with
-// a global buffer sized to its tile (exact, rarely taken).
+// candidates can produce: it is final and is emitted, and a ray stops
+// scanning as soon as it terminates.  Pending (t_mid, g, w) entries live in a
+// per-thread ring in shared memory; a ray that overflows it is redone by
+// k_hits_slow with a global buffer sized to its tile (exact, rarely taken).
 //
-// Execution: one thread per ray, one block per half tile (8 x 16 rays).  Each
-// warp streams the tile's candidate list on its own (warp-private staging,
-// __syncwarp only, warp-level early exit), testing candidates in groups of 4
-// for instruction-level parallelism; the emission check runs once per group
-// with the bound of the group's first candidate (hits of the group are all
-// >= that bound, so the emitted order is unchanged).
+// Execution: one thread per ray, 64-thread blocks (a 4 x 16 quarter tile, so
+// the whole grid is resident at once).  Each warp streams its tile's
+// candidate list on its own in chunks of CH:
+//   1. stage the chunk's fp32 filter data (bounding sphere, whitened ellipsoid)
+//      in warp-private shared memory (coalesced gathers, __syncwarp only);
+//   2. every lane tests all CH candidates against its ray from shared memory
+//      (no divergent global latency), building a survivor mask;
+//   3. survivors run the reference's fp64 disc prefilter + quadratic and are
+//      inserted in (t_mid, g) order;
+//   4. pending hits below the next chunk's bound are emitted.
+// Emitting once per chunk instead of per candidate does not change the order:
+// every hit of the chunk is >= its first candidate's bound.
 //
-// Arithmetic: fp32 bounding-sphere and whitened-ellipsoid tests with proven
-// margins reject most candidates; survivors run the reference's fp64 disc
-// prefilter and quadratic with the reference's operation order and no FMA
-// contraction (explicit __d*_rn), so exact ties order like the reference.
-// Ray directions come from a table built with the reference's formula
-// (render.py:103-117).  T is carried in fp64.
+// Arithmetic: the fp32 tests carry proven margins (project.cu) so they never
+// reject an fp64 hit; the fp64 test follows the reference's operation order
+// with no FMA contraction (explicit __d*_rn), so exact ties order like the
+// reference.  Ray directions come from a table built with the reference's
+// formula (render.py:103-117).  T is carried in fp64.
 #include "rfs_common.cuh"
 
 namespace {
 
-constexpr int GRP = 4;  // candidates per ILP group
 constexpr double DINF = 1.0e300;
 
 #define DM(a, b) __dmul_rn((a), (b))
@@ -85,10 +89,8 @@ __device__ __forceinline__ bool sphere_pass(float4 s, float d0, float d1, float 
     return cx * cx + cy * cy + cz * cz <= s.w;
 }
 
-__device__ __forceinline__ bool whitened_pass(const float4* __restrict__ wp, float d0, float d1, float d2) {
-    // L rows: (a.x a.y a.z) (a.w b.x b.y) (b.z b.w c.x); p = (c.y c.z c.w); threshold e.x
-    const float4 a = __ldg(wp), b = __ldg(wp + 1), c = __ldg(wp + 2);
-    const float thr = __ldg(wp + 3).x;
+// L rows: (a.x a.y a.z) (a.w b.x b.y) (b.z b.w c.x); p = (c.y c.z c.w); threshold e.x
+__device__ __forceinline__ bool whitened_pass(float4 a, float4 b, float4 c, float thr, float d0, float d1, float d2) {
     float q0 = a.x * d0 + a.y * d1 + a.z * d2;
     float q1 = a.w * d0 + b.x * d1 + b.y * d2;
     float q2 = b.z * d0 + b.w * d1 + c.x * d2;
@@ -133,22 +135,22 @@ __device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, float w, const Rfs
     st.tim = ni;
 }
 
-struct __align__(16) Cand {
-    float4 sph;
-    double lb;
-    uint32_t g;
-    uint32_t pad;
+template <int CH>
+struct WarpStage {
+    float4 sph[CH];
+    float4 wh[CH][4];
+    uint32_t g[CH];
 };
 
-template <int PCAP, int NT>
+template <int PCAP, int NT, int CH>
 struct HitsSmem {
     double pt[PCAP][NT];
     uint32_t pg[PCAP][NT];
     float pw[PCAP][NT];
-    Cand cand[NT / 32][32];
+    WarpStage<CH> ws[NT / 32];
 };
 
-template <int PCAP, int NT>
+template <int PCAP, int NT, int CH>
 __global__ void __launch_bounds__(NT) k_hits(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ vals, const double* __restrict__ lb,
     const float4* __restrict__ sph, const float4* __restrict__ whit, const RfsGeom* __restrict__ geom,
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(NT) k_hits(
     int tiles_u, int hcap, RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ slow_list,
     int* __restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    HitsSmem<PCAP, NT>& S = *reinterpret_cast<HitsSmem<PCAP, NT>*>(smem_raw);
+    HitsSmem<PCAP, NT, CH>& S = *reinterpret_cast<HitsSmem<PCAP, NT, CH>*>(smem_raw);
     constexpr int PARTS = 256 / NT;
     const int tile = blockIdx.x / PARTS, part = blockIdx.x % PARTS;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -180,87 +182,90 @@ __global__ void __launch_bounds__(NT) k_hits(
     RfsHit* slab_ray = slab + (size_t)r * hcap;
     bool pend_over = false;
     int head = 0, npend = 0, max_pend = 0;
+    int n_sph = 0, n_wh = 0;
     double head_t = DINF;
     const int2 rg = ranges[tile];
-    Cand* W = S.cand[wid];
+    WarpStage<CH>& W = S.ws[wid];
 
-    for (int base = rg.x; base < rg.y; base += 32) {
+    for (int base = rg.x; base < rg.y; base += CH) {
         if (__all_sync(0xffffffffu, st.done)) break;
-        const int nb = min(32, rg.y - base);
+        const int nb = min(CH, rg.y - base);
+        // 1. stage filter data (lane j < nb loads candidate base + j)
         if (lane < nb) {
-            Cand c;
-            c.g = vals[base + lane];
-            c.sph = __ldg(&sph[c.g]);
-            c.lb = lb[base + lane];
-            c.pad = 0;
-            W[lane] = c;
+            const uint32_t g = vals[base + lane];
+            W.g[lane] = g;
+            W.sph[lane] = __ldg(&sph[g]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) W.wh[lane][q] = __ldg(&whit[4 * g + q]);
         }
+        const double lb_next = base + nb < rg.y ? lb[base + nb] : DINF;
         __syncwarp();
         if (!st.done) {
-            for (int j = 0; j < nb; j += GRP) {
-                // emit every pending hit that precedes all candidates >= j
-                const double lbj = W[j].lb;
-                while (head_t < lbj) {
-                    emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap);
-                    if (++head == PCAP) head = 0;
-                    --npend;
-                    head_t = npend > 0 ? S.pt[head][tid] : DINF;
-                    if (st.done) break;
-                }
-                if (st.done) break;
-                unsigned pass = 0;
-#pragma unroll
-                for (int q = 0; q < GRP; ++q)
-                    if (j + q < nb && sphere_pass(W[j + q].sph, st.fx, st.fy, st.fz)) pass |= 1u << q;
-                while (pass) {
-                    const int q = __ffs(pass) - 1;
-                    pass &= pass - 1;
-                    const uint32_t g = W[j + q].g;
-                    if (!whitened_pass(whit + 4 * g, st.fx, st.fy, st.fz)) continue;
-                    double t_mid;
-                    float w;
-                    if (!exact_hit(geom + g, st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid, w))
-                        continue;
-                    if (npend == PCAP) {
-                        pend_over = true;
-                        st.done = true;
-                        break;
+            // 2. survivor mask from shared memory
+            unsigned mask = 0;
+#pragma unroll 4
+            for (int j = 0; j < nb; ++j) {
+                if (sphere_pass(W.sph[j], st.fx, st.fy, st.fz)) {
+                    ++n_sph;
+                    if (whitened_pass(W.wh[j][0], W.wh[j][1], W.wh[j][2], W.wh[j][3].x, st.fx, st.fy, st.fz)) {
+                        mask |= 1u << j;
+                        ++n_wh;
                     }
-                    // sorted insertion by (t_mid, g) into the ring [head, head + npend)
-                    int k = npend;
-                    int ps = head + k - 1;
-                    if (ps >= PCAP) ps -= PCAP;
-                    while (k > 0) {
-                        const double pt = S.pt[ps][tid];
-                        if (!(pt > t_mid || (pt == t_mid && S.pg[ps][tid] > g))) break;
-                        int qs = ps + 1 == PCAP ? 0 : ps + 1;
-                        S.pt[qs][tid] = pt;
-                        S.pg[qs][tid] = S.pg[ps][tid];
-                        S.pw[qs][tid] = S.pw[ps][tid];
-                        --k;
-                        ps = ps == 0 ? PCAP - 1 : ps - 1;
-                    }
-                    int qs = ps + 1 == PCAP ? 0 : ps + 1;
-                    S.pt[qs][tid] = t_mid;
-                    S.pg[qs][tid] = g;
-                    S.pw[qs][tid] = w;
-                    ++npend;
-                    max_pend = max(max_pend, npend);
-                    head_t = fmin(head_t, t_mid);
                 }
-                if (st.done) break;
+            }
+            // 3. exact fp64 test and sorted insertion by (t_mid, g)
+            while (mask) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const uint32_t g = W.g[j];
+                double t_mid;
+                float w;
+                if (!exact_hit(geom + g, st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid, w)) continue;
+                if (npend == PCAP) {
+                    pend_over = true;
+                    st.done = true;
+                    break;
+                }
+                int k = npend;
+                int ps = (head + k - 1) & (PCAP - 1);
+                while (k > 0) {
+                    const double pt = S.pt[ps][tid];
+                    if (!(pt > t_mid || (pt == t_mid && S.pg[ps][tid] > g))) break;
+                    const int qs = (ps + 1) & (PCAP - 1);
+                    S.pt[qs][tid] = pt;
+                    S.pg[qs][tid] = S.pg[ps][tid];
+                    S.pw[qs][tid] = S.pw[ps][tid];
+                    --k;
+                    ps = (ps - 1) & (PCAP - 1);
+                }
+                const int qs = (ps + 1) & (PCAP - 1);
+                S.pt[qs][tid] = t_mid;
+                S.pg[qs][tid] = g;
+                S.pw[qs][tid] = w;
+                ++npend;
+                max_pend = max(max_pend, npend);
+                head_t = fmin(head_t, t_mid);
+            }
+            // 4. emit every pending hit that precedes all later candidates
+            while (!st.done && head_t < lb_next) {
+                emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap);
+                head = (head + 1) & (PCAP - 1);
+                --npend;
+                head_t = npend > 0 ? S.pt[head][tid] : DINF;
             }
         }
         __syncwarp();
     }
-    // drain: every candidate was seen, the pending hits are final
+    // drain (also covers rays whose tile list ended with pending hits)
     while (!st.done && npend > 0) {
         emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap);
-        if (++head == PCAP) head = 0;
+        head = (head + 1) & (PCAP - 1);
         --npend;
     }
     if (!valid) return;
     atomicMax(&stats[5], max_pend);
+    atomicAdd(&stats[6], n_sph);
+    atomicAdd(&stats[7], n_wh);
     if (pend_over) {
         int idx = atomicAdd(&stats[0], 1);
         slow_list[idx] = r;
@@ -316,7 +321,9 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
         if (st.done) break;
         const uint32_t g = vals[j];
         if (!sphere_pass(__ldg(&sph[g]), st.fx, st.fy, st.fz)) continue;
-        if (!whitened_pass(whit + 4 * g, st.fx, st.fy, st.fz)) continue;
+        if (!whitened_pass(__ldg(&whit[4 * g]), __ldg(&whit[4 * g + 1]), __ldg(&whit[4 * g + 2]),
+                           __ldg(&whit[4 * g + 3]).x, st.fx, st.fy, st.fz))
+            continue;
         double t_mid;
         float w;
         if (!exact_hit(geom + g, st.dx, st.dy, st.dz, (double)u, (double)v, (double)n_az, rx0, rx1, rx2, min_t,
@@ -366,17 +373,18 @@ __global__ void k_ray_dirs(int n_az, int n_el, double* __restrict__ dirs) {
     dirs[3 * r + 2] = sin(be);
 }
 
-template <int PCAP, int NT>
+template <int PCAP, int NT, int CH>
 int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const double* lb, const void* sph,
                 const void* whit, const void* geom, const double* dirs, const double* rx, double min_t, int n_az,
                 int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, cudaStream_t st) {
     static bool attr = false;
-    size_t smem = sizeof(HitsSmem<PCAP, NT>);
+    size_t smem = sizeof(HitsSmem<PCAP, NT, CH>);
     if (!attr) {
-        RFS_CUDA_TRY(cudaFuncSetAttribute(k_hits<PCAP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        RFS_CUDA_TRY(
+            cudaFuncSetAttribute(k_hits<PCAP, NT, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    k_hits<PCAP, NT><<<n_tiles * (256 / NT), NT, smem, st>>>(
+    k_hits<PCAP, NT, CH><<<n_tiles * (256 / NT), NT, smem, st>>>(
         (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom, dirs, rx[0],
         rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats);
     return RFS_OK;
@@ -394,8 +402,9 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
     return RFS_OK;
 }
 
-// pcap selects the pending-ring template: 24 entries (128-thread blocks,
-// 4 blocks/SM) or 48 entries (64-thread blocks) for dense scenes.
+// pcap selects the pending-ring template: 16 entries (64-thread blocks, 9
+// blocks/SM), 32 entries (64-thread blocks) or 64 entries (32-thread blocks)
+// for dense scenes.
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
              int pcap, void* slab, int* counts, int* slow_list, int* stats, void* stream) {
@@ -405,12 +414,15 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
     RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)n_az * n_el, st));
     if (n_tiles <= 0) return RFS_OK;
     int rc;
-    if (pcap <= 24)
-        rc = launch_hits<24, 128>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                  tiles_u, hcap, slab, counts, slow_list, stats, st);
+    if (pcap <= 16)
+        rc = launch_hits<16, 64, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
+                                     tiles_u, hcap, slab, counts, slow_list, stats, st);
+    else if (pcap <= 32)
+        rc = launch_hits<32, 64, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
+                                     tiles_u, hcap, slab, counts, slow_list, stats, st);
     else
-        rc = launch_hits<48, 64>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                 tiles_u, hcap, slab, counts, slow_list, stats, st);
+        rc = launch_hits<64, 32, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
+                                     tiles_u, hcap, slab, counts, slow_list, stats, st);
     if (rc != RFS_OK) return rc;
     k_max_range<<<rfs_ceil_div(n_tiles, 256), 256, 0, st>>>((const int2*)ranges, n_tiles, stats + 4);
     RFS_LAUNCH_CHECK();

@@ -136,7 +136,7 @@ class Geometry:
 
 
 # adaptive capacities, remembered across steps
-_CAPS = {"hcap": 64, "pcap": 24}
+_CAPS = {"hcap": 64, "pcap": 16}
 _DIRS: dict = {}
 
 
@@ -259,8 +259,8 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         if s[0] > 0:
             # rays whose pending ring overflowed: exact slow path, and a larger
             # ring for the next steps if it happens often
-            if s[0] > R // 1000 and pc < 48:
-                _CAPS["pcap"] = 48
+            if s[0] > R // 1000 and pc < 64:
+                _CAPS["pcap"] = 2 * pc
             pcap = max(int(s[4]), 1)
             nr = int(s[0])
             pt = torch.empty(nr * pcap, dtype=torch.float64, device=dev)
