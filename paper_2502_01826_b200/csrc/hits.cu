@@ -135,11 +135,51 @@ __device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, float w, const Rfs
     st.tim = ni;
 }
 
+// Reference quadratic on a shared-memory copy of the first 13 doubles of an
+// RfsGeom record (mu[3], inv[6], norm, cu, cv, r2); same arithmetic as exact_hit.
+__device__ __forceinline__ bool exact_hit_s(const double* __restrict__ G, double dx, double dy, double dz, double u,
+                                            double v, double n_az, double rx0, double rx1, double rx2, double min_t,
+                                            double& t_mid, float& w_out) {
+    double r2 = G[12];
+    if (r2 < 0.0) return false;
+    double du = fabs(DS(u, G[10]));
+    if (DS(n_az, du) < du) du = DS(n_az, du);
+    double dv = DS(v, G[11]);
+    if (DA(DM(du, du), DM(dv, dv)) > r2) return false;
+    double mx = DS(rx0, G[0]), my = DS(rx1, G[1]), mz = DS(rx2, G[2]);
+    double i00 = G[3], i01 = G[4], i02 = G[5], i11 = G[6], i12 = G[7], i22 = G[8];
+    double sx = DA(DA(DM(i00, dx), DM(i01, dy)), DM(i02, dz));
+    double sy = DA(DA(DM(i01, dx), DM(i11, dy)), DM(i12, dz));
+    double sz = DA(DA(DM(i02, dx), DM(i12, dy)), DM(i22, dz));
+    double a = DA(DA(DM(sx, dx), DM(sy, dy)), DM(sz, dz));
+    double b = DA(DA(DM(sx, mx), DM(sy, my)), DM(sz, mz));
+    double c = DA(DA(DM(DA(DA(DM(i00, mx), DM(i01, my)), DM(i02, mz)), mx),
+                     DM(DA(DA(DM(i01, mx), DM(i11, my)), DM(i12, mz)), my)),
+                  DM(DA(DA(DM(i02, mx), DM(i12, my)), DM(i22, mz)), mz));
+    double disc = DS(DM(b, b), DM(a, DS(c, 9.0)));
+    if (disc < 0.0) return false;
+    double sq = __dsqrt_rn(disc);
+    double d2 = __ddiv_rn(DA(-b, sq), a);
+    if (d2 < min_t) return false;
+    double d1 = __ddiv_rn(DS(-b, sq), a);
+    double t_in = d1 < min_t ? min_t : d1;
+    t_mid = DM(0.5, DA(t_in, d2));
+    double ex = DA(DM(t_mid, dx), mx), ey = DA(DM(t_mid, dy), my), ez = DA(DM(t_mid, dz), mz);
+    double qf = DA(DA(DM(DA(DA(DM(i00, ex), DM(i01, ey)), DM(i02, ez)), ex),
+                      DM(DA(DA(DM(i01, ex), DM(i11, ey)), DM(i12, ez)), ey)),
+                   DM(DA(DA(DM(i02, ex), DM(i12, ey)), DM(i22, ez)), ez));
+    w_out = (float)DM(G[9], exp(DM(-0.5, qf)));
+    return true;
+}
+
+constexpr int GD = 13;  // doubles of an RfsGeom record used by the exact test
+
 template <int CH>
 struct WarpStage {
     float4 sph[CH];
     float4 wh[CH][4];
     uint32_t g[CH];
+    double gd[CH][GD];  // fp64 records of the chunk's survivor union
 };
 
 template <int PCAP, int NT, int CH>
@@ -187,22 +227,37 @@ __global__ void __launch_bounds__(NT) k_hits(
     const int2 rg = ranges[tile];
     WarpStage<CH>& W = S.ws[wid];
 
+    // register prefetch of the next chunk's filter data (lane j loads candidate base + j)
+    uint32_t pf_g = 0;
+    float4 pf_s = make_float4(0.f, 0.f, 0.f, 0.f), pf_w[4];
+    double pf_lb = DINF;
+    auto prefetch = [&](int b0) {
+        if (b0 + lane < rg.y) {
+            pf_g = vals[b0 + lane];
+            pf_s = __ldg(&sph[pf_g]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pf_w[q] = __ldg(&whit[4 * pf_g + q]);
+        }
+        pf_lb = b0 + CH < rg.y ? lb[b0 + CH] : DINF;
+    };
+    prefetch(rg.x);
+
     for (int base = rg.x; base < rg.y; base += CH) {
         if (__all_sync(0xffffffffu, st.done)) break;
         const int nb = min(CH, rg.y - base);
-        // 1. stage filter data (lane j < nb loads candidate base + j)
+        // 1. stage the prefetched chunk, start loading the next one
         if (lane < nb) {
-            const uint32_t g = vals[base + lane];
-            W.g[lane] = g;
-            W.sph[lane] = __ldg(&sph[g]);
+            W.g[lane] = pf_g;
+            W.sph[lane] = pf_s;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) W.wh[lane][q] = __ldg(&whit[4 * g + q]);
+            for (int q = 0; q < 4; ++q) W.wh[lane][q] = pf_w[q];
         }
-        const double lb_next = base + nb < rg.y ? lb[base + nb] : DINF;
+        const double lb_next = pf_lb;
         __syncwarp();
+        if (base + CH < rg.y) prefetch(base + CH);
+        // 2. survivor mask from shared memory
+        unsigned mask = 0;
         if (!st.done) {
-            // 2. survivor mask from shared memory
-            unsigned mask = 0;
 #pragma unroll 4
             for (int j = 0; j < nb; ++j) {
                 if (sphere_pass(W.sph[j], st.fx, st.fy, st.fz)) {
@@ -213,14 +268,26 @@ __global__ void __launch_bounds__(NT) k_hits(
                     }
                 }
             }
-            // 3. exact fp64 test and sorted insertion by (t_mid, g)
+        }
+        // 3a. fp64 records of the warp's survivor union -> shared memory (one load round)
+        const unsigned umask = __reduce_or_sync(0xffffffffu, mask);
+        const int nu = __popc(umask);
+        for (int e = lane; e < nu * GD; e += 32) {
+            const int s = e / GD, f = e - s * GD;
+            const int j = __fns(umask, 0, s + 1);
+            W.gd[s][f] = __ldg(reinterpret_cast<const double*>(geom + W.g[j]) + f);
+        }
+        __syncwarp();
+        if (!st.done) {
+            // 3b. exact fp64 test and sorted insertion by (t_mid, g)
             while (mask) {
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const uint32_t g = W.g[j];
+                const int s = __popc(umask & ((1u << j) - 1u));
                 double t_mid;
                 float w;
-                if (!exact_hit(geom + g, st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid, w)) continue;
+                if (!exact_hit_s(W.gd[s], st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid, w)) continue;
                 if (npend == PCAP) {
                     pend_over = true;
                     st.done = true;
