@@ -202,8 +202,10 @@ __global__ void __launch_bounds__(NT) k_hits(
     constexpr int PARTS = 256 / NT;
     const int tile = blockIdx.x / PARTS, part = blockIdx.x % PARTS;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int u = (tile % tiles_u) * RFS_TILE + part * (NT / 16) + (tid >> 4);
-    const int v = (tile / tiles_u) * RFS_TILE + (tid & 15);
+    // each warp owns a 4 (u) x 8 (v) patch of the 16 x 16 tile
+    const int q = part * (NT / 32) + wid, pu = q >> 1, pv = q & 1;
+    const int u = (tile % tiles_u) * RFS_TILE + 4 * pu + (lane >> 3);
+    const int v = (tile / tiles_u) * RFS_TILE + 8 * pv + (lane & 7);
     const bool valid = u < n_az && v < n_el;
     const int r = valid ? u * n_el + v : 0;
     Ray st;
@@ -227,6 +229,25 @@ __global__ void __launch_bounds__(NT) k_hits(
     const int2 rg = ranges[tile];
     WarpStage<CH>& W = S.ws[wid];
 
+    // Warp cone: axis c through the patch, half-angle th_p covering its rays.
+    // A ray can only hit a Gaussian whose bounding-sphere cone (axis mu - rx,
+    // half-angle th_g = asin(r3/depth)) contains it, so a candidate is
+    // relevant to the warp only if angle(c, mu - rx) <= th_p + th_g.
+    float cx = valid ? st.fx : 0.f, cy = valid ? st.fy : 0.f, cz = valid ? st.fz : 0.f;
+    cx = warp_sum(cx);
+    cy = warp_sum(cy);
+    cz = warp_sum(cz);
+    {
+        const float inv = rsqrtf(fmaxf(cx * cx + cy * cy + cz * cz, 1e-30f));
+        cx *= inv;
+        cy *= inv;
+        cz *= inv;
+    }
+    float cmin = valid ? cx * st.fx + cy * st.fy + cz * st.fz : 1.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+    const float th_p = acosf(fminf(cmin, 1.f)) + 1e-4f;
+
     // register prefetch of the next chunk's filter data (lane j loads candidate base + j)
     uint32_t pf_g = 0;
     float4 pf_s = make_float4(0.f, 0.f, 0.f, 0.f), pf_w[4];
@@ -236,7 +257,7 @@ __global__ void __launch_bounds__(NT) k_hits(
             pf_g = vals[b0 + lane];
             pf_s = __ldg(&sph[pf_g]);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) pf_w[q] = __ldg(&whit[4 * pf_g + q]);
+            for (int k = 0; k < 4; ++k) pf_w[k] = __ldg(&whit[4 * pf_g + k]);
         }
         pf_lb = b0 + CH < rg.y ? lb[b0 + CH] : DINF;
     };
@@ -245,21 +266,33 @@ __global__ void __launch_bounds__(NT) k_hits(
     for (int base = rg.x; base < rg.y; base += CH) {
         if (__all_sync(0xffffffffu, st.done)) break;
         const int nb = min(CH, rg.y - base);
-        // 1. stage the prefetched chunk, start loading the next one
+        // 1. stage the prefetched chunk, cone-cull it for the warp, start loading the next one
+        bool rel = false;
         if (lane < nb) {
             W.g[lane] = pf_g;
             W.sph[lane] = pf_s;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) W.wh[lane][q] = pf_w[q];
+            for (int k = 0; k < 4; ++k) W.wh[lane][k] = pf_w[k];
+            const float ang = th_p + pf_w[3].y;
+            if (ang >= 3.1415f) {
+                rel = true;
+            } else {
+                const float m2 = pf_s.x * pf_s.x + pf_s.y * pf_s.y + pf_s.z * pf_s.z;
+                const float dotc = (cx * pf_s.x + cy * pf_s.y + cz * pf_s.z) * rsqrtf(m2);
+                rel = dotc >= cosf(ang) - 1e-5f;
+            }
         }
+        const unsigned relmask = __ballot_sync(0xffffffffu, rel);
         const double lb_next = pf_lb;
         __syncwarp();
         if (base + CH < rg.y) prefetch(base + CH);
         // 2. survivor mask from shared memory
         unsigned mask = 0;
         if (!st.done) {
-#pragma unroll 4
-            for (int j = 0; j < nb; ++j) {
+            unsigned rm = relmask;
+            while (rm) {
+                const int j = __ffs(rm) - 1;
+                rm &= rm - 1;
                 if (sphere_pass(W.sph[j], st.fx, st.fy, st.fz)) {
                     ++n_sph;
                     if (whitened_pass(W.wh[j][0], W.wh[j][1], W.wh[j][2], W.wh[j][3].x, st.fx, st.fy, st.fz)) {

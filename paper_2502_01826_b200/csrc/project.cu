@@ -173,7 +173,11 @@ __global__ void __launch_bounds__(256) k_project(
         whit[4 * g + 0] = make_float4((float)L[0], (float)L[1], (float)L[2], (float)L[3]);
         whit[4 * g + 1] = make_float4((float)L[4], (float)L[5], (float)L[6], (float)L[7]);
         whit[4 * g + 2] = make_float4((float)L[8], (float)p[0], (float)p[1], (float)p[2]);
-        whit[4 * g + 3] = make_float4(__double2float_ru(thw), 0.f, 0.f, 0.f);
+        // .y: half-angle of the bounding-sphere cone seen from rx, asin(r3/depth)
+        // (pi when rx is inside the ball), for the per-warp cone cull in K6;
+        // its axis is sph.xyz normalised.
+        double th = inside ? RFS_PI : asin(fmin(r3 / depth, 1.0)) + 1e-6;
+        whit[4 * g + 3] = make_float4(__double2float_ru(thw), __double2float_ru(th), 0.f, 0.f);
     }
 
     float fd = __double2float_rn(depth);
