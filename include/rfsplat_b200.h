@@ -118,43 +118,56 @@ int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs,
 int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, int n_tx, int n_rays, void* S,
                 void* stream);
 
-/* K8a: TX-batched reverse sweep (_ray_backward's complex part,
- * _kernels.py:369-387, 522): per hit, accumulates (+=) the TX-reduced
- * scalars {Re(T C), d|rho|, d(phase)} into gslab.  Optionally writes lambda
- * transposed (lamT complex64[R*n_tx], for the deterministic p_acc gather)
- * and/or adds p_acc[g][b] += conj(lam_b) w T with vector atomics into P
- * (complex64[N*n_tx], zeroed by the caller).  Both are nullable.
- * n_tx <= 256 per call; gslab must be zeroed before the first call. */
-int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam,
-                      const void* rho32, int n_tx, int n_rays, void* gslab, void* lamT, void* P, void* stream);
-
-/* K8i: by-Gaussian index of the live hit slots (TX independent):
- * keys[ray_off[r]+k] = Gaussian id, slots[...] = r*hcap + k; sort the pairs
- * with rfs_sort_pairs_u64 and take g_off = rfs_gauss_offsets (int32[N+1]). */
+/* K8i: by-Gaussian index of the live hits (TX independent).
+ * rfs_hit_keys: keys[ray_off[r]+k] = Gaussian id, slots[...] = r*hcap + k
+ * (ray_off = exclusive scan of counts); sort the pairs with
+ * rfs_sort_pairs_u64 (stable: (ray, k) order within a Gaussian, the slot
+ * order of the reference's bincount, grad.py:243-254);
+ * rfs_gather_sorted: per sorted hit p its ray s_ray[p], w s_w[p], w T
+ * s_wt[p] (complex64) and inv_slot[slot] = p (u32[R*hcap]);
+ * rfs_gauss_offsets: g_off (int32[N+1]) over the sorted keys. */
 int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays, uint64_t* keys,
                  uint32_t* slots, void* stream);
+int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, int hcap, const void* slab, uint32_t* s_ray,
+                      float* s_w, void* s_wt, uint32_t* inv_slot, void* stream);
 int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream);
 
-/* K9a: per-Gaussian TX-independent chains, one warp per Gaussian over its
- * hits, fp64, fixed slot order (the reference's bincount, grad.py:243-254):
- * mean / covariance (_kernels.py:387-520), d|rho|, d(phase); then
- * chain_cov_to_shape (grad.py:134-164) and d_trans_mag_raw =
- * d|rho| sigma(1-sigma) (train.py:161-162).  Writes d_mean (direct term),
- * d_quat, d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov
- * (nullable).  Deterministic. */
-int rfs_grad_geom(int n, const float* quats, const float* log_scales, const float* trans_mag_raw, const void* geom,
-                  const void* slab, int hcap, const void* gslab, const int* g_off, const uint32_t* g_slots,
-                  const double* dirs, const double* rx, double ress_radius, float* d_mean, float* d_quat,
-                  float* d_log_scale, float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov,
-                  void* stream);
+/* K8a: TX-batched reverse sweep (_ray_backward's complex part,
+ * _kernels.py:369-387, 522): per hit, accumulates (+=) the TX-reduced
+ * scalars {Re(T C), d|rho|, d(phase), 0} into s_gs (float4 per sorted hit,
+ * zeroed before the first call of a step) at the hit's sorted position.
+ * Optionally writes lambda transposed (lamT complex64[R*n_tx], for the
+ * deterministic p_acc gather) and/or adds p_acc[g][b] += conj(lam_b) w T
+ * with vector atomics into P (complex64[N*n_tx], zeroed by the caller);
+ * both are nullable.  n_tx <= 256 per call. */
+int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam,
+                      const void* rho32, int n_tx, int n_rays, const uint32_t* inv_slot, void* s_gs, void* lamT,
+                      void* P, void* stream);
+
+/* K9a/K9c: per-Gaussian TX-independent chains in fp64 with a fixed
+ * summation order (deterministic): thread per sorted hit with a warp
+ * segmented scan, per-warp partials added in warp order for Gaussians whose
+ * hits straddle warps, then per Gaussian: mean / covariance chains
+ * (_kernels.py:387-520), d|rho|, d(phase), chain_cov_to_shape
+ * (grad.py:134-164) and d_trans_mag_raw = d|rho| sigma(1-sigma)
+ * (train.py:161-162).  Writes d_mean (direct term), d_quat, d_log_scale,
+ * d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov (nullable).
+ * Scratch: acc64 f64[N*14], part_g i32[rfs_geom_part_elems(H)],
+ * part_v f64[14*rfs_geom_part_elems(H)]. */
+size_t rfs_geom_part_elems(int n_hits);
+int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
+                  const void* s_gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
+                  double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
+                  double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
+                  float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, void* stream);
 
 /* K9b: per-Gaussian TX-dependent terms: d_coeffs = conj(p_acc) conj(basis)
  * (grad.py:255) and the bearing chain added to d_mean (grad.py:167-189).
  * p_acc is read from P (atomic mode) or, when P is NULL, gathered from lamT
- * over the by-Gaussian index in fixed order (deterministic mode).
- * accumulate = 1 adds a further TX chunk's terms.  Run after rfs_grad_geom. */
+ * over the sorted hits in fixed order (deterministic mode).  accumulate = 1
+ * adds a further TX chunk's terms.  Run after rfs_grad_geom. */
 int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
-                const void* slab, int hcap, const void* lamT, const int* g_off, const uint32_t* g_slots,
+                const uint32_t* s_ray, const void* s_wt, const void* lamT, const int* g_off,
                 int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs, void* stream);
 
 /* Library / build identification. */

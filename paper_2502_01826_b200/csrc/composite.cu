@@ -2,12 +2,19 @@
 //
 //   K5  k_psi          psi[g][b] = sum_k c_gk basis_k(bearing mu_g -> tx_b)
 //   K7  k_forward      S[b][r]  = sum_k w_k T_k psi[g_k][b]                 (SpMM)
+//   K8i k_hit_keys / k_gather_sorted / k_gauss_offsets
+//                      by-Gaussian index of the live hits (TX independent):
+//                      hits sorted by Gaussian id (stable, so (ray, k) order
+//                      within a Gaussian = the reference's bincount slot
+//                      order), per sorted hit its ray, w and w T, the inverse
+//                      map slot -> sorted position, and per-Gaussian offsets
 //   K8a k_backward_rays per ray, back to front, lanes over TX:
 //                      C_k = sum_b conj(lam_b) psi[g_k][b]                  (SDDMM)
 //                      A_k = w_{k+1} C_{k+1} + rho_{k+1} A_{k+1}  (suffix recursion)
 //                      -> per-hit scalars GW_k = Re(T_k C_k), d|rho|_k, d(phase)_k
-//                      and lamT[r][b] (lambda transposed for K9, grad.cu)
-//   K8i k_hit_keys     by-Gaussian index of the hit slots (TX independent)
+//                      written at the hit's sorted position; optionally
+//                      p_acc[g][b] += conj(lam_b) w T (vector atomics) and
+//                      lambda transposed (for the deterministic gather)
 //
 // Because the backward is linear in the upstream lambda, every sum over the
 // TX batch is taken before the TX-independent geometry: per hit only GW_k
@@ -69,6 +76,48 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward(const RfsHit* __restrict
     }
 }
 
+// ------------------------------------------- K8i by-Gaussian hit index
+// keys[c] = Gaussian id, vals[c] = slab slot r*hcap + k, c = ray_off[r] + k
+__global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
+                           const uint32_t* __restrict__ ray_off, int hcap, int R, uint64_t* __restrict__ keys,
+                           uint32_t* __restrict__ slots) {
+    const int lane = threadIdx.x & 31;
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= R) return;
+    const int cnt = min(counts[r], hcap);
+    const uint32_t base = ray_off[r];
+    for (int k = lane; k < cnt; k += 32) {
+        keys[base + k] = slab[(size_t)r * hcap + k].g;
+        slots[base + k] = (uint32_t)((size_t)r * hcap + k);
+    }
+}
+
+// per sorted hit p: its ray, w, w T; inverse map slot -> p
+__global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h, int hcap,
+                                const RfsHit* __restrict__ slab, uint32_t* __restrict__ s_ray,
+                                float* __restrict__ s_w, float2* __restrict__ s_wt, uint32_t* __restrict__ inv_slot) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= h) return;
+    const uint32_t s = sorted_slots[p];
+    const RfsHit hk = slab[s];
+    s_ray[p] = s / (uint32_t)hcap;
+    s_w[p] = hk.w;
+    s_wt[p] = make_float2(hk.w * hk.t_re, hk.w * hk.t_im);
+    inv_slot[s] = (uint32_t)p;
+}
+
+// g_off[g] = lower_bound(g) over the sorted Gaussian keys, g in [0, n]
+__global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, int n, int* __restrict__ g_off) {
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g > n) return;
+    int lo = 0, hi = h;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if ((long long)keys[mid] < g) lo = mid + 1; else hi = mid;
+    }
+    g_off[g] = lo;
+}
+
 // ------------------------------------------------------- K8a backward rays
 constexpr int BR_RAYS = 32;
 constexpr int BR_THREADS = 256;
@@ -76,8 +125,9 @@ constexpr int BR_MAXJ = 8;  // up to 256 TX per launch (lane owns b = lane + 32 
 
 __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
     const RfsHit* __restrict__ slab, const int* __restrict__ counts, int hcap, const float2* __restrict__ psi,
-    const float2* __restrict__ lam, const float4* __restrict__ rho32, int nb, int R, float4* __restrict__ gslab,
-    float2* __restrict__ lamT, float2* __restrict__ P) {
+    const float2* __restrict__ lam, const float4* __restrict__ rho32, int nb, int R,
+    const uint32_t* __restrict__ inv_slot, float4* __restrict__ s_gs, float2* __restrict__ lamT,
+    float2* __restrict__ P) {
     extern __shared__ __align__(16) float2 s_lam[];  // [nb][BR_RAYS + 1]
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int r0 = blockIdx.x * BR_RAYS;
@@ -86,10 +136,11 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
         s_lam[b * (BR_RAYS + 1) + rl] = r < R ? lam[(size_t)b * R + r] : make_float2(0.f, 0.f);
     }
     __syncthreads();
-    // lambda transposed to [R][nb] rows for the per-Gaussian gather of K9
-    for (int i = threadIdx.x; i < nb * BR_RAYS; i += BR_THREADS) {
-        int rl = i / nb, b = i % nb, r = r0 + rl;
-        if (lamT && r < R) lamT[(size_t)r * nb + b] = s_lam[b * (BR_RAYS + 1) + rl];
+    if (lamT) {  // lambda transposed to [R][nb] rows for the deterministic p_acc gather
+        for (int i = threadIdx.x; i < nb * BR_RAYS; i += BR_THREADS) {
+            int rl = i / nb, b = i % nb, r = r0 + rl;
+            if (r < R) lamT[(size_t)r * nb + b] = s_lam[b * (BR_RAYS + 1) + rl];
+        }
     }
     const int nj = (nb + 31) >> 5;
     for (int rl = wid; rl < BR_RAYS; rl += BR_THREADS / 32) {
@@ -104,83 +155,93 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
             float2 l = (j < nj && b < nb) ? s_lam[b * (BR_RAYS + 1) + rl] : make_float2(0.f, 0.f);
             cl[j] = make_float2(l.x, -l.y);
         }
-        const RfsHit* h = slab + (size_t)r * hcap;
-        float4* gs = gslab + (size_t)r * hcap;
         // A: sum_b conj(lam_b) suffix_{k,b}; (wn, rn, cn) = w, rho, C of hit k+1.
         // The TX reduction and the scalar recursion run in fp64: for a
         // Gaussian that every ray crosses first, d(phase) sums ~1e3 strongly
         // cancelling Im(.) terms.
         double Ar = 0.0, Ai = 0.0, wn = 0.0, rnr = 0.0, rni = 0.0, cnr = 0.0, cni = 0.0;
-        for (int k = cnt - 1; k >= 0; --k) {
-            RfsHit hk = h[k];
-            const float2* row = psi + (size_t)hk.g * nb;
-            float2 c = make_float2(0.f, 0.f);
-            const float2 wt = make_float2(hk.w * hk.t_re, hk.w * hk.t_im);
+        for (int kc = ((cnt - 1) >> 5) << 5; kc >= 0; kc -= 32) {
+            // lane i holds hit kc + i: record, transmittance, sorted position
+            const int kk = kc + lane;
+            RfsHit hl;
+            float4 rq = make_float4(0.f, 0.f, 0.f, 0.f);
+            uint32_t pos = 0;
+            if (kk < cnt) {
+                hl = slab[(size_t)r * hcap + kk];
+                rq = __ldg(&rho32[hl.g]);
+                pos = inv_slot[(size_t)r * hcap + kk];
+            } else {
+                hl.g = 0;
+                hl.w = 0.f;
+                hl.t_re = hl.t_im = 0.f;
+            }
+            const int n_in = min(32, cnt - kc);
+            // software pipeline: psi row of the next (lower) hit in flight
+            float2 pv[BR_MAXJ], pn[BR_MAXJ];
+            {
+                const uint32_t g0 = __shfl_sync(0xffffffffu, hl.g, n_in - 1);
 #pragma unroll
-            for (int j = 0; j < BR_MAXJ; ++j) {
-                int b = lane + 32 * j;
-                if (j < nj && b < nb) {
-                    c = caddf(c, cmulf(cl[j], __ldg(&row[b])));
-                    // p_acc[g][b] += conj(lam_b) w T (inc_pg + bincount, grad.py:252-254):
-                    // one 8-byte vector reduction per lane, coalesced over the row
-                    if (P) atomicAdd(&P[(size_t)hk.g * nb + b], cmulf(cl[j], wt));
+                for (int j = 0; j < BR_MAXJ; ++j) {
+                    const int b = lane + 32 * j;
+                    pn[j] = (j < nj && b < nb) ? __ldg(&psi[(size_t)g0 * nb + b]) : make_float2(0.f, 0.f);
                 }
             }
-            double cr = (double)c.x, ci = (double)c.y;
+            for (int i = n_in - 1; i >= 0; --i) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                cr += __shfl_xor_sync(0xffffffffu, cr, o);
-                ci += __shfl_xor_sync(0xffffffffu, ci, o);
+                for (int j = 0; j < BR_MAXJ; ++j) pv[j] = pn[j];
+                const uint32_t g = __shfl_sync(0xffffffffu, hl.g, i);
+                const uint32_t gprev = __shfl_sync(0xffffffffu, hl.g, i > 0 ? i - 1 : 0);
+                if (i > 0) {
+#pragma unroll
+                    for (int j = 0; j < BR_MAXJ; ++j) {
+                        const int b = lane + 32 * j;
+                        if (j < nj && b < nb) pn[j] = __ldg(&psi[(size_t)gprev * nb + b]);
+                    }
+                }
+                const float w = __shfl_sync(0xffffffffu, hl.w, i);
+                const float tre = __shfl_sync(0xffffffffu, hl.t_re, i);
+                const float tim = __shfl_sync(0xffffffffu, hl.t_im, i);
+                const float2 wt = make_float2(w * tre, w * tim);
+                float2 c = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < BR_MAXJ; ++j) {
+                    const int b = lane + 32 * j;
+                    if (j < nj && b < nb) {
+                        c = caddf(c, cmulf(cl[j], pv[j]));
+                        // p_acc[g][b] += conj(lam_b) w T (inc_pg + bincount, grad.py:252-254):
+                        // one 8-byte vector reduction per lane, coalesced over the row
+                        if (P) atomicAdd(&P[(size_t)g * nb + b], cmulf(cl[j], wt));
+                    }
+                }
+                double cr = (double)c.x, ci = (double)c.y;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    cr += __shfl_xor_sync(0xffffffffu, cr, o);
+                    ci += __shfl_xor_sync(0xffffffffu, ci, o);
+                }
+                {
+                    double nr = wn * cnr + (rnr * Ar - rni * Ai);
+                    double ni = wn * cni + (rnr * Ai + rni * Ar);
+                    Ar = nr;
+                    Ai = ni;
+                }
+                if (lane == i) {  // the lane holding hit k writes its scalars
+                    double tr = tre, ti = tim;
+                    double gw = tr * cr - ti * ci;                     // Re(T C)          (_kernels.py:387-388)
+                    double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
+                    double dmag = tar * rq.z - tai * rq.w;             // Re(T e^{jphi} A) (_kernels.py:382-383)
+                    double dph = -(tar * rq.y + tai * rq.x);           // -Im(T rho A)     (_kernels.py:384-385)
+                    float4 o = s_gs[pos];
+                    s_gs[pos] = make_float4((float)(o.x + gw), (float)(o.y + dmag), (float)(o.z + dph), 0.f);
+                }
+                wn = w;
+                rnr = __shfl_sync(0xffffffffu, rq.x, i);
+                rni = __shfl_sync(0xffffffffu, rq.y, i);
+                cnr = cr;
+                cni = ci;
             }
-            {
-                double nr = wn * cnr + (rnr * Ar - rni * Ai);
-                double ni = wn * cni + (rnr * Ai + rni * Ar);
-                Ar = nr;
-                Ai = ni;
-            }
-            float4 rq = __ldg(&rho32[hk.g]);
-            if (lane == 0) {
-                double tr = hk.t_re, ti = hk.t_im;
-                double gw = tr * cr - ti * ci;                     // Re(T C)          (_kernels.py:387-388)
-                double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
-                double dmag = tar * rq.z - tai * rq.w;             // Re(T e^{jphi} A) (_kernels.py:382-383)
-                double dph = -(tar * rq.y + tai * rq.x);           // -Im(T rho A)     (_kernels.py:384-385)
-                float4 o = gs[k];
-                gs[k] = make_float4((float)(o.x + gw), (float)(o.y + dmag), (float)(o.z + dph), 0.f);
-            }
-            wn = hk.w;
-            rnr = rq.x;
-            rni = rq.y;
-            cnr = cr;
-            cni = ci;
         }
     }
-}
-
-// ------------------------------------------- K8i by-Gaussian hit-slot index
-__global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restrict__ counts, const uint32_t* __restrict__ ray_off,
-                           int hcap, int R, uint64_t* __restrict__ keys, uint32_t* __restrict__ slots) {
-    const int lane = threadIdx.x & 31;
-    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (r >= R) return;
-    const int cnt = min(counts[r], hcap);
-    const uint32_t base = ray_off[r];
-    for (int k = lane; k < cnt; k += 32) {
-        keys[base + k] = slab[(size_t)r * hcap + k].g;
-        slots[base + k] = (uint32_t)((size_t)r * hcap + k);
-    }
-}
-
-// g_off[g] = lower_bound(g) over the sorted Gaussian keys, g in [0, n]
-__global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, int n, int* __restrict__ g_off) {
-    int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g > n) return;
-    int lo = 0, hi = h;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if ((long long)keys[mid] < g) lo = mid + 1; else hi = mid;
-    }
-    g_off[g] = lo;
 }
 
 template <int L>
@@ -221,8 +282,32 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
     return RFS_OK;
 }
 
+int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays, uint64_t* keys,
+                 uint32_t* slots, void* stream) {
+    if (n_rays <= 0) return RFS_OK;
+    k_hit_keys<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const RfsHit*)slab, counts, ray_off, hcap, n_rays, keys, slots);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, int hcap, const void* slab, uint32_t* s_ray,
+                      float* s_w, void* s_wt, uint32_t* inv_slot, void* stream) {
+    if (n_hits <= 0) return RFS_OK;
+    k_gather_sorted<<<rfs_ceil_div(n_hits, 256), 256, 0, (cudaStream_t)stream>>>(
+        sorted_slots, n_hits, hcap, (const RfsHit*)slab, s_ray, s_w, (float2*)s_wt, inv_slot);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream) {
+    k_gauss_offsets<<<rfs_ceil_div(n + 1, 256), 256, 0, (cudaStream_t)stream>>>(keys, n_hits, n, g_off);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
 int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam, const void* rho32,
-                      int n_tx, int n_rays, void* gslab, void* lamT, void* P, void* stream) {
+                      int n_tx, int n_rays, const uint32_t* inv_slot, void* s_gs, void* lamT, void* P, void* stream) {
     if (n_rays <= 0 || n_tx <= 0) return RFS_OK;
     if (n_tx > 32 * BR_MAXJ) return RFS_ERR_SHAPE;
     size_t smem = (size_t)n_tx * (BR_RAYS + 1) * sizeof(float2);
@@ -233,22 +318,7 @@ int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void*
     }
     k_backward_rays<<<rfs_ceil_div(n_rays, BR_RAYS), BR_THREADS, smem, (cudaStream_t)stream>>>(
         (const RfsHit*)slab, counts, hcap, (const float2*)psi, (const float2*)lam, (const float4*)rho32, n_tx, n_rays,
-        (float4*)gslab, (float2*)lamT, (float2*)P);
-    RFS_LAUNCH_CHECK();
-    return RFS_OK;
-}
-
-int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays, uint64_t* keys,
-                 uint32_t* slots, void* stream) {
-    if (n_rays <= 0) return RFS_OK;
-    k_hit_keys<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-        (const RfsHit*)slab, counts, ray_off, hcap, n_rays, keys, slots);
-    RFS_LAUNCH_CHECK();
-    return RFS_OK;
-}
-
-int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream) {
-    k_gauss_offsets<<<rfs_ceil_div(n + 1, 256), 256, 0, (cudaStream_t)stream>>>(keys, n_hits, n, g_off);
+        inv_slot, (float4*)s_gs, (float2*)lamT, (float2*)P);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

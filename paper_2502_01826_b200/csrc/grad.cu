@@ -1,45 +1,152 @@
-// grad.cu -- K9: per-Gaussian backward.
+// grad.cu -- K9: per-Gaussian backward over the by-Gaussian hit index.
 //
-// K9a k_grad_geom (one warp per Gaussian, lanes over its hits, fp64, fixed
-//     order -- the slot order of the reference's bincount, grad.py:243-254):
+// K9a k_geom_seg  (thread per hit, hits in Gaussian-sorted order, fp64):
 //     mean / covariance chains of every hit (_kernels.py:387-520) scaled by
-//     the TX-reduced weight gradient GW_k of K8a, d|rho|, d(phase); then
-//     chain_cov_to_shape (grad.py:134-164) and d_trans_mag_raw
-//     = d|rho| sigma (1 - sigma) (train.py:161-162).  Deterministic.
-// K9b k_grad_tx (one warp per Gaussian, lanes over TX): p_acc[g][b]
-//     (grad.py:252-254), d_coeffs = conj(p_acc) conj(basis) (grad.py:255) and
-//     the bearing chain into d_mean (grad.py:167-189).  p_acc comes either
+//     the TX-reduced weight gradient GW_k of K8a, plus d|rho| and d(phase);
+//     a warp-level segmented scan sums the hits of each Gaussian.  Gaussians
+//     whose hits straddle warps leave per-warp partials that
+// K9a' k_geom_fix (thread per Gaussian) adds in warp order -- so every sum
+//     has a fixed order (the slot order of the reference's bincount,
+//     grad.py:243-254) and the result is deterministic.
+// K9c k_geom_final (thread per Gaussian, fp64): d_mean direct term, d_cov,
+//     d|rho|, d(phase), chain_cov_to_shape (grad.py:134-164) and
+//     d_trans_mag_raw = d|rho| sigma (1 - sigma) (train.py:161-162).
+// K9b k_grad_tx (warp per Gaussian, lanes over TX): p_acc[g][b]
+//     (grad.py:252-254), d_coeffs = conj(p_acc) conj(basis) (grad.py:255)
+//     and the bearing chain added to d_mean (grad.py:167-189).  p_acc comes
 //     from K8a's vector atomics (default) or, in deterministic mode, from a
-//     gather of lambda rows over the Gaussian's hits in fixed order.
+//     fixed-order gather of lambda rows over the Gaussian's hits.
 #include "fle.cuh"
 #include "rfs_common.cuh"
 
 namespace {
 
-constexpr int GA_THREADS = 64;   // 2 Gaussians per block (hit counts range 1 .. ~1e3)
+constexpr int NACC = 14;         // dmu[3], dcov[9], d|rho|, d(phase)
 constexpr int GB_THREADS = 128;
 constexpr int GB_MAXJ = 8;       // up to 256 TX per launch
 
-__device__ __forceinline__ double warp_sum_d(double v) {
+// ------------------------------------------------------------------ K9a
+__global__ void __launch_bounds__(256) k_geom_seg(
+    int h, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_ray, const float* __restrict__ s_w,
+    const float4* __restrict__ s_gs, const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
+    const int* __restrict__ g_off, double rx0, double rx1, double rx2, double min_t, double* __restrict__ acc64,
+    int* __restrict__ part_g, double* __restrict__ part_v) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int wglob = p >> 5;
+    const bool valid = p < h;
+    const int g = valid ? (int)sorted_g[p] : -1;
+    double v[NACC];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Sum of 32 per-lane values over the warp; afterwards lane l holds the total
-// of value l (31 shuffles instead of 32 x 5).
-__device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
+    for (int i = 0; i < NACC; ++i) v[i] = 0.0;
+    if (valid) {
+        const RfsGeom* G = geom + g;
+        const double mx = rx0 - G->mu[0], my = rx1 - G->mu[1], mz = rx2 - G->mu[2];
+        const double i00 = G->inv[0], i01 = G->inv[1], i02 = G->inv[2], i11 = G->inv[3], i12 = G->inv[4],
+                     i22 = G->inv[5];
+        const int r = (int)s_ray[p];
+        const double w = s_w[p];
+        const float4 gs = s_gs[p];
+        const double dx = dirs[3 * r], dy = dirs[3 * r + 1], dz = dirs[3 * r + 2];
+        const double e0 = i00 * mx + i01 * my + i02 * mz, e1 = i01 * mx + i11 * my + i12 * mz,
+                     e2 = i02 * mx + i12 * my + i22 * mz;
+        const double c = e0 * mx + e1 * my + e2 * mz;
+        const double p0 = i00 * dx + i01 * dy + i02 * dz, p1 = i01 * dx + i11 * dy + i12 * dz,
+                     p2 = i02 * dx + i12 * dy + i22 * dz;
+        const double a = p0 * dx + p1 * dy + p2 * dz;
+        const double b = p0 * mx + p1 * my + p2 * mz;
+        const double disc = b * b - a * (c - 9.0);
+        const double sq = sqrt(fmax(disc, 0.0));
+        const double d2 = (-b + sq) / a, d1 = (-b - sq) / a;
+        const bool clamped = d1 < min_t;
+        const double t_mid = 0.5 * ((clamped ? min_t : d1) + d2);
+        // q = Sigma^-1 (x_mid - mu) = t_mid p + e
+        const double q0 = t_mid * p0 + e0, q1 = t_mid * p1 + e1, q2 = t_mid * p2 + e2;
+        const double gww = (double)gs.x * w;
+        const double f = 0.5 * gww;
+        v[0] = gww * q0;
+        v[1] = gww * q1;
+        v[2] = gww * q2;
+        v[3] = f * (q0 * q0 - i00); v[4] = f * (q0 * q1 - i01); v[5] = f * (q0 * q2 - i02);
+        v[6] = f * (q1 * q0 - i01); v[7] = f * (q1 * q1 - i11); v[8] = f * (q1 * q2 - i12);
+        v[9] = f * (q2 * q0 - i02); v[10] = f * (q2 * q1 - i12); v[11] = f * (q2 * q2 - i22);
+        // Midpoint chain (_kernels.py:432-507).  For an unclamped chord the
+        // midpoint minimises the quadratic form along the ray, so
+        // q.d = t_mid a + b = 0 and the chain vanishes; only clamped hits
+        // carry it (the reference evaluates it to round-off).
+        if (clamped && disc >= RFS_TANGENT_EPS) {
+            const double pv[3] = {p0, p1, p2}, ev[3] = {e0, e1, e2};
+            const double s_dv = q0 * dx + q1 * dy + q2 * dz;
+            const double half = -0.5 * gww * s_dv;
+            const double inv2sq = 0.5 / sq;
+#pragma unroll 1
+            for (int ax = 0; ax < 3; ++ax) {
+                double bmu = -pv[ax], cmu = -2.0 * ev[ax];
+                double dd = (2.0 * b * bmu - a * cmu) * inv2sq;
+                v[ax] += half * ((-bmu + dd) / a);
+            }
+            const double cm9 = c - 9.0;
+#pragma unroll 1
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    double da = -pv[i] * pv[j], db = -pv[i] * ev[j], dc = -ev[i] * ev[j];
+                    double ddisc = 2.0 * b * db - cm9 * da - a * dc;
+                    v[3 + 3 * i + j] += half * ((-db + ddisc * inv2sq) / a - d2 * da / a);
+                }
+        }
+        v[12] = gs.y;
+        v[13] = gs.z;
+    }
+    // warp segmented inclusive scan by Gaussian id (segments are contiguous)
 #pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-        const bool upper = (lane & s) != 0;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int gu = __shfl_up_sync(0xffffffffu, g, o);
 #pragma unroll
-        for (int j = 0; j < s; ++j) {
-            float send = upper ? v[j] : v[j + s];
-            float keep = upper ? v[j + s] : v[j];
-            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        for (int i = 0; i < NACC; ++i) {
+            const double t = __shfl_up_sync(0xffffffffu, v[i], o);
+            if (lane >= o && gu == g) v[i] += t;
         }
     }
-    return v[0];
+    const int gd = __shfl_down_sync(0xffffffffu, g, 1);
+    const bool tail = valid && (lane == 31 || gd != g);
+    if (!tail) return;
+    const int h0 = g_off[g], h1 = g_off[g + 1];
+    const int wb = wglob << 5;
+    if (h0 >= wb && h1 - 1 <= wb + 31) {  // whole segment inside this warp
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) acc64[(size_t)g * NACC + i] = v[i];
+        return;
+    }
+    // straddling segment: partial of this warp's first (slot 0) or last (slot 1) segment
+    if (h0 < wb) {
+        part_g[2 * wglob] = g;
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) part_v[(size_t)(2 * wglob) * NACC + i] = v[i];
+    }
+    if (h1 - 1 > wb + 31) {
+        part_g[2 * wglob + 1] = g;
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) part_v[(size_t)(2 * wglob + 1) * NACC + i] = v[i];
+    }
+}
+
+// Gaussians whose hits straddle warps: add the per-warp partials in warp order.
+__global__ void k_geom_fix(int n, const int* __restrict__ g_off, const double* __restrict__ part_v,
+                           double* __restrict__ acc64) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const int h0 = g_off[g], h1 = g_off[g + 1];
+    if (h1 <= h0) return;
+    const int w0 = h0 >> 5, w1 = (h1 - 1) >> 5;
+    if (w0 == w1) return;
+    double s[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) s[i] = part_v[(size_t)(2 * w0 + 1) * NACC + i];  // last segment of w0
+    for (int w = w0 + 1; w <= w1; ++w)                                             // first segments after
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) s[i] += part_v[(size_t)(2 * w) * NACC + i];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) acc64[(size_t)g * NACC + i] = s[i];
 }
 
 // chain_cov_to_shape for one Gaussian (grad.py:123-164), fp64.
@@ -85,107 +192,54 @@ __device__ void cov_to_shape(const float* q4, const float* s3, const double* dcv
     for (int qi = 0; qi < 4; ++qi) dq[qi] = (float)((gq[qi] - dot * qu[qi]) / nrm);
 }
 
-// ------------------------------------------------------------------ K9a
-__global__ void __launch_bounds__(GA_THREADS) k_grad_geom(
-    int n, const float* __restrict__ quats, const float* __restrict__ log_scales, const float* __restrict__ raw,
-    const RfsGeom* __restrict__ geom, const RfsHit* __restrict__ slab, int hcap, const float4* __restrict__ gslab,
-    const int* __restrict__ g_off, const uint32_t* __restrict__ g_slots, const double* __restrict__ dirs, double rx0,
-    double rx1, double rx2, double min_t, float* __restrict__ d_mean, float* __restrict__ d_quat,
-    float* __restrict__ d_log_scale, float* __restrict__ d_mag, float* __restrict__ d_mag_raw,
-    float* __restrict__ d_phase, float* __restrict__ d_cov) {
-    const int lane = threadIdx.x & 31;
-    const int g = (blockIdx.x * GA_THREADS + threadIdx.x) >> 5;
+// ------------------------------------------------------------------ K9c
+__global__ void __launch_bounds__(128) k_geom_final(int n, const double* __restrict__ acc64, const float* __restrict__ quats,
+                                                   const float* __restrict__ log_scales, const float* __restrict__ raw,
+                                                   float* __restrict__ d_mean, float* __restrict__ d_quat,
+                                                   float* __restrict__ d_log_scale, float* __restrict__ d_mag,
+                                                   float* __restrict__ d_mag_raw, float* __restrict__ d_phase,
+                                                   float* __restrict__ d_cov) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
-    const int h0 = g_off[g], h1 = g_off[g + 1];
-    double acc[14];
+    double a[NACC];
 #pragma unroll
-    for (int i = 0; i < 14; ++i) acc[i] = 0.0;
-    if (h1 > h0) {
-        const RfsGeom* G = geom + g;
-        const double mx = rx0 - G->mu[0], my = rx1 - G->mu[1], mz = rx2 - G->mu[2];
-        const double i00 = G->inv[0], i01 = G->inv[1], i02 = G->inv[2], i11 = G->inv[3], i12 = G->inv[4],
-                     i22 = G->inv[5];
-        const double e0 = i00 * mx + i01 * my + i02 * mz, e1 = i01 * mx + i11 * my + i12 * mz,
-                     e2 = i02 * mx + i12 * my + i22 * mz;
-        const double c = e0 * mx + e1 * my + e2 * mz;
-        for (int h = h0 + lane; h < h1; h += 32) {
-            const uint32_t s = g_slots[h];
-            const int r = (int)(s / (uint32_t)hcap);
-            const float w = slab[s].w;
-            const float4 gs = gslab[s];
-            const double dx = dirs[3 * r], dy = dirs[3 * r + 1], dz = dirs[3 * r + 2];
-            const double p0 = i00 * dx + i01 * dy + i02 * dz, p1 = i01 * dx + i11 * dy + i12 * dz,
-                         p2 = i02 * dx + i12 * dy + i22 * dz;
-            const double a = p0 * dx + p1 * dy + p2 * dz;
-            const double b = p0 * mx + p1 * my + p2 * mz;
-            const double disc = b * b - a * (c - 9.0);
-            const double sq = sqrt(fmax(disc, 0.0));
-            const double d2 = (-b + sq) / a, d1 = (-b - sq) / a;
-            const bool clamped = d1 < min_t;
-            const double t_mid = 0.5 * ((clamped ? min_t : d1) + d2);
-            // q = Sigma^-1 (x_mid - mu) = t_mid p + e
-            const double q0 = t_mid * p0 + e0, q1 = t_mid * p1 + e1, q2 = t_mid * p2 + e2;
-            const double gww = (double)gs.x * (double)w;
-            const double f = 0.5 * gww;
-            double gmu[3] = {gww * q0, gww * q1, gww * q2};
-            double cv9[9] = {f * (q0 * q0 - i00), f * (q0 * q1 - i01), f * (q0 * q2 - i02),
-                             f * (q1 * q0 - i01), f * (q1 * q1 - i11), f * (q1 * q2 - i12),
-                             f * (q2 * q0 - i02), f * (q2 * q1 - i12), f * (q2 * q2 - i22)};
-            // Midpoint chain (_kernels.py:432-507).  For an unclamped chord the
-            // midpoint minimises the quadratic form along the ray, so
-            // q.d = t_mid a + b = 0 and the chain vanishes; only clamped hits
-            // carry it (the reference evaluates it to round-off).
-            if (clamped && disc >= RFS_TANGENT_EPS) {
-                const double pv[3] = {p0, p1, p2}, ev[3] = {e0, e1, e2};
-                const double s_dv = q0 * dx + q1 * dy + q2 * dz;
-                const double half = -0.5 * gww * s_dv;
-                const double inv2sq = 0.5 / sq;
-#pragma unroll 1
-                for (int ax = 0; ax < 3; ++ax) {
-                    double bmu = -pv[ax], cmu = -2.0 * ev[ax];
-                    double dd = (2.0 * b * bmu - a * cmu) * inv2sq;
-                    gmu[ax] += half * ((-bmu + dd) / a);
-                }
-                const double cm9 = c - 9.0;
-#pragma unroll 1
-                for (int i = 0; i < 3; ++i)
-                    for (int j = 0; j < 3; ++j) {
-                        double da = -pv[i] * pv[j], db = -pv[i] * ev[j], dc = -ev[i] * ev[j];
-                        double ddisc = 2.0 * b * db - cm9 * da - a * dc;
-                        cv9[3 * i + j] += half * ((-db + ddisc * inv2sq) / a - d2 * da / a);
-                    }
-            }
-            acc[0] += gmu[0];
-            acc[1] += gmu[1];
-            acc[2] += gmu[2];
+    for (int i = 0; i < NACC; ++i) a[i] = acc64[(size_t)g * NACC + i];
+    d_mean[3 * g + 0] = (float)a[0];
+    d_mean[3 * g + 1] = (float)a[1];
+    d_mean[3 * g + 2] = (float)a[2];
+    d_mag[g] = (float)a[12];
+    const float sg = 1.f / (1.f + expf(-raw[g]));
+    d_mag_raw[g] = (float)a[12] * sg * (1.f - sg);
+    d_phase[g] = (float)a[13];
+    if (d_cov) {
 #pragma unroll
-            for (int i = 0; i < 9; ++i) acc[3 + i] += cv9[i];
-            acc[12] += (double)gs.y;
-            acc[13] += (double)gs.z;
+        for (int i = 0; i < 9; ++i) d_cov[9 * g + i] = (float)a[3 + i];
+    }
+    cov_to_shape(quats + 4 * g, log_scales + 3 * g, a + 3, d_quat + 4 * g, d_log_scale + 3 * g);
+}
+
+// Sum of 32 per-lane values over the warp; afterwards lane l holds the total
+// of value l (31 shuffles instead of 32 x 5).
+__device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const bool upper = (lane & s) != 0;
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
+            float send = upper ? v[j] : v[j + s];
+            float keep = upper ? v[j + s] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
         }
     }
-#pragma unroll
-    for (int i = 0; i < 14; ++i) acc[i] = warp_sum_d(acc[i]);
-    if (lane != 0) return;
-    d_mean[3 * g + 0] = (float)acc[0];
-    d_mean[3 * g + 1] = (float)acc[1];
-    d_mean[3 * g + 2] = (float)acc[2];
-    d_mag[g] = (float)acc[12];
-    const float sg = 1.f / (1.f + expf(-raw[g]));
-    d_mag_raw[g] = (float)acc[12] * sg * (1.f - sg);
-    d_phase[g] = (float)acc[13];
-    if (d_cov) {
-        for (int i = 0; i < 9; ++i) d_cov[9 * g + i] = (float)acc[3 + i];
-    }
-    cov_to_shape(quats + 4 * g, log_scales + 3 * g, acc + 3, d_quat + 4 * g, d_log_scale + 3 * g);
+    return v[0];
 }
 
 // ------------------------------------------------------------------ K9b
 template <int L, bool GATHER>
 __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     int n, int nb, const float* __restrict__ means, const float2* __restrict__ coeffs, const float* __restrict__ tx,
-    const float2* __restrict__ P, const RfsHit* __restrict__ slab, int hcap, const float2* __restrict__ lamT,
-    const int* __restrict__ g_off, const uint32_t* __restrict__ g_slots, int include_dir, int accumulate,
+    const float2* __restrict__ P, const uint32_t* __restrict__ s_ray, const float2* __restrict__ s_wt,
+    const float2* __restrict__ lamT, const int* __restrict__ g_off, int include_dir, int accumulate,
     float* __restrict__ d_mean, float2* __restrict__ d_coeffs) {
     constexpr int K = Fle<L>::K;
     constexpr int NV = 2 * K;
@@ -197,7 +251,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     float2 Pj[GB_MAXJ];
     bool any = false;
     if (GATHER) {
-        // deterministic p_acc: fixed-order sum over the Gaussian's hits
+        // deterministic p_acc: fixed-order sum over the Gaussian's sorted hits
         const int h0 = g_off[g], h1 = g_off[g + 1];
 #pragma unroll
         for (int j = 0; j < GB_MAXJ; ++j) Pj[j] = make_float2(0.f, 0.f);
@@ -205,13 +259,10 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
         for (int hb = h0; hb < h1; hb += 32) {
             const int h = hb + lane;
             int r = 0;
-            float wtr = 0.f, wti = 0.f;
+            float2 wtl = make_float2(0.f, 0.f);
             if (h < h1) {
-                const uint32_t s = g_slots[h];
-                r = (int)(s / (uint32_t)hcap);
-                const RfsHit hk = slab[s];
-                wtr = hk.w * hk.t_re;
-                wti = hk.w * hk.t_im;
+                r = (int)s_ray[h];
+                wtl = s_wt[h];
             }
             const int nbh = min(32, h1 - hb);
 #pragma unroll 1
@@ -222,7 +273,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
                 for (int u = 0; u < 4; ++u) {
                     const int i = min(i0 + u, 31);
                     ri[u] = __shfl_sync(0xffffffffu, r, i);
-                    const float a = __shfl_sync(0xffffffffu, wtr, i), bq = __shfl_sync(0xffffffffu, wti, i);
+                    const float a = __shfl_sync(0xffffffffu, wtl.x, i), bq = __shfl_sync(0xffffffffu, wtl.y, i);
                     wt[u] = i0 + u < nbh ? make_float2(a, bq) : make_float2(0.f, 0.f);
                 }
 #pragma unroll
@@ -306,7 +357,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
         const int i = 32 * q + lane;
         if (i < NV) dcf[i] = accumulate ? dcf[i] + mine[q] : mine[q];
     }
-    if (lane == 0) {  // K9a wrote the direct mean term; add the bearing chain
+    if (lane == 0) {  // K9c wrote the direct mean term; add the bearing chain
         d_mean[3 * g + 0] += dm0;
         d_mean[3 * g + 1] += dm1;
         d_mean[3 * g + 2] += dm2;
@@ -315,46 +366,54 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
 
 template <int L>
 void launch_tx(bool gather, unsigned grid, cudaStream_t st, int n, int nb, const float* means, const float2* coeffs,
-               const float* tx, const float2* P, const RfsHit* slab, int hcap, const float2* lamT, const int* g_off,
-               const uint32_t* g_slots, int include_dir, int accumulate, float* d_mean, float2* d_coeffs) {
+               const float* tx, const float2* P, const uint32_t* s_ray, const float2* s_wt, const float2* lamT,
+               const int* g_off, int include_dir, int accumulate, float* d_mean, float2* d_coeffs) {
     if (gather)
-        k_grad_tx<L, true><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, slab, hcap, lamT, g_off, g_slots,
+        k_grad_tx<L, true><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, s_ray, s_wt, lamT, g_off,
                                                         include_dir, accumulate, d_mean, d_coeffs);
     else
-        k_grad_tx<L, false><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, slab, hcap, lamT, g_off,
-                                                         g_slots, include_dir, accumulate, d_mean, d_coeffs);
+        k_grad_tx<L, false><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, s_ray, s_wt, lamT, g_off,
+                                                         include_dir, accumulate, d_mean, d_coeffs);
 }
 
 }  // namespace
 
 extern "C" {
 
-int rfs_grad_geom(int n, const float* quats, const float* log_scales, const float* trans_mag_raw, const void* geom,
-                  const void* slab, int hcap, const void* gslab, const int* g_off, const uint32_t* g_slots,
-                  const double* dirs, const double* rx, double ress_radius, float* d_mean, float* d_quat,
-                  float* d_log_scale, float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov,
-                  void* stream) {
+size_t rfs_geom_part_elems(int n_hits) { return (size_t)2 * (size_t)((n_hits + 31) / 32 + 1); }
+
+int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
+                  const void* s_gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
+                  double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
+                  double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
+                  float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, void* stream) {
     if (n <= 0) return RFS_OK;
-    k_grad_geom<<<rfs_ceil_div((long long)n * 32, GA_THREADS), GA_THREADS, 0, (cudaStream_t)stream>>>(
-        n, quats, log_scales, trans_mag_raw, (const RfsGeom*)geom, (const RfsHit*)slab, hcap, (const float4*)gslab,
-        g_off, g_slots, dirs, rx[0], rx[1], rx[2], ress_radius, d_mean, d_quat, d_log_scale, d_trans_mag,
-        d_trans_mag_raw, d_trans_phase, d_cov);
+    cudaStream_t st = (cudaStream_t)stream;
+    RFS_CUDA_TRY(cudaMemsetAsync(acc64, 0, sizeof(double) * NACC * (size_t)n, st));
+    if (n_hits > 0) {
+        k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, sorted_g, s_ray, s_w, (const float4*)s_gs,
+                                                               (const RfsGeom*)geom, dirs, g_off, rx[0], rx[1], rx[2],
+                                                               ress_radius, acc64, part_g, part_v);
+        k_geom_fix<<<rfs_ceil_div(n, 256), 256, 0, st>>>(n, g_off, part_v, acc64);
+    }
+    k_geom_final<<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, acc64, quats, log_scales, trans_mag_raw, d_mean, d_quat,
+                                                       d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
 int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
-                const void* slab, int hcap, const void* lamT, const int* g_off, const uint32_t* g_slots,
+                const uint32_t* s_ray, const void* s_wt, const void* lamT, const int* g_off,
                 int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs, void* stream) {
     if (n <= 0) return RFS_OK;
     if (n_tx > 32 * GB_MAXJ) return RFS_ERR_SHAPE;
     const bool gather = P == nullptr;
-    if (gather && (lamT == nullptr || g_off == nullptr || g_slots == nullptr)) return RFS_ERR_CONTRACT;
+    if (gather && (lamT == nullptr || g_off == nullptr || s_ray == nullptr || s_wt == nullptr)) return RFS_ERR_CONTRACT;
     cudaStream_t st = (cudaStream_t)stream;
     unsigned grid = (unsigned)rfs_ceil_div((long long)n * 32, GB_THREADS);
-#define RFS_TX(LL)                                                                                               \
-    launch_tx<LL>(gather, grid, st, n, n_tx, means, (const float2*)coeffs, tx, (const float2*)P, (const RfsHit*)slab, \
-                  hcap, (const float2*)lamT, g_off, g_slots, include_direction_chain, accumulate, d_mean,        \
+#define RFS_TX(LL)                                                                                                   \
+    launch_tx<LL>(gather, grid, st, n, n_tx, means, (const float2*)coeffs, tx, (const float2*)P, s_ray,               \
+                  (const float2*)s_wt, (const float2*)lamT, g_off, include_direction_chain, accumulate, d_mean,       \
                   (float2*)d_coeffs)
     switch (degree) {
         case 0: RFS_TX(0); break;

@@ -119,8 +119,7 @@ class Geometry:
     sort_backend: str = "hand"
     rx: tuple = (0.0, 0.0, 0.0)
     ress_radius: float = 1.0
-    g_off: torch.Tensor | None = None    # by-Gaussian hit index (built on first backward)
-    g_slots: torch.Tensor | None = None
+    gidx: dict | None = None             # by-Gaussian hit index (built on first backward)
 
     @property
     def n_tiles(self) -> int:
@@ -308,8 +307,13 @@ def forward(geo: Geometry, psi: torch.Tensor) -> torch.Tensor:
 
 
 def gauss_index(geo: Geometry) -> None:
-    """K8i: by-Gaussian index of the live hit slots (TX independent, cached)."""
-    if geo.g_off is not None:
+    """K8i: by-Gaussian index of the live hits (TX independent, cached on geo).
+
+    Hits sorted by Gaussian id with a stable sort, so within a Gaussian they
+    keep the (ray, k) order of the reference's bincount slots
+    (grad.py:222-254); per sorted hit: ray, w, w T; inverse slot map.
+    """
+    if geo.gidx is not None:
         return
     lib = _native.load()
     dev = geo.slab.device
@@ -325,10 +329,18 @@ def gauss_index(geo: Geometry) -> None:
     _native.call("rfs_hit_keys", _ptr(geo.slab), _ptr(geo.ray_counts), _ptr(ray_off), geo.hcap, R, _ptr(keys),
                  _ptr(slots), st)
     bits = max(1, math.ceil(math.log2(max(geo.n, 2))))
-    keys, slots = sort_pairs(keys[:h], slots[:h], bits, geo.sort_backend)
+    if h > 1:
+        keys, slots = sort_pairs(keys[:h], slots[:h], bits, geo.sort_backend)
     g_off = torch.empty(geo.n + 1, dtype=torch.int32, device=dev)
     _native.call("rfs_gauss_offsets", _ptr(keys), h, geo.n, _ptr(g_off), st)
-    geo.g_off, geo.g_slots = g_off, slots
+    s_ray = torch.empty(max(h, 1), dtype=torch.int32, device=dev)
+    s_w = torch.empty(max(h, 1), dtype=torch.float32, device=dev)
+    s_wt = torch.empty(max(h, 1), dtype=torch.complex64, device=dev)
+    inv_slot = torch.empty(R * geo.hcap, dtype=torch.int32, device=dev)
+    _native.call("rfs_gather_sorted", _ptr(slots), h, geo.hcap, _ptr(geo.slab), _ptr(s_ray), _ptr(s_w), _ptr(s_wt),
+                 _ptr(inv_slot), st)
+    geo.gidx = {"h": h, "sorted_g": keys, "g_off": g_off, "s_ray": s_ray, "s_w": s_w, "s_wt": s_wt,
+                "inv_slot": inv_slot}
 
 
 def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.Tensor,
@@ -369,7 +381,12 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
             v.zero_()
         return out
     R = geo.n_rays
-    gslab = torch.zeros(R * geo.hcap * 4, dtype=torch.float32, device=dev)
+    lib = _native.load()
+    gauss_index(geo)
+    gi = geo.gidx
+    h = gi["h"]
+    _mark(marks, "gauss_index")
+    s_gs = torch.zeros((max(h, 1), 4), dtype=torch.float32, device=dev)
     chunks = []
     for c0 in range(0, b, MAX_TX_PER_LAUNCH):
         c1 = min(b, c0 + MAX_TX_PER_LAUNCH)
@@ -383,21 +400,23 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
             lamT = None
             P = torch.zeros((n, c1 - c0), dtype=torch.complex64, device=dev)
         _native.call("rfs_backward_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, _ptr(psic), _ptr(lam),
-                     _ptr(geo.rho32), c1 - c0, R, _ptr(gslab), _ptr(lamT), _ptr(P), st)
+                     _ptr(geo.rho32), c1 - c0, R, _ptr(gi["inv_slot"]), _ptr(s_gs), _ptr(lamT), _ptr(P), st)
         chunks.append((txc, lamT, P))
     _mark(marks, "backward_rays")
-    gauss_index(geo)
-    _mark(marks, "gauss_index")
     rx = (_native.C.c_double * 3)(*geo.rx)
-    _native.call("rfs_grad_geom", n, _ptr(scene.quats), _ptr(scene.log_scales), _ptr(scene.trans_mag_raw),
-                 _ptr(geo.geom), _ptr(geo.slab), geo.hcap, _ptr(gslab), _ptr(geo.g_off), _ptr(geo.g_slots),
-                 _ptr(geo.dirs), rx, float(geo.ress_radius), _ptr(out["d_mean"]), _ptr(out["d_quat"]),
-                 _ptr(out["d_log_scale"]), _ptr(out["d_trans_mag"]), _ptr(out["d_trans_mag_raw"]),
-                 _ptr(out["d_trans_phase"]), _ptr(out["d_cov"]), st)
+    npart = int(lib.rfs_geom_part_elems(h))
+    acc64 = torch.empty((n, 14), dtype=torch.float64, device=dev)
+    part_g = torch.empty(npart, dtype=torch.int32, device=dev)
+    part_v = torch.empty((npart, 14), dtype=torch.float64, device=dev)
+    _native.call("rfs_grad_geom", n, h, _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(s_gs),
+                 _ptr(gi["g_off"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius), _ptr(scene.quats),
+                 _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(acc64), _ptr(part_g), _ptr(part_v),
+                 _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]), _ptr(out["d_trans_mag"]),
+                 _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]), _ptr(out["d_cov"]), st)
     _mark(marks, "grad_geom")
     for i, (txc, lamT, P) in enumerate(chunks):
         _native.call("rfs_grad_tx", n, int(txc.shape[0]), scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs),
-                     _ptr(txc), _ptr(P), _ptr(geo.slab), geo.hcap, _ptr(lamT), _ptr(geo.g_off), _ptr(geo.g_slots),
+                     _ptr(txc), _ptr(P), _ptr(gi["s_ray"]), _ptr(gi["s_wt"]), _ptr(lamT), _ptr(gi["g_off"]),
                      int(bool(include_direction_chain)), int(i > 0), _ptr(out["d_mean"]), _ptr(out["d_coeffs"]), st)
     _mark(marks, "grad_tx")
     return out
