@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--batch", type=int, default=64, help="TX per GPU")
     p.add_argument("--sort", default="hand", choices=["hand", "cub"])
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--deterministic", action="store_true", help="fixed-order p_acc (no atomics)")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=4, help="TX in the bounded CPU-baseline sample")
     return p.parse_args()
@@ -182,7 +183,7 @@ def run_ours(args):
         raster._mark(marks, "psi")
         S = raster.forward(g0, psi)
         raster._mark(marks, "forward")
-        g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks)
+        g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks, deterministic=args.deterministic)
         allreduce(g)
         raster._mark(marks, "allreduce")
         return S, g

@@ -130,10 +130,13 @@ __global__ void __launch_bounds__(256) k_geom_seg(
     }
 }
 
-// Gaussians whose hits straddle warps: add the per-warp partials in warp order.
-__global__ void k_geom_fix(int n, const int* __restrict__ g_off, const double* __restrict__ part_v,
-                           double* __restrict__ acc64) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+// Gaussians whose hits straddle warps: one warp per Gaussian, lane l adds the
+// partials of warps w0 + l, w0 + l + 32, ...; the warp tree then combines the
+// lanes -- a fixed order, so the result stays deterministic.
+__global__ void __launch_bounds__(256) k_geom_fix(int n, const int* __restrict__ g_off,
+                                                  const double* __restrict__ part_v, double* __restrict__ acc64) {
+    const int lane = threadIdx.x & 31;
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= n) return;
     const int h0 = g_off[g], h1 = g_off[g + 1];
     if (h1 <= h0) return;
@@ -141,12 +144,20 @@ __global__ void k_geom_fix(int n, const int* __restrict__ g_off, const double* _
     if (w0 == w1) return;
     double s[NACC];
 #pragma unroll
-    for (int i = 0; i < NACC; ++i) s[i] = part_v[(size_t)(2 * w0 + 1) * NACC + i];  // last segment of w0
-    for (int w = w0 + 1; w <= w1; ++w)                                             // first segments after
+    for (int i = 0; i < NACC; ++i) s[i] = 0.0;
+    for (int w = w0 + lane; w <= w1; w += 32) {
+        // warp w0 holds g's segment as its last one, later warps as their first
+        const size_t slot = w == w0 ? (size_t)(2 * w0 + 1) : (size_t)(2 * w);
 #pragma unroll
-        for (int i = 0; i < NACC; ++i) s[i] += part_v[(size_t)(2 * w) * NACC + i];
+        for (int i = 0; i < NACC; ++i) s[i] += part_v[slot * NACC + i];
+    }
 #pragma unroll
-    for (int i = 0; i < NACC; ++i) acc64[(size_t)g * NACC + i] = s[i];
+    for (int i = 0; i < NACC; ++i) {
+        double t = s[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) acc64[(size_t)g * NACC + i] = t;
+    }
 }
 
 // chain_cov_to_shape for one Gaussian (grad.py:123-164), fp64.
@@ -394,7 +405,7 @@ int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s
         k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, sorted_g, s_ray, s_w, (const float4*)s_gs,
                                                                (const RfsGeom*)geom, dirs, g_off, rx[0], rx[1], rx[2],
                                                                ress_radius, acc64, part_g, part_v);
-        k_geom_fix<<<rfs_ceil_div(n, 256), 256, 0, st>>>(n, g_off, part_v, acc64);
+        k_geom_fix<<<rfs_ceil_div((long long)n * 32, 256), 256, 0, st>>>(n, g_off, part_v, acc64);
     }
     k_geom_final<<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, acc64, quats, log_scales, trans_mag_raw, d_mean, d_quat,
                                                        d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov);
