@@ -231,8 +231,9 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
                     double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
                     double dmag = tar * rq.z - tai * rq.w;             // Re(T e^{jphi} A) (_kernels.py:382-383)
                     double dph = -(tar * rq.y + tai * rq.x);           // -Im(T rho A)     (_kernels.py:384-385)
-                    float4 o = s_gs[pos];
-                    s_gs[pos] = make_float4((float)(o.x + gw), (float)(o.y + dmag), (float)(o.z + dph), 0.f);
+                    // fire-and-forget vector reduction (one writer per launch, chunks
+                    // are stream-ordered: deterministic) -- no read-modify-write stall
+                    atomicAdd(&s_gs[pos], make_float4((float)gw, (float)dmag, (float)dph, 0.f));
                 }
                 wn = w;
                 rnr = __shfl_sync(0xffffffffu, rq.x, i);
