@@ -123,6 +123,9 @@ constexpr int BR_RAYS = 32;
 constexpr int BR_THREADS = 256;
 constexpr int BR_MAXJ = 8;  // up to 256 TX per launch (lane owns b = lane + 32 j)
 
+// NJ = ceil(n_tx / 32): TX blocks per lane, a compile-time constant so the
+// per-hit loops carry no dead predicated iterations.
+template <int NJ>
 __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
     const RfsHit* __restrict__ slab, const int* __restrict__ counts, int hcap, const float2* __restrict__ psi,
     const float2* __restrict__ lam, const float4* __restrict__ rho32, int nb, int R,
@@ -148,9 +151,9 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
         if (r >= R) break;
         const int cnt = min(counts[r], hcap);
         if (cnt == 0) continue;
-        float2 cl[BR_MAXJ];  // conj(lambda_b) for this lane's b
+        float2 cl[NJ];  // conj(lambda_b) for this lane's b
 #pragma unroll
-        for (int j = 0; j < BR_MAXJ; ++j) {
+        for (int j = 0; j < NJ; ++j) {
             int b = lane + 32 * j;
             float2 l = (j < nj && b < nb) ? s_lam[b * (BR_RAYS + 1) + rl] : make_float2(0.f, 0.f);
             cl[j] = make_float2(l.x, -l.y);
@@ -177,23 +180,23 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
             }
             const int n_in = min(32, cnt - kc);
             // software pipeline: psi row of the next (lower) hit in flight
-            float2 pv[BR_MAXJ], pn[BR_MAXJ];
+            float2 pv[NJ], pn[NJ];
             {
                 const uint32_t g0 = __shfl_sync(0xffffffffu, hl.g, n_in - 1);
 #pragma unroll
-                for (int j = 0; j < BR_MAXJ; ++j) {
+                for (int j = 0; j < NJ; ++j) {
                     const int b = lane + 32 * j;
                     pn[j] = (j < nj && b < nb) ? __ldg(&psi[(size_t)g0 * nb + b]) : make_float2(0.f, 0.f);
                 }
             }
             for (int i = n_in - 1; i >= 0; --i) {
 #pragma unroll
-                for (int j = 0; j < BR_MAXJ; ++j) pv[j] = pn[j];
+                for (int j = 0; j < NJ; ++j) pv[j] = pn[j];
                 const uint32_t g = __shfl_sync(0xffffffffu, hl.g, i);
                 const uint32_t gprev = __shfl_sync(0xffffffffu, hl.g, i > 0 ? i - 1 : 0);
                 if (i > 0) {
 #pragma unroll
-                    for (int j = 0; j < BR_MAXJ; ++j) {
+                    for (int j = 0; j < NJ; ++j) {
                         const int b = lane + 32 * j;
                         if (j < nj && b < nb) pn[j] = __ldg(&psi[(size_t)gprev * nb + b]);
                     }
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
                 const float2 wt = make_float2(w * tre, w * tim);
                 float2 c = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int j = 0; j < BR_MAXJ; ++j) {
+                for (int j = 0; j < NJ; ++j) {
                     const int b = lane + 32 * j;
                     if (j < nj && b < nb) {
                         c = caddf(c, cmulf(cl[j], pv[j]));
@@ -312,14 +315,26 @@ int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void*
     if (n_rays <= 0 || n_tx <= 0) return RFS_OK;
     if (n_tx > 32 * BR_MAXJ) return RFS_ERR_SHAPE;
     size_t smem = (size_t)n_tx * (BR_RAYS + 1) * sizeof(float2);
-    static int attr = 0;
-    if (smem > 48 * 1024 && attr < (int)smem) {
-        RFS_CUDA_TRY(cudaFuncSetAttribute(k_backward_rays, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = (int)smem;
-    }
-    k_backward_rays<<<rfs_ceil_div(n_rays, BR_RAYS), BR_THREADS, smem, (cudaStream_t)stream>>>(
-        (const RfsHit*)slab, counts, hcap, (const float2*)psi, (const float2*)lam, (const float4*)rho32, n_tx, n_rays,
-        inv_slot, (float4*)s_gs, (float2*)lamT, (float2*)P);
+    const int nj = (n_tx + 31) / 32;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned grid = (unsigned)rfs_ceil_div(n_rays, BR_RAYS);
+#define RFS_BR(NJV)                                                                                                 \
+    do {                                                                                                            \
+        static int attr = 0;                                                                                        \
+        if (smem > 48 * 1024 && attr < (int)smem) {                                                                 \
+            RFS_CUDA_TRY(                                                                                           \
+                cudaFuncSetAttribute(k_backward_rays<NJV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+            attr = (int)smem;                                                                                       \
+        }                                                                                                           \
+        k_backward_rays<NJV><<<grid, BR_THREADS, smem, st>>>(                                                       \
+            (const RfsHit*)slab, counts, hcap, (const float2*)psi, (const float2*)lam, (const float4*)rho32, n_tx,  \
+            n_rays, inv_slot, (float4*)s_gs, (float2*)lamT, (float2*)P);                                            \
+    } while (0)
+    if (nj == 1) RFS_BR(1);
+    else if (nj == 2) RFS_BR(2);
+    else if (nj <= 4) RFS_BR(4);
+    else RFS_BR(8);
+#undef RFS_BR
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -246,7 +246,8 @@ __device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
 }
 
 // ------------------------------------------------------------------ K9b
-template <int L, bool GATHER>
+// NJ = TX blocks of 32 per lane (compile time: no dead predicated iterations)
+template <int L, bool GATHER, int NJ>
 __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     int n, int nb, const float* __restrict__ means, const float2* __restrict__ coeffs, const float* __restrict__ tx,
     const float2* __restrict__ P, const uint32_t* __restrict__ s_ray, const float2* __restrict__ s_wt,
@@ -259,13 +260,13 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     const int g = (blockIdx.x * GB_THREADS + threadIdx.x) >> 5;
     if (g >= n) return;
     const int nj = (nb + 31) >> 5;
-    float2 Pj[GB_MAXJ];
+    float2 Pj[NJ];
     bool any = false;
     if (GATHER) {
         // deterministic p_acc: fixed-order sum over the Gaussian's sorted hits
         const int h0 = g_off[g], h1 = g_off[g + 1];
 #pragma unroll
-        for (int j = 0; j < GB_MAXJ; ++j) Pj[j] = make_float2(0.f, 0.f);
+        for (int j = 0; j < NJ; ++j) Pj[j] = make_float2(0.f, 0.f);
         any = h1 > h0;
         for (int hb = h0; hb < h1; hb += 32) {
             const int h = hb + lane;
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
                     wt[u] = i0 + u < nbh ? make_float2(a, bq) : make_float2(0.f, 0.f);
                 }
 #pragma unroll
-                for (int j = 0; j < GB_MAXJ; ++j) {
+                for (int j = 0; j < NJ; ++j) {
                     const int b = lane + 32 * j;
                     if (j < nj && b < nb) {
                         float2 l[4];
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < GB_MAXJ; ++j) {
+        for (int j = 0; j < NJ; ++j) {
             const int b = lane + 32 * j;
             Pj[j] = (j < nj && b < nb) ? P[(size_t)g * nb + b] : make_float2(0.f, 0.f);
             any |= (Pj[j].x != 0.f) || (Pj[j].y != 0.f);
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     const float mxf = means[3 * g], myf = means[3 * g + 1], mzf = means[3 * g + 2];
     const float2* co = coeffs + (size_t)g * K;
 #pragma unroll 1
-    for (int j = 0; j < GB_MAXJ; ++j) {
+    for (int j = 0; j < NJ; ++j) {
         const int b = lane + 32 * j;
         if (j >= nj) break;
         if (b >= nb) continue;
@@ -379,12 +380,16 @@ template <int L>
 void launch_tx(bool gather, unsigned grid, cudaStream_t st, int n, int nb, const float* means, const float2* coeffs,
                const float* tx, const float2* P, const uint32_t* s_ray, const float2* s_wt, const float2* lamT,
                const int* g_off, int include_dir, int accumulate, float* d_mean, float2* d_coeffs) {
-    if (gather)
-        k_grad_tx<L, true><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, s_ray, s_wt, lamT, g_off,
-                                                        include_dir, accumulate, d_mean, d_coeffs);
-    else
-        k_grad_tx<L, false><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, s_ray, s_wt, lamT, g_off,
-                                                         include_dir, accumulate, d_mean, d_coeffs);
+    const int nj = (nb + 31) / 32;
+#define RFS_GT(G, NJV)                                                                                             \
+    k_grad_tx<L, G, NJV><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, s_ray, s_wt, lamT, g_off,       \
+                                                      include_dir, accumulate, d_mean, d_coeffs)
+    if (gather) {
+        if (nj <= 2) RFS_GT(true, 2); else RFS_GT(true, 8);
+    } else {
+        if (nj <= 2) RFS_GT(false, 2); else RFS_GT(false, 8);
+    }
+#undef RFS_GT
 }
 
 }  // namespace
