@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--deterministic", action="store_true", help="fixed-order p_acc (no atomics)")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-sample", type=int, default=4, help="TX in the bounded CPU-baseline sample")
+    p.add_argument("--cpu-sample", type=int, default=32, help="TX in the bounded CPU-baseline sample (~10 s on 16 cores)")
     return p.parse_args()
 
 

@@ -216,12 +216,11 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
                         if (P) atomicAdd(&P[(size_t)g * nb + b], cmulf(cl[j], wt));
                     }
                 }
-                double cr = (double)c.x, ci = (double)c.y;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    cr += __shfl_xor_sync(0xffffffffu, cr, o);
-                    ci += __shfl_xor_sync(0xffffffffu, ci, o);
-                }
+                // TX reduction of C in fp32 (<= 256 products); the suffix
+                // recursion below runs in fp64
+                c.x = warp_sum(c.x);
+                c.y = warp_sum(c.y);
+                const double cr = (double)c.x, ci = (double)c.y;
                 {
                     double nr = wn * cnr + (rnr * Ar - rni * Ai);
                     double ni = wn * cni + (rnr * Ai + rni * Ar);
