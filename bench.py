@@ -154,15 +154,12 @@ def run_ours(args):
     tx = torch.as_tensor(txs, dtype=torch.float32, device=dev)
     B = tx.shape[0]
 
+    from paper_2502_01826_b200 import parallel
+
     def allreduce(g):
+        # one NCCL all-reduce (sum) of the packed gradient buffer
         if world > 1:
-            flat = torch.cat([g[k].reshape(-1).view(torch.float32) for k in raster.GRAD_FIELDS])
-            dist.all_reduce(flat)
-            o = 0
-            for k in raster.GRAD_FIELDS:
-                v = g[k].reshape(-1).view(torch.float32)
-                v.copy_(flat[o:o + v.numel()])
-                o += v.numel()
+            g.update(parallel.allreduce_grads(g))
 
     # fixed synthetic upstream: lambda = upstream_to_ray(dL1/dP, S), target 1.3 P + 0.05
     geo = raster.build_geometry(ds, sort_backend=args.sort)
