@@ -175,9 +175,10 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step(marks=None):
-        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks)
-        psi = raster.compute_psi(ds, tx)
-        raster._mark(marks, "psi")
+        # psi and the by-Gaussian hit index run on a side stream, overlapped
+        # with the tile / sort / hit-list chain and the forward composite
+        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, index=True)
+        psi = g0.psi
         S = raster.forward(g0, psi)
         raster._mark(marks, "forward")
         g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks, deterministic=args.deterministic)

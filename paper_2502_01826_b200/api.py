@@ -225,8 +225,8 @@ def fwd_bwd_host(host_scene: dict, tx_host: torch.Tensor, lam_host: torch.Tensor
                             d["coeffs"], tuple(float(x) for x in rx), float(ress_radius), n_az, n_el, fle_degree)
     tx = tx_host.to(dev, non_blocking=True)
     lam = lam_host.to(dev, non_blocking=True)
-    geo = raster.build_geometry(ds, sort_backend=sort_backend)
-    psi = raster.compute_psi(ds, tx)
+    geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True)
+    psi = geo.psi
     S = raster.forward(geo, psi)
     g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=psi)
     if reduce_fn is not None:

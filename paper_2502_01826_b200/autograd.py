@@ -38,8 +38,9 @@ class RFSplat(torch.autograd.Function):
             rx_t, float(ress_radius), int(n_az), int(n_el), degree,
         )
         txc = tx.detach().to(device=means.device, dtype=torch.float32).contiguous()
-        geo = raster.build_geometry(scene)
-        psi = raster.compute_psi(scene, txc)
+        # psi and the backward's by-Gaussian index overlap the geometry chain
+        geo = raster.build_geometry(scene, psi_tx=txc, index=True)
+        psi = geo.psi
         S = raster.forward(geo, psi)
         ctx.scene, ctx.geo, ctx.psi, ctx.tx = scene, geo, psi, txc
         ctx.include_direction_chain = bool(include_direction_chain)

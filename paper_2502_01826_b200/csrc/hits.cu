@@ -168,7 +168,8 @@ __device__ __forceinline__ bool exact_hit_s(const double* __restrict__ G, double
     double qf = DA(DA(DM(DA(DA(DM(i00, ex), DM(i01, ey)), DM(i02, ez)), ex),
                       DM(DA(DA(DM(i01, ex), DM(i11, ey)), DM(i12, ez)), ey)),
                    DM(DA(DA(DM(i02, ex), DM(i12, ey)), DM(i22, ez)), ez));
-    w_out = (float)DM(G[9], exp(DM(-0.5, qf)));
+    // w is stored in fp32: an fp32 exp of the fp64 exponent is within ~2 ulp
+    w_out = (float)G[9] * expf((float)DM(-0.5, qf));
     return true;
 }
 
@@ -247,6 +248,8 @@ __global__ void __launch_bounds__(NT) k_hits(
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
     const float th_p = acosf(fminf(cmin, 1.f)) + 1e-4f;
+    float sin_p, cos_p;
+    sincosf(th_p, &sin_p, &cos_p);
 
     // register prefetch of the next chunk's filter data (lane j loads candidate base + j)
     uint32_t pf_g = 0;
@@ -277,9 +280,10 @@ __global__ void __launch_bounds__(NT) k_hits(
             if (ang >= 3.1415f) {
                 rel = true;
             } else {
+                // cos(th_p + th_g) by angle addition (cos/sin th_g precomputed in K1)
                 const float m2 = pf_s.x * pf_s.x + pf_s.y * pf_s.y + pf_s.z * pf_s.z;
                 const float dotc = (cx * pf_s.x + cy * pf_s.y + cz * pf_s.z) * rsqrtf(m2);
-                rel = dotc >= cosf(ang) - 1e-5f;
+                rel = dotc >= cos_p * pf_w[3].z - sin_p * pf_w[3].w - 1e-5f;
             }
         }
         const unsigned relmask = __ballot_sync(0xffffffffu, rel);

@@ -176,8 +176,10 @@ __global__ void __launch_bounds__(256) k_project(
         // .y: half-angle of the bounding-sphere cone seen from rx, asin(r3/depth)
         // (pi when rx is inside the ball), for the per-warp cone cull in K6;
         // its axis is sph.xyz normalised.
+        // .z/.w: cos / sin of that angle (rounded so cos(th_p + th) is not overestimated)
         double th = inside ? RFS_PI : asin(fmin(r3 / depth, 1.0)) + 1e-6;
-        whit[4 * g + 3] = make_float4(__double2float_ru(thw), __double2float_ru(th), 0.f, 0.f);
+        whit[4 * g + 3] = make_float4(__double2float_ru(thw), __double2float_ru(th), __double2float_rd(cos(th)),
+                                      __double2float_ru(sin(th)));
     }
 
     float fd = __double2float_rn(depth);

@@ -120,6 +120,9 @@ class Geometry:
     rx: tuple = (0.0, 0.0, 0.0)
     ress_radius: float = 1.0
     gidx: dict | None = None             # by-Gaussian hit index (built on first backward)
+    psi: torch.Tensor | None = None      # psi computed on the side stream (build_geometry(psi_tx=...))
+    psi_ready: object = None             # cuda.Event recorded after it
+    idx_ready: object = None             # cuda.Event recorded after the side-stream index build
 
     @property
     def n_tiles(self) -> int:
@@ -137,6 +140,17 @@ class Geometry:
 # adaptive capacities, remembered across steps
 _CAPS = {"hcap": 64, "pcap": 16}
 _DIRS: dict = {}
+_SIDE: dict = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    """Second stream for work independent of the tile / sort / hit chain."""
+    key = str(dev)
+    s = _SIDE.get(key)
+    if s is None:
+        s = torch.cuda.Stream(device=dev)
+        _SIDE[key] = s
+    return s
 
 
 def ray_directions(n_az: int, n_el: int) -> np.ndarray:
@@ -190,15 +204,31 @@ def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand"):
 
 
 def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bool = False,
-                   hcap: int | None = None, marks: list | None = None) -> Geometry:
+                   hcap: int | None = None, marks: list | None = None, psi_tx: torch.Tensor | None = None,
+                   index: bool = False) -> Geometry:
     """K1-K6: projection, binning, sort, ranges, emission bounds, hit lists.
 
-    `marks` (optional list) receives (phase, cuda.Event) pairs recorded after
-    each phase on the current stream, for per-kernel timing in bench.py.
+    `psi_tx` (optional [B,3]) computes psi for that batch on a side stream,
+    concurrently with the tile / sort / hit chain (psi depends only on the
+    scene and the transmitters); `index=True` builds the by-Gaussian hit
+    index for the backward on the side stream after the hit lists, so it
+    overlaps the forward composite.  `marks` (optional list) receives
+    (phase, cuda.Event) pairs recorded after each phase on the current
+    stream, for per-kernel timing in bench.py.
     """
     scene.validate()
     lib = _native.load()
     dev = scene.means.device
+    main = torch.cuda.current_stream(dev)
+    psi = psi_ready = None
+    if psi_tx is not None:
+        side = _side_stream(dev)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            psi = compute_psi(scene, psi_tx)
+            psi_ready = torch.cuda.Event()
+            psi_ready.record(side)
+        psi.record_stream(main)
     n, n_az, n_el = scene.n, scene.n_az, scene.n_el
     tiles_u = (n_az + TILE - 1) // TILE
     tiles_v = (n_el + TILE - 1) // TILE
@@ -275,8 +305,22 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             _CAPS["hcap"] = max(_CAPS["hcap"], hc)
             continue
         break
-    return Geometry(n, n_az, n_el, tiles_u, tiles_v, m, geom, rho32, dirs, ckeys[:max(m, 0)], vals[:max(m, 0)],
-                    ranges, hc, slab, ray_counts, s, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
+    geo = Geometry(n, n_az, n_el, tiles_u, tiles_v, m, geom, rho32, dirs, ckeys[:max(m, 0)], vals[:max(m, 0)],
+                   ranges, hc, slab, ray_counts, s, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
+    geo.psi, geo.psi_ready = psi, psi_ready
+    if index:
+        side = _side_stream(dev)
+        side.wait_stream(main)
+        for t in (slab, ray_counts):
+            t.record_stream(side)
+        with torch.cuda.stream(side):
+            gauss_index(geo)
+            geo.idx_ready = torch.cuda.Event()
+            geo.idx_ready.record(side)
+        for t in geo.gidx.values():
+            if isinstance(t, torch.Tensor):
+                t.record_stream(main)
+    return geo
 
 
 def _check_tx(tx: torch.Tensor) -> torch.Tensor:
@@ -298,6 +342,8 @@ def compute_psi(scene: DeviceScene, tx: torch.Tensor) -> torch.Tensor:
 
 def forward(geo: Geometry, psi: torch.Tensor) -> torch.Tensor:
     """K7: S [B, n_az, n_el] complex64 from shared hit lists and psi [N, B]."""
+    if geo.psi_ready is not None and psi is geo.psi:
+        torch.cuda.current_stream().wait_event(geo.psi_ready)
     b = int(psi.shape[1])
     S = torch.empty((b, geo.n_az, geo.n_el), dtype=torch.complex64, device=psi.device)
     if b:
@@ -383,6 +429,10 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     R = geo.n_rays
     lib = _native.load()
     gauss_index(geo)
+    if geo.idx_ready is not None:  # built on the side stream by build_geometry(index=True)
+        torch.cuda.current_stream().wait_event(geo.idx_ready)
+    if psi is not None and psi is geo.psi and geo.psi_ready is not None:
+        torch.cuda.current_stream().wait_event(geo.psi_ready)
     gi = geo.gidx
     h = gi["h"]
     _mark(marks, "gauss_index")
