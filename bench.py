@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--sort", default="hand", choices=["hand", "cub"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--deterministic", action="store_true", help="fixed-order p_acc (no atomics)")
+    p.add_argument("--index-side", action="store_true", help="build the backward index on the side stream")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=32, help="TX in the bounded CPU-baseline sample (~10 s on 16 cores)")
     return p.parse_args()
@@ -177,7 +178,7 @@ def run_ours(args):
     def step(marks=None):
         # psi and the by-Gaussian hit index run on a side stream, overlapped
         # with the tile / sort / hit-list chain and the forward composite
-        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, index=True)
+        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, index=args.index_side)
         psi = g0.psi
         S = raster.forward(g0, psi)
         raster._mark(marks, "forward")

@@ -221,14 +221,6 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     dev = scene.means.device
     main = torch.cuda.current_stream(dev)
     psi = psi_ready = None
-    if psi_tx is not None:
-        side = _side_stream(dev)
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            psi = compute_psi(scene, psi_tx)
-            psi_ready = torch.cuda.Event()
-            psi_ready.record(side)
-        psi.record_stream(main)
     n, n_az, n_el = scene.n, scene.n_az, scene.n_el
     tiles_u = (n_az + TILE - 1) // TILE
     tiles_v = (n_el + TILE - 1) // TILE
@@ -273,6 +265,15 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     _native.call("rfs_lower_bounds", _ptr(ranges), n_tiles, _ptr(vals), _ptr(geom), _ptr(lb), st)
     _mark(marks, "ranges+lb")
 
+    if psi_tx is not None:
+        # psi on a side stream, concurrent with the latency-bound hit-list kernel
+        side = _side_stream(dev)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            psi = compute_psi(scene, psi_tx)
+            psi_ready = torch.cuda.Event()
+            psi_ready.record(side)
+        psi.record_stream(main)
     hc = int(hcap or _CAPS["hcap"])
     pc = _CAPS["pcap"]
     ray_counts = torch.empty(R, dtype=torch.int32, device=dev)
