@@ -47,7 +47,8 @@ def parse():
     p.add_argument("--sort", default="hand", choices=["hand", "cub"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--deterministic", action="store_true", help="fixed-order p_acc (no atomics)")
-    p.add_argument("--index-side", action="store_true", help="build the backward index on the side stream")
+    p.add_argument("--overlap", action="store_true", help="psi on a side stream concurrent with the hit lists")
+    p.add_argument("--index-side", action="store_true", help="with --overlap: backward index on the side stream")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=32, help="TX in the bounded CPU-baseline sample (~10 s on 16 cores)")
     return p.parse_args()
@@ -176,10 +177,16 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step(marks=None):
-        # psi and the by-Gaussian hit index run on a side stream, overlapped
-        # with the tile / sort / hit-list chain and the forward composite
-        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, index=args.index_side)
-        psi = g0.psi
+        if args.overlap:
+            # psi on a side stream concurrent with the hit-list kernel (and optionally
+            # the backward index concurrent with the forward composite)
+            g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, index=args.index_side)
+            psi = g0.psi
+        else:
+            g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks)
+            psi = raster.compute_psi(ds, tx)
+            raster._mark(marks, "psi")
+        raster._mark(marks, "sync")
         S = raster.forward(g0, psi)
         raster._mark(marks, "forward")
         g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks, deterministic=args.deterministic)

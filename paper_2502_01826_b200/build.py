@@ -27,6 +27,7 @@ SOURCES = {
     "radix_sort.cu": [],
     "hits.cu": [],
     "composite.cu": [],
+    "backward.cu": [],
     "grad.cu": [],
     "capi.cu": [],
 }

@@ -8,18 +8,7 @@
 //                      within a Gaussian = the reference's bincount slot
 //                      order), per sorted hit its ray, w and w T, the inverse
 //                      map slot -> sorted position, and per-Gaussian offsets
-//   K8a k_backward_rays per ray, back to front, lanes over TX:
-//                      C_k = sum_b conj(lam_b) psi[g_k][b]                  (SDDMM)
-//                      A_k = w_{k+1} C_{k+1} + rho_{k+1} A_{k+1}  (suffix recursion)
-//                      -> per-hit scalars GW_k = Re(T_k C_k), d|rho|_k, d(phase)_k
-//                      written at the hit's sorted position; optionally
-//                      p_acc[g][b] += conj(lam_b) w T (vector atomics) and
-//                      lambda transposed (for the deterministic gather)
-//
-// Because the backward is linear in the upstream lambda, every sum over the
-// TX batch is taken before the TX-independent geometry: per hit only GW_k
-// and A_k are needed, and A_k obeys the reference's suffix recursion
-// (_kernels.py:382, 522) with psi replaced by C.
+//   (K8a, the TX-batched backward sweep, is in backward.cu)
 #include "fle.cuh"
 #include "rfs_common.cuh"
 
@@ -118,135 +107,6 @@ __global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, int n,
     g_off[g] = lo;
 }
 
-// ------------------------------------------------------- K8a backward rays
-constexpr int BR_RAYS = 32;
-constexpr int BR_THREADS = 256;
-constexpr int BR_MAXJ = 8;  // up to 256 TX per launch (lane owns b = lane + 32 j)
-
-// NJ = ceil(n_tx / 32): TX blocks per lane, a compile-time constant so the
-// per-hit loops carry no dead predicated iterations.
-template <int NJ>
-__global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
-    const RfsHit* __restrict__ slab, const int* __restrict__ counts, int hcap, const float2* __restrict__ psi,
-    const float2* __restrict__ lam, const float4* __restrict__ rho32, int nb, int R,
-    const uint32_t* __restrict__ inv_slot, float4* __restrict__ s_gs, float2* __restrict__ lamT,
-    float2* __restrict__ P) {
-    extern __shared__ __align__(16) float2 s_lam[];  // [nb][BR_RAYS + 1]
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int r0 = blockIdx.x * BR_RAYS;
-    for (int i = threadIdx.x; i < nb * BR_RAYS; i += BR_THREADS) {
-        int b = i / BR_RAYS, rl = i % BR_RAYS, r = r0 + rl;
-        s_lam[b * (BR_RAYS + 1) + rl] = r < R ? lam[(size_t)b * R + r] : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
-    if (lamT) {  // lambda transposed to [R][nb] rows for the deterministic p_acc gather
-        for (int i = threadIdx.x; i < nb * BR_RAYS; i += BR_THREADS) {
-            int rl = i / nb, b = i % nb, r = r0 + rl;
-            if (r < R) lamT[(size_t)r * nb + b] = s_lam[b * (BR_RAYS + 1) + rl];
-        }
-    }
-    const int nj = (nb + 31) >> 5;
-    for (int rl = wid; rl < BR_RAYS; rl += BR_THREADS / 32) {
-        const int r = r0 + rl;
-        if (r >= R) break;
-        const int cnt = min(counts[r], hcap);
-        if (cnt == 0) continue;
-        float2 cl[NJ];  // conj(lambda_b) for this lane's b
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            int b = lane + 32 * j;
-            float2 l = (j < nj && b < nb) ? s_lam[b * (BR_RAYS + 1) + rl] : make_float2(0.f, 0.f);
-            cl[j] = make_float2(l.x, -l.y);
-        }
-        // A: sum_b conj(lam_b) suffix_{k,b}; (wn, rn, cn) = w, rho, C of hit k+1.
-        // The TX reduction and the scalar recursion run in fp64: for a
-        // Gaussian that every ray crosses first, d(phase) sums ~1e3 strongly
-        // cancelling Im(.) terms.
-        double Ar = 0.0, Ai = 0.0, wn = 0.0, rnr = 0.0, rni = 0.0, cnr = 0.0, cni = 0.0;
-        for (int kc = ((cnt - 1) >> 5) << 5; kc >= 0; kc -= 32) {
-            // lane i holds hit kc + i: record, transmittance, sorted position
-            const int kk = kc + lane;
-            RfsHit hl;
-            float4 rq = make_float4(0.f, 0.f, 0.f, 0.f);
-            uint32_t pos = 0;
-            if (kk < cnt) {
-                hl = slab[(size_t)r * hcap + kk];
-                rq = __ldg(&rho32[hl.g]);
-                pos = inv_slot[(size_t)r * hcap + kk];
-            } else {
-                hl.g = 0;
-                hl.w = 0.f;
-                hl.t_re = hl.t_im = 0.f;
-            }
-            const int n_in = min(32, cnt - kc);
-            // software pipeline: psi row of the next (lower) hit in flight
-            float2 pv[NJ], pn[NJ];
-            {
-                const uint32_t g0 = __shfl_sync(0xffffffffu, hl.g, n_in - 1);
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    const int b = lane + 32 * j;
-                    pn[j] = (j < nj && b < nb) ? __ldg(&psi[(size_t)g0 * nb + b]) : make_float2(0.f, 0.f);
-                }
-            }
-            for (int i = n_in - 1; i >= 0; --i) {
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) pv[j] = pn[j];
-                const uint32_t g = __shfl_sync(0xffffffffu, hl.g, i);
-                const uint32_t gprev = __shfl_sync(0xffffffffu, hl.g, i > 0 ? i - 1 : 0);
-                if (i > 0) {
-#pragma unroll
-                    for (int j = 0; j < NJ; ++j) {
-                        const int b = lane + 32 * j;
-                        if (j < nj && b < nb) pn[j] = __ldg(&psi[(size_t)gprev * nb + b]);
-                    }
-                }
-                const float w = __shfl_sync(0xffffffffu, hl.w, i);
-                const float tre = __shfl_sync(0xffffffffu, hl.t_re, i);
-                const float tim = __shfl_sync(0xffffffffu, hl.t_im, i);
-                const float2 wt = make_float2(w * tre, w * tim);
-                float2 c = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    const int b = lane + 32 * j;
-                    if (j < nj && b < nb) {
-                        c = caddf(c, cmulf(cl[j], pv[j]));
-                        // p_acc[g][b] += conj(lam_b) w T (inc_pg + bincount, grad.py:252-254):
-                        // one 8-byte vector reduction per lane, coalesced over the row
-                        if (P) atomicAdd(&P[(size_t)g * nb + b], cmulf(cl[j], wt));
-                    }
-                }
-                // TX reduction of C in fp32 (<= 256 products); the suffix
-                // recursion below runs in fp64
-                c.x = warp_sum(c.x);
-                c.y = warp_sum(c.y);
-                const double cr = (double)c.x, ci = (double)c.y;
-                {
-                    double nr = wn * cnr + (rnr * Ar - rni * Ai);
-                    double ni = wn * cni + (rnr * Ai + rni * Ar);
-                    Ar = nr;
-                    Ai = ni;
-                }
-                if (lane == i) {  // the lane holding hit k writes its scalars
-                    double tr = tre, ti = tim;
-                    double gw = tr * cr - ti * ci;                     // Re(T C)          (_kernels.py:387-388)
-                    double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
-                    double dmag = tar * rq.z - tai * rq.w;             // Re(T e^{jphi} A) (_kernels.py:382-383)
-                    double dph = -(tar * rq.y + tai * rq.x);           // -Im(T rho A)     (_kernels.py:384-385)
-                    // fire-and-forget vector reduction (one writer per launch, chunks
-                    // are stream-ordered: deterministic) -- no read-modify-write stall
-                    atomicAdd(&s_gs[pos], make_float4((float)gw, (float)dmag, (float)dph, 0.f));
-                }
-                wn = w;
-                rnr = __shfl_sync(0xffffffffu, rq.x, i);
-                rni = __shfl_sync(0xffffffffu, rq.y, i);
-                cnr = cr;
-                cni = ci;
-            }
-        }
-    }
-}
-
 template <int L>
 void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, float2* psi, cudaStream_t st) {
     long long tot = (long long)n * nb;
@@ -305,35 +165,6 @@ int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, int hcap, const 
 
 int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream) {
     k_gauss_offsets<<<rfs_ceil_div(n + 1, 256), 256, 0, (cudaStream_t)stream>>>(keys, n_hits, n, g_off);
-    RFS_LAUNCH_CHECK();
-    return RFS_OK;
-}
-
-int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam, const void* rho32,
-                      int n_tx, int n_rays, const uint32_t* inv_slot, void* s_gs, void* lamT, void* P, void* stream) {
-    if (n_rays <= 0 || n_tx <= 0) return RFS_OK;
-    if (n_tx > 32 * BR_MAXJ) return RFS_ERR_SHAPE;
-    size_t smem = (size_t)n_tx * (BR_RAYS + 1) * sizeof(float2);
-    const int nj = (n_tx + 31) / 32;
-    cudaStream_t st = (cudaStream_t)stream;
-    const unsigned grid = (unsigned)rfs_ceil_div(n_rays, BR_RAYS);
-#define RFS_BR(NJV)                                                                                                 \
-    do {                                                                                                            \
-        static int attr = 0;                                                                                        \
-        if (smem > 48 * 1024 && attr < (int)smem) {                                                                 \
-            RFS_CUDA_TRY(                                                                                           \
-                cudaFuncSetAttribute(k_backward_rays<NJV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-            attr = (int)smem;                                                                                       \
-        }                                                                                                           \
-        k_backward_rays<NJV><<<grid, BR_THREADS, smem, st>>>(                                                       \
-            (const RfsHit*)slab, counts, hcap, (const float2*)psi, (const float2*)lam, (const float4*)rho32, n_tx,  \
-            n_rays, inv_slot, (float4*)s_gs, (float2*)lamT, (float2*)P);                                            \
-    } while (0)
-    if (nj == 1) RFS_BR(1);
-    else if (nj == 2) RFS_BR(2);
-    else if (nj <= 4) RFS_BR(4);
-    else RFS_BR(8);
-#undef RFS_BR
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
