@@ -15,32 +15,21 @@
 // p_acc[g][b] += conj(lam_b) w_k T_k (inc_pg + bincount, grad.py:252-254) with
 // vector atomics, and writes lambda transposed for the deterministic gather.
 //
-// Mapping: one warp sweeps two rays at once (16 lanes per ray); a lane owns
-// TX pairs (2l, 2l+1) + 32 j, so psi rows are read as contiguous 8-byte pairs
-// and the per-hit TX reduction is a 4-step half-warp butterfly.  Hit records
-// are loaded 16 at a time lane-parallel and broadcast with width-16 shuffles;
-// the next hit's psi row is prefetched while the current one is reduced.
+// Mapping: one warp per ray, lanes over TX (b = lane + 32 j); hit records are
+// loaded 32 at a time lane-parallel and broadcast with shuffles; the next
+// hit's psi row is prefetched while the current one is reduced.  (A two-rays-
+// per-warp variant measured slower: it pads each step to the longer hit list.)
 #include "rfs_common.cuh"
 
 namespace {
 
-constexpr int BR_RAYS = 32;      // rays per block (lambda staged in shared memory)
-constexpr int BR_THREADS = 256;  // 8 warps x 2 rays x 2 rounds
-constexpr int BR_MAXJ = 8;       // up to 256 TX per launch
+// ------------------------------------------------------- K8a backward rays
+constexpr int BR_RAYS = 32;
+constexpr int BR_THREADS = 256;
+constexpr int BR_MAXJ = 8;  // up to 256 TX per launch (lane owns b = lane + 32 j)
 
-template <int NJ>
-__device__ __forceinline__ void load_row(const float2* __restrict__ psi, uint32_t g, int nb, int hl,
-                                         float2 (&p)[NJ][2]) {
-    const float2* row = psi + (size_t)g * nb;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-        const int b = 2 * hl + 32 * j;
-        p[j][0] = b < nb ? __ldg(&row[b]) : make_float2(0.f, 0.f);
-        p[j][1] = b + 1 < nb ? __ldg(&row[b + 1]) : make_float2(0.f, 0.f);
-    }
-}
-
-// NJ = ceil(n_tx / 32) (compile time: no dead predicated iterations)
+// NJ = ceil(n_tx / 32): TX blocks per lane, a compile-time constant so the
+// per-hit loops carry no dead predicated iterations.
 template <int NJ>
 __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
     const RfsHit* __restrict__ slab, const int* __restrict__ counts, int hcap, const float2* __restrict__ psi,
@@ -49,7 +38,6 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
     float2* __restrict__ P) {
     extern __shared__ __align__(16) float2 s_lam[];  // [nb][BR_RAYS + 1]
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int half = lane >> 4, hl = lane & 15;
     const int r0 = blockIdx.x * BR_RAYS;
     for (int i = threadIdx.x; i < nb * BR_RAYS; i += BR_THREADS) {
         int b = i / BR_RAYS, rl = i % BR_RAYS, r = r0 + rl;
@@ -62,94 +50,101 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
             if (r < R) lamT[(size_t)r * nb + b] = s_lam[b * (BR_RAYS + 1) + rl];
         }
     }
-    for (int pr = wid; pr < BR_RAYS / 2; pr += BR_THREADS / 32) {
-        const int rl = 2 * pr + half, r = r0 + rl;
-        const int cnt = r < R ? min(counts[r], hcap) : 0;
-        const int cmax = max(cnt, __shfl_xor_sync(0xffffffffu, cnt, 16));
-        if (cmax == 0) continue;
-        float2 cl[NJ][2];  // conj(lambda_b) of this lane's TX
+    const int nj = (nb + 31) >> 5;
+    for (int rl = wid; rl < BR_RAYS; rl += BR_THREADS / 32) {
+        const int r = r0 + rl;
+        if (r >= R) break;
+        const int cnt = min(counts[r], hcap);
+        if (cnt == 0) continue;
+        float2 cl[NJ];  // conj(lambda_b) for this lane's b
 #pragma unroll
-        for (int j = 0; j < NJ; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int b = 2 * hl + e + 32 * j;
-                const float2 l = b < nb ? s_lam[b * (BR_RAYS + 1) + rl] : make_float2(0.f, 0.f);
-                cl[j][e] = make_float2(l.x, -l.y);
-            }
-        const RfsHit* hrow = slab + (size_t)r * hcap;
-        const uint32_t* irow = inv_slot + (size_t)r * hcap;
-        // suffix recursion state in fp64 (a Gaussian every ray crosses first makes
-        // d(phase) a sum of ~1e3 cancelling terms)
+        for (int j = 0; j < NJ; ++j) {
+            int b = lane + 32 * j;
+            float2 l = (j < nj && b < nb) ? s_lam[b * (BR_RAYS + 1) + rl] : make_float2(0.f, 0.f);
+            cl[j] = make_float2(l.x, -l.y);
+        }
+        // A: sum_b conj(lam_b) suffix_{k,b}; (wn, rn, cn) = w, rho, C of hit k+1.
+        // The TX reduction and the scalar recursion run in fp64: for a
+        // Gaussian that every ray crosses first, d(phase) sums ~1e3 strongly
+        // cancelling Im(.) terms.
         double Ar = 0.0, Ai = 0.0, wn = 0.0, rnr = 0.0, rni = 0.0, cnr = 0.0, cni = 0.0;
-        RfsHit hc;
-        hc.g = 0; hc.w = 0.f; hc.t_re = 0.f; hc.t_im = 0.f;
-        float4 rq = make_float4(0.f, 0.f, 0.f, 0.f);
-        uint32_t pos = 0;
-        float2 pv[NJ][2], pn[NJ][2];
-        for (int k = cmax - 1; k >= 0; --k) {
-            const int ks = k & 15;
-            if (k == cmax - 1 || ks == 15) {
-                // lane-parallel load of this ray's hits [k - ks, k - ks + 16)
-                const int kk = (k - ks) + hl;
-                if (kk < cnt) {
-                    hc = hrow[kk];
-                    rq = __ldg(&rho32[hc.g]);
-                    pos = irow[kk];
+        for (int kc = ((cnt - 1) >> 5) << 5; kc >= 0; kc -= 32) {
+            // lane i holds hit kc + i: record, transmittance, sorted position
+            const int kk = kc + lane;
+            RfsHit hl;
+            float4 rq = make_float4(0.f, 0.f, 0.f, 0.f);
+            uint32_t pos = 0;
+            if (kk < cnt) {
+                hl = slab[(size_t)r * hcap + kk];
+                rq = __ldg(&rho32[hl.g]);
+                pos = inv_slot[(size_t)r * hcap + kk];
+            } else {
+                hl.g = 0;
+                hl.w = 0.f;
+                hl.t_re = hl.t_im = 0.f;
+            }
+            const int n_in = min(32, cnt - kc);
+            // software pipeline: psi row of the next (lower) hit in flight
+            float2 pv[NJ], pn[NJ];
+            {
+                const uint32_t g0 = __shfl_sync(0xffffffffu, hl.g, n_in - 1);
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    const int b = lane + 32 * j;
+                    pn[j] = (j < nj && b < nb) ? __ldg(&psi[(size_t)g0 * nb + b]) : make_float2(0.f, 0.f);
                 }
-                const uint32_t g0 = __shfl_sync(0xffffffffu, hc.g, ks, 16);
-                load_row<NJ>(psi, g0, nb, hl, pn);
             }
+            for (int i = n_in - 1; i >= 0; --i) {
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-                pv[j][0] = pn[j][0];
-                pv[j][1] = pn[j][1];
-            }
-            const bool act = k < cnt;
-            const float w = __shfl_sync(0xffffffffu, hc.w, ks, 16);
-            const float tre = __shfl_sync(0xffffffffu, hc.t_re, ks, 16);
-            const float tim = __shfl_sync(0xffffffffu, hc.t_im, ks, 16);
-            const uint32_t g = __shfl_sync(0xffffffffu, hc.g, ks, 16);
-            const float rqx = __shfl_sync(0xffffffffu, rq.x, ks, 16);
-            const float rqy = __shfl_sync(0xffffffffu, rq.y, ks, 16);
-            // prefetch the next (lower) hit's psi row within the loaded chunk
-            const uint32_t gp = __shfl_sync(0xffffffffu, hc.g, ks > 0 ? ks - 1 : 0, 16);
-            if (ks > 0) load_row<NJ>(psi, gp, nb, hl, pn);
-            const float2 wt = make_float2(w * tre, w * tim);
-            float2 c = make_float2(0.f, 0.f);
-            if (act) {
+                for (int j = 0; j < NJ; ++j) pv[j] = pn[j];
+                const uint32_t g = __shfl_sync(0xffffffffu, hl.g, i);
+                const uint32_t gprev = __shfl_sync(0xffffffffu, hl.g, i > 0 ? i - 1 : 0);
+                if (i > 0) {
 #pragma unroll
-                for (int j = 0; j < NJ; ++j)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        c = caddf(c, cmulf(cl[j][e], pv[j][e]));
-                        const int b = 2 * hl + e + 32 * j;
-                        if (P && b < nb) atomicAdd(&P[(size_t)g * nb + b], cmulf(cl[j][e], wt));
+                    for (int j = 0; j < NJ; ++j) {
+                        const int b = lane + 32 * j;
+                        if (j < nj && b < nb) pn[j] = __ldg(&psi[(size_t)gprev * nb + b]);
                     }
-            }
+                }
+                const float w = __shfl_sync(0xffffffffu, hl.w, i);
+                const float tre = __shfl_sync(0xffffffffu, hl.t_re, i);
+                const float tim = __shfl_sync(0xffffffffu, hl.t_im, i);
+                const float2 wt = make_float2(w * tre, w * tim);
+                float2 c = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int o = 8; o > 0; o >>= 1) {
-                c.x += __shfl_xor_sync(0xffffffffu, c.x, o);
-                c.y += __shfl_xor_sync(0xffffffffu, c.y, o);
-            }
-            if (act) {
-                const double cr = c.x, ci = c.y;
-                const double nr = wn * cnr + (rnr * Ar - rni * Ai);
-                const double ni = wn * cni + (rnr * Ai + rni * Ar);
-                Ar = nr;
-                Ai = ni;
-                if (hl == ks) {  // the lane holding hit k writes its scalars
-                    const double tr = tre, ti = tim;
-                    const double gw = tr * cr - ti * ci;               // Re(T C)
-                    const double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
-                    const double dmag = tar * rq.z - tai * rq.w;       // Re(T e^{j phi} A)
-                    const double dph = -(tar * rq.y + tai * rq.x);     // -Im(T rho A)
-                    // fire-and-forget vector reduction: one writer per launch and
-                    // TX chunks are stream-ordered, so the result is deterministic
+                for (int j = 0; j < NJ; ++j) {
+                    const int b = lane + 32 * j;
+                    if (j < nj && b < nb) {
+                        c = caddf(c, cmulf(cl[j], pv[j]));
+                        // p_acc[g][b] += conj(lam_b) w T (inc_pg + bincount, grad.py:252-254):
+                        // one 8-byte vector reduction per lane, coalesced over the row
+                        if (P) atomicAdd(&P[(size_t)g * nb + b], cmulf(cl[j], wt));
+                    }
+                }
+                // TX reduction of C in fp32 (<= 256 products); the suffix
+                // recursion below runs in fp64
+                c.x = warp_sum(c.x);
+                c.y = warp_sum(c.y);
+                const double cr = (double)c.x, ci = (double)c.y;
+                {
+                    double nr = wn * cnr + (rnr * Ar - rni * Ai);
+                    double ni = wn * cni + (rnr * Ai + rni * Ar);
+                    Ar = nr;
+                    Ai = ni;
+                }
+                if (lane == i) {  // the lane holding hit k writes its scalars
+                    double tr = tre, ti = tim;
+                    double gw = tr * cr - ti * ci;                     // Re(T C)          (_kernels.py:387-388)
+                    double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
+                    double dmag = tar * rq.z - tai * rq.w;             // Re(T e^{jphi} A) (_kernels.py:382-383)
+                    double dph = -(tar * rq.y + tai * rq.x);           // -Im(T rho A)     (_kernels.py:384-385)
+                    // fire-and-forget vector reduction (one writer per launch, chunks
+                    // are stream-ordered: deterministic) -- no read-modify-write stall
                     atomicAdd(&s_gs[pos], make_float4((float)gw, (float)dmag, (float)dph, 0.f));
                 }
                 wn = w;
-                rnr = rqx;
-                rni = rqy;
+                rnr = __shfl_sync(0xffffffffu, rq.x, i);
+                rni = __shfl_sync(0xffffffffu, rq.y, i);
                 cnr = cr;
                 cni = ci;
             }
