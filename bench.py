@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--batch", type=int, default=64, help="TX per GPU")
     p.add_argument("--sort", default="hand", choices=["hand", "cub"])
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--deterministic", action="store_true", help="fixed-order p_acc (no atomics)")
+    p.add_argument("--deterministic", action="store_true", help="(no-op: the backward is always atomic-free and deterministic)")
     p.add_argument("--overlap", action="store_true", help="psi on a side stream concurrent with the hit lists")
     p.add_argument("--index-side", action="store_true", help="with --overlap: backward index on the side stream")
     p.add_argument("--no-cpu", action="store_true")

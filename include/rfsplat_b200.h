@@ -132,17 +132,26 @@ int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, int hcap, const 
                       float* s_w, void* s_wt, uint32_t* inv_slot, void* stream);
 int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream);
 
-/* K8a: TX-batched reverse sweep (_ray_backward's complex part,
- * _kernels.py:369-387, 522): per hit, accumulates (+=) the TX-reduced
- * scalars {Re(T C), d|rho|, d(phase), 0} into s_gs (float4 per sorted hit,
- * zeroed before the first call of a step) at the hit's sorted position.
- * Optionally writes lambda transposed (lamT complex64[R*n_tx], for the
- * deterministic p_acc gather) and/or adds p_acc[g][b] += conj(lam_b) w T
- * with vector atomics into P (complex64[N*n_tx], zeroed by the caller);
- * both are nullable.  n_tx <= 256 per call. */
-int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam,
-                      const void* rho32, int n_tx, int n_rays, const uint32_t* inv_slot, void* s_gs, void* lamT,
-                      void* P, void* stream);
+/* K8: TX-batched backward over the shared hit lists, atomic-free and
+ * deterministic (every sum in a fixed order).  Replaces the complex part of
+ * _ray_backward (_kernels.py:360-387, 522) and the p_acc bincount
+ * (grad.py:252-254) for a batch of transmitters.
+ * rfs_lam_transpose: lam complex64[B*R] -> lamT complex64[R*B].
+ * rfs_bwd_gauss: over the Gaussian-sorted hits, C[p] = sum_b conj(lam_b[ray])
+ *   psi[g][b] (complex64[H]; accumulate = 1 adds a further TX chunk) and
+ *   P[g][b] = p_acc (complex64[N*B]; rows of Gaussians without hits are left
+ *   unwritten).  part: complex64[rfs_bwd_part_elems(H, B)] scratch.
+ * rfs_bwd_rays: per ray the suffix recursion A_k = w_{k+1} C_{k+1} +
+ *   rho_{k+1} A_{k+1} and the per-hit scalars {Re(T C), d|rho|, d(phase), 0}
+ *   stored (float4) at the hit's sorted position in s_gs.
+ * n_tx <= 256 per rfs_bwd_gauss call. */
+int rfs_lam_transpose(const void* lam, int n_tx, int n_rays, void* lamT, void* stream);
+size_t rfs_bwd_part_elems(int n_hits, int n_tx);
+int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const uint32_t* s_ray, const void* s_wt,
+                  const int* g_off, const void* psi, const void* lamT, int accumulate, void* C, void* P, void* part,
+                  void* stream);
+int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32,
+                 const uint32_t* inv_slot, const void* C, void* s_gs, void* stream);
 
 /* K9a/K9c: per-Gaussian TX-independent chains in fp64 with a fixed
  * summation order (deterministic): thread per sorted hit with a warp
@@ -162,13 +171,13 @@ int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, void* stream);
 
 /* K9b: per-Gaussian TX-dependent terms: d_coeffs = conj(p_acc) conj(basis)
- * (grad.py:255) and the bearing chain added to d_mean (grad.py:167-189).
- * p_acc is read from P (atomic mode) or, when P is NULL, gathered from lamT
- * over the sorted hits in fixed order (deterministic mode).  accumulate = 1
- * adds a further TX chunk's terms.  Run after rfs_grad_geom. */
+ * (grad.py:255) and the bearing chain added to d_mean (grad.py:167-189),
+ * from P of rfs_bwd_gauss (g_off marks Gaussians without hits, whose terms
+ * are zero).  accumulate = 1 adds a further TX chunk's terms.  Run after
+ * rfs_grad_geom. */
 int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
-                const uint32_t* s_ray, const void* s_wt, const void* lamT, const int* g_off,
-                int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs, void* stream);
+                const int* g_off, int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs,
+                void* stream);
 
 /* Library / build identification. */
 int rfs_version(void);

@@ -1,154 +1,274 @@
-// backward.cu -- K8a: TX-batched reverse sweep over the shared hit lists.
+// backward.cu -- K8: TX-batched backward over the shared hit lists, atomic-free.
 //
-// Restates the complex part of _ray_backward (_kernels.py:360-387, 522) for a
-// batch of transmitters.  Because the backward is linear in the upstream
-// lambda, every sum over the TX batch is taken before the TX-independent
-// geometry, so per hit only two TX-reduced quantities are needed:
-//   C_k = sum_b conj(lam_b) psi[g_k][b]                          (SDDMM)
-//   A_k = sum_b conj(lam_b) suffix_{k,b}
-//       = w_{k+1} C_{k+1} + rho_{k+1} A_{k+1}                    (the reference's
-//         suffix recursion with psi replaced by C, _kernels.py:522)
-// giving the per-hit scalars GW_k = Re(T_k C_k) (_kernels.py:387-388),
-// d|rho|_k = Re(T_k e^{j phi} A_k) and d(phase)_k = -Im(T_k rho A_k)
-// (_kernels.py:382-385), written at the hit's Gaussian-sorted position for the
-// fixed-order per-Gaussian reduction of grad.cu.  Optionally accumulates
-// p_acc[g][b] += conj(lam_b) w_k T_k (inc_pg + bincount, grad.py:252-254) with
-// vector atomics, and writes lambda transposed for the deterministic gather.
-//
-// Mapping: one warp per ray, lanes over TX (b = lane + 32 j); hit records are
-// loaded 32 at a time lane-parallel and broadcast with shuffles; the next
-// hit's psi row is prefetched while the current one is reduced.  (A two-rays-
-// per-warp variant measured slower: it pads each step to the longer hit list.)
+// Restates the complex part of _ray_backward (_kernels.py:360-387, 522) and
+// the p_acc bincount (grad.py:252-254) for a batch of transmitters.  The
+// backward is linear in the upstream lambda, so every sum over the TX batch
+// is taken before the TX-independent geometry; per live hit k (ray r,
+// Gaussian g) only two TX-reduced complex scalars are needed:
+//   C_k = sum_b conj(lam_b[r]) psi[g][b]                              (SDDMM)
+//   A_k = sum_b conj(lam_b[r]) suffix_{k,b}
+//       = w_{k+1} C_{k+1} + rho_{k+1} A_{k+1}   (the reference's suffix
+//         recursion, _kernels.py:522, with psi replaced by C)
+// and per Gaussian the TX-dependent row
+//   p_acc[g][b] = sum_{hits k of g} conj(lam_b[r_k]) w_k T_k          (SpMM^T)
+// Three kernels, none with atomics, every sum in a fixed order:
+//   K8t k_lam_transpose  lam [B][R] -> lamT [R][B] (a ray's TX row contiguous)
+//   K8c k_bwd_gauss      hits in Gaussian-sorted order, one warp per chunk of
+//                        BG_CHUNK hits, lanes over TX: C_k for every hit and
+//                        p_acc rows accumulated in registers -- the
+//                        Gaussian's psi row is loaded once per segment, the
+//                        lambda rows of its rays are gathered four hits at a
+//                        time.  Gaussians straddling chunks leave per-chunk
+//                        partial rows that
+//   K8f k_bwd_pfix       adds in chunk order.
+//   K8r k_bwd_rays       one warp per ray, lanes over its hits: the suffix
+//                        recursion as a warp scan of complex affine maps in
+//                        fp64, then GW_k = Re(T_k C_k) (_kernels.py:387-388),
+//                        d|rho|_k = Re(T_k e^{j phi} A_k), d(phase)_k =
+//                        -Im(T_k rho A_k) (_kernels.py:382-385), stored at
+//                        the hit's sorted position for K9a.
 #include "rfs_common.cuh"
 
 namespace {
 
-// ------------------------------------------------------- K8a backward rays
-constexpr int BR_RAYS = 32;
-constexpr int BR_THREADS = 256;
-constexpr int BR_MAXJ = 8;  // up to 256 TX per launch (lane owns b = lane + 32 j)
-
-// NJ = ceil(n_tx / 32): TX blocks per lane, a compile-time constant so the
-// per-hit loops carry no dead predicated iterations.
-template <int NJ>
-__global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
-    const RfsHit* __restrict__ slab, const int* __restrict__ counts, int hcap, const float2* __restrict__ psi,
-    const float2* __restrict__ lam, const float4* __restrict__ rho32, int nb, int R,
-    const uint32_t* __restrict__ inv_slot, float4* __restrict__ s_gs, float2* __restrict__ lamT,
-    float2* __restrict__ P) {
-    extern __shared__ __align__(16) float2 s_lam[];  // [nb][BR_RAYS + 1]
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int r0 = blockIdx.x * BR_RAYS;
-    for (int i = threadIdx.x; i < nb * BR_RAYS; i += BR_THREADS) {
-        int b = i / BR_RAYS, rl = i % BR_RAYS, r = r0 + rl;
-        s_lam[b * (BR_RAYS + 1) + rl] = r < R ? lam[(size_t)b * R + r] : make_float2(0.f, 0.f);
+// ------------------------------------------------------------ K8t transpose
+__global__ void __launch_bounds__(256) k_lam_transpose(const float2* __restrict__ lam, int nb, int R,
+                                                       float2* __restrict__ lamT) {
+    __shared__ float2 t[32][33];
+    const int r0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int i = ty; i < 32; i += 8) {
+        const int b = b0 + i, r = r0 + tx;
+        t[i][tx] = (b < nb && r < R) ? lam[(size_t)b * R + r] : make_float2(0.f, 0.f);
     }
     __syncthreads();
-    if (lamT) {  // lambda transposed to [R][nb] rows for the deterministic p_acc gather
-        for (int i = threadIdx.x; i < nb * BR_RAYS; i += BR_THREADS) {
-            int rl = i / nb, b = i % nb, r = r0 + rl;
-            if (r < R) lamT[(size_t)r * nb + b] = s_lam[b * (BR_RAYS + 1) + rl];
+    for (int i = ty; i < 32; i += 8) {
+        const int r = r0 + i, b = b0 + tx;
+        if (r < R && b < nb) lamT[(size_t)r * nb + b] = t[tx][i];
+    }
+}
+
+// ------------------------------------------------------------ K8c by Gaussian
+constexpr int BG_CHUNK = 128;   // sorted hits per warp
+constexpr int BG_WARPS = 4;     // warps per block
+constexpr int BG_MAXJ = 8;      // lanes own b = lane + 32 j: up to 256 TX per launch
+constexpr int BG_U = 4;         // hits in flight per warp
+
+// Sum of 8 per-lane values over the warp in 9 shuffles (instead of 40):
+// afterwards value i is held by lanes 4i .. 4i+3.
+__device__ __forceinline__ float reduce8(float (&v)[8], int lane) {
+#pragma unroll
+    for (int s = 16, h = 4; s >= 4; s >>= 1, h >>= 1) {
+        const bool upper = (lane & s) != 0;
+#pragma unroll
+        for (int j = 0; j < h; ++j) {
+            const float send = upper ? v[j] : v[j + h];
+            const float keep = upper ? v[j + h] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
         }
     }
-    const int nj = (nb + 31) >> 5;
-    for (int rl = wid; rl < BR_RAYS; rl += BR_THREADS / 32) {
-        const int r = r0 + rl;
-        if (r >= R) break;
-        const int cnt = min(counts[r], hcap);
-        if (cnt == 0) continue;
-        float2 cl[NJ];  // conj(lambda_b) for this lane's b
+    float x = v[0];
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    return x;
+}
+
+template <int NJ>
+__global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
+    int h_tot, int nb, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_ray,
+    const float2* __restrict__ s_wt, const int* __restrict__ g_off, const float2* __restrict__ psi,
+    const float2* __restrict__ lamT, int accumulate, float2* __restrict__ C, float2* __restrict__ P,
+    float2* __restrict__ part) {
+    __shared__ uint32_t sh_g[BG_WARPS][BG_CHUNK];
+    __shared__ uint32_t sh_r[BG_WARPS][BG_CHUNK];
+    __shared__ float2 sh_wt[BG_WARPS][BG_CHUNK];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int wglob = blockIdx.x * BG_WARPS + wl;
+    const int c0 = wglob * BG_CHUNK;
+    if (c0 >= h_tot) return;
+    const int c1 = min(c0 + BG_CHUNK, h_tot);
+    for (int i = lane; i < c1 - c0; i += 32) {
+        sh_g[wl][i] = (uint32_t)sorted_g[c0 + i];
+        sh_r[wl][i] = s_ray[c0 + i];
+        sh_wt[wl][i] = s_wt[c0 + i];
+    }
+    __syncwarp();
+    int h = c0;
+    while (h < c1) {
+        const int g = (int)sh_g[wl][h - c0];
+        const int hs = g_off[g], he = g_off[g + 1];
+        const int send = min(he, c1);
+        float2 ps[NJ], pa[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-            int b = lane + 32 * j;
-            float2 l = (j < nj && b < nb) ? s_lam[b * (BR_RAYS + 1) + rl] : make_float2(0.f, 0.f);
-            cl[j] = make_float2(l.x, -l.y);
+            const int b = lane + 32 * j;
+            ps[j] = b < nb ? __ldg(&psi[(size_t)g * nb + b]) : make_float2(0.f, 0.f);
+            pa[j] = make_float2(0.f, 0.f);
         }
-        // A: sum_b conj(lam_b) suffix_{k,b}; (wn, rn, cn) = w, rho, C of hit k+1.
-        // The TX reduction and the scalar recursion run in fp64: for a
-        // Gaussian that every ray crosses first, d(phase) sums ~1e3 strongly
-        // cancelling Im(.) terms.
-        double Ar = 0.0, Ai = 0.0, wn = 0.0, rnr = 0.0, rni = 0.0, cnr = 0.0, cni = 0.0;
-        for (int kc = ((cnt - 1) >> 5) << 5; kc >= 0; kc -= 32) {
-            // lane i holds hit kc + i: record, transmittance, sorted position
-            const int kk = kc + lane;
-            RfsHit hl;
-            float4 rq = make_float4(0.f, 0.f, 0.f, 0.f);
-            uint32_t pos = 0;
-            if (kk < cnt) {
-                hl = slab[(size_t)r * hcap + kk];
-                rq = __ldg(&rho32[hl.g]);
-                pos = inv_slot[(size_t)r * hcap + kk];
-            } else {
-                hl.g = 0;
-                hl.w = 0.f;
-                hl.t_re = hl.t_im = 0.f;
-            }
-            const int n_in = min(32, cnt - kc);
-            // software pipeline: psi row of the next (lower) hit in flight
-            float2 pv[NJ], pn[NJ];
-            {
-                const uint32_t g0 = __shfl_sync(0xffffffffu, hl.g, n_in - 1);
+        for (int hh = h; hh < send; hh += BG_U) {
+            float2 l[BG_U][NJ];
+            float2 wt[BG_U];
+#pragma unroll
+            for (int u = 0; u < BG_U; ++u) {
+                const bool ok = hh + u < send;
+                const int r = ok ? (int)sh_r[wl][hh + u - c0] : 0;
+                wt[u] = ok ? sh_wt[wl][hh + u - c0] : make_float2(0.f, 0.f);
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
                     const int b = lane + 32 * j;
-                    pn[j] = (j < nj && b < nb) ? __ldg(&psi[(size_t)g0 * nb + b]) : make_float2(0.f, 0.f);
+                    l[u][j] = (ok && b < nb) ? __ldg(&lamT[(size_t)r * nb + b]) : make_float2(0.f, 0.f);
                 }
             }
-            for (int i = n_in - 1; i >= 0; --i) {
+            float v[8];
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) pv[j] = pn[j];
-                const uint32_t g = __shfl_sync(0xffffffffu, hl.g, i);
-                const uint32_t gprev = __shfl_sync(0xffffffffu, hl.g, i > 0 ? i - 1 : 0);
-                if (i > 0) {
-#pragma unroll
-                    for (int j = 0; j < NJ; ++j) {
-                        const int b = lane + 32 * j;
-                        if (j < nj && b < nb) pn[j] = __ldg(&psi[(size_t)gprev * nb + b]);
-                    }
-                }
-                const float w = __shfl_sync(0xffffffffu, hl.w, i);
-                const float tre = __shfl_sync(0xffffffffu, hl.t_re, i);
-                const float tim = __shfl_sync(0xffffffffu, hl.t_im, i);
-                const float2 wt = make_float2(w * tre, w * tim);
+            for (int u = 0; u < BG_U; ++u) {
                 float2 c = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
-                    const int b = lane + 32 * j;
-                    if (j < nj && b < nb) {
-                        c = caddf(c, cmulf(cl[j], pv[j]));
-                        // p_acc[g][b] += conj(lam_b) w T (inc_pg + bincount, grad.py:252-254):
-                        // one 8-byte vector reduction per lane, coalesced over the row
-                        if (P) atomicAdd(&P[(size_t)g * nb + b], cmulf(cl[j], wt));
-                    }
+                    c = caddf(c, cmulf_cj(l[u][j], ps[j]));         // conj(lam) psi
+                    pa[j] = caddf(pa[j], cmulf_cj(l[u][j], wt[u]));  // conj(lam) w T
                 }
-                // TX reduction of C in fp32 (<= 256 products); the suffix
-                // recursion below runs in fp64
-                c.x = warp_sum(c.x);
-                c.y = warp_sum(c.y);
-                const double cr = (double)c.x, ci = (double)c.y;
-                {
-                    double nr = wn * cnr + (rnr * Ar - rni * Ai);
-                    double ni = wn * cni + (rnr * Ai + rni * Ar);
-                    Ar = nr;
-                    Ai = ni;
+                v[2 * u] = c.x;
+                v[2 * u + 1] = c.y;
+            }
+            const float x = reduce8(v, lane);
+            // lanes 4i hold value i = 2u + component of hit hh + u
+            if ((lane & 3) == 0) {
+                const int i = lane >> 2, u = i >> 1;
+                if (hh + u < send) {
+                    float* cf = reinterpret_cast<float*>(C + hh + u) + (i & 1);
+                    *cf = accumulate ? *cf + x : x;
                 }
-                if (lane == i) {  // the lane holding hit k writes its scalars
-                    double tr = tre, ti = tim;
-                    double gw = tr * cr - ti * ci;                     // Re(T C)          (_kernels.py:387-388)
-                    double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
-                    double dmag = tar * rq.z - tai * rq.w;             // Re(T e^{jphi} A) (_kernels.py:382-383)
-                    double dph = -(tar * rq.y + tai * rq.x);           // -Im(T rho A)     (_kernels.py:384-385)
-                    // fire-and-forget vector reduction (one writer per launch, chunks
-                    // are stream-ordered: deterministic) -- no read-modify-write stall
-                    atomicAdd(&s_gs[pos], make_float4((float)gw, (float)dmag, (float)dph, 0.f));
-                }
-                wn = w;
-                rnr = __shfl_sync(0xffffffffu, rq.x, i);
-                rni = __shfl_sync(0xffffffffu, rq.y, i);
-                cnr = cr;
-                cni = ci;
             }
         }
+        // flush p_acc for g: whole row if g's hits lie inside this chunk,
+        // else this chunk's partial (slot 2w: first segment, 2w+1: last)
+        float2* dst;
+        if (hs >= c0 && he <= c1) {
+            dst = P + (size_t)g * nb;
+        } else {
+            dst = part + (size_t)(hs < c0 ? 2 * wglob : 2 * wglob + 1) * nb;
+        }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int b = lane + 32 * j;
+            if (b < nb) dst[b] = pa[j];
+        }
+        if (hs < c0 && he > c1) {  // g covers the whole chunk: first and last segment
+            float2* d2 = part + (size_t)(2 * wglob + 1) * nb;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                const int b = lane + 32 * j;
+                if (b < nb) d2[b] = pa[j];
+            }
+        }
+        h = send;
+    }
+}
+
+// Gaussians whose hits straddle chunks: one warp per Gaussian sums the
+// chunk partials in chunk order (deterministic).
+__global__ void __launch_bounds__(256) k_bwd_pfix(int n, int nb, const int* __restrict__ g_off,
+                                                  const float2* __restrict__ part, float2* __restrict__ P) {
+    const int lane = threadIdx.x & 31;
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= n) return;
+    const int h0 = g_off[g], h1 = g_off[g + 1];
+    if (h1 <= h0) return;
+    const int w0 = h0 / BG_CHUNK, w1 = (h1 - 1) / BG_CHUNK;
+    if (w0 == w1) return;
+    for (int b = lane; b < nb; b += 32) {
+        float2 s = part[(size_t)(2 * w0 + 1) * nb + b];
+        for (int w = w0 + 1; w <= w1; ++w) s = caddf(s, part[(size_t)(2 * w) * nb + b]);
+        P[(size_t)g * nb + b] = s;
+    }
+}
+
+// ------------------------------------------------------------ K8r ray scan
+struct Aff {  // x -> a x + c, complex fp64
+    double ar, ai, cr, ci;
+};
+
+__device__ __forceinline__ Aff compose(const Aff& f, const Aff& h) {  // f(h(x))
+    Aff o;
+    o.ar = f.ar * h.ar - f.ai * h.ai;
+    o.ai = f.ar * h.ai + f.ai * h.ar;
+    o.cr = f.ar * h.cr - f.ai * h.ci + f.cr;
+    o.ci = f.ar * h.ci + f.ai * h.cr + f.ci;
+    return o;
+}
+
+__global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
+                                                  int hcap, int R, const float4* __restrict__ rho32,
+                                                  const uint32_t* __restrict__ inv_slot, const float2* __restrict__ C,
+                                                  float4* __restrict__ s_gs) {
+    const int lane = threadIdx.x & 31;
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= R) return;
+    const int cnt = min(counts[r], hcap);
+    if (cnt == 0) return;
+    // carried from the chunk above: A_{kc+32} and f_{kc+32} = (rho, w C) of hit kc+32
+    double Anr = 0.0, Ani = 0.0, Ur = 1.0, Ui = 0.0, Wr = 0.0, Wi = 0.0;
+    for (int kc = ((cnt - 1) >> 5) << 5; kc >= 0; kc -= 32) {
+        const int k = kc + lane;
+        const bool ok = k < cnt;
+        RfsHit hk;
+        uint32_t pos = 0;
+        float2 ck = make_float2(0.f, 0.f);
+        if (ok) {
+            hk = slab[(size_t)r * hcap + k];
+            pos = inv_slot[(size_t)r * hcap + k];
+            ck = C[pos];
+        } else {
+            hk.g = 0;
+            hk.w = 0.f;
+            hk.t_re = hk.t_im = 0.f;
+        }
+        const float4 rq = ok ? __ldg(&rho32[hk.g]) : make_float4(1.f, 0.f, 1.f, 0.f);
+        // f_k(A) = w_k C_k + rho_k A; lane k holds F_k = f_{k+1} (identity past the end)
+        const double wc_r = (double)hk.w * (double)ck.x, wc_i = (double)hk.w * (double)ck.y;
+        const double rr = rq.x, ri = rq.y;
+        Aff F;
+        {
+            const double nr = __shfl_down_sync(0xffffffffu, rr, 1);
+            const double ni = __shfl_down_sync(0xffffffffu, ri, 1);
+            const double ncr = __shfl_down_sync(0xffffffffu, wc_r, 1);
+            const double nci = __shfl_down_sync(0xffffffffu, wc_i, 1);
+            if (k + 1 >= cnt) {
+                F.ar = 1.0; F.ai = 0.0; F.cr = 0.0; F.ci = 0.0;
+            } else if (lane < 31) {
+                F.ar = nr; F.ai = ni; F.cr = ncr; F.ci = nci;
+            } else {
+                F.ar = Ur; F.ai = Ui; F.cr = Wr; F.ci = Wi;
+            }
+        }
+        // inclusive suffix scan: G_k = F_k o F_{k+1} o ... o F_{kc+31}
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            Aff H;
+            H.ar = __shfl_down_sync(0xffffffffu, F.ar, o);
+            H.ai = __shfl_down_sync(0xffffffffu, F.ai, o);
+            H.cr = __shfl_down_sync(0xffffffffu, F.cr, o);
+            H.ci = __shfl_down_sync(0xffffffffu, F.ci, o);
+            if (lane + o < 32) F = compose(F, H);
+        }
+        // A_k = G_k(A_{kc+32}) (A_cnt = 0 at the top)
+        const double Ar = F.ar * Anr - F.ai * Ani + F.cr;
+        const double Ai = F.ar * Ani + F.ai * Anr + F.ci;
+        if (ok) {
+            const double tr = hk.t_re, ti = hk.t_im;
+            const double gw = tr * (double)ck.x - ti * (double)ck.y;     // Re(T C)          (_kernels.py:387-388)
+            const double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
+            const double dmag = tar * rq.z - tai * rq.w;                  // Re(T e^{jphi} A) (_kernels.py:382-383)
+            const double dph = -(tar * rq.y + tai * rq.x);                // -Im(T rho A)     (_kernels.py:384-385)
+            s_gs[pos] = make_float4((float)gw, (float)dmag, (float)dph, 0.f);
+        }
+        Anr = __shfl_sync(0xffffffffu, Ar, 0);
+        Ani = __shfl_sync(0xffffffffu, Ai, 0);
+        Ur = __shfl_sync(0xffffffffu, rr, 0);
+        Ui = __shfl_sync(0xffffffffu, ri, 0);
+        Wr = __shfl_sync(0xffffffffu, wc_r, 0);
+        Wi = __shfl_sync(0xffffffffu, wc_i, 0);
     }
 }
 
@@ -156,31 +276,47 @@ __global__ void __launch_bounds__(BR_THREADS) k_backward_rays(
 
 extern "C" {
 
-int rfs_backward_rays(const void* slab, const int* counts, int hcap, const void* psi, const void* lam, const void* rho32,
-                      int n_tx, int n_rays, const uint32_t* inv_slot, void* s_gs, void* lamT, void* P, void* stream) {
+int rfs_lam_transpose(const void* lam, int n_tx, int n_rays, void* lamT, void* stream) {
     if (n_rays <= 0 || n_tx <= 0) return RFS_OK;
-    if (n_tx > 32 * BR_MAXJ) return RFS_ERR_SHAPE;
-    size_t smem = (size_t)n_tx * (BR_RAYS + 1) * sizeof(float2);
-    const int nj = (n_tx + 31) / 32;
+    dim3 grid(rfs_ceil_div(n_rays, 32), rfs_ceil_div(n_tx, 32));
+    k_lam_transpose<<<grid, 256, 0, (cudaStream_t)stream>>>((const float2*)lam, n_tx, n_rays, (float2*)lamT);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+size_t rfs_bwd_part_elems(int n_hits, int n_tx) {
+    return (size_t)2 * (size_t)((n_hits + BG_CHUNK - 1) / BG_CHUNK + 1) * (size_t)(n_tx > 0 ? n_tx : 1);
+}
+
+int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const uint32_t* s_ray, const void* s_wt,
+                  const int* g_off, const void* psi, const void* lamT, int accumulate, void* C, void* P, void* part,
+                  void* stream) {
+    if (n <= 0 || n_hits <= 0 || n_tx <= 0) return RFS_OK;
+    if (n_tx > 32 * BG_MAXJ) return RFS_ERR_SHAPE;
     cudaStream_t st = (cudaStream_t)stream;
-    const unsigned grid = (unsigned)rfs_ceil_div(n_rays, BR_RAYS);
-#define RFS_BR(NJV)                                                                                                 \
-    do {                                                                                                            \
-        static int attr = 0;                                                                                        \
-        if (smem > 48 * 1024 && attr < (int)smem) {                                                                 \
-            RFS_CUDA_TRY(                                                                                           \
-                cudaFuncSetAttribute(k_backward_rays<NJV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-            attr = (int)smem;                                                                                       \
-        }                                                                                                           \
-        k_backward_rays<NJV><<<grid, BR_THREADS, smem, st>>>(                                                       \
-            (const RfsHit*)slab, counts, hcap, (const float2*)psi, (const float2*)lam, (const float4*)rho32, n_tx,  \
-            n_rays, inv_slot, (float4*)s_gs, (float2*)lamT, (float2*)P);                                            \
-    } while (0)
-    if (nj == 1) RFS_BR(1);
-    else if (nj == 2) RFS_BR(2);
-    else if (nj <= 4) RFS_BR(4);
-    else RFS_BR(8);
-#undef RFS_BR
+    const int nwarps = rfs_ceil_div(n_hits, BG_CHUNK);
+    const unsigned grid = (unsigned)rfs_ceil_div(nwarps, BG_WARPS);
+    const int nj = (n_tx + 31) / 32;
+#define RFS_BG(NJV)                                                                                              \
+    k_bwd_gauss<NJV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, n_tx, sorted_g, s_ray, (const float2*)s_wt, g_off,  \
+                                                     (const float2*)psi, (const float2*)lamT, accumulate,        \
+                                                     (float2*)C, (float2*)P, (float2*)part)
+    if (nj == 1) RFS_BG(1);
+    else if (nj == 2) RFS_BG(2);
+    else if (nj <= 4) RFS_BG(4);
+    else RFS_BG(8);
+#undef RFS_BG
+    k_bwd_pfix<<<rfs_ceil_div((long long)n * 32, 256), 256, 0, st>>>(n, n_tx, g_off, (const float2*)part,
+                                                                     (float2*)P);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32,
+                 const uint32_t* inv_slot, const void* C, void* s_gs, void* stream) {
+    if (n_rays <= 0) return RFS_OK;
+    k_bwd_rays<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const RfsHit*)slab, counts, hcap, n_rays, (const float4*)rho32, inv_slot, (const float2*)C, (float4*)s_gs);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -11,11 +11,10 @@
 // K9c k_geom_final (thread per Gaussian, fp64): d_mean direct term, d_cov,
 //     d|rho|, d(phase), chain_cov_to_shape (grad.py:134-164) and
 //     d_trans_mag_raw = d|rho| sigma (1 - sigma) (train.py:161-162).
-// K9b k_grad_tx (warp per Gaussian, lanes over TX): p_acc[g][b]
-//     (grad.py:252-254), d_coeffs = conj(p_acc) conj(basis) (grad.py:255)
-//     and the bearing chain added to d_mean (grad.py:167-189).  p_acc comes
-//     from K8a's vector atomics (default) or, in deterministic mode, from a
-//     fixed-order gather of lambda rows over the Gaussian's hits.
+// K9b k_grad_tx (warp per Gaussian, lanes over TX): from p_acc[g][b]
+//     (grad.py:252-254, built by K8c in fixed order), d_coeffs =
+//     conj(p_acc) conj(basis) (grad.py:255) and the bearing chain added to
+//     d_mean (grad.py:167-189).
 #include "fle.cuh"
 #include "rfs_common.cuh"
 
@@ -247,11 +246,10 @@ __device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
 
 // ------------------------------------------------------------------ K9b
 // NJ = TX blocks of 32 per lane (compile time: no dead predicated iterations)
-template <int L, bool GATHER, int NJ>
+template <int L, int NJ>
 __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     int n, int nb, const float* __restrict__ means, const float2* __restrict__ coeffs, const float* __restrict__ tx,
-    const float2* __restrict__ P, const uint32_t* __restrict__ s_ray, const float2* __restrict__ s_wt,
-    const float2* __restrict__ lamT, const int* __restrict__ g_off, int include_dir, int accumulate,
+    const float2* __restrict__ P, const int* __restrict__ g_off, int include_dir, int accumulate,
     float* __restrict__ d_mean, float2* __restrict__ d_coeffs) {
     constexpr int K = Fle<L>::K;
     constexpr int NV = 2 * K;
@@ -261,54 +259,13 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     if (g >= n) return;
     const int nj = (nb + 31) >> 5;
     float2 Pj[NJ];
-    bool any = false;
-    if (GATHER) {
-        // deterministic p_acc: fixed-order sum over the Gaussian's sorted hits
-        const int h0 = g_off[g], h1 = g_off[g + 1];
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) Pj[j] = make_float2(0.f, 0.f);
-        any = h1 > h0;
-        for (int hb = h0; hb < h1; hb += 32) {
-            const int h = hb + lane;
-            int r = 0;
-            float2 wtl = make_float2(0.f, 0.f);
-            if (h < h1) {
-                r = (int)s_ray[h];
-                wtl = s_wt[h];
-            }
-            const int nbh = min(32, h1 - hb);
-#pragma unroll 1
-            for (int i0 = 0; i0 < nbh; i0 += 4) {
-                int ri[4];
-                float2 wt[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = min(i0 + u, 31);
-                    ri[u] = __shfl_sync(0xffffffffu, r, i);
-                    const float a = __shfl_sync(0xffffffffu, wtl.x, i), bq = __shfl_sync(0xffffffffu, wtl.y, i);
-                    wt[u] = i0 + u < nbh ? make_float2(a, bq) : make_float2(0.f, 0.f);
-                }
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    const int b = lane + 32 * j;
-                    if (j < nj && b < nb) {
-                        float2 l[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) l[u] = __ldg(&lamT[(size_t)ri[u] * nb + b]);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) Pj[j] = caddf(Pj[j], cmulf(make_float2(l[u].x, -l[u].y), wt[u]));
-                    }
-                }
-            }
-        }
-    } else {
+    const bool any = g_off[g + 1] > g_off[g];  // rows of Gaussians without hits are not written by K8c
+    if (any) {
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             const int b = lane + 32 * j;
             Pj[j] = (j < nj && b < nb) ? P[(size_t)g * nb + b] : make_float2(0.f, 0.f);
-            any |= (Pj[j].x != 0.f) || (Pj[j].y != 0.f);
         }
-        any = __any_sync(0xffffffffu, any);
     }
     if (!any) {  // Gaussian not hit: d_coeffs and the bearing term are zero
         if (!accumulate) {
@@ -377,18 +334,14 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
 }
 
 template <int L>
-void launch_tx(bool gather, unsigned grid, cudaStream_t st, int n, int nb, const float* means, const float2* coeffs,
-               const float* tx, const float2* P, const uint32_t* s_ray, const float2* s_wt, const float2* lamT,
-               const int* g_off, int include_dir, int accumulate, float* d_mean, float2* d_coeffs) {
+void launch_tx(unsigned grid, cudaStream_t st, int n, int nb, const float* means, const float2* coeffs,
+               const float* tx, const float2* P, const int* g_off, int include_dir, int accumulate, float* d_mean,
+               float2* d_coeffs) {
     const int nj = (nb + 31) / 32;
-#define RFS_GT(G, NJV)                                                                                             \
-    k_grad_tx<L, G, NJV><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, s_ray, s_wt, lamT, g_off,       \
-                                                      include_dir, accumulate, d_mean, d_coeffs)
-    if (gather) {
-        if (nj <= 2) RFS_GT(true, 2); else RFS_GT(true, 8);
-    } else {
-        if (nj <= 2) RFS_GT(false, 2); else RFS_GT(false, 8);
-    }
+#define RFS_GT(NJV)                                                                                                \
+    k_grad_tx<L, NJV><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, g_off, include_dir, accumulate,   \
+                                                   d_mean, d_coeffs)
+    if (nj <= 2) RFS_GT(2); else RFS_GT(8);
 #undef RFS_GT
 }
 
@@ -419,18 +372,16 @@ int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s
 }
 
 int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
-                const uint32_t* s_ray, const void* s_wt, const void* lamT, const int* g_off,
-                int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs, void* stream) {
+                const int* g_off, int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs,
+                void* stream) {
     if (n <= 0) return RFS_OK;
     if (n_tx > 32 * GB_MAXJ) return RFS_ERR_SHAPE;
-    const bool gather = P == nullptr;
-    if (gather && (lamT == nullptr || g_off == nullptr || s_ray == nullptr || s_wt == nullptr)) return RFS_ERR_CONTRACT;
+    if (P == nullptr || g_off == nullptr) return RFS_ERR_CONTRACT;
     cudaStream_t st = (cudaStream_t)stream;
     unsigned grid = (unsigned)rfs_ceil_div((long long)n * 32, GB_THREADS);
 #define RFS_TX(LL)                                                                                                   \
-    launch_tx<LL>(gather, grid, st, n, n_tx, means, (const float2*)coeffs, tx, (const float2*)P, s_ray,               \
-                  (const float2*)s_wt, (const float2*)lamT, g_off, include_direction_chain, accumulate, d_mean,       \
-                  (float2*)d_coeffs)
+    launch_tx<LL>(grid, st, n, n_tx, means, (const float2*)coeffs, tx, (const float2*)P, g_off,                     \
+                  include_direction_chain, accumulate, d_mean, (float2*)d_coeffs)
     switch (degree) {
         case 0: RFS_TX(0); break;
         case 1: RFS_TX(1); break;

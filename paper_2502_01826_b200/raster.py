@@ -400,10 +400,9 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     tensors.  Returns fp32 tensors with the GradientBuffer meaning plus
     d_trans_mag_raw (the logit chain of train.py:161-162).
 
-    Every per-Gaussian sum is taken in a fixed order except p_acc (the
-    TX-dependent sum behind d_coeffs and the bearing chain), which by default
-    uses fp32 vector atomics; `deterministic=True` gathers it in fixed order
-    instead, making the whole buffer bitwise reproducible.
+    Every sum has a fixed order and there are no atomics: the buffer is
+    bitwise reproducible.  `deterministic` is accepted for
+    API compatibility (it was the opt-in for this before).
     """
     tx = _check_tx(tx)
     b = int(tx.shape[0])
@@ -437,22 +436,23 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     gi = geo.gidx
     h = gi["h"]
     _mark(marks, "gauss_index")
-    s_gs = torch.zeros((max(h, 1), 4), dtype=torch.float32, device=dev)
+    C = torch.empty(max(h, 1), dtype=torch.complex64, device=dev)
+    s_gs = torch.empty((max(h, 1), 4), dtype=torch.float32, device=dev)  # every live hit written by K8r
     chunks = []
     for c0 in range(0, b, MAX_TX_PER_LAUNCH):
         c1 = min(b, c0 + MAX_TX_PER_LAUNCH)
+        nbc = c1 - c0
         txc = tx[c0:c1].contiguous()
         psic = psi if (psi is not None and c0 == 0 and c1 == b) else compute_psi(scene, txc)
-        lam = grad_S[c0:c1].contiguous()
-        if deterministic:
-            lamT = torch.empty((R, c1 - c0), dtype=torch.complex64, device=dev)
-            P = None
-        else:
-            lamT = None
-            P = torch.zeros((n, c1 - c0), dtype=torch.complex64, device=dev)
-        _native.call("rfs_backward_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, _ptr(psic), _ptr(lam),
-                     _ptr(geo.rho32), c1 - c0, R, _ptr(gi["inv_slot"]), _ptr(s_gs), _ptr(lamT), _ptr(P), st)
-        chunks.append((txc, lamT, P))
+        lamT = torch.empty((R, nbc), dtype=torch.complex64, device=dev)
+        _native.call("rfs_lam_transpose", _ptr(grad_S[c0:c1]), nbc, R, _ptr(lamT), st)
+        P = torch.empty((n, nbc), dtype=torch.complex64, device=dev)
+        part = torch.empty(int(lib.rfs_bwd_part_elems(h, nbc)), dtype=torch.complex64, device=dev)
+        _native.call("rfs_bwd_gauss", n, h, nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_wt"]),
+                     _ptr(gi["g_off"]), _ptr(psic), _ptr(lamT), int(c0 > 0), _ptr(C), _ptr(P), _ptr(part), st)
+        chunks.append((txc, P))
+    _native.call("rfs_bwd_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, _ptr(geo.rho32),
+                 _ptr(gi["inv_slot"]), _ptr(C), _ptr(s_gs), st)
     _mark(marks, "backward_rays")
     rx = (_native.C.c_double * 3)(*geo.rx)
     npart = int(lib.rfs_geom_part_elems(h))
@@ -465,10 +465,10 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
                  _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]), _ptr(out["d_trans_mag"]),
                  _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]), _ptr(out["d_cov"]), st)
     _mark(marks, "grad_geom")
-    for i, (txc, lamT, P) in enumerate(chunks):
+    for i, (txc, P) in enumerate(chunks):
         _native.call("rfs_grad_tx", n, int(txc.shape[0]), scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs),
-                     _ptr(txc), _ptr(P), _ptr(gi["s_ray"]), _ptr(gi["s_wt"]), _ptr(lamT), _ptr(gi["g_off"]),
-                     int(bool(include_direction_chain)), int(i > 0), _ptr(out["d_mean"]), _ptr(out["d_coeffs"]), st)
+                     _ptr(txc), _ptr(P), _ptr(gi["g_off"]), int(bool(include_direction_chain)), int(i > 0),
+                     _ptr(out["d_mean"]), _ptr(out["d_coeffs"]), st)
     _mark(marks, "grad_tx")
     return out
 
