@@ -124,7 +124,8 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
  * rfs_sort_pairs_u64 (stable: (ray, k) order within a Gaussian, the slot
  * order of the reference's bincount, grad.py:243-254);
  * rfs_gather_sorted: per sorted hit p its ray s_ray[p], w s_w[p], w T
- * s_wt[p] (complex64) and inv_slot[slot] = p (u32[R*hcap]);
+ * s_wt[p] (complex64) and, if inv_slot is not NULL, inv_slot[slot] = p
+ * (u32[R*hcap]);
  * rfs_gauss_offsets: g_off (int32[N+1]) over the sorted keys. */
 int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays, uint64_t* keys,
                  uint32_t* slots, void* stream);
@@ -137,21 +138,23 @@ int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void*
  * _ray_backward (_kernels.py:360-387, 522) and the p_acc bincount
  * (grad.py:252-254) for a batch of transmitters.
  * rfs_lam_transpose: lam complex64[B*R] -> lamT complex64[R*B].
- * rfs_bwd_gauss: over the Gaussian-sorted hits, C[p] = sum_b conj(lam_b[ray])
- *   psi[g][b] (complex64[H]; accumulate = 1 adds a further TX chunk) and
- *   P[g][b] = p_acc (complex64[N*B]; rows of Gaussians without hits are left
- *   unwritten).  part: complex64[rfs_bwd_part_elems(H, B)] scratch.
+ * rfs_bwd_gauss: over the Gaussian-sorted hits (s_slot = slab slot r*hcap+k
+ *   of each sorted hit, hcap a power of two), C[slot] = sum_b
+ *   conj(lam_b[ray]) psi[g][b] (complex64[R*hcap]; accumulate = 1 adds a
+ *   further TX chunk) and P[g][b] = p_acc (complex64[N*B]; rows of Gaussians
+ *   without hits are left unwritten).  part: complex64[rfs_bwd_part_elems(H,
+ *   B)] scratch.  B a multiple of 64 takes the 16-byte-vector path.
  * rfs_bwd_rays: per ray the suffix recursion A_k = w_{k+1} C_{k+1} +
  *   rho_{k+1} A_{k+1} and the per-hit scalars {Re(T C), d|rho|, d(phase), 0}
- *   stored (float4) at the hit's sorted position in s_gs.
+ *   (float4[R*hcap], slab order) in gs.
  * n_tx <= 256 per rfs_bwd_gauss call. */
 int rfs_lam_transpose(const void* lam, int n_tx, int n_rays, void* lamT, void* stream);
 size_t rfs_bwd_part_elems(int n_hits, int n_tx);
-int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const uint32_t* s_ray, const void* s_wt,
-                  const int* g_off, const void* psi, const void* lamT, int accumulate, void* C, void* P, void* part,
-                  void* stream);
-int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32,
-                 const uint32_t* inv_slot, const void* C, void* s_gs, void* stream);
+int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot, int hcap,
+                  const void* s_wt, const int* g_off, const void* psi, const void* lamT, int accumulate, void* C,
+                  void* P, void* part, void* stream);
+int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32, const void* C,
+                 void* gs, void* stream);
 
 /* K9a/K9c: per-Gaussian TX-independent chains in fp64 with a fixed
  * summation order (deterministic): thread per sorted hit with a warp
@@ -165,7 +168,7 @@ int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, cons
  * part_v f64[14*rfs_geom_part_elems(H)]. */
 size_t rfs_geom_part_elems(int n_hits);
 int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
-                  const void* s_gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
+                  const uint32_t* s_slot, const void* gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, void* stream);

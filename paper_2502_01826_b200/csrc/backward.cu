@@ -73,9 +73,10 @@ __device__ __forceinline__ float reduce8(float (&v)[8], int lane) {
     return x;
 }
 
+// Generic TX count: lanes own b = lane + 32 j (float2 loads).
 template <int NJ>
 __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
-    int h_tot, int nb, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_ray,
+    int h_tot, int nb, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_slot, int hshift,
     const float2* __restrict__ s_wt, const int* __restrict__ g_off, const float2* __restrict__ psi,
     const float2* __restrict__ lamT, int accumulate, float2* __restrict__ C, float2* __restrict__ P,
     float2* __restrict__ part) {
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
     const int c1 = min(c0 + BG_CHUNK, h_tot);
     for (int i = lane; i < c1 - c0; i += 32) {
         sh_g[wl][i] = (uint32_t)sorted_g[c0 + i];
-        sh_r[wl][i] = s_ray[c0 + i];
+        sh_r[wl][i] = s_slot[c0 + i];
         sh_wt[wl][i] = s_wt[c0 + i];
     }
     __syncwarp();
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
 #pragma unroll
             for (int u = 0; u < BG_U; ++u) {
                 const bool ok = hh + u < send;
-                const int r = ok ? (int)sh_r[wl][hh + u - c0] : 0;
+                const int r = ok ? (int)(sh_r[wl][hh + u - c0] >> hshift) : 0;
                 wt[u] = ok ? sh_wt[wl][hh + u - c0] : make_float2(0.f, 0.f);
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
             if ((lane & 3) == 0) {
                 const int i = lane >> 2, u = i >> 1;
                 if (hh + u < send) {
-                    float* cf = reinterpret_cast<float*>(C + hh + u) + (i & 1);
+                    float* cf = reinterpret_cast<float*>(C + sh_r[wl][hh + u - c0]) + (i & 1);
                     *cf = accumulate ? *cf + x : x;
                 }
             }
@@ -166,20 +167,146 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
     }
 }
 
-// Gaussians whose hits straddle chunks: one warp per Gaussian sums the
-// chunk partials in chunk order (deterministic).
-__global__ void __launch_bounds__(256) k_bwd_pfix(int n, int nb, const int* __restrict__ g_off,
-                                                  const float2* __restrict__ part, float2* __restrict__ P) {
+// B a multiple of 64: lanes own TX pairs b = 2 lane + 64 j + {0, 1}, so a
+// lambda / psi / p_acc row is one 16-byte vector per lane and NP = B / 64
+// vectors per row.  Segments (runs of one Gaussian) are found from a ballot
+// mask of the staged chunk, chunk-straddling from the neighbouring keys; the
+// next segment's psi row is prefetched while the current one is reduced.
+template <int NP>
+__global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
+    int h_tot, int nb, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_slot, int hshift,
+    const float2* __restrict__ s_wt, const float4* __restrict__ psi, const float4* __restrict__ lamT,
+    int accumulate, float2* __restrict__ C, float4* __restrict__ P, float4* __restrict__ part) {
+    __shared__ uint32_t sh_g[BG_WARPS][BG_CHUNK + 1];
+    __shared__ uint32_t sh_s[BG_WARPS][BG_CHUNK];
+    __shared__ float2 sh_wt[BG_WARPS][BG_CHUNK];
+    __shared__ uint32_t sh_m[BG_WARPS][BG_CHUNK / 32];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int wglob = blockIdx.x * BG_WARPS + wl;
+    const int c0 = wglob * BG_CHUNK;
+    if (c0 >= h_tot) return;
+    const int n = min(BG_CHUNK, h_tot - c0);
+    const int nq = nb >> 1;  // float4 per row
+    for (int i = lane; i < n; i += 32) {
+        sh_g[wl][i] = (uint32_t)sorted_g[c0 + i];
+        sh_s[wl][i] = s_slot[c0 + i];
+        sh_wt[wl][i] = s_wt[c0 + i];
+    }
+    __syncwarp();
+    const bool first_out = c0 > 0 && (uint32_t)sorted_g[c0 - 1] == sh_g[wl][0];
+    const bool last_out = c0 + n < h_tot && (uint32_t)sorted_g[c0 + n] == sh_g[wl][n - 1];
+#pragma unroll
+    for (int q = 0; q < BG_CHUNK / 32; ++q) {
+        const int i = 32 * q + lane;
+        const bool st = i < n && (i == 0 || sh_g[wl][i] != sh_g[wl][i - 1]);
+        const uint32_t m = __ballot_sync(0xffffffffu, st);
+        if (lane == 0) sh_m[wl][q] = m;
+    }
+    if (lane == 0) sh_g[wl][n] = 0xffffffffu;
+    __syncwarp();
+    // next segment start after position s (or n)
+    auto next_start = [&](int s) -> int {
+        for (int q = (s + 1) >> 5; q < BG_CHUNK / 32; ++q) {
+            const int sh = (s + 1) - 32 * q;
+            uint32_t m = sh_m[wl][q];
+            if (sh > 0) m &= 0xffffffffu << sh;
+            if (m) return min(32 * q + __ffs(m) - 1, n);
+        }
+        return n;
+    };
+    float4 ps[NP], pn[NP];
+    {
+        const int g = (int)sh_g[wl][0];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) pn[j] = __ldg(&psi[(size_t)g * nq + lane + 32 * j]);
+    }
+    int s0 = 0;
+    while (s0 < n) {
+        const int e = next_start(s0);
+        const int g = (int)sh_g[wl][s0];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) ps[j] = pn[j];
+        if (e < n) {
+            const int gn = (int)sh_g[wl][e];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) pn[j] = __ldg(&psi[(size_t)gn * nq + lane + 32 * j]);
+        }
+        float4 pa[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) pa[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i0 = s0; i0 < e; i0 += BG_U) {
+            float4 l[BG_U][NP];
+            float2 wt[BG_U];
+#pragma unroll
+            for (int u = 0; u < BG_U; ++u) {
+                const int i = min(i0 + u, e - 1);
+                const uint32_t r = sh_s[wl][i] >> hshift;
+                const float2 w = sh_wt[wl][i];
+                wt[u] = i0 + u < e ? w : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < NP; ++j) l[u][j] = __ldg(&lamT[(size_t)r * nq + lane + 32 * j]);
+            }
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < BG_U; ++u) {
+                float cr = 0.f, ci = 0.f;
+#pragma unroll
+                for (int j = 0; j < NP; ++j) {
+                    const float4 a = l[u][j], q = ps[j];
+                    // conj(lam) psi for the two TX of this lane
+                    cr += a.x * q.x + a.y * q.y + a.z * q.z + a.w * q.w;
+                    ci += a.x * q.y - a.y * q.x + a.z * q.w - a.w * q.z;
+                    // p_acc += conj(lam) w T
+                    pa[j].x += a.x * wt[u].x + a.y * wt[u].y;
+                    pa[j].y += a.x * wt[u].y - a.y * wt[u].x;
+                    pa[j].z += a.z * wt[u].x + a.w * wt[u].y;
+                    pa[j].w += a.z * wt[u].y - a.w * wt[u].x;
+                }
+                v[2 * u] = cr;
+                v[2 * u + 1] = ci;
+            }
+            const float x = reduce8(v, lane);
+            if ((lane & 3) == 0) {  // lanes 4i hold value i = 2u + component of hit i0 + u
+                const int i = lane >> 2, u = i >> 1;
+                if (i0 + u < e) {
+                    float* cf = reinterpret_cast<float*>(C + sh_s[wl][i0 + u]) + (i & 1);
+                    *cf = accumulate ? *cf + x : x;
+                }
+            }
+        }
+        // flush p_acc: whole row, or this chunk's partial (2w: first segment, 2w+1: last)
+        const bool fo = s0 == 0 && first_out, lo = e == n && last_out;
+        float4* dst = fo ? part + (size_t)(2 * wglob) * nq : (lo ? part + (size_t)(2 * wglob + 1) * nq
+                                                                 : P + (size_t)g * nq);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) dst[lane + 32 * j] = pa[j];
+        if (fo && lo) {
+#pragma unroll
+            for (int j = 0; j < NP; ++j) part[(size_t)(2 * wglob + 1) * nq + lane + 32 * j] = pa[j];
+        }
+        s0 = e;
+    }
+}
+
+// Gaussians whose hits straddle chunks: the warp of the chunk where such a
+// Gaussian starts sums the chunk partials in chunk order (deterministic).
+__global__ void __launch_bounds__(256) k_bwd_pfix(int h_tot, int nb, const uint64_t* __restrict__ sorted_g,
+                                                  const int* __restrict__ g_off, const float2* __restrict__ part,
+                                                  float2* __restrict__ P) {
     const int lane = threadIdx.x & 31;
-    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (g >= n) return;
-    const int h0 = g_off[g], h1 = g_off[g + 1];
-    if (h1 <= h0) return;
-    const int w0 = h0 / BG_CHUNK, w1 = (h1 - 1) / BG_CHUNK;
-    if (w0 == w1) return;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int c0 = w * BG_CHUNK;
+    if (c0 >= h_tot) return;
+    const int c1 = min(c0 + BG_CHUNK, h_tot);
+    if (c1 >= h_tot) return;
+    const uint64_t g = sorted_g[c1 - 1];
+    if (sorted_g[c1] != g) return;  // last segment ends inside the chunk
+    const int h0 = g_off[g];
+    if (h0 < c0) return;            // started in an earlier chunk, handled there
+    const int w1 = (g_off[g + 1] - 1) / BG_CHUNK;
     for (int b = lane; b < nb; b += 32) {
-        float2 s = part[(size_t)(2 * w0 + 1) * nb + b];
-        for (int w = w0 + 1; w <= w1; ++w) s = caddf(s, part[(size_t)(2 * w) * nb + b]);
+        float2 s = part[(size_t)(2 * w + 1) * nb + b];
+        for (int v = w + 1; v <= w1; ++v) s = caddf(s, part[(size_t)(2 * v) * nb + b]);
         P[(size_t)g * nb + b] = s;
     }
 }
@@ -200,8 +327,7 @@ __device__ __forceinline__ Aff compose(const Aff& f, const Aff& h) {  // f(h(x))
 
 __global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
                                                   int hcap, int R, const float4* __restrict__ rho32,
-                                                  const uint32_t* __restrict__ inv_slot, const float2* __restrict__ C,
-                                                  float4* __restrict__ s_gs) {
+                                                  const float2* __restrict__ C, float4* __restrict__ gs) {
     const int lane = threadIdx.x & 31;
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= R) return;
@@ -213,11 +339,10 @@ __global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ sla
         const int k = kc + lane;
         const bool ok = k < cnt;
         RfsHit hk;
-        uint32_t pos = 0;
+        const size_t pos = (size_t)r * hcap + k;
         float2 ck = make_float2(0.f, 0.f);
         if (ok) {
-            hk = slab[(size_t)r * hcap + k];
-            pos = inv_slot[(size_t)r * hcap + k];
+            hk = slab[pos];
             ck = C[pos];
         } else {
             hk.g = 0;
@@ -261,7 +386,7 @@ __global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ sla
             const double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
             const double dmag = tar * rq.z - tai * rq.w;                  // Re(T e^{jphi} A) (_kernels.py:382-383)
             const double dph = -(tar * rq.y + tai * rq.x);                // -Im(T rho A)     (_kernels.py:384-385)
-            s_gs[pos] = make_float4((float)gw, (float)dmag, (float)dph, 0.f);
+            gs[pos] = make_float4((float)gw, (float)dmag, (float)dph, 0.f);
         }
         Anr = __shfl_sync(0xffffffffu, Ar, 0);
         Ani = __shfl_sync(0xffffffffu, Ai, 0);
@@ -288,35 +413,52 @@ size_t rfs_bwd_part_elems(int n_hits, int n_tx) {
     return (size_t)2 * (size_t)((n_hits + BG_CHUNK - 1) / BG_CHUNK + 1) * (size_t)(n_tx > 0 ? n_tx : 1);
 }
 
-int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const uint32_t* s_ray, const void* s_wt,
-                  const int* g_off, const void* psi, const void* lamT, int accumulate, void* C, void* P, void* part,
-                  void* stream) {
+int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot, int hcap,
+                  const void* s_wt, const int* g_off, const void* psi, const void* lamT, int accumulate, void* C,
+                  void* P, void* part, void* stream) {
     if (n <= 0 || n_hits <= 0 || n_tx <= 0) return RFS_OK;
     if (n_tx > 32 * BG_MAXJ) return RFS_ERR_SHAPE;
+    if (hcap <= 0 || (hcap & (hcap - 1))) return RFS_ERR_SHAPE;
+    const int hshift = __builtin_ctz((unsigned)hcap);
     cudaStream_t st = (cudaStream_t)stream;
     const int nwarps = rfs_ceil_div(n_hits, BG_CHUNK);
     const unsigned grid = (unsigned)rfs_ceil_div(nwarps, BG_WARPS);
-    const int nj = (n_tx + 31) / 32;
+    if (n_tx % 64 == 0) {
+#define RFS_BV(NPV)                                                                                              \
+    k_bwd_gauss_v<NPV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, n_tx, sorted_g, s_slot, hshift,                   \
+                                                       (const float2*)s_wt, (const float4*)psi,                  \
+                                                       (const float4*)lamT, accumulate, (float2*)C, (float4*)P,  \
+                                                       (float4*)part)
+        switch (n_tx / 64) {
+            case 1: RFS_BV(1); break;
+            case 2: RFS_BV(2); break;
+            case 3: RFS_BV(3); break;
+            default: RFS_BV(4); break;
+        }
+#undef RFS_BV
+    } else {
+        const int nj = (n_tx + 31) / 32;
 #define RFS_BG(NJV)                                                                                              \
-    k_bwd_gauss<NJV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, n_tx, sorted_g, s_ray, (const float2*)s_wt, g_off,  \
-                                                     (const float2*)psi, (const float2*)lamT, accumulate,        \
+    k_bwd_gauss<NJV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, n_tx, sorted_g, s_slot, hshift, (const float2*)s_wt, \
+                                                     g_off, (const float2*)psi, (const float2*)lamT, accumulate, \
                                                      (float2*)C, (float2*)P, (float2*)part)
-    if (nj == 1) RFS_BG(1);
-    else if (nj == 2) RFS_BG(2);
-    else if (nj <= 4) RFS_BG(4);
-    else RFS_BG(8);
+        if (nj == 1) RFS_BG(1);
+        else if (nj == 2) RFS_BG(2);
+        else if (nj <= 4) RFS_BG(4);
+        else RFS_BG(8);
 #undef RFS_BG
-    k_bwd_pfix<<<rfs_ceil_div((long long)n * 32, 256), 256, 0, st>>>(n, n_tx, g_off, (const float2*)part,
-                                                                     (float2*)P);
+    }
+    k_bwd_pfix<<<rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st>>>(n_hits, n_tx, sorted_g, g_off,
+                                                                          (const float2*)part, (float2*)P);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
-int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32,
-                 const uint32_t* inv_slot, const void* C, void* s_gs, void* stream) {
+int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32, const void* C,
+                 void* gs, void* stream) {
     if (n_rays <= 0) return RFS_OK;
     k_bwd_rays<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-        (const RfsHit*)slab, counts, hcap, n_rays, (const float4*)rho32, inv_slot, (const float2*)C, (float4*)s_gs);
+        (const RfsHit*)slab, counts, hcap, n_rays, (const float4*)rho32, (const float2*)C, (float4*)gs);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

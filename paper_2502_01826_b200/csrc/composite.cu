@@ -81,7 +81,7 @@ __global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restric
     }
 }
 
-// per sorted hit p: its ray, w, w T; inverse map slot -> p
+// per sorted hit p: its ray, w, w T; inverse map slot -> p (nullable)
 __global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h, int hcap,
                                 const RfsHit* __restrict__ slab, uint32_t* __restrict__ s_ray,
                                 float* __restrict__ s_w, float2* __restrict__ s_wt, uint32_t* __restrict__ inv_slot) {
@@ -92,7 +92,7 @@ __global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h
     s_ray[p] = s / (uint32_t)hcap;
     s_w[p] = hk.w;
     s_wt[p] = make_float2(hk.w * hk.t_re, hk.w * hk.t_im);
-    inv_slot[s] = (uint32_t)p;
+    if (inv_slot) inv_slot[s] = (uint32_t)p;
 }
 
 // g_off[g] = lower_bound(g) over the sorted Gaussian keys, g in [0, n]

@@ -27,7 +27,7 @@ constexpr int GB_MAXJ = 8;       // up to 256 TX per launch
 // ------------------------------------------------------------------ K9a
 __global__ void __launch_bounds__(256) k_geom_seg(
     int h, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_ray, const float* __restrict__ s_w,
-    const float4* __restrict__ s_gs, const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
+    const uint32_t* __restrict__ s_slot, const float4* __restrict__ gs, const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
     const int* __restrict__ g_off, double rx0, double rx1, double rx2, double min_t, double* __restrict__ acc64,
     int* __restrict__ part_g, double* __restrict__ part_v) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) k_geom_seg(
                      i22 = G->inv[5];
         const int r = (int)s_ray[p];
         const double w = s_w[p];
-        const float4 gs = s_gs[p];
+        const float4 gsv = gs[s_slot[p]];  // K8r's per-hit scalars, slab order
         const double dx = dirs[3 * r], dy = dirs[3 * r + 1], dz = dirs[3 * r + 2];
         const double e0 = i00 * mx + i01 * my + i02 * mz, e1 = i01 * mx + i11 * my + i12 * mz,
                      e2 = i02 * mx + i12 * my + i22 * mz;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_geom_seg(
         const double t_mid = 0.5 * ((clamped ? min_t : d1) + d2);
         // q = Sigma^-1 (x_mid - mu) = t_mid p + e
         const double q0 = t_mid * p0 + e0, q1 = t_mid * p1 + e1, q2 = t_mid * p2 + e2;
-        const double gww = (double)gs.x * w;
+        const double gww = (double)gsv.x * w;
         const double f = 0.5 * gww;
         v[0] = gww * q0;
         v[1] = gww * q1;
@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(256) k_geom_seg(
                     v[3 + 3 * i + j] += half * ((-db + ddisc * inv2sq) / a - d2 * da / a);
                 }
         }
-        v[12] = gs.y;
-        v[13] = gs.z;
+        v[12] = gsv.y;
+        v[13] = gsv.z;
     }
     // warp segmented inclusive scan by Gaussian id (segments are contiguous)
 #pragma unroll
@@ -352,7 +352,7 @@ extern "C" {
 size_t rfs_geom_part_elems(int n_hits) { return (size_t)2 * (size_t)((n_hits + 31) / 32 + 1); }
 
 int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
-                  const void* s_gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
+                  const uint32_t* s_slot, const void* gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, void* stream) {
@@ -360,7 +360,7 @@ int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s
     cudaStream_t st = (cudaStream_t)stream;
     RFS_CUDA_TRY(cudaMemsetAsync(acc64, 0, sizeof(double) * NACC * (size_t)n, st));
     if (n_hits > 0) {
-        k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, sorted_g, s_ray, s_w, (const float4*)s_gs,
+        k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
                                                                (const RfsGeom*)geom, dirs, g_off, rx[0], rx[1], rx[2],
                                                                ress_radius, acc64, part_g, part_v);
         k_geom_fix<<<rfs_ceil_div((long long)n * 32, 256), 256, 0, st>>>(n, g_off, part_v, acc64);

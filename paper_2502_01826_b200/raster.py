@@ -274,7 +274,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             psi_ready = torch.cuda.Event()
             psi_ready.record(side)
         psi.record_stream(main)
-    hc = int(hcap or _CAPS["hcap"])
+    hc = 1 << max(0, math.ceil(math.log2(max(int(hcap or _CAPS["hcap"]), 1))))  # power of two: slot >> log2(hcap) = ray
     pc = _CAPS["pcap"]
     ray_counts = torch.empty(R, dtype=torch.int32, device=dev)
     slow = torch.empty(R, dtype=torch.int32, device=dev)
@@ -383,11 +383,10 @@ def gauss_index(geo: Geometry) -> None:
     s_ray = torch.empty(max(h, 1), dtype=torch.int32, device=dev)
     s_w = torch.empty(max(h, 1), dtype=torch.float32, device=dev)
     s_wt = torch.empty(max(h, 1), dtype=torch.complex64, device=dev)
-    inv_slot = torch.empty(R * geo.hcap, dtype=torch.int32, device=dev)
     _native.call("rfs_gather_sorted", _ptr(slots), h, geo.hcap, _ptr(geo.slab), _ptr(s_ray), _ptr(s_w), _ptr(s_wt),
-                 _ptr(inv_slot), st)
+                 None, st)
     geo.gidx = {"h": h, "sorted_g": keys, "g_off": g_off, "s_ray": s_ray, "s_w": s_w, "s_wt": s_wt,
-                "inv_slot": inv_slot}
+                "s_slot": slots}
 
 
 def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.Tensor,
@@ -436,8 +435,8 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     gi = geo.gidx
     h = gi["h"]
     _mark(marks, "gauss_index")
-    C = torch.empty(max(h, 1), dtype=torch.complex64, device=dev)
-    s_gs = torch.empty((max(h, 1), 4), dtype=torch.float32, device=dev)  # every live hit written by K8r
+    C = torch.empty(R * geo.hcap, dtype=torch.complex64, device=dev)        # slab order, live slots written
+    gs = torch.empty((R * geo.hcap, 4), dtype=torch.float32, device=dev)   # per-hit scalars of K8r, slab order
     chunks = []
     for c0 in range(0, b, MAX_TX_PER_LAUNCH):
         c1 = min(b, c0 + MAX_TX_PER_LAUNCH)
@@ -448,18 +447,20 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         _native.call("rfs_lam_transpose", _ptr(grad_S[c0:c1]), nbc, R, _ptr(lamT), st)
         P = torch.empty((n, nbc), dtype=torch.complex64, device=dev)
         part = torch.empty(int(lib.rfs_bwd_part_elems(h, nbc)), dtype=torch.complex64, device=dev)
-        _native.call("rfs_bwd_gauss", n, h, nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_wt"]),
-                     _ptr(gi["g_off"]), _ptr(psic), _ptr(lamT), int(c0 > 0), _ptr(C), _ptr(P), _ptr(part), st)
+        _native.call("rfs_bwd_gauss", n, h, nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_slot"]), geo.hcap,
+                     _ptr(gi["s_wt"]), _ptr(gi["g_off"]), _ptr(psic), _ptr(lamT), int(c0 > 0), _ptr(C), _ptr(P),
+                     _ptr(part), st)
         chunks.append((txc, P))
-    _native.call("rfs_bwd_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, _ptr(geo.rho32),
-                 _ptr(gi["inv_slot"]), _ptr(C), _ptr(s_gs), st)
+    _native.call("rfs_bwd_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, _ptr(geo.rho32), _ptr(C),
+                 _ptr(gs), st)
     _mark(marks, "backward_rays")
     rx = (_native.C.c_double * 3)(*geo.rx)
     npart = int(lib.rfs_geom_part_elems(h))
     acc64 = torch.empty((n, 14), dtype=torch.float64, device=dev)
     part_g = torch.empty(npart, dtype=torch.int32, device=dev)
     part_v = torch.empty((npart, 14), dtype=torch.float64, device=dev)
-    _native.call("rfs_grad_geom", n, h, _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(s_gs),
+    _native.call("rfs_grad_geom", n, h, _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(gi["s_slot"]),
+                 _ptr(gs),
                  _ptr(gi["g_off"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius), _ptr(scene.quats),
                  _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(acc64), _ptr(part_g), _ptr(part_v),
                  _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]), _ptr(out["d_trans_mag"]),
