@@ -115,7 +115,7 @@ int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs,
 
 /* K7: S[b][r] = sum over live hits of w * T * psi[g][b].  Replaces the
  * composite of forward_tiled (_kernels.py:184-192) for a TX batch. */
-int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, int n_tx, int n_rays, void* S,
+int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, int n_tx, int n_az, int n_el, void* S,
                 void* stream);
 
 /* K8i: by-Gaussian index of the live hits (TX independent).

@@ -15,17 +15,18 @@
 namespace {
 
 // ------------------------------------------------------------------ K5: psi
+// block (64 TX, 4 Gaussians); a Gaussian's coefficient row is an L1 broadcast
 template <int L>
 __global__ void __launch_bounds__(256) k_psi(int n, int nb, const float* __restrict__ means,
                                              const float2* __restrict__ coeffs, const float* __restrict__ tx,
                                              float2* __restrict__ psi) {
-    long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (long long)n * nb) return;
-    int g = (int)(idx / nb), b = (int)(idx % nb);
+    const int b = blockIdx.x * 64 + threadIdx.x;
+    const int g = blockIdx.y * 4 + threadIdx.y;
+    if (b >= nb || g >= n) return;
     float rx = tx[3 * b] - means[3 * g];
     float ry = tx[3 * b + 1] - means[3 * g + 1];
     float rz = tx[3 * b + 2] - means[3 * g + 2];
-    psi[idx] = Fle<L>::psi(rx, ry, rz, coeffs + (size_t)g * Fle<L>::K);
+    psi[(size_t)g * nb + b] = Fle<L>::psi(rx, ry, rz, coeffs + (size_t)g * Fle<L>::K);
 }
 
 // --------------------------------------------------------------- K7 forward
@@ -65,6 +66,73 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward(const RfsHit* __restrict
     }
 }
 
+// Even TX count: lanes own TX pairs (one 16-byte psi vector per hit), hit
+// records loaded lane-parallel and broadcast, four psi rows in flight.  A
+// block covers an FP_U x FP_V patch of rays (neighbouring rays cross mostly
+// the same Gaussians, so their psi rows are L1 hits).
+constexpr int FV_U = 4;
+constexpr int FP_U = 1, FP_V = 32, FP_RAYS = FP_U * FP_V;
+__global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restrict__ slab,
+                                                          const int* __restrict__ counts, int hcap,
+                                                          const float4* __restrict__ psi, int nb, int n_az, int n_el,
+                                                          float2* __restrict__ S) {
+    __shared__ float2 s_out[CP_BCH][FP_RAYS + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int pv_blocks = (n_el + FP_V - 1) / FP_V;
+    const int u0 = (blockIdx.x / pv_blocks) * FP_U, v0 = (blockIdx.x % pv_blocks) * FP_V;
+    const int bc = blockIdx.y * CP_BCH;
+    const int R = n_az * n_el;
+    const int nq = nb >> 1, q = (bc >> 1) + lane;  // this lane's float4 column
+    const bool on = 2 * lane + bc < nb;
+    for (int rl = wid; rl < FP_RAYS; rl += CP_THREADS / 32) {
+        const int u = u0 + rl / FP_V, v = v0 + rl % FP_V;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (u < n_az && v < n_el) {
+            const int r = u * n_el + v;
+            const int cnt = min(counts[r], hcap);
+            const RfsHit* h = slab + (size_t)r * hcap;
+            for (int kc = 0; kc < cnt; kc += 32) {
+                RfsHit hl;
+                if (kc + lane < cnt) {
+                    hl = h[kc + lane];
+                } else {
+                    hl.g = 0; hl.w = 0.f; hl.t_re = 0.f; hl.t_im = 0.f;
+                }
+                const float2 wtl = make_float2(hl.w * hl.t_re, hl.w * hl.t_im);
+                const int n_in = min(32, cnt - kc);
+                for (int i0 = 0; i0 < n_in; i0 += FV_U) {
+                    float4 pv[FV_U];
+                    float2 wt[FV_U];
+#pragma unroll
+                    for (int u = 0; u < FV_U; ++u) {
+                        const int i = i0 + u;  // lanes >= n_in carry w = 0, g = 0
+                        const uint32_t g = __shfl_sync(0xffffffffu, hl.g, i & 31);
+                        wt[u].x = __shfl_sync(0xffffffffu, wtl.x, i & 31);
+                        wt[u].y = __shfl_sync(0xffffffffu, wtl.y, i & 31);
+                        pv[u] = on ? __ldg(&psi[(size_t)g * nq + q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < FV_U; ++u) {
+                        acc.x += wt[u].x * pv[u].x - wt[u].y * pv[u].y;
+                        acc.y += wt[u].x * pv[u].y + wt[u].y * pv[u].x;
+                        acc.z += wt[u].x * pv[u].z - wt[u].y * pv[u].w;
+                        acc.w += wt[u].x * pv[u].w + wt[u].y * pv[u].z;
+                    }
+                }
+            }
+        }
+        s_out[2 * lane][rl] = make_float2(acc.x, acc.y);
+        s_out[2 * lane + 1][rl] = make_float2(acc.z, acc.w);
+    }
+    __syncthreads();
+    const int nbc = min(CP_BCH, nb - bc);
+    for (int i = threadIdx.x; i < nbc * FP_RAYS; i += CP_THREADS) {
+        const int bl = i / FP_RAYS, rl = i % FP_RAYS;
+        const int u = u0 + rl / FP_V, v = v0 + rl % FP_V;
+        if (u < n_az && v < n_el) S[(size_t)(bc + bl) * R + u * n_el + v] = s_out[bl][rl];
+    }
+}
+
 // ------------------------------------------- K8i by-Gaussian hit index
 // keys[c] = Gaussian id, vals[c] = slab slot r*hcap + k, c = ray_off[r] + k
 __global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
@@ -95,22 +163,20 @@ __global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h
     if (inv_slot) inv_slot[s] = (uint32_t)p;
 }
 
-// g_off[g] = lower_bound(g) over the sorted Gaussian keys, g in [0, n]
+// g_off[g] = lower_bound(g) over the sorted Gaussian keys, g in [0, n]: the
+// thread of sorted position p writes every g in (keys[p-1], keys[p]]
 __global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, int n, int* __restrict__ g_off) {
-    int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g > n) return;
-    int lo = 0, hi = h;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if ((long long)keys[mid] < g) lo = mid + 1; else hi = mid;
-    }
-    g_off[g] = lo;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > h) return;
+    const long long prev = p > 0 ? (long long)keys[p - 1] : -1;
+    const long long cur = p < h ? (long long)keys[p] : (long long)n;
+    for (long long g = prev + 1; g <= cur; ++g) g_off[g] = p;
 }
 
 template <int L>
 void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, float2* psi, cudaStream_t st) {
-    long long tot = (long long)n * nb;
-    k_psi<L><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, nb, means, coeffs, tx, psi);
+    dim3 grid(rfs_ceil_div(nb, 64), rfs_ceil_div(n, 4));
+    k_psi<L><<<grid, dim3(64, 4), 0, st>>>(n, nb, means, coeffs, tx, psi);
 }
 
 }  // namespace
@@ -135,12 +201,18 @@ int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs,
     return RFS_OK;
 }
 
-int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, int n_tx, int n_rays, void* S,
+int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, int n_tx, int n_az, int n_el, void* S,
                 void* stream) {
+    const int n_rays = n_az * n_el;
     if (n_rays <= 0 || n_tx <= 0) return RFS_OK;
     dim3 grid(rfs_ceil_div(n_rays, CP_RAYS), rfs_ceil_div(n_tx, CP_BCH));
-    k_forward<<<grid, CP_THREADS, 0, (cudaStream_t)stream>>>((const RfsHit*)slab, counts, hcap, (const float2*)psi,
-                                                             n_tx, n_rays, (float2*)S);
+    if (n_tx % 2 == 0) {
+        dim3 gv(rfs_ceil_div(n_az, FP_U) * rfs_ceil_div(n_el, FP_V), rfs_ceil_div(n_tx, CP_BCH));
+        k_forward_v<<<gv, CP_THREADS, 0, (cudaStream_t)stream>>>((const RfsHit*)slab, counts, hcap,
+                                                                 (const float4*)psi, n_tx, n_az, n_el, (float2*)S);
+    } else
+        k_forward<<<grid, CP_THREADS, 0, (cudaStream_t)stream>>>((const RfsHit*)slab, counts, hcap,
+                                                                 (const float2*)psi, n_tx, n_rays, (float2*)S);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -164,7 +236,7 @@ int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, int hcap, const 
 }
 
 int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream) {
-    k_gauss_offsets<<<rfs_ceil_div(n + 1, 256), 256, 0, (cudaStream_t)stream>>>(keys, n_hits, n, g_off);
+    k_gauss_offsets<<<rfs_ceil_div(n_hits + 1, 256), 256, 0, (cudaStream_t)stream>>>(keys, n_hits, n, g_off);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

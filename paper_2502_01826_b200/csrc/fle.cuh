@@ -19,17 +19,20 @@ struct Fle {
     };
 
     __device__ static __forceinline__ void tables(float rx, float ry, float rz, Tables& T) {
-        float d = sqrtf(rx * rx + ry * ry + rz * rz);
-        bool valid = d > 1e-12f;  // render.py:231 (bearing_valid)
-        float rho = sqrtf(rx * rx + ry * ry);
+        const float d2 = rx * rx + ry * ry + rz * rz;
+        const float rho2 = rx * rx + ry * ry;
+        bool valid = d2 > 1e-24f;  // render.py:231 (bearing_valid: |r| > 1e-12)
         float x, sig, ca, sa;
         if (valid) {
-            x = rho / d;
-            sig = rz / d;
-            if (rho > 0.f) {
-                ca = rx / rho;
-                sa = ry / rho;
+            const float id = rsqrtf(d2);
+            sig = rz * id;
+            if (rho2 > 0.f) {
+                const float ir = rsqrtf(rho2);
+                x = rho2 * ir * id;
+                ca = rx * ir;
+                sa = ry * ir;
             } else {
+                x = 0.f;
                 float a = atan2f(ry, rx);
                 sincosf(a, &sa, &ca);
             }

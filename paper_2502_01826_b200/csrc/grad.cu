@@ -258,15 +258,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     const int g = (blockIdx.x * GB_THREADS + threadIdx.x) >> 5;
     if (g >= n) return;
     const int nj = (nb + 31) >> 5;
-    float2 Pj[NJ];
     const bool any = g_off[g + 1] > g_off[g];  // rows of Gaussians without hits are not written by K8c
-    if (any) {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int b = lane + 32 * j;
-            Pj[j] = (j < nj && b < nb) ? P[(size_t)g * nb + b] : make_float2(0.f, 0.f);
-        }
-    }
     if (!any) {  // Gaussian not hit: d_coeffs and the bearing term are zero
         if (!accumulate) {
             float* dcf = reinterpret_cast<float*>(d_coeffs + (size_t)g * K);
@@ -285,7 +277,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
         const int b = lane + 32 * j;
         if (j >= nj) break;
         if (b >= nb) continue;
-        const float2 p = Pj[j];
+        const float2 p = P[(size_t)g * nb + b];
         const float rx = tx[3 * b] - mxf, ry = tx[3 * b + 1] - myf, rz = tx[3 * b + 2] - mzf;
         typename Fle<L>::Tables T;
         Fle<L>::tables(rx, ry, rz, T);

@@ -5,7 +5,7 @@
 // compact tile keys of project.cu (tile << 31 | float32 depth bits), so a
 // 276-tile grid needs 40 key bits = 5 passes of 8 bits.
 //
-// Each pass is ONE kernel ("onesweep"): a block ranks a 4096-key tile with
+// Each pass is ONE kernel ("onesweep"): a block ranks a 1024-4096-key tile with
 // warp-level match_any multisplit, publishes its per-digit counts through a
 // decoupled look-back chain, scatters block-locally through shared memory and
 // writes runs of equal digits with coalesced stores.  Block tiles are claimed
@@ -19,8 +19,7 @@ namespace {
 
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 16;
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys per block
+// keys per block = RS_THREADS * ITEMS (ITEMS a template parameter)
 constexpr int RS_BITS = 8;
 constexpr int RS_RADIX = 1 << RS_BITS;
 constexpr int RS_MAX_PASSES = 8;
@@ -71,9 +70,11 @@ __global__ void k_hist_scan(uint32_t* __restrict__ hist, int passes) {
     }
 }
 
+template <int ITEMS>
 struct OnesweepSmem {
-    uint64_t keys[RS_TILE];
-    uint32_t vals[RS_TILE];
+    static constexpr int TILE = RS_THREADS * ITEMS;
+    uint64_t keys[TILE];
+    uint32_t vals[TILE];
     uint32_t warp_hist[RS_WARPS][RS_RADIX];
     uint32_t digit_excl[RS_RADIX];  // block-local exclusive start of each digit
     uint32_t global_base[RS_RADIX]; // global start of this block's run of each digit
@@ -81,12 +82,14 @@ struct OnesweepSmem {
     int tile_id;
 };
 
+template <int RS_ITEMS>
 __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                                                         uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int m,
                                                         int shift, const uint32_t* __restrict__ digit_start,
                                                         uint32_t* __restrict__ lookback, int* __restrict__ tile_counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
+    constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
+    OnesweepSmem<RS_ITEMS>& S = *reinterpret_cast<OnesweepSmem<RS_ITEMS>*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1);
     for (int i = tid; i < RS_WARPS * RS_RADIX; i += RS_THREADS) (&S.warp_hist[0][0])[i] = 0;
@@ -214,7 +217,32 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const uint64_t* __restr
 }
 
 inline int num_passes(int end_bit) { return (end_bit + RS_BITS - 1) / RS_BITS; }
-inline int num_tiles(int m) { return rfs_ceil_div(m > 0 ? m : 1, RS_TILE); }
+inline int items_for(int m) {
+    // measured on B200 (483k and 1.15M keys): 16 items per thread beats 4 / 8
+    // -- a pass is bound by the look-back chain, which smaller tiles lengthen
+    return m >= 0 ? 16 : 4;
+}
+inline int num_tiles(int m) { return rfs_ceil_div(m > 0 ? m : 1, RS_THREADS * items_for(m)); }
+
+template <int ITEMS>
+int run_passes(uint64_t* kin, uint32_t* vin, uint64_t* kout, uint32_t* vout, int m, int passes, const uint32_t* hist,
+               uint32_t* lb, int* ctr, cudaStream_t st) {
+    static bool attr_set = false;
+    const size_t smem = sizeof(OnesweepSmem<ITEMS>);
+    if (!attr_set) {
+        RFS_CUDA_TRY(cudaFuncSetAttribute(k_onesweep<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    const int nt = num_tiles(m);
+    for (int p = 0; p < passes; ++p) {
+        k_onesweep<ITEMS><<<nt, RS_THREADS, smem, st>>>(kin, vin, kout, vout, m, p * RS_BITS, hist + p * RS_RADIX,
+                                                        lb + (size_t)p * nt * RS_RADIX, ctr + p);
+        uint64_t* tk = kin; kin = kout; kout = tk;
+        uint32_t* tv = vin; vin = vout; vout = tv;
+    }
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
 
 }  // namespace
 
@@ -249,23 +277,13 @@ int rfs_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint3
     RFS_CUDA_TRY(cudaMemsetAsync(temp, 0, rfs_sort_temp_bytes(m, end_bit), st));
     k_hist<<<rfs_ceil_div(m, HIST_THREADS * HIST_ITEMS), HIST_THREADS, 0, st>>>(keys, m, passes, hist);
     k_hist_scan<<<1, 32 * RS_MAX_PASSES, 0, st>>>(hist, passes);
-    static bool attr_set = false;
-    size_t smem = sizeof(OnesweepSmem);
-    if (!attr_set) {
-        RFS_CUDA_TRY(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
+    int rc;
+    switch (items_for(m)) {
+        case 16: rc = run_passes<16>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, st); break;
+        case 8: rc = run_passes<8>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, st); break;
+        default: rc = run_passes<4>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, st); break;
     }
-    uint64_t* kin = keys;
-    uint32_t* vin = vals;
-    uint64_t* kout = keys_alt;
-    uint32_t* vout = vals_alt;
-    for (int p = 0; p < passes; ++p) {
-        k_onesweep<<<nt, RS_THREADS, smem, st>>>(kin, vin, kout, vout, m, p * RS_BITS, hist + p * RS_RADIX,
-                                                 lb + (size_t)p * nt * RS_RADIX, ctr + p);
-        uint64_t* tk = kin; kin = kout; kout = tk;
-        uint32_t* tv = vin; vin = vout; vout = tv;
-    }
-    RFS_LAUNCH_CHECK();
+    if (rc != RFS_OK) return rc;
     *result_in_alt = (passes & 1);
     return RFS_OK;
 }

@@ -348,8 +348,8 @@ def forward(geo: Geometry, psi: torch.Tensor) -> torch.Tensor:
     b = int(psi.shape[1])
     S = torch.empty((b, geo.n_az, geo.n_el), dtype=torch.complex64, device=psi.device)
     if b:
-        _native.call("rfs_forward", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, _ptr(psi), b, geo.n_rays,
-                     _ptr(S), _stream())
+        _native.call("rfs_forward", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, _ptr(psi), b, geo.n_az,
+                     geo.n_el, _ptr(S), _stream())
     return S
 
 
