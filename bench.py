@@ -168,11 +168,27 @@ def run_ours(args):
     S0 = raster.forward(geo, raster.compute_psi(ds, tx))
     P0 = S0.abs() ** 2
     lam = (2.0 * torch.sign(P0 - (1.3 * P0 + 0.05)) / P0[0].numel() * S0).to(torch.complex64).contiguous()
+    gt_frames = (1.3 * P0 + 0.05).to(torch.float32).contiguous()  # measured spectra of the e2e training step
     M, H = geo.m, geo.total_hits
     hit_stats = {"max_live": geo.stats[2], "max_tile_list": geo.stats[4], "max_pending": geo.stats[5],
                  "sphere_pass": geo.stats[6], "whitened_pass": geo.stats[7], "slow_rays": geo.stats[0]}
     R = geo.n_rays
     del S0, P0
+    # spectrum loss alone (not part of `value`): timed separately
+    from paper_2502_01826_b200 import loss as _loss
+    S1 = raster.forward(geo, raster.compute_psi(ds, tx))
+    for _ in range(3):
+        _loss.spectrum_loss_frames(S1, gt_frames)
+    torch.cuda.synchronize()
+    l0 = torch.cuda.Event(enable_timing=True)
+    l1 = torch.cuda.Event(enable_timing=True)
+    l0.record()
+    for _ in range(5):
+        _loss.spectrum_loss_frames(S1, gt_frames)
+    l1.record()
+    torch.cuda.synchronize()
+    loss_ms = l0.elapsed_time(l1) / 5
+    del S1
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -249,16 +265,18 @@ def run_ours(args):
     rl["traffic"] = None
     rl["peak_source"] = pk["source"]
 
-    # ---- end to end through the host-buffer API (pinned H2D / D2H inside the timed region)
+    # ---- end to end: one training step through the public API (api.train_step_host):
+    # TX batch + measured power frames H2D from pinned memory, render, spectrum
+    # loss, upstream, backward (+ all-reduce), per-frame loss report D2H -- all
+    # inside the timed region; the gradients stay on the device for the optimizer
     e2e = None
     if not args.no_e2e:
-        hs = api.pinned_host_scene(scene)
         txh = torch.as_tensor(txs, dtype=torch.float32).pin_memory()
-        lamh = lam.cpu().pin_memory()
-        out = api.alloc_host_outputs(ds.n, ds.coeffs.shape[1], B, 360, 180)
+        gth = gt_frames.cpu().pin_memory()
+        reph = torch.empty((B, 4), dtype=torch.float64).pin_memory()
         red = allreduce if world > 1 else None
         for _ in range(max(1, args.warmup)):
-            api.fwd_bwd_host(hs, txh, lamh, out, ds.rx, ds.ress_radius, 360, 180, 3, True, args.sort, red)
+            api.train_step_host(ds, txh, gth, reph, sort_backend=args.sort, reduce_fn=red)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -266,7 +284,7 @@ def run_ours(args):
         ee = torch.cuda.Event(enable_timing=True)
         es.record()
         for _ in range(args.steps):
-            h2d, d2h = api.fwd_bwd_host(hs, txh, lamh, out, ds.rx, ds.ress_radius, 360, 180, 3, True, args.sort, red)
+            _, h2d, d2h = api.train_step_host(ds, txh, gth, reph, sort_backend=args.sort, reduce_fn=red)
         ee.record()
         torch.cuda.synchronize()
         te = es.elapsed_time(ee)
@@ -275,7 +293,9 @@ def run_ours(args):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
         e2e = {"value": round(world * B * args.steps / (te / 1e3), 2), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(te / args.steps, 4)}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(te / args.steps, 4),
+               "api": "api.train_step_host: TX + target power frames in, loss report out, spectrum loss on device",
+               "loss": [round(float(x), 6) for x in reph[:, 0].tolist()[:2]]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -293,7 +313,7 @@ def run_ours(args):
                        "parallelism": f"dp{world} (TX-sharded, grads all-reduced)",
                        "l2": "flushed between steps (256 MB write)"},
             "roofline": rl, "kernels_roofline": roof, "phase_ms": {k: round(v, 4) for k, v in ph_ms.items()},
-            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clk,
+            "loss_ms": round(loss_ms, 4), "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clk,
         }
         print(json.dumps(line))
     if world > 1:

@@ -182,6 +182,20 @@ int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coe
                 const int* g_off, int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs,
                 void* stream);
 
+/* Spectrum loss (loss.py:65-155) for n_frames frames [B][n_az*n_el], chained
+ * into the rasterizer's upstream (upstream_to_ray, grad.py:104-120).  The
+ * predicted power is pred (f32, nullable) or |S|^2 (S complex64, nullable);
+ * gt is the ground-truth power (f32).  report (f64[B*4], device) = {total,
+ * L1, SSIM, Fourier} per frame; grad (f32[B*R], nullable) = dL/dP; lam
+ * (complex64[B*R], nullable, needs S) = 2 dL/dP S.  L1 = mean|d|; SSIM = 1 -
+ * mean of the 11x11 sigma-1.5 zero-padded windowed SSIM with C1, C2 from the
+ * ground-truth range; Fourier = sum d^2 (= the mean squared DFT difference by
+ * Parseval).  Deterministic.  scratch: rfs_loss_scratch_bytes bytes. */
+size_t rfs_loss_scratch_bytes(int n_frames, int n_az, int n_el);
+int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const float* pred, const float* gt,
+                      double w_ssim, double w_fourier, double* report, float* grad, void* lam, void* scratch,
+                      size_t scratch_bytes, void* stream);
+
 /* Library / build identification. */
 int rfs_version(void);
 int rfs_device_arch(void); /* compute capability the library was built for, e.g. 100 */

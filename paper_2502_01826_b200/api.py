@@ -32,6 +32,7 @@ __all__ = [
     "GradientBuffer", "TileIndex", "SceneProjection", "RenderContextGPU",
     "prepare_context", "render_complex_frame", "render_complex_frames", "render_spectrum", "render_scalar",
     "backward_frame", "backward_frames", "upstream_to_ray", "build_tiles_for_render", "project_scene",
+    "fwd_bwd_host", "train_step_host",
 ]
 
 
@@ -238,6 +239,38 @@ def fwd_bwd_host(host_scene: dict, tx_host: torch.Tensor, lam_host: torch.Tensor
     h2d += tx_host.numel() * tx_host.element_size() + lam_host.numel() * lam_host.element_size()
     d2h = sum(out[k].numel() * out[k].element_size() for k in ("S",) + OUT_GRADS)
     return h2d, d2h
+
+
+def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torch.Tensor, report_host: torch.Tensor,
+                    w_ssim: float = 0.2, w_fourier: float = 0.2, include_direction_chain: bool = True,
+                    sort_backend: str = "hand", reduce_fn=None) -> tuple:
+    """One training step of a device-resident scene on a TX batch from HOST buffers.
+
+    The batched counterpart of the reference iteration (train.py:266-281,
+    324-336): render, spectrum loss against the measured power frames,
+    upstream_to_ray, backward_frame.  Per step the TX positions [B, 3] and the
+    ground-truth power frames [B, n_az, n_el] (pinned host float32) go to the
+    device, and the per-frame loss report [B, 4] = (total, L1, SSIM, Fourier)
+    comes back into `report_host` (pinned float64); the gradient dict stays on
+    the device for the optimizer.  Copies are stream-ordered (non_blocking);
+    the caller synchronizes.  Returns (grads, h2d_bytes, d2h_bytes).
+    """
+    from . import loss as _loss
+
+    dev = ds.means.device
+    tx = tx_host.to(dev, non_blocking=True)
+    gt = gt_host.to(dev, non_blocking=True)
+    geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True)
+    psi = geo.psi
+    S = raster.forward(geo, psi)
+    rep, lam, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier)
+    g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=psi)
+    if reduce_fn is not None:
+        reduce_fn(g)
+    report_host.copy_(rep, non_blocking=True)
+    h2d = tx_host.numel() * tx_host.element_size() + gt_host.numel() * gt_host.element_size()
+    d2h = report_host.numel() * report_host.element_size()
+    return g, h2d, d2h
 
 
 def build_tiles_for_render(scene, proj=None, sort_backend: str = "hand") -> TileIndex:

@@ -29,6 +29,7 @@ SOURCES = {
     "composite.cu": [],
     "backward.cu": [],
     "grad.cu": [],
+    "loss.cu": [],
     "capi.cu": [],
 }
 
