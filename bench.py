@@ -47,8 +47,6 @@ def parse():
     p.add_argument("--sort", default="hand", choices=["hand", "cub"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--deterministic", action="store_true", help="(no-op: the backward is always atomic-free and deterministic)")
-    p.add_argument("--overlap", action="store_true", help="psi on a side stream concurrent with the hit lists")
-    p.add_argument("--index-side", action="store_true", help="with --overlap: backward index on the side stream")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=32, help="TX in the bounded CPU-baseline sample (~10 s on 16 cores)")
     return p.parse_args()
@@ -193,18 +191,9 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step(marks=None):
-        if args.overlap:
-            # psi on a side stream concurrent with the hit-list kernel (and optionally
-            # the backward index concurrent with the forward composite)
-            g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, index=args.index_side)
-            psi = g0.psi
-        else:
-            g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks)
-            psi = raster.compute_psi(ds, tx)
-            raster._mark(marks, "psi")
-        raster._mark(marks, "sync")
-        S = raster.forward(g0, psi)
-        raster._mark(marks, "forward")
+        # psi queued behind the M read, the composite behind the hit-statistics read
+        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, forward=True)
+        psi, S = g0.psi, g0.S
         g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks, deterministic=args.deterministic)
         allreduce(g)
         raster._mark(marks, "allreduce")

@@ -226,7 +226,7 @@ def fwd_bwd_host(host_scene: dict, tx_host: torch.Tensor, lam_host: torch.Tensor
                             d["coeffs"], tuple(float(x) for x in rx), float(ress_radius), n_az, n_el, fle_degree)
     tx = tx_host.to(dev, non_blocking=True)
     lam = lam_host.to(dev, non_blocking=True)
-    geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True)
+    geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True, forward=True)
     psi = geo.psi
     S = raster.forward(geo, psi)
     g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=psi)
@@ -239,6 +239,16 @@ def fwd_bwd_host(host_scene: dict, tx_host: torch.Tensor, lam_host: torch.Tensor
     h2d += tx_host.numel() * tx_host.element_size() + lam_host.numel() * lam_host.element_size()
     d2h = sum(out[k].numel() * out[k].element_size() for k in ("S",) + OUT_GRADS)
     return h2d, d2h
+
+
+_COPY: dict = {}
+
+
+def _copy_stream(dev) -> torch.cuda.Stream:
+    k = str(dev)
+    if k not in _COPY:
+        _COPY[k] = torch.cuda.Stream(device=dev)
+    return _COPY[k]
 
 
 def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torch.Tensor, report_host: torch.Tensor,
@@ -258,11 +268,23 @@ def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torc
     from . import loss as _loss
 
     dev = ds.means.device
-    tx = tx_host.to(dev, non_blocking=True)
-    gt = gt_host.to(dev, non_blocking=True)
-    geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True)
+    main = torch.cuda.current_stream(dev)
+    cs = _copy_stream(dev)
+    cs.wait_stream(main)
+    with torch.cuda.stream(cs):  # H2D on the copy engine, overlapping the TX-independent geometry
+        tx = tx_host.to(dev, non_blocking=True)
+        tx_ready = torch.cuda.Event()
+        tx_ready.record(cs)
+        gt = gt_host.to(dev, non_blocking=True)
+        gt_ready = torch.cuda.Event()
+        gt_ready.record(cs)
+    tx.record_stream(main)
+    gt.record_stream(main)
+    main.wait_event(tx_ready)
+    geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True, forward=True)
     psi = geo.psi
     S = raster.forward(geo, psi)
+    main.wait_event(gt_ready)
     rep, lam, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier)
     g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=psi)
     if reduce_fn is not None:

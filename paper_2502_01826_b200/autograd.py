@@ -38,8 +38,8 @@ class RFSplat(torch.autograd.Function):
             rx_t, float(ress_radius), int(n_az), int(n_el), degree,
         )
         txc = tx.detach().to(device=means.device, dtype=torch.float32).contiguous()
-        # psi and the backward's by-Gaussian index overlap the geometry chain
-        geo = raster.build_geometry(scene, psi_tx=txc, index=True)
+        # psi and the composite are queued behind the geometry's two host reads
+        geo = raster.build_geometry(scene, psi_tx=txc, index=True, forward=True)
         psi = geo.psi
         S = raster.forward(geo, psi)
         ctx.scene, ctx.geo, ctx.psi, ctx.tx = scene, geo, psi, txc

@@ -342,6 +342,8 @@ __global__ void __launch_bounds__(NT) k_hits(
                     --k;
                     ps = (ps - 1) & (PCAP - 1);
                 }
+                // emit_hit reads rho from the record later: bring its line into L1 now
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(&geom[g].rho_re));
                 const int qs = (ps + 1) & (PCAP - 1);
                 S.pt[qs][tid] = t_mid;
                 S.pg[qs][tid] = g;
@@ -519,10 +521,10 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
     if (n_tiles <= 0) return RFS_OK;
     int rc;
     if (pcap <= 16)
-        rc = launch_hits<16, 64, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
+        rc = launch_hits<16, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
                                      tiles_u, hcap, slab, counts, slow_list, stats, st);
     else if (pcap <= 32)
-        rc = launch_hits<32, 64, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
+        rc = launch_hits<32, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
                                      tiles_u, hcap, slab, counts, slow_list, stats, st);
     else
         rc = launch_hits<64, 32, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,

@@ -12,8 +12,9 @@
 //             this takes the direct form), dF/dx = 2 (x - y)
 //   total   = (1 - w_ssim - w_fourier) L1 + w_ssim SSIM + w_fourier Fourier
 // and lam = 2 dL/dx S (upstream_to_ray), the complex-packed upstream of the
-// backward.  The window statistics run in fp64 (E[x^2] - E[x]^2 cancels);
-// every reduction uses fixed-order per-block partials (deterministic).
+// backward.  The window statistics run in fp32 on tile-centred frames (the
+// centring removes the E[x^2] - E[x]^2 cancellation), the per-cell SSIM terms
+// in fp64; every reduction uses fixed-order per-block partials (deterministic).
 //
 // Kernels: k_frame_range (per-frame min / max of y), k_ssim_fwd (tile of 16 x
 // 32 cells + 5-cell halo in shared memory: the five blurred statistics, s and
@@ -28,7 +29,7 @@ constexpr int TU = 16, TV = 32;             // output tile (u rows, v columns)
 constexpr int HU = TU + 2 * LH, HV = TV + 2 * LH;
 constexpr int LT = 256;                     // threads per tile block
 
-__constant__ double c_win[LW];
+__constant__ float c_winf[LW];
 
 // the predicted power frame: given directly (pred) or |S|^2
 __device__ __forceinline__ double power(const float2* __restrict__ S, const float* __restrict__ pred, size_t i) {
@@ -37,12 +38,15 @@ __device__ __forceinline__ double power(const float2* __restrict__ S, const floa
     return (double)s.x * s.x + (double)s.y * s.y;
 }
 
-// per-frame min / max of the ground truth (loss.py:108)
+// per-(frame, chunk) min / max of the ground truth (loss.py:108); the tile
+// kernels reduce a frame's RCH partials themselves
+constexpr int RCH = 32;
 __global__ void __launch_bounds__(256) k_frame_range(const float* __restrict__ gt, int R, float2* __restrict__ range) {
-    const int b = blockIdx.x;
+    const int b = blockIdx.y, c = blockIdx.x;
     const float* y = gt + (size_t)b * R;
+    const int per = (R + RCH - 1) / RCH, i0 = c * per, i1 = min(R, i0 + per);
     float lo = INFINITY, hi = -INFINITY;
-    for (int i = threadIdx.x; i < R; i += 256) {
+    for (int i = i0 + threadIdx.x; i < i1; i += 256) {
         const float v = y[i];
         lo = fminf(lo, v);
         hi = fmaxf(hi, v);
@@ -63,7 +67,7 @@ __global__ void __launch_bounds__(256) k_frame_range(const float* __restrict__ g
             lo = fminf(lo, sl[w]);
             hi = fmaxf(hi, sh[w]);
         }
-        range[b] = make_float2(lo, hi);
+        range[b * RCH + c] = make_float2(lo, hi);
     }
 }
 
@@ -80,11 +84,18 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 struct FwdSmem {
-    double x[HU][HV], y[HU][HV];
-    double h[5][HU][TV];  // v-blurred x, y, xx, yy, xy
+    float x[HU][HV], y[HU][HV];  // centred: x - cx, y - cy (padding cells hold -cx, -cy)
+    float h[5][HU][TV];          // v-blurred x, y, xx, yy, xy of the centred frames
     double red[LT / 32];
+    float c[2];
 };
 
+// The five window statistics in fp32 on frames centred by a per-tile constant
+// c: with the normalised window and the zero padding written as x = 0, the
+// centred frame x - c is -c in the padding, so blur(x - c) = mu_x - c and the
+// (co)variances blur((x-c)^2) - blur(x-c)^2 equal vx - mu_x^2 exactly -- the
+// centring removes the E[x^2] - E[x]^2 cancellation that made fp64 necessary.
+// s, its partials and the sums are then evaluated in fp64 per cell.
 // grid (v tiles, u tiles, frames)
 __global__ void __launch_bounds__(LT) k_ssim_fwd(const float2* __restrict__ S, const float* __restrict__ pred,
                                                  const float* __restrict__ gt,
@@ -94,32 +105,44 @@ __global__ void __launch_bounds__(LT) k_ssim_fwd(const float2* __restrict__ S, c
     FwdSmem& M = *reinterpret_cast<FwdSmem*>(smem_raw);
     const int b = blockIdx.z, u0 = blockIdx.y * TU, v0 = blockIdx.x * TV;
     const size_t R = (size_t)n_az * n_el, fb = (size_t)b * R;
-    const float2 rg = range[b];
-    const double D = fmax((double)rg.y - (double)rg.x, 1e-6);
+    float lo = INFINITY, hi = -INFINITY;
+    for (int k = 0; k < RCH; ++k) {
+        const float2 rg = range[b * RCH + k];
+        lo = fminf(lo, rg.x);
+        hi = fmaxf(hi, rg.y);
+    }
+    const double D = fmax((double)hi - (double)lo, 1e-6);
     const double c1 = (0.01 * D) * (0.01 * D), c2 = (0.03 * D) * (0.03 * D);
+    if (threadIdx.x == 0) {  // centre: the tile's first in-range cell
+        const size_t r0 = fb + (size_t)u0 * n_el + v0;
+        M.c[0] = (float)power(S, pred, r0);
+        M.c[1] = gt[r0];
+    }
+    __syncthreads();
+    const float cx = M.c[0], cy = M.c[1];
     for (int i = threadIdx.x; i < HU * HV; i += LT) {
         const int hu = i / HV, hv = i % HV, u = u0 - LH + hu, v = v0 - LH + hv;
-        double xv = 0.0, yv = 0.0;
+        float xv = 0.f, yv = 0.f;
         if (u >= 0 && u < n_az && v >= 0 && v < n_el) {
             const size_t r = fb + (size_t)u * n_el + v;
-            xv = power(S, pred, r);
+            xv = (float)power(S, pred, r);
             yv = gt[r];
         }
-        M.x[hu][hv] = xv;
-        M.y[hu][hv] = yv;
+        M.x[hu][hv] = xv - cx;
+        M.y[hu][hv] = yv - cy;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < HU * TV; i += LT) {  // correlate along v (axis 1)
         const int hu = i / TV, ov = i % TV;
-        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
 #pragma unroll
         for (int t = 0; t < LW; ++t) {
-            const double w = c_win[t], xv = M.x[hu][ov + t], yv = M.y[hu][ov + t];
-            a0 += w * xv;
-            a1 += w * yv;
-            a2 += w * (xv * xv);
-            a3 += w * (yv * yv);
-            a4 += w * (xv * yv);
+            const float w = c_winf[t], xv = M.x[hu][ov + t], yv = M.y[hu][ov + t];
+            a0 = fmaf(w, xv, a0);
+            a1 = fmaf(w, yv, a1);
+            a2 = fmaf(w, xv * xv, a2);
+            a3 = fmaf(w, yv * yv, a3);
+            a4 = fmaf(w, xv * yv, a4);
         }
         M.h[0][hu][ov] = a0; M.h[1][hu][ov] = a1; M.h[2][hu][ov] = a2; M.h[3][hu][ov] = a3; M.h[4][hu][ov] = a4;
     }
@@ -128,26 +151,29 @@ __global__ void __launch_bounds__(LT) k_ssim_fwd(const float2* __restrict__ S, c
     for (int i = threadIdx.x; i < TU * TV; i += LT) {  // correlate along u (axis 0)
         const int ou = i / TV, ov = i % TV, u = u0 + ou, v = v0 + ov;
         if (u >= n_az || v >= n_el) continue;
-        double m[5] = {0, 0, 0, 0, 0};
+        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int t = 0; t < LW; ++t) {
-            const double w = c_win[t];
+            const float w = c_winf[t];
 #pragma unroll
-            for (int k = 0; k < 5; ++k) m[k] += w * M.h[k][ou + t][ov];
+            for (int k = 0; k < 5; ++k) m[k] = fmaf(w, M.h[k][ou + t][ov], m[k]);
         }
-        const double mx = m[0], my = m[1], vx = m[2], vy = m[3], wxy = m[4];
-        const double A1 = 2.0 * mx * my + c1, A2 = 2.0 * (wxy - mx * my) + c2;
-        const double B1 = mx * mx + my * my + c1, B2 = (vx - mx * mx) + (vy - my * my) + c2;
-        const double s = (A1 * A2) / (B1 * B2);
+        const double ex = m[0], ey = m[1];  // centred means
+        const double mx = (double)cx + ex, my = (double)cy + ey;
+        const double varx = (double)m[2] - ex * ex, vary = (double)m[3] - ey * ey, cov = (double)m[4] - ex * ey;
+        const double A1 = 2.0 * mx * my + c1, A2 = 2.0 * cov + c2;
+        const double B1 = mx * mx + my * my + c1, B2 = varx + vary + c2;
+        const double inv = 1.0 / (B1 * B2);  // one division: 1/B1 = B2 inv, 1/B2 = B1 inv
+        const double s = A1 * A2 * inv;
         s_sum += s;
-        const double ds_dmu = 2.0 * my * (A2 - A1) / (B1 * B2) - 2.0 * mx * s * (1.0 / B1 - 1.0 / B2);
-        const double ds_dv = -s / B2;
-        const double ds_dw = 2.0 * A1 / (B1 * B2);
+        const double ds_dmu = 2.0 * my * (A2 - A1) * inv - 2.0 * mx * s * ((B2 - B1) * inv);
+        const double ds_dv = -s * (B1 * inv);
+        const double ds_dw = 2.0 * A1 * inv;
         const size_t r = fb + (size_t)u * n_el + v;
         maps[r] = (float)ds_dmu;
         maps[R * gridDim.z + r] = (float)ds_dv;
         maps[2 * R * gridDim.z + r] = (float)ds_dw;
-        const double d = M.x[ou + LH][ov + LH] - M.y[ou + LH][ov + LH];
+        const double d = power(S, pred, r) - (double)gt[r];  // exact inputs, not the centred copies
         l1 += fabs(d);
         sq += d * d;
     }
@@ -165,7 +191,7 @@ __global__ void __launch_bounds__(LT) k_ssim_fwd(const float2* __restrict__ S, c
 
 struct BwdSmem {
     float m[3][HU][HV];
-    double h[3][HU][TV];
+    float h[3][HU][TV];
 };
 
 __global__ void __launch_bounds__(LT) k_ssim_bwd(const float2* __restrict__ S, const float* __restrict__ pred,
@@ -186,12 +212,12 @@ __global__ void __launch_bounds__(LT) k_ssim_bwd(const float2* __restrict__ S, c
     __syncthreads();
     for (int i = threadIdx.x; i < HU * TV; i += LT) {  // adjoint of the zero-padded correlation = itself
         const int hu = i / TV, ov = i % TV;
-        double a[3] = {0, 0, 0};
+        float a[3] = {0.f, 0.f, 0.f};
 #pragma unroll
         for (int t = 0; t < LW; ++t) {
-            const double w = c_win[t];
+            const float w = c_winf[t];
 #pragma unroll
-            for (int k = 0; k < 3; ++k) a[k] += w * (double)M.m[k][hu][ov + t];
+            for (int k = 0; k < 3; ++k) a[k] = fmaf(w, M.m[k][hu][ov + t], a[k]);
         }
 #pragma unroll
         for (int k = 0; k < 3; ++k) M.h[k][hu][ov] = a[k];
@@ -201,17 +227,17 @@ __global__ void __launch_bounds__(LT) k_ssim_bwd(const float2* __restrict__ S, c
     for (int i = threadIdx.x; i < TU * TV; i += LT) {
         const int ou = i / TV, ov = i % TV, u = u0 + ou, v = v0 + ov;
         if (u >= n_az || v >= n_el) continue;
-        double a[3] = {0, 0, 0};
+        float a[3] = {0.f, 0.f, 0.f};
 #pragma unroll
         for (int t = 0; t < LW; ++t) {
-            const double w = c_win[t];
+            const float w = c_winf[t];
 #pragma unroll
-            for (int k = 0; k < 3; ++k) a[k] += w * M.h[k][ou + t][ov];
+            for (int k = 0; k < 3; ++k) a[k] = fmaf(w, M.h[k][ou + t][ov], a[k]);
         }
         const size_t r = fb + (size_t)u * n_el + v;
         const double x = power(S, pred, r), y = gt[r], d = x - y;
         const double g1 = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_n;          // loss.py:65-72
-        const double g2 = -(a[0] + a[1] * 2.0 * x + a[2] * y) * inv_n;                // loss.py:124-128
+        const double g2 = -((double)a[0] + (double)a[1] * 2.0 * x + (double)a[2] * y) * inv_n;                // loss.py:124-128
         const double g3 = 2.0 * d;                                                    // loss.py:146
         const double gx = (double)w1 * g1 + (double)ws * g2 + (double)wf * g3;        // loss.py:149-155
         if (grad) grad[r] = (float)gx;
@@ -222,18 +248,26 @@ __global__ void __launch_bounds__(LT) k_ssim_bwd(const float2* __restrict__ S, c
     }
 }
 
-// report[b] = {total, l1, ssim, fourier}
+// report[b] = {total, l1, ssim, fourier}; one warp per frame, fixed order
 __global__ void k_loss_final(const double* __restrict__ part, int nblk, int n_frames, double n_cells, double w1,
                              double ws, double wf, double* __restrict__ report) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (b >= n_frames) return;
     double s = 0.0, l1 = 0.0, sq = 0.0;
-    for (int k = 0; k < nblk; ++k) {
+    for (int k = lane; k < nblk; k += 32) {
         const double* p = part + ((size_t)b * nblk + k) * 3;
         s += p[0];
         l1 += p[1];
         sq += p[2];
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    }
+    if (lane) return;
     const double L1 = l1 / n_cells, SS = 1.0 - s / n_cells, FO = sq;
     report[4 * b + 0] = w1 * L1 + ws * SS + wf * FO;
     report[4 * b + 1] = L1;
@@ -251,8 +285,9 @@ int ensure_window() {
         w[i] = exp(-(x * x) / (2.0 * 1.5 * 1.5));
         sum += w[i];
     }
-    for (int i = 0; i < LW; ++i) w[i] /= sum;
-    RFS_CUDA_TRY(cudaMemcpyToSymbol(c_win, w, sizeof(w)));
+    float wf[LW];
+    for (int i = 0; i < LW; ++i) wf[i] = (float)(w[i] / sum);
+    RFS_CUDA_TRY(cudaMemcpyToSymbol(c_winf, wf, sizeof(wf)));
     RFS_CUDA_TRY(cudaFuncSetAttribute(k_ssim_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwdSmem)));
     RFS_CUDA_TRY(cudaFuncSetAttribute(k_ssim_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem)));
     g_win_ready = true;
@@ -266,7 +301,8 @@ extern "C" {
 size_t rfs_loss_scratch_bytes(int n_frames, int n_az, int n_el) {
     const size_t R = (size_t)n_az * n_el;
     const size_t nblk = (size_t)rfs_ceil_div(n_el, TV) * rfs_ceil_div(n_az, TU);
-    return 3 * R * n_frames * sizeof(float) + nblk * n_frames * 3 * sizeof(double) + n_frames * sizeof(float2) + 256;
+    return 3 * R * n_frames * sizeof(float) + nblk * n_frames * 3 * sizeof(double) +
+           (size_t)n_frames * RCH * sizeof(float2) + 256;
 }
 
 int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const float* pred, const float* gt,
@@ -288,12 +324,12 @@ int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const flo
     p += (size_t)nblk * n_frames * 3 * sizeof(double);
     float2* range = (float2*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
     const double w1 = 1.0 - w_ssim - w_fourier;
-    k_frame_range<<<n_frames, 256, 0, st>>>(gt, (int)R, range);
+    k_frame_range<<<dim3(RCH, n_frames), 256, 0, st>>>(gt, (int)R, range);
     k_ssim_fwd<<<grid, LT, sizeof(FwdSmem), st>>>((const float2*)S, pred, gt, range, n_az, n_el, maps, part);
     k_ssim_bwd<<<grid, LT, sizeof(BwdSmem), st>>>((const float2*)S, pred, gt, maps, n_az, n_el, (float)w1,
                                                   (float)w_ssim, (float)w_fourier, grad, (float2*)lam);
-    k_loss_final<<<rfs_ceil_div(n_frames, 128), 128, 0, st>>>(part, nblk, n_frames, (double)R, w1, w_ssim,
-                                                              w_fourier, report);
+    k_loss_final<<<rfs_ceil_div((long long)n_frames * 32, 128), 128, 0, st>>>(part, nblk, n_frames, (double)R, w1,
+                                                                                w_ssim, w_fourier, report);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

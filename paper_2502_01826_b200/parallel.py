@@ -86,7 +86,7 @@ def dp_step(scene, txs_global, lam_global, include_direction_chain: bool = True,
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     a, b = shard_bounds(int(txs_global.shape[0]), rank, world)
     tx = txs_global[a:b].contiguous()
-    geo = raster.build_geometry(scene, sort_backend=sort_backend, psi_tx=tx, index=True)
+    geo = raster.build_geometry(scene, sort_backend=sort_backend, psi_tx=tx, index=True, forward=True)
     psi = geo.psi
     S = raster.forward(geo, psi)
     g = raster.backward(scene, geo, tx, lam_global[a:b].contiguous(), include_direction_chain, psi=psi)

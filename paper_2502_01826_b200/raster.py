@@ -120,9 +120,8 @@ class Geometry:
     rx: tuple = (0.0, 0.0, 0.0)
     ress_radius: float = 1.0
     gidx: dict | None = None             # by-Gaussian hit index (built on first backward)
-    psi: torch.Tensor | None = None      # psi computed on the side stream (build_geometry(psi_tx=...))
-    psi_ready: object = None             # cuda.Event recorded after it
-    idx_ready: object = None             # cuda.Event recorded after the side-stream index build
+    psi: torch.Tensor | None = None      # psi of build_geometry(psi_tx=...)
+    S: torch.Tensor | None = None        # forward of build_geometry(psi_tx=..., forward=True)
 
     @property
     def n_tiles(self) -> int:
@@ -140,19 +139,6 @@ class Geometry:
 # adaptive capacities, remembered across steps
 _CAPS = {"hcap": 64, "pcap": 16}
 _DIRS: dict = {}
-_SIDE: dict = {}
-
-
-def _side_stream(dev) -> torch.cuda.Stream:
-    """Second stream for work independent of the tile / sort / hit chain."""
-    key = str(dev)
-    s = _SIDE.get(key)
-    if s is None:
-        s = torch.cuda.Stream(device=dev)
-        _SIDE[key] = s
-    return s
-
-
 def ray_directions(n_az: int, n_el: int) -> np.ndarray:
     """render.ray_directions (render.py:103-117) with numpy, as the reference."""
     cell = 360.0 / n_az
@@ -203,24 +189,39 @@ def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand"):
     return (kalt, valt) if res.value else (ckeys, vals)
 
 
+_PINNED: dict = {}
+
+
+def _pinned(dev, name: str, n: int) -> torch.Tensor:
+    """Reusable pinned int32 host buffer (status / statistics readbacks)."""
+    k = (str(dev), name)
+    t = _PINNED.get(k)
+    if t is None or t.numel() < n:
+        t = torch.empty(n, dtype=torch.int32).pin_memory()
+        _PINNED[k] = t
+    return t[:n]
+
+
 def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bool = False,
                    hcap: int | None = None, marks: list | None = None, psi_tx: torch.Tensor | None = None,
-                   index: bool = False) -> Geometry:
+                   index: bool = False, forward: bool = False) -> Geometry:
     """K1-K6: projection, binning, sort, ranges, emission bounds, hit lists.
 
-    `psi_tx` (optional [B,3]) computes psi for that batch on a side stream,
-    concurrently with the tile / sort / hit chain (psi depends only on the
-    scene and the transmitters); `index=True` builds the by-Gaussian hit
-    index for the backward on the side stream after the hit lists, so it
-    overlaps the forward composite.  `marks` (optional list) receives
-    (phase, cuda.Event) pairs recorded after each phase on the current
-    stream, for per-kernel timing in bench.py.
+    Two small device->host reads size the later buffers (M after the scan,
+    the hit statistics after K6).  Each is an asynchronous copy into pinned
+    memory followed by independent GPU work before the host waits, so the
+    device never idles on the round trip: `psi_tx` (optional [B, 3]) enqueues
+    K5 psi for that batch behind the M read (-> geo.psi), and `forward=True`
+    (needs psi_tx) enqueues the K7 composite behind the statistics read
+    (-> geo.S, recomputed in the rare case the hit lists had to be redone).
+    `index=True` builds the by-Gaussian hit index for the backward.  `marks`
+    (optional list) receives (phase, cuda.Event) pairs recorded after each
+    phase on the current stream, for per-kernel timing in bench.py.
     """
     scene.validate()
     lib = _native.load()
     dev = scene.means.device
-    main = torch.cuda.current_stream(dev)
-    psi = psi_ready = None
+    psi = None
     n, n_az, n_el = scene.n, scene.n_az, scene.n_el
     tiles_u = (n_az + TILE - 1) // TILE
     tiles_v = (n_el + TILE - 1) // TILE
@@ -248,7 +249,15 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     temp = torch.empty(int(lib.rfs_scan_temp_elems(nn)), dtype=torch.int32, device=dev)
     _native.call("rfs_exclusive_scan_u32", _ptr(counts), n, _ptr(offsets), status.data_ptr() + 4, _ptr(temp), st)
     _mark(marks, "project+scan")
-    host = status.cpu()  # sync #1: error flags and M
+    status_h = _pinned(dev, "status", 8)
+    status_h.copy_(status, non_blocking=True)
+    ev_m = torch.cuda.Event()
+    ev_m.record()
+    if psi_tx is not None:  # independent work queued behind the M read
+        psi = compute_psi(scene, psi_tx)
+        _mark(marks, "psi")
+    ev_m.synchronize()  # read #1: error flags and M
+    host = status_h.tolist()
     if int(host[0]) & (1 << 1):
         raise GeometryError("a Gaussian is centered on the receiver")
     m = int(host[1]) & 0xFFFFFFFF
@@ -265,27 +274,28 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     _native.call("rfs_lower_bounds", _ptr(ranges), n_tiles, _ptr(vals), _ptr(geom), _ptr(lb), st)
     _mark(marks, "ranges+lb")
 
-    if psi_tx is not None:
-        # psi on a side stream, concurrent with the latency-bound hit-list kernel
-        side = _side_stream(dev)
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            psi = compute_psi(scene, psi_tx)
-            psi_ready = torch.cuda.Event()
-            psi_ready.record(side)
-        psi.record_stream(main)
     hc = 1 << max(0, math.ceil(math.log2(max(int(hcap or _CAPS["hcap"]), 1))))  # power of two: slot >> log2(hcap) = ray
     pc = _CAPS["pcap"]
     ray_counts = torch.empty(R, dtype=torch.int32, device=dev)
     slow = torch.empty(R, dtype=torch.int32, device=dev)
     stats = torch.zeros(8, dtype=torch.int32, device=dev)
+    stats_h = _pinned(dev, "stats", 8)
+    S = None
+    redo_forward = False
     while True:
         slab = torch.empty(R * hc * 16, dtype=torch.uint8, device=dev)
         _native.call("rfs_hits", _ptr(ranges), n_tiles, _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit), _ptr(geom),
                      _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, pc, _ptr(slab), _ptr(ray_counts),
                      _ptr(slow), _ptr(stats), st)
         _mark(marks, "hits")
-        s = stats.cpu().tolist()  # sync #2
+        stats_h.copy_(stats, non_blocking=True)
+        ev_s = torch.cuda.Event()
+        ev_s.record()
+        if forward and psi is not None and S is None:  # queued behind the statistics read
+            S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
+            _mark(marks, "forward")
+        ev_s.synchronize()  # read #2: hit-list statistics
+        s = stats_h.tolist()
         if s[0] > 0:
             # rays whose pending ring overflowed: exact slow path, and a larger
             # ring for the next steps if it happens often
@@ -301,26 +311,21 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                          _ptr(ray_counts), _ptr(pt), _ptr(pg), _ptr(pw), pcap, _ptr(stats), st)
             s2 = stats.cpu().tolist()
             s[1], s[2], s[3] = s2[1], s2[2], s2[3]
+            redo_forward = True
         if s[1] > 0:
             hc = 1 << max(6, math.ceil(math.log2(max(s[2], 1))))
             _CAPS["hcap"] = max(_CAPS["hcap"], hc)
+            redo_forward = True
             continue
         break
     geo = Geometry(n, n_az, n_el, tiles_u, tiles_v, m, geom, rho32, dirs, ckeys[:max(m, 0)], vals[:max(m, 0)],
                    ranges, hc, slab, ray_counts, s, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
-    geo.psi, geo.psi_ready = psi, psi_ready
+    geo.psi = psi
+    if forward and psi is not None:
+        geo.S = S if (S is not None and not redo_forward) else _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
     if index:
-        side = _side_stream(dev)
-        side.wait_stream(main)
-        for t in (slab, ray_counts):
-            t.record_stream(side)
-        with torch.cuda.stream(side):
-            gauss_index(geo)
-            geo.idx_ready = torch.cuda.Event()
-            geo.idx_ready.record(side)
-        for t in geo.gidx.values():
-            if isinstance(t, torch.Tensor):
-                t.record_stream(main)
+        gauss_index(geo)
+        _mark(marks, "gauss_index")
     return geo
 
 
@@ -341,16 +346,19 @@ def compute_psi(scene: DeviceScene, tx: torch.Tensor) -> torch.Tensor:
     return psi
 
 
+def _forward_raw(slab, ray_counts, hcap: int, psi: torch.Tensor, n_az: int, n_el: int) -> torch.Tensor:
+    b = int(psi.shape[1])
+    S = torch.empty((b, n_az, n_el), dtype=torch.complex64, device=psi.device)
+    if b:
+        _native.call("rfs_forward", _ptr(slab), _ptr(ray_counts), hcap, _ptr(psi), b, n_az, n_el, _ptr(S), _stream())
+    return S
+
+
 def forward(geo: Geometry, psi: torch.Tensor) -> torch.Tensor:
     """K7: S [B, n_az, n_el] complex64 from shared hit lists and psi [N, B]."""
-    if geo.psi_ready is not None and psi is geo.psi:
-        torch.cuda.current_stream().wait_event(geo.psi_ready)
-    b = int(psi.shape[1])
-    S = torch.empty((b, geo.n_az, geo.n_el), dtype=torch.complex64, device=psi.device)
-    if b:
-        _native.call("rfs_forward", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, _ptr(psi), b, geo.n_az,
-                     geo.n_el, _ptr(S), _stream())
-    return S
+    if geo.S is not None and psi is geo.psi:
+        return geo.S
+    return _forward_raw(geo.slab, geo.ray_counts, geo.hcap, psi, geo.n_az, geo.n_el)
 
 
 def gauss_index(geo: Geometry) -> None:
@@ -428,10 +436,6 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     R = geo.n_rays
     lib = _native.load()
     gauss_index(geo)
-    if geo.idx_ready is not None:  # built on the side stream by build_geometry(index=True)
-        torch.cuda.current_stream().wait_event(geo.idx_ready)
-    if psi is not None and psi is geo.psi and geo.psi_ready is not None:
-        torch.cuda.current_stream().wait_event(geo.psi_ready)
     gi = geo.gidx
     h = gi["h"]
     _mark(marks, "gauss_index")

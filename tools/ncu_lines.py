@@ -61,5 +61,6 @@ for off, ie, st, src in offs:
 tot_i = sum(v[0] for v in agg.values())
 tot_s = sum(v[1] for v in agg.values())
 print(f"total warp-instructions {tot_i:,}  stall samples {tot_s:,}")
-for ln, (ie, st) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+key = 1 if os.environ.get("BY_STALL") else 0
+for ln, (ie, st) in sorted(agg.items(), key=lambda x: -x[1][key])[:top]:
     print(f"{ie:14,d} {100*ie/tot_i:5.1f}%  stalls {100*st/max(tot_s,1):5.1f}%  {ln}")
