@@ -241,7 +241,7 @@ def run_ours(args):
     kern = {
         "forward": (ab["forward"], ph_ms.get("forward")),
         "backward": (ab["backward"] + ab["epilogue"],
-                     sum(ph_ms.get(k, 0) for k in ("backward_rays", "gauss_index", "grad_geom", "grad_tx"))),
+                     sum(ph_ms.get(k, 0) for k in ("backward_tx", "backward_rays", "gauss_index", "grad_geom"))),
     }
     roof = {}
     for k, (byts, ms) in kern.items():

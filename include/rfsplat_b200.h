@@ -163,7 +163,8 @@ int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, cons
  * (_kernels.py:387-520), d|rho|, d(phase), chain_cov_to_shape
  * (grad.py:134-164) and d_trans_mag_raw = d|rho| sigma(1-sigma)
  * (train.py:161-162).  Writes d_mean (direct term), d_quat, d_log_scale,
- * d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov (nullable).
+ * d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov (nullable); d_mean =
+ * direct term + dm_dir (the bearing chain of rfs_grad_tx, nullable).
  * Scratch: acc64 f64[N*14], part_g i32[rfs_geom_part_elems(H)],
  * part_v f64[14*rfs_geom_part_elems(H)]. */
 size_t rfs_geom_part_elems(int n_hits);
@@ -171,15 +172,16 @@ int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s
                   const uint32_t* s_slot, const void* gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
-                  float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, void* stream);
+                  float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
+                  void* stream);
 
 /* K9b: per-Gaussian TX-dependent terms: d_coeffs = conj(p_acc) conj(basis)
- * (grad.py:255) and the bearing chain added to d_mean (grad.py:167-189),
- * from P of rfs_bwd_gauss (g_off marks Gaussians without hits, whose terms
- * are zero).  accumulate = 1 adds a further TX chunk's terms.  Run after
- * rfs_grad_geom. */
+ * (grad.py:255) and the bearing chain of d_mean (grad.py:167-189) into dm_dir
+ * (f32[N*3]), from P of rfs_bwd_gauss (g_off marks Gaussians without hits,
+ * whose terms are zero).  accumulate = 1 adds a further TX chunk's terms.
+ * Run before rfs_grad_geom, which adds dm_dir to d_mean. */
 int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
-                const int* g_off, int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs,
+                const int* g_off, int include_direction_chain, int accumulate, float* dm_dir, void* d_coeffs,
                 void* stream);
 
 /* Spectrum loss (loss.py:65-155) for n_frames frames [B][n_az*n_el], chained

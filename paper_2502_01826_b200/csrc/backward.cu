@@ -304,9 +304,16 @@ __global__ void __launch_bounds__(256) k_bwd_pfix(int h_tot, int nb, const uint6
     const int h0 = g_off[g];
     if (h0 < c0) return;            // started in an earlier chunk, handled there
     const int w1 = (g_off[g + 1] - 1) / BG_CHUNK;
+    // four chunk partials in flight per lane (fixed order: sequential in v)
     for (int b = lane; b < nb; b += 32) {
         float2 s = part[(size_t)(2 * w + 1) * nb + b];
-        for (int v = w + 1; v <= w1; ++v) s = caddf(s, part[(size_t)(2 * v) * nb + b]);
+        int v = w + 1;
+        for (; v + 3 <= w1; v += 4) {
+            const float2 a0 = part[(size_t)(2 * v) * nb + b], a1 = part[(size_t)(2 * v + 2) * nb + b];
+            const float2 a2 = part[(size_t)(2 * v + 4) * nb + b], a3 = part[(size_t)(2 * v + 6) * nb + b];
+            s = caddf(caddf(caddf(caddf(s, a0), a1), a2), a3);
+        }
+        for (; v <= w1; ++v) s = caddf(s, part[(size_t)(2 * v) * nb + b]);
         P[(size_t)g * nb + b] = s;
     }
 }

@@ -2,19 +2,22 @@
 //
 // K9a k_geom_seg  (thread per hit, hits in Gaussian-sorted order, fp64):
 //     mean / covariance chains of every hit (_kernels.py:387-520) scaled by
-//     the TX-reduced weight gradient GW_k of K8a, plus d|rho| and d(phase);
-//     a warp-level segmented scan sums the hits of each Gaussian.  Gaussians
-//     whose hits straddle warps leave per-warp partials that
-// K9a' k_geom_fix (thread per Gaussian) adds in warp order -- so every sum
-//     has a fixed order (the slot order of the reference's bincount,
-//     grad.py:243-254) and the result is deterministic.
+//     the TX-reduced weight gradient GW_k of K8r, plus d|rho| and d(phase);
+//     each warp sums its runs of equal Gaussian id through shared memory
+//     (one lane per (run, value)).  Gaussians whose hits straddle warps
+//     leave per-warp partials that
+// K9a' k_geom_fix (one warp per 32-hit group where such a Gaussian starts)
+//     adds in group order -- so every sum has a fixed order (the slot order
+//     of the reference's bincount, grad.py:243-254): deterministic.
 // K9c k_geom_final (thread per Gaussian, fp64): d_mean direct term, d_cov,
 //     d|rho|, d(phase), chain_cov_to_shape (grad.py:134-164) and
 //     d_trans_mag_raw = d|rho| sigma (1 - sigma) (train.py:161-162).
-// K9b k_grad_tx (warp per Gaussian, lanes over TX): from p_acc[g][b]
-//     (grad.py:252-254, built by K8c in fixed order), d_coeffs =
-//     conj(p_acc) conj(basis) (grad.py:255) and the bearing chain added to
-//     d_mean (grad.py:167-189).
+// K9b k_grad_tx (warp per Gaussian, lanes over TX; runs right after K8c):
+//     from p_acc[g][b] (grad.py:252-254, built by K8c in fixed order),
+//     d_coeffs = conj(p_acc) conj(basis) (grad.py:255) and the bearing chain
+//     of d_mean (grad.py:167-189) into dm_dir, which K9c adds.
+#include <algorithm>
+
 #include "fle.cuh"
 #include "rfs_common.cuh"
 
@@ -96,57 +99,70 @@ __global__ void __launch_bounds__(256) k_geom_seg(
         v[12] = gsv.y;
         v[13] = gsv.z;
     }
-    // warp segmented inclusive scan by Gaussian id (segments are contiguous)
+    // Segmented sums by Gaussian (segments are contiguous runs of lanes): the
+    // lanes' values go to shared memory and task (segment k, value i) is summed
+    // by one lane over the segment's hits in lane order -- fixed order,
+    // deterministic, and no shuffle-bound scan.
+    __shared__ double sv[256 / 32][32][NACC + 1];
+    __shared__ int sg[256 / 32][32];
+    const int wl = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int gu = __shfl_up_sync(0xffffffffu, g, o);
-#pragma unroll
-        for (int i = 0; i < NACC; ++i) {
-            const double t = __shfl_up_sync(0xffffffffu, v[i], o);
-            if (lane >= o && gu == g) v[i] += t;
-        }
-    }
-    const int gd = __shfl_down_sync(0xffffffffu, g, 1);
-    const bool tail = valid && (lane == 31 || gd != g);
-    if (!tail) return;
-    const int h0 = g_off[g], h1 = g_off[g + 1];
+    for (int i = 0; i < NACC; ++i) sv[wl][lane][i] = v[i];
+    sg[wl][lane] = g;
+    const int gp = __shfl_up_sync(0xffffffffu, g, 1);
+    const unsigned smask = __ballot_sync(0xffffffffu, valid && (lane == 0 || gp != g));
+    const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
+    const int ns = __popc(smask);
+    __syncwarp();
     const int wb = wglob << 5;
-    if (h0 >= wb && h1 - 1 <= wb + 31) {  // whole segment inside this warp
-#pragma unroll
-        for (int i = 0; i < NACC; ++i) acc64[(size_t)g * NACC + i] = v[i];
-        return;
-    }
-    // straddling segment: partial of this warp's first (slot 0) or last (slot 1) segment
-    if (h0 < wb) {
-        part_g[2 * wglob] = g;
-#pragma unroll
-        for (int i = 0; i < NACC; ++i) part_v[(size_t)(2 * wglob) * NACC + i] = v[i];
-    }
-    if (h1 - 1 > wb + 31) {
-        part_g[2 * wglob + 1] = g;
-#pragma unroll
-        for (int i = 0; i < NACC; ++i) part_v[(size_t)(2 * wglob + 1) * NACC + i] = v[i];
+    for (int t = lane; t < ns * NACC; t += 32) {
+        const int k = t / NACC, i = t - k * NACC;
+        const int h_start = __fns(smask, 0, k + 1);
+        const int h_end = k + 1 < ns ? __fns(smask, 0, k + 2) : nvalid;
+        double sum = 0.0;
+        for (int q = h_start; q < h_end; ++q) sum += sv[wl][q][i];
+        const int gk = sg[wl][h_start];
+        const int h0 = g_off[gk], h1 = g_off[gk + 1];
+        if (h0 >= wb && h1 - 1 <= wb + 31) {  // whole segment inside this warp
+            acc64[(size_t)gk * NACC + i] = sum;
+            continue;
+        }
+        // straddling segment: partial of this warp's first (slot 0) or last (slot 1) segment
+        if (h0 < wb) {
+            if (i == 0) part_g[2 * wglob] = gk;
+            part_v[(size_t)(2 * wglob) * NACC + i] = sum;
+        }
+        if (h1 - 1 > wb + 31) {
+            if (i == 0) part_g[2 * wglob + 1] = gk;
+            part_v[(size_t)(2 * wglob + 1) * NACC + i] = sum;
+        }
     }
 }
 
-// Gaussians whose hits straddle warps: one warp per Gaussian, lane l adds the
-// partials of warps w0 + l, w0 + l + 32, ...; the warp tree then combines the
-// lanes -- a fixed order, so the result stays deterministic.
-__global__ void __launch_bounds__(256) k_geom_fix(int n, const int* __restrict__ g_off,
-                                                  const double* __restrict__ part_v, double* __restrict__ acc64) {
+// Gaussians whose hits straddle warps: the warp of the 32-hit group where
+// such a Gaussian starts adds the group partials in group order (lanes over
+// the 14 sums) -- a fixed order, so the result stays deterministic.
+__global__ void __launch_bounds__(256) k_geom_fix(int h, const uint64_t* __restrict__ sorted_g,
+                                                  const int* __restrict__ g_off, const double* __restrict__ part_v,
+                                                  double* __restrict__ acc64) {
     const int lane = threadIdx.x & 31;
-    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (g >= n) return;
-    const int h0 = g_off[g], h1 = g_off[g + 1];
-    if (h1 <= h0) return;
-    const int w0 = h0 >> 5, w1 = (h1 - 1) >> 5;
-    if (w0 == w1) return;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int c0 = w << 5;
+    if (c0 >= h) return;
+    const int c1 = min(c0 + 32, h);
+    if (c1 >= h) return;
+    const uint64_t g = sorted_g[c1 - 1];
+    if (sorted_g[c1] != g) return;  // the last segment ends inside this group
+    const int h0 = g_off[g];
+    if (h0 < c0) return;            // started in an earlier group, handled there
+    const int w1 = (g_off[g + 1] - 1) >> 5;
+    // lane l adds groups w + l, w + l + 32, ... (group w holds g as its last
+    // segment, later groups as their first); then a fixed butterfly over lanes
     double s[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; ++i) s[i] = 0.0;
-    for (int w = w0 + lane; w <= w1; w += 32) {
-        // warp w0 holds g's segment as its last one, later warps as their first
-        const size_t slot = w == w0 ? (size_t)(2 * w0 + 1) : (size_t)(2 * w);
+    for (int v = w + lane; v <= w1; v += 32) {
+        const size_t slot = v == w ? (size_t)(2 * w + 1) : (size_t)(2 * v);
 #pragma unroll
         for (int i = 0; i < NACC; ++i) s[i] += part_v[slot * NACC + i];
     }
@@ -208,15 +224,16 @@ __global__ void __launch_bounds__(128) k_geom_final(int n, const double* __restr
                                                    float* __restrict__ d_mean, float* __restrict__ d_quat,
                                                    float* __restrict__ d_log_scale, float* __restrict__ d_mag,
                                                    float* __restrict__ d_mag_raw, float* __restrict__ d_phase,
-                                                   float* __restrict__ d_cov) {
+                                                   float* __restrict__ d_cov, const float* __restrict__ dm_dir) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     double a[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; ++i) a[i] = acc64[(size_t)g * NACC + i];
-    d_mean[3 * g + 0] = (float)a[0];
-    d_mean[3 * g + 1] = (float)a[1];
-    d_mean[3 * g + 2] = (float)a[2];
+    // direct term + the bearing chain of K9b (which ran before)
+    d_mean[3 * g + 0] = (float)a[0] + (dm_dir ? dm_dir[3 * g + 0] : 0.f);
+    d_mean[3 * g + 1] = (float)a[1] + (dm_dir ? dm_dir[3 * g + 1] : 0.f);
+    d_mean[3 * g + 2] = (float)a[2] + (dm_dir ? dm_dir[3 * g + 2] : 0.f);
     d_mag[g] = (float)a[12];
     const float sg = 1.f / (1.f + expf(-raw[g]));
     d_mag_raw[g] = (float)a[12] * sg * (1.f - sg);
@@ -245,94 +262,114 @@ __device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
 }
 
 // ------------------------------------------------------------------ K9b
-// NJ = TX blocks of 32 per lane (compile time: no dead predicated iterations)
+// NJ = TX blocks of 32 per lane (compile time: no dead predicated iterations).
+// Persistent warps walk Gaussians g, g + nwarps, ...; the next Gaussian's hit
+// range and p_acc row are requested while the current one is evaluated.
 template <int L, int NJ>
 __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     int n, int nb, const float* __restrict__ means, const float2* __restrict__ coeffs, const float* __restrict__ tx,
     const float2* __restrict__ P, const int* __restrict__ g_off, int include_dir, int accumulate,
-    float* __restrict__ d_mean, float2* __restrict__ d_coeffs) {
+    float* __restrict__ dm_dir, float2* __restrict__ d_coeffs) {
     constexpr int K = Fle<L>::K;
     constexpr int NV = 2 * K;
     constexpr int NG = (NV + 31) / 32;
     const int lane = threadIdx.x & 31;
-    const int g = (blockIdx.x * GB_THREADS + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * GB_THREADS) >> 5;
+    int g = (blockIdx.x * GB_THREADS + threadIdx.x) >> 5;
     if (g >= n) return;
     const int nj = (nb + 31) >> 5;
-    const bool any = g_off[g + 1] > g_off[g];  // rows of Gaussians without hits are not written by K8c
-    if (!any) {  // Gaussian not hit: d_coeffs and the bearing term are zero
-        if (!accumulate) {
-            float* dcf = reinterpret_cast<float*>(d_coeffs + (size_t)g * K);
-            for (int i = lane; i < NV; i += 32) dcf[i] = 0.f;
-        }
-        return;
-    }
-    float vals[NG * 32];
+    int h0 = g_off[g], h1 = g_off[g + 1];
+    for (;;) {
+        const int gn = g + nw;
+        int nh0 = 0, nh1 = 0;
+        if (gn < n) {
+            nh0 = g_off[gn];
+            nh1 = g_off[gn + 1];
 #pragma unroll
-    for (int i = 0; i < NG * 32; ++i) vals[i] = 0.f;
-    float dm0 = 0.f, dm1 = 0.f, dm2 = 0.f;
-    const float mxf = means[3 * g], myf = means[3 * g + 1], mzf = means[3 * g + 2];
-    const float2* co = coeffs + (size_t)g * K;
-#pragma unroll 1
-    for (int j = 0; j < NJ; ++j) {
-        const int b = lane + 32 * j;
-        if (j >= nj) break;
-        if (b >= nb) continue;
-        const float2 p = P[(size_t)g * nb + b];
-        const float rx = tx[3 * b] - mxf, ry = tx[3 * b + 1] - myf, rz = tx[3 * b + 2] - mzf;
-        typename Fle<L>::Tables T;
-        Fle<L>::tables(rx, ry, rz, T);
-        float2 dpa = make_float2(0.f, 0.f), dpb = make_float2(0.f, 0.f);
-        Fle<L>::for_each(T, [&](int idx, int m, float2 bv, float2 dbv) {
-            vals[2 * idx] += p.x * bv.x - p.y * bv.y;          // Re conj(P) conj(basis)
-            vals[2 * idx + 1] += -(p.x * bv.y + p.y * bv.x);   // Im
+            for (int j = 0; j < NJ; ++j) {
+                const int b = lane + 32 * j;
+                if (j < nj && b < nb) asm volatile("prefetch.global.L1 [%0];" ::"l"(P + (size_t)gn * nb + b));
+            }
+        }
+        float* dcf = reinterpret_cast<float*>(d_coeffs + (size_t)g * K);
+        if (h1 <= h0) {  // Gaussian not hit (its p_acc row is not written by K8c): zero terms
+            if (!accumulate) {
+                for (int i = lane; i < NV; i += 32) dcf[i] = 0.f;
+                if (lane < 3) dm_dir[3 * g + lane] = 0.f;
+            }
+        } else {
+        float vals[NG * 32];
+    #pragma unroll
+        for (int i = 0; i < NG * 32; ++i) vals[i] = 0.f;
+        float dm0 = 0.f, dm1 = 0.f, dm2 = 0.f;
+        const float mxf = means[3 * g], myf = means[3 * g + 1], mzf = means[3 * g + 2];
+        const float2* co = coeffs + (size_t)g * K;
+    #pragma unroll 1
+        for (int j = 0; j < NJ; ++j) {
+            const int b = lane + 32 * j;
+            if (j >= nj) break;
+            if (b >= nb) continue;
+            const float2 p = P[(size_t)g * nb + b];
+            const float rx = tx[3 * b] - mxf, ry = tx[3 * b + 1] - myf, rz = tx[3 * b + 2] - mzf;
+            typename Fle<L>::Tables T;
+            Fle<L>::tables(rx, ry, rz, T);
+            float2 dpa = make_float2(0.f, 0.f), dpb = make_float2(0.f, 0.f);
+            Fle<L>::for_each(T, [&](int idx, int m, float2 bv, float2 dbv) {
+                vals[2 * idx] += p.x * bv.x - p.y * bv.y;          // Re conj(P) conj(basis)
+                vals[2 * idx + 1] += -(p.x * bv.y + p.y * bv.x);   // Im
+                if (include_dir) {
+                    const float2 cc = __ldg(&co[idx]);
+                    const float2 cb = cmulf(cc, bv);
+                    dpa.x += -(float)m * cb.y;  // d psi / d alpha = sum c (i m) basis
+                    dpa.y += (float)m * cb.x;
+                    dpb = caddf(dpb, cmulf(cc, dbv));
+                }
+            });
             if (include_dir) {
-                const float2 cc = __ldg(&co[idx]);
-                const float2 cb = cmulf(cc, bv);
-                dpa.x += -(float)m * cb.y;  // d psi / d alpha = sum c (i m) basis
-                dpa.y += (float)m * cb.x;
-                dpb = caddf(dpb, cmulf(cc, dbv));
-            }
-        });
-        if (include_dir) {
-            const float zeta2 = rx * rx + ry * ry + rz * rz;
-            const float rho2 = rx * rx + ry * ry;
-            if (sqrtf(zeta2) > 1e-12f && rho2 > 1e-18f * zeta2) {
-                const float rho = sqrtf(rho2);
-                const float ga = p.x * dpa.x - p.y * dpa.y;  // Re(p dpsi/dalpha)
-                const float gb = p.x * dpb.x - p.y * dpb.y;
-                dm0 -= ga * (-ry / rho2) + gb * (-rz * rx / (rho * zeta2));
-                dm1 -= ga * (rx / rho2) + gb * (-rz * ry / (rho * zeta2));
-                dm2 -= gb * (rho / zeta2);
+                const float zeta2 = rx * rx + ry * ry + rz * rz;
+                const float rho2 = rx * rx + ry * ry;
+                if (sqrtf(zeta2) > 1e-12f && rho2 > 1e-18f * zeta2) {
+                    const float rho = sqrtf(rho2);
+                    const float ga = p.x * dpa.x - p.y * dpa.y;  // Re(p dpsi/dalpha)
+                    const float gb = p.x * dpb.x - p.y * dpb.y;
+                    dm0 -= ga * (-ry / rho2) + gb * (-rz * rx / (rho * zeta2));
+                    dm1 -= ga * (rx / rho2) + gb * (-rz * ry / (rho * zeta2));
+                    dm2 -= gb * (rho / zeta2);
+                }
             }
         }
-    }
-    float mine[NG];
+            float mine[NG];
 #pragma unroll
-    for (int q = 0; q < NG; ++q) mine[q] = transpose_reduce32(vals + 32 * q, lane);
-    dm0 = warp_sum(dm0);
-    dm1 = warp_sum(dm1);
-    dm2 = warp_sum(dm2);
-    float* dcf = reinterpret_cast<float*>(d_coeffs + (size_t)g * K);
+            for (int q = 0; q < NG; ++q) mine[q] = transpose_reduce32(vals + 32 * q, lane);
+            dm0 = warp_sum(dm0);
+            dm1 = warp_sum(dm1);
+            dm2 = warp_sum(dm2);
 #pragma unroll
-    for (int q = 0; q < NG; ++q) {
-        const int i = 32 * q + lane;
-        if (i < NV) dcf[i] = accumulate ? dcf[i] + mine[q] : mine[q];
-    }
-    if (lane == 0) {  // K9c wrote the direct mean term; add the bearing chain
-        d_mean[3 * g + 0] += dm0;
-        d_mean[3 * g + 1] += dm1;
-        d_mean[3 * g + 2] += dm2;
+            for (int q = 0; q < NG; ++q) {
+                const int i = 32 * q + lane;
+                if (i < NV) dcf[i] = accumulate ? dcf[i] + mine[q] : mine[q];
+            }
+            if (lane == 0) {  // bearing chain of d_mean (grad.py:167-189); K9c adds the direct term
+                dm_dir[3 * g + 0] = accumulate ? dm_dir[3 * g + 0] + dm0 : dm0;
+                dm_dir[3 * g + 1] = accumulate ? dm_dir[3 * g + 1] + dm1 : dm1;
+                dm_dir[3 * g + 2] = accumulate ? dm_dir[3 * g + 2] + dm2 : dm2;
+            }
+        }
+        if (gn >= n) break;
+        g = gn;
+        h0 = nh0;
+        h1 = nh1;
     }
 }
 
 template <int L>
 void launch_tx(unsigned grid, cudaStream_t st, int n, int nb, const float* means, const float2* coeffs,
-               const float* tx, const float2* P, const int* g_off, int include_dir, int accumulate, float* d_mean,
+               const float* tx, const float2* P, const int* g_off, int include_dir, int accumulate, float* dm_dir,
                float2* d_coeffs) {
     const int nj = (nb + 31) / 32;
 #define RFS_GT(NJV)                                                                                                \
     k_grad_tx<L, NJV><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, g_off, include_dir, accumulate,   \
-                                                   d_mean, d_coeffs)
+                                                   dm_dir, d_coeffs)
     if (nj <= 2) RFS_GT(2); else RFS_GT(8);
 #undef RFS_GT
 }
@@ -347,7 +384,8 @@ int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s
                   const uint32_t* s_slot, const void* gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
-                  float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, void* stream) {
+                  float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
+                  void* stream) {
     if (n <= 0) return RFS_OK;
     cudaStream_t st = (cudaStream_t)stream;
     RFS_CUDA_TRY(cudaMemsetAsync(acc64, 0, sizeof(double) * NACC * (size_t)n, st));
@@ -355,25 +393,28 @@ int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s
         k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
                                                                (const RfsGeom*)geom, dirs, g_off, rx[0], rx[1], rx[2],
                                                                ress_radius, acc64, part_g, part_v);
-        k_geom_fix<<<rfs_ceil_div((long long)n * 32, 256), 256, 0, st>>>(n, g_off, part_v, acc64);
+        k_geom_fix<<<rfs_ceil_div((long long)rfs_ceil_div(n_hits, 32) * 32, 256), 256, 0, st>>>(n_hits, sorted_g,
+                                                                                              g_off, part_v, acc64);
     }
     k_geom_final<<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, acc64, quats, log_scales, trans_mag_raw, d_mean, d_quat,
-                                                       d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov);
+                                                       d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov,
+                                                       dm_dir);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
 int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
-                const int* g_off, int include_direction_chain, int accumulate, float* d_mean, void* d_coeffs,
+                const int* g_off, int include_direction_chain, int accumulate, float* dm_dir, void* d_coeffs,
                 void* stream) {
     if (n <= 0) return RFS_OK;
     if (n_tx > 32 * GB_MAXJ) return RFS_ERR_SHAPE;
     if (P == nullptr || g_off == nullptr) return RFS_ERR_CONTRACT;
     cudaStream_t st = (cudaStream_t)stream;
-    unsigned grid = (unsigned)rfs_ceil_div((long long)n * 32, GB_THREADS);
+    // persistent: 4 blocks of 4 warps per SM (128 registers per thread)
+    unsigned grid = (unsigned)std::min<long long>(rfs_ceil_div((long long)n * 32, GB_THREADS), 148LL * 4);
 #define RFS_TX(LL)                                                                                                   \
     launch_tx<LL>(grid, st, n, n_tx, means, (const float2*)coeffs, tx, (const float2*)P, g_off,                     \
-                  include_direction_chain, accumulate, d_mean, (float2*)d_coeffs)
+                  include_direction_chain, accumulate, dm_dir, (float2*)d_coeffs)
     switch (degree) {
         case 0: RFS_TX(0); break;
         case 1: RFS_TX(1); break;

@@ -441,7 +441,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     _mark(marks, "gauss_index")
     C = torch.empty(R * geo.hcap, dtype=torch.complex64, device=dev)        # slab order, live slots written
     gs = torch.empty((R * geo.hcap, 4), dtype=torch.float32, device=dev)   # per-hit scalars of K8r, slab order
-    chunks = []
+    dm_dir = torch.empty((n, 3), dtype=torch.float32, device=dev)          # bearing chain of d_mean (K9b)
     for c0 in range(0, b, MAX_TX_PER_LAUNCH):
         c1 = min(b, c0 + MAX_TX_PER_LAUNCH)
         nbc = c1 - c0
@@ -454,7 +454,10 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         _native.call("rfs_bwd_gauss", n, h, nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_slot"]), geo.hcap,
                      _ptr(gi["s_wt"]), _ptr(gi["g_off"]), _ptr(psic), _ptr(lamT), int(c0 > 0), _ptr(C), _ptr(P),
                      _ptr(part), st)
-        chunks.append((txc, P))
+        _native.call("rfs_grad_tx", n, nbc, scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs), _ptr(txc),
+                     _ptr(P), _ptr(gi["g_off"]), int(bool(include_direction_chain)), int(c0 > 0), _ptr(dm_dir),
+                     _ptr(out["d_coeffs"]), st)
+    _mark(marks, "backward_tx")
     _native.call("rfs_bwd_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, _ptr(geo.rho32), _ptr(C),
                  _ptr(gs), st)
     _mark(marks, "backward_rays")
@@ -464,17 +467,12 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     part_g = torch.empty(npart, dtype=torch.int32, device=dev)
     part_v = torch.empty((npart, 14), dtype=torch.float64, device=dev)
     _native.call("rfs_grad_geom", n, h, _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(gi["s_slot"]),
-                 _ptr(gs),
-                 _ptr(gi["g_off"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius), _ptr(scene.quats),
-                 _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(acc64), _ptr(part_g), _ptr(part_v),
-                 _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]), _ptr(out["d_trans_mag"]),
-                 _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]), _ptr(out["d_cov"]), st)
+                 _ptr(gs), _ptr(gi["g_off"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius),
+                 _ptr(scene.quats), _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(acc64), _ptr(part_g),
+                 _ptr(part_v), _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]),
+                 _ptr(out["d_trans_mag"]), _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]), _ptr(out["d_cov"]),
+                 _ptr(dm_dir), st)
     _mark(marks, "grad_geom")
-    for i, (txc, P) in enumerate(chunks):
-        _native.call("rfs_grad_tx", n, int(txc.shape[0]), scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs),
-                     _ptr(txc), _ptr(P), _ptr(gi["g_off"]), int(bool(include_direction_chain)), int(i > 0),
-                     _ptr(out["d_mean"]), _ptr(out["d_coeffs"]), st)
-    _mark(marks, "grad_tx")
     return out
 
 
