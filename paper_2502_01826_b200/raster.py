@@ -139,6 +139,17 @@ class Geometry:
 # adaptive capacities, remembered across steps
 _CAPS = {"hcap": 64, "pcap": 16}
 _DIRS: dict = {}
+_SIDE: dict = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    """Second stream for work independent of the main chain (K9b)."""
+    k = str(dev)
+    if k not in _SIDE:
+        _SIDE[k] = torch.cuda.Stream(device=dev)
+    return _SIDE[k]
+
+
 def ray_directions(n_az: int, n_el: int) -> np.ndarray:
     """render.ray_directions (render.py:103-117) with numpy, as the reference."""
     cell = 360.0 / n_az
@@ -439,6 +450,8 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     gi = geo.gidx
     h = gi["h"]
     _mark(marks, "gauss_index")
+    main = torch.cuda.current_stream(dev)
+    side = _side_stream(dev)
     C = torch.empty(R * geo.hcap, dtype=torch.complex64, device=dev)        # slab order, live slots written
     gs = torch.empty((R * geo.hcap, 4), dtype=torch.float32, device=dev)   # per-hit scalars of K8r, slab order
     dm_dir = torch.empty((n, 3), dtype=torch.float32, device=dev)          # bearing chain of d_mean (K9b)
@@ -454,9 +467,15 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         _native.call("rfs_bwd_gauss", n, h, nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_slot"]), geo.hcap,
                      _ptr(gi["s_wt"]), _ptr(gi["g_off"]), _ptr(psic), _ptr(lamT), int(c0 > 0), _ptr(C), _ptr(P),
                      _ptr(part), st)
-        _native.call("rfs_grad_tx", n, nbc, scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs), _ptr(txc),
-                     _ptr(P), _ptr(gi["g_off"]), int(bool(include_direction_chain)), int(c0 > 0), _ptr(dm_dir),
-                     _ptr(out["d_coeffs"]), st)
+        # K9b on a second stream: it needs only P, so it overlaps the ray
+        # recursion and the geometry sums below (K9c waits for it)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            _native.call("rfs_grad_tx", n, nbc, scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs),
+                         _ptr(txc), _ptr(P), _ptr(gi["g_off"]), int(bool(include_direction_chain)), int(c0 > 0),
+                         _ptr(dm_dir), _ptr(out["d_coeffs"]), side.cuda_stream)
+        for t in (txc, P, dm_dir, out["d_coeffs"]):
+            t.record_stream(side)
     _mark(marks, "backward_tx")
     _native.call("rfs_bwd_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, _ptr(geo.rho32), _ptr(C),
                  _ptr(gs), st)
@@ -466,6 +485,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     acc64 = torch.empty((n, 14), dtype=torch.float64, device=dev)
     part_g = torch.empty(npart, dtype=torch.int32, device=dev)
     part_v = torch.empty((npart, 14), dtype=torch.float64, device=dev)
+    main.wait_stream(side)  # K9c adds K9b's bearing chain (dm_dir)
     _native.call("rfs_grad_geom", n, h, _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(gi["s_slot"]),
                  _ptr(gs), _ptr(gi["g_off"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius),
                  _ptr(scene.quats), _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(acc64), _ptr(part_g),
