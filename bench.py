@@ -192,9 +192,11 @@ def run_ours(args):
 
     def step(marks=None):
         # psi queued behind the M read, the composite behind the hit-statistics read
-        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, forward=True)
+        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, forward=True,
+                                   after_forward=lambda S: raster.transpose_upstream(lam))
         psi, S = g0.psi, g0.S
-        g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks, deterministic=args.deterministic)
+        g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks, deterministic=args.deterministic,
+                            lamT=g0.after_result)
         allreduce(g)
         raster._mark(marks, "allreduce")
         return S, g

@@ -98,7 +98,23 @@ KERNELS_PER_CALL = {
 launch_counter = {"kernels": 0}
 
 
+_FN: dict = {}
+_CUDA_OK = False
+
+
 def call(name: str, *args) -> None:
-    rc = getattr(load(), name)(*args)
-    raise_for_status(int(rc), name)
+    """Call an entry point; raises the rfsplat error class of a non-zero status.
+
+    Hot path (tens of calls per step): the bound ctypes function is cached
+    after the first (checked) load, so a call costs the ctypes dispatch only.
+    """
+    global _CUDA_OK
+    fn = _FN.get(name)
+    if fn is None or not _CUDA_OK:
+        fn = getattr(load(), name)
+        _FN[name] = fn
+        _CUDA_OK = True
+    rc = fn(*args)
+    if rc:
+        raise_for_status(int(rc), name)
     launch_counter["kernels"] += KERNELS_PER_CALL.get(name, 0)

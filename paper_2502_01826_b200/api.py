@@ -281,12 +281,17 @@ def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torc
     tx.record_stream(main)
     gt.record_stream(main)
     main.wait_event(tx_ready)
-    geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True, forward=True)
-    psi = geo.psi
-    S = raster.forward(geo, psi)
-    main.wait_event(gt_ready)
-    rep, lam, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier)
-    g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=psi)
+
+    def loss_and_upstream(S):  # queued behind the geometry's hit-statistics read
+        main.wait_event(gt_ready)
+        rep, lam, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier)
+        lamT = raster.transpose_upstream(lam) if lam.shape[0] <= raster.MAX_TX_PER_LAUNCH else None
+        return rep, lam, lamT
+
+    geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True, forward=True,
+                                after_forward=loss_and_upstream)
+    rep, lam, lamT = geo.after_result
+    g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=geo.psi, lamT=lamT)
     if reduce_fn is not None:
         reduce_fn(g)
     report_host.copy_(rep, non_blocking=True)

@@ -22,7 +22,8 @@ import torch
 from . import _native
 from .errors import GeometryError, ShapeError
 
-__all__ = ["DeviceScene", "Geometry", "build_geometry", "compute_psi", "forward", "backward", "GRAD_FIELDS",
+__all__ = ["DeviceScene", "Geometry", "build_geometry", "compute_psi", "forward", "backward", "transpose_upstream",
+           "GRAD_FIELDS",
            "ray_directions"]
 
 TILE = 16
@@ -36,7 +37,8 @@ def _ptr(t: torch.Tensor | None):
 
 
 def _stream():
-    return torch.cuda.current_stream().cuda_stream
+    """Raw cudaStream_t of the current stream (the cheap accessor: no Stream object)."""
+    return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())
 
 
 def _mark(marks, name):
@@ -122,6 +124,7 @@ class Geometry:
     gidx: dict | None = None             # by-Gaussian hit index (built on first backward)
     psi: torch.Tensor | None = None      # psi of build_geometry(psi_tx=...)
     S: torch.Tensor | None = None        # forward of build_geometry(psi_tx=..., forward=True)
+    after_result: object = None          # return value of build_geometry(after_forward=...)
 
     @property
     def n_tiles(self) -> int:
@@ -215,7 +218,7 @@ def _pinned(dev, name: str, n: int) -> torch.Tensor:
 
 def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bool = False,
                    hcap: int | None = None, marks: list | None = None, psi_tx: torch.Tensor | None = None,
-                   index: bool = False, forward: bool = False) -> Geometry:
+                   index: bool = False, forward: bool = False, after_forward=None) -> Geometry:
     """K1-K6: projection, binning, sort, ranges, emission bounds, hit lists.
 
     Two small device->host reads size the later buffers (M after the scan,
@@ -224,7 +227,10 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     device never idles on the round trip: `psi_tx` (optional [B, 3]) enqueues
     K5 psi for that batch behind the M read (-> geo.psi), and `forward=True`
     (needs psi_tx) enqueues the K7 composite behind the statistics read
-    (-> geo.S, recomputed in the rare case the hit lists had to be redone).
+    (-> geo.S, recomputed in the rare case the hit lists had to be redone);
+    `after_forward(S)` (optional) enqueues further work on S in the same
+    window (e.g. the loss and the upstream transpose), result in
+    geo.after_result.
     `index=True` builds the by-Gaussian hit index for the backward.  `marks`
     (optional list) receives (phase, cuda.Event) pairs recorded after each
     phase on the current stream, for per-kernel timing in bench.py.
@@ -305,6 +311,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         if forward and psi is not None and S is None:  # queued behind the statistics read
             S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
             _mark(marks, "forward")
+            after = after_forward(S) if after_forward is not None else None
         ev_s.synchronize()  # read #2: hit-list statistics
         s = stats_h.tolist()
         if s[0] > 0:
@@ -333,7 +340,11 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                    ranges, hc, slab, ray_counts, s, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
     geo.psi = psi
     if forward and psi is not None:
-        geo.S = S if (S is not None and not redo_forward) else _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
+        if S is None or redo_forward:
+            S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
+            after = after_forward(S) if after_forward is not None else None
+        geo.S = S
+        geo.after_result = after
     if index:
         gauss_index(geo)
         _mark(marks, "gauss_index")
@@ -408,9 +419,23 @@ def gauss_index(geo: Geometry) -> None:
                 "s_slot": slots}
 
 
+def transpose_upstream(grad_S: torch.Tensor) -> torch.Tensor:
+    """K8t: lam [B, n_az, n_el] -> lamT [R, B] (a ray's TX row contiguous).
+
+    backward() does this itself; callers that know lambda early may enqueue
+    it sooner and pass the result as backward(lamT=...).  B <= 256.
+    """
+    b = int(grad_S.shape[0])
+    R = int(grad_S.shape[1]) * int(grad_S.shape[2])
+    grad_S = grad_S.to(torch.complex64).contiguous()
+    lamT = torch.empty((R, b), dtype=torch.complex64, device=grad_S.device)
+    _native.call("rfs_lam_transpose", _ptr(grad_S), b, R, _ptr(lamT), _stream())
+    return lamT
+
+
 def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.Tensor,
              include_direction_chain: bool = True, psi: torch.Tensor | None = None,
-             marks: list | None = None, deterministic: bool = False) -> dict:
+             marks: list | None = None, deterministic: bool = False, lamT: torch.Tensor | None = None) -> dict:
     """K8a/K8i/K9: gradients summed over the TX batch (GradientBuffer.add, grad.py:85-92).
 
     grad_S is the complex-packed upstream lambda = dL/dRe S + i dL/dIm S
@@ -460,12 +485,15 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         nbc = c1 - c0
         txc = tx[c0:c1].contiguous()
         psic = psi if (psi is not None and c0 == 0 and c1 == b) else compute_psi(scene, txc)
-        lamT = torch.empty((R, nbc), dtype=torch.complex64, device=dev)
-        _native.call("rfs_lam_transpose", _ptr(grad_S[c0:c1]), nbc, R, _ptr(lamT), st)
+        if lamT is not None and c0 == 0 and c1 == b:
+            lamTc = lamT
+        else:
+            lamTc = torch.empty((R, nbc), dtype=torch.complex64, device=dev)
+            _native.call("rfs_lam_transpose", _ptr(grad_S[c0:c1]), nbc, R, _ptr(lamTc), st)
         P = torch.empty((n, nbc), dtype=torch.complex64, device=dev)
         part = torch.empty(int(lib.rfs_bwd_part_elems(h, nbc)), dtype=torch.complex64, device=dev)
         _native.call("rfs_bwd_gauss", n, h, nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_slot"]), geo.hcap,
-                     _ptr(gi["s_wt"]), _ptr(gi["g_off"]), _ptr(psic), _ptr(lamT), int(c0 > 0), _ptr(C), _ptr(P),
+                     _ptr(gi["s_wt"]), _ptr(gi["g_off"]), _ptr(psic), _ptr(lamTc), int(c0 > 0), _ptr(C), _ptr(P),
                      _ptr(part), st)
         # K9b on a second stream: it needs only P, so it overlaps the ray
         # recursion and the geometry sums below (K9c waits for it)
