@@ -361,21 +361,19 @@ __global__ void __launch_bounds__(256) k_fill(int n, const Rect* __restrict__ re
 }
 
 // K4: per-tile [start, end) = searchsorted left/right (splat.py:340-343)
+// thread per sorted incidence i in [0, m]: where the tile id steps from
+// prev to cur, i starts tiles prev+1..cur and ends tiles prev..cur-1
+// (searchsorted left / right, splat.py:340-343); tiles with no incidence
+// get an empty range at the right place.
 __global__ void k_ranges(const uint64_t* __restrict__ ckeys, int m, int n_tiles, int2* __restrict__ ranges) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_tiles) return;
-    int lo = 0, hi = m;
-    while (lo < hi) {  // lower bound of tile t
-        int mid = (lo + hi) >> 1;
-        if ((long long)(ckeys[mid] >> 31) < t) lo = mid + 1; else hi = mid;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > m) return;
+    const long long prev = i > 0 ? (long long)(ckeys[i - 1] >> 31) : -1;
+    const long long cur = i < m ? (long long)(ckeys[i] >> 31) : (long long)n_tiles;
+    for (long long t = prev + 1; t <= cur; ++t) {
+        if (t < n_tiles) ranges[t].x = i;
+        if (t >= 1) ranges[t - 1].y = i;
     }
-    int a = lo;
-    hi = m;
-    while (lo < hi) {  // upper bound
-        int mid = (lo + hi) >> 1;
-        if ((long long)(ckeys[mid] >> 31) <= t) lo = mid + 1; else hi = mid;
-    }
-    ranges[t] = make_int2(a, lo);
 }
 
 // Restore reference keys (tile << 32 | code) for TileIndex.keys.
@@ -393,25 +391,39 @@ __global__ void k_expand_keys(const uint64_t* __restrict__ ckeys, int m, uint64_
 constexpr int LB_THREADS = 256;
 __global__ void __launch_bounds__(LB_THREADS) k_lower_bounds(const int2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                                                               const RfsGeom* __restrict__ geom, double* __restrict__ lb) {
-    __shared__ double s[LB_THREADS];
-    int2 rg = ranges[blockIdx.x];
+    __shared__ double wmin[LB_THREADS / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int2 rg = ranges[blockIdx.x];
     double carry = INFINITY;
-    for (int end = rg.y; end > rg.x; end -= LB_THREADS) {
-        int i = end - 1 - (int)threadIdx.x;  // thread 0 handles the last element
-        double v = i >= rg.x ? geom[vals[i]].lbv : INFINITY;
-        s[threadIdx.x] = v;
-        __syncthreads();
-        // inclusive min-scan over increasing thread index (= decreasing i)
-        for (int o = 1; o < LB_THREADS; o <<= 1) {
-            double t = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : INFINITY;
-            __syncthreads();
-            v = fmin(v, t);
-            s[threadIdx.x] = v;
-            __syncthreads();
+    int end = rg.y;
+    double v_next = INFINITY;
+    {
+        const int i = end - 1 - (int)threadIdx.x;
+        if (i >= rg.x) v_next = geom[vals[i]].lbv;
+    }
+    for (; end > rg.x; end -= LB_THREADS) {
+        const int i = end - 1 - (int)threadIdx.x;  // thread 0 handles the last element
+        double v = v_next;
+        {   // next chunk's gather in flight during this chunk's scan
+            const int j = i - LB_THREADS;
+            v_next = j >= rg.x ? geom[vals[j]].lbv : INFINITY;
         }
-        v = fmin(v, carry);
+        // inclusive min-scan over increasing thread index (= decreasing i)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v = fmin(v, t);
+        }
+        if (lane == 31) wmin[wid] = v;
+        __syncthreads();
+        double pre = carry;
+        for (int w = 0; w < wid; ++w) pre = fmin(pre, wmin[w]);
+        v = fmin(v, pre);
         if (i >= rg.x) lb[i] = v;
-        carry = fmin(carry, s[LB_THREADS - 1]);
+        double tot = carry;
+#pragma unroll
+        for (int w = 0; w < LB_THREADS / 32; ++w) tot = fmin(tot, wmin[w]);
+        carry = tot;
         __syncthreads();
     }
 }
@@ -464,7 +476,7 @@ int rfs_bin_fill(int n, const void* rects, const uint32_t* depth_code, const uin
 }
 
 int rfs_tile_ranges(const uint64_t* ckeys, int m, int n_tiles, int* ranges, void* stream) {
-    k_ranges<<<rfs_ceil_div(n_tiles, 128), 128, 0, (cudaStream_t)stream>>>(ckeys, m, n_tiles, (int2*)ranges);
+    k_ranges<<<rfs_ceil_div(m + 1, 256), 256, 0, (cudaStream_t)stream>>>(ckeys, m, n_tiles, (int2*)ranges);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

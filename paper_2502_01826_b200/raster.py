@@ -216,6 +216,13 @@ def _pinned(dev, name: str, n: int) -> torch.Tensor:
     return t[:n]
 
 
+def _spin(ev: torch.cuda.Event) -> None:
+    """Wait for an event by polling: a blocking wait sleeps and wakes tens of
+    microseconds late, time in which the device would drain its queue."""
+    while not ev.query():
+        pass
+
+
 def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bool = False,
                    hcap: int | None = None, marks: list | None = None, psi_tx: torch.Tensor | None = None,
                    index: bool = False, forward: bool = False, after_forward=None) -> Geometry:
@@ -273,7 +280,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     if psi_tx is not None:  # independent work queued behind the M read
         psi = compute_psi(scene, psi_tx)
         _mark(marks, "psi")
-    ev_m.synchronize()  # read #1: error flags and M
+    _spin(ev_m)  # read #1: error flags and M
     host = status_h.tolist()
     if int(host[0]) & (1 << 1):
         raise GeometryError("a Gaussian is centered on the receiver")
@@ -312,7 +319,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
             _mark(marks, "forward")
             after = after_forward(S) if after_forward is not None else None
-        ev_s.synchronize()  # read #2: hit-list statistics
+        _spin(ev_s)  # read #2: hit-list statistics
         s = stats_h.tolist()
         if s[0] > 0:
             # rays whose pending ring overflowed: exact slow path, and a larger
