@@ -129,6 +129,18 @@ def algo_bytes(n: int, m: int, r: int, b: int) -> dict:
     }
 
 
+def load_traffic() -> dict:
+    """ncu dram bytes per launch of the compositing kernels (profiles/*_traffic.json, newest)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", "*_traffic.json")), key=os.path.getmtime)
+    if not files:
+        return {}
+    d = json.load(open(files[-1]))
+    d["_source"] = os.path.relpath(files[-1], REPO)
+    return d
+
+
 def peaks() -> dict:
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -236,25 +248,39 @@ def run_ours(args):
     ms_per_step = t_ms / args.steps
     value = world * B * args.steps / (t_ms / 1e3)
 
-    # roofline of the compositing kernels (SURVEY.md §8(d) bytes / measured time)
+    # roofline of the compositing kernels (SURVEY.md §8(d) algorithmic bytes per launch / the
+    # launch's mean duration from the CUDA-event marks of the timed steps); traffic = ncu
+    # dram bytes of the same launches from the committed --set full capture (profiles/)
     pk = peaks()
     ab = algo_bytes(ds.n, M, R, B)
     ph_ms = {k: float(np.mean(v)) for k, v in phases.items()}
+    traffic = load_traffic()
     kern = {
-        "forward": (ab["forward"], ph_ms.get("forward")),
-        "backward": (ab["backward"] + ab["epilogue"],
-                     sum(ph_ms.get(k, 0) for k in ("backward_tx", "backward_rays", "gauss_index", "grad_geom"))),
+        "K7 forward composite (k_forward_v)": (ab["forward"], ph_ms.get("forward"), ("k_forward_v",)),
+        "K8 backward composite (k_lam_transpose + k_bwd_gauss_v + k_bwd_pfix + k_bwd_rays)":
+            (ab["backward"], ph_ms.get("backward_tx", 0) + ph_ms.get("backward_rays", 0),
+             ("k_lam_transpose", "k_bwd_gauss_v", "k_bwd_pfix", "k_bwd_rays")),
+        "K9 epilogue (k_grad_tx || k_geom_seg + k_geom_fix + k_geom_final)":
+            (ab["epilogue"], ph_ms.get("grad_geom", 0), ("k_grad_tx", "k_geom_seg", "k_geom_fix", "k_geom_final")),
     }
     roof = {}
-    for k, (byts, ms) in kern.items():
+    for k, (byts, ms, knames) in kern.items():
         ach = byts / (ms / 1e3) / 1e9
+        tr = [traffic.get(kn) for kn in knames]
         roof[k] = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                   "frac": round(ach / pk["hbm_gbs"], 4), "algo_bytes": byts, "ms": round(ms, 4)}
-    dom = max(kern, key=lambda k: kern[k][1])
+                   "frac": round(ach / pk["hbm_gbs"], 4), "algo_bytes": byts, "ms": round(ms, 4),
+                   "traffic": int(sum(tr)) if all(t is not None for t in tr) else None}
+    dom = max((k for k in kern if not k.startswith("K9")), key=lambda k: kern[k][1])
     rl = dict(roof[dom])
     rl["kernel"] = dom
-    rl["traffic"] = None
     rl["peak_source"] = pk["source"]
+    rl["traffic_source"] = traffic.get("_source")
+    # K6 (hit lists) is the longest single kernel; its bound is FP32/FP64 issue + latency, not HBM
+    # (SURVEY.md §8(d)): report its algorithmic flops for context
+    flops_k6 = 64800 * (765 * 10 + 423 * 60)
+    roof["K6 hit lists (k_hits), not HBM-bound"] = {
+        "bound": "fp32 issue", "achieved_tflops": round(flops_k6 / (ph_ms.get("hits", 1) / 1e3) / 1e12, 3),
+        "algo_flops": flops_k6, "ms": round(ph_ms.get("hits", 0), 4)}
 
     # ---- end to end: one training step through the public API (api.train_step_host):
     # TX batch + measured power frames H2D from pinned memory, render, spectrum

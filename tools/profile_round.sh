@@ -8,10 +8,9 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/${TAG}_gpu.txt 2>&1
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --sort cub > gpurun_out/${TAG}_bench_cub.json 2>/dev/null
-timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --deterministic > gpurun_out/${TAG}_bench_det.json 2>/dev/null
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_hits|k_backward_rays|k_forward|k_grad_tx|k_geom_seg|k_onesweep|k_psi" -s 22 -c 14 \
+    -k regex:"k_hits|k_forward_v|k_bwd_gauss_v|k_bwd_pfix|k_bwd_rays|k_lam_transpose|k_grad_tx|k_geom|k_onesweep|k_psi" -c 40 \
     -o gpurun_out/${TAG}_full python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
 echo done

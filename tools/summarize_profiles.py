@@ -24,7 +24,7 @@ def last_json(path):
         return None
 
 
-bench = {k: last_json(os.path.join(G, f"{tag}_{k}.json")) for k in ("bench", "bench_cub", "bench_det")}
+bench = {k: last_json(os.path.join(G, f"{tag}_{k}.json")) for k in ("bench", "bench_cub")}
 json.dump(bench, open(os.path.join(P, f"{tag}_bench.json"), "w"), indent=1)
 
 # launch list: last step only (from the last k_project)
@@ -61,6 +61,17 @@ if os.path.exists(rep):
             "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
             "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct", "launch__grid_size",
             "launch__block_size", "sm__inst_executed.sum"]
+    traffic = {}
+    for r in rows[2:]:
+        kn = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("<unnamed>::", "").split("<")[0]
+        try:
+            byts = float(r[hdr.index("dram__bytes_read.sum")]) + float(r[hdr.index("dram__bytes_write.sum")])
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[units[hdr.index("dram__bytes_read.sum")]]
+        except (ValueError, KeyError):
+            continue
+        traffic.setdefault(kn, []).append(byts * scale)
+    json.dump({k: sum(v) / len(v) for k, v in traffic.items()}, open(os.path.join(P, f"{tag}_traffic.json"), "w"),
+              indent=1)
     with open(os.path.join(P, f"{tag}_ncu_full.txt"), "w") as f:
         f.write("# ncu --set full --clock-control none, kernels of one timed bench step\n")
         for r in rows[2:]:
