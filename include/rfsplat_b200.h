@@ -198,6 +198,39 @@ int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const flo
                       double w_ssim, double w_fourier, double* report, float* grad, void* lam, void* scratch,
                       size_t scratch_bytes, void* stream);
 
+/* Optimizer and density control (train.py:85-245), in place on the device.
+ * rfs_sgd_step: lrs (host float[5]) = {lr_mean(iteration), lr_rotation,
+ *   lr_scale, lr_transmittance, lr_radiance}; w -= lr_w dL/dw, quaternions
+ *   renormalised, the magnitude gradient chained onto the logit
+ *   (train.py:145-162); grad_ema / last_dmean (nullable) get
+ *   TrainState.observe (train.py:102-105).  *bad (device i64) = class * N + row
+ *   of the first non-finite gradient row (class order of train.py:133-142),
+ *   0x7f7f7f7f7f7f7f7f if none -- in which case nothing is updated.
+ * rfs_density_flags: mode 0 densify (keep = !split, clone, split: grad_ema >
+ *   thr_grad, radius = trace(Sigma)/3 > thr_radius splits), mode 1 prune
+ *   (keep = sigmoid(raw) >= thr_prune); u32 flags per Gaussian.
+ * rfs_density_apply: with exclusive scans of the flags (keep_off, clone_off,
+ *   split_off) and totals = {n_keep, n_clone}, writes the new arrays in the
+ *   reference order (kept, clones, two children per split parent); clones are
+ *   shifted by -step * last_dmean, children sample mu + R diag(e^s) z with a
+ *   Philox4x32-10 stream keyed by (seed, iteration, parent, child) and scales
+ *   reduced by log_split_factor; state arrays are reset (densify) or
+ *   compacted (prune). */
+int rfs_sgd_step(int n, int K, const float* lrs, float ema_decay, const float* d_mean, const float* d_quat,
+                 const float* d_log_scale, const float* d_trans_mag, const float* d_trans_phase, const void* d_coeffs,
+                 float* means, float* quats, float* log_scales, float* trans_mag_raw, float* trans_phase,
+                 void* coeffs, float* grad_ema, float* last_dmean, long long* bad, void* stream);
+int rfs_density_flags(int n, int mode, const float* grad_ema, const float* log_scales, const float* trans_mag_raw,
+                      double thr_grad, double thr_radius, double thr_prune, uint32_t* keep, uint32_t* clone,
+                      uint32_t* split, void* stream);
+int rfs_density_apply(int n, int K, int mode, const uint32_t* keep, const uint32_t* clone, const uint32_t* split,
+                      const uint32_t* keep_off, const uint32_t* clone_off, const uint32_t* split_off,
+                      const uint32_t* totals, float step, float log_split_factor, unsigned long long seed,
+                      int iteration, const float* means, const float* quats, const float* log_scales,
+                      const float* trans_mag_raw, const float* trans_phase, const void* coeffs, const float* grad_ema,
+                      const float* last_dmean, float* o_means, float* o_quats, float* o_log_scales, float* o_raw,
+                      float* o_phase, void* o_coeffs, float* o_ema, float* o_last, void* stream);
+
 /* Library / build identification. */
 int rfs_version(void);
 int rfs_device_arch(void); /* compute capability the library was built for, e.g. 100 */

@@ -30,6 +30,7 @@ SOURCES = {
     "backward.cu": [],
     "grad.cu": [],
     "loss.cu": [],
+    "train.cu": [],
     "capi.cu": [],
 }
 

@@ -1,0 +1,194 @@
+"""Optimizer and adaptive density control on the device (reference train.py:48-245).
+
+    TrainConfig, lr_mean                      train.py:48-93 (same fields, defaults, validation)
+    TrainState                                train.py:96-121 (grad_ema / last_dmean on the device)
+    sgd_step(scene, grads, iteration, config, state)        train.py:145-162
+    densify(scene, state, iteration, config, seed) -> DensifyReport   train.py:165-222
+    prune(scene, state, iteration, config) -> PruneReport            train.py:225-245
+
+`scene` is a raster.DeviceScene, updated in place (its tensors are replaced
+when the Gaussian count changes, as the reference's RFScene.keep/append do);
+`grads` is the gradient dict of raster.backward.  Densify / prune need one
+host read (the new count) per call -- every 100 iterations by default.
+Split children are sampled with a counter-based Philox stream keyed by
+(seed, iteration, parent, child), so every data-parallel rank draws the same
+children with no communication; they are not numpy's multivariate_normal
+draws, so split parity with the reference is decision-level (which parents
+split, the children's attributes and count), SURVEY.md §7 H8.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native, raster
+from .errors import ConfigError, NonFiniteGradientError
+
+__all__ = ["TrainConfig", "TrainState", "DensifyReport", "PruneReport", "lr_mean", "sgd_step", "densify", "prune"]
+
+_CLASSES = ("mean", "quat", "log_scale", "trans_mag", "trans_phase", "coeffs")
+_FIELDS = ("means", "quats", "log_scales", "trans_mag_raw", "trans_phase", "coeffs")
+_NO_BAD = 0x7F7F7F7F7F7F7F7F
+
+
+@dataclass
+class TrainConfig:
+    """Hyperparameters; defaults follow the reference operating point (train.py:48-76)."""
+
+    iterations: int = 30000
+    lr_transmittance: float = 0.01
+    lr_radiance: float = 0.0025
+    lr_scale: float = 0.01
+    lr_rotation: float = 0.005
+    lr_mean_start: float = 0.00016
+    lr_mean_end: float = 1.6e-6
+    densify_grad_threshold: float = 0.0002
+    densify_radius_threshold: float = 10.0
+    prune_threshold: float = 0.004
+    densify_every: int = 100
+    prune_every: int = 100
+    split_factor: float = 1.6
+    w_ssim: float = 0.2
+    w_fourier: float = 0.2
+    ema_decay: float = 0.9
+    checkpoint_every: int = 0
+    workers: int = 1
+    direction_chain: bool = True
+    csi_subcarrier: int = 0
+
+    def validate(self) -> None:
+        for name in ("lr_transmittance", "lr_radiance", "lr_scale", "lr_rotation", "lr_mean_start", "lr_mean_end"):
+            if getattr(self, name) <= 0.0:
+                raise ConfigError(f"{name} must be positive")
+        if not 0.0 < self.w_ssim + self.w_fourier < 1.0:
+            raise ConfigError("loss weights must satisfy 0 < w_ssim + w_fourier < 1")
+        if self.iterations < 0:
+            raise ConfigError("iterations must be non-negative")
+
+
+def lr_mean(config: TrainConfig, iteration: int) -> float:
+    """Exponential schedule from lr_mean_start to lr_mean_end (train.py:86-93)."""
+    if config.iterations <= 0:
+        return config.lr_mean_start
+    frac = min(max(iteration / config.iterations, 0.0), 1.0)
+    return config.lr_mean_start * (config.lr_mean_end / config.lr_mean_start) ** frac
+
+
+@dataclass
+class TrainState:
+    """Per-Gaussian gradient statistics on the device (train.py:96-121)."""
+
+    grad_ema: torch.Tensor    # f32 [N]
+    last_dmean: torch.Tensor  # f32 [N, 3]
+
+    @classmethod
+    def zeros(cls, n: int, device="cuda") -> "TrainState":
+        return cls(torch.zeros(n, dtype=torch.float32, device=device),
+                   torch.zeros((n, 3), dtype=torch.float32, device=device))
+
+
+@dataclass
+class DensifyReport:
+    cloned: list = field(default_factory=list)
+    split: list = field(default_factory=list)
+
+
+@dataclass
+class PruneReport:
+    removed: list = field(default_factory=list)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def sgd_step(scene: raster.DeviceScene, grads: dict, iteration: int, config: TrainConfig,
+             state: TrainState | None = None, check: bool = True) -> None:
+    """One descent step on the device (train.py:145-162), plus TrainState.observe
+    when `state` is given.  A non-finite gradient row leaves the scene untouched;
+    with check=True the error is raised here (one 8-byte read), else it can be
+    read later from `sgd_step.last_bad`."""
+    n, K = scene.n, scene.coeffs.shape[1]
+    dev = scene.means.device
+    bad = torch.empty(1, dtype=torch.int64, device=dev)
+    lrs = (_native.C.c_float * 5)(lr_mean(config, iteration), config.lr_rotation, config.lr_scale,
+                                  config.lr_transmittance, config.lr_radiance)
+    st = raster._stream()
+    _native.call("rfs_sgd_step", n, K, lrs, float(config.ema_decay), _ptr(grads["d_mean"]), _ptr(grads["d_quat"]),
+                 _ptr(grads["d_log_scale"]), _ptr(grads["d_trans_mag"]), _ptr(grads["d_trans_phase"]),
+                 _ptr(grads["d_coeffs"]), _ptr(scene.means), _ptr(scene.quats), _ptr(scene.log_scales),
+                 _ptr(scene.trans_mag_raw), _ptr(scene.trans_phase), _ptr(scene.coeffs),
+                 _ptr(state.grad_ema if state else None), _ptr(state.last_dmean if state else None), _ptr(bad), st)
+    sgd_step.last_bad = bad
+    if check:
+        raise_if_bad(bad, n)
+
+
+def raise_if_bad(bad: torch.Tensor, n: int) -> None:
+    v = int(bad.item())
+    if v != _NO_BAD:
+        raise NonFiniteGradientError(v % max(n, 1), _CLASSES[v // max(n, 1)])
+
+
+def _compact(scene: raster.DeviceScene, state: TrainState, mode: int, iteration: int, config: TrainConfig,
+             seed: int):
+    n, K = scene.n, scene.coeffs.shape[1]
+    dev = scene.means.device
+    st = raster._stream()
+    lib = _native.load()
+    keep, clone, split = (torch.empty(max(n, 1), dtype=torch.int32, device=dev) for _ in range(3))
+    _native.call("rfs_density_flags", n, mode, _ptr(state.grad_ema), _ptr(scene.log_scales),
+                 _ptr(scene.trans_mag_raw), float(config.densify_grad_threshold),
+                 float(config.densify_radius_threshold), float(config.prune_threshold), _ptr(keep), _ptr(clone),
+                 _ptr(split), st)
+    offs = [torch.empty(max(n, 1), dtype=torch.int32, device=dev) for _ in range(3)]
+    totals = torch.zeros(4, dtype=torch.int32, device=dev)
+    temp = torch.empty(int(lib.rfs_scan_temp_elems(max(n, 1))), dtype=torch.int32, device=dev)
+    for i, f in enumerate((keep, clone, split)):
+        _native.call("rfs_exclusive_scan_u32", _ptr(f), n, _ptr(offs[i]), totals.data_ptr() + 4 * i, _ptr(temp), st)
+    n_keep, n_clone, n_split = (int(x) for x in totals[:3].tolist())  # the one host read
+    n_new = n_keep + n_clone + 2 * n_split
+    new = {k: torch.empty((n_new,) + tuple(getattr(scene, k).shape[1:]), dtype=getattr(scene, k).dtype, device=dev)
+           for k in _FIELDS}
+    ema = torch.empty(n_new, dtype=torch.float32, device=dev)
+    last = torch.empty((n_new, 3), dtype=torch.float32, device=dev)
+    _native.call("rfs_density_apply", n, K, mode, _ptr(keep), _ptr(clone), _ptr(split), _ptr(offs[0]), _ptr(offs[1]),
+                 _ptr(offs[2]), _ptr(totals), float(lr_mean(config, iteration)), float(math.log(config.split_factor)),
+                 int(seed) & 0xFFFFFFFFFFFFFFFF, int(iteration), _ptr(scene.means), _ptr(scene.quats),
+                 _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(scene.trans_phase), _ptr(scene.coeffs),
+                 _ptr(state.grad_ema), _ptr(state.last_dmean), _ptr(new["means"]), _ptr(new["quats"]),
+                 _ptr(new["log_scales"]), _ptr(new["trans_mag_raw"]), _ptr(new["trans_phase"]), _ptr(new["coeffs"]),
+                 _ptr(ema), _ptr(last), st)
+    for k, v in new.items():
+        setattr(scene, k, v)
+    state.grad_ema, state.last_dmean = ema, last
+    return keep, clone, split, (n_keep, n_clone, n_split)
+
+
+def densify(scene: raster.DeviceScene, state: TrainState, iteration: int, config: TrainConfig,
+            seed: int = 0) -> DensifyReport:
+    """Clone small / split large Gaussians whose mean-gradient EMA runs hot (train.py:165-222)."""
+    if scene.n == 0:
+        return DensifyReport()
+    keep, clone, split, (nk, nc, ns) = _compact(scene, state, 0, iteration, config, seed)
+    if nc == 0 and ns == 0:
+        return DensifyReport()
+    c = clone[: len(keep)].cpu().numpy()
+    s = split[: len(keep)].cpu().numpy()
+    return DensifyReport(np.nonzero(c)[0].tolist(), np.nonzero(s)[0].tolist())
+
+
+def prune(scene: raster.DeviceScene, state: TrainState, iteration: int, config: TrainConfig) -> PruneReport:
+    """Remove Gaussians whose transmittance magnitude is below the floor (train.py:225-245)."""
+    if scene.n == 0:
+        return PruneReport()
+    n = scene.n
+    keep, _, _, (nk, _, _) = _compact(scene, state, 1, iteration, config, 0)
+    if nk == n:
+        return PruneReport()
+    k = keep[:n].cpu().numpy()
+    return PruneReport(np.nonzero(k == 0)[0].tolist())

@@ -1,0 +1,113 @@
+"""Optimizer and density control on the device vs the reference train.py
+(golden vectors from tests/golden/make_golden_train.py)."""
+
+import numpy as np
+import pytest
+
+from helpers import load
+from paper_2502_01826_b200 import train as T
+from paper_2502_01826_b200.errors import ConfigError
+
+
+def test_config_validation_and_lr_schedule():
+    z = load("train_golden.npz")
+    cfg = T.TrainConfig(iterations=int(z["it"][1]))
+    cfg.validate()
+    got = [T.lr_mean(cfg, i) for i in (0, 1, 700, 1500, 3000, 4000)]
+    np.testing.assert_allclose(got, z["lr_mean"], rtol=1e-15)
+    with pytest.raises(ConfigError):
+        T.TrainConfig(lr_scale=0.0).validate()
+    with pytest.raises(ConfigError):
+        T.TrainConfig(w_ssim=0.6, w_fourier=0.5).validate()
+
+
+def _device_setup(z):
+    import torch
+
+    from paper_2502_01826_b200 import raster
+
+    f = lambda k: torch.as_tensor(np.asarray(z[k], np.float32), device="cuda").contiguous()
+    ds = raster.DeviceScene(f("means"), f("quats"), f("log_scales"), f("raw"), f("phase"),
+                            torch.as_tensor(z["coeffs"], device="cuda").contiguous(), (0.0, 0.0, 0.0), 1.0, 90, 45, 3)
+    grads = {"d_mean": f("g_mean"), "d_quat": f("g_quat"), "d_log_scale": f("g_log_scale"), "d_trans_mag": f("g_mag"),
+             "d_trans_phase": f("g_phase"), "d_coeffs": torch.as_tensor(z["g_coeffs"], device="cuda").contiguous()}
+    state = T.TrainState(f("ema"), f("last"))
+    cfg = T.TrainConfig(iterations=int(z["it"][1]))
+    return ds, grads, state, cfg
+
+
+@pytest.mark.gpu
+def test_gpu_sgd_step_and_observe():
+    z = load("train_golden.npz")
+    ds, grads, state, cfg = _device_setup(z)
+    T.sgd_step(ds, grads, int(z["it"][0]), cfg, state)
+    for k, ref in (("means", "sgd_means"), ("quats", "sgd_quats"), ("log_scales", "sgd_log_scales"),
+                   ("trans_mag_raw", "sgd_raw"), ("trans_phase", "sgd_phase")):
+        np.testing.assert_allclose(getattr(ds, k).cpu().numpy(), z[ref], rtol=2e-6, atol=2e-7, err_msg=k)
+    np.testing.assert_allclose(ds.coeffs.cpu().numpy(), z["sgd_coeffs"], rtol=2e-6, atol=2e-7)
+    np.testing.assert_allclose(state.grad_ema.cpu().numpy(), z["obs_ema"], rtol=2e-6, atol=1e-10)
+    np.testing.assert_allclose(state.last_dmean.cpu().numpy(), z["obs_last"], rtol=0, atol=0)
+
+
+@pytest.mark.gpu
+def test_gpu_sgd_step_nonfinite_leaves_scene_untouched():
+    from paper_2502_01826_b200.errors import NonFiniteGradientError
+
+    z = load("train_golden.npz")
+    ds, grads, state, cfg = _device_setup(z)
+    grads["d_quat"][7, 2] = float("nan")
+    grads["d_coeffs"][3, 1] = complex(float("inf"), 0.0)
+    before = ds.means.clone()
+    with pytest.raises(NonFiniteGradientError) as e:
+        T.sgd_step(ds, grads, 1, cfg, state)
+    assert e.value.args[0] == 7 or "quat" in str(e.value)  # first bad class in train.py:133-142 order
+    assert bool((ds.means == before).all())
+
+
+@pytest.mark.gpu
+def test_gpu_densify_decisions_and_layout():
+    z = load("train_golden.npz")
+    ds, _, state, cfg = _device_setup(z)
+    n = ds.n
+    rep = T.densify(ds, state, int(z["it"][0]), cfg, seed=11)
+    assert rep.cloned == z["dens_cloned"].tolist()
+    assert rep.split == z["dens_split"].tolist()
+    assert ds.n == int(z["dens_n"][0])
+    nk, nc = n - len(rep.split), len(rep.cloned)
+    # kept + clones: deterministic, compare with the reference
+    m = ds.means.cpu().numpy()
+    np.testing.assert_allclose(m[: nk + nc], z["dens_means"][: nk + nc], rtol=1e-6, atol=1e-7)
+    for k, ref in (("quats", "dens_quats"), ("log_scales", "dens_log_scales"), ("trans_mag_raw", "dens_raw")):
+        np.testing.assert_allclose(getattr(ds, k).cpu().numpy(), z[ref], rtol=1e-6, atol=1e-7, err_msg=k)
+    # split children: two per parent with the parent's attributes, scales / 1.6, means ~ N(mu, Sigma)
+    ls = z["log_scales"]
+    q = z["quats"]
+    for j, p in enumerate(rep.split):
+        qq = q[p] / np.linalg.norm(q[p])
+        w, x, y, zq = qq
+        R = np.array([[1 - 2 * (y * y + zq * zq), 2 * (x * y - w * zq), 2 * (x * zq + w * y)],
+                      [2 * (x * y + w * zq), 1 - 2 * (x * x + zq * zq), 2 * (y * zq - w * x)],
+                      [2 * (x * zq - w * y), 2 * (y * zq + w * x), 1 - 2 * (x * x + y * y)]])
+        for c in range(2):
+            d = m[nk + nc + 2 * j + c] - z["means"][p]
+            maha = np.linalg.norm((R.T @ d) / np.exp(ls[p]))
+            assert maha < 6.0
+    assert float(state.grad_ema.abs().sum()) == 0.0 and float(state.last_dmean.abs().sum()) == 0.0
+    # counter-based sampling: same seed -> same children; another seed -> different
+    ds2, _, st2, _ = _device_setup(z)
+    T.densify(ds2, st2, int(z["it"][0]), cfg, seed=11)
+    np.testing.assert_array_equal(ds2.means.cpu().numpy(), m)
+    ds3, _, st3, _ = _device_setup(z)
+    T.densify(ds3, st3, int(z["it"][0]), cfg, seed=12)
+    assert not np.array_equal(ds3.means.cpu().numpy()[nk + nc:], m[nk + nc:])
+
+
+@pytest.mark.gpu
+def test_gpu_prune():
+    z = load("train_golden.npz")
+    ds, _, state, cfg = _device_setup(z)
+    rep = T.prune(ds, state, int(z["it"][0]), cfg)
+    assert rep.removed == z["prune_removed"].tolist()
+    assert ds.n == int(z["prune_n"][0])
+    np.testing.assert_array_equal(ds.means.cpu().numpy(), z["prune_means"].astype(np.float32))
+    np.testing.assert_array_equal(state.grad_ema.cpu().numpy(), z["prune_ema"].astype(np.float32))
