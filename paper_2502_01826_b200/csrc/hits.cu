@@ -78,7 +78,9 @@ __device__ __forceinline__ bool exact_hit(const RfsGeom* __restrict__ G, double 
     double qf = DA(DA(DM(DA(DA(DM(i00, ex), DM(i01, ey)), DM(i02, ez)), ex),
                       DM(DA(DA(DM(i01, ex), DM(i11, ey)), DM(i12, ez)), ey)),
                    DM(DA(DA(DM(i02, ex), DM(i12, ey)), DM(i22, ez)), ez));
-    w_out = (float)DM(__ldg(&G->norm), exp(DM(-0.5, qf)));
+    // same arithmetic as exact_hit_s (fp32 exp of the fp64 exponent), so the
+    // slow path and the ring path produce bitwise identical hit lists
+    w_out = (float)__ldg(&G->norm) * expf((float)DM(-0.5, qf));
     return true;
 }
 

@@ -192,3 +192,79 @@ def prune(scene: raster.DeviceScene, state: TrainState, iteration: int, config: 
         return PruneReport()
     k = keep[:n].cpu().numpy()
     return PruneReport(np.nonzero(k == 0)[0].tolist())
+
+
+@dataclass
+class TraceRow:
+    """train.TraceRow (train.py:248-255); losses averaged over the iteration's TX batch."""
+
+    iteration: int
+    total: float
+    l1: float
+    ssim: float
+    fourier: float
+    n_primitives: int
+
+
+def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tensor, config: TrainConfig,
+               batch: int = 1, seed: int = 0, timings: list | None = None):
+    """Batched counterpart of train.train_loop (train.py:284-361) on the device.
+
+    Each iteration draws `batch` samples (TX position + measured power frame)
+    with a seeded generator, renders, evaluates the spectrum loss and its
+    upstream, runs the backward, the SGD step and TrainState.observe; density
+    control runs on the reference schedule during the first half of
+    training.  The scene stays in HBM throughout; the loss trace is read back
+    once at the end.  `timings` (optional list) receives (iteration,
+    milliseconds, n_gaussians, event) per iteration from CUDA events.
+    Returns (trace, densify_reports, prune_reports).
+    """
+    from . import loss as _loss
+
+    config.validate()
+    dev = scene.means.device
+    if tuple(frames.shape[1:]) != (scene.n_az, scene.n_el):
+        raise ConfigError(f"dataset grid {tuple(frames.shape[1:])} does not match scene grid "
+                          f"{(scene.n_az, scene.n_el)}")
+    rng = np.random.default_rng(seed)
+    state = TrainState.zeros(scene.n, dev)
+    reports_d, reports_p, rows, bads = [], [], [], []
+    for it in range(1, config.iterations + 1):
+        idx = torch.as_tensor(rng.integers(len(txs), size=batch), device=dev)
+        tx, gt = txs[idx].contiguous(), frames[idx].contiguous()
+        e0 = torch.cuda.Event(enable_timing=True) if timings is not None else None
+        if e0 is not None:
+            e0.record()
+        event = ""
+        if scene.n > 0:
+            def loss_up(S):
+                rep, lam, _ = _loss.spectrum_loss_frames(S, gt, config.w_ssim, config.w_fourier)
+                return rep, lam
+            geo = raster.build_geometry(scene, psi_tx=tx, forward=True, after_forward=loss_up)
+            rep, lam = geo.after_result
+            g = raster.backward(scene, geo, tx, lam, config.direction_chain, psi=geo.psi)
+            sgd_step(scene, g, it, config, state, check=False)
+            bads.append((sgd_step.last_bad, scene.n))
+            rows.append((it, rep.mean(0), scene.n))
+        if it < config.iterations / 2:
+            if it % config.densify_every == 0 and scene.n > 0:
+                r = densify(scene, state, it, config, seed)
+                if r.cloned or r.split:
+                    reports_d.append((it, r))
+                    event += "densify "
+            if it % config.prune_every == 0 and scene.n > 0:
+                r = prune(scene, state, it, config)
+                if r.removed:
+                    reports_p.append((it, r))
+                    event += "prune "
+        if e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            timings.append((it, e0, e1, scene.n, event.strip()))
+    torch.cuda.synchronize()
+    for bad, n in bads:  # the reference raises at the first non-finite step (train.py:150)
+        raise_if_bad(bad, n)
+    if timings is not None:
+        timings[:] = [(it, a.elapsed_time(b), n, ev) for it, a, b, n, ev in timings]
+    trace = [TraceRow(it, *(float(x) for x in r.tolist()), n) for it, r, n in rows]
+    return trace, reports_d, reports_p

@@ -246,3 +246,37 @@ def test_empty_scene_renders_zero():
     assert np.all(S == 0)
     t = api.build_tiles_for_render(s)
     assert t.keys.size == 0 and np.all(t.ranges == 0)
+
+
+@pytest.mark.gpu
+def test_slow_path_bitwise_equals_ring_path():
+    """Rays whose pending ring overflows are redone by the global-memory slow
+    path; both must give bitwise the same hit lists (run-to-run determinism
+    must not depend on the adaptive ring size) and match the oracle."""
+    import torch
+
+    from paper_2502_01826_b200 import raster
+    from paper_2502_01826_b200.scene import HostScene, cube_init
+
+    c = cube_init([-15] * 3, [15] * 3, 2.5, 72, 36, c00=1.0)
+    rng = np.random.default_rng(4)
+    dup = lambda a, eps=0.0: np.concatenate([a, a + eps * rng.normal(size=a.shape)])  # near-duplicates (clones)
+    s = round_to_f32(HostScene(dup(c.means, 1e-3), dup(c.quats), dup(c.log_scales), dup(c.trans_mag_raw),
+                               dup(c.trans_phase), dup(c.coeffs), c.rx, c.ress_radius, 72, 36, 3))
+    ds = raster.DeviceScene.from_host(s, "cuda")
+    tx = torch.as_tensor(default_txs(2, seed=3), dtype=torch.float32, device="cuda")
+    saved = dict(raster._CAPS)
+    try:
+        out = {}
+        for pc in (16, 64):
+            raster._CAPS["pcap"] = pc
+            g = raster.build_geometry(ds, psi_tx=tx, forward=True)
+            out[pc] = (g.S.cpu().numpy(), g.ray_counts.cpu().numpy(), g.stats[0])
+    finally:
+        raster._CAPS.update(saved)
+    assert out[16][2] > 0 and out[64][2] == 0  # the small ring overflowed somewhere, the large one did not
+    np.testing.assert_array_equal(out[16][0], out[64][0])
+    np.testing.assert_array_equal(out[16][1], out[64][1])
+    ref = oracle.render_complex_frame(s, default_txs(2, seed=3)[0])
+    P, Pr = np.abs(out[64][0][0]) ** 2, np.abs(ref) ** 2
+    assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= 1e-4
