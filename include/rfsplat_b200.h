@@ -198,6 +198,15 @@ int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const flo
                       double w_ssim, double w_fourier, double* report, float* grad, void* lam, void* scratch,
                       size_t scratch_bytes, void* stream);
 
+/* Scalar (single-antenna) modes: total_b = sum_r S[b][r] (render_scalar,
+ * render.py:301-307) and scalar_loss (loss.py:158-180) per frame; mode 0
+ * 'complex' (target complex64[B], CSI), mode 1 'real_power' (target[b].x =
+ * ground-truth dBm, RSSI).  report f64[B*4] = {value, value, 0, 0}; total
+ * (complex64[B], nullable); lam (complex64[B*R], nullable) = the constant
+ * per-frame upstream of the coherent sum (train.py:288). */
+int rfs_scalar_loss(int n_frames, int n_rays, int mode, const void* S, const void* target, double* report,
+                    void* total, void* lam, void* stream);
+
 /* Optimizer and density control (train.py:85-245), in place on the device.
  * rfs_sgd_step: lrs (host float[5]) = {lr_mean(iteration), lr_rotation,
  *   lr_scale, lr_transmittance, lr_radiance}; w -= lr_w dL/dw, quaternions

@@ -275,6 +275,79 @@ __global__ void k_loss_final(const double* __restrict__ part, int nblk, int n_fr
     report[4 * b + 3] = FO;
 }
 
+// ------------------------------------------------------------------ scalar modes
+// Single-antenna output: total = coherent sum of the frame (render_scalar,
+// render.py:301-307) and scalar_loss (loss.py:158-180): mode 0 'complex'
+// |total - target|^2 with upstream 2 (total - target); mode 1 'real_power'
+// |10 log10 |total|^2 - dBm| with upstream sign(.) 20/ln10 total / |total|^2,
+// and |total|^2 <= 1e-20 floored at -200 dBm with zero upstream.  The upstream
+// of a coherent sum is the same for every ray (train.py:288): lam[b][r].
+// One block per frame, fixed-order reduction.
+__global__ void __launch_bounds__(256) k_scalar_loss(const float2* __restrict__ S, int R, int mode,
+                                                     const float2* __restrict__ target, double* __restrict__ report,
+                                                     float2* __restrict__ total_out, float2* __restrict__ lam) {
+    const int b = blockIdx.x;
+    const float2* f = S + (size_t)b * R;
+    double sr = 0.0, si = 0.0;
+    for (int i = threadIdx.x; i < R; i += 256) {
+        const float2 v = f[i];
+        sr += v.x;
+        si += v.y;
+    }
+    __shared__ double red[2][8];
+    __shared__ double up[2];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(0xffffffffu, sr, o);
+        si += __shfl_xor_sync(0xffffffffu, si, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = sr;
+        red[1][threadIdx.x >> 5] = si;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tr = 0.0, ti = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            tr += red[0][w];
+            ti += red[1][w];
+        }
+        const float2 t = target[b];
+        double value, ur, ui;
+        if (mode == 0) {
+            const double dr = tr - t.x, di = ti - t.y;
+            value = dr * dr + di * di;
+            ur = 2.0 * dr;
+            ui = 2.0 * di;
+        } else {
+            const double gt = t.x, p = tr * tr + ti * ti;
+            if (p <= 1e-20) {
+                value = fabs(-200.0 - gt);
+                ur = ui = 0.0;
+            } else {
+                const double dbm = 10.0 * log10(p);
+                const double sgn = dbm > gt ? 1.0 : (dbm < gt ? -1.0 : 0.0);
+                const double sc = sgn * (20.0 / log(10.0)) / p;
+                value = fabs(dbm - gt);
+                ur = sc * tr;
+                ui = sc * ti;
+            }
+        }
+        report[4 * b + 0] = value;
+        report[4 * b + 1] = value;
+        report[4 * b + 2] = 0.0;
+        report[4 * b + 3] = 0.0;
+        if (total_out) total_out[b] = make_float2((float)tr, (float)ti);
+        up[0] = ur;
+        up[1] = ui;
+    }
+    __syncthreads();
+    if (lam) {
+        const float2 u = make_float2((float)up[0], (float)up[1]);
+        for (int i = threadIdx.x; i < R; i += 256) lam[(size_t)b * R + i] = u;
+    }
+}
+
 bool g_win_ready = false;
 
 int ensure_window() {
@@ -330,6 +403,16 @@ int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const flo
                                                   (float)w_ssim, (float)w_fourier, grad, (float2*)lam);
     k_loss_final<<<rfs_ceil_div((long long)n_frames * 32, 128), 128, 0, st>>>(part, nblk, n_frames, (double)R, w1,
                                                                                 w_ssim, w_fourier, report);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
+int rfs_scalar_loss(int n_frames, int n_rays, int mode, const void* S, const void* target, double* report,
+                    void* total, void* lam, void* stream) {
+    if (n_frames <= 0 || n_rays <= 0) return RFS_OK;
+    if (mode != 0 && mode != 1) return RFS_ERR_SHAPE;
+    k_scalar_loss<<<n_frames, 256, 0, (cudaStream_t)stream>>>((const float2*)S, n_rays, mode, (const float2*)target,
+                                                              report, (float2*)total, (float2*)lam);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -22,7 +22,7 @@ from . import _native
 from .errors import ShapeError
 
 __all__ = ["LossReport", "spectrum_loss_frames", "spectrum_loss", "l1_loss", "ssim_loss", "fourier_loss",
-           "SpectrumLoss"]
+           "SpectrumLoss", "scalar_loss_frames", "scalar_loss"]
 
 
 @dataclass
@@ -138,3 +138,45 @@ class SpectrumLoss(torch.autograd.Function):
     def backward(ctx, grad_out):
         (lam,) = ctx.saved_tensors
         return lam * grad_out.to(torch.float32).reshape(-1, 1, 1), None, None, None
+
+
+_SCALAR_MODES = {"complex": 0, "real_power": 1}
+
+
+def scalar_loss_frames(S: torch.Tensor, target: torch.Tensor, mode: str, want_lam: bool = True):
+    """Single-antenna loss of B frames on the device (render_scalar + scalar_loss,
+    render.py:301-307, loss.py:158-180; mode 'complex' = CSI, 'real_power' = RSSI dBm).
+
+    S complex64 [B, n_az, n_el]; target complex64 [B] ('complex') or float [B]
+    of dBm ('real_power').  Returns (report float64 [B, 4] = (value, value, 0,
+    0), total complex64 [B], lam complex64 [B, n_az, n_el] or None) -- lam is
+    the per-frame constant upstream of the coherent sum (train.py:288).
+    """
+    if mode not in _SCALAR_MODES:
+        raise ValueError(f"unknown scalar loss mode {mode!r}")
+    b, n_az, n_el = (int(x) for x in S.shape)
+    dev = S.device
+    S = S.to(torch.complex64).contiguous()
+    t = torch.as_tensor(target, device=dev).reshape(-1)
+    if t.numel() != b:
+        raise ShapeError("one scalar target per frame")
+    t = t.to(torch.complex64).contiguous()
+    report = torch.empty((b, 4), dtype=torch.float64, device=dev)
+    total = torch.empty(b, dtype=torch.complex64, device=dev)
+    lam = torch.empty((b, n_az, n_el), dtype=torch.complex64, device=dev) if want_lam else None
+    _native.call("rfs_scalar_loss", b, n_az * n_el, _SCALAR_MODES[mode], _ptr(S), _ptr(t), _ptr(report), _ptr(total),
+                 _ptr(lam), torch.cuda.current_stream(dev).cuda_stream)
+    return report, total, lam
+
+
+def scalar_loss(pred: complex, gt, mode: str):
+    """loss.scalar_loss (loss.py:158-180) for one complex prediction, on the device."""
+    if mode not in _SCALAR_MODES:
+        raise ValueError(f"unknown scalar loss mode {mode!r}")
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+    if dev is None:
+        _native.load()  # raises NativeLibraryError: no CPU fallback
+    S = torch.tensor([[[complex(pred)]]], dtype=torch.complex64, device=dev)
+    tgt = complex(gt) if mode == "complex" else complex(float(gt), 0.0)
+    rep, total, lam = scalar_loss_frames(S, torch.tensor([tgt], dtype=torch.complex64), mode)
+    return float(rep[0, 0]), complex(lam[0, 0, 0].item())

@@ -207,7 +207,7 @@ class TraceRow:
 
 
 def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tensor, config: TrainConfig,
-               batch: int = 1, seed: int = 0, timings: list | None = None):
+               batch: int = 1, seed: int = 0, timings: list | None = None, mode: str = "spectrum"):
     """Batched counterpart of train.train_loop (train.py:284-361) on the device.
 
     Each iteration draws `batch` samples (TX position + measured power frame)
@@ -217,13 +217,18 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
     training.  The scene stays in HBM throughout; the loss trace is read back
     once at the end.  `timings` (optional list) receives (iteration,
     milliseconds, n_gaussians, event) per iteration from CUDA events.
+    `mode` is the dataset mode (train.py:266-291): "spectrum" (frames = power
+    frames [S, n_az, n_el]), "rssi" (frames = dBm [S]) or "csi" (frames =
+    complex targets [S], one subcarrier).
     Returns (trace, densify_reports, prune_reports).
     """
     from . import loss as _loss
 
     config.validate()
     dev = scene.means.device
-    if tuple(frames.shape[1:]) != (scene.n_az, scene.n_el):
+    if mode not in ("spectrum", "rssi", "csi"):
+        raise ConfigError(f"unknown sample mode {mode!r}")
+    if mode == "spectrum" and tuple(frames.shape[1:]) != (scene.n_az, scene.n_el):
         raise ConfigError(f"dataset grid {tuple(frames.shape[1:])} does not match scene grid "
                           f"{(scene.n_az, scene.n_el)}")
     rng = np.random.default_rng(seed)
@@ -238,7 +243,10 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
         event = ""
         if scene.n > 0:
             def loss_up(S):
-                rep, lam, _ = _loss.spectrum_loss_frames(S, gt, config.w_ssim, config.w_fourier)
+                if mode == "spectrum":
+                    rep, lam, _ = _loss.spectrum_loss_frames(S, gt, config.w_ssim, config.w_fourier)
+                else:
+                    rep, _, lam = _loss.scalar_loss_frames(S, gt, "real_power" if mode == "rssi" else "complex")
                 return rep, lam
             geo = raster.build_geometry(scene, psi_tx=tx, forward=True, after_forward=loss_up)
             rep, lam = geo.after_result

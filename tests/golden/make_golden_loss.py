@@ -49,6 +49,19 @@ def main():
         out[name + "_w"] = np.array([ws, wf])
         out[name + "_vals"] = np.array([rep.total, rep.l1, rep.ssim, rep.fourier])
         out[name + "_grad"] = rep.grad_frame
+    # scalar modes (loss.py:158-180): (pred, gt, mode) -> (value, upstream)
+    sc = [(0.3 + 0.4j, 0.1 - 0.2j, "complex"), (-1.5 + 2.0j, -1.0 + 2.5j, "complex"),
+          (0.02 + 0.01j, -30.0, "real_power"), (3.0 - 4.0j, 20.0, "real_power"), (1e-12 + 0j, -50.0, "real_power")]
+    out["scalar_pred"] = np.array([complex(np.complex64(c[0])) for c in sc])
+    out["scalar_gt"] = np.array([complex(np.complex64(c[1])) for c in sc])
+    out["scalar_mode"] = np.array([c[2] for c in sc])
+    vals, ups = [], []
+    for p, g, m in zip(out["scalar_pred"], out["scalar_gt"], out["scalar_mode"]):
+        v, u = loss.scalar_loss(complex(p), complex(g) if m == "complex" else float(g.real), str(m))
+        vals.append(v)
+        ups.append(u)
+    out["scalar_value"] = np.array(vals)
+    out["scalar_up"] = np.array(ups, dtype=np.complex128)
     np.savez_compressed(os.path.join(HERE, "loss_frames.npz"), **out)
     print("wrote loss_frames.npz")
 

@@ -120,3 +120,24 @@ def test_gpu_train_step_matches_oracle():
     for k in GRAD_KEYS:
         a = grads[k].cpu().numpy()
         assert class_rel(a, ref[k]) <= 1e-3, k
+
+
+@pytest.mark.gpu
+def test_gpu_scalar_loss_matches_reference():
+    import torch
+
+    from paper_2502_01826_b200 import loss
+
+    z = load("loss_frames.npz")
+    for p, g, m, v, u in zip(z["scalar_pred"], z["scalar_gt"], z["scalar_mode"], z["scalar_value"], z["scalar_up"]):
+        gt = complex(g) if str(m) == "complex" else float(np.real(g))
+        val, up = loss.scalar_loss(complex(p), gt, str(m))
+        assert abs(val - v) <= 1e-5 * max(abs(v), 1e-6), (m, val, v)
+        assert abs(up - u) <= 1e-4 * max(abs(u), 1e-9), (m, up, u)
+    # batched frames: the total is the coherent frame sum, lam is constant per frame
+    S = torch.randn(3, 20, 10, dtype=torch.complex64, device="cuda")
+    rep, total, lam = loss.scalar_loss_frames(S, torch.tensor([0.1 + 0.2j, -1.0, 2.0j]), "complex")
+    np.testing.assert_allclose(total.cpu().numpy(), S.sum(dim=(1, 2)).cpu().numpy(), rtol=1e-5, atol=1e-5)
+    ref_up = 2.0 * (S.sum(dim=(1, 2)) - torch.tensor([0.1 + 0.2j, -1.0, 2.0j], device="cuda"))
+    np.testing.assert_allclose(lam[:, 7, 3].cpu().numpy(), ref_up.cpu().numpy(), rtol=1e-4, atol=1e-5)
+    assert bool((lam == lam[:, :1, :1]).all())
