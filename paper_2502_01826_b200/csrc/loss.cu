@@ -25,9 +25,12 @@
 namespace {
 
 constexpr int LW = 11, LH = 5;              // window, half width
-constexpr int TU = 16, TV = 32;             // output tile (u rows, v columns)
+constexpr int TU = 32, TV = 32;             // output tile (u rows, v columns)
 constexpr int HU = TU + 2 * LH, HV = TV + 2 * LH;
 constexpr int LT = 256;                     // threads per tile block
+constexpr int SEG = 4;                      // outputs per thread per pass (register sliding window)
+constexpr int HVP = HV + 1, TVP = TV + 1;   // padded row pitches (conflict-free column walks)
+static_assert(LT == TV * TU / SEG, "one vertical-pass item per thread");
 
 __constant__ float c_winf[LW];
 
@@ -84,10 +87,9 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 struct FwdSmem {
-    float x[HU][HV], y[HU][HV];  // centred: x - cx, y - cy (padding cells hold -cx, -cy)
-    float h[5][HU][TV];          // v-blurred x, y, xx, yy, xy of the centred frames
+    float x[HU][HVP], y[HU][HVP];  // raw frames (0 in the padding)
+    float h[5][HU][TVP];           // v-blurred x, y, xx, yy, xy of the centred frames
     double red[LT / 32];
-    float c[2];
 };
 
 // The five window statistics in fp32 on frames centred by a per-tile constant
@@ -95,7 +97,9 @@ struct FwdSmem {
 // centred frame x - c is -c in the padding, so blur(x - c) = mu_x - c and the
 // (co)variances blur((x-c)^2) - blur(x-c)^2 equal vx - mu_x^2 exactly -- the
 // centring removes the E[x^2] - E[x]^2 cancellation that made fp64 necessary.
-// s, its partials and the sums are then evaluated in fp64 per cell.
+// s, its partials and the sums are then evaluated in fp64 per cell.  Both
+// separable passes slide an 11-value window through registers, SEG outputs
+// per thread (one shared-memory load per input instead of eleven).
 // grid (v tiles, u tiles, frames)
 __global__ void __launch_bounds__(LT) k_ssim_fwd(const float2* __restrict__ S, const float* __restrict__ pred,
                                                  const float* __restrict__ gt,
@@ -113,69 +117,111 @@ __global__ void __launch_bounds__(LT) k_ssim_fwd(const float2* __restrict__ S, c
     }
     const double D = fmax((double)hi - (double)lo, 1e-6);
     const double c1 = (0.01 * D) * (0.01 * D), c2 = (0.03 * D) * (0.03 * D);
-    if (threadIdx.x == 0) {  // centre: the tile's first in-range cell
-        const size_t r0 = fb + (size_t)u0 * n_el + v0;
-        M.c[0] = (float)power(S, pred, r0);
-        M.c[1] = gt[r0];
-    }
-    __syncthreads();
-    const float cx = M.c[0], cy = M.c[1];
-    for (int i = threadIdx.x; i < HU * HV; i += LT) {
-        const int hu = i / HV, hv = i % HV, u = u0 - LH + hu, v = v0 - LH + hv;
-        float xv = 0.f, yv = 0.f;
-        if (u >= 0 && u < n_az && v >= 0 && v < n_el) {
-            const size_t r = fb + (size_t)u * n_el + v;
-            xv = (float)power(S, pred, r);
-            yv = gt[r];
-        }
-        M.x[hu][hv] = xv - cx;
-        M.y[hu][hv] = yv - cy;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < HU * TV; i += LT) {  // correlate along v (axis 1)
-        const int hu = i / TV, ov = i % TV;
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+    {   // halo load: row-major, every load of the thread in flight before the stores
+        constexpr int RS = LT / 64, NR = (HU + RS - 1) / RS;
+        const int hv = threadIdx.x & 63, v = v0 - LH + hv;
+        const bool vok = hv < HV && v >= 0 && v < n_el;
+        float xv[NR], yv[NR];
 #pragma unroll
-        for (int t = 0; t < LW; ++t) {
-            const float w = c_winf[t], xv = M.x[hu][ov + t], yv = M.y[hu][ov + t];
-            a0 = fmaf(w, xv, a0);
-            a1 = fmaf(w, yv, a1);
-            a2 = fmaf(w, xv * xv, a2);
-            a3 = fmaf(w, yv * yv, a3);
-            a4 = fmaf(w, xv * yv, a4);
+        for (int k = 0; k < NR; ++k) {
+            const int hu = (threadIdx.x >> 6) + k * RS, u = u0 - LH + hu;
+            xv[k] = yv[k] = 0.f;
+            if (vok && hu < HU && u >= 0 && u < n_az) {
+                const size_t r = fb + (size_t)u * n_el + v;
+                xv[k] = (float)power(S, pred, r);
+                yv[k] = gt[r];
+            }
         }
-        M.h[0][hu][ov] = a0; M.h[1][hu][ov] = a1; M.h[2][hu][ov] = a2; M.h[3][hu][ov] = a3; M.h[4][hu][ov] = a4;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const int hu = (threadIdx.x >> 6) + k * RS;
+            if (hv < HV && hu < HU) {
+                M.x[hu][hv] = xv[k];
+                M.y[hu][hv] = yv[k];
+            }
+        }
     }
     __syncthreads();
+    const float cx = M.x[LH][LH], cy = M.y[LH][LH];  // centre: the tile's first cell
+    // correlate along v (axis 1): item = (segment, row), rows fastest -> conflict-free
+    for (int it = threadIdx.x; it < (TV / SEG) * HU; it += LT) {
+        const int sg = it / HU, hu = it - sg * HU, o0 = sg * SEG;
+        float wx[SEG + LW - 1], wy[SEG + LW - 1];
+#pragma unroll
+        for (int j = 0; j < SEG + LW - 1; ++j) {
+            wx[j] = M.x[hu][o0 + j] - cx;
+            wy[j] = M.y[hu][o0 + j] - cy;
+        }
+#pragma unroll
+        for (int o = 0; o < SEG; ++o) {
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+#pragma unroll
+            for (int t = 0; t < LW; ++t) {
+                const float w = c_winf[t], xv = wx[o + t], yv = wy[o + t];
+                a0 = fmaf(w, xv, a0);
+                a1 = fmaf(w, yv, a1);
+                a2 = fmaf(w, xv * xv, a2);
+                a3 = fmaf(w, yv * yv, a3);
+                a4 = fmaf(w, xv * yv, a4);
+            }
+            M.h[0][hu][o0 + o] = a0; M.h[1][hu][o0 + o] = a1; M.h[2][hu][o0 + o] = a2;
+            M.h[3][hu][o0 + o] = a3; M.h[4][hu][o0 + o] = a4;
+        }
+    }
+    __syncthreads();
+    // correlate along u (axis 0): item = (segment of SEG rows, column), columns fastest
     double s_sum = 0.0, l1 = 0.0, sq = 0.0;
-    for (int i = threadIdx.x; i < TU * TV; i += LT) {  // correlate along u (axis 0)
-        const int ou = i / TV, ov = i % TV, u = u0 + ou, v = v0 + ov;
-        if (u >= n_az || v >= n_el) continue;
-        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    {
+        const int ov = threadIdx.x % TV, o0 = (threadIdx.x / TV) * SEG;  // LT = TV * TU / SEG
+        const int v = v0 + ov;
+        double dx[SEG];  // exact d = x - y of this thread's cells, loaded ahead of the blur
 #pragma unroll
-        for (int t = 0; t < LW; ++t) {
-            const float w = c_winf[t];
-#pragma unroll
-            for (int k = 0; k < 5; ++k) m[k] = fmaf(w, M.h[k][ou + t][ov], m[k]);
+        for (int o = 0; o < SEG; ++o) {
+            const int u = u0 + o0 + o;
+            dx[o] = 0.0;
+            if (u < n_az && v < n_el) {
+                const size_t r = fb + (size_t)u * n_el + v;
+                dx[o] = power(S, pred, r) - (double)gt[r];
+            }
         }
-        const double ex = m[0], ey = m[1];  // centred means
-        const double mx = (double)cx + ex, my = (double)cy + ey;
-        const double varx = (double)m[2] - ex * ex, vary = (double)m[3] - ey * ey, cov = (double)m[4] - ex * ey;
-        const double A1 = 2.0 * mx * my + c1, A2 = 2.0 * cov + c2;
-        const double B1 = mx * mx + my * my + c1, B2 = varx + vary + c2;
-        const double inv = 1.0 / (B1 * B2);  // one division: 1/B1 = B2 inv, 1/B2 = B1 inv
-        const double s = A1 * A2 * inv;
-        s_sum += s;
-        const double ds_dmu = 2.0 * my * (A2 - A1) * inv - 2.0 * mx * s * ((B2 - B1) * inv);
-        const double ds_dv = -s * (B1 * inv);
-        const double ds_dw = 2.0 * A1 * inv;
-        const size_t r = fb + (size_t)u * n_el + v;
-        maps[r] = (float)ds_dmu;
-        maps[R * gridDim.z + r] = (float)ds_dv;
-        maps[2 * R * gridDim.z + r] = (float)ds_dw;
-        const double d = power(S, pred, r) - (double)gt[r];  // exact inputs, not the centred copies
-        l1 += fabs(d);
-        sq += d * d;
+        float m[5][SEG];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            float wv[SEG + LW - 1];
+#pragma unroll
+            for (int j = 0; j < SEG + LW - 1; ++j) wv[j] = M.h[k][o0 + j][ov];
+#pragma unroll
+            for (int o = 0; o < SEG; ++o) {
+                float a = 0.f;
+#pragma unroll
+                for (int t = 0; t < LW; ++t) a = fmaf(c_winf[t], wv[o + t], a);
+                m[k][o] = a;
+            }
+        }
+#pragma unroll
+        for (int o = 0; o < SEG; ++o) {
+            const int u = u0 + o0 + o;
+            if (u >= n_az || v >= n_el) continue;
+            const double ex = m[0][o], ey = m[1][o];  // centred means
+            const double mx = (double)cx + ex, my = (double)cy + ey;
+            const double varx = (double)m[2][o] - ex * ex, vary = (double)m[3][o] - ey * ey;
+            const double cov = (double)m[4][o] - ex * ey;
+            const double A1 = 2.0 * mx * my + c1, A2 = 2.0 * cov + c2;
+            const double B1 = mx * mx + my * my + c1, B2 = varx + vary + c2;
+            const double inv = 1.0 / (B1 * B2);  // one division: 1/B1 = B2 inv, 1/B2 = B1 inv
+            const double sv = A1 * A2 * inv;
+            s_sum += sv;
+            const double ds_dmu = 2.0 * my * (A2 - A1) * inv - 2.0 * mx * sv * ((B2 - B1) * inv);
+            const double ds_dv = -sv * (B1 * inv);
+            const double ds_dw = 2.0 * A1 * inv;
+            const size_t r = fb + (size_t)u * n_el + v;
+            maps[r] = (float)ds_dmu;
+            maps[R * gridDim.z + r] = (float)ds_dv;
+            maps[2 * R * gridDim.z + r] = (float)ds_dw;
+            const double d = dx[o];
+            l1 += fabs(d);
+            sq += d * d;
+        }
     }
     const int blk = blockIdx.y * gridDim.x + blockIdx.x, nblk = gridDim.x * gridDim.y;
     double* pb = part + ((size_t)b * nblk + blk) * 3;
@@ -190,8 +236,8 @@ __global__ void __launch_bounds__(LT) k_ssim_fwd(const float2* __restrict__ S, c
 }
 
 struct BwdSmem {
-    float m[3][HU][HV];
-    float h[3][HU][TV];
+    float m[3][HU][HVP];
+    float h[3][HU][TVP];
 };
 
 __global__ void __launch_bounds__(LT) k_ssim_bwd(const float2* __restrict__ S, const float* __restrict__ pred,
@@ -202,49 +248,91 @@ __global__ void __launch_bounds__(LT) k_ssim_bwd(const float2* __restrict__ S, c
     BwdSmem& M = *reinterpret_cast<BwdSmem*>(smem_raw);
     const int b = blockIdx.z, u0 = blockIdx.y * TU, v0 = blockIdx.x * TV;
     const size_t R = (size_t)n_az * n_el, fb = (size_t)b * R, plane = R * gridDim.z;
-    for (int i = threadIdx.x; i < HU * HV; i += LT) {
-        const int hu = i / HV, hv = i % HV, u = u0 - LH + hu, v = v0 - LH + hv;
-        const bool in = u >= 0 && u < n_az && v >= 0 && v < n_el;
-        const size_t r = fb + (size_t)u * n_el + v;
+    {   // halo load: row-major, every load of the thread in flight before the stores
+        constexpr int RS = LT / 64, NR = (HU + RS - 1) / RS;
+        const int hv = threadIdx.x & 63, v = v0 - LH + hv;
+        const bool vok = hv < HV && v >= 0 && v < n_el;
+        float mv[3][NR];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) M.m[k][hu][hv] = in ? maps[k * plane + r] : 0.f;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < HU * TV; i += LT) {  // adjoint of the zero-padded correlation = itself
-        const int hu = i / TV, ov = i % TV;
-        float a[3] = {0.f, 0.f, 0.f};
+        for (int k = 0; k < NR; ++k) {
+            const int hu = (threadIdx.x >> 6) + k * RS, u = u0 - LH + hu;
+            const bool in = vok && hu < HU && u >= 0 && u < n_az;
+            const size_t r = fb + (size_t)u * n_el + v;
 #pragma unroll
-        for (int t = 0; t < LW; ++t) {
-            const float w = c_winf[t];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) a[k] = fmaf(w, M.m[k][hu][ov + t], a[k]);
+            for (int q = 0; q < 3; ++q) mv[q][k] = in ? maps[q * plane + r] : 0.f;
         }
 #pragma unroll
-        for (int k = 0; k < 3; ++k) M.h[k][hu][ov] = a[k];
+        for (int k = 0; k < NR; ++k) {
+            const int hu = (threadIdx.x >> 6) + k * RS;
+            if (hv < HV && hu < HU) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) M.m[q][hu][hv] = mv[q][k];
+            }
+        }
+    }
+    __syncthreads();
+    // adjoint of the zero-padded correlation = the same correlation
+    for (int it = threadIdx.x; it < (TV / SEG) * HU; it += LT) {
+        const int sg = it / HU, hu = it - sg * HU, o0 = sg * SEG;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float wv[SEG + LW - 1];
+#pragma unroll
+            for (int j = 0; j < SEG + LW - 1; ++j) wv[j] = M.m[k][hu][o0 + j];
+#pragma unroll
+            for (int o = 0; o < SEG; ++o) {
+                float a = 0.f;
+#pragma unroll
+                for (int t = 0; t < LW; ++t) a = fmaf(c_winf[t], wv[o + t], a);
+                M.h[k][hu][o0 + o] = a;
+            }
+        }
     }
     __syncthreads();
     const double inv_n = 1.0 / (double)R;
-    for (int i = threadIdx.x; i < TU * TV; i += LT) {
-        const int ou = i / TV, ov = i % TV, u = u0 + ou, v = v0 + ov;
+    const int ov = threadIdx.x % TV, o0 = (threadIdx.x / TV) * SEG;
+    const int v = v0 + ov;
+    float2 sv[SEG];  // this thread's cells, loaded ahead of the blur
+    float xp[SEG], yv[SEG];
+#pragma unroll
+    for (int o = 0; o < SEG; ++o) {
+        const int u = u0 + o0 + o;
+        sv[o] = make_float2(0.f, 0.f);
+        xp[o] = yv[o] = 0.f;
+        if (u < n_az && v < n_el) {
+            const size_t r = fb + (size_t)u * n_el + v;
+            if (S) sv[o] = S[r];
+            if (pred) xp[o] = pred[r];
+            yv[o] = gt[r];
+        }
+    }
+    float a[3][SEG];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float wv[SEG + LW - 1];
+#pragma unroll
+        for (int j = 0; j < SEG + LW - 1; ++j) wv[j] = M.h[k][o0 + j][ov];
+#pragma unroll
+        for (int o = 0; o < SEG; ++o) {
+            float acc = 0.f;
+#pragma unroll
+            for (int t = 0; t < LW; ++t) acc = fmaf(c_winf[t], wv[o + t], acc);
+            a[k][o] = acc;
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < SEG; ++o) {
+        const int u = u0 + o0 + o;
         if (u >= n_az || v >= n_el) continue;
-        float a[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-        for (int t = 0; t < LW; ++t) {
-            const float w = c_winf[t];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) a[k] = fmaf(w, M.h[k][ou + t][ov], a[k]);
-        }
         const size_t r = fb + (size_t)u * n_el + v;
-        const double x = power(S, pred, r), y = gt[r], d = x - y;
-        const double g1 = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_n;          // loss.py:65-72
-        const double g2 = -((double)a[0] + (double)a[1] * 2.0 * x + (double)a[2] * y) * inv_n;                // loss.py:124-128
-        const double g3 = 2.0 * d;                                                    // loss.py:146
-        const double gx = (double)w1 * g1 + (double)ws * g2 + (double)wf * g3;        // loss.py:149-155
+        const double x = pred ? (double)xp[o] : (double)sv[o].x * sv[o].x + (double)sv[o].y * sv[o].y;
+        const double y = yv[o], d = x - y;
+        const double g1 = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_n;                   // loss.py:65-72
+        const double g2 = -((double)a[0][o] + (double)a[1][o] * 2.0 * x + (double)a[2][o] * y) * inv_n;  // loss.py:124-128
+        const double g3 = 2.0 * d;                                                              // loss.py:146
+        const double gx = (double)w1 * g1 + (double)ws * g2 + (double)wf * g3;                  // loss.py:149-155
         if (grad) grad[r] = (float)gx;
-        if (lam) {
-            const float2 s = S[r];
-            lam[r] = make_float2((float)(2.0 * gx * s.x), (float)(2.0 * gx * s.y));   // grad.py:119
-        }
+        if (lam) lam[r] = make_float2((float)(2.0 * gx * sv[o].x), (float)(2.0 * gx * sv[o].y));  // grad.py:119
     }
 }
 
