@@ -332,9 +332,15 @@ __device__ __forceinline__ Aff compose(const Aff& f, const Aff& h) {  // f(h(x))
     return o;
 }
 
+// Precision: rho in fp64 from the geometry record (the reference's value);
+// for rays with <= 32 live hits (all of them at 100k, max 28) T is rebuilt in
+// fp64 as a warp prefix product of rho instead of the slab's fp32 copy; and
+// d(phase) -- a sum of strongly cancelling terms for Gaussians crossed by
+// many rays -- is stored as a float pair (hi, lo) for the fp64 sums of K9a.
 __global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
                                                   int hcap, int R, const float4* __restrict__ rho32,
-                                                  const float2* __restrict__ C, float4* __restrict__ gs) {
+                                                  const RfsGeom* __restrict__ geom, const float2* __restrict__ C,
+                                                  float4* __restrict__ gs) {
     const int lane = threadIdx.x & 31;
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= R) return;
@@ -357,9 +363,26 @@ __global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ sla
             hk.t_re = hk.t_im = 0.f;
         }
         const float4 rq = ok ? __ldg(&rho32[hk.g]) : make_float4(1.f, 0.f, 1.f, 0.f);
+        const double rr = ok ? __ldg(&geom[hk.g].rho_re) : 1.0, ri = ok ? __ldg(&geom[hk.g].rho_im) : 0.0;
+        // T_k in fp64: exclusive prefix product of rho over the ray's hits (single chunk)
+        double tr = hk.t_re, ti = hk.t_im;
+        if (cnt <= 32) {
+            double pr = rr, pi = ri;  // inclusive scan
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double qr = __shfl_up_sync(0xffffffffu, pr, o), qi = __shfl_up_sync(0xffffffffu, pi, o);
+                if (lane >= o) {
+                    const double nr = qr * pr - qi * pi;
+                    pi = qr * pi + qi * pr;
+                    pr = nr;
+                }
+            }
+            const double er = __shfl_up_sync(0xffffffffu, pr, 1), ei = __shfl_up_sync(0xffffffffu, pi, 1);
+            tr = lane == 0 ? 1.0 : er;
+            ti = lane == 0 ? 0.0 : ei;
+        }
         // f_k(A) = w_k C_k + rho_k A; lane k holds F_k = f_{k+1} (identity past the end)
         const double wc_r = (double)hk.w * (double)ck.x, wc_i = (double)hk.w * (double)ck.y;
-        const double rr = rq.x, ri = rq.y;
         Aff F;
         {
             const double nr = __shfl_down_sync(0xffffffffu, rr, 1);
@@ -388,12 +411,12 @@ __global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ sla
         const double Ar = F.ar * Anr - F.ai * Ani + F.cr;
         const double Ai = F.ar * Ani + F.ai * Anr + F.ci;
         if (ok) {
-            const double tr = hk.t_re, ti = hk.t_im;
             const double gw = tr * (double)ck.x - ti * (double)ck.y;     // Re(T C)          (_kernels.py:387-388)
             const double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
             const double dmag = tar * rq.z - tai * rq.w;                  // Re(T e^{jphi} A) (_kernels.py:382-383)
-            const double dph = -(tar * rq.y + tai * rq.x);                // -Im(T rho A)     (_kernels.py:384-385)
-            gs[pos] = make_float4((float)gw, (float)dmag, (float)dph, 0.f);
+            const double dph = -(tar * ri + tai * rr);                    // -Im(T rho A)     (_kernels.py:384-385)
+            const float dph_hi = (float)dph;
+            gs[pos] = make_float4((float)gw, (float)dmag, dph_hi, (float)(dph - (double)dph_hi));
         }
         Anr = __shfl_sync(0xffffffffu, Ar, 0);
         Ani = __shfl_sync(0xffffffffu, Ai, 0);
@@ -461,11 +484,12 @@ int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const u
     return RFS_OK;
 }
 
-int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32, const void* C,
-                 void* gs, void* stream) {
+int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32, const void* geom,
+                 const void* C, void* gs, void* stream) {
     if (n_rays <= 0) return RFS_OK;
     k_bwd_rays<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-        (const RfsHit*)slab, counts, hcap, n_rays, (const float4*)rho32, (const float2*)C, (float4*)gs);
+        (const RfsHit*)slab, counts, hcap, n_rays, (const float4*)rho32, (const RfsGeom*)geom, (const float2*)C,
+        (float4*)gs);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) k_geom_seg(
                 }
         }
         v[12] = gsv.y;
-        v[13] = gsv.z;
+        v[13] = (double)gsv.z + (double)gsv.w;  // d(phase) as a float pair (K8r)
     }
     // Segmented sums by Gaussian (segments are contiguous runs of lanes): the
     // lanes' values go to shared memory and task (segment k, value i) is summed

@@ -512,8 +512,8 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         for t in (txc, P, dm_dir, out["d_coeffs"]):
             t.record_stream(side)
     _mark(marks, "backward_tx")
-    _native.call("rfs_bwd_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, _ptr(geo.rho32), _ptr(C),
-                 _ptr(gs), st)
+    _native.call("rfs_bwd_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, _ptr(geo.rho32), _ptr(geo.geom),
+                 _ptr(C), _ptr(gs), st)
     _mark(marks, "backward_rays")
     rx = (_native.C.c_double * 3)(*geo.rx)
     npart = int(lib.rfs_geom_part_elems(h))
