@@ -64,25 +64,28 @@ int rfs_exclusive_scan_u32(const uint32_t* in, int n, uint32_t* out, uint32_t* t
 
 /* K2b: fill (compact key, Gaussian id) pairs in the reference expansion
  * order (_kernels.py:545-558).  Compact key = tile << 31 | float32 depth
- * bits; rfs_expand_keys restores the reference key tile << 32 | bits. */
-int rfs_bin_fill(int n, const void* rects, const uint32_t* depth_code, const uint32_t* offsets, int n_az,
+ * bits; rfs_expand_keys restores the reference key tile << 32 | bits.
+ * Only positions < cap are written (compare M with cap afterwards). */
+int rfs_bin_fill(int n, const void* rects, const uint32_t* depth_code, const uint32_t* offsets, int n_az, int cap,
                  uint64_t* ckeys, uint32_t* vals, void* stream);
 int rfs_expand_keys(const uint64_t* ckeys, int m, uint64_t* keys, void* stream);
 
 /* K3: stable LSD radix sort of (u64 key, u32 value) on bits [0, end_bit).
  * Replaces np.argsort(keys, kind="stable") (splat.py:337).  Hand-written
  * onesweep passes; the _cub variant calls cub::DeviceRadixSort::SortPairs for
- * comparison.  *result_in_alt (host) = 1 if the sorted data is in *_alt. */
+ * comparison.  *result_in_alt (host) = 1 if the sorted data is in *_alt.
+ * m_dev (nullable, hand-written sort only): device-side count; m is then the
+ * capacity and min(*m_dev, m) keys are sorted without a host read. */
 size_t rfs_sort_temp_bytes(int m, int end_bit);
 int rfs_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int m, int end_bit,
-                       void* temp, size_t temp_bytes, int* result_in_alt, void* stream);
+                       void* temp, size_t temp_bytes, int* result_in_alt, const uint32_t* m_dev, void* stream);
 size_t rfs_sort_cub_temp_bytes(int m, int end_bit);
 int rfs_sort_pairs_u64_cub(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int m, int end_bit,
                            void* temp, size_t temp_bytes, int* result_in_alt, void* stream);
 
 /* K4: per-tile [start, end) ranges = searchsorted left/right of each tile id
  * (splat.py:340-343); ranges is int32[n_tiles*2]. */
-int rfs_tile_ranges(const uint64_t* ckeys, int m, int n_tiles, int* ranges, void* stream);
+int rfs_tile_ranges(const uint64_t* ckeys, int m, const uint32_t* m_dev, int n_tiles, int* ranges, void* stream);
 
 /* K4b: per-incidence emission bound for the exact streaming re-sort:
  * lb[i] = min_{j >= i, same tile} (depth_j - r3_j). */

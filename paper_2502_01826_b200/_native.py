@@ -27,13 +27,13 @@ _SIGS = {
     "rfs_project": (i32, [i32, vp, vp, vp, vp, vp, vp, f64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rfs_scan_temp_elems": (sz, [i32]),
     "rfs_exclusive_scan_u32": (i32, [vp, i32, vp, vp, vp, vp]),
-    "rfs_bin_fill": (i32, [i32, vp, vp, vp, i32, vp, vp, vp]),
+    "rfs_bin_fill": (i32, [i32, vp, vp, vp, i32, i32, vp, vp, vp]),
     "rfs_expand_keys": (i32, [vp, i32, vp, vp]),
     "rfs_sort_temp_bytes": (sz, [i32, i32]),
-    "rfs_sort_pairs_u64": (i32, [vp, vp, vp, vp, i32, i32, vp, sz, C.POINTER(i32), vp]),
+    "rfs_sort_pairs_u64": (i32, [vp, vp, vp, vp, i32, i32, vp, sz, C.POINTER(i32), vp, vp]),
     "rfs_sort_cub_temp_bytes": (sz, [i32, i32]),
     "rfs_sort_pairs_u64_cub": (i32, [vp, vp, vp, vp, i32, i32, vp, sz, C.POINTER(i32), vp]),
-    "rfs_tile_ranges": (i32, [vp, i32, i32, vp, vp]),
+    "rfs_tile_ranges": (i32, [vp, i32, vp, i32, vp, vp]),
     "rfs_lower_bounds": (i32, [vp, i32, vp, vp, vp, vp]),
     "rfs_ray_dirs": (i32, [i32, i32, vp, vp]),
     "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp]),

@@ -336,8 +336,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const uint32_t* __r
 // (_kernels.py:545-558): per splat, tv ascending, s1 tiles then s2 tiles.
 // Compact key = tile << 31 | depth_code (the code's sign bit is always 0),
 // so the radix sort needs 31 + ceil(log2 tiles) bits.
+// Writes only positions < cap (the caller's capacity); the caller compares the
+// scan total M with cap after the fact and redoes the binning if it overflowed.
 __global__ void __launch_bounds__(256) k_fill(int n, const Rect* __restrict__ rects, const uint32_t* __restrict__ code,
-                                              const uint32_t* __restrict__ offs, int tiles_u,
+                                              const uint32_t* __restrict__ offs, int tiles_u, uint32_t cap,
                                               uint64_t* __restrict__ ckeys, uint32_t* __restrict__ vals) {
     int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
@@ -348,11 +350,13 @@ __global__ void __launch_bounds__(256) k_fill(int n, const Rect* __restrict__ re
     for (int tv = r.tv_lo; tv <= r.tv_hi; ++tv) {
         int row = tv * tiles_u;
         for (int tu = r.s1_lo; tu <= r.s1_hi; ++tu) {
+            if (pos >= cap) return;
             ckeys[pos] = ((uint64_t)(row + tu) << 31) | c;
             vals[pos] = (uint32_t)g;
             ++pos;
         }
         for (int tu = 0; tu <= r.s2_hi; ++tu) {
+            if (pos >= cap) return;
             ckeys[pos] = ((uint64_t)(row + tu) << 31) | c;
             vals[pos] = (uint32_t)g;
             ++pos;
@@ -365,8 +369,11 @@ __global__ void __launch_bounds__(256) k_fill(int n, const Rect* __restrict__ re
 // prev to cur, i starts tiles prev+1..cur and ends tiles prev..cur-1
 // (searchsorted left / right, splat.py:340-343); tiles with no incidence
 // get an empty range at the right place.
-__global__ void k_ranges(const uint64_t* __restrict__ ckeys, int m, int n_tiles, int2* __restrict__ ranges) {
+// m_dev (nullable): the device-side count, clamped to m (then the capacity)
+__global__ void k_ranges(const uint64_t* __restrict__ ckeys, int m, const uint32_t* __restrict__ m_dev, int n_tiles,
+                         int2* __restrict__ ranges) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m_dev) m = min(m, (int)*m_dev);
     if (i > m) return;
     const long long prev = i > 0 ? (long long)(ckeys[i - 1] >> 31) : -1;
     const long long cur = i < m ? (long long)(ckeys[i] >> 31) : (long long)n_tiles;
@@ -465,18 +472,18 @@ int rfs_exclusive_scan_u32(const uint32_t* in, int n, uint32_t* out, uint32_t* t
     return RFS_OK;
 }
 
-int rfs_bin_fill(int n, const void* rects, const uint32_t* depth_code, const uint32_t* offsets, int n_az,
+int rfs_bin_fill(int n, const void* rects, const uint32_t* depth_code, const uint32_t* offsets, int n_az, int cap,
                  uint64_t* ckeys, uint32_t* vals, void* stream) {
-    if (n <= 0) return RFS_OK;
+    if (n <= 0 || cap <= 0) return RFS_OK;
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     k_fill<<<rfs_ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(n, (const Rect*)rects, depth_code, offsets, tiles_u,
-                                                                    ckeys, vals);
+                                                                    (uint32_t)cap, ckeys, vals);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
-int rfs_tile_ranges(const uint64_t* ckeys, int m, int n_tiles, int* ranges, void* stream) {
-    k_ranges<<<rfs_ceil_div(m + 1, 256), 256, 0, (cudaStream_t)stream>>>(ckeys, m, n_tiles, (int2*)ranges);
+int rfs_tile_ranges(const uint64_t* ckeys, int m, const uint32_t* m_dev, int n_tiles, int* ranges, void* stream) {
+    k_ranges<<<rfs_ceil_div(m + 1, 256), 256, 0, (cudaStream_t)stream>>>(ckeys, m, m_dev, n_tiles, (int2*)ranges);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -30,8 +30,11 @@ constexpr int HIST_THREADS = 256;
 constexpr int HIST_ITEMS = 16;
 
 // one read: digit histograms of every pass at once
-__global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint64_t* __restrict__ keys, int m, int passes,
+__global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint64_t* __restrict__ keys, int m,
+                                                      const uint32_t* __restrict__ m_dev, int passes,
                                                       uint32_t* __restrict__ hist) {
+    if (m_dev) m = min(m, (int)*m_dev);
+    if ((long long)blockIdx.x * HIST_THREADS * HIST_ITEMS >= m) return;
     __shared__ uint32_t sh[RS_MAX_PASSES][RS_RADIX];
     for (int i = threadIdx.x; i < passes * RS_RADIX; i += HIST_THREADS) sh[i / RS_RADIX][i % RS_RADIX] = 0;
     __syncthreads();
@@ -86,7 +89,8 @@ template <int RS_ITEMS>
 __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                                                         uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int m,
                                                         int shift, const uint32_t* __restrict__ digit_start,
-                                                        uint32_t* __restrict__ lookback, int* __restrict__ tile_counter) {
+                                                        uint32_t* __restrict__ lookback, int* __restrict__ tile_counter,
+                                                        const uint32_t* __restrict__ m_dev) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
     OnesweepSmem<RS_ITEMS>& S = *reinterpret_cast<OnesweepSmem<RS_ITEMS>*>(smem_raw);
@@ -96,6 +100,10 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const uint64_t* __restr
     __syncthreads();
     const int tile = S.tile_id;
     const long long tile_base = (long long)tile * RS_TILE;
+    if (m_dev) m = min(m, (int)*m_dev);
+    // tiles past the device-side count: no data, and every later tile (the
+    // only ones that would look back at this one) is empty too
+    if (tile_base >= m && tile > 0) return;
     const int tile_n = (int)min((long long)RS_TILE, (long long)m - tile_base);
 
     // warp-striped load: warp w owns keys [w*512, w*512+512) of the tile
@@ -226,7 +234,7 @@ inline int num_tiles(int m) { return rfs_ceil_div(m > 0 ? m : 1, RS_THREADS * it
 
 template <int ITEMS>
 int run_passes(uint64_t* kin, uint32_t* vin, uint64_t* kout, uint32_t* vout, int m, int passes, const uint32_t* hist,
-               uint32_t* lb, int* ctr, cudaStream_t st) {
+               uint32_t* lb, int* ctr, const uint32_t* m_dev, cudaStream_t st) {
     static bool attr_set = false;
     const size_t smem = sizeof(OnesweepSmem<ITEMS>);
     if (!attr_set) {
@@ -236,7 +244,7 @@ int run_passes(uint64_t* kin, uint32_t* vin, uint64_t* kout, uint32_t* vout, int
     const int nt = num_tiles(m);
     for (int p = 0; p < passes; ++p) {
         k_onesweep<ITEMS><<<nt, RS_THREADS, smem, st>>>(kin, vin, kout, vout, m, p * RS_BITS, hist + p * RS_RADIX,
-                                                        lb + (size_t)p * nt * RS_RADIX, ctr + p);
+                                                        lb + (size_t)p * nt * RS_RADIX, ctr + p, m_dev);
         uint64_t* tk = kin; kin = kout; kout = tk;
         uint32_t* tv = vin; vin = vout; vout = tv;
     }
@@ -257,11 +265,13 @@ size_t rfs_sort_temp_bytes(int m, int end_bit) {
     return hist + ctr + lb;
 }
 
-// Stable LSD radix sort of (keys, vals) on bits [0, end_bit).  Ping-pongs
+// Stable LSD radix sort of (keys, vals) on bits [0, end_bit); m is the
+// capacity (grid size) and, when m_dev is given, the device-side count
+// min(*m_dev, m) is sorted (no host read needed).  Ping-pongs
 // between (keys, vals) and (keys_alt, vals_alt); *result_in_alt tells the
 // caller which pair holds the sorted output.
 int rfs_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int m, int end_bit,
-                       void* temp, size_t temp_bytes, int* result_in_alt, void* stream) {
+                       void* temp, size_t temp_bytes, int* result_in_alt, const uint32_t* m_dev, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     *result_in_alt = 0;
     if (m <= 1) return RFS_OK;
@@ -275,13 +285,13 @@ int rfs_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint3
     uint32_t* lb = (uint32_t*)((unsigned char*)ctr + 64 * sizeof(int));
     int nt = num_tiles(m);
     RFS_CUDA_TRY(cudaMemsetAsync(temp, 0, rfs_sort_temp_bytes(m, end_bit), st));
-    k_hist<<<rfs_ceil_div(m, HIST_THREADS * HIST_ITEMS), HIST_THREADS, 0, st>>>(keys, m, passes, hist);
+    k_hist<<<rfs_ceil_div(m, HIST_THREADS * HIST_ITEMS), HIST_THREADS, 0, st>>>(keys, m, m_dev, passes, hist);
     k_hist_scan<<<1, 32 * RS_MAX_PASSES, 0, st>>>(hist, passes);
     int rc;
     switch (items_for(m)) {
-        case 16: rc = run_passes<16>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, st); break;
-        case 8: rc = run_passes<8>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, st); break;
-        default: rc = run_passes<4>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, st); break;
+        case 16: rc = run_passes<16>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, m_dev, st); break;
+        case 8: rc = run_passes<8>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, m_dev, st); break;
+        default: rc = run_passes<4>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, m_dev, st); break;
     }
     if (rc != RFS_OK) return rc;
     *result_in_alt = (passes & 1);

@@ -140,7 +140,7 @@ class Geometry:
 
 
 # adaptive capacities, remembered across steps
-_CAPS = {"hcap": 64, "pcap": 16}
+_CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}}
 _DIRS: dict = {}
 _SIDE: dict = {}
 
@@ -176,8 +176,13 @@ def sort_end_bit(n_tiles: int) -> int:
     return 31 + max(0, math.ceil(math.log2(max(n_tiles, 1))))
 
 
-def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand"):
-    """K3: stable sort of u64 keys with u32 payload; returns sorted (keys, vals)."""
+def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand", m_dev_ptr: int | None = None):
+    """K3: stable sort of u64 keys with u32 payload; returns sorted (keys, vals).
+
+    With `m_dev_ptr` (device address of a u32 count; hand-written sort only)
+    the buffers are a capacity and the first min(count, capacity) keys are
+    sorted without a host read.
+    """
     m = int(ckeys.numel())
     dev = ckeys.device
     if m <= 1:
@@ -191,9 +196,11 @@ def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand"):
         tb = int(lib.rfs_sort_temp_bytes(m, end_bit))
         temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
         _native.call("rfs_sort_pairs_u64", _ptr(ckeys), _ptr(vals), _ptr(kalt), _ptr(valt), m, end_bit,
-                     _ptr(temp), tb, _native.C.byref(res), _stream())
+                     _ptr(temp), tb, _native.C.byref(res), m_dev_ptr, _stream())
         _native.launch_counter["kernels"] += 2 + (end_bit + 7) // 8
     elif backend == "cub":
+        if m_dev_ptr is not None:
+            raise ValueError("the cub backend needs a host-side count")
         tb = int(lib.rfs_sort_cub_temp_bytes(m, end_bit))
         temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
         _native.call("rfs_sort_pairs_u64_cub", _ptr(ckeys), _ptr(vals), _ptr(kalt), _ptr(valt), m, end_bit,
@@ -274,29 +281,46 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     _native.call("rfs_exclusive_scan_u32", _ptr(counts), n, _ptr(offsets), status.data_ptr() + 4, _ptr(temp), st)
     _mark(marks, "project+scan")
     status_h = _pinned(dev, "status", 8)
-    status_h.copy_(status, non_blocking=True)
-    ev_m = torch.cuda.Event()
-    ev_m.record()
-    if psi_tx is not None:  # independent work queued behind the M read
-        psi = compute_psi(scene, psi_tx)
-        _mark(marks, "psi")
-    _spin(ev_m)  # read #1: error flags and M
-    host = status_h.tolist()
-    if int(host[0]) & (1 << 1):
-        raise GeometryError("a Gaussian is centered on the receiver")
-    m = int(host[1]) & 0xFFFFFFFF
-    ckeys = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
-    vals = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
-    if m > 0:
-        _native.call("rfs_bin_fill", n, _ptr(rects), _ptr(code), _ptr(offsets), n_az, _ptr(ckeys), _ptr(vals), st)
-        _mark(marks, "fill")
-        ckeys, vals = sort_pairs(ckeys[:m], vals[:m], sort_end_bit(n_tiles), sort_backend)
-        _mark(marks, "sort")
-    ranges = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
-    _native.call("rfs_tile_ranges", _ptr(ckeys), m, n_tiles, _ptr(ranges), st)
-    lb = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
-    _native.call("rfs_lower_bounds", _ptr(ranges), n_tiles, _ptr(vals), _ptr(geom), _ptr(lb), st)
-    _mark(marks, "ranges+lb")
+    m_dev_ptr = status.data_ptr() + 4
+
+    def bin_tiles(cap: int, device_count: bool):
+        """K2b fill, K3 sort, K4 ranges, K4b bounds into buffers of capacity `cap`."""
+        ck = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+        vl = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        mp = m_dev_ptr if device_count else None
+        if cap > 0:
+            _native.call("rfs_bin_fill", n, _ptr(rects), _ptr(code), _ptr(offsets), n_az, cap, _ptr(ck), _ptr(vl), st)
+            _mark(marks, "fill")
+            ck, vl = sort_pairs(ck[:cap], vl[:cap], sort_end_bit(n_tiles), sort_backend, mp)
+            _mark(marks, "sort")
+        rg = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
+        _native.call("rfs_tile_ranges", _ptr(ck), cap, mp, n_tiles, _ptr(rg), st)
+        lbv = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
+        _native.call("rfs_lower_bounds", _ptr(rg), n_tiles, _ptr(vl), _ptr(geom), _ptr(lbv), st)
+        _mark(marks, "ranges+lb")
+        return ck, vl, rg, lbv
+
+    # Read #1 (M) is skipped when a capacity from earlier steps is known: the
+    # binning then runs on the device-side count and M is checked at read #2.
+    m_cap = _CAPS.get("m_cap", {}).get((n, n_az, n_el)) if sort_backend == "hand" else None
+    if m_cap is None:
+        status_h.copy_(status, non_blocking=True)
+        ev_m = torch.cuda.Event()
+        ev_m.record()
+        if psi_tx is not None:  # independent work queued behind the M read
+            psi = compute_psi(scene, psi_tx)
+            _mark(marks, "psi")
+        _spin(ev_m)  # read #1: error flags and M
+        host = status_h.tolist()
+        if int(host[0]) & (1 << 1):
+            raise GeometryError("a Gaussian is centered on the receiver")
+        m = int(host[1]) & 0xFFFFFFFF
+        ckeys, vals, ranges, lb = bin_tiles(m, False)
+    else:
+        if psi_tx is not None:
+            psi = compute_psi(scene, psi_tx)
+            _mark(marks, "psi")
+        ckeys, vals, ranges, lb = bin_tiles(m_cap, True)
 
     hc = 1 << max(0, math.ceil(math.log2(max(int(hcap or _CAPS["hcap"]), 1))))  # power of two: slot >> log2(hcap) = ray
     pc = _CAPS["pcap"]
@@ -313,14 +337,28 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                      _ptr(slow), _ptr(stats), st)
         _mark(marks, "hits")
         stats_h.copy_(stats, non_blocking=True)
+        if m_cap is not None:
+            status_h.copy_(status, non_blocking=True)
         ev_s = torch.cuda.Event()
         ev_s.record()
         if forward and psi is not None and S is None:  # queued behind the statistics read
             S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
             _mark(marks, "forward")
             after = after_forward(S) if after_forward is not None else None
-        _spin(ev_s)  # read #2: hit-list statistics
+        _spin(ev_s)  # read #2: hit-list statistics (and M when read #1 was skipped)
         s = stats_h.tolist()
+        if m_cap is not None:
+            host = status_h.tolist()
+            if int(host[0]) & (1 << 1):
+                raise GeometryError("a Gaussian is centered on the receiver")
+            m = int(host[1]) & 0xFFFFFFFF
+            _CAPS["m_cap"][(n, n_az, n_el)] = max(m_cap, m + m // 8 + 1024) if m <= m_cap else m + m // 4 + 1024
+            if m > m_cap:  # capacity overflow: re-bin with the exact count, redo the hit lists
+                m_cap = None
+                ckeys, vals, ranges, lb = bin_tiles(m, False)
+                redo_forward = True
+                continue
+            m_cap = None
         if s[0] > 0:
             # rays whose pending ring overflowed: exact slow path, and a larger
             # ring for the next steps if it happens often
@@ -343,6 +381,8 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             redo_forward = True
             continue
         break
+    if sort_backend == "hand":
+        _CAPS.setdefault("m_cap", {}).setdefault((n, n_az, n_el), m + m // 8 + 1024)
     geo = Geometry(n, n_az, n_el, tiles_u, tiles_v, m, geom, rho32, dirs, ckeys[:max(m, 0)], vals[:max(m, 0)],
                    ranges, hc, slab, ray_counts, s, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
     geo.psi = psi
