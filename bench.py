@@ -204,7 +204,7 @@ def run_ours(args):
 
     def step(marks=None):
         # psi queued behind the M read, the composite behind the hit-statistics read
-        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, forward=True,
+        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, forward=True, index=True,
                                    after_forward=lambda S: raster.transpose_upstream(lam))
         psi, S = g0.psi, g0.S
         g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks, deterministic=args.deterministic,

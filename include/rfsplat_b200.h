@@ -129,12 +129,16 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
  * rfs_gather_sorted: per sorted hit p its ray s_ray[p], w s_w[p], w T
  * s_wt[p] (complex64) and, if inv_slot is not NULL, inv_slot[slot] = p
  * (u32[R*hcap]);
- * rfs_gauss_offsets: g_off (int32[N+1]) over the sorted keys. */
+ * rfs_gauss_offsets: g_off (int32[N+1]) over the sorted keys.
+ * Entry points taking (n_hits, h_dev) treat n_hits as the capacity and, when
+ * h_dev (device u32) is given, process min(*h_dev, n_hits) hits -- the hit
+ * index and the backward then need no host read of the hit count. */
 int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays, uint64_t* keys,
                  uint32_t* slots, void* stream);
-int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, int hcap, const void* slab, uint32_t* s_ray,
+int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* h_dev, int hcap, const void* slab,
+                      uint32_t* s_ray,
                       float* s_w, void* s_wt, uint32_t* inv_slot, void* stream);
-int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream);
+int rfs_gauss_offsets(const uint64_t* keys, int n_hits, const uint32_t* h_dev, int n, int* g_off, void* stream);
 
 /* K8: TX-batched backward over the shared hit lists, atomic-free and
  * deterministic (every sum in a fixed order).  Replaces the complex part of
@@ -154,7 +158,8 @@ int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void*
  * n_tx <= 256 per rfs_bwd_gauss call. */
 int rfs_lam_transpose(const void* lam, int n_tx, int n_rays, void* lamT, void* stream);
 size_t rfs_bwd_part_elems(int n_hits, int n_tx);
-int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot, int hcap,
+int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot,
+                  int hcap,
                   const void* s_wt, const int* g_off, const void* psi, const void* lamT, int accumulate, void* C,
                   void* P, void* part, void* stream);
 int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32, const void* geom,
@@ -172,7 +177,7 @@ int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, cons
  * Scratch: acc64 f64[N*14], part_g i32[rfs_geom_part_elems(H)],
  * part_v f64[14*rfs_geom_part_elems(H)]. */
 size_t rfs_geom_part_elems(int n_hits);
-int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
+int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
                   const uint32_t* s_slot, const void* gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,

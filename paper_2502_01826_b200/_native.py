@@ -43,13 +43,13 @@ _SIGS = {
     "rfs_forward": (i32, [vp, vp, i32, vp, i32, i32, i32, vp, vp]),
     "rfs_lam_transpose": (i32, [vp, i32, i32, vp, vp]),
     "rfs_bwd_part_elems": (sz, [i32, i32]),
-    "rfs_bwd_gauss": (i32, [i32, i32, i32, vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp]),
+    "rfs_bwd_gauss": (i32, [i32, i32, vp, i32, vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp]),
     "rfs_bwd_rays": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp]),
     "rfs_hit_keys": (i32, [vp, vp, vp, i32, i32, vp, vp, vp]),
-    "rfs_gather_sorted": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, vp]),
-    "rfs_gauss_offsets": (i32, [vp, i32, i32, vp, vp]),
+    "rfs_gather_sorted": (i32, [vp, i32, vp, i32, vp, vp, vp, vp, vp, vp]),
+    "rfs_gauss_offsets": (i32, [vp, i32, vp, i32, vp, vp]),
     "rfs_geom_part_elems": (sz, [i32]),
-    "rfs_grad_geom": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+    "rfs_grad_geom": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                             vp, vp, vp, vp, vp, vp]),
     "rfs_grad_tx": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
     "rfs_loss_scratch_bytes": (sz, [i32, i32, i32]),

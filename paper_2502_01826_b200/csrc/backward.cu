@@ -76,10 +76,11 @@ __device__ __forceinline__ float reduce8(float (&v)[8], int lane) {
 // Generic TX count: lanes own b = lane + 32 j (float2 loads).
 template <int NJ>
 __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
-    int h_tot, int nb, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_slot, int hshift,
-    const float2* __restrict__ s_wt, const int* __restrict__ g_off, const float2* __restrict__ psi,
-    const float2* __restrict__ lamT, int accumulate, float2* __restrict__ C, float2* __restrict__ P,
-    float2* __restrict__ part) {
+    int h_tot, const uint32_t* __restrict__ h_dev, int nb, const uint64_t* __restrict__ sorted_g,
+    const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const int* __restrict__ g_off,
+    const float2* __restrict__ psi, const float2* __restrict__ lamT, int accumulate, float2* __restrict__ C,
+    float2* __restrict__ P, float2* __restrict__ part) {
+    if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     __shared__ uint32_t sh_g[BG_WARPS][BG_CHUNK];
     __shared__ uint32_t sh_r[BG_WARPS][BG_CHUNK];
     __shared__ float2 sh_wt[BG_WARPS][BG_CHUNK];
@@ -174,9 +175,11 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
 // next segment's psi row is prefetched while the current one is reduced.
 template <int NP>
 __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
-    int h_tot, int nb, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_slot, int hshift,
-    const float2* __restrict__ s_wt, const float4* __restrict__ psi, const float4* __restrict__ lamT,
-    int accumulate, float2* __restrict__ C, float4* __restrict__ P, float4* __restrict__ part) {
+    int h_tot, const uint32_t* __restrict__ h_dev, int nb, const uint64_t* __restrict__ sorted_g,
+    const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const float4* __restrict__ psi,
+    const float4* __restrict__ lamT, int accumulate, float2* __restrict__ C, float4* __restrict__ P,
+    float4* __restrict__ part) {
+    if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     __shared__ uint32_t sh_g[BG_WARPS][BG_CHUNK + 1];
     __shared__ uint32_t sh_s[BG_WARPS][BG_CHUNK];
     __shared__ float2 sh_wt[BG_WARPS][BG_CHUNK];
@@ -290,9 +293,11 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
 
 // Gaussians whose hits straddle chunks: the warp of the chunk where such a
 // Gaussian starts sums the chunk partials in chunk order (deterministic).
-__global__ void __launch_bounds__(256) k_bwd_pfix(int h_tot, int nb, const uint64_t* __restrict__ sorted_g,
+__global__ void __launch_bounds__(256) k_bwd_pfix(int h_tot, const uint32_t* __restrict__ h_dev, int nb,
+                                                  const uint64_t* __restrict__ sorted_g,
                                                   const int* __restrict__ g_off, const float2* __restrict__ part,
                                                   float2* __restrict__ P) {
+    if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int c0 = w * BG_CHUNK;
@@ -443,7 +448,8 @@ size_t rfs_bwd_part_elems(int n_hits, int n_tx) {
     return (size_t)2 * (size_t)((n_hits + BG_CHUNK - 1) / BG_CHUNK + 1) * (size_t)(n_tx > 0 ? n_tx : 1);
 }
 
-int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot, int hcap,
+int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot,
+                  int hcap,
                   const void* s_wt, const int* g_off, const void* psi, const void* lamT, int accumulate, void* C,
                   void* P, void* part, void* stream) {
     if (n <= 0 || n_hits <= 0 || n_tx <= 0) return RFS_OK;
@@ -455,7 +461,7 @@ int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const u
     const unsigned grid = (unsigned)rfs_ceil_div(nwarps, BG_WARPS);
     if (n_tx % 64 == 0) {
 #define RFS_BV(NPV)                                                                                              \
-    k_bwd_gauss_v<NPV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, n_tx, sorted_g, s_slot, hshift,                   \
+    k_bwd_gauss_v<NPV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,                   \
                                                        (const float2*)s_wt, (const float4*)psi,                  \
                                                        (const float4*)lamT, accumulate, (float2*)C, (float4*)P,  \
                                                        (float4*)part)
@@ -469,7 +475,8 @@ int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const u
     } else {
         const int nj = (n_tx + 31) / 32;
 #define RFS_BG(NJV)                                                                                              \
-    k_bwd_gauss<NJV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, n_tx, sorted_g, s_slot, hshift, (const float2*)s_wt, \
+    k_bwd_gauss<NJV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,             \
+                                                     (const float2*)s_wt,                                        \
                                                      g_off, (const float2*)psi, (const float2*)lamT, accumulate, \
                                                      (float2*)C, (float2*)P, (float2*)part)
         if (nj == 1) RFS_BG(1);
@@ -478,7 +485,7 @@ int rfs_bwd_gauss(int n, int n_hits, int n_tx, const uint64_t* sorted_g, const u
         else RFS_BG(8);
 #undef RFS_BG
     }
-    k_bwd_pfix<<<rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st>>>(n_hits, n_tx, sorted_g, g_off,
+    k_bwd_pfix<<<rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, g_off,
                                                                           (const float2*)part, (float2*)P);
     RFS_LAUNCH_CHECK();
     return RFS_OK;

@@ -150,9 +150,11 @@ __global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restric
 }
 
 // per sorted hit p: its ray, w, w T; inverse map slot -> p (nullable)
-__global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h, int hcap,
+__global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h, const uint32_t* __restrict__ h_dev,
+                                int hcap,
                                 const RfsHit* __restrict__ slab, uint32_t* __restrict__ s_ray,
                                 float* __restrict__ s_w, float2* __restrict__ s_wt, uint32_t* __restrict__ inv_slot) {
+    if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= h) return;
     const uint32_t s = sorted_slots[p];
@@ -165,7 +167,9 @@ __global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h
 
 // g_off[g] = lower_bound(g) over the sorted Gaussian keys, g in [0, n]: the
 // thread of sorted position p writes every g in (keys[p-1], keys[p]]
-__global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, int n, int* __restrict__ g_off) {
+__global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, const uint32_t* __restrict__ h_dev, int n,
+                                int* __restrict__ g_off) {
+    if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p > h) return;
     const long long prev = p > 0 ? (long long)keys[p - 1] : -1;
@@ -226,17 +230,18 @@ int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, i
     return RFS_OK;
 }
 
-int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, int hcap, const void* slab, uint32_t* s_ray,
+int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* h_dev, int hcap, const void* slab,
+                      uint32_t* s_ray,
                       float* s_w, void* s_wt, uint32_t* inv_slot, void* stream) {
     if (n_hits <= 0) return RFS_OK;
     k_gather_sorted<<<rfs_ceil_div(n_hits, 256), 256, 0, (cudaStream_t)stream>>>(
-        sorted_slots, n_hits, hcap, (const RfsHit*)slab, s_ray, s_w, (float2*)s_wt, inv_slot);
+        sorted_slots, n_hits, h_dev, hcap, (const RfsHit*)slab, s_ray, s_w, (float2*)s_wt, inv_slot);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
-int rfs_gauss_offsets(const uint64_t* keys, int n_hits, int n, int* g_off, void* stream) {
-    k_gauss_offsets<<<rfs_ceil_div(n_hits + 1, 256), 256, 0, (cudaStream_t)stream>>>(keys, n_hits, n, g_off);
+int rfs_gauss_offsets(const uint64_t* keys, int n_hits, const uint32_t* h_dev, int n, int* g_off, void* stream) {
+    k_gauss_offsets<<<rfs_ceil_div(n_hits + 1, 256), 256, 0, (cudaStream_t)stream>>>(keys, n_hits, h_dev, n, g_off);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -29,13 +29,16 @@ constexpr int GB_MAXJ = 8;       // up to 256 TX per launch
 
 // ------------------------------------------------------------------ K9a
 __global__ void __launch_bounds__(256) k_geom_seg(
-    int h, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_ray, const float* __restrict__ s_w,
+    int h, const uint32_t* __restrict__ h_dev, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_ray,
+    const float* __restrict__ s_w,
     const uint32_t* __restrict__ s_slot, const float4* __restrict__ gs, const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
     const int* __restrict__ g_off, double rx0, double rx1, double rx2, double min_t, double* __restrict__ acc64,
     int* __restrict__ part_g, double* __restrict__ part_v) {
+    if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int wglob = p >> 5;
+    if ((wglob << 5) >= h) return;  // whole warp past the device-side count
     const bool valid = p < h;
     const int g = valid ? (int)sorted_g[p] : -1;
     double v[NACC];
@@ -142,9 +145,11 @@ __global__ void __launch_bounds__(256) k_geom_seg(
 // Gaussians whose hits straddle warps: the warp of the 32-hit group where
 // such a Gaussian starts adds the group partials in group order (lanes over
 // the 14 sums) -- a fixed order, so the result stays deterministic.
-__global__ void __launch_bounds__(256) k_geom_fix(int h, const uint64_t* __restrict__ sorted_g,
+__global__ void __launch_bounds__(256) k_geom_fix(int h, const uint32_t* __restrict__ h_dev,
+                                                  const uint64_t* __restrict__ sorted_g,
                                                   const int* __restrict__ g_off, const double* __restrict__ part_v,
                                                   double* __restrict__ acc64) {
+    if (h_dev) h = min(h, (int)*h_dev);
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int c0 = w << 5;
@@ -380,7 +385,7 @@ extern "C" {
 
 size_t rfs_geom_part_elems(int n_hits) { return (size_t)2 * (size_t)((n_hits + 31) / 32 + 1); }
 
-int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
+int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
                   const uint32_t* s_slot, const void* gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
@@ -390,10 +395,10 @@ int rfs_grad_geom(int n, int n_hits, const uint64_t* sorted_g, const uint32_t* s
     cudaStream_t st = (cudaStream_t)stream;
     RFS_CUDA_TRY(cudaMemsetAsync(acc64, 0, sizeof(double) * NACC * (size_t)n, st));
     if (n_hits > 0) {
-        k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
+        k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
                                                                (const RfsGeom*)geom, dirs, g_off, rx[0], rx[1], rx[2],
                                                                ress_radius, acc64, part_g, part_v);
-        k_geom_fix<<<rfs_ceil_div((long long)rfs_ceil_div(n_hits, 32) * 32, 256), 256, 0, st>>>(n_hits, sorted_g,
+        k_geom_fix<<<rfs_ceil_div((long long)rfs_ceil_div(n_hits, 32) * 32, 256), 256, 0, st>>>(n_hits, h_dev, sorted_g,
                                                                                               g_off, part_v, acc64);
     }
     k_geom_final<<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, acc64, quats, log_scales, trans_mag_raw, d_mean, d_quat,

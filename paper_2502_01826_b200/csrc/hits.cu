@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(NT) k_hits(
         slow_list[idx] = r;
         return;
     }
-    counts[r] = st.live;
+    counts[r] = min(st.live, hcap);  // stored hits; live > hcap is flagged in stats[1]
     if (st.hcap_over) atomicAdd(&stats[1], 1);
     atomicMax(&stats[2], st.live);
     atomicAdd(&stats[3], min(st.live, hcap));
@@ -455,7 +455,7 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
         ++head;
         --npend;
     }
-    counts[r] = st.live;
+    counts[r] = min(st.live, hcap);  // stored hits; live > hcap is flagged in stats[1]
     if (st.hcap_over) atomicAdd(&stats[1], 1);
     atomicMax(&stats[2], st.live);
     atomicAdd(&stats[3], min(st.live, hcap));

@@ -140,7 +140,7 @@ class Geometry:
 
 
 # adaptive capacities, remembered across steps
-_CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}}
+_CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {}}
 _DIRS: dict = {}
 _SIDE: dict = {}
 
@@ -329,6 +329,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     stats = torch.zeros(8, dtype=torch.int32, device=dev)
     stats_h = _pinned(dev, "stats", 8)
     S = None
+    early = None
     redo_forward = False
     while True:
         slab = torch.empty(R * hc * 16, dtype=torch.uint8, device=dev)
@@ -345,6 +346,13 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
             _mark(marks, "forward")
             after = after_forward(S) if after_forward is not None else None
+        h_cap = _CAPS["h_cap"].get((n_az, n_el, hc)) if index and sort_backend == "hand" else None
+        early = None
+        if h_cap is not None:  # the by-Gaussian index, also behind the statistics read
+            early = Geometry(n, n_az, n_el, tiles_u, tiles_v, -1, geom, rho32, dirs, ckeys, vals, ranges, hc, slab,
+                             ray_counts, [0] * 8, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
+            gauss_index(early, h_cap)
+            _mark(marks, "gauss_index")
         _spin(ev_s)  # read #2: hit-list statistics (and M when read #1 was skipped)
         s = stats_h.tolist()
         if m_cap is not None:
@@ -393,8 +401,15 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         geo.S = S
         geo.after_result = after
     if index:
-        gauss_index(geo)
-        _mark(marks, "gauss_index")
+        hh = int(s[3])
+        if early is not None and not redo_forward and hh <= h_cap:
+            geo.gidx = early.gidx
+        else:
+            gauss_index(geo)
+            _mark(marks, "gauss_index")
+        if sort_backend == "hand":
+            key = (n_az, n_el, hc)
+            _CAPS["h_cap"][key] = max(_CAPS["h_cap"].get(key, 0), hh + hh // 8 + 4096)
     return geo
 
 
@@ -430,12 +445,15 @@ def forward(geo: Geometry, psi: torch.Tensor) -> torch.Tensor:
     return _forward_raw(geo.slab, geo.ray_counts, geo.hcap, psi, geo.n_az, geo.n_el)
 
 
-def gauss_index(geo: Geometry) -> None:
+def gauss_index(geo: Geometry, h_cap: int | None = None) -> None:
     """K8i: by-Gaussian index of the live hits (TX independent, cached on geo).
 
     Hits sorted by Gaussian id with a stable sort, so within a Gaussian they
     keep the (ray, k) order of the reference's bincount slots
-    (grad.py:222-254); per sorted hit: ray, w, w T; inverse slot map.
+    (grad.py:222-254); per sorted hit: ray, slab slot, w, w T.  The hit count
+    H stays on the device: `h_cap` (default: the exact H of the hit-list
+    statistics) sizes the buffers and grids, every kernel reads min(H, h_cap)
+    -- so build_geometry can enqueue this before it reads the statistics.
     """
     if geo.gidx is not None:
         return
@@ -443,27 +461,32 @@ def gauss_index(geo: Geometry) -> None:
     dev = geo.slab.device
     st = _stream()
     R = geo.n_rays
+    cap = int(h_cap if h_cap is not None else geo.total_hits)
     ray_off = torch.empty(R, dtype=torch.int32, device=dev)
     tot = torch.empty(1, dtype=torch.int32, device=dev)
     temp = torch.empty(int(lib.rfs_scan_temp_elems(R)), dtype=torch.int32, device=dev)
     _native.call("rfs_exclusive_scan_u32", _ptr(geo.ray_counts), R, _ptr(ray_off), _ptr(tot), _ptr(temp), st)
-    h = geo.total_hits  # counts <= hcap here (hit-capacity overflow was resolved in build_geometry)
-    keys = torch.empty(max(h, 1), dtype=torch.int64, device=dev)
-    slots = torch.empty(max(h, 1), dtype=torch.int32, device=dev)
+    # hit keys land at ray_off[r] + k < H; positions >= cap are never read (H <= cap is checked)
+    keys = torch.empty(max(R * geo.hcap, 1), dtype=torch.int64, device=dev)
+    slots = torch.empty(max(R * geo.hcap, 1), dtype=torch.int32, device=dev)
     _native.call("rfs_hit_keys", _ptr(geo.slab), _ptr(geo.ray_counts), _ptr(ray_off), geo.hcap, R, _ptr(keys),
                  _ptr(slots), st)
     bits = max(1, math.ceil(math.log2(max(geo.n, 2))))
-    if h > 1:
-        keys, slots = sort_pairs(keys[:h], slots[:h], bits, geo.sort_backend)
+    hd = tot.data_ptr()
+    if cap > 1:
+        if geo.sort_backend == "hand":
+            keys, slots = sort_pairs(keys[:cap], slots[:cap], bits, "hand", hd)
+        else:  # cub needs the exact count: only reached after the statistics read
+            keys, slots = sort_pairs(keys[:cap], slots[:cap], bits, geo.sort_backend)
     g_off = torch.empty(geo.n + 1, dtype=torch.int32, device=dev)
-    _native.call("rfs_gauss_offsets", _ptr(keys), h, geo.n, _ptr(g_off), st)
-    s_ray = torch.empty(max(h, 1), dtype=torch.int32, device=dev)
-    s_w = torch.empty(max(h, 1), dtype=torch.float32, device=dev)
-    s_wt = torch.empty(max(h, 1), dtype=torch.complex64, device=dev)
-    _native.call("rfs_gather_sorted", _ptr(slots), h, geo.hcap, _ptr(geo.slab), _ptr(s_ray), _ptr(s_w), _ptr(s_wt),
-                 None, st)
-    geo.gidx = {"h": h, "sorted_g": keys, "g_off": g_off, "s_ray": s_ray, "s_w": s_w, "s_wt": s_wt,
-                "s_slot": slots}
+    _native.call("rfs_gauss_offsets", _ptr(keys), cap, hd, geo.n, _ptr(g_off), st)
+    s_ray = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    s_w = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+    s_wt = torch.empty(max(cap, 1), dtype=torch.complex64, device=dev)
+    _native.call("rfs_gather_sorted", _ptr(slots), cap, hd, geo.hcap, _ptr(geo.slab), _ptr(s_ray), _ptr(s_w),
+                 _ptr(s_wt), None, st)
+    geo.gidx = {"h": cap, "h_dev": hd, "tot": tot, "sorted_g": keys, "g_off": g_off, "s_ray": s_ray, "s_w": s_w,
+                "s_wt": s_wt, "s_slot": slots}
 
 
 def transpose_upstream(grad_S: torch.Tensor) -> torch.Tensor:
@@ -518,10 +541,12 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         return out
     R = geo.n_rays
     lib = _native.load()
+    built = geo.gidx is None
     gauss_index(geo)
     gi = geo.gidx
+    if built:
+        _mark(marks, "gauss_index")
     h = gi["h"]
-    _mark(marks, "gauss_index")
     main = torch.cuda.current_stream(dev)
     side = _side_stream(dev)
     C = torch.empty(R * geo.hcap, dtype=torch.complex64, device=dev)        # slab order, live slots written
@@ -539,7 +564,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
             _native.call("rfs_lam_transpose", _ptr(grad_S[c0:c1]), nbc, R, _ptr(lamTc), st)
         P = torch.empty((n, nbc), dtype=torch.complex64, device=dev)
         part = torch.empty(int(lib.rfs_bwd_part_elems(h, nbc)), dtype=torch.complex64, device=dev)
-        _native.call("rfs_bwd_gauss", n, h, nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_slot"]), geo.hcap,
+        _native.call("rfs_bwd_gauss", n, h, gi["h_dev"], nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_slot"]), geo.hcap,
                      _ptr(gi["s_wt"]), _ptr(gi["g_off"]), _ptr(psic), _ptr(lamTc), int(c0 > 0), _ptr(C), _ptr(P),
                      _ptr(part), st)
         # K9b on a second stream: it needs only P, so it overlaps the ray
@@ -561,7 +586,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     part_g = torch.empty(npart, dtype=torch.int32, device=dev)
     part_v = torch.empty((npart, 14), dtype=torch.float64, device=dev)
     main.wait_stream(side)  # K9c adds K9b's bearing chain (dm_dir)
-    _native.call("rfs_grad_geom", n, h, _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(gi["s_slot"]),
+    _native.call("rfs_grad_geom", n, h, gi["h_dev"], _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(gi["s_slot"]),
                  _ptr(gs), _ptr(gi["g_off"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius),
                  _ptr(scene.quats), _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(acc64), _ptr(part_g),
                  _ptr(part_v), _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]),
