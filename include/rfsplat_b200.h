@@ -150,10 +150,12 @@ int rfs_gauss_offsets(const uint64_t* keys, int n_hits, const uint32_t* h_dev, i
  *   conj(lam_b[ray]) psi[g][b] (complex64[R*hcap]; accumulate = 1 adds a
  *   further TX chunk) and P[g][b] = p_acc (complex64[N*B]; rows of Gaussians
  *   without hits are left unwritten).  part: complex64[rfs_bwd_part_elems(H,
- *   B)] scratch.  B a multiple of 64 takes the 16-byte-vector path.
+ *   B)] and cnt (i32[N]) scratch.  B a multiple of 64 takes the 16-byte-vector
+ *   path, whose chunks complete straddling Gaussians themselves (last chunk
+ *   to finish sums the partials in chunk order).
  * rfs_bwd_rays: per ray the suffix recursion A_k = w_{k+1} C_{k+1} +
- *   rho_{k+1} A_{k+1} (rho fp64 from geom, T rebuilt in fp64 for rays with
- *   <= 32 hits) and the per-hit scalars {Re(T C), d|rho|, d(phase) hi, lo}
+ *   rho_{k+1} A_{k+1} (rho fp64 from geom) and the per-hit scalars
+ *   {Re(T C), d|rho|, d(phase) hi, lo}
  *   (float4[R*hcap], slab order) in gs.
  * n_tx <= 256 per rfs_bwd_gauss call. */
 int rfs_lam_transpose(const void* lam, int n_tx, int n_rays, void* lamT, void* stream);
@@ -161,7 +163,7 @@ size_t rfs_bwd_part_elems(int n_hits, int n_tx);
 int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot,
                   int hcap,
                   const void* s_wt, const int* g_off, const void* psi, const void* lamT, int accumulate, void* C,
-                  void* P, void* part, void* stream);
+                  void* P, void* part, int* cnt, void* stream);
 int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32, const void* geom,
                  const void* C, void* gs, void* stream);
 

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
     int h_tot, const uint32_t* __restrict__ h_dev, int nb, const uint64_t* __restrict__ sorted_g,
     const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const float4* __restrict__ psi,
     const float4* __restrict__ lamT, int accumulate, float2* __restrict__ C, float4* __restrict__ P,
-    float4* __restrict__ part) {
+    float4* __restrict__ part, const int* __restrict__ g_off, int* __restrict__ cnt) {
     if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     __shared__ uint32_t sh_g[BG_WARPS][BG_CHUNK + 1];
     __shared__ uint32_t sh_s[BG_WARPS][BG_CHUNK];
@@ -289,6 +289,33 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
         }
         s0 = e;
     }
+    // Gaussians straddling chunks: the last chunk to finish (counted on cnt[g])
+    // adds the chunk partials in chunk order -- deterministic, no fix-up launch
+    if (!first_out && !last_out) return;
+    __threadfence();
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (k == 0 ? !first_out : !last_out) continue;
+        const int gk = (int)sh_g[wl][k == 0 ? 0 : n - 1];
+        if (k == 1 && first_out && gk == (int)sh_g[wl][0]) break;  // one Gaussian spans the chunk: counted once
+        const int w0 = g_off[gk] / BG_CHUNK, w1 = (g_off[gk + 1] - 1) / BG_CHUNK;
+        int last = 0;
+        if (lane == 0) last = atomicAdd(&cnt[gk], 1) == w1 - w0;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) continue;
+        __threadfence();
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            const int q = lane + 32 * j;
+            float4 acc = __ldcg(&part[(size_t)(2 * w0 + 1) * nq + q]);
+            for (int w = w0 + 1; w <= w1; ++w) {
+                const float4 t = __ldcg(&part[(size_t)(2 * w) * nq + q]);
+                acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+            }
+            P[(size_t)gk * nq + q] = acc;
+        }
+    }
 }
 
 // Gaussians whose hits straddle chunks: the warp of the chunk where such a
@@ -337,10 +364,8 @@ __device__ __forceinline__ Aff compose(const Aff& f, const Aff& h) {  // f(h(x))
     return o;
 }
 
-// Precision: rho in fp64 from the geometry record (the reference's value);
-// for rays with <= 32 live hits (all of them at 100k, max 28) T is rebuilt in
-// fp64 as a warp prefix product of rho instead of the slab's fp32 copy; and
-// d(phase) -- a sum of strongly cancelling terms for Gaussians crossed by
+// Precision: rho in fp64 from the geometry record (the reference's value),
+// and d(phase) -- a sum of strongly cancelling terms for Gaussians crossed by
 // many rays -- is stored as a float pair (hi, lo) for the fp64 sums of K9a.
 __global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
                                                   int hcap, int R, const float4* __restrict__ rho32,
@@ -369,23 +394,7 @@ __global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ sla
         }
         const float4 rq = ok ? __ldg(&rho32[hk.g]) : make_float4(1.f, 0.f, 1.f, 0.f);
         const double rr = ok ? __ldg(&geom[hk.g].rho_re) : 1.0, ri = ok ? __ldg(&geom[hk.g].rho_im) : 0.0;
-        // T_k in fp64: exclusive prefix product of rho over the ray's hits (single chunk)
-        double tr = hk.t_re, ti = hk.t_im;
-        if (cnt <= 32) {
-            double pr = rr, pi = ri;  // inclusive scan
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double qr = __shfl_up_sync(0xffffffffu, pr, o), qi = __shfl_up_sync(0xffffffffu, pi, o);
-                if (lane >= o) {
-                    const double nr = qr * pr - qi * pi;
-                    pi = qr * pi + qi * pr;
-                    pr = nr;
-                }
-            }
-            const double er = __shfl_up_sync(0xffffffffu, pr, 1), ei = __shfl_up_sync(0xffffffffu, pi, 1);
-            tr = lane == 0 ? 1.0 : er;
-            ti = lane == 0 ? 0.0 : ei;
-        }
+        const double tr = hk.t_re, ti = hk.t_im;
         // f_k(A) = w_k C_k + rho_k A; lane k holds F_k = f_{k+1} (identity past the end)
         const double wc_r = (double)hk.w * (double)ck.x, wc_i = (double)hk.w * (double)ck.y;
         Aff F;
@@ -451,7 +460,7 @@ size_t rfs_bwd_part_elems(int n_hits, int n_tx) {
 int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot,
                   int hcap,
                   const void* s_wt, const int* g_off, const void* psi, const void* lamT, int accumulate, void* C,
-                  void* P, void* part, void* stream) {
+                  void* P, void* part, int* cnt, void* stream) {
     if (n <= 0 || n_hits <= 0 || n_tx <= 0) return RFS_OK;
     if (n_tx > 32 * BG_MAXJ) return RFS_ERR_SHAPE;
     if (hcap <= 0 || (hcap & (hcap - 1))) return RFS_ERR_SHAPE;
@@ -460,11 +469,12 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
     const int nwarps = rfs_ceil_div(n_hits, BG_CHUNK);
     const unsigned grid = (unsigned)rfs_ceil_div(nwarps, BG_WARPS);
     if (n_tx % 64 == 0) {
+        RFS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)n, st));
 #define RFS_BV(NPV)                                                                                              \
     k_bwd_gauss_v<NPV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,                   \
                                                        (const float2*)s_wt, (const float4*)psi,                  \
                                                        (const float4*)lamT, accumulate, (float2*)C, (float4*)P,  \
-                                                       (float4*)part)
+                                                       (float4*)part, g_off, cnt)
         switch (n_tx / 64) {
             case 1: RFS_BV(1); break;
             case 2: RFS_BV(2); break;
@@ -484,9 +494,9 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
         else if (nj <= 4) RFS_BG(4);
         else RFS_BG(8);
 #undef RFS_BG
+        k_bwd_pfix<<<rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, g_off,
+                                                                              (const float2*)part, (float2*)P);
     }
-    k_bwd_pfix<<<rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, g_off,
-                                                                          (const float2*)part, (float2*)P);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -275,58 +275,56 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t& excl) {
     return total;
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(const uint32_t* __restrict__ in, int n, uint32_t* __restrict__ part) {
-    long long base = (long long)blockIdx.x * SCAN_TILE;
-    uint32_t s = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        long long j = base + (long long)i * SCAN_THREADS + threadIdx.x;
-        if (j < n) s += in[j];
-    }
-    uint32_t ex;
-    uint32_t tot = block_excl_scan(s, ex);
-    if (threadIdx.x == 0) part[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_top(uint32_t* __restrict__ part, int nparts, uint32_t* __restrict__ total_out) {
-    // single block; nparts <= SCAN_THREADS * SCAN_ITEMS
+// Single-pass exclusive scan (chained, decoupled look-back): blocks claim
+// 4096-element tiles in order through an atomic counter, publish their
+// aggregate, then look back over predecessors' published aggregates /
+// inclusive prefixes (status word: 2 flag bits << 32 | value).
+constexpr unsigned long long SC_AGG = 1ull << 32, SC_INC = 2ull << 32;
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const uint32_t* __restrict__ in, int n,
+                                                              uint32_t* __restrict__ out, uint32_t* __restrict__ total_out,
+                                                              unsigned int* __restrict__ counter,
+                                                              unsigned long long* __restrict__ status) {
+    __shared__ int tile_s;
+    __shared__ uint32_t prefix_s;
+    if (threadIdx.x == 0) tile_s = (int)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int tile = tile_s;
+    const long long base = (long long)tile * SCAN_TILE + (long long)threadIdx.x * SCAN_ITEMS;
     uint32_t v[SCAN_ITEMS];
-    uint32_t s = 0;
+    uint32_t sum = 0;
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
-        int j = threadIdx.x * SCAN_ITEMS + i;
-        v[i] = j < nparts ? part[j] : 0;
-        s += v[i];
+        const long long j = base + i;
+        v[i] = j < n ? in[j] : 0u;
+        sum += v[i];
     }
     uint32_t ex;
-    uint32_t tot = block_excl_scan(s, ex);
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        int j = threadIdx.x * SCAN_ITEMS + i;
-        if (j < nparts) part[j] = ex;
-        ex += v[i];
+    const uint32_t agg = block_excl_scan(sum, ex);
+    if (threadIdx.x == 0) {
+        volatile unsigned long long* st = status;
+        uint32_t prefix = 0;
+        if (tile == 0) {
+            atomicExch(&status[0], SC_INC | agg);
+        } else {
+            atomicExch(&status[tile], SC_AGG | agg);
+            for (int j = tile - 1; j >= 0; --j) {
+                unsigned long long w;
+                do {
+                    w = st[j];
+                } while ((w >> 32) == 0);
+                prefix += (uint32_t)w;
+                if ((w >> 32) == 2) break;
+            }
+            atomicExch(&status[tile], SC_INC | (unsigned long long)(prefix + agg));
+        }
+        prefix_s = prefix;
+        if ((long long)(tile + 1) * SCAN_TILE >= n) *total_out = prefix + agg;
     }
-    if (threadIdx.x == 0) *total_out = tot;
-}
-
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const uint32_t* __restrict__ in, int n, const uint32_t* __restrict__ part,
-                                                             uint32_t* __restrict__ out) {
-    // blocked arrangement: thread t owns SCAN_ITEMS consecutive elements
-    long long base = (long long)blockIdx.x * SCAN_TILE + (long long)threadIdx.x * SCAN_ITEMS;
-    uint32_t v[SCAN_ITEMS];
-    uint32_t s = 0;
+    __syncthreads();
+    ex += prefix_s;
 #pragma unroll
     for (int i = 0; i < SCAN_ITEMS; ++i) {
-        long long j = base + i;
-        v[i] = j < n ? in[j] : 0;
-        s += v[i];
-    }
-    uint32_t ex;
-    block_excl_scan(s, ex);
-    ex += part[blockIdx.x];
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        long long j = base + i;
+        const long long j = base + i;
         if (j < n) out[j] = ex;
         ex += v[i];
     }
@@ -455,7 +453,8 @@ int rfs_project(int n, const float* means, const float* quats, const float* log_
     return RFS_OK;
 }
 
-size_t rfs_scan_temp_elems(int n) { return (size_t)rfs_ceil_div(n > 0 ? n : 1, SCAN_TILE) + 1; }
+// temp (u32 elements): a claim counter and one 64-bit status word per tile
+size_t rfs_scan_temp_elems(int n) { return 2 + 2 * ((size_t)rfs_ceil_div(n > 0 ? n : 1, SCAN_TILE) + 1); }
 
 int rfs_exclusive_scan_u32(const uint32_t* in, int n, uint32_t* out, uint32_t* total, uint32_t* temp, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -463,11 +462,10 @@ int rfs_exclusive_scan_u32(const uint32_t* in, int n, uint32_t* out, uint32_t* t
         RFS_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(uint32_t), st));
         return RFS_OK;
     }
-    int nb = rfs_ceil_div(n, SCAN_TILE);
-    if (nb > SCAN_THREADS * SCAN_ITEMS) return RFS_ERR_CAPACITY;
-    k_scan_partials<<<nb, SCAN_THREADS, 0, st>>>(in, n, temp);
-    k_scan_top<<<1, SCAN_THREADS, 0, st>>>(temp, nb, total);
-    k_scan_final<<<nb, SCAN_THREADS, 0, st>>>(in, n, temp, out);
+    const int nb = rfs_ceil_div(n, SCAN_TILE);
+    RFS_CUDA_TRY(cudaMemsetAsync(temp, 0, rfs_scan_temp_elems(n) * sizeof(uint32_t), st));
+    k_scan_onepass<<<nb, SCAN_THREADS, 0, st>>>(in, n, out, total, (unsigned int*)temp,
+                                                (unsigned long long*)(temp + 2));
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
