@@ -20,8 +20,8 @@ template <int L>
 __global__ void __launch_bounds__(256) k_psi(int n, int nb, const float* __restrict__ means,
                                              const float2* __restrict__ coeffs, const float* __restrict__ tx,
                                              float2* __restrict__ psi) {
-    const int b = blockIdx.x * 64 + threadIdx.x;
-    const int g = blockIdx.y * 4 + threadIdx.y;
+    const int b = blockIdx.y * 64 + threadIdx.x;
+    const int g = blockIdx.x * 4 + threadIdx.y;  // Gaussians on grid x (y is limited to 65535)
     if (b >= nb || g >= n) return;
     float rx = tx[3 * b] - means[3 * g];
     float ry = tx[3 * b + 1] - means[3 * g + 1];
@@ -179,7 +179,7 @@ __global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, const 
 
 template <int L>
 void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, float2* psi, cudaStream_t st) {
-    dim3 grid(rfs_ceil_div(nb, 64), rfs_ceil_div(n, 4));
+    dim3 grid(rfs_ceil_div(n, 4), rfs_ceil_div(nb, 64));
     k_psi<L><<<grid, dim3(64, 4), 0, st>>>(n, nb, means, coeffs, tx, psi);
 }
 

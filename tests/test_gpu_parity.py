@@ -280,3 +280,19 @@ def test_slow_path_bitwise_equals_ring_path():
     ref = oracle.render_complex_frame(s, default_txs(2, seed=3)[0])
     P, Pr = np.abs(out[64][0][0]) ** 2, np.abs(ref) ** 2
     assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= 1e-4
+
+
+@pytest.mark.gpu
+def test_psi_large_scene_grid():
+    """psi for > 262,140 Gaussians (the launch grid must not overflow a 65,535 dimension)
+    vs the oracle's directional response (render.py:229-238)."""
+    import torch
+
+    s = round_to_f32(bench_scene(np.random.default_rng(21), 300_000, 36, 18))
+    ds = raster.DeviceScene.from_host(s, "cuda")
+    tx = default_txs(2, seed=4)
+    psi = raster.compute_psi(ds, torch.as_tensor(tx, dtype=torch.float32, device="cuda")).cpu().numpy()
+    oc = oracle.OracleContext(s)
+    oc.set_tx(tx[1])
+    ref = oc.psi
+    assert np.max(np.abs(psi[:, 1] - ref)) <= 1e-4 * np.max(np.abs(ref))
