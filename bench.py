@@ -175,7 +175,7 @@ def run_ours(args):
 
     # fixed synthetic upstream: lambda = upstream_to_ray(dL1/dP, S), target 1.3 P + 0.05
     geo = raster.build_geometry(ds, sort_backend=args.sort)
-    S0 = raster.forward(geo, raster.compute_psi(ds, tx))
+    S0 = raster.forward(geo, raster.compute_psi(ds, tx, geo.used))
     P0 = S0.abs() ** 2
     lam = (2.0 * torch.sign(P0 - (1.3 * P0 + 0.05)) / P0[0].numel() * S0).to(torch.complex64).contiguous()
     gt_frames = (1.3 * P0 + 0.05).to(torch.float32).contiguous()  # measured spectra of the e2e training step
@@ -186,7 +186,7 @@ def run_ours(args):
     del S0, P0
     # spectrum loss alone (not part of `value`): timed separately
     from paper_2502_01826_b200 import loss as _loss
-    S1 = raster.forward(geo, raster.compute_psi(ds, tx))
+    S1 = raster.forward(geo, raster.compute_psi(ds, tx, geo.used))
     for _ in range(3):
         _loss.spectrum_loss_frames(S1, gt_frames)
     torch.cuda.synchronize()

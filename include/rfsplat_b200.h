@@ -102,19 +102,23 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream);
  * else 48 entries, 64-thread blocks).  stats (device
  * int[8]): [0] rays needing rfs_hits_slow (listed in slow_list), [1] rays
  * with live > hcap (caller must retry with larger hcap), [2] max live,
- * [3] total live hits, [4] longest tile list, [5] largest pending set. */
+ * [3] total live hits, [4] longest tile list, [5] largest pending set.
+ * used (nullable u8[n], zeroed here): 1 for every Gaussian with a live hit. */
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
-             int pcap, void* slab, int* counts, int* slow_list, int* stats, void* stream);
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, void* stream);
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
-                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, void* stream);
+                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, uint8_t* used, void* stream);
 
-/* K5: psi[g][b] = sum_k coeffs[g][k] * basis_k(bearing of tx_b from mu_g).
+/* K5: psi[g][b] = sum_k coeffs[g][k] * basis_k(bearing of tx_b from mu_g);
+ * with used (nullable, rfs_hits' u8 marks) only rows of Gaussians with live
+ * hits -- the only rows K7 / K8 read -- are computed.
  * Replaces render.py:229-238 + fle.fle_basis_with_derivs (fle.py:153-212). */
-int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, void* psi,
-            void* stream);
+int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const uint8_t* used,
+            void* psi, void* stream);
+
 
 /* K7: S[b][r] = sum over live hits of w * T * psi[g][b].  Replaces the
  * composite of forward_tiled (_kernels.py:184-192) for a TX batch. */

@@ -36,10 +36,10 @@ _SIGS = {
     "rfs_tile_ranges": (i32, [vp, i32, vp, i32, vp, vp]),
     "rfs_lower_bounds": (i32, [vp, i32, vp, vp, vp, vp]),
     "rfs_ray_dirs": (i32, [i32, i32, vp, vp]),
-    "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp]),
+    "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i32, vp]),
     "rfs_hits_slow": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, vp, vp, vp, vp, vp, i32,
-                            vp, vp]),
-    "rfs_psi": (i32, [i32, i32, i32, vp, vp, vp, vp, vp]),
+                            vp, vp, vp]),
+    "rfs_psi": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "rfs_forward": (i32, [vp, vp, i32, vp, i32, i32, i32, vp, vp]),
     "rfs_lam_transpose": (i32, [vp, i32, i32, vp, vp]),
     "rfs_bwd_part_elems": (sz, [i32, i32]),

@@ -125,7 +125,7 @@ def render_complex_frames(scene, txs, ctx: RenderContextGPU | None = None) -> np
     """Complex frames for a TX batch, shape (B, n_az, n_el)."""
     ctx = ctx or prepare_context(scene)
     tx = _tx_tensor(txs, ctx.scene.means.device)
-    psi = raster.compute_psi(ctx.scene, tx)
+    psi = raster.compute_psi(ctx.scene, tx, ctx.geometry.used)
     return raster.forward(ctx.geometry, psi).cpu().numpy().astype(np.complex128)
 
 

@@ -16,13 +16,16 @@ namespace {
 
 // ------------------------------------------------------------------ K5: psi
 // block (64 TX, 4 Gaussians); a Gaussian's coefficient row is an L1 broadcast
+// used (nullable): Gaussians with at least one live hit (marked by K6); the
+// rows of the others are never read by K7 / K8c and are left unwritten.
 template <int L>
 __global__ void __launch_bounds__(256) k_psi(int n, int nb, const float* __restrict__ means,
                                              const float2* __restrict__ coeffs, const float* __restrict__ tx,
-                                             float2* __restrict__ psi) {
+                                             const uint8_t* __restrict__ used, float2* __restrict__ psi) {
     const int b = blockIdx.y * 64 + threadIdx.x;
     const int g = blockIdx.x * 4 + threadIdx.y;  // Gaussians on grid x (y is limited to 65535)
     if (b >= nb || g >= n) return;
+    if (used && !used[g]) return;
     float rx = tx[3 * b] - means[3 * g];
     float ry = tx[3 * b + 1] - means[3 * g + 1];
     float rz = tx[3 * b + 2] - means[3 * g + 2];
@@ -178,27 +181,28 @@ __global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, const 
 }
 
 template <int L>
-void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, float2* psi, cudaStream_t st) {
+void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, const uint8_t* used,
+                float2* psi, cudaStream_t st) {
     dim3 grid(rfs_ceil_div(n, 4), rfs_ceil_div(nb, 64));
-    k_psi<L><<<grid, dim3(64, 4), 0, st>>>(n, nb, means, coeffs, tx, psi);
+    k_psi<L><<<grid, dim3(64, 4), 0, st>>>(n, nb, means, coeffs, tx, used, psi);
 }
 
 }  // namespace
 
 extern "C" {
 
-int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, void* psi,
-            void* stream) {
+int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const uint8_t* used,
+            void* psi, void* stream) {
     if (n <= 0 || n_tx <= 0) return RFS_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const float2* c = (const float2*)coeffs;
     float2* p = (float2*)psi;
     switch (degree) {
-        case 0: launch_psi<0>(n, n_tx, means, c, tx, p, st); break;
-        case 1: launch_psi<1>(n, n_tx, means, c, tx, p, st); break;
-        case 2: launch_psi<2>(n, n_tx, means, c, tx, p, st); break;
-        case 3: launch_psi<3>(n, n_tx, means, c, tx, p, st); break;
-        case 4: launch_psi<4>(n, n_tx, means, c, tx, p, st); break;
+        case 0: launch_psi<0>(n, n_tx, means, c, tx, used, p, st); break;
+        case 1: launch_psi<1>(n, n_tx, means, c, tx, used, p, st); break;
+        case 2: launch_psi<2>(n, n_tx, means, c, tx, used, p, st); break;
+        case 3: launch_psi<3>(n, n_tx, means, c, tx, used, p, st); break;
+        case 4: launch_psi<4>(n, n_tx, means, c, tx, used, p, st); break;
         default: return RFS_ERR_SHAPE;
     }
     RFS_LAUNCH_CHECK();

@@ -113,11 +113,12 @@ struct Ray {
 
 // Emit one hit in sorted order: terminate, record, advance T (_kernels.py:186-191).
 __device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, float w, const RfsGeom* __restrict__ geom,
-                                         RfsHit* __restrict__ slab_ray, int hcap) {
+                                         RfsHit* __restrict__ slab_ray, int hcap, uint8_t* __restrict__ used) {
     if (st.tre * st.tre + st.tim * st.tim < RFS_TERM_EPS2) {
         st.done = true;
         return;
     }
+    if (used) used[g] = 1;  // Gaussian has a live hit: its psi row is needed
     if (st.live < hcap) {
         RfsHit h;
         h.g = g;
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(NT) k_hits(
     const float4* __restrict__ sph, const float4* __restrict__ whit, const RfsGeom* __restrict__ geom,
     const double* __restrict__ dirs, double rx0, double rx1, double rx2, double min_t, int n_az, int n_el,
     int tiles_u, int hcap, RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ slow_list,
-    int* __restrict__ stats) {
+    int* __restrict__ stats, uint8_t* __restrict__ used) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HitsSmem<PCAP, NT, CH>& S = *reinterpret_cast<HitsSmem<PCAP, NT, CH>*>(smem_raw);
     constexpr int PARTS = 256 / NT;
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(NT) k_hits(
             }
             // 4. emit every pending hit that precedes all later candidates
             while (!st.done && head_t < lb_next) {
-                emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap);
+                emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
                 head = (head + 1) & (PCAP - 1);
                 --npend;
                 head_t = npend > 0 ? S.pt[head][tid] : DINF;
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(NT) k_hits(
     }
     // drain (also covers rays whose tile list ended with pending hits)
     while (!st.done && npend > 0) {
-        emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap);
+        emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
         head = (head + 1) & (PCAP - 1);
         --npend;
     }
@@ -394,7 +395,8 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
                             const RfsGeom* __restrict__ geom, const double* __restrict__ dirs, double rx0, double rx1,
                             double rx2, double min_t, int n_az, int n_el, int tiles_u, int hcap,
                             RfsHit* __restrict__ slab, int* __restrict__ counts, double* __restrict__ pt,
-                            uint32_t* __restrict__ pg, float* __restrict__ pw, int pcap, int* __restrict__ stats) {
+                            uint32_t* __restrict__ pg, float* __restrict__ pw, int pcap, int* __restrict__ stats,
+                            uint8_t* __restrict__ used) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_rays) return;
     const int r = rays[i];
@@ -421,7 +423,7 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
     for (int j = rg.x; j < rg.y && !st.done; ++j) {
         const double lbj = lb[j];
         while (npend > 0 && my_t[head] < lbj) {
-            emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap);
+            emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap, used);
             ++head;
             --npend;
             if (st.done) break;
@@ -451,7 +453,7 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
         ++npend;
     }
     while (!st.done && npend > 0) {
-        emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap);
+        emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap, used);
         ++head;
         --npend;
     }
@@ -484,7 +486,8 @@ __global__ void k_ray_dirs(int n_az, int n_el, double* __restrict__ dirs) {
 template <int PCAP, int NT, int CH>
 int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const double* lb, const void* sph,
                 const void* whit, const void* geom, const double* dirs, const double* rx, double min_t, int n_az,
-                int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, cudaStream_t st) {
+                int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used,
+                cudaStream_t st) {
     static bool attr = false;
     size_t smem = sizeof(HitsSmem<PCAP, NT, CH>);
     if (!attr) {
@@ -494,7 +497,7 @@ int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const doub
     }
     k_hits<PCAP, NT, CH><<<n_tiles * (256 / NT), NT, smem, st>>>(
         (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom, dirs, rx[0],
-        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats);
+        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used);
     return RFS_OK;
 }
 
@@ -515,8 +518,9 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
 // for dense scenes.
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
-             int pcap, void* slab, int* counts, int* slow_list, int* stats, void* stream) {
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    if (used && n > 0) RFS_CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)n, st));
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     RFS_CUDA_TRY(cudaMemsetAsync(stats, 0, 8 * sizeof(int), st));
     RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)n_az * n_el, st));
@@ -524,13 +528,13 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
     int rc;
     if (pcap <= 16)
         rc = launch_hits<16, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
     else if (pcap <= 32)
         rc = launch_hits<32, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
     else
         rc = launch_hits<64, 32, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
     if (rc != RFS_OK) return rc;
     k_max_range<<<rfs_ceil_div(n_tiles, 256), 256, 0, st>>>((const int2*)ranges, n_tiles, stats + 4);
     RFS_LAUNCH_CHECK();
@@ -540,13 +544,13 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
-                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, void* stream) {
+                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, uint8_t* used, void* stream) {
     if (n_rays <= 0) return RFS_OK;
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     k_hits_slow<<<rfs_ceil_div(n_rays, 64), 64, 0, (cudaStream_t)stream>>>(
         rays, n_rays, (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom,
         dirs, rx[0], rx[1], rx[2], ress_radius, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, pend_t, pend_g,
-        pend_w, pcap, stats);
+        pend_w, pcap, stats, used);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -124,6 +124,7 @@ class Geometry:
     gidx: dict | None = None             # by-Gaussian hit index (built on first backward)
     psi: torch.Tensor | None = None      # psi of build_geometry(psi_tx=...)
     S: torch.Tensor | None = None        # forward of build_geometry(psi_tx=..., forward=True)
+    used: torch.Tensor | None = None     # u8 [N]: Gaussian has a live hit (psi rows needed)
     after_result: object = None          # return value of build_geometry(after_forward=...)
 
     @property
@@ -307,9 +308,6 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         status_h.copy_(status, non_blocking=True)
         ev_m = torch.cuda.Event()
         ev_m.record()
-        if psi_tx is not None:  # independent work queued behind the M read
-            psi = compute_psi(scene, psi_tx)
-            _mark(marks, "psi")
         _spin(ev_m)  # read #1: error flags and M
         host = status_h.tolist()
         if int(host[0]) & (1 << 1):
@@ -317,9 +315,6 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         m = int(host[1]) & 0xFFFFFFFF
         ckeys, vals, ranges, lb = bin_tiles(m, False)
     else:
-        if psi_tx is not None:
-            psi = compute_psi(scene, psi_tx)
-            _mark(marks, "psi")
         ckeys, vals, ranges, lb = bin_tiles(m_cap, True)
 
     hc = 1 << max(0, math.ceil(math.log2(max(int(hcap or _CAPS["hcap"]), 1))))  # power of two: slot >> log2(hcap) = ray
@@ -331,17 +326,21 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     S = None
     early = None
     redo_forward = False
+    used = torch.empty(nn, dtype=torch.uint8, device=dev)
     while True:
         slab = torch.empty(R * hc * 16, dtype=torch.uint8, device=dev)
         _native.call("rfs_hits", _ptr(ranges), n_tiles, _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit), _ptr(geom),
                      _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, pc, _ptr(slab), _ptr(ray_counts),
-                     _ptr(slow), _ptr(stats), st)
+                     _ptr(slow), _ptr(stats), _ptr(used), n, st)
         _mark(marks, "hits")
         stats_h.copy_(stats, non_blocking=True)
         if m_cap is not None:
             status_h.copy_(status, non_blocking=True)
         ev_s = torch.cuda.Event()
         ev_s.record()
+        if psi_tx is not None and psi is None:  # psi of the Gaussians with live hits only (K6 marks them)
+            psi = compute_psi(scene, psi_tx, used)
+            _mark(marks, "psi")
         if forward and psi is not None and S is None:  # queued behind the statistics read
             S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
             _mark(marks, "forward")
@@ -379,7 +378,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             pw = torch.empty(nr * pcap, dtype=torch.float32, device=dev)
             _native.call("rfs_hits_slow", _ptr(slow), nr, _ptr(ranges), _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit),
                          _ptr(geom), _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, _ptr(slab),
-                         _ptr(ray_counts), _ptr(pt), _ptr(pg), _ptr(pw), pcap, _ptr(stats), st)
+                         _ptr(ray_counts), _ptr(pt), _ptr(pg), _ptr(pw), pcap, _ptr(stats), _ptr(used), st)
             s2 = stats.cpu().tolist()
             s[1], s[2], s[3] = s2[1], s2[2], s2[3]
             redo_forward = True
@@ -393,7 +392,10 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         _CAPS.setdefault("m_cap", {}).setdefault((n, n_az, n_el), m + m // 8 + 1024)
     geo = Geometry(n, n_az, n_el, tiles_u, tiles_v, m, geom, rho32, dirs, ckeys[:max(m, 0)], vals[:max(m, 0)],
                    ranges, hc, slab, ray_counts, s, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
+    if psi_tx is not None and redo_forward:  # the hit lists changed: new used set
+        psi = compute_psi(scene, psi_tx, used)
     geo.psi = psi
+    geo.used = used
     if forward and psi is not None:
         if S is None or redo_forward:
             S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
@@ -419,14 +421,15 @@ def _check_tx(tx: torch.Tensor) -> torch.Tensor:
     return tx.to(dtype=torch.float32).contiguous()
 
 
-def compute_psi(scene: DeviceScene, tx: torch.Tensor) -> torch.Tensor:
-    """K5: psi [N, B] complex64."""
+def compute_psi(scene: DeviceScene, tx: torch.Tensor, used: torch.Tensor | None = None) -> torch.Tensor:
+    """K5: psi [N, B] complex64; with `used` (u8 [N], Geometry.used) only the
+    rows of Gaussians with live hits are computed -- the only rows K7 / K8c read."""
     tx = _check_tx(tx)
     b = int(tx.shape[0])
     psi = torch.empty((scene.n, b), dtype=torch.complex64, device=scene.means.device)
     if scene.n and b:
         _native.call("rfs_psi", scene.n, b, scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs), _ptr(tx),
-                     _ptr(psi), _stream())
+                     _ptr(used), _ptr(psi), _stream())
     return psi
 
 
@@ -556,7 +559,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         c1 = min(b, c0 + MAX_TX_PER_LAUNCH)
         nbc = c1 - c0
         txc = tx[c0:c1].contiguous()
-        psic = psi if (psi is not None and c0 == 0 and c1 == b) else compute_psi(scene, txc)
+        psic = psi if (psi is not None and c0 == 0 and c1 == b) else compute_psi(scene, txc, geo.used)
         if lamT is not None and c0 == 0 and c1 == b:
             lamTc = lamT
         else:

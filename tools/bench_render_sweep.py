@@ -37,7 +37,7 @@ def sweep(marks):
     e1 = ev(); e1.record()
     out = torch.empty((a.tx, 360, 180), dtype=torch.complex64, device="cuda")  # every spectrum kept
     for c in range(0, a.tx, a.chunk):
-        psi = raster.compute_psi(ds, txs[c:c + a.chunk])
+        psi = raster.compute_psi(ds, txs[c:c + a.chunk], geo.used)
         out[c:c + a.chunk] = raster.forward(geo, psi)
     e2 = ev(); e2.record()
     marks.append((e0, e1, e2, geo))
