@@ -45,6 +45,14 @@ del tds, g
 
 ds = raster.DeviceScene.from_host(s0, "cuda")
 cfg = train.TrainConfig(iterations=a.iterations, densify_grad_threshold=a.threshold)
+# warm-up of the density-control kernels and allocator sizes on a throwaway copy
+_w = raster.DeviceScene.from_host(s0, "cuda")
+_st = train.TrainState.zeros(_w.n, "cuda")
+_st.grad_ema.fill_(1.0)
+train.densify(_w, _st, 1, cfg, 0)
+train.prune(_w, _st, 1, cfg)
+del _w, _st
+torch.cuda.synchronize()
 tim = []
 trace, dens, pr = train.train_loop(ds, txs, frames, cfg, batch=a.batch, seed=1, timings=tim)
 warm = 5
