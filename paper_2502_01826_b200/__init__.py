@@ -12,6 +12,9 @@ Public API:
     raster.*                                device-level pipeline (raster.py)
     scene.HostScene, bench_scene, random_scene, cube_init
     parallel.*                              TX-sharded data parallelism (parallel.py)
+    loss.*                                  spectrum / scalar losses on the device (loss.py)
+    train.*                                 SGD, density control, training loop on the device (train.py)
+    io.*                                    dataset / checkpoint formats, device dataset loading (io.py)
 
 Importing the package does not need a GPU; calling any compute entry point
 without the built library or a CUDA device raises NativeLibraryError.
@@ -32,7 +35,7 @@ def __getattr__(name):
         from . import autograd
 
         return getattr(autograd, name)
-    if name in ("api", "raster", "autograd", "parallel"):
+    if name in ("api", "raster", "autograd", "parallel", "loss", "train", "io"):
         import importlib
 
         return importlib.import_module(f".{name}", __name__)
