@@ -263,9 +263,9 @@ def run_ours(args):
     traffic = load_traffic()
     kern = {
         "K7 forward composite (k_forward_v)": (ab["forward"], ph_ms.get("forward"), ("k_forward_v",)),
-        "K8 backward composite (k_lam_transpose + k_bwd_gauss_v + k_bwd_pfix + k_bwd_rays)":
+        "K8 backward composite (k_lam_transpose + k_bwd_gauss_v + k_bwd_rays)":
             (ab["backward"], ph_ms.get("backward_tx", 0) + ph_ms.get("backward_rays", 0),
-             ("k_lam_transpose", "k_bwd_gauss_v", "k_bwd_pfix", "k_bwd_rays")),
+             ("k_lam_transpose", "k_bwd_gauss_v", "k_bwd_rays")),
         "K9 epilogue (k_grad_tx || k_geom_seg + k_geom_fix + k_geom_final)":
             (ab["epilogue"], ph_ms.get("grad_geom", 0), ("k_grad_tx", "k_geom_seg", "k_geom_fix", "k_geom_final")),
     }
