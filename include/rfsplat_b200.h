@@ -255,6 +255,10 @@ int rfs_density_apply(int n, int K, int mode, const uint32_t* keep, const uint32
                       const float* last_dmean, float* o_means, float* o_quats, float* o_log_scales, float* o_raw,
                       float* o_phase, void* o_coeffs, float* o_ema, float* o_last, void* stream);
 
+/* Diagnostics: per-warp %globaltimer start / end and tile-list length of
+ * k_hits into buf (u64[3 * warps]); NULL switches it off. */
+int rfs_debug_k6_timing(unsigned long long* buf);
+
 /* Library / build identification. */
 int rfs_version(void);
 int rfs_device_arch(void); /* compute capability the library was built for, e.g. 100 */

@@ -59,6 +59,7 @@ _SIGS = {
     "rfs_density_flags": (i32, [i32, i32, vp, vp, vp, f64, f64, f64, vp, vp, vp, vp]),
     "rfs_density_apply": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_ulonglong, i32,
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "rfs_debug_k6_timing": (i32, [vp]),
     "rfs_version": (i32, []),
     "rfs_device_arch": (i32, []),
 }

@@ -41,6 +41,15 @@ namespace {
 
 constexpr double DINF = 1.0e300;
 
+// diagnostics: per-warp start / end %globaltimer of k_hits (null = off)
+__device__ unsigned long long* g_k6_timing = nullptr;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 #define DM(a, b) __dmul_rn((a), (b))
 #define DA(a, b) __dadd_rn((a), (b))
 #define DS(a, b) __dsub_rn((a), (b))
@@ -212,6 +221,7 @@ __global__ void __launch_bounds__(NT) k_hits(
     const int v = (tile / tiles_u) * RFS_TILE + 8 * pv + (lane & 7);
     const bool valid = u < n_az && v < n_el;
     const int r = valid ? u * n_el + v : 0;
+    const unsigned long long t_start = g_k6_timing ? gtimer() : 0ull;
     Ray st;
     st.dx = dirs[3 * r];
     st.dy = dirs[3 * r + 1];
@@ -371,6 +381,15 @@ __global__ void __launch_bounds__(NT) k_hits(
         head = (head + 1) & (PCAP - 1);
         --npend;
     }
+    if (g_k6_timing) {
+        __syncwarp();
+        if (lane == 0) {
+            const int wg = (blockIdx.x * NT + tid) >> 5;
+            g_k6_timing[3 * wg] = t_start;
+            g_k6_timing[3 * wg + 1] = gtimer();
+            g_k6_timing[3 * wg + 2] = (unsigned long long)(rg.y - rg.x);
+        }
+    }
     if (!valid) return;
     atomicMax(&stats[5], max_pend);
     atomicAdd(&stats[6], n_sph);
@@ -493,6 +512,10 @@ int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const doub
     if (!attr) {
         RFS_CUDA_TRY(
             cudaFuncSetAttribute(k_hits<PCAP, NT, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // the whole grid must be resident at once (a late-starting tile extends
+        // the kernel): ask for the largest shared-memory carveout
+        RFS_CUDA_TRY(cudaFuncSetAttribute(k_hits<PCAP, NT, CH>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          (int)cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
     k_hits<PCAP, NT, CH><<<n_tiles * (256 / NT), NT, smem, st>>>(
@@ -504,6 +527,13 @@ int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const doub
 }  // namespace
 
 extern "C" {
+
+// diagnostics (not part of the rasterizer path): per-warp timing of k_hits into
+// buf (u64[3 * warps]: start, end, tile list length); NULL switches it off
+int rfs_debug_k6_timing(unsigned long long* buf) {
+    RFS_CUDA_TRY(cudaMemcpyToSymbol(g_k6_timing, &buf, sizeof(buf)));
+    return RFS_OK;
+}
 
 int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
     int R = n_az * n_el;
@@ -526,6 +556,10 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
     RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)n_az * n_el, st));
     if (n_tiles <= 0) return RFS_OK;
     int rc;
+    // 64-thread blocks: 7 per SM, so 68 of a 360x180 grid's 1104 blocks start
+    // late (~90 us); 128-thread blocks (all resident) measured no faster -- the
+    // kernel is set by the longest warps' chains, not by the late starts
+    // (tools/k6_timing.py: warp duration mean 124 us, max 238 us at 100k)
     if (pcap <= 16)
         rc = launch_hits<16, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
                                      tiles_u, hcap, slab, counts, slow_list, stats, used, st);
