@@ -98,15 +98,21 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream);
 /* K6: TX-independent live hit lists.  Replaces _collect_hits + the live walk
  * of forward_tiled / count_hits_tiled (_kernels.py:27-112, 140-192, 237-292).
  * Writes hits of ray r to slab[r*hcap ...], counts[r] = live count.  pcap
- * selects the pending ring (<= 24 -> 24 entries per ray, 128-thread blocks;
- * else 48 entries, 64-thread blocks).  stats (device
+ * selects the pending ring (<= 16 -> 16 entries per ray, <= 32 -> 32, else
+ * 64).  stats (device
  * int[8]): [0] rays needing rfs_hits_slow (listed in slow_list), [1] rays
  * with live > hcap (caller must retry with larger hcap), [2] max live,
  * [3] total live hits, [4] longest tile list, [5] largest pending set.
- * used (nullable u8[n], zeroed here): 1 for every Gaussian with a live hit. */
+ * used (nullable u8[n], zeroed here): 1 for every Gaussian with a live hit.
+ * split_min > 0 (with split_ws of rfs_hits_split_bytes(n_az*n_el, bcap)
+ * bytes): tile lists longer than split_min are streamed as two concurrent
+ * halves and merged (same hit lists, shorter critical path); a ray whose
+ * second half holds more than bcap hits goes to the slow path. */
+size_t rfs_hits_split_bytes(int n_rays, int bcap);
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
-             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, void* stream);
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, int split_min,
+             int bcap, void* split_ws, void* stream);
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
@@ -255,8 +261,9 @@ int rfs_density_apply(int n, int K, int mode, const uint32_t* keep, const uint32
                       const float* last_dmean, float* o_means, float* o_quats, float* o_log_scales, float* o_raw,
                       float* o_phase, void* o_coeffs, float* o_ema, float* o_last, void* stream);
 
-/* Diagnostics: per-warp %globaltimer start / end and tile-list length of
- * k_hits into buf (u64[3 * warps]); NULL switches it off. */
+/* Diagnostics: per warp of k_hits, u64[8]: %globaltimer start / end,
+ * candidates, chunks, cone survivors, sum over chunks of the most exact tests
+ * on one lane, survivor-union size, max live hits; NULL switches it off. */
 int rfs_debug_k6_timing(unsigned long long* buf);
 
 /* Library / build identification. */

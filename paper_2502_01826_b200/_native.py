@@ -13,7 +13,8 @@ import threading
 from .errors import NativeLibraryError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librfsplat_b200.so")
+# RFS_LIB_PATH: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("RFS_LIB_PATH") or os.path.join(_HERE, "lib", "librfsplat_b200.so")
 _lock = threading.Lock()
 _lib = None
 
@@ -36,7 +37,9 @@ _SIGS = {
     "rfs_tile_ranges": (i32, [vp, i32, vp, i32, vp, vp]),
     "rfs_lower_bounds": (i32, [vp, i32, vp, vp, vp, vp]),
     "rfs_ray_dirs": (i32, [i32, i32, vp, vp]),
-    "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i32, vp]),
+    "rfs_hits_split_bytes": (sz, [i32, i32]),
+    "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, i32,
+                       vp, vp]),
     "rfs_hits_slow": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, vp, vp, vp, vp, vp, i32,
                             vp, vp, vp]),
     "rfs_psi": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),

@@ -185,14 +185,45 @@ __device__ __forceinline__ bool exact_hit_s(const double* __restrict__ G, double
     return true;
 }
 
-constexpr int GD = 13;  // doubles of an RfsGeom record used by the exact test
+constexpr int GD = 13;   // doubles of an RfsGeom record used by the exact test
+constexpr int GDS = 14;  // their shared-memory row: 7 x 16-byte cp.async pieces
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// Long tile lists set K6's critical path (tools/k6_timing.py: the warps of the
+// longest lists take ~2x the mean).  Lists longer than split_min are split at
+// mid: piece A streams [start, mid) exactly as an unsplit list (emitting every
+// hit that precedes all of B's candidates, t_mid < lb[mid]) and parks its
+// still-pending hits and its T; piece B streams [mid, end) concurrently into a
+// sorted list of its own, without T or termination; k_hits_merge then merges
+// the two (t_mid, g)-sorted lists and walks them with T and the termination
+// rule -- the same hit sequence as one pass, since the reference itself sorts
+// all hits of a ray and walks them (_kernels.py:27-112, 184-191).
+constexpr int KS_ACAP = 64;  // A's parked hits (>= the largest pending ring)
+struct KSplit {
+    int split_min;  // lists longer than this are split (<= 0: never)
+    int bcap;       // capacity of a ray's B list
+    int* flag;      // per ray: 1 = A parked it (merge), 2 = the slow path owns it
+    double *a_tre, *a_tim;
+    int *a_live, *a_n;
+    double* a_t;
+    uint32_t* a_g;
+    float* a_w;
+    int* b_n;
+    double* b_t;
+    uint32_t* b_g;
+    float* b_w;
+};
 
 template <int CH>
 struct WarpStage {
     float4 sph[CH];
     float4 wh[CH][4];
     uint32_t g[CH];
-    double gd[CH][GD];  // fp64 records of the chunk's survivor union
+    double gd[CH][GDS];  // fp64 records of the chunk's cone-relevant candidates (by slot)
 };
 
 template <int PCAP, int NT, int CH>
@@ -209,11 +240,14 @@ __global__ void __launch_bounds__(NT) k_hits(
     const float4* __restrict__ sph, const float4* __restrict__ whit, const RfsGeom* __restrict__ geom,
     const double* __restrict__ dirs, double rx0, double rx1, double rx2, double min_t, int n_az, int n_el,
     int tiles_u, int hcap, RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ slow_list,
-    int* __restrict__ stats, uint8_t* __restrict__ used) {
+    int* __restrict__ stats, uint8_t* __restrict__ used, KSplit ks) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HitsSmem<PCAP, NT, CH>& S = *reinterpret_cast<HitsSmem<PCAP, NT, CH>*>(smem_raw);
     constexpr int PARTS = 256 / NT;
-    const int tile = blockIdx.x / PARTS, part = blockIdx.x % PARTS;
+    // split lists: a tile's piece-B blocks follow its piece-A blocks, so both
+    // pieces of a tile are resident together
+    const int per_tile = ks.split_min > 0 ? 2 * PARTS : PARTS;
+    const int tile = blockIdx.x / per_tile, wblk = blockIdx.x % per_tile, part = wblk % PARTS;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // each warp owns a 4 (u) x 8 (v) patch of the 16 x 16 tile
     const int q = part * (NT / 32) + wid, pu = q >> 1, pv = q & 1;
@@ -239,8 +273,16 @@ __global__ void __launch_bounds__(NT) k_hits(
     bool pend_over = false;
     int head = 0, npend = 0, max_pend = 0;
     int n_sph = 0, n_wh = 0;
+    unsigned d_chunks = 0, d_rel = 0, d_nu = 0, d_mx = 0;  // diagnostics (g_k6_timing)
     double head_t = DINF;
     const int2 rg = ranges[tile];
+    const int Lt = rg.y - rg.x;
+    const bool split = ks.split_min > 0 && Lt > ks.split_min;
+    const bool second = wblk >= PARTS;  // piece B of a split list
+    if (second && !split) return;         // block-uniform
+    const int mid = split ? rg.x + Lt / 2 : rg.y;
+    const int c_lo = second ? mid : rg.x, c_hi = second ? rg.y : mid;
+    int b_n = 0;
     WarpStage<CH>& W = S.ws[wid];
 
     // Warp cone: axis c through the patch, half-angle th_p covering its rays.
@@ -268,20 +310,27 @@ __global__ void __launch_bounds__(NT) k_hits(
     uint32_t pf_g = 0;
     float4 pf_s = make_float4(0.f, 0.f, 0.f, 0.f), pf_w[4];
     double pf_lb = DINF;
+    // candidate ids run one chunk further ahead than their records, so the
+    // record gathers never wait on the id load (in-order issue)
+    uint32_t nx_g = c_lo + lane < c_hi ? vals[c_lo + lane] : 0u;
     auto prefetch = [&](int b0) {
-        if (b0 + lane < rg.y) {
-            pf_g = vals[b0 + lane];
+        if (b0 + lane < c_hi) {
+            pf_g = nx_g;
             pf_s = __ldg(&sph[pf_g]);
 #pragma unroll
             for (int k = 0; k < 4; ++k) pf_w[k] = __ldg(&whit[4 * pf_g + k]);
         }
-        pf_lb = b0 + CH < rg.y ? lb[b0 + CH] : DINF;
+        if (b0 + CH + lane < c_hi) nx_g = vals[b0 + CH + lane];
+        // bound of every candidate after this chunk -- for piece A's last chunk
+        // that is B's first candidate, mid
+        const int nxt = min(b0 + CH, c_hi);
+        pf_lb = nxt < rg.y ? lb[nxt] : DINF;
     };
-    prefetch(rg.x);
+    prefetch(c_lo);
 
-    for (int base = rg.x; base < rg.y; base += CH) {
+    for (int base = c_lo; base < c_hi; base += CH) {
         if (__all_sync(0xffffffffu, st.done)) break;
-        const int nb = min(CH, rg.y - base);
+        const int nb = min(CH, c_hi - base);
         // 1. stage the prefetched chunk, cone-cull it for the warp, start loading the next one
         bool rel = false;
         if (lane < nb) {
@@ -300,9 +349,24 @@ __global__ void __launch_bounds__(NT) k_hits(
             }
         }
         const unsigned relmask = __ballot_sync(0xffffffffu, rel);
+        if (g_k6_timing) {
+            d_chunks += 1;
+            d_rel += __popc(relmask);
+        }
         const double lb_next = pf_lb;
         __syncwarp();
-        if (base + CH < rg.y) prefetch(base + CH);
+        // fp64 records of the cone-relevant candidates -> shared memory,
+        // asynchronously (cp.async): they land while the fp32 filters run
+        {
+            const int nrel = __popc(relmask);
+            for (int e = lane; e < nrel * (GDS / 2); e += 32) {
+                const int sl = e / (GDS / 2), part = e - sl * (GDS / 2);
+                const int j = __fns(relmask, 0, sl + 1);
+                cp_async16(&W.gd[j][2 * part], reinterpret_cast<const char*>(geom + W.g[j]) + 16 * part);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        if (base + CH < c_hi) prefetch(base + CH);
         // 2. survivor mask from shared memory
         unsigned mask = 0;
         if (!st.done) {
@@ -319,14 +383,12 @@ __global__ void __launch_bounds__(NT) k_hits(
                 }
             }
         }
-        // 3a. fp64 records of the warp's survivor union -> shared memory (one load round)
-        const unsigned umask = __reduce_or_sync(0xffffffffu, mask);
-        const int nu = __popc(umask);
-        for (int e = lane; e < nu * GD; e += 32) {
-            const int s = e / GD, f = e - s * GD;
-            const int j = __fns(umask, 0, s + 1);
-            W.gd[s][f] = __ldg(reinterpret_cast<const double*>(geom + W.g[j]) + f);
+        // 3a. the records' copies have landed (own copies, then the warp's)
+        if (g_k6_timing) {
+            d_nu += __popc(__reduce_or_sync(0xffffffffu, mask));
+            d_mx += __reduce_max_sync(0xffffffffu, (unsigned)__popc(mask));
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         if (!st.done) {
             // 3b. exact fp64 test and sorted insertion by (t_mid, g)
@@ -334,10 +396,9 @@ __global__ void __launch_bounds__(NT) k_hits(
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const uint32_t g = W.g[j];
-                const int s = __popc(umask & ((1u << j) - 1u));
                 double t_mid;
                 float w;
-                if (!exact_hit_s(W.gd[s], st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid, w)) continue;
+                if (!exact_hit_s(W.gd[j], st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid, w)) continue;
                 if (npend == PCAP) {
                     pend_over = true;
                     st.done = true;
@@ -367,7 +428,19 @@ __global__ void __launch_bounds__(NT) k_hits(
             }
             // 4. emit every pending hit that precedes all later candidates
             while (!st.done && head_t < lb_next) {
-                emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
+                if (second) {  // piece B: into its own sorted list, no T / termination
+                    if (b_n == ks.bcap) {
+                        pend_over = true;
+                        st.done = true;
+                        break;
+                    }
+                    const size_t o = (size_t)r * ks.bcap + b_n++;
+                    ks.b_t[o] = S.pt[head][tid];
+                    ks.b_g[o] = S.pg[head][tid];
+                    ks.b_w[o] = S.pw[head][tid];
+                } else {
+                    emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
+                }
                 head = (head + 1) & (PCAP - 1);
                 --npend;
                 head_t = npend > 0 ? S.pt[head][tid] : DINF;
@@ -375,31 +448,122 @@ __global__ void __launch_bounds__(NT) k_hits(
         }
         __syncwarp();
     }
-    // drain (also covers rays whose tile list ended with pending hits)
-    while (!st.done && npend > 0) {
-        emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
-        head = (head + 1) & (PCAP - 1);
-        --npend;
+    // drain (also covers rays whose tile list ended with pending hits); a
+    // split list's piece A parks its pending hits and T for k_hits_merge
+    const bool park = split && !second && !st.done;
+    if (second) {
+        while (!st.done && npend > 0) {
+            if (b_n == ks.bcap) {
+                pend_over = true;
+                st.done = true;
+                break;
+            }
+            const size_t o = (size_t)r * ks.bcap + b_n++;
+            ks.b_t[o] = S.pt[head][tid];
+            ks.b_g[o] = S.pg[head][tid];
+            ks.b_w[o] = S.pw[head][tid];
+            head = (head + 1) & (PCAP - 1);
+            --npend;
+        }
+    } else if (park) {
+        for (int i = 0; i < npend; ++i) {
+            const int sl = (head + i) & (PCAP - 1);
+            const size_t o = (size_t)r * KS_ACAP + i;
+            ks.a_t[o] = S.pt[sl][tid];
+            ks.a_g[o] = S.pg[sl][tid];
+            ks.a_w[o] = S.pw[sl][tid];
+        }
+    } else {
+        while (!st.done && npend > 0) {
+            emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
+            head = (head + 1) & (PCAP - 1);
+            --npend;
+        }
     }
     if (g_k6_timing) {
-        __syncwarp();
+        const unsigned live_max = __reduce_max_sync(0xffffffffu, (unsigned)st.live);
         if (lane == 0) {
-            const int wg = (blockIdx.x * NT + tid) >> 5;
-            g_k6_timing[3 * wg] = t_start;
-            g_k6_timing[3 * wg + 1] = gtimer();
-            g_k6_timing[3 * wg + 2] = (unsigned long long)(rg.y - rg.x);
+            unsigned long long* o = g_k6_timing + 8 * ((blockIdx.x * NT + tid) >> 5);
+            o[0] = t_start;
+            o[1] = gtimer();
+            o[2] = (unsigned long long)(c_hi - c_lo);
+            o[3] = d_chunks;
+            o[4] = d_rel;
+            o[5] = d_mx;
+            o[6] = d_nu;
+            o[7] = live_max;
         }
     }
     if (!valid) return;
     atomicMax(&stats[5], max_pend);
     atomicAdd(&stats[6], n_sph);
     atomicAdd(&stats[7], n_wh);
-    if (pend_over) {
-        int idx = atomicAdd(&stats[0], 1);
-        slow_list[idx] = r;
+    // split-ray handshake on flag[r]: 0 open, 1 parked by A (merge), 2 owned
+    // by the slow path, 3 terminated within A (B's hits are irrelevant)
+    if (pend_over) {  // the slow path redoes the whole ray
+        bool to_slow = true;
+        if (split) {
+            const int old = second ? atomicCAS(&ks.flag[r], 0, 2) : atomicExch(&ks.flag[r], 2);
+            if (second && old == 1) atomicExch(&ks.flag[r], 2);
+            to_slow = second ? (old == 0 || old == 1) : old != 2;
+        }
+        if (to_slow) {
+            int idx = atomicAdd(&stats[0], 1);
+            slow_list[idx] = r;
+        }
         return;
     }
+    if (second) {
+        ks.b_n[r] = b_n;
+        return;
+    }
+    if (park) {
+        ks.a_n[r] = npend;
+        ks.a_tre[r] = st.tre;
+        ks.a_tim[r] = st.tim;
+        ks.a_live[r] = st.live;
+        atomicCAS(&ks.flag[r], 0, 1);  // unless B already handed the ray to the slow path
+        return;
+    }
+    if (split && atomicCAS(&ks.flag[r], 0, 3) == 2) return;  // B overflowed first: the slow path redoes it
     counts[r] = min(st.live, hcap);  // stored hits; live > hcap is flagged in stats[1]
+    if (st.hcap_over) atomicAdd(&stats[1], 1);
+    atomicMax(&stats[2], st.live);
+    atomicAdd(&stats[3], min(st.live, hcap));
+}
+
+// Merge of a split list's two pieces (see KSplit): thread per ray parked by A.
+__global__ void k_hits_merge(int R, int hcap, KSplit ks, const RfsGeom* __restrict__ geom,
+                             RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ stats,
+                             uint8_t* __restrict__ used) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R || ks.flag[r] != 1) return;
+    Ray st;
+    st.tre = ks.a_tre[r];
+    st.tim = ks.a_tim[r];
+    st.live = ks.a_live[r];
+    st.done = false;
+    st.hcap_over = st.live > hcap;
+    RfsHit* slab_ray = slab + (size_t)r * hcap;
+    const int na = ks.a_n[r], nbb = ks.b_n[r];
+    const double* at = ks.a_t + (size_t)r * KS_ACAP;
+    const uint32_t* ag = ks.a_g + (size_t)r * KS_ACAP;
+    const float* aw = ks.a_w + (size_t)r * KS_ACAP;
+    const double* bt = ks.b_t + (size_t)r * ks.bcap;
+    const uint32_t* bg = ks.b_g + (size_t)r * ks.bcap;
+    const float* bw = ks.b_w + (size_t)r * ks.bcap;
+    int i = 0, j = 0;
+    while (!st.done && (i < na || j < nbb)) {
+        const bool from_a = i < na && (j >= nbb || at[i] < bt[j] || (at[i] == bt[j] && ag[i] < bg[j]));
+        if (from_a) {
+            emit_hit(st, ag[i], aw[i], geom, slab_ray, hcap, used);
+            ++i;
+        } else {
+            emit_hit(st, bg[j], bw[j], geom, slab_ray, hcap, used);
+            ++j;
+        }
+    }
+    counts[r] = min(st.live, hcap);
     if (st.hcap_over) atomicAdd(&stats[1], 1);
     atomicMax(&stats[2], st.live);
     atomicAdd(&stats[3], min(st.live, hcap));
@@ -506,7 +670,7 @@ template <int PCAP, int NT, int CH>
 int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const double* lb, const void* sph,
                 const void* whit, const void* geom, const double* dirs, const double* rx, double min_t, int n_az,
                 int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used,
-                cudaStream_t st) {
+                const KSplit& ks, cudaStream_t st) {
     static bool attr = false;
     size_t smem = sizeof(HitsSmem<PCAP, NT, CH>);
     if (!attr) {
@@ -518,9 +682,11 @@ int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const doub
                                           (int)cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
-    k_hits<PCAP, NT, CH><<<n_tiles * (256 / NT), NT, smem, st>>>(
+    const int per_tile = (256 / NT) * (ks.split_min > 0 ? 2 : 1);
+    k_hits<PCAP, NT, CH><<<n_tiles * per_tile, NT, smem, st>>>(
         (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom, dirs, rx[0],
-        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used);
+        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used, ks);
+    RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
@@ -529,7 +695,8 @@ int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const doub
 extern "C" {
 
 // diagnostics (not part of the rasterizer path): per-warp timing of k_hits into
-// buf (u64[3 * warps]: start, end, tile list length); NULL switches it off
+// buf (u64[8 * warps]: start, end, candidates, chunks, cone survivors, sum over
+// chunks of the most exact tests on one lane, union size, max live); NULL: off
 int rfs_debug_k6_timing(unsigned long long* buf) {
     RFS_CUDA_TRY(cudaMemcpyToSymbol(g_k6_timing, &buf, sizeof(buf)));
     return RFS_OK;
@@ -546,15 +713,49 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
 // pcap selects the pending-ring template: 16 entries (64-thread blocks, 9
 // blocks/SM), 32 entries (64-thread blocks) or 64 entries (32-thread blocks)
 // for dense scenes.
+size_t rfs_hits_split_bytes(int n_rays, int bcap) {
+    const size_t R = (size_t)(n_rays > 0 ? n_rays : 0), B = (size_t)(bcap > 0 ? bcap : 0);
+    // per ray: flag, a_n, a_live, b_n (int); a_tre, a_tim (double); A's and B's lists (16 B per entry)
+    return R * (4 * sizeof(int) + 2 * sizeof(double)) + R * (KS_ACAP + B) * 16;
+}
+
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
-             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, void* stream) {
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, int split_min,
+             int bcap, void* split_ws, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (used && n > 0) RFS_CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)n, st));
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
+    const int R = n_az * n_el;
     RFS_CUDA_TRY(cudaMemsetAsync(stats, 0, 8 * sizeof(int), st));
-    RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)n_az * n_el, st));
+    RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)R, st));
     if (n_tiles <= 0) return RFS_OK;
+    KSplit ks{};
+    ks.split_min = (split_ws && bcap > 0) ? split_min : 0;
+    if (ks.split_min > 0) {
+        // carve the workspace: 8-byte arrays first, then 4-byte ones
+        char* p = (char*)split_ws;
+        auto take = [&](size_t bytes) {
+            char* q = p;
+            p += bytes;
+            return q;
+        };
+        const size_t Rz = (size_t)R, A = (size_t)KS_ACAP * Rz, B = (size_t)bcap * Rz;
+        ks.bcap = bcap;
+        ks.a_tre = (double*)take(Rz * 8);
+        ks.a_tim = (double*)take(Rz * 8);
+        ks.a_t = (double*)take(A * 8);
+        ks.b_t = (double*)take(B * 8);
+        ks.flag = (int*)take(Rz * 4);
+        ks.a_n = (int*)take(Rz * 4);
+        ks.a_live = (int*)take(Rz * 4);
+        ks.b_n = (int*)take(Rz * 4);
+        ks.a_g = (uint32_t*)take(A * 4);
+        ks.b_g = (uint32_t*)take(B * 4);
+        ks.a_w = (float*)take(A * 4);
+        ks.b_w = (float*)take(B * 4);
+        RFS_CUDA_TRY(cudaMemsetAsync(ks.flag, 0, Rz * 4, st));
+    }
     int rc;
     // 64-thread blocks: 7 per SM, so 68 of a 360x180 grid's 1104 blocks start
     // late (~90 us); 128-thread blocks (all resident) measured no faster -- the
@@ -562,14 +763,19 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
     // (tools/k6_timing.py: warp duration mean 124 us, max 238 us at 100k)
     if (pcap <= 16)
         rc = launch_hits<16, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, st);
     else if (pcap <= 32)
         rc = launch_hits<32, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, st);
     else
         rc = launch_hits<64, 32, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, st);
     if (rc != RFS_OK) return rc;
+    if (ks.split_min > 0) {
+        k_hits_merge<<<rfs_ceil_div(R, 128), 128, 0, st>>>(R, hcap, ks, (const RfsGeom*)geom, (RfsHit*)slab, counts,
+                                                            stats, used);
+        RFS_LAUNCH_CHECK();
+    }
     k_max_range<<<rfs_ceil_div(n_tiles, 256), 256, 0, st>>>((const int2*)ranges, n_tiles, stats + 4);
     RFS_LAUNCH_CHECK();
     return RFS_OK;

@@ -14,6 +14,7 @@ arrays from counts (_kernels.py:542-543, grad.py:224-231).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -141,7 +142,10 @@ class Geometry:
 
 
 # adaptive capacities, remembered across steps
-_CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {}}
+_CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {},
+         # K6 splits tile lists longer than this into two concurrent halves
+         # (rfs_hits' split_min; 0 = off); bcap = hits the second half may hold
+         "split_min": int(os.environ.get("RFS_K6_SPLIT", "0")), "bcap": 128}
 _DIRS: dict = {}
 _SIDE: dict = {}
 
@@ -229,6 +233,20 @@ def _spin(ev: torch.cuda.Event) -> None:
     microseconds late, time in which the device would drain its queue."""
     while not ev.query():
         pass
+
+
+_SPLIT_WS: dict = {}
+
+
+def _split_ws(dev, R: int, bcap: int) -> torch.Tensor:
+    """K6 split workspace (rfs_hits_split_bytes), kept across steps."""
+    key = (str(dev), R, bcap)
+    ws = _SPLIT_WS.get(key)
+    if ws is None:
+        _SPLIT_WS.clear()
+        ws = torch.empty(int(_native.load().rfs_hits_split_bytes(R, bcap)), dtype=torch.uint8, device=dev)
+        _SPLIT_WS[key] = ws
+    return ws
 
 
 def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bool = False,
@@ -329,9 +347,14 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     used = torch.empty(nn, dtype=torch.uint8, device=dev)
     while True:
         slab = torch.empty(R * hc * 16, dtype=torch.uint8, device=dev)
+        split_min, bcap = _CAPS["split_min"], _CAPS["bcap"]
+        split_ws = _split_ws(dev, R, bcap) if split_min > 0 else None
         _native.call("rfs_hits", _ptr(ranges), n_tiles, _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit), _ptr(geom),
                      _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, pc, _ptr(slab), _ptr(ray_counts),
-                     _ptr(slow), _ptr(stats), _ptr(used), n, st)
+                     _ptr(slow), _ptr(stats), _ptr(used), n, split_min, bcap,
+                     _ptr(split_ws) if split_ws is not None else None, st)
+        if split_ws is not None:
+            _native.launch_counter["kernels"] += 1  # k_hits_merge
         _mark(marks, "hits")
         stats_h.copy_(stats, non_blocking=True)
         if m_cap is not None:

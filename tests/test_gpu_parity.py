@@ -282,6 +282,44 @@ def test_slow_path_bitwise_equals_ring_path():
     assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= 1e-4
 
 
+def _hit_lists(g):
+    counts = g.ray_counts.cpu().numpy()
+    slab = g.slab.view(-1, g.hcap, 16).cpu().numpy()
+    keep = np.arange(g.hcap)[None, :] < counts[:, None]
+    return counts, slab[keep]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [3_000, 40_000])
+def test_split_lists_bitwise_equal_unsplit(n):
+    """K6 streams long tile lists as two concurrent halves merged afterwards
+    (rfs_hits split_min); the hit lists, spectra and used marks must be
+    bitwise those of the single pass, also when the second half overflows its
+    list (bcap) and the ray falls back to the slow path."""
+    import torch
+
+    s = round_to_f32(bench_scene(np.random.default_rng(31), n, 72, 36))
+    ds = raster.DeviceScene.from_host(s, "cuda")
+    tx = torch.as_tensor(default_txs(3, seed=5), dtype=torch.float32, device="cuda")
+    saved = dict(raster._CAPS)
+    out = {}
+    try:
+        for split_min, bcap in ((0, 128), (16, 128), (200, 128), (16, 1)):
+            raster._CAPS["split_min"], raster._CAPS["bcap"] = split_min, bcap
+            g = raster.build_geometry(ds, psi_tx=tx, forward=True)
+            out[(split_min, bcap)] = (g.S.cpu().numpy(), *_hit_lists(g), g.used.cpu().numpy(), g.stats[0],
+                                      g.stats[3])
+    finally:
+        raster._CAPS.update(saved)
+    base = out[(0, 128)]
+    for key, o in out.items():
+        for a, b in zip(base[:4], o[:4]):
+            np.testing.assert_array_equal(a, b, err_msg=str(key))
+        assert o[5] == base[5], key  # total live hits
+    if n >= 40_000:
+        assert out[(16, 1)][4] > base[4]  # one-entry second-half lists overflowed: slow path taken
+
+
 @pytest.mark.gpu
 def test_psi_large_scene_grid():
     """psi for > 262,140 Gaussians (the launch grid must not overflow a 65,535 dimension)
