@@ -356,16 +356,14 @@ __global__ void __launch_bounds__(NT) k_hits(
         const double lb_next = pf_lb;
         __syncwarp();
         // fp64 records of the cone-relevant candidates -> shared memory,
-        // asynchronously (cp.async): they land while the fp32 filters run
-        {
-            const int nrel = __popc(relmask);
-            for (int e = lane; e < nrel * (GDS / 2); e += 32) {
-                const int sl = e / (GDS / 2), part = e - sl * (GDS / 2);
-                const int j = __fns(relmask, 0, sl + 1);
-                cp_async16(&W.gd[j][2 * part], reinterpret_cast<const char*>(geom + W.g[j]) + 16 * part);
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
+        // asynchronously (cp.async; lane j copies its own candidate's): they
+        // land while the fp32 filters run
+        if (rel) {
+            const char* src = reinterpret_cast<const char*>(geom + pf_g);
+#pragma unroll
+            for (int part = 0; part < GDS / 2; ++part) cp_async16(&W.gd[lane][2 * part], src + 16 * part);
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
         if (base + CH < c_hi) prefetch(base + CH);
         // 2. survivor mask from shared memory
         unsigned mask = 0;
