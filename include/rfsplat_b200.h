@@ -87,6 +87,21 @@ int rfs_sort_pairs_u64_cub(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, u
  * (splat.py:340-343); ranges is int32[n_tiles*2]. */
 int rfs_tile_ranges(const uint64_t* ckeys, int m, const uint32_t* m_dev, int n_tiles, int* ranges, void* stream);
 
+/* K2b + K3 + K4 + K4b by tile buckets (bucket.cu): a stable counting sort
+ * by tile (per-block tile counts, offsets = the ranges, clamped to cap; a fill
+ * that keeps expansion order inside each tile's bucket), then one stable
+ * shared-memory radix sort of the depth codes per tile, which writes the
+ * sorted compact keys, Gaussian ids and emission bounds -- bitwise the outputs
+ * of rfs_bin_fill + rfs_sort_pairs_u64 + rfs_tile_ranges + rfs_lower_bounds
+ * (splat.py:337-343).  bcodes / bvals u32[cap] and temp
+ * (rfs_bin_bucket_temp_bytes) are scratch.  A tile list longer than 12288 is
+ * left empty and sets status[0] bit 2 (use the radix sort).  Grids up to 512
+ * tiles. */
+size_t rfs_bin_bucket_temp_bytes(int n, int n_az, int n_el);
+int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_az, int n_el, int cap, const void* geom,
+                   uint32_t* bcodes, uint32_t* bvals, void* temp, uint64_t* ckeys, uint32_t* vals, int* ranges,
+                   double* lb, int* status, void* stream);
+
 /* K4b: per-incidence emission bound for the exact streaming re-sort:
  * lb[i] = min_{j >= i, same tile} (depth_j - r3_j). */
 int rfs_lower_bounds(const int* ranges, int n_tiles, const uint32_t* vals, const void* geom, double* lb, void* stream);

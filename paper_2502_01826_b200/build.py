@@ -25,6 +25,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, "
 SOURCES = {
     "project.cu": ["-fmad=false"],
     "radix_sort.cu": [],
+    "bucket.cu": [],
     "hits.cu": [],
     "composite.cu": [],
     "backward.cu": [],

@@ -145,7 +145,11 @@ class Geometry:
 _CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {},
          # K6 splits tile lists longer than this into two concurrent halves
          # (rfs_hits' split_min; 0 = off); bcap = hits the second half may hold
-         "split_min": int(os.environ.get("RFS_K6_SPLIT", "0")), "bcap": 128}
+         "split_min": int(os.environ.get("RFS_K6_SPLIT", "0")), "bcap": 128,
+         # tile-key sort of the hand-written backend: "bucket" (per-tile buckets
+         # sorted in shared memory, bucket.cu) or "radix" (global onesweep);
+         # scenes whose tile lists outgrow the buckets are remembered here
+         "tile_sort": os.environ.get("RFS_TILE_SORT", "bucket"), "long_tiles": set()}
 _DIRS: dict = {}
 _SIDE: dict = {}
 
@@ -302,10 +306,22 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     status_h = _pinned(dev, "status", 8)
     m_dev_ptr = status.data_ptr() + 4
 
-    def bin_tiles(cap: int, device_count: bool):
+    scene_key = (n, n_az, n_el)
+
+    def bin_tiles(cap: int, device_count: bool, bucket: bool):
         """K2b fill, K3 sort, K4 ranges, K4b bounds into buffers of capacity `cap`."""
         ck = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
         vl = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        if bucket:  # bucket.cu: the same outputs without a global sort
+            rg = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
+            lbv = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
+            bc = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+            bv = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+            tt = torch.empty(max(int(lib.rfs_bin_bucket_temp_bytes(n, n_az, n_el)), 16), dtype=torch.uint8, device=dev)
+            _native.call("rfs_bin_bucket", n, _ptr(rects), _ptr(code), n_az, n_el, cap, _ptr(geom), _ptr(bc),
+                         _ptr(bv), _ptr(tt), _ptr(ck), _ptr(vl), _ptr(rg), _ptr(lbv), _ptr(status), st)
+            _mark(marks, "bin+sort")
+            return ck, vl, rg, lbv
         mp = m_dev_ptr if device_count else None
         if cap > 0:
             _native.call("rfs_bin_fill", n, _ptr(rects), _ptr(code), _ptr(offsets), n_az, cap, _ptr(ck), _ptr(vl), st)
@@ -322,6 +338,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     # Read #1 (M) is skipped when a capacity from earlier steps is known: the
     # binning then runs on the device-side count and M is checked at read #2.
     m_cap = _CAPS.get("m_cap", {}).get((n, n_az, n_el)) if sort_backend == "hand" else None
+    bucket = sort_backend == "hand" and _CAPS["tile_sort"] == "bucket" and scene_key not in _CAPS["long_tiles"]
     if m_cap is None:
         status_h.copy_(status, non_blocking=True)
         ev_m = torch.cuda.Event()
@@ -331,9 +348,9 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         if int(host[0]) & (1 << 1):
             raise GeometryError("a Gaussian is centered on the receiver")
         m = int(host[1]) & 0xFFFFFFFF
-        ckeys, vals, ranges, lb = bin_tiles(m, False)
+        ckeys, vals, ranges, lb = bin_tiles(m, False, bucket)
     else:
-        ckeys, vals, ranges, lb = bin_tiles(m_cap, True)
+        ckeys, vals, ranges, lb = bin_tiles(m_cap, True, bucket)
 
     hc = 1 << max(0, math.ceil(math.log2(max(int(hcap or _CAPS["hcap"]), 1))))  # power of two: slot >> log2(hcap) = ray
     pc = _CAPS["pcap"]
@@ -357,7 +374,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             _native.launch_counter["kernels"] += 1  # k_hits_merge
         _mark(marks, "hits")
         stats_h.copy_(stats, non_blocking=True)
-        if m_cap is not None:
+        if m_cap is not None or bucket:
             status_h.copy_(status, non_blocking=True)
         ev_s = torch.cuda.Event()
         ev_s.record()
@@ -385,10 +402,18 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             _CAPS["m_cap"][(n, n_az, n_el)] = max(m_cap, m + m // 8 + 1024) if m <= m_cap else m + m // 4 + 1024
             if m > m_cap:  # capacity overflow: re-bin with the exact count, redo the hit lists
                 m_cap = None
-                ckeys, vals, ranges, lb = bin_tiles(m, False)
+                ckeys, vals, ranges, lb = bin_tiles(m, False, bucket)
                 redo_forward = True
                 continue
             m_cap = None
+        if bucket and int(status_h.tolist()[0]) & 4:
+            # a tile list outgrew the shared-memory buckets (bucket.cu): the
+            # radix sort for this call and, for this scene shape, from now on
+            _CAPS["long_tiles"].add(scene_key)
+            bucket = False
+            ckeys, vals, ranges, lb = bin_tiles(m, False, False)
+            redo_forward = True
+            continue
         if s[0] > 0:
             # rays whose pending ring overflowed: exact slow path, and a larger
             # ring for the next steps if it happens often

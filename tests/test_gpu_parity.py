@@ -282,6 +282,38 @@ def test_slow_path_bitwise_equals_ring_path():
     assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= 1e-4
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["config1", "cube_", "special_", "hemi_", "bench20k", "bench100k"])
+def test_bucket_binning_bitwise_equals_radix(which):
+    """bucket.cu (per-tile buckets sorted in shared memory) must give bitwise
+    the sorted keys, ids, ranges and emission bounds of the radix-sort path
+    (K2b + K3 + K4 + K4b), hence the same hit lists and spectra."""
+    import torch
+
+    if which == "config1":
+        s = config1_scene()
+    elif which.endswith("_"):
+        s = scene_from(load("edge_scenes.npz"), which)
+    else:
+        s = round_to_f32(bench_scene(np.random.default_rng(7), 20_000 if which == "bench20k" else 100_000, 360, 180))
+    ds = raster.DeviceScene.from_host(s, "cuda")
+    tx = torch.as_tensor(default_txs(2, seed=9), dtype=torch.float32, device="cuda")
+    saved = dict(raster._CAPS)
+    out = {}
+    try:
+        for mode in ("radix", "bucket"):
+            raster._CAPS["tile_sort"] = mode
+            raster._CAPS["m_cap"] = {}
+            g = raster.build_geometry(ds, psi_tx=tx, forward=True)
+            m = g.m
+            out[mode] = [g.ckeys[:m].cpu().numpy(), g.vals[:m].cpu().numpy(), g.ranges.cpu().numpy(),
+                         g.S.cpu().numpy(), *_hit_lists(g)]
+    finally:
+        raster._CAPS.update(saved)
+    for a, b in zip(out["radix"], out["bucket"]):
+        np.testing.assert_array_equal(a, b)
+
+
 def _hit_lists(g):
     counts = g.ray_counts.cpu().numpy()
     slab = g.slab.view(-1, g.hcap, 16).cpu().numpy()
