@@ -108,20 +108,24 @@ __global__ void __launch_bounds__(256) k_geom_seg(
     // deterministic, and no shuffle-bound scan.
     __shared__ double sv[256 / 32][32][NACC + 1];
     __shared__ int sg[256 / 32][32];
+    __shared__ int sst[256 / 32][33];  // lane of each segment's first hit, then the end
     const int wl = threadIdx.x >> 5;
 #pragma unroll
     for (int i = 0; i < NACC; ++i) sv[wl][lane][i] = v[i];
     sg[wl][lane] = g;
     const int gp = __shfl_up_sync(0xffffffffu, g, 1);
-    const unsigned smask = __ballot_sync(0xffffffffu, valid && (lane == 0 || gp != g));
+    const bool is_start = valid && (lane == 0 || gp != g);
+    const unsigned smask = __ballot_sync(0xffffffffu, is_start);
     const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
     const int ns = __popc(smask);
+    if (is_start) sst[wl][__popc(smask & ((1u << lane) - 1u))] = lane;
+    if (lane == 0) sst[wl][ns] = nvalid;
     __syncwarp();
     const int wb = wglob << 5;
     for (int t = lane; t < ns * NACC; t += 32) {
         const int k = t / NACC, i = t - k * NACC;
-        const int h_start = __fns(smask, 0, k + 1);
-        const int h_end = k + 1 < ns ? __fns(smask, 0, k + 2) : nvalid;
+        const int h_start = sst[wl][k];
+        const int h_end = sst[wl][k + 1];
         double sum = 0.0;
         for (int q = h_start; q < h_end; ++q) sum += sv[wl][q][i];
         const int gk = sg[wl][h_start];
