@@ -165,6 +165,20 @@ int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* 
                       float* s_w, void* s_wt, uint32_t* inv_slot, void* stream);
 int rfs_gauss_offsets(const uint64_t* keys, int n_hits, const uint32_t* h_dev, int n, int* g_off, void* stream);
 
+/* K8i by counting (gindex.cu): hits per Gaussian, g_off (int[n+1], g_off[n]
+ * = H), each hit's slot scattered into its Gaussian's segment, then each
+ * segment put in slot order (a warp sort for <= 256 hits, else a bitmap over
+ * the Gaussian's rays: one hit per ray) with the per-hit Gaussian id, ray, w
+ * and w T gathered -- bitwise the outputs of rfs_hit_keys +
+ * rfs_sort_pairs_u64 + rfs_gauss_offsets + rfs_gather_sorted.  Writes
+ * positions < cap only.  Grids up to 65536 rays.  scratch:
+ * rfs_gauss_index_scratch_elems(n, cap) u32; scan_temp:
+ * rfs_scan_temp_elems(n) u32. */
+size_t rfs_gauss_index_scratch_elems(int n, int cap);
+int rfs_gauss_index(const void* slab, const int* counts, int hcap, int n_rays, int n, int cap, uint32_t* scratch,
+                    uint32_t* scan_temp, int* g_off, uint64_t* sorted_g, uint32_t* s_slot, uint32_t* s_ray, float* s_w,
+                    void* s_wt, void* stream);
+
 /* K8: TX-batched backward over the shared hit lists, atomic-free and
  * deterministic (every sum in a fixed order).  Replaces the complex part of
  * _ray_backward (_kernels.py:360-387, 522) and the p_acc bincount

@@ -26,6 +26,7 @@ SOURCES = {
     "project.cu": ["-fmad=false"],
     "radix_sort.cu": [],
     "bucket.cu": [],
+    "gindex.cu": [],
     "hits.cu": [],
     "composite.cu": [],
     "backward.cu": [],

@@ -314,6 +314,53 @@ def test_bucket_binning_bitwise_equals_radix(which):
         np.testing.assert_array_equal(a, b)
 
 
+def _huge_gaussian_scene():
+    """bench scene + one Gaussian whose 3-sigma ball holds the receiver: it is
+    hit by (nearly) every ray, a segment far longer than gindex's shared-memory
+    sort (the bitmap path)."""
+    s = bench_scene(np.random.default_rng(17), 20_000, 360, 180)
+    s.means[0] = [3.0, 0.5, -0.2]
+    s.log_scales[0] = np.log([2.5, 2.0, 2.2])
+    s.trans_mag_raw[0] = -2.0
+    return round_to_f32(s)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["config1", "special_", "bench100k", "huge"])
+def test_counting_gauss_index_bitwise_equals_radix(which):
+    """gindex.cu (per-Gaussian counting + segment sorts) must give bitwise the
+    by-Gaussian index of the radix path (hit keys + onesweep + offsets +
+    gather): the backward's fixed summation order depends on it."""
+    import torch
+
+    if which == "config1":
+        s = config1_scene()
+    elif which.endswith("_"):
+        s = scene_from(load("edge_scenes.npz"), which)
+    elif which == "huge":
+        s = _huge_gaussian_scene()
+    else:
+        s = round_to_f32(bench_scene(np.random.default_rng(8), 100_000, 360, 180))
+    ds = raster.DeviceScene.from_host(s, "cuda")
+    saved = dict(raster._CAPS)
+    out = {}
+    try:
+        for mode in ("radix", "count"):
+            raster._CAPS["gindex"] = mode
+            raster._CAPS["h_cap"] = {}
+            g = raster.build_geometry(ds, index=True)
+            gi = g.gidx
+            H = g.total_hits
+            out[mode] = [gi["g_off"][: g.n + 1].cpu().numpy()] + [
+                gi[k][:H].cpu().numpy() for k in ("sorted_g", "s_slot", "s_ray", "s_w", "s_wt")]
+    finally:
+        raster._CAPS.update(saved)
+    if which == "huge":
+        assert np.diff(out["count"][0]).max() > 8192  # the bitmap path was taken
+    for a, b in zip(out["radix"], out["count"]):
+        np.testing.assert_array_equal(a, b)
+
+
 def _hit_lists(g):
     counts = g.ray_counts.cpu().numpy()
     slab = g.slab.view(-1, g.hcap, 16).cpu().numpy()
