@@ -90,14 +90,13 @@ int rfs_tile_ranges(const uint64_t* ckeys, int m, const uint32_t* m_dev, int n_t
 /* K2b + K3 + K4 + K4b by tile buckets (bucket.cu): a stable counting sort
  * by tile (per-block tile counts, offsets = the ranges, clamped to cap; a fill
  * that keeps expansion order inside each tile's bucket), then one stable
- * shared-memory radix sort of the depth codes per tile, which writes the
- * sorted compact keys, Gaussian ids and emission bounds -- bitwise the outputs
- * of rfs_bin_fill + rfs_sort_pairs_u64 + rfs_tile_ranges + rfs_lower_bounds
- * (splat.py:337-343).  bcodes / bvals u32[cap] and temp
- * (rfs_bin_bucket_temp_bytes) are scratch.  A tile list longer than 12288 is
- * left empty and sets status[0] bit 2 (use the radix sort).  Grids up to 512
- * tiles. */
-size_t rfs_bin_bucket_temp_bytes(int n, int n_az, int n_el);
+ * radix sort of the depth codes per tile (shared memory up to 12288 entries,
+ * L2-resident global buffers beyond), which writes the sorted compact keys,
+ * Gaussian ids and emission bounds -- bitwise the outputs of rfs_bin_fill +
+ * rfs_sort_pairs_u64 + rfs_tile_ranges + rfs_lower_bounds (splat.py:337-343).
+ * bcodes / bvals u32[cap] and temp (rfs_bin_bucket_temp_bytes) are scratch;
+ * status is reserved.  Grids up to 512 tiles. */
+size_t rfs_bin_bucket_temp_bytes(int n, int n_az, int n_el, int cap);
 int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_az, int n_el, int cap, const void* geom,
                    uint32_t* bcodes, uint32_t* bvals, void* temp, uint64_t* ckeys, uint32_t* vals, int* ranges,
                    double* lb, int* status, void* stream);

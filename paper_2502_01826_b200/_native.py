@@ -35,7 +35,7 @@ _SIGS = {
     "rfs_sort_cub_temp_bytes": (sz, [i32, i32]),
     "rfs_sort_pairs_u64_cub": (i32, [vp, vp, vp, vp, i32, i32, vp, sz, C.POINTER(i32), vp]),
     "rfs_tile_ranges": (i32, [vp, i32, vp, i32, vp, vp]),
-    "rfs_bin_bucket_temp_bytes": (sz, [i32, i32, i32]),
+    "rfs_bin_bucket_temp_bytes": (sz, [i32, i32, i32, i32]),
     "rfs_bin_bucket": (i32, [i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rfs_lower_bounds": (i32, [vp, i32, vp, vp, vp, vp]),
     "rfs_ray_dirs": (i32, [i32, i32, vp, vp]),
@@ -103,7 +103,7 @@ def load(require_cuda: bool = True):
 # kernels launched per entry-point call (sort: 2 + passes, added by raster.sort_pairs)
 KERNELS_PER_CALL = {
     "rfs_project": 1, "rfs_exclusive_scan_u32": 1, "rfs_bin_fill": 1, "rfs_expand_keys": 1,
-    "rfs_tile_ranges": 1, "rfs_lower_bounds": 1, "rfs_bin_bucket": 6, "rfs_hits": 2, "rfs_hits_slow": 1, "rfs_psi": 1,
+    "rfs_tile_ranges": 1, "rfs_lower_bounds": 1, "rfs_bin_bucket": 7, "rfs_hits": 2, "rfs_hits_slow": 1, "rfs_psi": 1,
     "rfs_forward": 1, "rfs_lam_transpose": 1, "rfs_bwd_gauss": 1, "rfs_bwd_rays": 1, "rfs_hit_keys": 1, "rfs_gauss_offsets": 1, "rfs_grad_geom": 3,
     "rfs_grad_tx": 1, "rfs_gather_sorted": 1, "rfs_gauss_index": 5,
     "rfs_ray_dirs": 1, "rfs_spectrum_loss": 4, "rfs_sgd_step": 2, "rfs_scalar_loss": 1, "rfs_density_flags": 1,

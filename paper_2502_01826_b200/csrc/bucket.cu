@@ -19,9 +19,9 @@
 //                  sorted compact keys, Gaussian ids and the emission bounds
 //                  lb[i] = min_{j >= i} lbv[g_j] of K4b.
 // Same outputs, bitwise, as K2b + K3 + K4 + K4b (rfs_bin_fill, the radix
-// sort, rfs_tile_ranges, rfs_lower_bounds).  A tile list longer than the
-// shared-memory capacity (BK_SEG_MAX) is left empty and sets status bit 2:
-// the caller redoes the binning with the radix sort.
+// sort, rfs_tile_ranges, rfs_lower_bounds).  Three k_seg_sort classes: lists
+// up to 4096 (512 threads) and 12288 (1024 threads) in shared memory, longer
+// ones with the same passes over global (L2-resident) ping-pong buffers.
 #include "rfs_common.cuh"
 
 namespace {
@@ -30,7 +30,6 @@ constexpr int BK_MAX_TILES = 512;   // >= 23 x 12 (rfs_project caps the grid at 
 constexpr int BK_BLK = 256;         // Gaussians per fill block
 constexpr int BK_SEG_SMALL = 4096;  // tile lists sorted by 512-thread blocks
 constexpr int BK_SEG_MAX = 12288;   // longest tile list sorted in shared memory (1024 threads)
-constexpr uint32_t BK_STATUS_LONG = 4u;
 
 struct __align__(16) Rect {  // project.cu's splat rectangle
     short s1_lo, s1_hi, s2_hi, tv_lo, tv_hi, pad0, pad1, pad2;
@@ -130,12 +129,8 @@ __global__ void __launch_bounds__(BK_MAX_TILES) k_tile_offsets(int n_tiles, cons
     uint32_t off = v - c;
     for (int w = 0; w < wid; ++w) off += wsum[w];
     if (t >= n_tiles) return;
-    // a list too long for the shared-memory sort is left empty (flagged):
-    // nothing downstream may read its unsorted bucket
-    const bool too_long = c > (uint32_t)BK_SEG_MAX;
-    ranges[t] = make_int2((int)min(off, cap), (int)min(too_long ? off : off + c, cap));
+    ranges[t] = make_int2((int)min(off, cap), (int)min(off + c, cap));
     off_out[t] = off;
-    if (too_long) atomicOr(status, (int)BK_STATUS_LONG);
 }
 
 __global__ void __launch_bounds__(BK_BLK) k_fill_stable(int n, const Rect* __restrict__ rects,
@@ -204,28 +199,41 @@ __device__ __forceinline__ uint32_t scan256_excl(uint32_t c, uint32_t* wsc) {
 // 32 * ITEMS of them taken 32 at a time, so a warp's digit ranks come from
 // match_any plus its running per-digit counts, and the round's per-digit
 // offsets from a scan over the warps -- order within a digit is kept.
+// CAP == 0: lists longer than every shared-memory class -- the same passes
+// with the ping-pong buffers in global memory (the bucket itself and an
+// alternate pair), L2-resident.
 template <int CAP, int NT>
-__global__ void __launch_bounds__(NT) k_seg_sort(const int2* __restrict__ ranges, int lo,
-                                                 const uint32_t* __restrict__ bcodes,
-                                                 const uint32_t* __restrict__ bvals, const RfsGeom* __restrict__ geom,
+__global__ void __launch_bounds__(NT) k_seg_sort(const int2* __restrict__ ranges, int lo, uint32_t* __restrict__ bcodes,
+                                                 uint32_t* __restrict__ bvals, uint32_t* __restrict__ altc,
+                                                 uint32_t* __restrict__ altv, const RfsGeom* __restrict__ geom,
                                                  uint64_t* __restrict__ ckeys, uint32_t* __restrict__ vals,
                                                  double* __restrict__ lb) {
     constexpr int NW = NT / 32, ITEMS = 8, ROUND = NT * ITEMS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t* k0 = reinterpret_cast<uint32_t*>(smem_raw);  // ping-pong codes / ids, 4 x CAP
-    uint32_t* v0 = k0 + CAP;
-    uint32_t* k1 = v0 + CAP;
-    uint32_t* v1 = k1 + CAP;
-    __shared__ uint32_t dbase[256], rtot[256], wsc[8];
-    __shared__ uint16_t wcnt[NW][256];
-    __shared__ double wmin[NW];
     const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int2 rg = ranges[tile];
     const int L = rg.y - rg.x;
-    if (L <= lo || L > CAP) return;  // another launch's class (block-uniform)
-    for (int i = tid; i < L; i += NT) {
-        k0[i] = bcodes[rg.x + i];
-        v0[i] = bvals[rg.x + i];
+    if (L <= lo || (CAP > 0 && L > CAP)) return;  // another launch's class (block-uniform)
+    uint32_t *k0, *v0, *k1, *v1;
+    if (CAP > 0) {  // ping-pong codes / ids in shared memory, 4 x CAP
+        k0 = reinterpret_cast<uint32_t*>(smem_raw);
+        v0 = k0 + CAP;
+        k1 = v0 + CAP;
+        v1 = k1 + CAP;
+    } else {
+        k0 = bcodes + rg.x;
+        v0 = bvals + rg.x;
+        k1 = altc + rg.x;
+        v1 = altv + rg.x;
+    }
+    __shared__ uint32_t dbase[256], rtot[256], wsc[8];
+    __shared__ uint16_t wcnt[NW][256];
+    __shared__ double wmin[NW];
+    if (CAP > 0) {
+        for (int i = tid; i < L; i += NT) {
+            k0[i] = bcodes[rg.x + i];
+            v0[i] = bvals[rg.x + i];
+        }
     }
     const unsigned lt = lanemask_lt();
     const bool multi = L > ROUND;
@@ -295,9 +303,9 @@ __global__ void __launch_bounds__(NT) k_seg_sort(const int2* __restrict__ ranges
         __syncthreads();
     }
     // sorted compact keys (tile << 31 | depth code), Gaussian ids, lbv -> the
-    // now free ping-pong buffer (as doubles)
+    // now free ping-pong buffer (as doubles; in global mode lb itself)
     const uint64_t th = (uint64_t)tile << 31;
-    double* sl = reinterpret_cast<double*>(dk);  // dk + dv: 8 B x CAP
+    double* sl = CAP > 0 ? reinterpret_cast<double*>(dk) : lb + rg.x;  // dk + dv: 8 B x CAP
     for (int i = tid; i < L; i += NT) {
         const uint32_t g = sv[i];
         ckeys[rg.x + i] = th | sk[i];
@@ -322,23 +330,23 @@ __global__ void __launch_bounds__(NT) k_seg_sort(const int2* __restrict__ ranges
     double carry = __shfl_down_sync(0xffffffffu, v, 1);
     if (lane == 31) carry = INFINITY;
     for (int w = wid + 1; w < NW; ++w) carry = fmin(carry, wmin[w]);
-    for (int i = i1 - 1; i >= i0; --i) {
+    for (int i = i1 - 1; i >= i0; --i) {  // (global mode: each thread rewrites its own run)
         carry = fmin(carry, sl[i]);
         lb[rg.x + i] = carry;
     }
 }
 
 template <int CAP, int NT>
-int launch_seg_sort(int n_tiles, const int* ranges, int lo, const uint32_t* bcodes, const uint32_t* bvals,
-                    const void* geom, uint64_t* ckeys, uint32_t* vals, double* lb, cudaStream_t st) {
+int launch_seg_sort(int n_tiles, const int* ranges, int lo, uint32_t* bcodes, uint32_t* bvals, uint32_t* altc,
+                    uint32_t* altv, const void* geom, uint64_t* ckeys, uint32_t* vals, double* lb, cudaStream_t st) {
     static bool attr = false;
     const size_t smem = (size_t)CAP * 16;
-    if (!attr) {
+    if (!attr && smem > 0) {
         RFS_CUDA_TRY(cudaFuncSetAttribute(k_seg_sort<CAP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    k_seg_sort<CAP, NT><<<n_tiles, NT, smem, st>>>((const int2*)ranges, lo, bcodes, bvals, (const RfsGeom*)geom,
-                                                   ckeys, vals, lb);
+    k_seg_sort<CAP, NT><<<n_tiles, NT, smem, st>>>((const int2*)ranges, lo, bcodes, bvals, altc, altv,
+                                                   (const RfsGeom*)geom, ckeys, vals, lb);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -347,10 +355,11 @@ int launch_seg_sort(int n_tiles, const int* ranges, int lo, const uint32_t* bcod
 
 extern "C" {
 
-size_t rfs_bin_bucket_temp_bytes(int n, int n_az, int n_el) {
+size_t rfs_bin_bucket_temp_bytes(int n, int n_az, int n_el, int cap) {
     const int n_tiles = ((n_az + RFS_TILE - 1) / RFS_TILE) * ((n_el + RFS_TILE - 1) / RFS_TILE);
     const size_t nb = (size_t)rfs_ceil_div(n > 0 ? n : 1, BK_BLK);
-    return sizeof(uint32_t) * (nb * (size_t)n_tiles + 2 * (size_t)n_tiles);
+    // block table, tile totals, tile offsets, alternate codes / ids for long lists
+    return sizeof(uint32_t) * (nb * (size_t)n_tiles + 2 * (size_t)n_tiles + 2 * (size_t)(cap > 0 ? cap : 0));
 }
 
 int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_az, int n_el, int cap, const void* geom,
@@ -364,6 +373,8 @@ int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_a
     uint32_t* tab = (uint32_t*)temp;  // [n_tiles][nb]
     uint32_t* tot = tab + (size_t)nb * n_tiles;
     uint32_t* toff = tot + n_tiles;
+    uint32_t* altc = toff + n_tiles;
+    uint32_t* altv = altc + (cap > 0 ? cap : 0);
     if (n > 0) {
         k_tile_count<<<nb, BK_BLK, 0, st>>>(n, (const Rect*)rects, tiles_u, n_tiles, nb, tab);
         RFS_LAUNCH_CHECK();
@@ -378,10 +389,13 @@ int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_a
     k_fill_stable<<<nb, BK_BLK, 0, st>>>(n, (const Rect*)rects, depth_code, tiles_u, n_tiles, nb, (uint32_t)cap, tab,
                                          toff, bcodes, bvals);
     RFS_LAUNCH_CHECK();
-    int rc = launch_seg_sort<BK_SEG_SMALL, 512>(n_tiles, ranges, 0, bcodes, bvals, geom, ckeys, vals, lb, st);
+    int rc = launch_seg_sort<BK_SEG_SMALL, 512>(n_tiles, ranges, 0, bcodes, bvals, altc, altv, geom, ckeys, vals, lb,
+                                                st);
     if (rc != RFS_OK) return rc;
-    return launch_seg_sort<BK_SEG_MAX, 1024>(n_tiles, ranges, BK_SEG_SMALL, bcodes, bvals, geom, ckeys, vals, lb,
-                                             st);
+    rc = launch_seg_sort<BK_SEG_MAX, 1024>(n_tiles, ranges, BK_SEG_SMALL, bcodes, bvals, altc, altv, geom, ckeys,
+                                           vals, lb, st);
+    if (rc != RFS_OK) return rc;
+    return launch_seg_sort<0, 1024>(n_tiles, ranges, BK_SEG_MAX, bcodes, bvals, altc, altv, geom, ckeys, vals, lb, st);
 }
 
 }  // extern "C"

@@ -146,10 +146,9 @@ _CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {},
          # K6 splits tile lists longer than this into two concurrent halves
          # (rfs_hits' split_min; 0 = off); bcap = hits the second half may hold
          "split_min": int(os.environ.get("RFS_K6_SPLIT", "0")), "bcap": 128,
-         # tile-key sort of the hand-written backend: "bucket" (per-tile buckets
-         # sorted in shared memory, bucket.cu) or "radix" (global onesweep);
-         # scenes whose tile lists outgrow the buckets are remembered here
-         "tile_sort": os.environ.get("RFS_TILE_SORT", "bucket"), "long_tiles": set(),
+         # tile-key sort of the hand-written backend: "bucket" (per-tile buckets,
+         # bucket.cu) or "radix" (global onesweep)
+         "tile_sort": os.environ.get("RFS_TILE_SORT", "bucket"), "tile_max": {},
          # by-Gaussian hit index of the hand-written backend: "radix" (hit keys +
          # global onesweep) or "count" (gindex.cu; bitwise the same, measured
          # ~10 us slower at config 2: 119 vs 111 us)
@@ -310,8 +309,6 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     status_h = _pinned(dev, "status", 8)
     m_dev_ptr = status.data_ptr() + 4
 
-    scene_key = (n, n_az, n_el)
-
     def bin_tiles(cap: int, device_count: bool, bucket: bool):
         """K2b fill, K3 sort, K4 ranges, K4b bounds into buffers of capacity `cap`."""
         ck = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
@@ -321,7 +318,8 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             lbv = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
             bc = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
             bv = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-            tt = torch.empty(max(int(lib.rfs_bin_bucket_temp_bytes(n, n_az, n_el)), 16), dtype=torch.uint8, device=dev)
+            tt = torch.empty(max(int(lib.rfs_bin_bucket_temp_bytes(n, n_az, n_el, cap)), 16), dtype=torch.uint8,
+                             device=dev)
             _native.call("rfs_bin_bucket", n, _ptr(rects), _ptr(code), n_az, n_el, cap, _ptr(geom), _ptr(bc),
                          _ptr(bv), _ptr(tt), _ptr(ck), _ptr(vl), _ptr(rg), _ptr(lbv), _ptr(status), st)
             _mark(marks, "bin+sort")
@@ -342,7 +340,10 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     # Read #1 (M) is skipped when a capacity from earlier steps is known: the
     # binning then runs on the device-side count and M is checked at read #2.
     m_cap = _CAPS.get("m_cap", {}).get((n, n_az, n_el)) if sort_backend == "hand" else None
-    bucket = sort_backend == "hand" and _CAPS["tile_sort"] == "bucket" and scene_key not in _CAPS["long_tiles"]
+    # the buckets' global-memory class (tile lists > 12288) is correct but slower
+    # than the radix sort: scenes whose lists ran that long last time use the radix sort
+    bucket = (sort_backend == "hand" and _CAPS["tile_sort"] == "bucket"
+              and _CAPS["tile_max"].get((n, n_az, n_el), 0) <= 12288)
     if m_cap is None:
         status_h.copy_(status, non_blocking=True)
         ev_m = torch.cuda.Event()
@@ -378,7 +379,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             _native.launch_counter["kernels"] += 1  # k_hits_merge
         _mark(marks, "hits")
         stats_h.copy_(stats, non_blocking=True)
-        if m_cap is not None or bucket:
+        if m_cap is not None:
             status_h.copy_(status, non_blocking=True)
         ev_s = torch.cuda.Event()
         ev_s.record()
@@ -410,14 +411,6 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                 redo_forward = True
                 continue
             m_cap = None
-        if bucket and int(status_h.tolist()[0]) & 4:
-            # a tile list outgrew the shared-memory buckets (bucket.cu): the
-            # radix sort for this call and, for this scene shape, from now on
-            _CAPS["long_tiles"].add(scene_key)
-            bucket = False
-            ckeys, vals, ranges, lb = bin_tiles(m, False, False)
-            redo_forward = True
-            continue
         if s[0] > 0:
             # rays whose pending ring overflowed: exact slow path, and a larger
             # ring for the next steps if it happens often
@@ -442,6 +435,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         break
     if sort_backend == "hand":
         _CAPS.setdefault("m_cap", {}).setdefault((n, n_az, n_el), m + m // 8 + 1024)
+        _CAPS["tile_max"][(n, n_az, n_el)] = int(s[4])  # longest tile list (k_max_range)
     geo = Geometry(n, n_az, n_el, tiles_u, tiles_v, m, geom, rho32, dirs, ckeys[:max(m, 0)], vals[:max(m, 0)],
                    ranges, hc, slab, ray_counts, s, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
     if psi_tx is not None and redo_forward:  # the hit lists changed: new used set

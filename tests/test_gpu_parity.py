@@ -283,7 +283,7 @@ def test_slow_path_bitwise_equals_ring_path():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("which", ["config1", "cube_", "special_", "hemi_", "bench20k", "bench100k"])
+@pytest.mark.parametrize("which", ["config1", "cube_", "special_", "hemi_", "bench20k", "bench100k", "bench500k"])
 def test_bucket_binning_bitwise_equals_radix(which):
     """bucket.cu (per-tile buckets sorted in shared memory) must give bitwise
     the sorted keys, ids, ranges and emission bounds of the radix-sort path
@@ -294,8 +294,9 @@ def test_bucket_binning_bitwise_equals_radix(which):
         s = config1_scene()
     elif which.endswith("_"):
         s = scene_from(load("edge_scenes.npz"), which)
-    else:
-        s = round_to_f32(bench_scene(np.random.default_rng(7), 20_000 if which == "bench20k" else 100_000, 360, 180))
+    else:  # bench500k: tile lists beyond the shared-memory classes (global-memory passes)
+        n = {"bench20k": 20_000, "bench100k": 100_000, "bench500k": 500_000}[which]
+        s = round_to_f32(bench_scene(np.random.default_rng(7), n, 360, 180))
     ds = raster.DeviceScene.from_host(s, "cuda")
     tx = torch.as_tensor(default_txs(2, seed=9), dtype=torch.float32, device="cuda")
     saved = dict(raster._CAPS)
@@ -304,6 +305,7 @@ def test_bucket_binning_bitwise_equals_radix(which):
         for mode in ("radix", "bucket"):
             raster._CAPS["tile_sort"] = mode
             raster._CAPS["m_cap"] = {}
+            raster._CAPS["tile_max"] = {}  # the bucket path even for long lists
             g = raster.build_geometry(ds, psi_tx=tx, forward=True)
             m = g.m
             out[mode] = [g.ckeys[:m].cpu().numpy(), g.vals[:m].cpu().numpy(), g.ranges.cpu().numpy(),
@@ -312,6 +314,9 @@ def test_bucket_binning_bitwise_equals_radix(which):
         raster._CAPS.update(saved)
     for a, b in zip(out["radix"], out["bucket"]):
         np.testing.assert_array_equal(a, b)
+    if which == "bench500k":
+        rg = out["bucket"][2]
+        assert (rg[:, 1] - rg[:, 0]).max() > 12288
 
 
 def _huge_gaussian_scene():
