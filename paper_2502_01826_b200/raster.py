@@ -152,7 +152,9 @@ _CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {},
          # by-Gaussian hit index of the hand-written backend: "radix" (hit keys +
          # global onesweep) or "count" (gindex.cu; bitwise the same, measured
          # ~10 us slower at config 2: 119 vs 111 us)
-         "gindex": os.environ.get("RFS_GINDEX", "radix")}
+         "gindex": os.environ.get("RFS_GINDEX", "radix"),
+         # the early by-Gaussian index on the side stream (overlapping psi / K7 / loss)
+         "index_side": os.environ.get("RFS_INDEX_SIDE", "1") == "1"}
 _DIRS: dict = {}
 _SIDE: dict = {}
 
@@ -377,6 +379,8 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                      _ptr(split_ws) if split_ws is not None else None, st)
         if split_ws is not None:
             _native.launch_counter["kernels"] += 1  # k_hits_merge
+        ev_hits = torch.cuda.Event()
+        ev_hits.record()
         _mark(marks, "hits")
         stats_h.copy_(stats, non_blocking=True)
         if m_cap is not None:
@@ -395,8 +399,22 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         if h_cap is not None:  # the by-Gaussian index, also behind the statistics read
             early = Geometry(n, n_az, n_el, tiles_u, tiles_v, -1, geom, rho32, dirs, ckeys, vals, ranges, hc, slab,
                              ray_counts, [0] * 8, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
-            gauss_index(early, h_cap)
-            _mark(marks, "gauss_index")
+            if _CAPS["index_side"]:
+                # on the side stream, right behind K6: overlaps psi, the forward composite and the loss
+                side = _side_stream(dev)
+                side.wait_event(ev_hits)
+                main = torch.cuda.current_stream(dev)
+                with torch.cuda.stream(side):
+                    gauss_index(early, h_cap)
+                    ready = torch.cuda.Event()
+                    ready.record(side)
+                for v in early.gidx.values():
+                    if isinstance(v, torch.Tensor):
+                        v.record_stream(main)
+                early.gidx["ready"] = ready
+            else:
+                gauss_index(early, h_cap)
+                _mark(marks, "gauss_index")
         _spin(ev_s)  # read #2: hit-list statistics (and M when read #1 was skipped)
         s = stats_h.tolist()
         if m_cap is not None:
@@ -610,6 +628,8 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     built = geo.gidx is None
     gauss_index(geo)
     gi = geo.gidx
+    if "ready" in gi:  # built on the side stream
+        torch.cuda.current_stream(geo.slab.device).wait_event(gi["ready"])
     if built:
         _mark(marks, "gauss_index")
     h = gi["h"]

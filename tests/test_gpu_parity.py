@@ -355,6 +355,8 @@ def test_counting_gauss_index_bitwise_equals_radix(which):
             raster._CAPS["h_cap"] = {}
             g = raster.build_geometry(ds, index=True)
             gi = g.gidx
+            if "ready" in gi:  # built on the side stream
+                torch.cuda.current_stream().wait_event(gi["ready"])
             H = g.total_hits
             out[mode] = [gi["g_off"][: g.n + 1].cpu().numpy()] + [
                 gi[k][:H].cpu().numpy() for k in ("sorted_g", "s_slot", "s_ray", "s_w", "s_wt")]
