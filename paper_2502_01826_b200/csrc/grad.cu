@@ -6,7 +6,7 @@
 //     each warp sums its runs of equal Gaussian id through shared memory
 //     (one lane per (run, value)).  Gaussians whose hits straddle warps
 //     leave per-warp partials that
-// K9a' k_geom_fix (one warp per 32-hit group where such a Gaussian starts)
+// K9a' k_geom_fix (thread per 32-hit group where such a Gaussian starts)
 //     adds in group order -- so every sum has a fixed order (the slot order
 //     of the reference's bincount, grad.py:243-254): deterministic.
 // K9c k_geom_final (thread per Gaussian, fp64): d_mean direct term, d_cov,
@@ -146,41 +146,64 @@ __global__ void __launch_bounds__(256) k_geom_seg(
     }
 }
 
-// Gaussians whose hits straddle warps: the warp of the 32-hit group where
-// such a Gaussian starts adds the group partials in group order (lanes over
-// the 14 sums) -- a fixed order, so the result stays deterministic.
+// Gaussians whose hits straddle warps: thread per 32-hit group; the group
+// where such a Gaussian starts adds the group partials (slot 2w+1 of its own
+// group, slot 2v of the later ones).  Spans of up to FIX_SHORT groups (almost
+// all) are summed by that thread left to right; longer ones by the whole
+// warp, lane-strided over the groups plus a fixed butterfly.  Fixed orders:
+// deterministic.
+constexpr int FIX_SHORT = 4;
 __global__ void __launch_bounds__(256) k_geom_fix(int h, const uint32_t* __restrict__ h_dev,
                                                   const uint64_t* __restrict__ sorted_g,
                                                   const int* __restrict__ g_off, const double* __restrict__ part_v,
                                                   double* __restrict__ acc64) {
     if (h_dev) h = min(h, (int)*h_dev);
     const int lane = threadIdx.x & 31;
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;  // group
     const int c0 = w << 5;
-    if (c0 >= h) return;
-    const int c1 = min(c0 + 32, h);
-    if (c1 >= h) return;
-    const uint64_t g = sorted_g[c1 - 1];
-    if (sorted_g[c1] != g) return;  // the last segment ends inside this group
-    const int h0 = g_off[g];
-    if (h0 < c0) return;            // started in an earlier group, handled there
-    const int w1 = (g_off[g + 1] - 1) >> 5;
-    // lane l adds groups w + l, w + l + 32, ... (group w holds g as its last
-    // segment, later groups as their first); then a fixed butterfly over lanes
-    double s[NACC];
-#pragma unroll
-    for (int i = 0; i < NACC; ++i) s[i] = 0.0;
-    for (int v = w + lane; v <= w1; v += 32) {
-        const size_t slot = v == w ? (size_t)(2 * w + 1) : (size_t)(2 * v);
-#pragma unroll
-        for (int i = 0; i < NACC; ++i) s[i] += part_v[slot * NACC + i];
+    bool mine = false;
+    int g = 0, w1 = 0;
+    if (c0 < h) {
+        const int c1 = min(c0 + 32, h);
+        if (c1 < h) {
+            g = (int)sorted_g[c1 - 1];
+            // the last segment continues past this group and starts in it
+            mine = (int)sorted_g[c1] == g && g_off[g] >= c0;
+            if (mine) w1 = (g_off[g + 1] - 1) >> 5;
+        }
     }
+    if (mine && w1 - w + 1 <= FIX_SHORT) {
+        double s[NACC];
 #pragma unroll
-    for (int i = 0; i < NACC; ++i) {
-        double t = s[i];
+        for (int i = 0; i < NACC; ++i) s[i] = part_v[(size_t)(2 * w + 1) * NACC + i];
+        for (int v = w + 1; v <= w1; ++v) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == 0) acc64[(size_t)g * NACC + i] = t;
+            for (int i = 0; i < NACC; ++i) s[i] += part_v[(size_t)(2 * v) * NACC + i];
+        }
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) acc64[(size_t)g * NACC + i] = s[i];
+    }
+    unsigned longs = __ballot_sync(0xffffffffu, mine && w1 - w + 1 > FIX_SHORT);
+    while (longs) {
+        const int src = __ffs(longs) - 1;
+        longs &= longs - 1;
+        const int gw = __shfl_sync(0xffffffffu, w, src), gg = __shfl_sync(0xffffffffu, g, src),
+                  gw1 = __shfl_sync(0xffffffffu, w1, src);
+        double s[NACC];
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) s[i] = 0.0;
+        for (int v = gw + lane; v <= gw1; v += 32) {
+            const size_t slot = v == gw ? (size_t)(2 * gw + 1) : (size_t)(2 * v);
+#pragma unroll
+            for (int i = 0; i < NACC; ++i) s[i] += part_v[slot * NACC + i];
+        }
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) {
+            double t = s[i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) acc64[(size_t)gg * NACC + i] = t;
+        }
     }
 }
 
@@ -402,8 +425,8 @@ int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sort
         k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
                                                                (const RfsGeom*)geom, dirs, g_off, rx[0], rx[1], rx[2],
                                                                ress_radius, acc64, part_g, part_v);
-        k_geom_fix<<<rfs_ceil_div((long long)rfs_ceil_div(n_hits, 32) * 32, 256), 256, 0, st>>>(n_hits, h_dev, sorted_g,
-                                                                                              g_off, part_v, acc64);
+        k_geom_fix<<<rfs_ceil_div(rfs_ceil_div(n_hits, 32), 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, g_off, part_v,
+                                                                              acc64);
     }
     k_geom_final<<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, acc64, quats, log_scales, trans_mag_raw, d_mean, d_quat,
                                                        d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov,
