@@ -5,15 +5,14 @@
 // position), then takes each tile's range (splat.py:340-343).  A 360 x 180
 // grid has at most 23 x 12 = 276 tiles, so the tile part is a stable counting
 // sort and only the depth part needs sorting, tile by tile:
-//   k_tile_count   incidences per (256-Gaussian block, tile), from one warp
-//                  ballot per tile (which of the warp's Gaussians hit it);
+//   k_tile_count   incidences per (256-Gaussian block, tile);
 //   k_tile_blockscan / k_tile_offsets
 //                  each block's base inside a tile's bucket (blocks in
 //                  order), the tile totals and offsets (= the ranges);
 //   k_fill_stable  each incidence to its tile's bucket at base + its rank
-//                  among the block's Gaussians hitting that tile (a Gaussian
-//                  hits a tile at most once): buckets hold their incidences
-//                  in expansion order;
+//                  among the block's Gaussians hitting that tile (one warp
+//                  ballot per tile; a Gaussian hits a tile at most once):
+//                  buckets hold their incidences in expansion order;
 //   k_seg_sort     one block per tile: stable LSD radix sort of the 31-bit
 //                  depth codes in shared memory (4 digit passes), then the
 //                  sorted compact keys, Gaussian ids and the emission bounds
@@ -48,44 +47,46 @@ __device__ __forceinline__ void for_each_tile(const Rect& r, int tiles_u, F&& f)
     }
 }
 
-__device__ __forceinline__ bool rect_has(const Rect& r, int tv, int tu) {
-    return tv >= r.tv_lo && tv <= r.tv_hi && ((tu >= r.s1_lo && tu <= r.s1_hi) || tu <= r.s2_hi);
+// bits lo..hi (inclusive) of a word; empty if hi < lo (tiles_u <= 23 < 32)
+__device__ __forceinline__ uint32_t bit_range(int lo, int hi) {
+    return hi < lo ? 0u : ((2u << hi) - 1u) & ~((1u << lo) - 1u);
 }
 
-// hit[t][w] = ballot of warp w's Gaussians whose rectangle contains tile t
-// (one ballot per tile: no atomics, and a Gaussian hits a tile at most once)
+// hit[t][w] = mask of warp w's lanes whose Gaussian's rectangle contains tile
+// t: per tile row, each lane's row of column bits, transposed across the warp
+// (32 x 32 bit transpose by shuffles), lane tu then holds column tu's mask
 __device__ __forceinline__ void block_hit_masks(const Rect& r, int tiles_u, int n_tiles,
                                                 uint32_t (*hit)[BK_BLK / 32]) {
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int tv = 0, tu = 0;
-    for (int t = 0; t < n_tiles; ++t) {
-        const unsigned m = __ballot_sync(0xffffffffu, rect_has(r, tv, tu));
-        if (lane == 0) hit[t][wid] = m;
-        if (++tu == tiles_u) {
-            tu = 0;
-            ++tv;
+    const uint32_t cols = bit_range(r.s1_lo, r.s1_hi) | bit_range(0, r.s2_hi);
+    const int tiles_v = n_tiles / tiles_u;
+    for (int tv = 0; tv < tiles_v; ++tv) {
+        uint32_t x = (tv >= r.tv_lo && tv <= r.tv_hi) ? cols : 0u;
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+            const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                             : j == 2 ? 0x33333333u : 0x55555555u;
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+            x = (lane & j) == 0 ? (x & m) | ((y & m) << j) : (x & ~m) | ((y & ~m) >> j);
         }
+        if (lane < tiles_u) hit[tv * tiles_u + lane][wid] = x;
     }
 }
 
 // per (tile, block) incidence counts, tile-major: tab[t * nb + b]
+// (shared-memory atomics: a count does not depend on the order)
 __global__ void __launch_bounds__(BK_BLK) k_tile_count(int n, const Rect* __restrict__ rects, int tiles_u,
                                                        int n_tiles, int nb, uint32_t* __restrict__ tab) {
-    constexpr int NW = BK_BLK / 32;
-    __shared__ uint32_t hit[BK_MAX_TILES][NW];
-    const int g = blockIdx.x * BK_BLK + threadIdx.x;
-    Rect r;
-    r.tv_lo = 1;
-    r.tv_hi = 0;
-    if (g < n) r = rects[g];
-    block_hit_masks(r, tiles_u, n_tiles, hit);
+    __shared__ uint32_t h[BK_MAX_TILES];
+    for (int t = threadIdx.x; t < n_tiles; t += BK_BLK) h[t] = 0;
     __syncthreads();
-    for (int t = threadIdx.x; t < n_tiles; t += BK_BLK) {
-        uint32_t c = 0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) c += __popc(hit[t][w]);
-        tab[(size_t)t * nb + blockIdx.x] = c;
+    const int g = blockIdx.x * BK_BLK + threadIdx.x;
+    if (g < n) {
+        const Rect r = rects[g];
+        for_each_tile(r, tiles_u, [&](int t, int) { atomicAdd(&h[t], 1u); });
     }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += BK_BLK) tab[(size_t)t * nb + blockIdx.x] = h[t];
 }
 
 // warp per tile: exclusive scan of its blocks' counts in place, total -> tot[t]
@@ -144,6 +145,8 @@ __global__ void __launch_bounds__(BK_BLK) k_fill_stable(int n, const Rect* __res
     const int g = blockIdx.x * BK_BLK + threadIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     Rect r;
+    r.s1_lo = 0;
+    r.s1_hi = r.s2_hi = -1;
     r.tv_lo = 1;
     r.tv_hi = 0;
     if (g < n) r = rects[g];
