@@ -190,7 +190,27 @@ def sort_end_bit(n_tiles: int) -> int:
     return 31 + max(0, math.ceil(math.log2(max(n_tiles, 1))))
 
 
-def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand", m_dev_ptr: int | None = None):
+def _fresh(name: str, n: int, dtype, dev) -> torch.Tensor:
+    return torch.empty(n, dtype=dtype, device=dev)
+
+
+_PBUF: dict = {}
+
+
+def _persistent(name: str, n: int, dtype, dev) -> torch.Tensor:
+    """Buffers of the early by-Gaussian index, reused every step: it is built on
+    the side stream, and per-step allocations there made the caching allocator
+    grow new segments mid-step (multi-ms host stalls at 1M Gaussians).  Safe to
+    reuse: step i+1's index starts behind its own K6, after step i's backward."""
+    key = (name, str(dev), dtype)
+    t = _PBUF.get(key)
+    if t is None or t.numel() < n:
+        t = torch.empty(max(n + n // 4, 1), dtype=dtype, device=dev)
+        _PBUF[key] = t
+    return t[:n]
+
+
+def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand", m_dev_ptr: int | None = None, alloc=_fresh):
     """K3: stable sort of u64 keys with u32 payload; returns sorted (keys, vals).
 
     With `m_dev_ptr` (device address of a u32 count; hand-written sort only)
@@ -202,13 +222,13 @@ def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand", m_dev_ptr: int 
     if m <= 1:
         return ckeys, vals
     end_bit = int(end_bit)
-    kalt = torch.empty_like(ckeys)
-    valt = torch.empty_like(vals)
+    kalt = alloc("sort_kalt", m, ckeys.dtype, dev)
+    valt = alloc("sort_valt", m, vals.dtype, dev)
     lib = _native.load()
     res = _native.C.c_int(0)
     if backend == "hand":
         tb = int(lib.rfs_sort_temp_bytes(m, end_bit))
-        temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
+        temp = alloc("sort_temp", max(tb, 16), torch.uint8, dev)
         _native.call("rfs_sort_pairs_u64", _ptr(ckeys), _ptr(vals), _ptr(kalt), _ptr(valt), m, end_bit,
                      _ptr(temp), tb, _native.C.byref(res), m_dev_ptr, _stream())
         _native.launch_counter["kernels"] += 2 + (end_bit + 7) // 8
@@ -403,14 +423,10 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                 # on the side stream, right behind K6: overlaps psi, the forward composite and the loss
                 side = _side_stream(dev)
                 side.wait_event(ev_hits)
-                main = torch.cuda.current_stream(dev)
                 with torch.cuda.stream(side):
-                    gauss_index(early, h_cap)
+                    gauss_index(early, h_cap, _persistent)
                     ready = torch.cuda.Event()
                     ready.record(side)
-                for v in early.gidx.values():
-                    if isinstance(v, torch.Tensor):
-                        v.record_stream(main)
                 early.gidx["ready"] = ready
             else:
                 gauss_index(early, h_cap)
@@ -512,7 +528,7 @@ def forward(geo: Geometry, psi: torch.Tensor) -> torch.Tensor:
     return _forward_raw(geo.slab, geo.ray_counts, geo.hcap, psi, geo.n_az, geo.n_el)
 
 
-def gauss_index(geo: Geometry, h_cap: int | None = None) -> None:
+def gauss_index(geo: Geometry, h_cap: int | None = None, alloc=_fresh) -> None:
     """K8i: by-Gaussian index of the live hits (TX independent, cached on geo).
 
     Hits sorted by Gaussian id with a stable sort, so within a Gaussian they
@@ -532,41 +548,41 @@ def gauss_index(geo: Geometry, h_cap: int | None = None) -> None:
     if geo.sort_backend == "hand" and _CAPS["gindex"] == "count" and geo.n > 0:
         # gindex.cu: counting + per-Gaussian segment sorts, no global radix sort
         n = geo.n
-        g_off = torch.empty(n + 1, dtype=torch.int32, device=dev)
-        scratch = torch.empty(int(lib.rfs_gauss_index_scratch_elems(n, cap)), dtype=torch.int32, device=dev)
-        temp = torch.empty(int(lib.rfs_scan_temp_elems(n)), dtype=torch.int32, device=dev)
+        g_off = alloc("gi_goff", n + 1, torch.int32, dev)
+        scratch = alloc("gi_scratch", int(lib.rfs_gauss_index_scratch_elems(n, cap)), torch.int32, dev)
+        temp = alloc("gi_temp", int(lib.rfs_scan_temp_elems(n)), torch.int32, dev)
         c1 = max(cap, 1)
-        sorted_g = torch.empty(c1, dtype=torch.int64, device=dev)
-        s_slot = torch.empty(c1, dtype=torch.int32, device=dev)
-        s_ray = torch.empty(c1, dtype=torch.int32, device=dev)
-        s_w = torch.empty(c1, dtype=torch.float32, device=dev)
-        s_wt = torch.empty(c1, dtype=torch.complex64, device=dev)
+        sorted_g = alloc("gi_sorted_g", c1, torch.int64, dev)
+        s_slot = alloc("gi_s_slot", c1, torch.int32, dev)
+        s_ray = alloc("gi_s_ray", c1, torch.int32, dev)
+        s_w = alloc("gi_s_w", c1, torch.float32, dev)
+        s_wt = alloc("gi_s_wt", c1, torch.complex64, dev)
         _native.call("rfs_gauss_index", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, n, cap, _ptr(scratch),
                      _ptr(temp), _ptr(g_off), _ptr(sorted_g), _ptr(s_slot), _ptr(s_ray), _ptr(s_w), _ptr(s_wt), st)
         geo.gidx = {"h": cap, "h_dev": g_off.data_ptr() + 4 * n, "tot": g_off[n:], "sorted_g": sorted_g,
                     "g_off": g_off, "s_ray": s_ray, "s_w": s_w, "s_wt": s_wt, "s_slot": s_slot}
         return
-    ray_off = torch.empty(R, dtype=torch.int32, device=dev)
-    tot = torch.empty(1, dtype=torch.int32, device=dev)
-    temp = torch.empty(int(lib.rfs_scan_temp_elems(R)), dtype=torch.int32, device=dev)
+    ray_off = alloc("gi_ray_off", R, torch.int32, dev)
+    tot = alloc("gi_tot", 1, torch.int32, dev)
+    temp = alloc("gi_rtemp", int(lib.rfs_scan_temp_elems(R)), torch.int32, dev)
     _native.call("rfs_exclusive_scan_u32", _ptr(geo.ray_counts), R, _ptr(ray_off), _ptr(tot), _ptr(temp), st)
     # hit keys land at ray_off[r] + k < H; positions >= cap are never read (H <= cap is checked)
-    keys = torch.empty(max(R * geo.hcap, 1), dtype=torch.int64, device=dev)
-    slots = torch.empty(max(R * geo.hcap, 1), dtype=torch.int32, device=dev)
+    keys = alloc("gi_keys", max(R * geo.hcap, 1), torch.int64, dev)
+    slots = alloc("gi_slots", max(R * geo.hcap, 1), torch.int32, dev)
     _native.call("rfs_hit_keys", _ptr(geo.slab), _ptr(geo.ray_counts), _ptr(ray_off), geo.hcap, R, _ptr(keys),
                  _ptr(slots), st)
     bits = max(1, math.ceil(math.log2(max(geo.n, 2))))
     hd = tot.data_ptr()
     if cap > 1:
         if geo.sort_backend == "hand":
-            keys, slots = sort_pairs(keys[:cap], slots[:cap], bits, "hand", hd)
+            keys, slots = sort_pairs(keys[:cap], slots[:cap], bits, "hand", hd, alloc)
         else:  # cub needs the exact count: only reached after the statistics read
             keys, slots = sort_pairs(keys[:cap], slots[:cap], bits, geo.sort_backend)
-    g_off = torch.empty(geo.n + 1, dtype=torch.int32, device=dev)
+    g_off = alloc("gi_goff", geo.n + 1, torch.int32, dev)
     _native.call("rfs_gauss_offsets", _ptr(keys), cap, hd, geo.n, _ptr(g_off), st)
-    s_ray = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-    s_w = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
-    s_wt = torch.empty(max(cap, 1), dtype=torch.complex64, device=dev)
+    s_ray = alloc("gi_s_ray", max(cap, 1), torch.int32, dev)
+    s_w = alloc("gi_s_w", max(cap, 1), torch.float32, dev)
+    s_wt = alloc("gi_s_wt", max(cap, 1), torch.complex64, dev)
     _native.call("rfs_gather_sorted", _ptr(slots), cap, hd, geo.hcap, _ptr(geo.slab), _ptr(s_ray), _ptr(s_w),
                  _ptr(s_wt), None, st)
     geo.gidx = {"h": cap, "h_dev": hd, "tot": tot, "sorted_g": keys, "g_off": g_off, "s_ray": s_ray, "s_w": s_w,
