@@ -101,7 +101,7 @@ struct FwdSmem {
 // separable passes slide an 11-value window through registers, SEG outputs
 // per thread (one shared-memory load per input instead of eleven).
 // grid (v tiles, u tiles, frames)
-__global__ void __launch_bounds__(LT) k_ssim_fwd(const float2* __restrict__ S, const float* __restrict__ pred,
+__global__ void __launch_bounds__(LT, 5) k_ssim_fwd(const float2* __restrict__ S, const float* __restrict__ pred,
                                                  const float* __restrict__ gt,
                                                  const float2* __restrict__ range, int n_az, int n_el,
                                                  float* __restrict__ maps, double* __restrict__ part) {
@@ -240,7 +240,7 @@ struct BwdSmem {
     float h[3][HU][TVP];
 };
 
-__global__ void __launch_bounds__(LT) k_ssim_bwd(const float2* __restrict__ S, const float* __restrict__ pred,
+__global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S, const float* __restrict__ pred,
                                                  const float* __restrict__ gt, const float* __restrict__ maps,
                                                  int n_az, int n_el, float w1, float ws, float wf,
                                                  float* __restrict__ grad, float2* __restrict__ lam) {
