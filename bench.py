@@ -20,6 +20,7 @@ pure Python, so there is no compiled `oracle/_ref` to run.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -231,6 +232,8 @@ def run_ours(args):
     # step's one hit-statistics read.  Each step is bracketed by its own
     # events; the L2 flush between steps sits outside them.
     all_marks = []
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed host loops (re-enabled after)
     for _ in range(args.steps):
         flush.fill_(1)  # evict L2 between steps (outside the timed events)
         marks = []
@@ -240,6 +243,7 @@ def run_ours(args):
         step(marks)
         all_marks.append(marks)
     torch.cuda.synchronize()
+    gc.enable()
     for marks in all_marks:
         per_step.append(marks[0][1].elapsed_time(marks[-1][1]))
         for (_, a), (name, bb) in zip(marks[:-1], marks[1:]):
@@ -305,11 +309,14 @@ def run_ours(args):
             dist.barrier()
         es = torch.cuda.Event(enable_timing=True)
         ee = torch.cuda.Event(enable_timing=True)
+        gc.collect()
+        gc.disable()
         es.record()
         for _ in range(args.steps):
             _, h2d, d2h = api.train_step_host(ds, txh, gth, reph, sort_backend=args.sort, reduce_fn=red)
         ee.record()
         torch.cuda.synchronize()
+        gc.enable()
         te = es.elapsed_time(ee)
         if world > 1:
             tt = torch.tensor([te], device=dev, dtype=torch.float64)
