@@ -123,10 +123,15 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream);
  * halves and merged (same hit lists, shorter critical path); a ray whose
  * second half holds more than bcap hits goes to the slow path. */
 size_t rfs_hits_split_bytes(int n_rays, int bcap);
+/* patch_ws (nullable, rfs_hits_patch_bytes(m_cap, n_tiles) bytes, m_cap >= the
+ * length of vals): first filter each tile list by the warp cone of each of the
+ * tile's 8 ray patches (k_patch_lists, with per-list emission bounds) and
+ * stream those -- the same hit lists; ignored when split_min > 0. */
+size_t rfs_hits_patch_bytes(int m_cap, int n_tiles);
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
              int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, int split_min,
-             int bcap, void* split_ws, void* stream);
+             int bcap, void* split_ws, int m_cap, void* patch_ws, void* stream);
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,

@@ -40,8 +40,9 @@ _SIGS = {
     "rfs_lower_bounds": (i32, [vp, i32, vp, vp, vp, vp]),
     "rfs_ray_dirs": (i32, [i32, i32, vp, vp]),
     "rfs_hits_split_bytes": (sz, [i32, i32]),
+    "rfs_hits_patch_bytes": (sz, [i32, i32]),
     "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, i32,
-                       vp, vp]),
+                       vp, i32, vp, vp]),
     "rfs_hits_slow": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, vp, vp, vp, vp, vp, i32,
                             vp, vp, vp]),
     "rfs_psi": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),

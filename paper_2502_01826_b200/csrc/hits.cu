@@ -218,12 +218,24 @@ struct KSplit {
     float* b_w;
 };
 
+// Per-patch candidate lists (k_patch_lists): a tile list filtered by the
+// warp cone of each of its 8 ray patches (4 x 8 rays), with the emission
+// bounds recomputed over each filtered list.  K6 then streams only the
+// cone-relevant candidates (~15 % of the tile list at config 2): the same
+// hits (the cone test never rejects a hit), far fewer chunks per warp.
+struct KPatch {
+    const uint32_t* vals;  // [8 * M]: tile t's patch p list at 8 * start(t) + p * len(t); null: off
+    const double* lb;      // same layout: min over the list's later entries of lbv
+    const int* cnt;        // [n_tiles * 8]
+};
+
 template <int CH>
 struct WarpStage {
     float4 sph[CH];
     float4 wh[CH][4];
     uint32_t g[CH];
     double gd[CH][GDS];  // fp64 records of the chunk's cone-relevant candidates (by slot)
+    double lbs[CH];      // patch mode: emission bound after candidate j (lb of candidate j + 1)
 };
 
 template <int PCAP, int NT, int CH>
@@ -240,7 +252,7 @@ __global__ void __launch_bounds__(NT) k_hits(
     const float4* __restrict__ sph, const float4* __restrict__ whit, const RfsGeom* __restrict__ geom,
     const double* __restrict__ dirs, double rx0, double rx1, double rx2, double min_t, int n_az, int n_el,
     int tiles_u, int hcap, RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ slow_list,
-    int* __restrict__ stats, uint8_t* __restrict__ used, KSplit ks) {
+    int* __restrict__ stats, uint8_t* __restrict__ used, KSplit ks, KPatch kp) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HitsSmem<PCAP, NT, CH>& S = *reinterpret_cast<HitsSmem<PCAP, NT, CH>*>(smem_raw);
     constexpr int PARTS = 256 / NT;
@@ -277,11 +289,25 @@ __global__ void __launch_bounds__(NT) k_hits(
     double head_t = DINF;
     const int2 rg = ranges[tile];
     const int Lt = rg.y - rg.x;
-    const bool split = ks.split_min > 0 && Lt > ks.split_min;
+    const bool pmode = kp.vals != nullptr;  // this warp's filtered patch list
+    const bool split = !pmode && ks.split_min > 0 && Lt > ks.split_min;
     const bool second = wblk >= PARTS;  // piece B of a split list
     if (second && !split) return;         // block-uniform
     const int mid = split ? rg.x + Lt / 2 : rg.y;
-    const int c_lo = second ? mid : rg.x, c_hi = second ? rg.y : mid;
+    const uint32_t* vl = vals;
+    const double* lbp = lb;
+    int c_lo, c_hi, c_end;
+    if (pmode) {
+        const size_t pb = 8 * (size_t)rg.x + (size_t)q * (size_t)Lt;
+        vl = kp.vals + pb;
+        lbp = kp.lb + pb;
+        c_lo = 0;
+        c_hi = c_end = kp.cnt[tile * 8 + q];
+    } else {
+        c_lo = second ? mid : rg.x;
+        c_hi = second ? rg.y : mid;
+        c_end = rg.y;
+    }
     int b_n = 0;
     WarpStage<CH>& W = S.ws[wid];
 
@@ -309,10 +335,10 @@ __global__ void __launch_bounds__(NT) k_hits(
     // register prefetch of the next chunk's filter data (lane j loads candidate base + j)
     uint32_t pf_g = 0;
     float4 pf_s = make_float4(0.f, 0.f, 0.f, 0.f), pf_w[4];
-    double pf_lb = DINF;
+    double pf_lb = DINF, pf_lbs = DINF;
     // candidate ids run one chunk further ahead than their records, so the
     // record gathers never wait on the id load (in-order issue)
-    uint32_t nx_g = c_lo + lane < c_hi ? vals[c_lo + lane] : 0u;
+    uint32_t nx_g = c_lo + lane < c_hi ? vl[c_lo + lane] : 0u;
     auto prefetch = [&](int b0) {
         if (b0 + lane < c_hi) {
             pf_g = nx_g;
@@ -320,13 +346,35 @@ __global__ void __launch_bounds__(NT) k_hits(
 #pragma unroll
             for (int k = 0; k < 4; ++k) pf_w[k] = __ldg(&whit[4 * pf_g + k]);
         }
-        if (b0 + CH + lane < c_hi) nx_g = vals[b0 + CH + lane];
+        if (b0 + CH + lane < c_hi) nx_g = vl[b0 + CH + lane];
         // bound of every candidate after this chunk -- for piece A's last chunk
         // that is B's first candidate, mid
         const int nxt = min(b0 + CH, c_hi);
-        pf_lb = nxt < rg.y ? lb[nxt] : DINF;
+        pf_lb = nxt < c_end ? lbp[nxt] : DINF;
+        if (pmode) pf_lbs = b0 + lane + 1 < c_end ? lbp[b0 + lane + 1] : DINF;
     };
     prefetch(c_lo);
+    // emit every pending hit below `bound` (in (t_mid, g) order)
+    auto emit_until = [&](double bound) {
+        while (!st.done && head_t < bound) {
+            if (second) {  // piece B: into its own sorted list, no T / termination
+                if (b_n == ks.bcap) {
+                    pend_over = true;
+                    st.done = true;
+                    break;
+                }
+                const size_t o = (size_t)r * ks.bcap + b_n++;
+                ks.b_t[o] = S.pt[head][tid];
+                ks.b_g[o] = S.pg[head][tid];
+                ks.b_w[o] = S.pw[head][tid];
+            } else {
+                emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
+            }
+            head = (head + 1) & (PCAP - 1);
+            --npend;
+            head_t = npend > 0 ? S.pt[head][tid] : DINF;
+        }
+    };
 
     for (int base = c_lo; base < c_hi; base += CH) {
         if (__all_sync(0xffffffffu, st.done)) break;
@@ -336,10 +384,11 @@ __global__ void __launch_bounds__(NT) k_hits(
         if (lane < nb) {
             W.g[lane] = pf_g;
             W.sph[lane] = pf_s;
+            if (pmode) W.lbs[lane] = pf_lbs;
 #pragma unroll
             for (int k = 0; k < 4; ++k) W.wh[lane][k] = pf_w[k];
             const float ang = th_p + pf_w[3].y;
-            if (ang >= 3.1415f) {
+            if (pmode || ang >= 3.1415f) {  // patch lists are cone-filtered already
                 rel = true;
             } else {
                 // cos(th_p + th_g) by angle addition (cos/sin th_g precomputed in K1)
@@ -423,26 +472,16 @@ __global__ void __launch_bounds__(NT) k_hits(
                 ++npend;
                 max_pend = max(max_pend, npend);
                 head_t = fmin(head_t, t_mid);
+                // patch lists are dense: emit as soon as a hit precedes every
+                // later candidate (this lane has tested all candidates <= j),
+                // which keeps the pending ring short
+                if (pmode) {
+                    emit_until(W.lbs[j]);
+                    if (st.done) break;
+                }
             }
             // 4. emit every pending hit that precedes all later candidates
-            while (!st.done && head_t < lb_next) {
-                if (second) {  // piece B: into its own sorted list, no T / termination
-                    if (b_n == ks.bcap) {
-                        pend_over = true;
-                        st.done = true;
-                        break;
-                    }
-                    const size_t o = (size_t)r * ks.bcap + b_n++;
-                    ks.b_t[o] = S.pt[head][tid];
-                    ks.b_g[o] = S.pg[head][tid];
-                    ks.b_w[o] = S.pw[head][tid];
-                } else {
-                    emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
-                }
-                head = (head + 1) & (PCAP - 1);
-                --npend;
-                head_t = npend > 0 ? S.pt[head][tid] : DINF;
-            }
+            emit_until(lb_next);
         }
         __syncwarp();
     }
@@ -528,6 +567,128 @@ __global__ void __launch_bounds__(NT) k_hits(
     if (st.hcap_over) atomicAdd(&stats[1], 1);
     atomicMax(&stats[2], st.live);
     atomicAdd(&stats[3], min(st.live, hcap));
+}
+
+// K6a: the per-patch candidate lists of KPatch.  Block per tile, warp w
+// computes patch w's cone exactly as k_hits does; every candidate is tested
+// against the 8 cones, compacted per patch in list order (ballots + warp
+// prefix), then each patch's emission bounds are the suffix minima of lbv
+// over its own list.
+constexpr int PL_NT = 1024;  // k_patch_lists threads: one tile list round of 1024 candidates
+__global__ void __launch_bounds__(PL_NT) k_patch_lists(const int2* __restrict__ ranges, const uint32_t* __restrict__ vals,
+                                                       const float4* __restrict__ sph, const float4* __restrict__ whit,
+                                                       const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
+                                                       int n_az, int n_el, int tiles_u, uint32_t* __restrict__ pvals,
+                                                       double* __restrict__ plb, int* __restrict__ pcnt) {
+    constexpr int NW = PL_NT / 32;
+    __shared__ float cone[8][6];  // cx, cy, cz, th_p, cos_p, sin_p
+    __shared__ int has[8], run[8];
+    __shared__ unsigned wb[NW][8];  // [warp][patch] ballots of the current round
+    const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (wid < 8) {  // warp q: the cone of patch q, as k_hits computes it
+        const int q = wid, pu = q >> 1, pv = q & 1;
+        const int u = (tile % tiles_u) * RFS_TILE + 4 * pu + (lane >> 3);
+        const int v = (tile / tiles_u) * RFS_TILE + 8 * pv + (lane & 7);
+        const bool valid = u < n_az && v < n_el;
+        const int r = valid ? u * n_el + v : 0;
+        const float fx = (float)dirs[3 * r], fy = (float)dirs[3 * r + 1], fz = (float)dirs[3 * r + 2];
+        float cx = valid ? fx : 0.f, cy = valid ? fy : 0.f, cz = valid ? fz : 0.f;
+        cx = warp_sum(cx);
+        cy = warp_sum(cy);
+        cz = warp_sum(cz);
+        {
+            const float inv = rsqrtf(fmaxf(cx * cx + cy * cy + cz * cz, 1e-30f));
+            cx *= inv;
+            cy *= inv;
+            cz *= inv;
+        }
+        float cmin = valid ? cx * fx + cy * fy + cz * fz : 1.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+        const float th_p = acosf(fminf(cmin, 1.f)) + 1e-4f;
+        float sin_p, cos_p;
+        sincosf(th_p, &sin_p, &cos_p);
+        const bool any = __any_sync(0xffffffffu, valid);
+        if (lane == 0) {
+            cone[q][0] = cx;
+            cone[q][1] = cy;
+            cone[q][2] = cz;
+            cone[q][3] = th_p;
+            cone[q][4] = cos_p;
+            cone[q][5] = sin_p;
+            has[q] = any;
+            run[q] = 0;
+        }
+    }
+    __syncthreads();
+    const int2 rg = ranges[tile];
+    const size_t L = (size_t)(rg.y - rg.x), tb = 8 * (size_t)rg.x;
+    unsigned lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    for (int b0 = rg.x; b0 < rg.y; b0 += PL_NT) {
+        const int i = b0 + tid;
+        uint32_t g = 0, pm = 0;
+        double lbv = 0.0;
+        if (i < rg.y) {
+            g = vals[i];
+            const float4 sp = __ldg(&sph[g]);
+            const float4 w3 = __ldg(&whit[4 * g + 3]);
+            lbv = __ldg(&geom[g].lbv);
+            const float m2 = sp.x * sp.x + sp.y * sp.y + sp.z * sp.z;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                if (!has[p]) continue;
+                bool rel;
+                const float ang = cone[p][3] + w3.y;
+                if (ang >= 3.1415f) {
+                    rel = true;
+                } else {  // the k_hits test
+                    const float dotc = (cone[p][0] * sp.x + cone[p][1] * sp.y + cone[p][2] * sp.z) * rsqrtf(m2);
+                    rel = dotc >= cone[p][4] * w3.z - cone[p][5] * w3.w - 1e-5f;
+                }
+                pm |= (uint32_t)rel << p;
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            const unsigned m = __ballot_sync(0xffffffffu, (pm >> p) & 1u);
+            if (lane == 0) wb[wid][p] = m;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            if (!((pm >> p) & 1u)) continue;
+            uint32_t pos = (uint32_t)run[p] + __popc(wb[wid][p] & lt);
+            for (int w = 0; w < wid; ++w) pos += __popc(wb[w][p]);
+            pvals[tb + (size_t)p * L + pos] = g;
+            plb[tb + (size_t)p * L + pos] = lbv;  // raw lbv; suffix minima below
+        }
+        __syncthreads();
+        if (tid < 8) {
+            int t = 0;
+            for (int w = 0; w < NW; ++w) t += __popc(wb[w][tid]);
+            run[tid] += t;
+        }
+        __syncthreads();
+    }
+    // warps 0-7: suffix minima of lbv over patch list p (contiguous, in place)
+    if (wid >= 8) return;
+    const int cnt = run[wid];
+    if (lane == 0) pcnt[tile * 8 + wid] = cnt;
+    double* pl = plb + tb + (size_t)wid * L;
+    double carry = INFINITY;
+    for (int k0 = ((cnt - 1) >> 5) << 5; k0 >= 0; k0 -= 32) {
+        const int k = k0 + lane;
+        double v = k < cnt ? pl[k] : INFINITY;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_down_sync(0xffffffffu, v, o);
+            if (lane + o < 32) v = fmin(v, y);
+        }
+        v = fmin(v, carry);
+        if (k < cnt) pl[k] = v;
+        carry = __shfl_sync(0xffffffffu, v, 0);
+    }
 }
 
 // Merge of a split list's two pieces (see KSplit): thread per ray parked by A.
@@ -668,7 +829,7 @@ template <int PCAP, int NT, int CH>
 int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const double* lb, const void* sph,
                 const void* whit, const void* geom, const double* dirs, const double* rx, double min_t, int n_az,
                 int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used,
-                const KSplit& ks, cudaStream_t st) {
+                const KSplit& ks, const KPatch& kp, cudaStream_t st) {
     static bool attr = false;
     size_t smem = sizeof(HitsSmem<PCAP, NT, CH>);
     if (!attr) {
@@ -683,7 +844,7 @@ int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const doub
     const int per_tile = (256 / NT) * (ks.split_min > 0 ? 2 : 1);
     k_hits<PCAP, NT, CH><<<n_tiles * per_tile, NT, smem, st>>>(
         (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom, dirs, rx[0],
-        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used, ks);
+        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used, ks, kp);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -717,10 +878,15 @@ size_t rfs_hits_split_bytes(int n_rays, int bcap) {
     return R * (4 * sizeof(int) + 2 * sizeof(double)) + R * (KS_ACAP + B) * 16;
 }
 
+size_t rfs_hits_patch_bytes(int m_cap, int n_tiles) {
+    const size_t M = (size_t)(m_cap > 0 ? m_cap : 0), T = (size_t)(n_tiles > 0 ? n_tiles : 0);
+    return 8 * M * sizeof(double) + 8 * M * sizeof(uint32_t) + 8 * T * sizeof(int) + 64;
+}
+
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
              int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, int split_min,
-             int bcap, void* split_ws, void* stream) {
+             int bcap, void* split_ws, int m_cap, void* patch_ws, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (used && n > 0) RFS_CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)n, st));
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
@@ -754,6 +920,18 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
         ks.b_w = (float*)take(B * 4);
         RFS_CUDA_TRY(cudaMemsetAsync(ks.flag, 0, Rz * 4, st));
     }
+    KPatch kp{};
+    if (patch_ws && ks.split_min <= 0 && m_cap > 0) {
+        double* plb = (double*)patch_ws;
+        uint32_t* pv = (uint32_t*)(plb + 8 * (size_t)m_cap);
+        int* pc = (int*)(pv + 8 * (size_t)m_cap);
+        k_patch_lists<<<n_tiles, PL_NT, 0, st>>>((const int2*)ranges, vals, (const float4*)sph, (const float4*)whit,
+                                               (const RfsGeom*)geom, dirs, n_az, n_el, tiles_u, pv, plb, pc);
+        RFS_LAUNCH_CHECK();
+        kp.vals = pv;
+        kp.lb = plb;
+        kp.cnt = pc;
+    }
     int rc;
     // 64-thread blocks: 7 per SM, so 68 of a 360x180 grid's 1104 blocks start
     // late (~90 us); 128-thread blocks (all resident) measured no faster -- the
@@ -761,13 +939,13 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
     // (tools/k6_timing.py: warp duration mean 124 us, max 238 us at 100k)
     if (pcap <= 16)
         rc = launch_hits<16, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, kp, st);
     else if (pcap <= 32)
         rc = launch_hits<32, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, kp, st);
     else
         rc = launch_hits<64, 32, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, kp, st);
     if (rc != RFS_OK) return rc;
     if (ks.split_min > 0) {
         k_hits_merge<<<rfs_ceil_div(R, 128), 128, 0, st>>>(R, hcap, ks, (const RfsGeom*)geom, (RfsHit*)slab, counts,

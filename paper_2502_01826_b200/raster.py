@@ -153,6 +153,9 @@ _CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {},
          # global onesweep) or "count" (gindex.cu; bitwise the same, measured
          # ~10 us slower at config 2: 119 vs 111 us)
          "gindex": os.environ.get("RFS_GINDEX", "radix"),
+         # K6 streams per-patch cone-filtered candidate lists (k_patch_lists): bitwise the
+         # same hits, K6 203 -> 182 us, but the prepass costs 58 us -- off until it is cheaper
+         "patch_lists": os.environ.get("RFS_K6_PATCH", "0") == "1",
          # the early by-Gaussian index on the side stream (overlapping psi / K7 / loss)
          "index_side": os.environ.get("RFS_INDEX_SIDE", "1") == "1"}
 _DIRS: dict = {}
@@ -393,12 +396,18 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         slab = torch.empty(R * hc * 16, dtype=torch.uint8, device=dev)
         split_min, bcap = _CAPS["split_min"], _CAPS["bcap"]
         split_ws = _split_ws(dev, R, bcap) if split_min > 0 else None
+        mcap_v = int(vals.numel())
+        patch_ws = (_persistent("k6_patch", int(lib.rfs_hits_patch_bytes(mcap_v, n_tiles)), torch.uint8, dev)
+                    if _CAPS["patch_lists"] and split_ws is None else None)
         _native.call("rfs_hits", _ptr(ranges), n_tiles, _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit), _ptr(geom),
                      _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, pc, _ptr(slab), _ptr(ray_counts),
                      _ptr(slow), _ptr(stats), _ptr(used), n, split_min, bcap,
-                     _ptr(split_ws) if split_ws is not None else None, st)
+                     _ptr(split_ws) if split_ws is not None else None, mcap_v,
+                     _ptr(patch_ws) if patch_ws is not None else None, st)
         if split_ws is not None:
             _native.launch_counter["kernels"] += 1  # k_hits_merge
+        if patch_ws is not None:
+            _native.launch_counter["kernels"] += 1  # k_patch_lists
         ev_hits = torch.cuda.Event()
         ev_hits.record()
         _mark(marks, "hits")

@@ -368,6 +368,35 @@ def test_counting_gauss_index_bitwise_equals_radix(which):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["config1", "special_", "hemi_", "bench20k", "bench100k"])
+def test_patch_lists_bitwise_equal_full_lists(which):
+    """K6 on per-patch cone-filtered candidate lists (k_patch_lists) must give
+    bitwise the hit lists, used marks and spectra of K6 on the full tile lists."""
+    import torch
+
+    if which == "config1":
+        s = config1_scene()
+    elif which.endswith("_"):
+        s = scene_from(load("edge_scenes.npz"), which)
+    else:
+        s = round_to_f32(bench_scene(np.random.default_rng(12), 20_000 if which == "bench20k" else 100_000, 360, 180))
+    ds = raster.DeviceScene.from_host(s, "cuda")
+    tx = torch.as_tensor(default_txs(3, seed=6), dtype=torch.float32, device="cuda")
+    saved = dict(raster._CAPS)
+    out = {}
+    try:
+        for mode in (False, True):
+            raster._CAPS["patch_lists"] = mode
+            g = raster.build_geometry(ds, psi_tx=tx, forward=True)
+            out[mode] = (g.S.cpu().numpy(), *_hit_lists(g), g.used.cpu().numpy(), g.stats[3])
+    finally:
+        raster._CAPS.update(saved)
+    for a, b in zip(out[False][:4], out[True][:4]):
+        np.testing.assert_array_equal(a, b)
+    assert out[False][4] == out[True][4]
+
+
 def _hit_lists(g):
     counts = g.ray_counts.cpu().numpy()
     slab = g.slab.view(-1, g.hcap, 16).cpu().numpy()
