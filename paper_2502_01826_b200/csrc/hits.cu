@@ -575,15 +575,17 @@ __global__ void __launch_bounds__(NT) k_hits(
 // prefix), then each patch's emission bounds are the suffix minima of lbv
 // over its own list.
 constexpr int PL_NT = 1024;  // k_patch_lists threads: one tile list round of 1024 candidates
-__global__ void __launch_bounds__(PL_NT) k_patch_lists(const int2* __restrict__ ranges, const uint32_t* __restrict__ vals,
+__global__ void __launch_bounds__(PL_NT, 2) k_patch_lists(const int2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                                                        const float4* __restrict__ sph, const float4* __restrict__ whit,
                                                        const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
                                                        int n_az, int n_el, int tiles_u, uint32_t* __restrict__ pvals,
                                                        double* __restrict__ plb, int* __restrict__ pcnt) {
     constexpr int NW = PL_NT / 32;
-    __shared__ float cone[8][6];  // cx, cy, cz, th_p, cos_p, sin_p
-    __shared__ int has[8], run[8];
+    __shared__ float4 ca[8];  // cx, cy, cz, th_p of patch p (a patch without rays never passes)
+    __shared__ float2 cb[8];  // cos_p, sin_p
+    __shared__ int run[8];
     __shared__ unsigned wb[NW][8];  // [warp][patch] ballots of the current round
+    __shared__ int wpre[NW][8];     // [warp][patch] first position of the warp's entries
     const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (wid < 8) {  // warp q: the cone of patch q, as k_hits computes it
         const int q = wid, pu = q >> 1, pv = q & 1;
@@ -610,13 +612,8 @@ __global__ void __launch_bounds__(PL_NT) k_patch_lists(const int2* __restrict__ 
         sincosf(th_p, &sin_p, &cos_p);
         const bool any = __any_sync(0xffffffffu, valid);
         if (lane == 0) {
-            cone[q][0] = cx;
-            cone[q][1] = cy;
-            cone[q][2] = cz;
-            cone[q][3] = th_p;
-            cone[q][4] = cos_p;
-            cone[q][5] = sin_p;
-            has[q] = any;
+            ca[q] = any ? make_float4(cx, cy, cz, th_p) : make_float4(0.f, 0.f, 0.f, -1e30f);
+            cb[q] = any ? make_float2(cos_p, sin_p) : make_float2(1e30f, -1e30f);
             run[q] = 0;
         }
     }
@@ -635,17 +632,14 @@ __global__ void __launch_bounds__(PL_NT) k_patch_lists(const int2* __restrict__ 
             const float4 w3 = __ldg(&whit[4 * g + 3]);
             lbv = __ldg(&geom[g].lbv);
             const float m2 = sp.x * sp.x + sp.y * sp.y + sp.z * sp.z;
+            const float rs = rsqrtf(m2);
 #pragma unroll
             for (int p = 0; p < 8; ++p) {
-                if (!has[p]) continue;
-                bool rel;
-                const float ang = cone[p][3] + w3.y;
-                if (ang >= 3.1415f) {
-                    rel = true;
-                } else {  // the k_hits test
-                    const float dotc = (cone[p][0] * sp.x + cone[p][1] * sp.y + cone[p][2] * sp.z) * rsqrtf(m2);
-                    rel = dotc >= cone[p][4] * w3.z - cone[p][5] * w3.w - 1e-5f;
-                }
+                const float4 c = ca[p];
+                const float2 d = cb[p];
+                // the k_hits test: cos(th_p + th_g) by angle addition
+                const float dotc = (c.x * sp.x + c.y * sp.y + c.z * sp.z) * rs;
+                const bool rel = (c.w + w3.y >= 3.1415f) || dotc >= d.x * w3.z - d.y * w3.w - 1e-5f;
                 pm |= (uint32_t)rel << p;
             }
         }
@@ -655,19 +649,21 @@ __global__ void __launch_bounds__(PL_NT) k_patch_lists(const int2* __restrict__ 
             if (lane == 0) wb[wid][p] = m;
         }
         __syncthreads();
+        if (tid < 8) {  // per patch: each warp's first position this round
+            int acc = run[tid];
+            for (int w = 0; w < NW; ++w) {
+                wpre[w][tid] = acc;
+                acc += __popc(wb[w][tid]);
+            }
+            run[tid] = acc;
+        }
+        __syncthreads();
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
             if (!((pm >> p) & 1u)) continue;
-            uint32_t pos = (uint32_t)run[p] + __popc(wb[wid][p] & lt);
-            for (int w = 0; w < wid; ++w) pos += __popc(wb[w][p]);
+            const uint32_t pos = wpre[wid][p] + __popc(wb[wid][p] & lt);
             pvals[tb + (size_t)p * L + pos] = g;
             plb[tb + (size_t)p * L + pos] = lbv;  // raw lbv; suffix minima below
-        }
-        __syncthreads();
-        if (tid < 8) {
-            int t = 0;
-            for (int w = 0; w < NW; ++w) t += __popc(wb[w][tid]);
-            run[tid] += t;
         }
         __syncthreads();
     }

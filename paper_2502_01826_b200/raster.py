@@ -154,7 +154,7 @@ _CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {},
          # ~10 us slower at config 2: 119 vs 111 us)
          "gindex": os.environ.get("RFS_GINDEX", "radix"),
          # K6 streams per-patch cone-filtered candidate lists (k_patch_lists): bitwise the
-         # same hits, K6 203 -> 182 us, but the prepass costs 58 us -- off until it is cheaper
+         # same hits, K6 203 -> 174 us, but the filter pass costs 31 us -- off until it is cheaper
          "patch_lists": os.environ.get("RFS_K6_PATCH", "0") == "1",
          # the early by-Gaussian index on the side stream (overlapping psi / K7 / loss)
          "index_side": os.environ.get("RFS_INDEX_SIDE", "1") == "1"}
