@@ -198,6 +198,7 @@ def _fresh(name: str, n: int, dtype, dev) -> torch.Tensor:
 
 
 _PBUF: dict = {}
+_INDEX_GEN = [0]  # generation of the index held in the persistent buffers
 
 
 def _persistent(name: str, n: int, dtype, dev) -> torch.Tensor:
@@ -436,7 +437,9 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                     gauss_index(early, h_cap, _persistent)
                     ready = torch.cuda.Event()
                     ready.record(side)
+                _INDEX_GEN[0] += 1
                 early.gidx["ready"] = ready
+                early.gidx["gen"] = _INDEX_GEN[0]
             else:
                 gauss_index(early, h_cap)
                 _mark(marks, "gauss_index")
@@ -651,6 +654,8 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     R = geo.n_rays
     lib = _native.load()
     built = geo.gidx is None
+    if geo.gidx is not None and geo.gidx.get("gen", _INDEX_GEN[0]) != _INDEX_GEN[0]:
+        geo.gidx = None  # its persistent buffers were reused by a later geometry: rebuild
     gauss_index(geo)
     gi = geo.gidx
     if "ready" in gi:  # built on the side stream

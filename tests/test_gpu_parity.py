@@ -397,6 +397,30 @@ def test_patch_lists_bitwise_equal_full_lists(which):
     assert out[False][4] == out[True][4]
 
 
+@pytest.mark.gpu
+def test_two_live_geometries_backward():
+    """The early by-Gaussian index lives in buffers reused by the next
+    geometry; a backward on an older geometry must rebuild its index, not read
+    the newer one's."""
+    import torch
+
+    s = round_to_f32(bench_scene(np.random.default_rng(3), 5_000, 72, 36))
+    s2 = round_to_f32(bench_scene(np.random.default_rng(4), 5_000, 72, 36))
+    ds, ds2 = raster.DeviceScene.from_host(s, "cuda"), raster.DeviceScene.from_host(s2, "cuda")
+    tx = torch.as_tensor(default_txs(2, seed=2), dtype=torch.float32, device="cuda")
+    for _ in range(2):  # second round: capacities known, the early index path is taken
+        g1 = raster.build_geometry(ds, psi_tx=tx, forward=True, index=True)
+        lam = (g1.S * 1e-3).contiguous()
+        ref = raster.backward(ds, g1, tx, lam, True, psi=g1.psi)
+        ref = {k: v.clone() for k, v in ref.items()}
+        g1b = raster.build_geometry(ds, psi_tx=tx, forward=True, index=True)
+        g2 = raster.build_geometry(ds2, psi_tx=tx, forward=True, index=True)  # reuses the buffers
+        out = raster.backward(ds, g1b, tx, lam, True, psi=g1b.psi)
+        for k in ref:
+            torch.testing.assert_close(out[k], ref[k], rtol=0, atol=0)
+        raster.backward(ds2, g2, tx, (g2.S * 1e-3).contiguous(), True, psi=g2.psi)
+
+
 def _hit_lists(g):
     counts = g.ray_counts.cpu().numpy()
     slab = g.slab.view(-1, g.hcap, 16).cpu().numpy()
