@@ -95,11 +95,14 @@ int rfs_tile_ranges(const uint64_t* ckeys, int m, const uint32_t* m_dev, int n_t
  * Gaussian ids and emission bounds -- bitwise the outputs of rfs_bin_fill +
  * rfs_sort_pairs_u64 + rfs_tile_ranges + rfs_lower_bounds (splat.py:337-343).
  * bcodes / bvals u32[cap] and temp (rfs_bin_bucket_temp_bytes) are scratch;
- * status is reserved.  Grids up to 512 tiles. */
+ * status is reserved.  patch_ws (nullable, rfs_hits_patch_bytes(cap, n_tiles)
+ * bytes; sph / whit / dirs then required): also K6's per-patch filtered lists
+ * (pass patch_built = 1 to rfs_hits).  Grids up to 512 tiles. */
 size_t rfs_bin_bucket_temp_bytes(int n, int n_az, int n_el, int cap);
 int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_az, int n_el, int cap, const void* geom,
                    uint32_t* bcodes, uint32_t* bvals, void* temp, uint64_t* ckeys, uint32_t* vals, int* ranges,
-                   double* lb, int* status, void* stream);
+                   double* lb, int* status, const void* sph, const void* whit, const double* dirs, void* patch_ws,
+                   void* stream);
 
 /* K4b: per-incidence emission bound for the exact streaming re-sort:
  * lb[i] = min_{j >= i, same tile} (depth_j - r3_j). */
@@ -126,12 +129,13 @@ size_t rfs_hits_split_bytes(int n_rays, int bcap);
 /* patch_ws (nullable, rfs_hits_patch_bytes(m_cap, n_tiles) bytes, m_cap >= the
  * length of vals): first filter each tile list by the warp cone of each of the
  * tile's 8 ray patches (k_patch_lists, with per-list emission bounds) and
- * stream those -- the same hit lists; ignored when split_min > 0. */
+ * stream those -- the same hit lists; ignored when split_min > 0.
+ * patch_built != 0: rfs_bin_bucket already wrote the lists into patch_ws. */
 size_t rfs_hits_patch_bytes(int m_cap, int n_tiles);
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
              int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, int split_min,
-             int bcap, void* split_ws, int m_cap, void* patch_ws, void* stream);
+             int bcap, void* split_ws, int m_cap, void* patch_ws, int patch_built, void* stream);
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,

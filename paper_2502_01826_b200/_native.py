@@ -36,13 +36,13 @@ _SIGS = {
     "rfs_sort_pairs_u64_cub": (i32, [vp, vp, vp, vp, i32, i32, vp, sz, C.POINTER(i32), vp]),
     "rfs_tile_ranges": (i32, [vp, i32, vp, i32, vp, vp]),
     "rfs_bin_bucket_temp_bytes": (sz, [i32, i32, i32, i32]),
-    "rfs_bin_bucket": (i32, [i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "rfs_bin_bucket": (i32, [i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rfs_lower_bounds": (i32, [vp, i32, vp, vp, vp, vp]),
     "rfs_ray_dirs": (i32, [i32, i32, vp, vp]),
     "rfs_hits_split_bytes": (sz, [i32, i32]),
     "rfs_hits_patch_bytes": (sz, [i32, i32]),
     "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, i32,
-                       vp, i32, vp, vp]),
+                       vp, i32, vp, i32, vp]),
     "rfs_hits_slow": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, vp, vp, vp, vp, vp, i32,
                             vp, vp, vp]),
     "rfs_psi": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),

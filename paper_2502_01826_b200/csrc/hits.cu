@@ -588,33 +588,13 @@ __global__ void __launch_bounds__(PL_NT, 2) k_patch_lists(const int2* __restrict
     __shared__ int wpre[NW][8];     // [warp][patch] first position of the warp's entries
     const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (wid < 8) {  // warp q: the cone of patch q, as k_hits computes it
-        const int q = wid, pu = q >> 1, pv = q & 1;
-        const int u = (tile % tiles_u) * RFS_TILE + 4 * pu + (lane >> 3);
-        const int v = (tile / tiles_u) * RFS_TILE + 8 * pv + (lane & 7);
-        const bool valid = u < n_az && v < n_el;
-        const int r = valid ? u * n_el + v : 0;
-        const float fx = (float)dirs[3 * r], fy = (float)dirs[3 * r + 1], fz = (float)dirs[3 * r + 2];
-        float cx = valid ? fx : 0.f, cy = valid ? fy : 0.f, cz = valid ? fz : 0.f;
-        cx = warp_sum(cx);
-        cy = warp_sum(cy);
-        cz = warp_sum(cz);
-        {
-            const float inv = rsqrtf(fmaxf(cx * cx + cy * cy + cz * cz, 1e-30f));
-            cx *= inv;
-            cy *= inv;
-            cz *= inv;
-        }
-        float cmin = valid ? cx * fx + cy * fy + cz * fz : 1.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
-        const float th_p = acosf(fminf(cmin, 1.f)) + 1e-4f;
-        float sin_p, cos_p;
-        sincosf(th_p, &sin_p, &cos_p);
-        const bool any = __any_sync(0xffffffffu, valid);
+        float4 a;
+        float2 c;
+        rfs_patch_cone(tile, wid, tiles_u, n_az, n_el, dirs, a, c);
         if (lane == 0) {
-            ca[q] = any ? make_float4(cx, cy, cz, th_p) : make_float4(0.f, 0.f, 0.f, -1e30f);
-            cb[q] = any ? make_float2(cos_p, sin_p) : make_float2(1e30f, -1e30f);
-            run[q] = 0;
+            ca[wid] = a;
+            cb[wid] = c;
+            run[wid] = 0;
         }
     }
     __syncthreads();
@@ -631,17 +611,7 @@ __global__ void __launch_bounds__(PL_NT, 2) k_patch_lists(const int2* __restrict
             const float4 sp = __ldg(&sph[g]);
             const float4 w3 = __ldg(&whit[4 * g + 3]);
             lbv = __ldg(&geom[g].lbv);
-            const float m2 = sp.x * sp.x + sp.y * sp.y + sp.z * sp.z;
-            const float rs = rsqrtf(m2);
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                const float4 c = ca[p];
-                const float2 d = cb[p];
-                // the k_hits test: cos(th_p + th_g) by angle addition
-                const float dotc = (c.x * sp.x + c.y * sp.y + c.z * sp.z) * rs;
-                const bool rel = (c.w + w3.y >= 3.1415f) || dotc >= d.x * w3.z - d.y * w3.w - 1e-5f;
-                pm |= (uint32_t)rel << p;
-            }
+            pm = rfs_patch_mask(ca, cb, sp, w3);
         }
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
@@ -882,7 +852,7 @@ size_t rfs_hits_patch_bytes(int m_cap, int n_tiles) {
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
              int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, int split_min,
-             int bcap, void* split_ws, int m_cap, void* patch_ws, void* stream) {
+             int bcap, void* split_ws, int m_cap, void* patch_ws, int patch_built, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (used && n > 0) RFS_CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)n, st));
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
@@ -921,9 +891,12 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
         double* plb = (double*)patch_ws;
         uint32_t* pv = (uint32_t*)(plb + 8 * (size_t)m_cap);
         int* pc = (int*)(pv + 8 * (size_t)m_cap);
-        k_patch_lists<<<n_tiles, PL_NT, 0, st>>>((const int2*)ranges, vals, (const float4*)sph, (const float4*)whit,
-                                               (const RfsGeom*)geom, dirs, n_az, n_el, tiles_u, pv, plb, pc);
-        RFS_LAUNCH_CHECK();
+        if (!patch_built) {  // else rfs_bin_bucket wrote them
+            k_patch_lists<<<n_tiles, PL_NT, 0, st>>>((const int2*)ranges, vals, (const float4*)sph,
+                                                     (const float4*)whit, (const RfsGeom*)geom, dirs, n_az, n_el,
+                                                     tiles_u, pv, plb, pc);
+            RFS_LAUNCH_CHECK();
+        }
         kp.vals = pv;
         kp.lb = plb;
         kp.cnt = pc;

@@ -80,3 +80,52 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 static inline int rfs_ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// K6 ray patches: warp q (0..7) of a 16 x 16 tile owns a 4 (u) x 8 (v) patch.
+// The patch cone (axis through the patch, half-angle covering its rays) as
+// k_hits computes it; called by a full warp.  ca = (cx, cy, cz, th_p),
+// cb = (cos_p, sin_p); a patch without rays gets a cone no candidate passes.
+__device__ __forceinline__ void rfs_patch_cone(int tile, int q, int tiles_u, int n_az, int n_el,
+                                               const double* __restrict__ dirs, float4& ca, float2& cb) {
+    const int lane = threadIdx.x & 31, pu = q >> 1, pv = q & 1;
+    const int u = (tile % tiles_u) * RFS_TILE + 4 * pu + (lane >> 3);
+    const int v = (tile / tiles_u) * RFS_TILE + 8 * pv + (lane & 7);
+    const bool valid = u < n_az && v < n_el;
+    const int r = valid ? u * n_el + v : 0;
+    const float fx = (float)dirs[3 * r], fy = (float)dirs[3 * r + 1], fz = (float)dirs[3 * r + 2];
+    float cx = valid ? fx : 0.f, cy = valid ? fy : 0.f, cz = valid ? fz : 0.f;
+    cx = warp_sum(cx);
+    cy = warp_sum(cy);
+    cz = warp_sum(cz);
+    {
+        const float inv = rsqrtf(fmaxf(cx * cx + cy * cy + cz * cz, 1e-30f));
+        cx *= inv;
+        cy *= inv;
+        cz *= inv;
+    }
+    float cmin = valid ? cx * fx + cy * fy + cz * fz : 1.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+    const float th_p = acosf(fminf(cmin, 1.f)) + 1e-4f;
+    float sin_p, cos_p;
+    sincosf(th_p, &sin_p, &cos_p);
+    const bool any = __any_sync(0xffffffffu, valid);
+    ca = any ? make_float4(cx, cy, cz, th_p) : make_float4(0.f, 0.f, 0.f, -1e30f);
+    cb = any ? make_float2(cos_p, sin_p) : make_float2(1e30f, -1e30f);
+}
+
+// 8-bit mask of the patch cones a candidate (bounding sphere sp = (mu - rx, .),
+// cone record w3 = whit[4 g + 3]) may reach: k_hits' cone test
+__device__ __forceinline__ uint32_t rfs_patch_mask(const float4* ca, const float2* cb, float4 sp, float4 w3) {
+    const float rs = rsqrtf(sp.x * sp.x + sp.y * sp.y + sp.z * sp.z);
+    uint32_t pm = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+        const float4 c = ca[p];
+        const float2 d = cb[p];
+        const float dotc = (c.x * sp.x + c.y * sp.y + c.z * sp.z) * rs;
+        const bool rel = (c.w + w3.y >= 3.1415f) || dotc >= d.x * w3.z - d.y * w3.w - 1e-5f;
+        pm |= (uint32_t)rel << p;
+    }
+    return pm;
+}

@@ -335,6 +335,8 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     status_h = _pinned(dev, "status", 8)
     m_dev_ptr = status.data_ptr() + 4
 
+    patch_state = {"built": False}  # K6 patch lists written by the bucket sort
+
     def bin_tiles(cap: int, device_count: bool, bucket: bool):
         """K2b fill, K3 sort, K4 ranges, K4b bounds into buffers of capacity `cap`."""
         ck = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
@@ -346,10 +348,15 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             bv = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
             tt = torch.empty(max(int(lib.rfs_bin_bucket_temp_bytes(n, n_az, n_el, cap)), 16), dtype=torch.uint8,
                              device=dev)
+            pw = (_persistent("k6_patch", int(lib.rfs_hits_patch_bytes(max(cap, 1), n_tiles)), torch.uint8, dev)
+                  if _CAPS["patch_lists"] and _CAPS["split_min"] <= 0 and cap > 0 else None)
             _native.call("rfs_bin_bucket", n, _ptr(rects), _ptr(code), n_az, n_el, cap, _ptr(geom), _ptr(bc),
-                         _ptr(bv), _ptr(tt), _ptr(ck), _ptr(vl), _ptr(rg), _ptr(lbv), _ptr(status), st)
+                         _ptr(bv), _ptr(tt), _ptr(ck), _ptr(vl), _ptr(rg), _ptr(lbv), _ptr(status), _ptr(sph),
+                         _ptr(whit), _ptr(dirs), _ptr(pw) if pw is not None else None, st)
             _mark(marks, "bin+sort")
+            patch_state["built"] = pw is not None
             return ck, vl, rg, lbv
+        patch_state["built"] = False
         mp = m_dev_ptr if device_count else None
         if cap > 0:
             _native.call("rfs_bin_fill", n, _ptr(rects), _ptr(code), _ptr(offsets), n_az, cap, _ptr(ck), _ptr(vl), st)
@@ -400,14 +407,15 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         mcap_v = int(vals.numel())
         patch_ws = (_persistent("k6_patch", int(lib.rfs_hits_patch_bytes(mcap_v, n_tiles)), torch.uint8, dev)
                     if _CAPS["patch_lists"] and split_ws is None else None)
+        built = int(patch_ws is not None and patch_state["built"])  # by the bucket sort
         _native.call("rfs_hits", _ptr(ranges), n_tiles, _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit), _ptr(geom),
                      _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, pc, _ptr(slab), _ptr(ray_counts),
                      _ptr(slow), _ptr(stats), _ptr(used), n, split_min, bcap,
                      _ptr(split_ws) if split_ws is not None else None, mcap_v,
-                     _ptr(patch_ws) if patch_ws is not None else None, st)
+                     _ptr(patch_ws) if patch_ws is not None else None, built, st)
         if split_ws is not None:
             _native.launch_counter["kernels"] += 1  # k_hits_merge
-        if patch_ws is not None:
+        if patch_ws is not None and not built:
             _native.launch_counter["kernels"] += 1  # k_patch_lists
         ev_hits = torch.cuda.Event()
         ev_hits.record()
