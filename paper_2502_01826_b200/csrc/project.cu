@@ -392,45 +392,39 @@ __global__ void k_expand_keys(const uint64_t* __restrict__ ckeys, int m, uint64_
 // K4b: emission bound lb[i] = min_{j >= i in tile} lbv[g_j] (reverse
 // segmented min-scan, one block per tile).  Used by the exact streaming
 // re-sort in K6: a pending hit with t_mid < lb[i] precedes every hit that
-// candidates i.. can still produce.
-constexpr int LB_THREADS = 256;
+// candidates i.. can still produce.  Each warp owns a contiguous stretch of
+// the tile list: it writes its stretch's suffix minima (32 at a time, from
+// the end), then, once every stretch's minimum is known, folds in the minimum
+// of the later stretches -- no block barrier inside the loops.
+constexpr int LB_THREADS = 1024;
 __global__ void __launch_bounds__(LB_THREADS) k_lower_bounds(const int2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                                                               const RfsGeom* __restrict__ geom, double* __restrict__ lb) {
-    __shared__ double wmin[LB_THREADS / 32];
+    constexpr int NW = LB_THREADS / 32;
+    __shared__ double smin[NW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int2 rg = ranges[blockIdx.x];
+    const int L = rg.y - rg.x;
+    const int per = (L + NW - 1) / NW;
+    const int s0 = rg.x + min(wid * per, L), s1 = rg.x + min(wid * per + per, L);
     double carry = INFINITY;
-    int end = rg.y;
-    double v_next = INFINITY;
-    {
-        const int i = end - 1 - (int)threadIdx.x;
-        if (i >= rg.x) v_next = geom[vals[i]].lbv;
-    }
-    for (; end > rg.x; end -= LB_THREADS) {
-        const int i = end - 1 - (int)threadIdx.x;  // thread 0 handles the last element
-        double v = v_next;
-        {   // next chunk's gather in flight during this chunk's scan
-            const int j = i - LB_THREADS;
-            v_next = j >= rg.x ? geom[vals[j]].lbv : INFINITY;
-        }
-        // inclusive min-scan over increasing thread index (= decreasing i)
+    for (int k0 = s1 - 32; k0 > s0 - 32; k0 -= 32) {
+        const int i = k0 + lane;
+        double v = i >= s0 ? geom[vals[i]].lbv : INFINITY;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const double t = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v = fmin(v, t);
+            const double y = __shfl_down_sync(0xffffffffu, v, o);
+            if (lane + o < 32) v = fmin(v, y);
         }
-        if (lane == 31) wmin[wid] = v;
-        __syncthreads();
-        double pre = carry;
-        for (int w = 0; w < wid; ++w) pre = fmin(pre, wmin[w]);
-        v = fmin(v, pre);
-        if (i >= rg.x) lb[i] = v;
-        double tot = carry;
-#pragma unroll
-        for (int w = 0; w < LB_THREADS / 32; ++w) tot = fmin(tot, wmin[w]);
-        carry = tot;
-        __syncthreads();
+        v = fmin(v, carry);
+        if (i >= s0) lb[i] = v;
+        carry = __shfl_sync(0xffffffffu, v, 0);
     }
+    if (lane == 0) smin[wid] = carry;
+    __syncthreads();
+    double later = INFINITY;
+    for (int w = wid + 1; w < NW; ++w) later = fmin(later, smin[w]);
+    if (later == INFINITY) return;
+    for (int i = s0 + lane; i < s1; i += 32) lb[i] = fmin(lb[i], later);
 }
 
 }  // namespace
