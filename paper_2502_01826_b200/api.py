@@ -29,10 +29,10 @@ from .errors import ContractViolationError, ShapeError
 from .scene import HostScene
 
 __all__ = [
-    "GradientBuffer", "TileIndex", "SceneProjection", "RenderContextGPU",
+    "GradientBuffer", "TileIndex", "SceneProjection", "SpectrumFrame", "RenderContextGPU",
     "prepare_context", "render_complex_frame", "render_complex_frames", "render_spectrum", "render_scalar",
     "backward_frame", "backward_frames", "upstream_to_ray", "build_tiles_for_render", "project_scene",
-    "fwd_bwd_host", "train_step_host",
+    "fwd_bwd_host", "fwd_bwd_device", "train_step_host",
 ]
 
 
@@ -135,9 +135,29 @@ def render_complex_frame(scene, tx, workers: int = 1, tiled: bool = True,
     return render_complex_frames(scene, np.asarray(tx, dtype=np.float64).reshape(1, 3), ctx)[0]
 
 
-def render_spectrum(scene, tx, workers: int = 1, ctx: RenderContextGPU | None = None) -> np.ndarray:
-    """render.render_spectrum (render.py:292-298): |S|^2."""
-    return np.abs(render_complex_frame(scene, tx, workers, ctx=ctx)) ** 2
+@dataclass
+class SpectrumFrame:
+    """render.SpectrumFrame (render.py:84-100): power per direction, (n_az, n_el) float64."""
+
+    data: np.ndarray
+
+    def __post_init__(self):
+        self.data = np.asarray(self.data, dtype=np.float64)
+        if self.data.ndim != 2:
+            raise ShapeError("spectrum frame must be 2-dimensional")
+
+    @property
+    def n_az(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def n_el(self) -> int:
+        return self.data.shape[1]
+
+
+def render_spectrum(scene, tx, workers: int = 1, ctx: RenderContextGPU | None = None) -> SpectrumFrame:
+    """render.render_spectrum (render.py:292-298): SpectrumFrame(|S|^2)."""
+    return SpectrumFrame(np.abs(render_complex_frame(scene, tx, workers, ctx=ctx)) ** 2)
 
 
 def render_scalar(scene, tx, workers: int = 1, ctx: RenderContextGPU | None = None) -> complex:
@@ -239,6 +259,25 @@ def fwd_bwd_host(host_scene: dict, tx_host: torch.Tensor, lam_host: torch.Tensor
     h2d += tx_host.numel() * tx_host.element_size() + lam_host.numel() * lam_host.element_size()
     d2h = sum(out[k].numel() * out[k].element_size() for k in ("S",) + OUT_GRADS)
     return h2d, d2h
+
+
+def fwd_bwd_device(ds: raster.DeviceScene, tx: torch.Tensor, lam: torch.Tensor, include_direction_chain: bool = True,
+                   sort_backend: str = "hand", marks: list | None = None) -> tuple:
+    """The benched step (bench.py): render + backward of a device-resident
+    scene for a TX batch [B, 3] under a fixed upstream lam [B, n_az, n_el].
+
+    render_complex_frame + backward_frame (render.py:282-289, grad.py:192-259)
+    for the whole batch, with psi queued behind the geometry's first host
+    read, the composite and the upstream transpose behind the second, and the
+    by-Gaussian index on the side stream.  Returns (S [B, n_az, n_el], grads).
+    """
+    b = int(tx.shape[0])
+    early_t = (lambda S: raster.transpose_upstream(lam)) if b <= raster.MAX_TX_PER_LAUNCH else None
+    geo = raster.build_geometry(ds, sort_backend=sort_backend, marks=marks, psi_tx=tx, forward=True, index=True,
+                                after_forward=early_t)
+    g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=geo.psi, marks=marks,
+                        lamT=geo.after_result)
+    return geo.S, g
 
 
 _COPY: dict = {}

@@ -1,0 +1,142 @@
+"""Parity of the exact benched step (bench.py -> api.fwd_bwd_device) against the oracle.
+
+bench.py times config 2 (100k Gaussians, 360x180, 64 TX) through
+`api.fwd_bwd_device`: psi behind the first host read, the composite and the
+upstream transpose behind the second, the by-Gaussian index on the side
+stream, and -- since B is a multiple of 64 -- the paired-TX backward kernel.
+These tests run that same call (twice: the second call takes the
+early-index / known-capacity path the timed steps take) at B = 64, 128 and
+256 and compare per-TX spectra and the batch-summed gradient buffer with the
+oracle (reference-pinned, tests/test_oracle_golden.py):
+  spectra: the per-ray bar of SURVEY.md §8(c), on every TX;
+  gradients: per class |a - r| / max(|a|, |r|, 1e-3 class max) <= 1e-3 on
+  all GradientBuffer fields (gradcheck.py:213-215 floor convention).
+"""
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+from helpers import GRAD_KEYS, class_rel, rel_err
+
+from paper_2502_01826_b200 import api, raster
+from paper_2502_01826_b200.scene import bench_scene, default_txs, round_to_f32
+
+pytestmark = pytest.mark.gpu
+
+SPEC_TOL = 1e-4
+GRAD_TOL = 1e-3
+_SCENES: dict = {}
+
+
+def _scene(n, seed=0, mutate=None):
+    key = (n, seed, mutate)
+    if key not in _SCENES:
+        s = bench_scene(np.random.default_rng(seed), n, 360, 180)
+        if mutate == "huge":
+            # one Gaussian whose 3-sigma ball holds the receiver: hit by nearly every
+            # ray, so its hits straddle many backward chunks (the last-arriver merge)
+            s.means[0] = [3.0, 0.5, -0.2]
+            s.log_scales[0] = np.log([2.5, 2.0, 2.2])
+            s.trans_mag_raw[0] = -2.0
+        _SCENES.clear()
+        _SCENES[key] = round_to_f32(s)
+    return _SCENES[key]
+
+
+def _oracle_batch(s, txs, lam_fn):
+    """Per-TX oracle frames, upstreams and the summed gradient buffer.
+
+    TX are split over a few worker threads, each with its own context (the C
+    oracle releases the GIL; each context parallelises over rays itself)."""
+    nthreads = os.cpu_count() or 1
+    workers = max(1, min(4, len(txs)))
+    chunks = np.array_split(np.arange(len(txs)), workers)
+
+    def run(idx):
+        oc = oracle.OracleContext(s, threads=max(1, nthreads // workers))
+        frames, lams, acc = {}, {}, None
+        for b in idx:
+            oc.set_tx(txs[b])
+            S = oc.forward()
+            lam = lam_fn(S)
+            g = oc.backward(lam)
+            frames[b], lams[b] = S, lam
+            acc = g if acc is None else {k: acc[k] + g[k] for k in acc}
+        return frames, lams, acc
+
+    with ThreadPoolExecutor(workers) as ex:
+        res = list(ex.map(run, chunks))
+    frames, lams, ref = {}, {}, None
+    for f, l, a in res:
+        frames.update(f)
+        lams.update(l)
+        if a is not None:
+            ref = a if ref is None else {k: ref[k] + a[k] for k in ref}
+    B = len(txs)
+    return np.stack([frames[b] for b in range(B)]), np.stack([lams[b] for b in range(B)]), ref
+
+
+def _spectrum_ok(S, ref, tag):
+    P, Pr = np.abs(S) ** 2, np.abs(ref) ** 2
+    assert rel_err(P, Pr) <= SPEC_TOL, (tag, rel_err(P, Pr))
+    floor = 1e-3 * Pr.max()
+    bad = np.abs(P - Pr) > SPEC_TOL * np.maximum(Pr, floor) + 1e-30
+    assert not bad.any(), f"{tag}: {bad.sum()} rays outside tolerance"
+
+
+def _run_bench_step(s, txs, lam):
+    ds = raster.DeviceScene.from_host(s, "cuda")
+    tx = torch.as_tensor(txs, dtype=torch.float32, device="cuda")
+    lam_d = torch.as_tensor(lam.astype(np.complex64), device="cuda")
+    out = None
+    for _ in range(2):  # 2nd call: capacities known -> early side-stream index, device-side M
+        S, g = api.fwd_bwd_device(ds, tx, lam_d)
+        out = (S.cpu().numpy(), api.GradientBuffer.from_device(g))
+    torch.cuda.synchronize()
+    return out
+
+
+def _check(s, txs, every_tx=True):
+    # the upstream comes from the oracle's own frames (the reference's L1
+    # gradcheck pattern); both sides then see the same lambda
+    Sref, lam, ref = _oracle_batch(s, txs, oracle.l1_upstream)
+    S, g = _run_bench_step(s, txs, lam)
+    for b in (range(len(txs)) if every_tx else (0, len(txs) // 2, len(txs) - 1)):
+        _spectrum_ok(S[b], Sref[b], f"tx {b}")
+    errs = {k: class_rel(getattr(g, k), ref[k]) for k in GRAD_KEYS}
+    assert max(errs.values()) <= GRAD_TOL, errs
+    return errs
+
+
+@pytest.mark.parametrize("B", [64, 128, 256])
+def test_bench_step_config2_vs_oracle(B):
+    """Config 2 (100k Gaussians, 360x180) at B = 64 / 128 / 256: drives the
+    paired-TX backward kernel with 1 / 2 / 4 TX pairs per lane."""
+    s = _scene(100_000)
+    _check(s, default_txs(B, seed=1))
+
+
+@pytest.mark.parametrize("B", [64, 128])
+def test_bench_step_straddling_gaussian_vs_oracle(B):
+    """A Gaussian around the receiver: ~R hits on one Gaussian, spread over
+    hundreds of backward chunks, completed by the last-arriving chunk."""
+    s = _scene(20_000, 17, "huge")
+    _check(s, default_txs(B, seed=4))
+
+
+def test_config3_500k_spectra_sampled_tx():
+    """Config 3 (500k Gaussians): spectra of 4 sampled TX of a 64-TX batch vs the oracle."""
+    s = _scene(500_000)
+    txs = default_txs(64, seed=1)
+    ds = raster.DeviceScene.from_host(s, "cuda")
+    S = api.render_complex_frames(ds, txs)
+    oc = oracle.OracleContext(s)
+    for b in (0, 21, 42, 63):
+        oc.set_tx(txs[b])
+        _spectrum_ok(S[b], oc.forward(), f"tx {b}")
