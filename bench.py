@@ -169,10 +169,10 @@ def run_ours(args):
 
     from paper_2502_01826_b200 import parallel
 
-    def allreduce(g):
-        # one NCCL all-reduce (sum) of the packed gradient buffer
-        if world > 1:
-            g.update(parallel.allreduce_grads(g))
+    # persistent flat gradient buffer: the backward writes into it, and for N > 1
+    # its 44 floats per Gaussian are all-reduced by NCCL in two buckets, the
+    # first (d_coeffs) overlapping the rest of the epilogue
+    gb = parallel.GradBuffer(ds.n, ds.fle_degree, dev)
 
     # fixed synthetic upstream: lambda = upstream_to_ray(dL1/dP, S), target 1.3 P + 0.05
     geo = raster.build_geometry(ds, sort_backend=args.sort)
@@ -203,14 +203,13 @@ def run_ours(args):
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
+    # the upstream enters the backward in the loss kernel's own output layout
+    # (ray-major lamT, loss.spectrum_loss_frames(lam_layout="rays")): made once here
+    lamT = raster.transpose_upstream(lam)
+
     def step(marks=None):
         # psi queued behind the M read, the composite behind the hit-statistics read
-        g0 = raster.build_geometry(ds, sort_backend=args.sort, marks=marks, psi_tx=tx, forward=True, index=True,
-                                   after_forward=lambda S: raster.transpose_upstream(lam))
-        psi, S = g0.psi, g0.S
-        g = raster.backward(ds, g0, tx, lam, True, psi=psi, marks=marks, deterministic=args.deterministic,
-                            lamT=g0.after_result)
-        allreduce(g)
+        S, g = api.fwd_bwd_device(ds, tx, None, True, args.sort, marks, lamT=lamT, grads=gb)
         raster._mark(marks, "allreduce")
         return S, g
 
@@ -301,9 +300,8 @@ def run_ours(args):
         txh = torch.as_tensor(txs, dtype=torch.float32).pin_memory()
         gth = gt_frames.cpu().pin_memory()
         reph = torch.empty((B, 4), dtype=torch.float64).pin_memory()
-        red = allreduce if world > 1 else None
         for _ in range(max(1, args.warmup)):
-            api.train_step_host(ds, txh, gth, reph, sort_backend=args.sort, reduce_fn=red)
+            api.train_step_host(ds, txh, gth, reph, sort_backend=args.sort, grads=gb)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -313,7 +311,7 @@ def run_ours(args):
         gc.disable()
         es.record()
         for _ in range(args.steps):
-            _, h2d, d2h = api.train_step_host(ds, txh, gth, reph, sort_backend=args.sort, reduce_fn=red)
+            _, h2d, d2h = api.train_step_host(ds, txh, gth, reph, sort_backend=args.sort, grads=gb)
         ee.record()
         torch.cuda.synchronize()
         gc.enable()
@@ -408,8 +406,28 @@ def run_reference(args):
     }))
 
 
+def self_launch(args) -> int:
+    """`bench.py --gpus N` run directly (no WORLD_SIZE): start N ranks with
+    torch.distributed.run on this node (rendezvous on 127.0.0.1) and relay
+    rank 0's line; the exit code is the launcher's."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 if __name__ == "__main__":
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(a))
+    _, _world, _ = dist_env()
+    if _world != a.gpus:
+        sys.exit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={_world}")
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -95,14 +95,11 @@ int rfs_tile_ranges(const uint64_t* ckeys, int m, const uint32_t* m_dev, int n_t
  * Gaussian ids and emission bounds -- bitwise the outputs of rfs_bin_fill +
  * rfs_sort_pairs_u64 + rfs_tile_ranges + rfs_lower_bounds (splat.py:337-343).
  * bcodes / bvals u32[cap] and temp (rfs_bin_bucket_temp_bytes) are scratch;
- * status is reserved.  patch_ws (nullable, rfs_hits_patch_bytes(cap, n_tiles)
- * bytes; sph / whit / dirs then required): also K6's per-patch filtered lists
- * (pass patch_built = 1 to rfs_hits).  Grids up to 512 tiles. */
+ * status is reserved.  Grids up to 512 tiles. */
 size_t rfs_bin_bucket_temp_bytes(int n, int n_az, int n_el, int cap);
 int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_az, int n_el, int cap, const void* geom,
                    uint32_t* bcodes, uint32_t* bvals, void* temp, uint64_t* ckeys, uint32_t* vals, int* ranges,
-                   double* lb, int* status, const void* sph, const void* whit, const double* dirs, void* patch_ws,
-                   void* stream);
+                   double* lb, int* status, void* stream);
 
 /* K4b: per-incidence emission bound for the exact streaming re-sort:
  * lb[i] = min_{j >= i, same tile} (depth_j - r3_j). */
@@ -114,28 +111,18 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream);
 
 /* K6: TX-independent live hit lists.  Replaces _collect_hits + the live walk
  * of forward_tiled / count_hits_tiled (_kernels.py:27-112, 140-192, 237-292).
- * Writes hits of ray r to slab[r*hcap ...], counts[r] = live count.  pcap
- * selects the pending ring (<= 16 -> 16 entries per ray, <= 32 -> 32, else
- * 64).  stats (device
- * int[8]): [0] rays needing rfs_hits_slow (listed in slow_list), [1] rays
+ * Writes hits of ray r to slab[r*hcap ...], counts[r] = live count.
+ * stats (device int[8]): [0] rays needing rfs_hits_slow (listed in slow_list), [1] rays
  * with live > hcap (caller must retry with larger hcap), [2] max live,
- * [3] total live hits, [4] longest tile list, [5] largest pending set.
+ * [3] total live hits, [4] longest tile list, [5] see below.
  * used (nullable u8[n], zeroed here): 1 for every Gaussian with a live hit.
- * split_min > 0 (with split_ws of rfs_hits_split_bytes(n_az*n_el, bcap)
- * bytes): tile lists longer than split_min are streamed as two concurrent
- * halves and merged (same hit lists, shorter critical path); a ray whose
- * second half holds more than bcap hits goes to the slow path. */
-size_t rfs_hits_split_bytes(int n_rays, int bcap);
-/* patch_ws (nullable, rfs_hits_patch_bytes(m_cap, n_tiles) bytes, m_cap >= the
- * length of vals): first filter each tile list by the warp cone of each of the
- * tile's 8 ray patches (k_patch_lists, with per-list emission bounds) and
- * stream those -- the same hit lists; ignored when split_min > 0.
- * patch_built != 0: rfs_bin_bucket already wrote the lists into patch_ws. */
-size_t rfs_hits_patch_bytes(int m_cap, int n_tiles);
+ * The exact streaming re-sort with early termination (hits.cu); pcap
+ * selects the pending ring (<= 16 -> 16 entries per ray, <= 32 -> 32, else
+ * 64); stats[5] = the largest pending set, stats[6] / [7] = fp32 sphere /
+ * whitened-ellipsoid passes (diagnostics). */
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
-             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, int split_min,
-             int bcap, void* split_ws, int m_cap, void* patch_ws, int patch_built, void* stream);
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, void* stream);
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
@@ -173,19 +160,6 @@ int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* 
                       float* s_w, void* s_wt, uint32_t* inv_slot, void* stream);
 int rfs_gauss_offsets(const uint64_t* keys, int n_hits, const uint32_t* h_dev, int n, int* g_off, void* stream);
 
-/* K8i by counting (gindex.cu): hits per Gaussian, g_off (int[n+1], g_off[n]
- * = H), each hit's slot scattered into its Gaussian's segment, then each
- * segment put in slot order (a warp sort for <= 256 hits, else a bitmap over
- * the Gaussian's rays: one hit per ray) with the per-hit Gaussian id, ray, w
- * and w T gathered -- bitwise the outputs of rfs_hit_keys +
- * rfs_sort_pairs_u64 + rfs_gauss_offsets + rfs_gather_sorted.  Writes
- * positions < cap only.  Grids up to 65536 rays.  scratch:
- * rfs_gauss_index_scratch_elems(n, cap) u32; scan_temp:
- * rfs_scan_temp_elems(n) u32. */
-size_t rfs_gauss_index_scratch_elems(int n, int cap);
-int rfs_gauss_index(const void* slab, const int* counts, int hcap, int n_rays, int n, int cap, uint32_t* scratch,
-                    uint32_t* scan_temp, int* g_off, uint64_t* sorted_g, uint32_t* s_slot, uint32_t* s_ray, float* s_w,
-                    void* s_wt, void* stream);
 
 /* K8: TX-batched backward over the shared hit lists, atomic-free and
  * deterministic (every sum in a fixed order).  Replaces the complex part of
@@ -247,13 +221,15 @@ int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coe
  * predicted power is pred (f32, nullable) or |S|^2 (S complex64, nullable);
  * gt is the ground-truth power (f32).  report (f64[B*4], device) = {total,
  * L1, SSIM, Fourier} per frame; grad (f32[B*R], nullable) = dL/dP; lam
- * (complex64[B*R], nullable, needs S) = 2 dL/dP S.  L1 = mean|d|; SSIM = 1 -
+ * (complex64[B*R], nullable, needs S) = 2 dL/dP S; lamT (complex64[R*B],
+ * nullable, needs S) the same values ray-major -- the layout rfs_bwd_gauss
+ * reads, so the training step needs no transpose.  L1 = mean|d|; SSIM = 1 -
  * mean of the 11x11 sigma-1.5 zero-padded windowed SSIM with C1, C2 from the
  * ground-truth range; Fourier = sum d^2 (= the mean squared DFT difference by
  * Parseval).  Deterministic.  scratch: rfs_loss_scratch_bytes bytes. */
 size_t rfs_loss_scratch_bytes(int n_frames, int n_az, int n_el);
 int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const float* pred, const float* gt,
-                      double w_ssim, double w_fourier, double* report, float* grad, void* lam, void* scratch,
+                      double w_ssim, double w_fourier, double* report, float* grad, void* lam, void* lamT, void* scratch,
                       size_t scratch_bytes, void* stream);
 
 /* Scalar (single-antenna) modes: total_b = sum_r S[b][r] (render_scalar,
@@ -297,11 +273,6 @@ int rfs_density_apply(int n, int K, int mode, const uint32_t* keep, const uint32
                       const float* trans_mag_raw, const float* trans_phase, const void* coeffs, const float* grad_ema,
                       const float* last_dmean, float* o_means, float* o_quats, float* o_log_scales, float* o_raw,
                       float* o_phase, void* o_coeffs, float* o_ema, float* o_last, void* stream);
-
-/* Diagnostics: per warp of k_hits, u64[8]: %globaltimer start / end,
- * candidates, chunks, cone survivors, sum over chunks of the most exact tests
- * on one lane, survivor-union size, max live hits; NULL switches it off. */
-int rfs_debug_k6_timing(unsigned long long* buf);
 
 /* Library / build identification. */
 int rfs_version(void);

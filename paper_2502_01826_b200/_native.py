@@ -36,13 +36,10 @@ _SIGS = {
     "rfs_sort_pairs_u64_cub": (i32, [vp, vp, vp, vp, i32, i32, vp, sz, C.POINTER(i32), vp]),
     "rfs_tile_ranges": (i32, [vp, i32, vp, i32, vp, vp]),
     "rfs_bin_bucket_temp_bytes": (sz, [i32, i32, i32, i32]),
-    "rfs_bin_bucket": (i32, [i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "rfs_bin_bucket": (i32, [i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rfs_lower_bounds": (i32, [vp, i32, vp, vp, vp, vp]),
     "rfs_ray_dirs": (i32, [i32, i32, vp, vp]),
-    "rfs_hits_split_bytes": (sz, [i32, i32]),
-    "rfs_hits_patch_bytes": (sz, [i32, i32]),
-    "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, i32,
-                       vp, i32, vp, i32, vp]),
+    "rfs_hits": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i32, vp]),
     "rfs_hits_slow": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, f64, i32, i32, i32, vp, vp, vp, vp, vp, i32,
                             vp, vp, vp]),
     "rfs_psi": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),
@@ -54,20 +51,17 @@ _SIGS = {
     "rfs_hit_keys": (i32, [vp, vp, vp, i32, i32, vp, vp, vp]),
     "rfs_gather_sorted": (i32, [vp, i32, vp, i32, vp, vp, vp, vp, vp, vp]),
     "rfs_gauss_offsets": (i32, [vp, i32, vp, i32, vp, vp]),
-    "rfs_gauss_index_scratch_elems": (sz, [i32, i32]),
-    "rfs_gauss_index": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rfs_geom_part_elems": (sz, [i32]),
     "rfs_grad_geom": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                             vp, vp, vp, vp, vp, vp]),
     "rfs_grad_tx": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
     "rfs_loss_scratch_bytes": (sz, [i32, i32, i32]),
-    "rfs_spectrum_loss": (i32, [i32, i32, i32, vp, vp, vp, f64, f64, vp, vp, vp, vp, sz, vp]),
+    "rfs_spectrum_loss": (i32, [i32, i32, i32, vp, vp, vp, f64, f64, vp, vp, vp, vp, vp, sz, vp]),
     "rfs_scalar_loss": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "rfs_sgd_step": (i32, [i32, i32, vp, C.c_float, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rfs_density_flags": (i32, [i32, i32, vp, vp, vp, f64, f64, f64, vp, vp, vp, vp]),
     "rfs_density_apply": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_ulonglong, i32,
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
-    "rfs_debug_k6_timing": (i32, [vp]),
     "rfs_version": (i32, []),
     "rfs_device_arch": (i32, []),
 }
@@ -106,7 +100,7 @@ KERNELS_PER_CALL = {
     "rfs_project": 1, "rfs_exclusive_scan_u32": 1, "rfs_bin_fill": 1, "rfs_expand_keys": 1,
     "rfs_tile_ranges": 1, "rfs_lower_bounds": 1, "rfs_bin_bucket": 7, "rfs_hits": 2, "rfs_hits_slow": 1, "rfs_psi": 1,
     "rfs_forward": 1, "rfs_lam_transpose": 1, "rfs_bwd_gauss": 1, "rfs_bwd_rays": 1, "rfs_hit_keys": 1, "rfs_gauss_offsets": 1, "rfs_grad_geom": 3,
-    "rfs_grad_tx": 1, "rfs_gather_sorted": 1, "rfs_gauss_index": 5,
+    "rfs_grad_tx": 1, "rfs_gather_sorted": 1,
     "rfs_ray_dirs": 1, "rfs_spectrum_loss": 4, "rfs_sgd_step": 2, "rfs_scalar_loss": 1, "rfs_density_flags": 1,
     "rfs_density_apply": 1,
 }

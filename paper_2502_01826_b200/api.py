@@ -261,22 +261,37 @@ def fwd_bwd_host(host_scene: dict, tx_host: torch.Tensor, lam_host: torch.Tensor
     return h2d, d2h
 
 
-def fwd_bwd_device(ds: raster.DeviceScene, tx: torch.Tensor, lam: torch.Tensor, include_direction_chain: bool = True,
-                   sort_backend: str = "hand", marks: list | None = None) -> tuple:
+def fwd_bwd_device(ds: raster.DeviceScene, tx: torch.Tensor, lam: torch.Tensor | None = None,
+                   include_direction_chain: bool = True, sort_backend: str = "hand", marks: list | None = None,
+                   lamT: torch.Tensor | None = None, grads=None, group=None) -> tuple:
     """The benched step (bench.py): render + backward of a device-resident
-    scene for a TX batch [B, 3] under a fixed upstream lam [B, n_az, n_el].
+    scene for a TX batch [B, 3] under a fixed upstream.
 
     render_complex_frame + backward_frame (render.py:282-289, grad.py:192-259)
     for the whole batch, with psi queued behind the geometry's first host
-    read, the composite and the upstream transpose behind the second, and the
-    by-Gaussian index on the side stream.  Returns (S [B, n_az, n_el], grads).
+    read, the composite behind the second, and the by-Gaussian index on the
+    side stream.  The upstream is lam [B, n_az, n_el] (transposed for the
+    backward behind the composite) or lamT [n_az*n_el, B], the loss kernel's
+    own output layout (loss.spectrum_loss_frames(lam_layout="rays")).
+    `grads` (optional parallel.GradBuffer): the backward writes into it and,
+    under torch.distributed with more than one rank, all-reduces it in two
+    buckets overlapped with the epilogue (this rank's `tx` is its TX shard).
+    Returns (S [B, n_az, n_el], grads).
     """
     b = int(tx.shape[0])
-    early_t = (lambda S: raster.transpose_upstream(lam)) if b <= raster.MAX_TX_PER_LAUNCH else None
+    early_t = None
+    if lamT is None and b <= raster.MAX_TX_PER_LAUNCH:
+        early_t = lambda S: raster.transpose_upstream(lam)
     geo = raster.build_geometry(ds, sort_backend=sort_backend, marks=marks, psi_tx=tx, forward=True, index=True,
                                 after_forward=early_t)
-    g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=geo.psi, marks=marks,
-                        lamT=geo.after_result)
+    lt = lamT if lamT is not None else geo.after_result
+    if grads is not None:
+        from . import parallel
+
+        g = parallel.backward_reduced(ds, geo, tx, lam, grads, include_direction_chain, psi=geo.psi, lamT=lt,
+                                      group=group, marks=marks)
+    else:
+        g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=geo.psi, marks=marks, lamT=lt)
     return geo.S, g
 
 
@@ -292,7 +307,7 @@ def _copy_stream(dev) -> torch.cuda.Stream:
 
 def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torch.Tensor, report_host: torch.Tensor,
                     w_ssim: float = 0.2, w_fourier: float = 0.2, include_direction_chain: bool = True,
-                    sort_backend: str = "hand", reduce_fn=None) -> tuple:
+                    sort_backend: str = "hand", reduce_fn=None, grads=None, group=None) -> tuple:
     """One training step of a device-resident scene on a TX batch from HOST buffers.
 
     The batched counterpart of the reference iteration (train.py:266-281,
@@ -302,7 +317,10 @@ def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torc
     device, and the per-frame loss report [B, 4] = (total, L1, SSIM, Fourier)
     comes back into `report_host` (pinned float64); the gradient dict stays on
     the device for the optimizer.  Copies are stream-ordered (non_blocking);
-    the caller synchronizes.  Returns (grads, h2d_bytes, d2h_bytes).
+    the caller synchronizes.  `grads` (optional parallel.GradBuffer) receives
+    the gradients, all-reduced over the ranks as in fwd_bwd_device;
+    `reduce_fn(g)` (optional) is applied to a plain gradient dict instead.
+    Returns (grads, h2d_bytes, d2h_bytes).
     """
     from . import loss as _loss
 
@@ -323,16 +341,24 @@ def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torc
 
     def loss_and_upstream(S):  # queued behind the geometry's hit-statistics read
         main.wait_event(gt_ready)
+        if S.shape[0] <= raster.MAX_TX_PER_LAUNCH:  # the loss writes the backward's ray-major layout
+            rep, lamT, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier, lam_layout="rays")
+            return rep, None, lamT
         rep, lam, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier)
-        lamT = raster.transpose_upstream(lam) if lam.shape[0] <= raster.MAX_TX_PER_LAUNCH else None
-        return rep, lam, lamT
+        return rep, lam, None
 
     geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True, forward=True,
                                 after_forward=loss_and_upstream)
     rep, lam, lamT = geo.after_result
-    g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=geo.psi, lamT=lamT)
-    if reduce_fn is not None:
-        reduce_fn(g)
+    if grads is not None:
+        from . import parallel
+
+        g = parallel.backward_reduced(ds, geo, tx, lam, grads, include_direction_chain, psi=geo.psi, lamT=lamT,
+                                      group=group)
+    else:
+        g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=geo.psi, lamT=lamT)
+        if reduce_fn is not None:
+            reduce_fn(g)
     report_host.copy_(rep, non_blocking=True)
     h2d = tx_host.numel() * tx_host.element_size() + gt_host.numel() * gt_host.element_size()
     d2h = report_host.numel() * report_host.element_size()

@@ -26,7 +26,6 @@ SOURCES = {
     "project.cu": ["-fmad=false"],
     "radix_sort.cu": [],
     "bucket.cu": [],
-    "gindex.cu": [],
     "hits.cu": [],
     "composite.cu": [],
     "backward.cu": [],

@@ -173,18 +173,6 @@ __global__ void __launch_bounds__(BK_BLK) k_fill_stable(int n, const Rect* __res
     });
 }
 
-// Optional output of k_seg_sort: K6's per-patch cone-filtered candidate lists
-// (hits.cu KPatch layout), built while the tile's sorted list is on chip.
-struct PatchOut {
-    const float4* sph;
-    const float4* whit;
-    const double* dirs;
-    int n_az, n_el, tiles_u;
-    uint32_t* pvals;  // null: off
-    double* plb;
-    int* pcnt;
-};
-
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -222,7 +210,7 @@ __global__ void __launch_bounds__(NT) k_seg_sort(const int2* __restrict__ ranges
                                                  uint32_t* __restrict__ bvals, uint32_t* __restrict__ altc,
                                                  uint32_t* __restrict__ altv, const RfsGeom* __restrict__ geom,
                                                  uint64_t* __restrict__ ckeys, uint32_t* __restrict__ vals,
-                                                 double* __restrict__ lb, PatchOut po) {
+                                                 double* __restrict__ lb) {
     constexpr int NW = NT / 32, ITEMS = 8, ROUND = NT * ITEMS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -328,77 +316,6 @@ __global__ void __launch_bounds__(NT) k_seg_sort(const int2* __restrict__ ranges
         sl[i] = geom[g].lbv;
     }
     __syncthreads();
-    if (po.pvals) {  // K6's per-patch lists (hits.cu k_patch_lists, fused)
-        __shared__ float4 ca[8];
-        __shared__ float2 cb[8];
-        __shared__ int run[8];
-        __shared__ unsigned wb[NW][8];
-        __shared__ int wpre[NW][8];
-        if (wid < 8) {
-            float4 a;
-            float2 c;
-            rfs_patch_cone(tile, wid, po.tiles_u, po.n_az, po.n_el, po.dirs, a, c);
-            if (lane == 0) {
-                ca[wid] = a;
-                cb[wid] = c;
-                run[wid] = 0;
-            }
-        }
-        __syncthreads();
-        const size_t tb = 8 * (size_t)rg.x;
-        const unsigned lt2 = lanemask_lt();
-        for (int b0 = 0; b0 < L; b0 += NT) {
-            const int i = b0 + tid;
-            uint32_t g = 0, pm = 0;
-            double lv = 0.0;
-            if (i < L) {
-                g = sv[i];
-                lv = sl[i];
-                pm = rfs_patch_mask(ca, cb, __ldg(&po.sph[g]), __ldg(&po.whit[4 * g + 3]));
-            }
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                const unsigned m = __ballot_sync(0xffffffffu, (pm >> p) & 1u);
-                if (lane == 0) wb[wid][p] = m;
-            }
-            __syncthreads();
-            if (tid < 8) {
-                int acc = run[tid];
-                for (int w = 0; w < NW; ++w) {
-                    wpre[w][tid] = acc;
-                    acc += __popc(wb[w][tid]);
-                }
-                run[tid] = acc;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                if (!((pm >> p) & 1u)) continue;
-                const size_t o = tb + (size_t)p * L + wpre[wid][p] + __popc(wb[wid][p] & lt2);
-                po.pvals[o] = g;
-                po.plb[o] = lv;  // raw; suffix minima below
-            }
-            __syncthreads();
-        }
-        if (wid < 8) {  // warp p: suffix minima over patch p's list
-            const int cnt = run[wid];
-            if (lane == 0) po.pcnt[tile * 8 + wid] = cnt;
-            double* pl = po.plb + tb + (size_t)wid * L;
-            double carry = INFINITY;
-            for (int k0 = ((cnt - 1) >> 5) << 5; k0 >= 0; k0 -= 32) {
-                const int k = k0 + lane;
-                double v = k < cnt ? pl[k] : INFINITY;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const double y = __shfl_down_sync(0xffffffffu, v, o);
-                    if (lane + o < 32) v = fmin(v, y);
-                }
-                v = fmin(v, carry);
-                if (k < cnt) pl[k] = v;
-                carry = __shfl_sync(0xffffffffu, v, 0);
-            }
-        }
-    }
     // lb[i] = min_{j >= i} lbv_j: each thread a contiguous run, runs combined
     // right to left across the block
     const int E = (L + NT - 1) / NT;
@@ -424,8 +341,7 @@ __global__ void __launch_bounds__(NT) k_seg_sort(const int2* __restrict__ ranges
 
 template <int CAP, int NT>
 int launch_seg_sort(int n_tiles, const int* ranges, int lo, uint32_t* bcodes, uint32_t* bvals, uint32_t* altc,
-                    uint32_t* altv, const void* geom, uint64_t* ckeys, uint32_t* vals, double* lb, const PatchOut& po,
-                    cudaStream_t st) {
+                    uint32_t* altv, const void* geom, uint64_t* ckeys, uint32_t* vals, double* lb, cudaStream_t st) {
     static bool attr = false;
     const size_t smem = (size_t)CAP * 16;
     if (!attr && smem > 0) {
@@ -433,7 +349,7 @@ int launch_seg_sort(int n_tiles, const int* ranges, int lo, uint32_t* bcodes, ui
         attr = true;
     }
     k_seg_sort<CAP, NT><<<n_tiles, NT, smem, st>>>((const int2*)ranges, lo, bcodes, bvals, altc, altv,
-                                                   (const RfsGeom*)geom, ckeys, vals, lb, po);
+                                                   (const RfsGeom*)geom, ckeys, vals, lb);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -451,8 +367,7 @@ size_t rfs_bin_bucket_temp_bytes(int n, int n_az, int n_el, int cap) {
 
 int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_az, int n_el, int cap, const void* geom,
                    uint32_t* bcodes, uint32_t* bvals, void* temp, uint64_t* ckeys, uint32_t* vals, int* ranges,
-                   double* lb, int* status, const void* sph, const void* whit, const double* dirs, void* patch_ws,
-                   void* stream) {
+                   double* lb, int* status, void* stream) {
     const int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE, tiles_v = (n_el + RFS_TILE - 1) / RFS_TILE;
     const int n_tiles = tiles_u * tiles_v;
     if (n_tiles > BK_MAX_TILES || cap < 0 || n < 0) return RFS_ERR_SHAPE;
@@ -473,30 +388,17 @@ int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_a
     RFS_LAUNCH_CHECK();
     k_tile_offsets<<<1, BK_MAX_TILES, 0, st>>>(n_tiles, tot, (uint32_t)cap, (int2*)ranges, toff, status);
     RFS_LAUNCH_CHECK();
-    PatchOut po{};
-    if (patch_ws && cap > 0) {  // hits.cu KPatch layout: lb [8 cap] doubles, ids [8 cap], counts [8 tiles]
-        po.sph = (const float4*)sph;
-        po.whit = (const float4*)whit;
-        po.dirs = dirs;
-        po.n_az = n_az;
-        po.n_el = n_el;
-        po.tiles_u = tiles_u;
-        po.plb = (double*)patch_ws;
-        po.pvals = (uint32_t*)(po.plb + 8 * (size_t)cap);
-        po.pcnt = (int*)(po.pvals + 8 * (size_t)cap);
-        RFS_CUDA_TRY(cudaMemsetAsync(po.pcnt, 0, sizeof(int) * 8 * (size_t)n_tiles, st));  // empty tiles
-    }
     if (n <= 0 || cap <= 0) return RFS_OK;
     k_fill_stable<<<nb, BK_BLK, 0, st>>>(n, (const Rect*)rects, depth_code, tiles_u, n_tiles, nb, (uint32_t)cap, tab,
                                          toff, bcodes, bvals);
     RFS_LAUNCH_CHECK();
     int rc = launch_seg_sort<BK_SEG_SMALL, 512>(n_tiles, ranges, 0, bcodes, bvals, altc, altv, geom, ckeys, vals, lb,
-                                                po, st);
+                                                st);
     if (rc != RFS_OK) return rc;
     rc = launch_seg_sort<BK_SEG_MAX, 1024>(n_tiles, ranges, BK_SEG_SMALL, bcodes, bvals, altc, altv, geom, ckeys,
-                                           vals, lb, po, st);
+                                           vals, lb, st);
     if (rc != RFS_OK) return rc;
-    return launch_seg_sort<0, 1024>(n_tiles, ranges, BK_SEG_MAX, bcodes, bvals, altc, altv, geom, ckeys, vals, lb, po,
+    return launch_seg_sort<0, 1024>(n_tiles, ranges, BK_SEG_MAX, bcodes, bvals, altc, altv, geom, ckeys, vals, lb,
                                     st);
 }
 

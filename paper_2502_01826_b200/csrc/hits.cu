@@ -8,47 +8,34 @@
 // order and T do not depend on the transmitter, so this
 // runs once per step and the TX batch composites from its output.
 //
-// Exact streaming re-sort: candidates arrive in tile-key
-// (depth) order; a hit's chord midpoint lies in the Gaussian's 3-sigma ball,
-// so t_mid >= depth - r3, and a pending hit whose t_mid is below
+// Exact streaming re-sort: one thread per ray walks its
+// tile's depth-ordered candidate list; a
+// hit's chord midpoint lies in the Gaussian's 3-sigma ball, so
+// t_mid >= depth - r3, and a pending hit whose t_mid is below
 // lb[i] = min_{j>=i} (depth_j - r3_j) precedes every hit the remaining
 // candidates can produce: it is final and is emitted, and a ray stops
 // scanning as soon as it terminates.  Pending (t_mid, g, w) entries live in a
 // per-thread ring in shared memory; a ray that overflows it is redone by
 // k_hits_slow with a global buffer sized to its tile (exact, rarely taken).
-//
-// Execution: one thread per ray, 64-thread blocks (a 4 x 16 quarter tile, so
-// the whole grid is resident at once).  Each warp streams its tile's
-// candidate list on its own in chunks of CH:
-//   1. stage the chunk's fp32 filter data (bounding sphere, whitened ellipsoid)
-//      in warp-private shared memory (coalesced gathers, __syncwarp only);
-//   2. every lane tests all CH candidates against its ray from shared memory
-//      (no divergent global latency), building a survivor mask;
-//   3. survivors run the reference's fp64 disc prefilter + quadratic and are
-//      inserted in (t_mid, g) order;
-//   4. pending hits below the next chunk's bound are emitted.
-// Emitting once per chunk instead of per candidate does not change the order:
-// every hit of the chunk is >= its first candidate's bound.
+//   Per warp (a 4 x 8 ray patch), chunks of CH candidates: stage the fp32
+//   filter data in warp-private shared memory and have the bulk-copy engine
+//   bring the fp64 records of the cone-relevant ones (cp.async.bulk, one per
+//   record, completion counted on a warp mbarrier); every lane tests the
+//   chunk against its ray;
+//   survivors run the fp64 test and are inserted in (t_mid, g) order; pending
+//   hits below the next chunk's bound are emitted.
 //
 // Arithmetic: the fp32 tests carry proven margins (project.cu) so they never
 // reject an fp64 hit; the fp64 test follows the reference's operation order
 // with no FMA contraction (explicit __d*_rn), so exact ties order like the
-// reference.  Ray directions come from a table built with the reference's
-// formula (render.py:103-117).  T is carried in fp64.
+// reference; T *= rho is the reference's complex product without contraction.
+// Ray directions come from a table built with the reference's formula
+// (render.py:103-117).
 #include "rfs_common.cuh"
 
 namespace {
 
 constexpr double DINF = 1.0e300;
-
-// diagnostics: per-warp start / end %globaltimer of k_hits (null = off)
-__device__ unsigned long long* g_k6_timing = nullptr;
-
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 
 #define DM(a, b) __dmul_rn((a), (b))
 #define DA(a, b) __dadd_rn((a), (b))
@@ -120,10 +107,22 @@ struct Ray {
     bool hcap_over;
 };
 
+// T *= rho (_kernels.py:191), complex128 product without contraction
+__device__ __forceinline__ void advance_t(double& tre, double& tim, double rr, double ri) {
+    const double nr = DS(DM(tre, rr), DM(tim, ri));
+    const double ni = DA(DM(tre, ri), DM(tim, rr));
+    tre = nr;
+    tim = ni;
+}
+
+__device__ __forceinline__ bool terminated(double tre, double tim) {
+    return DA(DM(tre, tre), DM(tim, tim)) < RFS_TERM_EPS2;  // _kernels.py:186-187
+}
+
 // Emit one hit in sorted order: terminate, record, advance T (_kernels.py:186-191).
 __device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, float w, const RfsGeom* __restrict__ geom,
                                          RfsHit* __restrict__ slab_ray, int hcap, uint8_t* __restrict__ used) {
-    if (st.tre * st.tre + st.tim * st.tim < RFS_TERM_EPS2) {
+    if (terminated(st.tre, st.tim)) {
         st.done = true;
         return;
     }
@@ -140,11 +139,7 @@ __device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, float w, const Rfs
     }
     st.live += 1;
     const RfsGeom* G = geom + g;
-    double rr = __ldg(&G->rho_re), ri = __ldg(&G->rho_im);
-    double nr = st.tre * rr - st.tim * ri;
-    double ni = st.tre * ri + st.tim * rr;
-    st.tre = nr;
-    st.tim = ni;
+    advance_t(st.tre, st.tim, __ldg(&G->rho_re), __ldg(&G->rho_im));
 }
 
 // Reference quadratic on a shared-memory copy of the first 13 doubles of an
@@ -186,48 +181,8 @@ __device__ __forceinline__ bool exact_hit_s(const double* __restrict__ G, double
 }
 
 constexpr int GD = 13;   // doubles of an RfsGeom record used by the exact test
-constexpr int GDS = 14;  // their shared-memory row: 7 x 16-byte cp.async pieces
+constexpr int GDS = 14;  // their shared-memory row (112 B: one bulk copy of the record head)
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-
-// Long tile lists set K6's critical path (tools/k6_timing.py: the warps of the
-// longest lists take ~2x the mean).  Lists longer than split_min are split at
-// mid: piece A streams [start, mid) exactly as an unsplit list (emitting every
-// hit that precedes all of B's candidates, t_mid < lb[mid]) and parks its
-// still-pending hits and its T; piece B streams [mid, end) concurrently into a
-// sorted list of its own, without T or termination; k_hits_merge then merges
-// the two (t_mid, g)-sorted lists and walks them with T and the termination
-// rule -- the same hit sequence as one pass, since the reference itself sorts
-// all hits of a ray and walks them (_kernels.py:27-112, 184-191).
-constexpr int KS_ACAP = 64;  // A's parked hits (>= the largest pending ring)
-struct KSplit {
-    int split_min;  // lists longer than this are split (<= 0: never)
-    int bcap;       // capacity of a ray's B list
-    int* flag;      // per ray: 1 = A parked it (merge), 2 = the slow path owns it
-    double *a_tre, *a_tim;
-    int *a_live, *a_n;
-    double* a_t;
-    uint32_t* a_g;
-    float* a_w;
-    int* b_n;
-    double* b_t;
-    uint32_t* b_g;
-    float* b_w;
-};
-
-// Per-patch candidate lists (k_patch_lists): a tile list filtered by the
-// warp cone of each of its 8 ray patches (4 x 8 rays), with the emission
-// bounds recomputed over each filtered list.  K6 then streams only the
-// cone-relevant candidates (~15 % of the tile list at config 2): the same
-// hits (the cone test never rejects a hit), far fewer chunks per warp.
-struct KPatch {
-    const uint32_t* vals;  // [8 * M]: tile t's patch p list at 8 * start(t) + p * len(t); null: off
-    const double* lb;      // same layout: min over the list's later entries of lbv
-    const int* cnt;        // [n_tiles * 8]
-};
 
 template <int CH>
 struct WarpStage {
@@ -235,7 +190,7 @@ struct WarpStage {
     float4 wh[CH][4];
     uint32_t g[CH];
     double gd[CH][GDS];  // fp64 records of the chunk's cone-relevant candidates (by slot)
-    double lbs[CH];      // patch mode: emission bound after candidate j (lb of candidate j + 1)
+    uint64_t bar;        // completion of the chunk's record copies (bulk-copy engine)
 };
 
 template <int PCAP, int NT, int CH>
@@ -246,20 +201,18 @@ struct HitsSmem {
     WarpStage<CH> ws[NT / 32];
 };
 
+// Streaming K6 (dense scenes): see the file comment.
 template <int PCAP, int NT, int CH>
 __global__ void __launch_bounds__(NT) k_hits(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ vals, const double* __restrict__ lb,
     const float4* __restrict__ sph, const float4* __restrict__ whit, const RfsGeom* __restrict__ geom,
     const double* __restrict__ dirs, double rx0, double rx1, double rx2, double min_t, int n_az, int n_el,
     int tiles_u, int hcap, RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ slow_list,
-    int* __restrict__ stats, uint8_t* __restrict__ used, KSplit ks, KPatch kp) {
+    int* __restrict__ stats, uint8_t* __restrict__ used) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HitsSmem<PCAP, NT, CH>& S = *reinterpret_cast<HitsSmem<PCAP, NT, CH>*>(smem_raw);
     constexpr int PARTS = 256 / NT;
-    // split lists: a tile's piece-B blocks follow its piece-A blocks, so both
-    // pieces of a tile are resident together
-    const int per_tile = ks.split_min > 0 ? 2 * PARTS : PARTS;
-    const int tile = blockIdx.x / per_tile, wblk = blockIdx.x % per_tile, part = wblk % PARTS;
+    const int tile = blockIdx.x / PARTS, part = blockIdx.x % PARTS;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // each warp owns a 4 (u) x 8 (v) patch of the 16 x 16 tile
     const int q = part * (NT / 32) + wid, pu = q >> 1, pv = q & 1;
@@ -267,7 +220,6 @@ __global__ void __launch_bounds__(NT) k_hits(
     const int v = (tile / tiles_u) * RFS_TILE + 8 * pv + (lane & 7);
     const bool valid = u < n_az && v < n_el;
     const int r = valid ? u * n_el + v : 0;
-    const unsigned long long t_start = g_k6_timing ? gtimer() : 0ull;
     Ray st;
     st.dx = dirs[3 * r];
     st.dy = dirs[3 * r + 1];
@@ -285,60 +237,29 @@ __global__ void __launch_bounds__(NT) k_hits(
     bool pend_over = false;
     int head = 0, npend = 0, max_pend = 0;
     int n_sph = 0, n_wh = 0;
-    unsigned d_chunks = 0, d_rel = 0, d_nu = 0, d_mx = 0;  // diagnostics (g_k6_timing)
     double head_t = DINF;
     const int2 rg = ranges[tile];
-    const int Lt = rg.y - rg.x;
-    const bool pmode = kp.vals != nullptr;  // this warp's filtered patch list
-    const bool split = !pmode && ks.split_min > 0 && Lt > ks.split_min;
-    const bool second = wblk >= PARTS;  // piece B of a split list
-    if (second && !split) return;         // block-uniform
-    const int mid = split ? rg.x + Lt / 2 : rg.y;
-    const uint32_t* vl = vals;
-    const double* lbp = lb;
-    int c_lo, c_hi, c_end;
-    if (pmode) {
-        const size_t pb = 8 * (size_t)rg.x + (size_t)q * (size_t)Lt;
-        vl = kp.vals + pb;
-        lbp = kp.lb + pb;
-        c_lo = 0;
-        c_hi = c_end = kp.cnt[tile * 8 + q];
-    } else {
-        c_lo = second ? mid : rg.x;
-        c_hi = second ? rg.y : mid;
-        c_end = rg.y;
-    }
-    int b_n = 0;
+    const int c_lo = rg.x, c_hi = rg.y;
     WarpStage<CH>& W = S.ws[wid];
+    if (lane == 0) rfs_mbar_init(&W.bar, 1);
+    __syncwarp();
+    unsigned bar_phase = 0;
 
     // Warp cone: axis c through the patch, half-angle th_p covering its rays.
     // A ray can only hit a Gaussian whose bounding-sphere cone (axis mu - rx,
     // half-angle th_g = asin(r3/depth)) contains it, so a candidate is
     // relevant to the warp only if angle(c, mu - rx) <= th_p + th_g.
-    float cx = valid ? st.fx : 0.f, cy = valid ? st.fy : 0.f, cz = valid ? st.fz : 0.f;
-    cx = warp_sum(cx);
-    cy = warp_sum(cy);
-    cz = warp_sum(cz);
-    {
-        const float inv = rsqrtf(fmaxf(cx * cx + cy * cy + cz * cz, 1e-30f));
-        cx *= inv;
-        cy *= inv;
-        cz *= inv;
-    }
-    float cmin = valid ? cx * st.fx + cy * st.fy + cz * st.fz : 1.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
-    const float th_p = acosf(fminf(cmin, 1.f)) + 1e-4f;
-    float sin_p, cos_p;
-    sincosf(th_p, &sin_p, &cos_p);
+    float4 ca;
+    float2 cb;
+    rfs_patch_cone(tile, q, tiles_u, n_az, n_el, dirs, ca, cb);
 
     // register prefetch of the next chunk's filter data (lane j loads candidate base + j)
     uint32_t pf_g = 0;
     float4 pf_s = make_float4(0.f, 0.f, 0.f, 0.f), pf_w[4];
-    double pf_lb = DINF, pf_lbs = DINF;
+    double pf_lb = DINF;
     // candidate ids run one chunk further ahead than their records, so the
     // record gathers never wait on the id load (in-order issue)
-    uint32_t nx_g = c_lo + lane < c_hi ? vl[c_lo + lane] : 0u;
+    uint32_t nx_g = c_lo + lane < c_hi ? vals[c_lo + lane] : 0u;
     auto prefetch = [&](int b0) {
         if (b0 + lane < c_hi) {
             pf_g = nx_g;
@@ -346,30 +267,15 @@ __global__ void __launch_bounds__(NT) k_hits(
 #pragma unroll
             for (int k = 0; k < 4; ++k) pf_w[k] = __ldg(&whit[4 * pf_g + k]);
         }
-        if (b0 + CH + lane < c_hi) nx_g = vl[b0 + CH + lane];
-        // bound of every candidate after this chunk -- for piece A's last chunk
-        // that is B's first candidate, mid
-        const int nxt = min(b0 + CH, c_hi);
-        pf_lb = nxt < c_end ? lbp[nxt] : DINF;
-        if (pmode) pf_lbs = b0 + lane + 1 < c_end ? lbp[b0 + lane + 1] : DINF;
+        if (b0 + CH + lane < c_hi) nx_g = vals[b0 + CH + lane];
+        const int nxt = min(b0 + CH, c_hi);  // bound of every candidate after this chunk
+        pf_lb = nxt < c_hi ? lb[nxt] : DINF;
     };
     prefetch(c_lo);
     // emit every pending hit below `bound` (in (t_mid, g) order)
     auto emit_until = [&](double bound) {
         while (!st.done && head_t < bound) {
-            if (second) {  // piece B: into its own sorted list, no T / termination
-                if (b_n == ks.bcap) {
-                    pend_over = true;
-                    st.done = true;
-                    break;
-                }
-                const size_t o = (size_t)r * ks.bcap + b_n++;
-                ks.b_t[o] = S.pt[head][tid];
-                ks.b_g[o] = S.pg[head][tid];
-                ks.b_w[o] = S.pw[head][tid];
-            } else {
-                emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
-            }
+            emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
             head = (head + 1) & (PCAP - 1);
             --npend;
             head_t = npend > 0 ? S.pt[head][tid] : DINF;
@@ -384,35 +290,21 @@ __global__ void __launch_bounds__(NT) k_hits(
         if (lane < nb) {
             W.g[lane] = pf_g;
             W.sph[lane] = pf_s;
-            if (pmode) W.lbs[lane] = pf_lbs;
 #pragma unroll
             for (int k = 0; k < 4; ++k) W.wh[lane][k] = pf_w[k];
-            const float ang = th_p + pf_w[3].y;
-            if (pmode || ang >= 3.1415f) {  // patch lists are cone-filtered already
-                rel = true;
-            } else {
-                // cos(th_p + th_g) by angle addition (cos/sin th_g precomputed in K1)
-                const float m2 = pf_s.x * pf_s.x + pf_s.y * pf_s.y + pf_s.z * pf_s.z;
-                const float dotc = (cx * pf_s.x + cy * pf_s.y + cz * pf_s.z) * rsqrtf(m2);
-                rel = dotc >= cos_p * pf_w[3].z - sin_p * pf_w[3].w - 1e-5f;
-            }
+            rel = rfs_cone_relevant(ca, cb, pf_s, pf_w[3]);
         }
         const unsigned relmask = __ballot_sync(0xffffffffu, rel);
-        if (g_k6_timing) {
-            d_chunks += 1;
-            d_rel += __popc(relmask);
-        }
         const double lb_next = pf_lb;
         __syncwarp();
-        // fp64 records of the cone-relevant candidates -> shared memory,
-        // asynchronously (cp.async; lane j copies its own candidate's): they
-        // land while the fp32 filters run
-        if (rel) {
-            const char* src = reinterpret_cast<const char*>(geom + pf_g);
-#pragma unroll
-            for (int part = 0; part < GDS / 2; ++part) cp_async16(&W.gd[lane][2 * part], src + 16 * part);
+        // fp64 records of the cone-relevant candidates -> shared memory by the
+        // bulk-copy engine (lane j requests its own candidate's 112 bytes):
+        // they land while the fp32 filters run
+        if (relmask) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the last chunk's reads
+            if (lane == 0) rfs_mbar_arrive_expect_tx(&W.bar, (unsigned)__popc(relmask) * (GDS * 8u));
+            if (rel) rfs_bulk_g2s(W.gd[lane], geom + pf_g, GDS * 8u, &W.bar);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
         if (base + CH < c_hi) prefetch(base + CH);
         // 2. survivor mask from shared memory
         unsigned mask = 0;
@@ -430,13 +322,11 @@ __global__ void __launch_bounds__(NT) k_hits(
                 }
             }
         }
-        // 3a. the records' copies have landed (own copies, then the warp's)
-        if (g_k6_timing) {
-            d_nu += __popc(__reduce_or_sync(0xffffffffu, mask));
-            d_mx += __reduce_max_sync(0xffffffffu, (unsigned)__popc(mask));
+        // 3a. the records' copies have landed
+        if (relmask) {
+            rfs_mbar_wait(&W.bar, bar_phase);
+            bar_phase ^= 1u;
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp();
         if (!st.done) {
             // 3b. exact fp64 test and sorted insertion by (t_mid, g)
             while (mask) {
@@ -472,223 +362,28 @@ __global__ void __launch_bounds__(NT) k_hits(
                 ++npend;
                 max_pend = max(max_pend, npend);
                 head_t = fmin(head_t, t_mid);
-                // patch lists are dense: emit as soon as a hit precedes every
-                // later candidate (this lane has tested all candidates <= j),
-                // which keeps the pending ring short
-                if (pmode) {
-                    emit_until(W.lbs[j]);
-                    if (st.done) break;
-                }
             }
             // 4. emit every pending hit that precedes all later candidates
             emit_until(lb_next);
         }
         __syncwarp();
     }
-    // drain (also covers rays whose tile list ended with pending hits); a
-    // split list's piece A parks its pending hits and T for k_hits_merge
-    const bool park = split && !second && !st.done;
-    if (second) {
-        while (!st.done && npend > 0) {
-            if (b_n == ks.bcap) {
-                pend_over = true;
-                st.done = true;
-                break;
-            }
-            const size_t o = (size_t)r * ks.bcap + b_n++;
-            ks.b_t[o] = S.pt[head][tid];
-            ks.b_g[o] = S.pg[head][tid];
-            ks.b_w[o] = S.pw[head][tid];
-            head = (head + 1) & (PCAP - 1);
-            --npend;
-        }
-    } else if (park) {
-        for (int i = 0; i < npend; ++i) {
-            const int sl = (head + i) & (PCAP - 1);
-            const size_t o = (size_t)r * KS_ACAP + i;
-            ks.a_t[o] = S.pt[sl][tid];
-            ks.a_g[o] = S.pg[sl][tid];
-            ks.a_w[o] = S.pw[sl][tid];
-        }
-    } else {
-        while (!st.done && npend > 0) {
-            emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
-            head = (head + 1) & (PCAP - 1);
-            --npend;
-        }
-    }
-    if (g_k6_timing) {
-        const unsigned live_max = __reduce_max_sync(0xffffffffu, (unsigned)st.live);
-        if (lane == 0) {
-            unsigned long long* o = g_k6_timing + 8 * ((blockIdx.x * NT + tid) >> 5);
-            o[0] = t_start;
-            o[1] = gtimer();
-            o[2] = (unsigned long long)(c_hi - c_lo);
-            o[3] = d_chunks;
-            o[4] = d_rel;
-            o[5] = d_mx;
-            o[6] = d_nu;
-            o[7] = live_max;
-        }
+    // drain (also covers rays whose tile list ended with pending hits)
+    while (!st.done && npend > 0) {
+        emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
+        head = (head + 1) & (PCAP - 1);
+        --npend;
     }
     if (!valid) return;
     atomicMax(&stats[5], max_pend);
     atomicAdd(&stats[6], n_sph);
     atomicAdd(&stats[7], n_wh);
-    // split-ray handshake on flag[r]: 0 open, 1 parked by A (merge), 2 owned
-    // by the slow path, 3 terminated within A (B's hits are irrelevant)
     if (pend_over) {  // the slow path redoes the whole ray
-        bool to_slow = true;
-        if (split) {
-            const int old = second ? atomicCAS(&ks.flag[r], 0, 2) : atomicExch(&ks.flag[r], 2);
-            if (second && old == 1) atomicExch(&ks.flag[r], 2);
-            to_slow = second ? (old == 0 || old == 1) : old != 2;
-        }
-        if (to_slow) {
-            int idx = atomicAdd(&stats[0], 1);
-            slow_list[idx] = r;
-        }
+        const int idx = atomicAdd(&stats[0], 1);
+        slow_list[idx] = r;
         return;
     }
-    if (second) {
-        ks.b_n[r] = b_n;
-        return;
-    }
-    if (park) {
-        ks.a_n[r] = npend;
-        ks.a_tre[r] = st.tre;
-        ks.a_tim[r] = st.tim;
-        ks.a_live[r] = st.live;
-        atomicCAS(&ks.flag[r], 0, 1);  // unless B already handed the ray to the slow path
-        return;
-    }
-    if (split && atomicCAS(&ks.flag[r], 0, 3) == 2) return;  // B overflowed first: the slow path redoes it
     counts[r] = min(st.live, hcap);  // stored hits; live > hcap is flagged in stats[1]
-    if (st.hcap_over) atomicAdd(&stats[1], 1);
-    atomicMax(&stats[2], st.live);
-    atomicAdd(&stats[3], min(st.live, hcap));
-}
-
-// K6a: the per-patch candidate lists of KPatch.  Block per tile, warp w
-// computes patch w's cone exactly as k_hits does; every candidate is tested
-// against the 8 cones, compacted per patch in list order (ballots + warp
-// prefix), then each patch's emission bounds are the suffix minima of lbv
-// over its own list.
-constexpr int PL_NT = 1024;  // k_patch_lists threads: one tile list round of 1024 candidates
-__global__ void __launch_bounds__(PL_NT, 2) k_patch_lists(const int2* __restrict__ ranges, const uint32_t* __restrict__ vals,
-                                                       const float4* __restrict__ sph, const float4* __restrict__ whit,
-                                                       const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
-                                                       int n_az, int n_el, int tiles_u, uint32_t* __restrict__ pvals,
-                                                       double* __restrict__ plb, int* __restrict__ pcnt) {
-    constexpr int NW = PL_NT / 32;
-    __shared__ float4 ca[8];  // cx, cy, cz, th_p of patch p (a patch without rays never passes)
-    __shared__ float2 cb[8];  // cos_p, sin_p
-    __shared__ int run[8];
-    __shared__ unsigned wb[NW][8];  // [warp][patch] ballots of the current round
-    __shared__ int wpre[NW][8];     // [warp][patch] first position of the warp's entries
-    const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (wid < 8) {  // warp q: the cone of patch q, as k_hits computes it
-        float4 a;
-        float2 c;
-        rfs_patch_cone(tile, wid, tiles_u, n_az, n_el, dirs, a, c);
-        if (lane == 0) {
-            ca[wid] = a;
-            cb[wid] = c;
-            run[wid] = 0;
-        }
-    }
-    __syncthreads();
-    const int2 rg = ranges[tile];
-    const size_t L = (size_t)(rg.y - rg.x), tb = 8 * (size_t)rg.x;
-    unsigned lt;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-    for (int b0 = rg.x; b0 < rg.y; b0 += PL_NT) {
-        const int i = b0 + tid;
-        uint32_t g = 0, pm = 0;
-        double lbv = 0.0;
-        if (i < rg.y) {
-            g = vals[i];
-            const float4 sp = __ldg(&sph[g]);
-            const float4 w3 = __ldg(&whit[4 * g + 3]);
-            lbv = __ldg(&geom[g].lbv);
-            pm = rfs_patch_mask(ca, cb, sp, w3);
-        }
-#pragma unroll
-        for (int p = 0; p < 8; ++p) {
-            const unsigned m = __ballot_sync(0xffffffffu, (pm >> p) & 1u);
-            if (lane == 0) wb[wid][p] = m;
-        }
-        __syncthreads();
-        if (tid < 8) {  // per patch: each warp's first position this round
-            int acc = run[tid];
-            for (int w = 0; w < NW; ++w) {
-                wpre[w][tid] = acc;
-                acc += __popc(wb[w][tid]);
-            }
-            run[tid] = acc;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int p = 0; p < 8; ++p) {
-            if (!((pm >> p) & 1u)) continue;
-            const uint32_t pos = wpre[wid][p] + __popc(wb[wid][p] & lt);
-            pvals[tb + (size_t)p * L + pos] = g;
-            plb[tb + (size_t)p * L + pos] = lbv;  // raw lbv; suffix minima below
-        }
-        __syncthreads();
-    }
-    // warps 0-7: suffix minima of lbv over patch list p (contiguous, in place)
-    if (wid >= 8) return;
-    const int cnt = run[wid];
-    if (lane == 0) pcnt[tile * 8 + wid] = cnt;
-    double* pl = plb + tb + (size_t)wid * L;
-    double carry = INFINITY;
-    for (int k0 = ((cnt - 1) >> 5) << 5; k0 >= 0; k0 -= 32) {
-        const int k = k0 + lane;
-        double v = k < cnt ? pl[k] : INFINITY;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_down_sync(0xffffffffu, v, o);
-            if (lane + o < 32) v = fmin(v, y);
-        }
-        v = fmin(v, carry);
-        if (k < cnt) pl[k] = v;
-        carry = __shfl_sync(0xffffffffu, v, 0);
-    }
-}
-
-// Merge of a split list's two pieces (see KSplit): thread per ray parked by A.
-__global__ void k_hits_merge(int R, int hcap, KSplit ks, const RfsGeom* __restrict__ geom,
-                             RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ stats,
-                             uint8_t* __restrict__ used) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= R || ks.flag[r] != 1) return;
-    Ray st;
-    st.tre = ks.a_tre[r];
-    st.tim = ks.a_tim[r];
-    st.live = ks.a_live[r];
-    st.done = false;
-    st.hcap_over = st.live > hcap;
-    RfsHit* slab_ray = slab + (size_t)r * hcap;
-    const int na = ks.a_n[r], nbb = ks.b_n[r];
-    const double* at = ks.a_t + (size_t)r * KS_ACAP;
-    const uint32_t* ag = ks.a_g + (size_t)r * KS_ACAP;
-    const float* aw = ks.a_w + (size_t)r * KS_ACAP;
-    const double* bt = ks.b_t + (size_t)r * ks.bcap;
-    const uint32_t* bg = ks.b_g + (size_t)r * ks.bcap;
-    const float* bw = ks.b_w + (size_t)r * ks.bcap;
-    int i = 0, j = 0;
-    while (!st.done && (i < na || j < nbb)) {
-        const bool from_a = i < na && (j >= nbb || at[i] < bt[j] || (at[i] == bt[j] && ag[i] < bg[j]));
-        if (from_a) {
-            emit_hit(st, ag[i], aw[i], geom, slab_ray, hcap, used);
-            ++i;
-        } else {
-            emit_hit(st, bg[j], bw[j], geom, slab_ray, hcap, used);
-            ++j;
-        }
-    }
-    counts[r] = min(st.live, hcap);
     if (st.hcap_over) atomicAdd(&stats[1], 1);
     atomicMax(&stats[2], st.live);
     atomicAdd(&stats[3], min(st.live, hcap));
@@ -795,7 +490,7 @@ template <int PCAP, int NT, int CH>
 int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const double* lb, const void* sph,
                 const void* whit, const void* geom, const double* dirs, const double* rx, double min_t, int n_az,
                 int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used,
-                const KSplit& ks, const KPatch& kp, cudaStream_t st) {
+                cudaStream_t st) {
     static bool attr = false;
     size_t smem = sizeof(HitsSmem<PCAP, NT, CH>);
     if (!attr) {
@@ -807,10 +502,9 @@ int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const doub
                                           (int)cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
-    const int per_tile = (256 / NT) * (ks.split_min > 0 ? 2 : 1);
-    k_hits<PCAP, NT, CH><<<n_tiles * per_tile, NT, smem, st>>>(
+    k_hits<PCAP, NT, CH><<<n_tiles * (256 / NT), NT, smem, st>>>(
         (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom, dirs, rx[0],
-        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used, ks, kp);
+        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -818,14 +512,6 @@ int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const doub
 }  // namespace
 
 extern "C" {
-
-// diagnostics (not part of the rasterizer path): per-warp timing of k_hits into
-// buf (u64[8 * warps]: start, end, candidates, chunks, cone survivors, sum over
-// chunks of the most exact tests on one lane, union size, max live); NULL: off
-int rfs_debug_k6_timing(unsigned long long* buf) {
-    RFS_CUDA_TRY(cudaMemcpyToSymbol(g_k6_timing, &buf, sizeof(buf)));
-    return RFS_OK;
-}
 
 int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
     int R = n_az * n_el;
@@ -835,92 +521,30 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
     return RFS_OK;
 }
 
-// pcap selects the pending-ring template: 16 entries (64-thread blocks, 9
-// blocks/SM), 32 entries (64-thread blocks) or 64 entries (32-thread blocks)
-// for dense scenes.
-size_t rfs_hits_split_bytes(int n_rays, int bcap) {
-    const size_t R = (size_t)(n_rays > 0 ? n_rays : 0), B = (size_t)(bcap > 0 ? bcap : 0);
-    // per ray: flag, a_n, a_live, b_n (int); a_tre, a_tim (double); A's and B's lists (16 B per entry)
-    return R * (4 * sizeof(int) + 2 * sizeof(double)) + R * (KS_ACAP + B) * 16;
-}
-
-size_t rfs_hits_patch_bytes(int m_cap, int n_tiles) {
-    const size_t M = (size_t)(m_cap > 0 ? m_cap : 0), T = (size_t)(n_tiles > 0 ? n_tiles : 0);
-    return 8 * M * sizeof(double) + 8 * M * sizeof(uint32_t) + 8 * T * sizeof(int) + 64;
-}
-
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
-             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, int split_min,
-             int bcap, void* split_ws, int m_cap, void* patch_ws, int patch_built, void* stream) {
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (used && n > 0) RFS_CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)n, st));
-    int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
+    const int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     const int R = n_az * n_el;
     RFS_CUDA_TRY(cudaMemsetAsync(stats, 0, 8 * sizeof(int), st));
     RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)R, st));
     if (n_tiles <= 0) return RFS_OK;
-    KSplit ks{};
-    ks.split_min = (split_ws && bcap > 0) ? split_min : 0;
-    if (ks.split_min > 0) {
-        // carve the workspace: 8-byte arrays first, then 4-byte ones
-        char* p = (char*)split_ws;
-        auto take = [&](size_t bytes) {
-            char* q = p;
-            p += bytes;
-            return q;
-        };
-        const size_t Rz = (size_t)R, A = (size_t)KS_ACAP * Rz, B = (size_t)bcap * Rz;
-        ks.bcap = bcap;
-        ks.a_tre = (double*)take(Rz * 8);
-        ks.a_tim = (double*)take(Rz * 8);
-        ks.a_t = (double*)take(A * 8);
-        ks.b_t = (double*)take(B * 8);
-        ks.flag = (int*)take(Rz * 4);
-        ks.a_n = (int*)take(Rz * 4);
-        ks.a_live = (int*)take(Rz * 4);
-        ks.b_n = (int*)take(Rz * 4);
-        ks.a_g = (uint32_t*)take(A * 4);
-        ks.b_g = (uint32_t*)take(B * 4);
-        ks.a_w = (float*)take(A * 4);
-        ks.b_w = (float*)take(B * 4);
-        RFS_CUDA_TRY(cudaMemsetAsync(ks.flag, 0, Rz * 4, st));
-    }
-    KPatch kp{};
-    if (patch_ws && ks.split_min <= 0 && m_cap > 0) {
-        double* plb = (double*)patch_ws;
-        uint32_t* pv = (uint32_t*)(plb + 8 * (size_t)m_cap);
-        int* pc = (int*)(pv + 8 * (size_t)m_cap);
-        if (!patch_built) {  // else rfs_bin_bucket wrote them
-            k_patch_lists<<<n_tiles, PL_NT, 0, st>>>((const int2*)ranges, vals, (const float4*)sph,
-                                                     (const float4*)whit, (const RfsGeom*)geom, dirs, n_az, n_el,
-                                                     tiles_u, pv, plb, pc);
-            RFS_LAUNCH_CHECK();
-        }
-        kp.vals = pv;
-        kp.lb = plb;
-        kp.cnt = pc;
-    }
     int rc;
     // 64-thread blocks: 7 per SM, so 68 of a 360x180 grid's 1104 blocks start
-    // late (~90 us); 128-thread blocks (all resident) measured no faster -- the
-    // kernel is set by the longest warps' chains, not by the late starts
-    // (tools/k6_timing.py: warp duration mean 124 us, max 238 us at 100k)
+    // late; 128-thread blocks (all resident) measured no faster -- the kernel
+    // is set by the longest warps' chains, not by the late starts
     if (pcap <= 16)
         rc = launch_hits<16, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, kp, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
     else if (pcap <= 32)
         rc = launch_hits<32, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, kp, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
     else
         rc = launch_hits<64, 32, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, ks, kp, st);
+                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
     if (rc != RFS_OK) return rc;
-    if (ks.split_min > 0) {
-        k_hits_merge<<<rfs_ceil_div(R, 128), 128, 0, st>>>(R, hcap, ks, (const RfsGeom*)geom, (RfsHit*)slab, counts,
-                                                            stats, used);
-        RFS_LAUNCH_CHECK();
-    }
     k_max_range<<<rfs_ceil_div(n_tiles, 256), 256, 0, st>>>((const int2*)ranges, n_tiles, stats + 4);
     RFS_LAUNCH_CHECK();
     return RFS_OK;

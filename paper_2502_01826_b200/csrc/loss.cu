@@ -243,7 +243,8 @@ struct BwdSmem {
 __global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S, const float* __restrict__ pred,
                                                  const float* __restrict__ gt, const float* __restrict__ maps,
                                                  int n_az, int n_el, float w1, float ws, float wf,
-                                                 float* __restrict__ grad, float2* __restrict__ lam) {
+                                                 float* __restrict__ grad, float2* __restrict__ lam,
+                                                 float2* __restrict__ lamT) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdSmem& M = *reinterpret_cast<BwdSmem*>(smem_raw);
     const int b = blockIdx.z, u0 = blockIdx.y * TU, v0 = blockIdx.x * TV;
@@ -332,7 +333,9 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S
         const double g3 = 2.0 * d;                                                              // loss.py:146
         const double gx = (double)w1 * g1 + (double)ws * g2 + (double)wf * g3;                  // loss.py:149-155
         if (grad) grad[r] = (float)gx;
-        if (lam) lam[r] = make_float2((float)(2.0 * gx * sv[o].x), (float)(2.0 * gx * sv[o].y));  // grad.py:119
+        const float2 l = make_float2((float)(2.0 * gx * sv[o].x), (float)(2.0 * gx * sv[o].y));  // grad.py:119
+        if (lam) lam[r] = l;
+        if (lamT) lamT[(r - fb) * gridDim.z + b] = l;  // [R][B]: the backward's layout (a ray's TX row)
     }
 }
 
@@ -467,10 +470,11 @@ size_t rfs_loss_scratch_bytes(int n_frames, int n_az, int n_el) {
 }
 
 int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const float* pred, const float* gt,
-                      double w_ssim, double w_fourier, double* report, float* grad, void* lam, void* scratch,
+                      double w_ssim, double w_fourier, double* report, float* grad, void* lam, void* lamT, void* scratch,
                       size_t scratch_bytes, void* stream) {
     if (n_frames <= 0 || n_az <= 0 || n_el <= 0) return RFS_OK;
-    if ((S == nullptr && pred == nullptr) || (lam != nullptr && S == nullptr)) return RFS_ERR_CONTRACT;
+    if ((S == nullptr && pred == nullptr) || ((lam != nullptr || lamT != nullptr) && S == nullptr))
+        return RFS_ERR_CONTRACT;
     if (scratch_bytes < rfs_loss_scratch_bytes(n_frames, n_az, n_el)) return RFS_ERR_CAPACITY;
     const int rc = ensure_window();
     if (rc != RFS_OK) return rc;
@@ -488,7 +492,8 @@ int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const flo
     k_frame_range<<<dim3(RCH, n_frames), 256, 0, st>>>(gt, (int)R, range);
     k_ssim_fwd<<<grid, LT, sizeof(FwdSmem), st>>>((const float2*)S, pred, gt, range, n_az, n_el, maps, part);
     k_ssim_bwd<<<grid, LT, sizeof(BwdSmem), st>>>((const float2*)S, pred, gt, maps, n_az, n_el, (float)w1,
-                                                  (float)w_ssim, (float)w_fourier, grad, (float2*)lam);
+                                                  (float)w_ssim, (float)w_fourier, grad, (float2*)lam,
+                                                  (float2*)lamT);
     k_loss_final<<<rfs_ceil_div((long long)n_frames * 32, 128), 128, 0, st>>>(part, nblk, n_frames, (double)R, w1,
                                                                                 w_ssim, w_fourier, report);
     RFS_LAUNCH_CHECK();

@@ -114,18 +114,47 @@ __device__ __forceinline__ void rfs_patch_cone(int tile, int q, int tiles_u, int
     cb = any ? make_float2(cos_p, sin_p) : make_float2(1e30f, -1e30f);
 }
 
-// 8-bit mask of the patch cones a candidate (bounding sphere sp = (mu - rx, .),
-// cone record w3 = whit[4 g + 3]) may reach: k_hits' cone test
-__device__ __forceinline__ uint32_t rfs_patch_mask(const float4* ca, const float2* cb, float4 sp, float4 w3) {
+// k_hits' cone test: may a candidate (bounding sphere sp = (mu - rx, .), cone
+// record w3 = whit[4 g + 3] = (., th_g, cos th_g, sin th_g)) reach a ray of
+// the patch cone (ca = (axis, th_p), cb = (cos th_p, sin th_p))?  cos(th_p +
+// th_g) by angle addition, with a margin.
+__device__ __forceinline__ bool rfs_cone_relevant(float4 ca, float2 cb, float4 sp, float4 w3) {
+    if (ca.w + w3.y >= 3.1415f) return true;
     const float rs = rsqrtf(sp.x * sp.x + sp.y * sp.y + sp.z * sp.z);
-    uint32_t pm = 0;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-        const float4 c = ca[p];
-        const float2 d = cb[p];
-        const float dotc = (c.x * sp.x + c.y * sp.y + c.z * sp.z) * rs;
-        const bool rel = (c.w + w3.y >= 3.1415f) || dotc >= d.x * w3.z - d.y * w3.w - 1e-5f;
-        pm |= (uint32_t)rel << p;
-    }
-    return pm;
+    const float dotc = (ca.x * sp.x + ca.y * sp.y + ca.z * sp.z) * rs;
+    return dotc >= cb.x * w3.z - cb.y * w3.w - 1e-5f;
+}
+
+// ---- Blackwell bulk-copy engine (cp.async.bulk, non-tensor) + mbarrier ----
+// A thread copies `bytes` (multiple of 16, both addresses 16-byte aligned)
+// global -> shared without staging registers; completion is counted in bytes
+// on an mbarrier (complete_tx), which one thread arms with the expected total.
+__device__ __forceinline__ unsigned rfs_smem_addr(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void rfs_mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(rfs_smem_addr(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void rfs_mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(rfs_smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void rfs_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            rfs_smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(rfs_smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void rfs_mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "RFS_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra RFS_WAIT_%=;\n"
+        "}\n" ::"r"(rfs_smem_addr(bar)),
+        "r"(phase)
+        : "memory");
 }

@@ -41,14 +41,20 @@ def _ptr(t):
 
 
 def spectrum_loss_frames(S: torch.Tensor | None, gt: torch.Tensor, w_ssim: float = 0.2, w_fourier: float = 0.2,
-                         pred: torch.Tensor | None = None, want_lam: bool = True, want_grad: bool = False):
+                         pred: torch.Tensor | None = None, want_lam: bool = True, want_grad: bool = False,
+                         lam_layout: str = "frames"):
     """Loss of B frames on the device.
 
     S: complex64 [B, n_az, n_el] (the predicted power is |S|^2) or None with
     `pred` float32 [B, n_az, n_el] given; gt: float32 [B, n_az, n_el].
     Returns (report float64 [B, 4] = total, L1, SSIM, Fourier per frame,
-    lam complex64 [B, n_az, n_el] or None, grad float32 [B, n_az, n_el] or None).
+    lam or None, grad float32 [B, n_az, n_el] or None).  lam is complex64
+    [B, n_az, n_el] (lam_layout "frames"), or [n_az*n_el, B] ("rays": the
+    backward's layout, raster.backward(lamT=...), written directly by the
+    loss kernel -- no transpose pass).
     """
+    if lam_layout not in ("frames", "rays"):
+        raise ValueError("lam_layout must be 'frames' or 'rays'")
     ref = S if S is not None else pred
     if ref is None:
         raise ShapeError("spectrum_loss_frames needs S or pred")
@@ -68,13 +74,18 @@ def spectrum_loss_frames(S: torch.Tensor | None, gt: torch.Tensor, w_ssim: float
     if pred is not None:
         pred = pred.reshape(b, n_az, n_el).to(device=dev, dtype=torch.float32).contiguous()
     report = torch.empty((b, 4), dtype=torch.float64, device=dev)
-    lam = torch.empty((b, n_az, n_el), dtype=torch.complex64, device=dev) if want_lam else None
+    rays = lam_layout == "rays"
+    lam = None
+    if want_lam:
+        shape = (n_az * n_el, b) if rays else (b, n_az, n_el)
+        lam = torch.empty(shape, dtype=torch.complex64, device=dev)
     grad = torch.empty((b, n_az, n_el), dtype=torch.float32, device=dev) if want_grad else None
     lib = _native.load()
     nbytes = int(lib.rfs_loss_scratch_bytes(b, n_az, n_el))
     scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     _native.call("rfs_spectrum_loss", b, n_az, n_el, _ptr(S), _ptr(pred), _ptr(gt), float(w_ssim), float(w_fourier),
-                 _ptr(report), _ptr(grad), _ptr(lam), _ptr(scratch), nbytes, torch.cuda.current_stream(dev).cuda_stream)
+                 _ptr(report), _ptr(grad), None if rays else _ptr(lam), _ptr(lam) if rays else None, _ptr(scratch),
+                 nbytes, torch.cuda.current_stream(dev).cuda_stream)
     return report, lam, grad
 
 
@@ -163,7 +174,11 @@ def scalar_loss_frames(S: torch.Tensor, target: torch.Tensor, mode: str, want_la
     t = t.to(torch.complex64).contiguous()
     report = torch.empty((b, 4), dtype=torch.float64, device=dev)
     total = torch.empty(b, dtype=torch.complex64, device=dev)
-    lam = torch.empty((b, n_az, n_el), dtype=torch.complex64, device=dev) if want_lam else None
+    rays = lam_layout == "rays"
+    lam = None
+    if want_lam:
+        shape = (n_az * n_el, b) if rays else (b, n_az, n_el)
+        lam = torch.empty(shape, dtype=torch.complex64, device=dev)
     _native.call("rfs_scalar_loss", b, n_az * n_el, _SCALAR_MODES[mode], _ptr(S), _ptr(t), _ptr(report), _ptr(total),
                  _ptr(lam), torch.cuda.current_stream(dev).cuda_stream)
     return report, total, lam

@@ -143,19 +143,9 @@ class Geometry:
 
 # adaptive capacities, remembered across steps
 _CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {},
-         # K6 splits tile lists longer than this into two concurrent halves
-         # (rfs_hits' split_min; 0 = off); bcap = hits the second half may hold
-         "split_min": int(os.environ.get("RFS_K6_SPLIT", "0")), "bcap": 128,
          # tile-key sort of the hand-written backend: "bucket" (per-tile buckets,
          # bucket.cu) or "radix" (global onesweep)
          "tile_sort": os.environ.get("RFS_TILE_SORT", "bucket"), "tile_max": {},
-         # by-Gaussian hit index of the hand-written backend: "radix" (hit keys +
-         # global onesweep) or "count" (gindex.cu; bitwise the same, measured
-         # ~10 us slower at config 2: 119 vs 111 us)
-         "gindex": os.environ.get("RFS_GINDEX", "radix"),
-         # K6 streams per-patch cone-filtered candidate lists (k_patch_lists): bitwise the
-         # same hits, K6 203 -> 174 us, but the filter pass costs 31 us -- off until it is cheaper
-         "patch_lists": os.environ.get("RFS_K6_PATCH", "0") == "1",
          # the early by-Gaussian index on the side stream (overlapping psi / K7 / loss)
          "index_side": os.environ.get("RFS_INDEX_SIDE", "1") == "1"}
 _DIRS: dict = {}
@@ -268,20 +258,6 @@ def _spin(ev: torch.cuda.Event) -> None:
         pass
 
 
-_SPLIT_WS: dict = {}
-
-
-def _split_ws(dev, R: int, bcap: int) -> torch.Tensor:
-    """K6 split workspace (rfs_hits_split_bytes), kept across steps."""
-    key = (str(dev), R, bcap)
-    ws = _SPLIT_WS.get(key)
-    if ws is None:
-        _SPLIT_WS.clear()
-        ws = torch.empty(int(_native.load().rfs_hits_split_bytes(R, bcap)), dtype=torch.uint8, device=dev)
-        _SPLIT_WS[key] = ws
-    return ws
-
-
 def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bool = False,
                    hcap: int | None = None, marks: list | None = None, psi_tx: torch.Tensor | None = None,
                    index: bool = False, forward: bool = False, after_forward=None) -> Geometry:
@@ -335,8 +311,6 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     status_h = _pinned(dev, "status", 8)
     m_dev_ptr = status.data_ptr() + 4
 
-    patch_state = {"built": False}  # K6 patch lists written by the bucket sort
-
     def bin_tiles(cap: int, device_count: bool, bucket: bool):
         """K2b fill, K3 sort, K4 ranges, K4b bounds into buffers of capacity `cap`."""
         ck = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
@@ -348,15 +322,10 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             bv = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
             tt = torch.empty(max(int(lib.rfs_bin_bucket_temp_bytes(n, n_az, n_el, cap)), 16), dtype=torch.uint8,
                              device=dev)
-            pw = (_persistent("k6_patch", int(lib.rfs_hits_patch_bytes(max(cap, 1), n_tiles)), torch.uint8, dev)
-                  if _CAPS["patch_lists"] and _CAPS["split_min"] <= 0 and cap > 0 else None)
             _native.call("rfs_bin_bucket", n, _ptr(rects), _ptr(code), n_az, n_el, cap, _ptr(geom), _ptr(bc),
-                         _ptr(bv), _ptr(tt), _ptr(ck), _ptr(vl), _ptr(rg), _ptr(lbv), _ptr(status), _ptr(sph),
-                         _ptr(whit), _ptr(dirs), _ptr(pw) if pw is not None else None, st)
+                         _ptr(bv), _ptr(tt), _ptr(ck), _ptr(vl), _ptr(rg), _ptr(lbv), _ptr(status), st)
             _mark(marks, "bin+sort")
-            patch_state["built"] = pw is not None
             return ck, vl, rg, lbv
-        patch_state["built"] = False
         mp = m_dev_ptr if device_count else None
         if cap > 0:
             _native.call("rfs_bin_fill", n, _ptr(rects), _ptr(code), _ptr(offsets), n_az, cap, _ptr(ck), _ptr(vl), st)
@@ -402,21 +371,9 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     used = torch.empty(nn, dtype=torch.uint8, device=dev)
     while True:
         slab = torch.empty(R * hc * 16, dtype=torch.uint8, device=dev)
-        split_min, bcap = _CAPS["split_min"], _CAPS["bcap"]
-        split_ws = _split_ws(dev, R, bcap) if split_min > 0 else None
-        mcap_v = int(vals.numel())
-        patch_ws = (_persistent("k6_patch", int(lib.rfs_hits_patch_bytes(mcap_v, n_tiles)), torch.uint8, dev)
-                    if _CAPS["patch_lists"] and split_ws is None else None)
-        built = int(patch_ws is not None and patch_state["built"])  # by the bucket sort
         _native.call("rfs_hits", _ptr(ranges), n_tiles, _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit), _ptr(geom),
                      _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, pc, _ptr(slab), _ptr(ray_counts),
-                     _ptr(slow), _ptr(stats), _ptr(used), n, split_min, bcap,
-                     _ptr(split_ws) if split_ws is not None else None, mcap_v,
-                     _ptr(patch_ws) if patch_ws is not None else None, built, st)
-        if split_ws is not None:
-            _native.launch_counter["kernels"] += 1  # k_hits_merge
-        if patch_ws is not None and not built:
-            _native.launch_counter["kernels"] += 1  # k_patch_lists
+                     _ptr(slow), _ptr(stats), _ptr(used), n, st)
         ev_hits = torch.cuda.Event()
         ev_hits.record()
         _mark(marks, "hits")
@@ -445,6 +402,10 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                     gauss_index(early, h_cap, _persistent)
                     ready = torch.cuda.Event()
                     ready.record(side)
+                # the side stream reads these main-stream buffers: keep them alive
+                # (a geometry dropped without a backward) until it is done
+                slab.record_stream(side)
+                ray_counts.record_stream(side)
                 _INDEX_GEN[0] += 1
                 early.gidx["ready"] = ready
                 early.gidx["gen"] = _INDEX_GEN[0]
@@ -453,6 +414,12 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                 _mark(marks, "gauss_index")
         _spin(ev_s)  # read #2: hit-list statistics (and M when read #1 was skipped)
         s = stats_h.tolist()
+
+        def join_early():
+            # a redo rewrites ray_counts / the slab in place: not while the early index reads them
+            if early is not None and "ready" in early.gidx:
+                torch.cuda.current_stream(dev).wait_event(early.gidx["ready"])
+
         if m_cap is not None:
             host = status_h.tolist()
             if int(host[0]) & (1 << 1):
@@ -460,6 +427,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             m = int(host[1]) & 0xFFFFFFFF
             _CAPS["m_cap"][(n, n_az, n_el)] = max(m_cap, m + m // 8 + 1024) if m <= m_cap else m + m // 4 + 1024
             if m > m_cap:  # capacity overflow: re-bin with the exact count, redo the hit lists
+                join_early()
                 m_cap = None
                 ckeys, vals, ranges, lb = bin_tiles(m, False, bucket)
                 redo_forward = True
@@ -470,6 +438,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             # ring for the next steps if it happens often
             if s[0] > R // 1000 and pc < 64:
                 _CAPS["pcap"] = 2 * pc
+            join_early()
             pcap = max(int(s[4]), 1)
             nr = int(s[0])
             pt = torch.empty(nr * pcap, dtype=torch.float64, device=dev)
@@ -482,6 +451,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             s[1], s[2], s[3] = s2[1], s2[2], s2[3]
             redo_forward = True
         if s[1] > 0:
+            join_early()
             hc = 1 << max(6, math.ceil(math.log2(max(s[2], 1))))
             _CAPS["hcap"] = max(_CAPS["hcap"], hc)
             redo_forward = True
@@ -565,23 +535,6 @@ def gauss_index(geo: Geometry, h_cap: int | None = None, alloc=_fresh) -> None:
     st = _stream()
     R = geo.n_rays
     cap = int(h_cap if h_cap is not None else geo.total_hits)
-    if geo.sort_backend == "hand" and _CAPS["gindex"] == "count" and geo.n > 0:
-        # gindex.cu: counting + per-Gaussian segment sorts, no global radix sort
-        n = geo.n
-        g_off = alloc("gi_goff", n + 1, torch.int32, dev)
-        scratch = alloc("gi_scratch", int(lib.rfs_gauss_index_scratch_elems(n, cap)), torch.int32, dev)
-        temp = alloc("gi_temp", int(lib.rfs_scan_temp_elems(n)), torch.int32, dev)
-        c1 = max(cap, 1)
-        sorted_g = alloc("gi_sorted_g", c1, torch.int64, dev)
-        s_slot = alloc("gi_s_slot", c1, torch.int32, dev)
-        s_ray = alloc("gi_s_ray", c1, torch.int32, dev)
-        s_w = alloc("gi_s_w", c1, torch.float32, dev)
-        s_wt = alloc("gi_s_wt", c1, torch.complex64, dev)
-        _native.call("rfs_gauss_index", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, n, cap, _ptr(scratch),
-                     _ptr(temp), _ptr(g_off), _ptr(sorted_g), _ptr(s_slot), _ptr(s_ray), _ptr(s_w), _ptr(s_wt), st)
-        geo.gidx = {"h": cap, "h_dev": g_off.data_ptr() + 4 * n, "tot": g_off[n:], "sorted_g": sorted_g,
-                    "g_off": g_off, "s_ray": s_ray, "s_w": s_w, "s_wt": s_wt, "s_slot": s_slot}
-        return
     ray_off = alloc("gi_ray_off", R, torch.int32, dev)
     tot = alloc("gi_tot", 1, torch.int32, dev)
     temp = alloc("gi_rtemp", int(lib.rfs_scan_temp_elems(R)), torch.int32, dev)
@@ -623,15 +576,25 @@ def transpose_upstream(grad_S: torch.Tensor) -> torch.Tensor:
     return lamT
 
 
-def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.Tensor,
+def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.Tensor | None,
              include_direction_chain: bool = True, psi: torch.Tensor | None = None,
-             marks: list | None = None, deterministic: bool = False, lamT: torch.Tensor | None = None) -> dict:
+             marks: list | None = None, deterministic: bool = False, lamT: torch.Tensor | None = None,
+             out: dict | None = None, on_coeffs=None) -> dict:
     """K8a/K8i/K9: gradients summed over the TX batch (GradientBuffer.add, grad.py:85-92).
 
     grad_S is the complex-packed upstream lambda = dL/dRe S + i dL/dIm S
     (grad.py:4-8), which is also PyTorch's gradient convention for complex
-    tensors.  Returns fp32 tensors with the GradientBuffer meaning plus
-    d_trans_mag_raw (the logit chain of train.py:161-162).
+    tensors.  `lamT` (optional, complex64 [n_az*n_el, B], B <= 256) is the
+    same upstream ray-major -- the layout K8 reads, written directly by the
+    loss kernel (loss.spectrum_loss_frames(lam_layout="rays")); with it,
+    grad_S may be None.  Returns fp32 tensors with the GradientBuffer meaning
+    plus d_trans_mag_raw (the logit chain of train.py:161-162).
+
+    `out` (optional): preallocated output tensors (e.g. the views of
+    parallel.GradBuffer, so the all-reduce needs no packing); `on_coeffs`
+    (optional callable) receives a CUDA event recorded when d_coeffs is final
+    (after K9b, on the side stream) -- the hook for an all-reduce bucket that
+    overlaps the rest of the epilogue.
 
     Every sum has a fixed order and there are no atomics: the buffer is
     bitwise reproducible.  `deterministic` is accepted for
@@ -639,27 +602,34 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     """
     tx = _check_tx(tx)
     b = int(tx.shape[0])
-    if tuple(grad_S.shape) != (b, geo.n_az, geo.n_el):
-        raise ShapeError("upstream frame shape does not match the scene grid")
+    R = geo.n_rays
+    if lamT is not None and (tuple(lamT.shape) != (R, b) or lamT.dtype != torch.complex64 or b > MAX_TX_PER_LAUNCH):
+        raise ShapeError("lamT must be complex64 [n_az*n_el, B] with B <= 256")
+    if grad_S is None:
+        if lamT is None:
+            raise ShapeError("backward needs grad_S or lamT")
+    else:
+        if tuple(grad_S.shape) != (b, geo.n_az, geo.n_el):
+            raise ShapeError("upstream frame shape does not match the scene grid")
+        grad_S = grad_S.to(torch.complex64).contiguous()
     dev = scene.means.device
     n, K = scene.n, (scene.fle_degree + 1) ** 2
-    grad_S = grad_S.to(torch.complex64).contiguous()
     st = _stream()
-    out = {
-        "d_mean": torch.empty((n, 3), dtype=torch.float32, device=dev),
-        "d_quat": torch.empty((n, 4), dtype=torch.float32, device=dev),
-        "d_log_scale": torch.empty((n, 3), dtype=torch.float32, device=dev),
-        "d_trans_mag": torch.empty(n, dtype=torch.float32, device=dev),
-        "d_trans_mag_raw": torch.empty(n, dtype=torch.float32, device=dev),
-        "d_trans_phase": torch.empty(n, dtype=torch.float32, device=dev),
-        "d_coeffs": torch.empty((n, K), dtype=torch.complex64, device=dev),
-        "d_cov": torch.empty((n, 3, 3), dtype=torch.float32, device=dev),
-    }
+    shapes = {"d_mean": ((n, 3), torch.float32), "d_quat": ((n, 4), torch.float32),
+              "d_log_scale": ((n, 3), torch.float32), "d_trans_mag": ((n,), torch.float32),
+              "d_trans_mag_raw": ((n,), torch.float32), "d_trans_phase": ((n,), torch.float32),
+              "d_coeffs": ((n, K), torch.complex64), "d_cov": ((n, 3, 3), torch.float32)}
+    if out is None:
+        out = {k: torch.empty(sh, dtype=dt, device=dev) for k, (sh, dt) in shapes.items()}
+    else:
+        for k, (sh, dt) in shapes.items():
+            t = out[k]
+            if tuple(t.shape) != sh or t.dtype != dt or not t.is_contiguous() or t.device != dev:
+                raise ShapeError(f"out[{k!r}] must be a contiguous {dt} tensor of shape {sh} on {dev}")
     if n == 0 or b == 0:
         for v in out.values():
             v.zero_()
         return out
-    R = geo.n_rays
     lib = _native.load()
     built = geo.gidx is None
     if geo.gidx is not None and geo.gidx.get("gen", _INDEX_GEN[0]) != _INDEX_GEN[0]:
@@ -701,6 +671,10 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
                          _ptr(dm_dir), _ptr(out["d_coeffs"]), side.cuda_stream)
         for t in (txc, P, dm_dir, out["d_coeffs"]):
             t.record_stream(side)
+    if on_coeffs is not None:  # d_coeffs is final once the side stream gets here
+        ev = torch.cuda.Event()
+        ev.record(side)
+        on_coeffs(ev)
     _mark(marks, "backward_tx")
     _native.call("rfs_bwd_rays", _ptr(geo.slab), _ptr(geo.ray_counts), geo.hcap, R, _ptr(geo.rho32), _ptr(geo.geom),
                  _ptr(C), _ptr(gs), st)

@@ -1,0 +1,93 @@
+"""Data-parallel step on the GPU: 2 ranks (gloo) sharing cuda:0 run
+parallel.dp_step -- each its TX shard, the backward writing into a
+GradBuffer, the bucketed all-reduce overlapped with the epilogue -- and the
+reduced gradients must equal the full-batch backward and the oracle's sum
+over all TX (grad.py:85-92).  (NCCL cannot put two ranks on one GPU; the
+driver's multi-GPU runs use NCCL through the same code.)"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+import oracle  # noqa: E402
+from helpers import GRAD_KEYS, class_rel, l1_upstream  # noqa: E402
+
+from paper_2502_01826_b200.scene import bench_scene, default_txs, round_to_f32  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+N, AZ, EL, B = 8_000, 180, 90, 6
+
+
+def _case():
+    s = round_to_f32(bench_scene(np.random.default_rng(5), N, AZ, EL))
+    txs = default_txs(B, seed=2)
+    oc = oracle.OracleContext(s)
+    lams, ref = [], None
+    for t in txs:
+        oc.set_tx(t)
+        lam = l1_upstream(oc.forward())
+        lams.append(lam)
+        g = oc.backward(lam)
+        ref = g if ref is None else {k: ref[k] + g[k] for k in ref}
+    return s, txs, np.stack(lams), ref
+
+
+def _worker(rank, world, port, s, txs, lams, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_01826_b200 import api, parallel, raster
+
+        ds = raster.DeviceScene.from_host(s, "cuda:0")
+        tx = torch.as_tensor(txs, dtype=torch.float32, device="cuda:0")
+        lam = torch.as_tensor(lams.astype(np.complex64), device="cuda:0")
+        gb = parallel.GradBuffer(ds.n, ds.fle_degree, "cuda:0")
+        for _ in range(2):  # second step: the early side-stream index, reused buffer
+            S, g = parallel.dp_step(ds, tx, lam, gb=gb)
+        torch.cuda.synchronize()
+        q.put((rank, api.GradientBuffer.from_device(g).__dict__, g["d_trans_mag_raw"].cpu().numpy(),
+               gb.payload_floats))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dp_step_two_ranks_equals_full_batch_and_oracle():
+    from paper_2502_01826_b200 import api, raster
+
+    s, txs, lams, ref = _case()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, s, txs, lams, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in procs:
+        r, g, raw, pf = q.get(timeout=300)
+        out[r] = (g, raw, pf)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = api.backward_frames(s, txs, lams)
+    for k in ("d_mean", "d_quat", "d_log_scale", "d_trans_mag", "d_trans_phase", "d_coeffs"):
+        # identical on both ranks, equal to the single-process batch, and to the oracle
+        np.testing.assert_array_equal(out[0][0][k], out[1][0][k])
+        # (the shard sums are rounded to fp32 before the reduce: d(phase), a sum
+        # of strongly cancelling terms, shows it most)
+        assert class_rel(out[0][0][k], getattr(full, k)) <= 2e-4, k
+        assert class_rel(out[0][0][k], ref[k]) <= 1e-3, k
+    sg = 1 / (1 + np.exp(-s.trans_mag_raw.astype(np.float64)))
+    assert class_rel(out[0][1], ref["d_trans_mag"] * sg * (1 - sg)) <= 1e-3
+    assert out[0][2] == 44  # reduced floats per Gaussian

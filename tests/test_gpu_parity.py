@@ -321,80 +321,12 @@ def test_bucket_binning_bitwise_equals_radix(which):
 
 def _huge_gaussian_scene():
     """bench scene + one Gaussian whose 3-sigma ball holds the receiver: it is
-    hit by (nearly) every ray, a segment far longer than gindex's shared-memory
-    sort (the bitmap path)."""
+    hit by (nearly) every ray: one by-Gaussian segment of ~R hits."""
     s = bench_scene(np.random.default_rng(17), 20_000, 360, 180)
     s.means[0] = [3.0, 0.5, -0.2]
     s.log_scales[0] = np.log([2.5, 2.0, 2.2])
     s.trans_mag_raw[0] = -2.0
     return round_to_f32(s)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("which", ["config1", "special_", "bench100k", "huge"])
-def test_counting_gauss_index_bitwise_equals_radix(which):
-    """gindex.cu (per-Gaussian counting + segment sorts) must give bitwise the
-    by-Gaussian index of the radix path (hit keys + onesweep + offsets +
-    gather): the backward's fixed summation order depends on it."""
-    import torch
-
-    if which == "config1":
-        s = config1_scene()
-    elif which.endswith("_"):
-        s = scene_from(load("edge_scenes.npz"), which)
-    elif which == "huge":
-        s = _huge_gaussian_scene()
-    else:
-        s = round_to_f32(bench_scene(np.random.default_rng(8), 100_000, 360, 180))
-    ds = raster.DeviceScene.from_host(s, "cuda")
-    saved = dict(raster._CAPS)
-    out = {}
-    try:
-        for mode in ("radix", "count"):
-            raster._CAPS["gindex"] = mode
-            raster._CAPS["h_cap"] = {}
-            g = raster.build_geometry(ds, index=True)
-            gi = g.gidx
-            if "ready" in gi:  # built on the side stream
-                torch.cuda.current_stream().wait_event(gi["ready"])
-            H = g.total_hits
-            out[mode] = [gi["g_off"][: g.n + 1].cpu().numpy()] + [
-                gi[k][:H].cpu().numpy() for k in ("sorted_g", "s_slot", "s_ray", "s_w", "s_wt")]
-    finally:
-        raster._CAPS.update(saved)
-    if which == "huge":
-        assert np.diff(out["count"][0]).max() > 8192  # the bitmap path was taken
-    for a, b in zip(out["radix"], out["count"]):
-        np.testing.assert_array_equal(a, b)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("which", ["config1", "special_", "hemi_", "bench20k", "bench100k"])
-def test_patch_lists_bitwise_equal_full_lists(which):
-    """K6 on per-patch cone-filtered candidate lists (k_patch_lists) must give
-    bitwise the hit lists, used marks and spectra of K6 on the full tile lists."""
-    import torch
-
-    if which == "config1":
-        s = config1_scene()
-    elif which.endswith("_"):
-        s = scene_from(load("edge_scenes.npz"), which)
-    else:
-        s = round_to_f32(bench_scene(np.random.default_rng(12), 20_000 if which == "bench20k" else 100_000, 360, 180))
-    ds = raster.DeviceScene.from_host(s, "cuda")
-    tx = torch.as_tensor(default_txs(3, seed=6), dtype=torch.float32, device="cuda")
-    saved = dict(raster._CAPS)
-    out = {}
-    try:
-        for mode in (False, True):
-            raster._CAPS["patch_lists"] = mode
-            g = raster.build_geometry(ds, psi_tx=tx, forward=True)
-            out[mode] = (g.S.cpu().numpy(), *_hit_lists(g), g.used.cpu().numpy(), g.stats[3])
-    finally:
-        raster._CAPS.update(saved)
-    for a, b in zip(out[False][:4], out[True][:4]):
-        np.testing.assert_array_equal(a, b)
-    assert out[False][4] == out[True][4]
 
 
 @pytest.mark.gpu
@@ -426,37 +358,6 @@ def _hit_lists(g):
     slab = g.slab.view(-1, g.hcap, 16).cpu().numpy()
     keep = np.arange(g.hcap)[None, :] < counts[:, None]
     return counts, slab[keep]
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("n", [3_000, 40_000])
-def test_split_lists_bitwise_equal_unsplit(n):
-    """K6 streams long tile lists as two concurrent halves merged afterwards
-    (rfs_hits split_min); the hit lists, spectra and used marks must be
-    bitwise those of the single pass, also when the second half overflows its
-    list (bcap) and the ray falls back to the slow path."""
-    import torch
-
-    s = round_to_f32(bench_scene(np.random.default_rng(31), n, 72, 36))
-    ds = raster.DeviceScene.from_host(s, "cuda")
-    tx = torch.as_tensor(default_txs(3, seed=5), dtype=torch.float32, device="cuda")
-    saved = dict(raster._CAPS)
-    out = {}
-    try:
-        for split_min, bcap in ((0, 128), (16, 128), (200, 128), (16, 1)):
-            raster._CAPS["split_min"], raster._CAPS["bcap"] = split_min, bcap
-            g = raster.build_geometry(ds, psi_tx=tx, forward=True)
-            out[(split_min, bcap)] = (g.S.cpu().numpy(), *_hit_lists(g), g.used.cpu().numpy(), g.stats[0],
-                                      g.stats[3])
-    finally:
-        raster._CAPS.update(saved)
-    base = out[(0, 128)]
-    for key, o in out.items():
-        for a, b in zip(base[:4], o[:4]):
-            np.testing.assert_array_equal(a, b, err_msg=str(key))
-        assert o[5] == base[5], key  # total live hits
-    if n >= 40_000:
-        assert out[(16, 1)][4] > base[4]  # one-entry second-half lists overflowed: slow path taken
 
 
 @pytest.mark.gpu
