@@ -237,30 +237,21 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
         float4 pa[NP];
 #pragma unroll
         for (int j = 0; j < NP; ++j) pa[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        // groups of BG_U hits (the last one padded with zero hits), one
-        // transposed 8-value reduction each; the lambda rows of the next group
-        // are requested before the current one is reduced (the kernel is
-        // bound by the latency of these row gathers)
-        auto load_group = [&](int base, float4 (&L)[BG_U][NP], float2 (&W)[BG_U]) {
+        // full groups of BG_U hits (one transposed 8-value reduction each),
+        // then the segment's 1-3 remaining hits one at a time: most segments
+        // in a chunk are short, so padding them to BG_U would waste ~2x
+        int i0 = s0;
+        for (; i0 + BG_U <= e; i0 += BG_U) {
+            float4 l[BG_U][NP];
+            float2 wt[BG_U];
 #pragma unroll
             for (int u = 0; u < BG_U; ++u) {
-                const int i = base + u;
-                const bool ok = i < e;
-                const uint32_t r = ok ? sh_s[wl][i] >> hshift : 0u;
-                W[u] = ok ? sh_wt[wl][i] : make_float2(0.f, 0.f);
+                const int i = i0 + u;
+                const uint32_t r = sh_s[wl][i] >> hshift;
+                wt[u] = sh_wt[wl][i];
 #pragma unroll
-                for (int j = 0; j < NP; ++j)
-                    L[u][j] = ok ? __ldg(&lamT[(size_t)r * nq + lane + 32 * j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int j = 0; j < NP; ++j) l[u][j] = __ldg(&lamT[(size_t)r * nq + lane + 32 * j]);
             }
-        };
-        float4 l[BG_U][NP];
-        float2 wt[BG_U];
-        load_group(s0, l, wt);
-        for (int i0 = s0; i0 < e; i0 += BG_U) {
-            float4 ln[BG_U][NP];
-            float2 wn[BG_U];
-            const bool more = i0 + BG_U < e;
-            if (more) load_group(i0 + BG_U, ln, wn);
             float v[8];
 #pragma unroll
             for (int u = 0; u < BG_U; ++u) {
@@ -283,18 +274,29 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
             const float x = reduce8(v, lane);
             if ((lane & 3) == 0) {  // lanes 4i hold value i = 2u + component of hit i0 + u
                 const int i = lane >> 2, u = i >> 1;
-                if (i0 + u < e) {
-                    float* cf = reinterpret_cast<float*>(C + sh_s[wl][i0 + u]) + (i & 1);
-                    *cf = accumulate ? *cf + x : x;
-                }
+                float* cf = reinterpret_cast<float*>(C + sh_s[wl][i0 + u]) + (i & 1);
+                *cf = accumulate ? *cf + x : x;
             }
-            if (more) {
+        }
+        for (; i0 < e; ++i0) {
+            const uint32_t r = sh_s[wl][i0] >> hshift;
+            const float2 w = sh_wt[wl][i0];
+            float cr = 0.f, ci = 0.f;
 #pragma unroll
-                for (int u = 0; u < BG_U; ++u) {
-                    wt[u] = wn[u];
-#pragma unroll
-                    for (int j = 0; j < NP; ++j) l[u][j] = ln[u][j];
-                }
+            for (int j = 0; j < NP; ++j) {
+                const float4 a = __ldg(&lamT[(size_t)r * nq + lane + 32 * j]), q = ps[j];
+                cr += a.x * q.x + a.y * q.y + a.z * q.z + a.w * q.w;
+                ci += a.x * q.y - a.y * q.x + a.z * q.w - a.w * q.z;
+                pa[j].x += a.x * w.x + a.y * w.y;
+                pa[j].y += a.x * w.y - a.y * w.x;
+                pa[j].z += a.z * w.x + a.w * w.y;
+                pa[j].w += a.z * w.y - a.w * w.x;
+            }
+            cr = warp_sum(cr);
+            ci = warp_sum(ci);
+            if (lane == 0) {
+                float2* cp = C + sh_s[wl][i0];
+                *cp = accumulate ? make_float2(cp->x + cr, cp->y + ci) : make_float2(cr, ci);
             }
         }
         // flush p_acc: whole row, or this chunk's partial (2w: first segment, 2w+1: last)

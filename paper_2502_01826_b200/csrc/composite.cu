@@ -69,15 +69,12 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward(const RfsHit* __restrict
     }
 }
 
-// Even TX count: lanes own TX pairs (one 16-byte psi vector per hit).  A
+// Even TX count: lanes own TX pairs (one 16-byte psi vector per hit), hit
+// records loaded lane-parallel and broadcast, four psi rows in flight.  A
 // block covers an FP_U x FP_V patch of rays (neighbouring rays cross mostly
-// the same Gaussians, so their psi rows are L1 hits); a warp owns 4 of its
-// rays.  The kernel is bound by the latency of the psi-row gathers, so the
-// warp first loads its 4 rays' counts and first 32 hit records together,
-// then walks each ray FV_U psi rows at a time (all FV_U loads in flight).
-constexpr int FV_U = 8;
-constexpr int FP_U = 2, FP_V = 16, FP_RAYS = FP_U * FP_V;
-constexpr int FV_RPW = FP_RAYS / (CP_THREADS / 32);  // rays per warp
+// the same Gaussians, so their psi rows are L1 hits).
+constexpr int FV_U = 4;
+constexpr int FP_U = 1, FP_V = 32, FP_RAYS = FP_U * FP_V;
 __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restrict__ slab,
                                                           const int* __restrict__ counts, int hcap,
                                                           const float4* __restrict__ psi, int nb, int n_az, int n_el,
@@ -90,63 +87,40 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
     const int R = n_az * n_el;
     const int nq = nb >> 1, q = (bc >> 1) + lane;  // this lane's float4 column
     const bool on = 2 * lane + bc < nb;
-    // this warp's rays rl = wid + 8 j: counts, then the first 32 records of each
-    int rid[FV_RPW], cnt[FV_RPW];
-    RfsHit rec[FV_RPW];
-#pragma unroll
-    for (int j = 0; j < FV_RPW; ++j) {
-        const int rl = wid + (CP_THREADS / 32) * j;
+    for (int rl = wid; rl < FP_RAYS; rl += CP_THREADS / 32) {
         const int u = u0 + rl / FP_V, v = v0 + rl % FP_V;
-        rid[j] = (u < n_az && v < n_el) ? u * n_el + v : -1;
-    }
-    {
-        int c = 0;
-        const int jj = lane & (FV_RPW - 1);
-        int rj = rid[0];
-#pragma unroll
-        for (int j = 1; j < FV_RPW; ++j)
-            if (jj == j) rj = rid[j];
-        if (lane < FV_RPW && rj >= 0) c = min(counts[rj], hcap);
-#pragma unroll
-        for (int j = 0; j < FV_RPW; ++j) cnt[j] = __shfl_sync(0xffffffffu, c, j);
-    }
-#pragma unroll
-    for (int j = 0; j < FV_RPW; ++j) {
-        rec[j].g = 0;
-        rec[j].w = rec[j].t_re = rec[j].t_im = 0.f;
-        if (lane < cnt[j]) rec[j] = slab[(size_t)rid[j] * hcap + lane];
-    }
-#pragma unroll
-    for (int j = 0; j < FV_RPW; ++j) {
-        const int rl = wid + (CP_THREADS / 32) * j;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int c = cnt[j];
-        for (int kc = 0; kc < c; kc += 32) {
-            RfsHit hl = rec[j];
-            if (kc > 0) {  // rays with more than 32 live hits
-                hl.g = 0;
-                hl.w = hl.t_re = hl.t_im = 0.f;
-                if (kc + lane < c) hl = slab[(size_t)rid[j] * hcap + kc + lane];
-            }
-            const float2 wtl = make_float2(hl.w * hl.t_re, hl.w * hl.t_im);
-            const int n_in = min(32, c - kc);
-            for (int i0 = 0; i0 < n_in; i0 += FV_U) {
-                float4 pv[FV_U];
-                float2 wt[FV_U];
-#pragma unroll
-                for (int uu = 0; uu < FV_U; ++uu) {
-                    const int i = (i0 + uu) & 31;  // lanes >= n_in carry w = 0, g = 0
-                    const uint32_t g = __shfl_sync(0xffffffffu, hl.g, i);
-                    wt[uu].x = __shfl_sync(0xffffffffu, wtl.x, i);
-                    wt[uu].y = __shfl_sync(0xffffffffu, wtl.y, i);
-                    pv[uu] = (on && i0 + uu < n_in) ? __ldg(&psi[(size_t)g * nq + q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (u < n_az && v < n_el) {
+            const int r = u * n_el + v;
+            const int cnt = min(counts[r], hcap);
+            const RfsHit* h = slab + (size_t)r * hcap;
+            for (int kc = 0; kc < cnt; kc += 32) {
+                RfsHit hl;
+                if (kc + lane < cnt) {
+                    hl = h[kc + lane];
+                } else {
+                    hl.g = 0; hl.w = 0.f; hl.t_re = 0.f; hl.t_im = 0.f;
                 }
+                const float2 wtl = make_float2(hl.w * hl.t_re, hl.w * hl.t_im);
+                const int n_in = min(32, cnt - kc);
+                for (int i0 = 0; i0 < n_in; i0 += FV_U) {
+                    float4 pv[FV_U];
+                    float2 wt[FV_U];
 #pragma unroll
-                for (int uu = 0; uu < FV_U; ++uu) {
-                    acc.x += wt[uu].x * pv[uu].x - wt[uu].y * pv[uu].y;
-                    acc.y += wt[uu].x * pv[uu].y + wt[uu].y * pv[uu].x;
-                    acc.z += wt[uu].x * pv[uu].z - wt[uu].y * pv[uu].w;
-                    acc.w += wt[uu].x * pv[uu].w + wt[uu].y * pv[uu].z;
+                    for (int u = 0; u < FV_U; ++u) {
+                        const int i = i0 + u;  // lanes >= n_in carry w = 0, g = 0
+                        const uint32_t g = __shfl_sync(0xffffffffu, hl.g, i & 31);
+                        wt[u].x = __shfl_sync(0xffffffffu, wtl.x, i & 31);
+                        wt[u].y = __shfl_sync(0xffffffffu, wtl.y, i & 31);
+                        pv[u] = on ? __ldg(&psi[(size_t)g * nq + q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < FV_U; ++u) {
+                        acc.x += wt[u].x * pv[u].x - wt[u].y * pv[u].y;
+                        acc.y += wt[u].x * pv[u].y + wt[u].y * pv[u].x;
+                        acc.z += wt[u].x * pv[u].z - wt[u].y * pv[u].w;
+                        acc.w += wt[u].x * pv[u].w + wt[u].y * pv[u].z;
+                    }
                 }
             }
         }
