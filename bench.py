@@ -130,6 +130,19 @@ def algo_bytes(n: int, m: int, r: int, b: int) -> dict:
     }
 
 
+def hitlist_bytes(n: int, used: int, h: int, r: int, b: int) -> dict:
+    """Algorithmic bytes per launch of the compositing kernels under the hit-list
+    design: H live hits (16 B slab records; the by-Gaussian index
+    = 8 B id + 4 B slot + 8 B wT per hit), `used` Gaussians with a live hit (their
+    psi / p_acc rows, B complex64 each), R rays (their S / lambda rows)."""
+    row = b * 8
+    return {
+        "K7": h * 16 + used * row + r * row,                        # slab, psi rows, S
+        "K8c": h * 20 + used * row + r * row + h * 8 + used * row,  # index, psi, lamT rows, C out, p_acc out
+        "K8r": h * 16 + h * 8 + used * 32 + h * 16,                 # slab, C, rho (fp32 + fp64), per-hit scalars out
+    }
+
+
 def load_traffic() -> dict:
     """ncu dram bytes per launch of the compositing kernels (profiles/*_traffic.json, newest)."""
     import glob
@@ -184,6 +197,7 @@ def run_ours(args):
     hit_stats = {"max_live": geo.stats[2], "max_tile_list": geo.stats[4], "max_pending": geo.stats[5],
                  "sphere_pass": geo.stats[6], "whitened_pass": geo.stats[7], "slow_rays": geo.stats[0]}
     R = geo.n_rays
+    n_used = int(geo.used[: ds.n].sum().item())  # Gaussians with a live hit (rows K7 / K8 touch)
     del S0, P0
     # spectrum loss alone (not part of `value`): timed separately
     from paper_2502_01826_b200 import loss as _loss
@@ -257,38 +271,46 @@ def run_ours(args):
     ms_per_step = t_ms / args.steps
     value = world * B * args.steps / (t_ms / 1e3)
 
-    # roofline of the compositing kernels (SURVEY.md §8(d) algorithmic bytes per launch / the
-    # launch's mean duration from the CUDA-event marks of the timed steps); traffic = ncu
-    # dram bytes of the same launches from the committed --set full capture (profiles/)
+    # Roofline of the compositing kernels.  Algorithmic bytes per launch under the
+    # hit-list design (every byte a kernel must move at least once --
+    # the live-hit slab / by-Gaussian index, each used psi / lambda / p_acc row once,
+    # the output), divided by the kernel's own duration: the CUDA events recorded on
+    # its stream right before and after it in every timed step (raster._mark).
+    # SURVEY.md §8(d)'s model (per-incidence tile gathers, M·68) is reported beside
+    # it for comparison.  traffic = ncu dram bytes of the same launch from the
+    # committed --set full capture (profiles/*_traffic.json).
     pk = peaks()
-    ab = algo_bytes(ds.n, M, R, B)
     ph_ms = {k: float(np.mean(v)) for k, v in phases.items()}
     traffic = load_traffic()
+    hb = hitlist_bytes(ds.n, n_used, H, R, B)
+    ab = algo_bytes(ds.n, M, R, B)
     kern = {
-        "K7 forward composite (k_forward_v)": (ab["forward"], ph_ms.get("forward"), ("k_forward_v",)),
-        "K8 backward composite (k_lam_transpose + k_bwd_gauss_v + k_bwd_rays)":
-            (ab["backward"], ph_ms.get("backward_tx", 0) + ph_ms.get("backward_rays", 0),
-             ("k_lam_transpose", "k_bwd_gauss_v", "k_bwd_rays")),
-        "K9 epilogue (k_grad_tx || k_geom_seg + k_geom_fix + k_geom_final)":
-            (ab["epilogue"], ph_ms.get("grad_geom", 0), ("k_grad_tx", "k_geom_seg", "k_geom_fix", "k_geom_final")),
+        "K7 forward composite (k_forward_v)": (hb["K7"], ph_ms.get("forward"), "k_forward_v", ab["forward"]),
+        "K8c backward by Gaussian (k_bwd_gauss_v)": (hb["K8c"], ph_ms.get("bwd_gauss"), "k_bwd_gauss_v", None),
+        "K8r backward ray recursion (k_bwd_rays)": (hb["K8r"], ph_ms.get("backward_rays"), "k_bwd_rays", None),
     }
     roof = {}
-    for k, (byts, ms, knames) in kern.items():
+    for k, (byts, ms, kname, survey) in kern.items():
+        if not ms:
+            continue
         ach = byts / (ms / 1e3) / 1e9
-        tr = [traffic.get(kn) for kn in knames]
         roof[k] = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                   "frac": round(ach / pk["hbm_gbs"], 4), "algo_bytes": byts, "ms": round(ms, 4),
-                   "traffic": int(sum(tr)) if all(t is not None for t in tr) else None}
-    dom = max((k for k in kern if not k.startswith("K9")), key=lambda k: kern[k][1])
+                   "frac": round(ach / pk["hbm_gbs"], 4), "algo_bytes": int(byts), "ms": round(ms, 4),
+                   "traffic": traffic.get(kname)}
+        if survey is not None:
+            roof[k]["survey_model_bytes"] = int(survey)  # SURVEY §8(d) K7 = M·68 + N·B·8 + R·B·8
+    # the dominant HBM-class kernel of the step (largest share of the step)
+    dom = max(roof, key=lambda k: roof[k]["ms"])
     rl = dict(roof[dom])
     rl["kernel"] = dom
     rl["peak_source"] = pk["source"]
     rl["traffic_source"] = traffic.get("_source")
-    # K6 (hit lists) is the longest single kernel; its bound is FP32/FP64 issue + latency, not HBM
-    # (SURVEY.md §8(d)): report its algorithmic flops for context
+    rl["bytes_model"] = "hit-list design, DESIGN.md §4"
+    # K6 (hit lists) is the longest single kernel; its bound is fp64 / latency, not HBM
+    # (SURVEY.md §8(d)): its algorithmic flops for context
     flops_k6 = 64800 * (765 * 10 + 423 * 60)
     roof["K6 hit lists (k_hits), not HBM-bound"] = {
-        "bound": "fp32 issue", "achieved_tflops": round(flops_k6 / (ph_ms.get("hits", 1) / 1e3) / 1e12, 3),
+        "bound": "fp64 / latency", "achieved_tflops": round(flops_k6 / (ph_ms.get("hits", 1) / 1e3) / 1e12, 3),
         "algo_flops": flops_k6, "ms": round(ph_ms.get("hits", 0), 4)}
 
     # ---- end to end: one training step through the public API (api.train_step_host):
@@ -337,6 +359,9 @@ def run_ours(args):
             "config": {"workload": "config 2: 100k Gaussians (cli._bench_scene seed 0), 360x180 grid, "
                                    f"{B} TX per GPU, fwd+bwd step", "gaussians": ds.n, "tx_per_gpu": B,
                        "global_tx": B * world, "grid": "360x180", "incidences_M": M, "live_hits_H": H,
+                       "used_gaussians": n_used,
+                       "upstream": "fixed synthetic lambda, given to the backward in the loss kernel's "
+                                   "ray-major output layout (made once, outside the timed steps)",
                        "sort": args.sort, "hit_stats": hit_stats,
                        "parallelism": f"dp{world} (TX-sharded, grads all-reduced)",
                        "l2": "flushed between steps (256 MB write)"},

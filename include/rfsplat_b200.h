@@ -248,7 +248,10 @@ int rfs_scalar_loss(int n_frames, int n_rays, int mode, const void* S, const voi
  *   (train.py:145-162); grad_ema / last_dmean (nullable) get
  *   TrainState.observe (train.py:102-105).  *bad (device i64) = class * N + row
  *   of the first non-finite gradient row (class order of train.py:133-142),
- *   0x7f7f7f7f7f7f7f7f if none -- in which case nothing is updated.
+ *   0x7f7f7f7f7f7f7f7f if none -- in which case nothing is updated; prior
+ *   (nullable, device i64): the first bad value of earlier steps -- a value
+ *   other than the sentinel skips the update too (a training loop that checks
+ *   only at its sync points leaves the scene as of its last good step).
  * rfs_density_flags: mode 0 densify (keep = !split, clone, split: grad_ema >
  *   thr_grad, radius = trace(Sigma)/3 > thr_radius splits), mode 1 prune
  *   (keep = sigmoid(raw) >= thr_prune); u32 flags per Gaussian.
@@ -262,7 +265,8 @@ int rfs_scalar_loss(int n_frames, int n_rays, int mode, const void* S, const voi
 int rfs_sgd_step(int n, int K, const float* lrs, float ema_decay, const float* d_mean, const float* d_quat,
                  const float* d_log_scale, const float* d_trans_mag, const float* d_trans_phase, const void* d_coeffs,
                  float* means, float* quats, float* log_scales, float* trans_mag_raw, float* trans_phase,
-                 void* coeffs, float* grad_ema, float* last_dmean, long long* bad, void* stream);
+                 void* coeffs, float* grad_ema, float* last_dmean, long long* bad,
+                 const long long* prior, void* stream);
 int rfs_density_flags(int n, int mode, const float* grad_ema, const float* log_scales, const float* trans_mag_raw,
                       double thr_grad, double thr_radius, double thr_prune, uint32_t* keep, uint32_t* clone,
                       uint32_t* split, void* stream);
@@ -273,6 +277,24 @@ int rfs_density_apply(int n, int K, int mode, const uint32_t* keep, const uint32
                       const float* trans_mag_raw, const float* trans_phase, const void* coeffs, const float* grad_ema,
                       const float* last_dmean, float* o_means, float* o_quats, float* o_log_scales, float* o_raw,
                       float* o_phase, void* o_coeffs, float* o_ema, float* o_last, void* stream);
+
+/* Synthetic datasets on the GPU (oracle.py:100-177: multipath_signal,
+ * spectrum_oracle, rssi_oracle, csi_oracle) for a batch of n_samples TX
+ * (tx f64[S*3], device).  paths: n_paths records of rfs_datagen_path_bytes()
+ * bytes {f64 reflector[3], amplitude, extra_phase; i32 direct, pad} (device).
+ * rfs_spectrum_dataset: gain (complex128[S*P]) / cell (i32[2*S*P]) are
+ * scratch, power32 (f32[S*n_az*n_el], nullable) / power64 (f64, nullable) the
+ * frames |coherent sum of gain x Gaussian beam|^2.  rfs_scalar_dataset:
+ * mode 0 rssi (f64[S] dBm), mode 1 csi (complex128[S*n_sub] at f_c + k
+ * spacing).  status (device i32): bit 0 = zero-length path, bit 1 = arrival
+ * point on the receiver (the reference's GeometryError). */
+size_t rfs_datagen_path_bytes(void);
+int rfs_spectrum_dataset(int n_samples, const double* tx, int n_paths, const void* paths, const double* rx,
+                         double f_c, int n_az, int n_el, double sigma_beam, int rolloff, void* gain, int* cell,
+                         float* power32, double* power64, int* status, void* stream);
+int rfs_scalar_dataset(int n_samples, const double* tx, int n_paths, const void* paths, const double* rx,
+                       double f_c, int mode, int n_sub, double spacing, int rolloff, double* rssi, void* csi,
+                       int* status, void* stream);
 
 /* Library / build identification. */
 int rfs_version(void);

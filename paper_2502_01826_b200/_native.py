@@ -58,10 +58,13 @@ _SIGS = {
     "rfs_loss_scratch_bytes": (sz, [i32, i32, i32]),
     "rfs_spectrum_loss": (i32, [i32, i32, i32, vp, vp, vp, f64, f64, vp, vp, vp, vp, vp, sz, vp]),
     "rfs_scalar_loss": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),
-    "rfs_sgd_step": (i32, [i32, i32, vp, C.c_float, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "rfs_sgd_step": (i32, [i32, i32, vp, C.c_float, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rfs_density_flags": (i32, [i32, i32, vp, vp, vp, f64, f64, f64, vp, vp, vp, vp]),
     "rfs_density_apply": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_ulonglong, i32,
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "rfs_datagen_path_bytes": (sz, []),
+    "rfs_spectrum_dataset": (i32, [i32, vp, i32, vp, vp, f64, i32, i32, f64, i32, vp, vp, vp, vp, vp, vp]),
+    "rfs_scalar_dataset": (i32, [i32, vp, i32, vp, vp, f64, i32, i32, f64, i32, vp, vp, vp, vp]),
     "rfs_version": (i32, []),
     "rfs_device_arch": (i32, []),
 }
@@ -102,7 +105,7 @@ KERNELS_PER_CALL = {
     "rfs_forward": 1, "rfs_lam_transpose": 1, "rfs_bwd_gauss": 1, "rfs_bwd_rays": 1, "rfs_hit_keys": 1, "rfs_gauss_offsets": 1, "rfs_grad_geom": 3,
     "rfs_grad_tx": 1, "rfs_gather_sorted": 1,
     "rfs_ray_dirs": 1, "rfs_spectrum_loss": 4, "rfs_sgd_step": 2, "rfs_scalar_loss": 1, "rfs_density_flags": 1,
-    "rfs_density_apply": 1,
+    "rfs_density_apply": 1, "rfs_spectrum_dataset": 2, "rfs_scalar_dataset": 1,
 }
 launch_counter = {"kernels": 0}
 

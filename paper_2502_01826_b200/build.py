@@ -32,6 +32,7 @@ SOURCES = {
     "grad.cu": [],
     "loss.cu": [],
     "train.cu": [],
+    "datagen.cu": [],
     "capi.cu": [],
 }
 

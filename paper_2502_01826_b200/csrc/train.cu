@@ -86,9 +86,11 @@ __global__ void k_sgd_update(int n, int K, float lr_mean, float lr_rot, float lr
                              float* __restrict__ means, float* __restrict__ quats, float* __restrict__ log_scales,
                              float* __restrict__ raw, float* __restrict__ phase, float* __restrict__ coeffs,
                              float* __restrict__ grad_ema, float* __restrict__ last_dmean,
-                             const long long* __restrict__ bad) {
+                             const long long* __restrict__ bad,
+                             const long long* __restrict__ prior) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n || *bad != 0x7f7f7f7f7f7f7f7fLL) return;
+    if (prior && *prior != 0x7f7f7f7f7f7f7f7fLL) return;  // an earlier step was bad: the scene stays as it was
     float dm[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -220,7 +222,8 @@ extern "C" {
 int rfs_sgd_step(int n, int K, const float* lrs, float ema_decay, const float* d_mean, const float* d_quat,
                  const float* d_log_scale, const float* d_trans_mag, const float* d_trans_phase, const void* d_coeffs,
                  float* means, float* quats, float* log_scales, float* trans_mag_raw, float* trans_phase,
-                 void* coeffs, float* grad_ema, float* last_dmean, long long* bad, void* stream) {
+                 void* coeffs, float* grad_ema, float* last_dmean, long long* bad, const long long* prior,
+                 void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     RFS_CUDA_TRY(cudaMemsetAsync(bad, 0x7f, sizeof(long long), st));  // sentinel 0x7f7f..7f = no bad row
     if (n <= 0) return RFS_OK;
@@ -230,7 +233,7 @@ int rfs_sgd_step(int n, int K, const float* lrs, float ema_decay, const float* d
     k_sgd_update<<<grid, 256, 0, st>>>(n, K, lrs[0], lrs[1], lrs[2], lrs[3], lrs[4], ema_decay, d_mean, d_quat,
                                        d_log_scale, d_trans_mag, d_trans_phase, (const float*)d_coeffs, means, quats,
                                        log_scales, trans_mag_raw, trans_phase, (float*)coeffs, grad_ema, last_dmean,
-                                       bad);
+                                       bad, prior);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -320,8 +320,17 @@ def load_checkpoint(path):
     return scene, doc["iteration"], doc["config"]
 
 
-def checkpoint_from_device(ds, carrier_freq: float = 2.4e9, bounds=((-60.0,) * 3, (60.0,) * 3)) -> CheckpointScene:
-    """A raster.DeviceScene (fp32 in HBM) as a checkpointable scene (values widened to float64)."""
+def checkpoint_from_device(ds, carrier_freq: float | None = None, bounds=None) -> CheckpointScene:
+    """A raster.DeviceScene (fp32 in HBM) as a checkpointable scene (values widened to float64).
+
+    carrier_freq / bounds default to the scene's own metadata (kept by
+    device_scene_from_checkpoint / DeviceScene.from_host), so a checkpoint
+    round trip through training keeps them; a scene without them needs both.
+    """
+    carrier_freq = carrier_freq if carrier_freq is not None else getattr(ds, "carrier_freq", None)
+    bounds = bounds if bounds is not None else getattr(ds, "bounds", None)
+    if carrier_freq is None or bounds is None:
+        raise DataError("checkpoint_from_device: the scene carries no carrier_freq / bounds; pass them")
     c = lambda t: t.detach().cpu().numpy()
     return CheckpointScene(c(ds.means).astype(np.float64), c(ds.quats).astype(np.float64),
                            c(ds.log_scales).astype(np.float64), c(ds.trans_mag_raw).astype(np.float64),

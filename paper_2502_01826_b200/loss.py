@@ -174,11 +174,7 @@ def scalar_loss_frames(S: torch.Tensor, target: torch.Tensor, mode: str, want_la
     t = t.to(torch.complex64).contiguous()
     report = torch.empty((b, 4), dtype=torch.float64, device=dev)
     total = torch.empty(b, dtype=torch.complex64, device=dev)
-    rays = lam_layout == "rays"
-    lam = None
-    if want_lam:
-        shape = (n_az * n_el, b) if rays else (b, n_az, n_el)
-        lam = torch.empty(shape, dtype=torch.complex64, device=dev)
+    lam = torch.empty((b, n_az, n_el), dtype=torch.complex64, device=dev) if want_lam else None
     _native.call("rfs_scalar_loss", b, n_az * n_el, _SCALAR_MODES[mode], _ptr(S), _ptr(t), _ptr(report), _ptr(total),
                  _ptr(lam), torch.cuda.current_stream(dev).cuda_stream)
     return report, total, lam

@@ -49,6 +49,21 @@ def _mark(marks, name):
         marks.append((name, ev))
 
 
+def _meta_carrier(scene):
+    c = getattr(scene, "carrier_freq", None)
+    return None if c is None else float(c)
+
+
+def _meta_bounds(scene):
+    b = getattr(scene, "bounds", None)  # RFScene: Box(lo, hi)
+    if b is not None and hasattr(b, "lo"):
+        return (tuple(float(x) for x in b.lo), tuple(float(x) for x in b.hi))
+    lo, hi = getattr(scene, "bounds_lo", None), getattr(scene, "bounds_hi", None)  # io.CheckpointScene
+    if lo is not None and hi is not None:
+        return (tuple(float(x) for x in np.asarray(lo).reshape(3)), tuple(float(x) for x in np.asarray(hi).reshape(3)))
+    return None
+
+
 @dataclass
 class DeviceScene:
     """fp32 device copy of a scene's SoA parameters (the boundary's inputs)."""
@@ -64,6 +79,10 @@ class DeviceScene:
     n_az: int = 360
     n_el: int = 180
     fle_degree: int = 3
+    # scene metadata the rasterizer does not use, carried for checkpoints
+    # (RFScene.carrier_freq / bounds, scene.py:205-246); None when unknown
+    carrier_freq: float | None = None
+    bounds: tuple | None = None
 
     @property
     def n(self) -> int:
@@ -78,6 +97,7 @@ class DeviceScene:
             torch.as_tensor(np.ascontiguousarray(scene.coeffs, dtype=np.complex64), device=device),
             tuple(float(x) for x in np.asarray(scene.rx, dtype=np.float64).reshape(3)),
             float(scene.ress_radius), int(scene.n_az), int(scene.n_el), int(getattr(scene, "fle_degree", 3)),
+            _meta_carrier(scene), _meta_bounds(scene),
         )
 
     def validate(self) -> None:
@@ -638,8 +658,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     gi = geo.gidx
     if "ready" in gi:  # built on the side stream
         torch.cuda.current_stream(geo.slab.device).wait_event(gi["ready"])
-    if built:
-        _mark(marks, "gauss_index")
+    _mark(marks, "gauss_index" if built else "index_wait")
     h = gi["h"]
     main = torch.cuda.current_stream(dev)
     side = _side_stream(dev)
@@ -662,6 +681,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         _native.call("rfs_bwd_gauss", n, h, gi["h_dev"], nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_slot"]), geo.hcap,
                      _ptr(gi["s_wt"]), _ptr(gi["g_off"]), _ptr(psic), _ptr(lamTc), int(c0 > 0), _ptr(C), _ptr(P),
                      _ptr(part), _ptr(pcnt), st)
+        _mark(marks, "bwd_gauss")
         # K9b on a second stream: it needs only P, so it overlaps the ray
         # recursion and the geometry sums below (K9c waits for it)
         side.wait_stream(main)

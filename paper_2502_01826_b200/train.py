@@ -107,11 +107,12 @@ def _ptr(t):
 
 
 def sgd_step(scene: raster.DeviceScene, grads: dict, iteration: int, config: TrainConfig,
-             state: TrainState | None = None, check: bool = True) -> None:
+             state: TrainState | None = None, check: bool = True, prior: torch.Tensor | None = None) -> None:
     """One descent step on the device (train.py:145-162), plus TrainState.observe
     when `state` is given.  A non-finite gradient row leaves the scene untouched;
     with check=True the error is raised here (one 8-byte read), else it can be
-    read later from `sgd_step.last_bad`."""
+    read later from `sgd_step.last_bad`.  `prior` (optional device i64, the
+    first bad value of earlier unchecked steps) skips the update once set."""
     n, K = scene.n, scene.coeffs.shape[1]
     dev = scene.means.device
     bad = torch.empty(1, dtype=torch.int64, device=dev)
@@ -122,7 +123,8 @@ def sgd_step(scene: raster.DeviceScene, grads: dict, iteration: int, config: Tra
                  _ptr(grads["d_log_scale"]), _ptr(grads["d_trans_mag"]), _ptr(grads["d_trans_phase"]),
                  _ptr(grads["d_coeffs"]), _ptr(scene.means), _ptr(scene.quats), _ptr(scene.log_scales),
                  _ptr(scene.trans_mag_raw), _ptr(scene.trans_phase), _ptr(scene.coeffs),
-                 _ptr(state.grad_ema if state else None), _ptr(state.last_dmean if state else None), _ptr(bad), st)
+                 _ptr(state.grad_ema if state else None), _ptr(state.last_dmean if state else None), _ptr(bad),
+                 _ptr(prior), st)
     sgd_step.last_bad = bad
     if check:
         raise_if_bad(bad, n)
@@ -151,6 +153,10 @@ def _compact(scene: raster.DeviceScene, state: TrainState, mode: int, iteration:
     for i, f in enumerate((keep, clone, split)):
         _native.call("rfs_exclusive_scan_u32", _ptr(f), n, _ptr(offs[i]), totals.data_ptr() + 4 * i, _ptr(temp), st)
     n_keep, n_clone, n_split = (int(x) for x in totals[:3].tolist())  # the one host read
+    if (mode == 0 and n_clone == 0 and n_split == 0) or (mode == 1 and n_keep == n):
+        # nothing to do: the reference returns before touching the scene or the
+        # statistics (train.py:184-186 -- no state.reset() when nothing is hot)
+        return keep, clone, split, (n_keep, n_clone, n_split)
     n_new = n_keep + n_clone + 2 * n_split
     new = {k: torch.empty((n_new,) + tuple(getattr(scene, k).shape[1:]), dtype=getattr(scene, k).dtype, device=dev)
            for k in _FIELDS}
@@ -207,22 +213,42 @@ class TraceRow:
 
 
 def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tensor, config: TrainConfig,
-               batch: int = 1, seed: int = 0, timings: list | None = None, mode: str = "spectrum"):
+               batch: int = 1, seed: int = 0, timings: list | None = None, mode: str = "spectrum",
+               check_every: int = 50, group=None):
     """Batched counterpart of train.train_loop (train.py:284-361) on the device.
 
-    Each iteration draws `batch` samples (TX position + measured power frame)
-    with a seeded generator, renders, evaluates the spectrum loss and its
-    upstream, runs the backward, the SGD step and TrainState.observe; density
-    control runs on the reference schedule during the first half of
-    training.  The scene stays in HBM throughout; the loss trace is read back
-    once at the end.  `timings` (optional list) receives (iteration,
-    milliseconds, n_gaussians, event) per iteration from CUDA events.
-    `mode` is the dataset mode (train.py:266-291): "spectrum" (frames = power
-    frames [S, n_az, n_el]), "rssi" (frames = dBm [S]) or "csi" (frames =
-    complex targets [S], one subcarrier).
+    Each iteration draws `batch` samples (TX position + measured target) with a
+    seeded generator, renders, evaluates the loss and its upstream, runs the
+    backward, the SGD step and TrainState.observe; density control runs on the
+    reference schedule during the first half of training.  The scene stays in
+    HBM throughout; the loss trace is read back once at the end.  `timings`
+    (optional list) receives (iteration, milliseconds, n_gaussians, event) per
+    iteration from CUDA events.  `mode` is the dataset mode (train.py:266-291):
+    "spectrum" (frames = power frames [S, n_az, n_el]), "rssi" (frames = dBm
+    [S]) or "csi" (frames = complex targets [S] or [S, subcarriers]; the
+    config's csi_subcarrier is used, train.py:282).
+
+    Non-finite gradients: the reference raises at the first bad step and
+    leaves the scene as it was (train.py:145-150, 324-336).  Here the steps
+    are not synchronised one by one: a bad step sets a device flag that makes
+    every later update a no-op, and the flag is read every `check_every`
+    iterations and before each densify / prune, raising
+    NonFiniteGradientError for the first bad step -- the scene the caller
+    sees is the one after the last good step.
+
+    Data parallel (`group`, or the default process group when
+    torch.distributed is initialised with more than one rank): every rank
+    draws the same samples, renders its contiguous shard of the batch and
+    all-reduces the gradients (parallel.GradBuffer, two buckets overlapped
+    with the epilogue), so every rank applies the same update and takes the
+    same densify / prune decisions (Philox children keyed by seed and
+    iteration); the loss trace is summed over the ranks once at the end.
     Returns (trace, densify_reports, prune_reports).
     """
+    import torch.distributed as dist
+
     from . import loss as _loss
+    from . import parallel
 
     config.validate()
     dev = scene.means.device
@@ -231,11 +257,28 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
     if mode == "spectrum" and tuple(frames.shape[1:]) != (scene.n_az, scene.n_el):
         raise ConfigError(f"dataset grid {tuple(frames.shape[1:])} does not match scene grid "
                           f"{(scene.n_az, scene.n_el)}")
+    if mode == "csi" and frames.dim() == 2:  # [S, subcarriers]: the configured one (train.py:282)
+        if not 0 <= config.csi_subcarrier < frames.shape[1]:
+            raise ConfigError(f"csi_subcarrier {config.csi_subcarrier} out of range")
+        frames = frames[:, config.csi_subcarrier].contiguous()
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
     rng = np.random.default_rng(seed)
     state = TrainState.zeros(scene.n, dev)
-    reports_d, reports_p, rows, bads = [], [], [], []
+    first_bad = torch.full((1,), _NO_BAD, dtype=torch.int64, device=dev)
+    first_n = torch.zeros(1, dtype=torch.int64, device=dev)  # Gaussian count of the first bad step
+    gb = None
+    reports_d, reports_p, rows = [], [], []
+
+    def check():
+        v = int(first_bad.item())
+        if v != _NO_BAD:
+            n0 = max(int(first_n.item()), 1)
+            raise NonFiniteGradientError(v % n0, _CLASSES[v // n0])
+
+    lo, hi = parallel.shard_bounds(batch, rank, world)
     for it in range(1, config.iterations + 1):
-        idx = torch.as_tensor(rng.integers(len(txs), size=batch), device=dev)
+        idx = torch.as_tensor(rng.integers(len(txs), size=batch)[lo:hi], device=dev)
         tx, gt = txs[idx].contiguous(), frames[idx].contiguous()
         e0 = torch.cuda.Event(enable_timing=True) if timings is not None else None
         if e0 is not None:
@@ -248,19 +291,32 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
                 else:
                     rep, _, lam = _loss.scalar_loss_frames(S, gt, "real_power" if mode == "rssi" else "complex")
                 return rep, lam
-            geo = raster.build_geometry(scene, psi_tx=tx, forward=True, after_forward=loss_up)
+            geo = raster.build_geometry(scene, psi_tx=tx, forward=True, index=True, after_forward=loss_up)
             rep, lam = geo.after_result
-            g = raster.backward(scene, geo, tx, lam, config.direction_chain, psi=geo.psi)
-            sgd_step(scene, g, it, config, state, check=False)
-            bads.append((sgd_step.last_bad, scene.n))
-            rows.append((it, rep.mean(0), scene.n))
+            if world > 1:
+                if gb is None or gb.n != scene.n:
+                    gb = parallel.GradBuffer(scene.n, scene.fle_degree, dev)
+                g = parallel.backward_reduced(scene, geo, tx, lam, gb, config.direction_chain, psi=geo.psi,
+                                              group=group)
+            else:
+                g = raster.backward(scene, geo, tx, lam, config.direction_chain, psi=geo.psi)
+            n_now = scene.n
+            sgd_step(scene, g, it, config, state, check=False, prior=first_bad)
+            fresh = (first_bad == _NO_BAD) & (sgd_step.last_bad != _NO_BAD)
+            first_n.copy_(torch.where(fresh, torch.full_like(first_n, n_now), first_n))
+            first_bad.copy_(torch.where(fresh, sgd_step.last_bad, first_bad))
+            rows.append((it, rep.sum(0), scene.n))
+        if check_every > 0 and it % check_every == 0:
+            check()
         if it < config.iterations / 2:
             if it % config.densify_every == 0 and scene.n > 0:
+                check()  # no density control after a bad step
                 r = densify(scene, state, it, config, seed)
                 if r.cloned or r.split:
                     reports_d.append((it, r))
                     event += "densify "
             if it % config.prune_every == 0 and scene.n > 0:
+                check()
                 r = prune(scene, state, it, config)
                 if r.removed:
                     reports_p.append((it, r))
@@ -270,9 +326,15 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
             e1.record()
             timings.append((it, e0, e1, scene.n, event.strip()))
     torch.cuda.synchronize()
-    for bad, n in bads:  # the reference raises at the first non-finite step (train.py:150)
-        raise_if_bad(bad, n)
+    check()
     if timings is not None:
         timings[:] = [(it, a.elapsed_time(b), n, ev) for it, a, b, n, ev in timings]
-    trace = [TraceRow(it, *(float(x) for x in r.tolist()), n) for it, r, n in rows]
+    if rows:
+        sums = torch.stack([r for _, r, _ in rows])
+        if world > 1:
+            dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+        means = (sums / max(batch, 1)).tolist()
+    else:
+        means = []
+    trace = [TraceRow(it, *(float(x) for x in m), n) for (it, _, n), m in zip(rows, means)]
     return trace, reports_d, reports_p

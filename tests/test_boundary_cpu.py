@@ -86,3 +86,19 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh")):
                 src = open(os.path.join(root, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/src/rfsplat"), reason="reference not present")
+def test_errors_are_the_reference_classes_when_installed():
+    """With the reference importable, callers catching rfsplat.errors.* catch
+    what this package raises (the classes are the reference's own)."""
+    import subprocess
+    import sys
+
+    code = ("import paper_2502_01826_b200.errors as e, rfsplat.errors as r;"
+            "assert e.GeometryError is r.GeometryError and e.ShapeError is r.ShapeError;"
+            "assert issubclass(e.CudaError, r.RFSplatError);"
+            "import rfsplat; assert rfsplat.GeometryError is e.GeometryError")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join(["/root/reference/pkg/src", REPO]),
+               NUMBA_CACHE_DIR="/tmp/nb")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)

@@ -91,3 +91,58 @@ def test_dp_step_two_ranks_equals_full_batch_and_oracle():
     sg = 1 / (1 + np.exp(-s.trans_mag_raw.astype(np.float64)))
     assert class_rel(out[0][1], ref["d_trans_mag"] * sg * (1 - sg)) <= 1e-3
     assert out[0][2] == 44  # reduced floats per Gaussian
+
+
+def _train_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank,) + _train_run())
+    finally:
+        dist.destroy_process_group()
+
+
+def _train_run():
+    from paper_2502_01826_b200 import raster
+    from paper_2502_01826_b200 import train as T
+    from paper_2502_01826_b200.scene import cube_init, default_txs, round_to_f32
+
+    init = round_to_f32(cube_init([-15] * 3, [15] * 3, 4.0, 72, 36, c00=30.0))
+    txs = torch.as_tensor(default_txs(8, seed=5), dtype=torch.float32, device="cuda:0")
+    geo = raster.build_geometry(raster.DeviceScene.from_host(init, "cuda:0"), psi_tx=txs, forward=True)
+    frames = (1.2 * geo.S.abs() ** 2 + 0.01).float().contiguous()
+    ds = raster.DeviceScene.from_host(init, "cuda:0")
+    cfg = T.TrainConfig(iterations=12, densify_every=5, prune_every=5, densify_grad_threshold=1e-10,
+                        lr_radiance=0.05, lr_transmittance=0.05)
+    trace, dens, _ = T.train_loop(ds, txs, frames, cfg, batch=4, seed=3)
+    return ds.means.cpu().numpy(), [r.total for r in trace], len(dens)
+
+
+def test_train_loop_data_parallel_two_ranks():
+    """train_loop over 2 ranks (each half of every batch, gradients
+    all-reduced): both ranks end with the same scene, the same densify
+    decisions and the loss trace of the single-process run."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    procs = [ctx.Process(target=_train_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in procs:
+        r, means, trace, nd = q.get(timeout=600)
+        out[r] = (means, trace, nd)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    assert out[0][2] == out[1][2] > 0
+    means1, trace1, nd1 = _train_run()
+    assert nd1 == out[0][2] and out[0][0].shape == means1.shape
+    np.testing.assert_allclose(out[0][0], means1, rtol=0, atol=1e-4)
+    np.testing.assert_allclose(out[0][1], trace1, rtol=1e-4)

@@ -86,4 +86,8 @@ def test_dataset_to_device_and_checkpoint_of_device_scene(tmp_path):
     assert isinstance(ds, raster.DeviceScene) and ds.n == 5
     back = io.checkpoint_from_device(ds)
     np.testing.assert_array_equal(back.means, scene.means.astype(np.float32).astype(np.float64))
+    # the scene metadata survives the device round trip (not replaced by defaults)
+    assert back.carrier_freq == scene.carrier_freq
+    np.testing.assert_array_equal(back.bounds_lo, scene.bounds_lo)
+    np.testing.assert_array_equal(back.bounds_hi, scene.bounds_hi)
     assert torch.cuda.is_available()

@@ -158,3 +158,81 @@ def test_gpu_train_loop_fits_and_densifies():
     trace2, _, ds2 = run()
     assert [r.total for r in trace] == [r.total for r in trace2]
     assert torch.equal(ds.means, ds2.means)
+
+
+def _small_fit_setup(n_tx=8):
+    import torch
+
+    from paper_2502_01826_b200 import raster
+    from paper_2502_01826_b200.scene import cube_init, default_txs, round_to_f32
+
+    init = round_to_f32(cube_init([-15] * 3, [15] * 3, 4.0, 72, 36, c00=30.0))
+    txs = torch.as_tensor(default_txs(n_tx, seed=5), dtype=torch.float32, device="cuda")
+    geo = raster.build_geometry(raster.DeviceScene.from_host(init, "cuda"), psi_tx=txs, forward=True)
+    frames = (1.2 * geo.S.abs() ** 2 + 0.01).float().contiguous()
+    return init, txs, frames
+
+
+@pytest.mark.gpu
+def test_gpu_train_loop_stops_at_first_nonfinite_step():
+    """A non-finite gradient from step 1 on: train_loop raises
+    NonFiniteGradientError and the scene is the one before that step
+    (reference train.py:145-150) -- no later update, densify or prune."""
+    import torch
+
+    from paper_2502_01826_b200 import raster
+    from paper_2502_01826_b200.errors import NonFiniteGradientError
+
+    init, txs, frames = _small_fit_setup()
+    ds = raster.DeviceScene.from_host(init, "cuda")
+    ds.coeffs[:, 3] = complex(float("nan"), 0.0)  # NaN coefficients: every live hit's gradients are NaN
+    before = {k: getattr(ds, k).clone() for k in ("means", "quats", "log_scales", "trans_mag_raw", "coeffs")}
+    cfg = T.TrainConfig(iterations=30, densify_every=10, prune_every=10, densify_grad_threshold=1e-12)
+    with pytest.raises(NonFiniteGradientError):
+        T.train_loop(ds, txs, frames, cfg, batch=2, seed=1, check_every=7)
+    for k, v in before.items():
+        assert torch.equal(getattr(ds, k), v) or (k == "coeffs" and torch.equal(torch.nan_to_num(getattr(ds, k)),
+                                                                                  torch.nan_to_num(v))), k
+
+
+@pytest.mark.gpu
+def test_gpu_densify_without_hot_gaussians_keeps_statistics():
+    """Nothing above the threshold: densify returns before touching the scene
+    or the EMA statistics (reference train.py:184-186, no state.reset())."""
+    import torch
+
+    from paper_2502_01826_b200 import raster
+
+    init, txs, frames = _small_fit_setup()
+    ds = raster.DeviceScene.from_host(init, "cuda")
+    state = T.TrainState(torch.rand(ds.n, device="cuda") * 1e-6, torch.rand((ds.n, 3), device="cuda"))
+    ema, last, means = state.grad_ema.clone(), state.last_dmean.clone(), ds.means.clone()
+    rep = T.densify(ds, state, 10, T.TrainConfig(densify_grad_threshold=1.0, densify_radius_threshold=1e9))
+    assert not rep.cloned and not rep.split
+    assert torch.equal(state.grad_ema, ema) and torch.equal(state.last_dmean, last) and torch.equal(ds.means, means)
+
+
+@pytest.mark.gpu
+def test_gpu_train_loop_csi_subcarrier():
+    """CSI targets [S, 26] train on config.csi_subcarrier (train.py:282)."""
+    import torch
+
+    from paper_2502_01826_b200 import raster
+
+    init, txs, _ = _small_fit_setup()
+    tg = (torch.randn((txs.shape[0], 26), device="cuda") + 1j * torch.randn((txs.shape[0], 26), device="cuda"))
+    tg = tg.to(torch.complex64)
+    out = {}
+    for sub in (0, 7):
+        ds = raster.DeviceScene.from_host(init, "cuda")
+        cfg = T.TrainConfig(iterations=3, csi_subcarrier=sub, lr_transmittance=1e-7, lr_radiance=1e-7,
+                            lr_scale=1e-7, lr_rotation=1e-7, lr_mean_start=1e-7, lr_mean_end=1e-8)
+        trace, _, _ = T.train_loop(ds, txs, tg, cfg, batch=2, seed=4, mode="csi")
+        ds1 = raster.DeviceScene.from_host(init, "cuda")
+        trace1, _, _ = T.train_loop(ds1, txs, tg[:, sub].contiguous(), cfg, batch=2, seed=4, mode="csi")
+        assert [r.total for r in trace] == [r.total for r in trace1]
+        out[sub] = trace[0].total
+    assert out[0] != out[7]
+    with pytest.raises(ConfigError):
+        T.train_loop(raster.DeviceScene.from_host(init, "cuda"), txs, tg, T.TrainConfig(iterations=1, csi_subcarrier=26),
+                     mode="csi")
