@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--deterministic", action="store_true", help="(no-op: the backward is always atomic-free and deterministic)")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--strong", action="store_true",
+                   help="strong scaling: --batch TX in total, the ray space (tiles) sharded over the ranks, "
+                        "frames and gradients all-reduced (parallel.tile_step); e.g. config 4: --gaussians 1000000")
     p.add_argument("--cpu-sample", type=int, default=32, help="TX in the bounded CPU-baseline sample (~10 s on 16 cores)")
     return p.parse_args()
 
@@ -175,7 +178,10 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    scene, txs = workload(args.gaussians, args.batch, rank, world)
+    if args.strong:  # every rank takes the whole batch; the rays are sharded
+        scene, txs = workload(args.gaussians, args.batch, 0, 1)
+    else:
+        scene, txs = workload(args.gaussians, args.batch, rank, world)
     ds = raster.DeviceScene.from_host(scene, dev)
     tx = torch.as_tensor(txs, dtype=torch.float32, device=dev)
     B = tx.shape[0]
@@ -221,9 +227,14 @@ def run_ours(args):
     # (ray-major lamT, loss.spectrum_loss_frames(lam_layout="rays")): made once here
     lamT = raster.transpose_upstream(lam)
 
+    sharder = parallel.TileSharder(world, rank)
+
     def step(marks=None):
         # psi queued behind the M read, the composite behind the hit-statistics read
-        S, g = api.fwd_bwd_device(ds, tx, None, True, args.sort, marks, lamT=lamT, grads=gb)
+        if args.strong:
+            S, g = parallel.tile_step(ds, tx, lamT, gb, sharder, True, sort_backend=args.sort, marks=marks)
+        else:
+            S, g = api.fwd_bwd_device(ds, tx, None, True, args.sort, marks, lamT=lamT, grads=gb)
         raster._mark(marks, "allreduce")
         return S, g
 
@@ -269,7 +280,7 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     ms_per_step = t_ms / args.steps
-    value = world * B * args.steps / (t_ms / 1e3)
+    value = (1 if args.strong else world) * B * args.steps / (t_ms / 1e3)
 
     # Roofline of the compositing kernels.  Algorithmic bytes per launch under the
     # hit-list design (every byte a kernel must move at least once --
@@ -318,7 +329,7 @@ def run_ours(args):
     # loss, upstream, backward (+ all-reduce), per-frame loss report D2H -- all
     # inside the timed region; the gradients stay on the device for the optimizer
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.strong:
         txh = torch.as_tensor(txs, dtype=torch.float32).pin_memory()
         gth = gt_frames.cpu().pin_memory()
         reph = torch.empty((B, 4), dtype=torch.float64).pin_memory()
@@ -355,15 +366,20 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 geometry)", "data": "synthetic",
-            "config": {"workload": "config 2: 100k Gaussians (cli._bench_scene seed 0), 360x180 grid, "
-                                   f"{B} TX per GPU, fwd+bwd step", "gaussians": ds.n, "tx_per_gpu": B,
-                       "global_tx": B * world, "grid": "360x180", "incidences_M": M, "live_hits_H": H,
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32 (fp64 geometry)",
+            "data": "synthetic",
+            "config": {"workload": (f"{'config 4 strong scaling' if args.strong else 'config 2'}: "
+                                    f"{ds.n // 1000}k Gaussians (cli._bench_scene seed 0), 360x180 grid, "
+                                    + (f"{B} TX in total" if args.strong else f"{B} TX per GPU") + ", fwd+bwd step"),
+                       "gaussians": ds.n, "tx_per_gpu": B // world if args.strong else B,
+                       "global_tx": B if args.strong else B * world, "grid": "360x180", "incidences_M": M,
+                       "live_hits_H": H,
                        "used_gaussians": n_used,
                        "upstream": "fixed synthetic lambda, given to the backward in the loss kernel's "
                                    "ray-major output layout (made once, outside the timed steps)",
                        "sort": args.sort, "hit_stats": hit_stats,
-                       "parallelism": f"dp{world} (TX-sharded, grads all-reduced)",
+                       "parallelism": (f"tile-sharded x{world} (rays split by tiles, frames + grads all-reduced)"
+                                       if args.strong else f"dp{world} (TX-sharded, grads all-reduced)"),
                        "l2": "flushed between steps (256 MB write)"},
             "roofline": rl, "kernels_roofline": roof, "phase_ms": {k: round(v, 4) for k, v in ph_ms.items()},
             "loss_ms": round(loss_ms, 4), "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clk,

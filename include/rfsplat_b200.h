@@ -114,25 +114,29 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream);
  * Writes hits of ray r to slab[r*hcap ...], counts[r] = live count.
  * stats (device int[8]): [0] rays needing rfs_hits_slow (listed in slow_list), [1] rays
  * with live > hcap (caller must retry with larger hcap), [2] max live,
- * [3] total live hits, [4] longest tile list, [5] see below.
- * used (nullable u8[n], zeroed here): 1 for every Gaussian with a live hit.
+ * [3] total live hits, [4] longest tile list, [5] see below, [8] Gaussians
+ * with a live hit (stats is int[16]).
+ * used (nullable u32[n], zeroed here): 1 for every Gaussian with a live hit.
  * The exact streaming re-sort with early termination (hits.cu); pcap
  * selects the pending ring (<= 16 -> 16 entries per ray, <= 32 -> 32, else
  * 64); stats[5] = the largest pending set, stats[6] / [7] = fp32 sphere /
- * whitened-ellipsoid passes (diagnostics). */
+ * whitened-ellipsoid passes (diagnostics).  Only the rays of tiles
+ * [tile_lo, tile_hi) are traced (tile_hi < 0: all tiles); the others get no
+ * hits -- the tile shard of a rank in the strong-scaling mode. */
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
-             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, void* stream);
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint32_t* used, int n, int tile_lo,
+             int tile_hi, void* stream);
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
-                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, uint8_t* used, void* stream);
+                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, uint32_t* used, int n, void* stream);
 
 /* K5: psi[g][b] = sum_k coeffs[g][k] * basis_k(bearing of tx_b from mu_g);
  * with used (nullable, rfs_hits' u8 marks) only rows of Gaussians with live
  * hits -- the only rows K7 / K8 read -- are computed.
  * Replaces render.py:229-238 + fle.fle_basis_with_derivs (fle.py:153-212). */
-int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const uint8_t* used,
+int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const uint32_t* used,
             void* psi, void* stream);
 
 
@@ -142,22 +146,24 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
                 void* stream);
 
 /* K8i: by-Gaussian index of the live hits (TX independent).
- * rfs_hit_keys: keys[ray_off[r]+k] = Gaussian id, slots[...] = r*hcap + k
- * (ray_off = exclusive scan of counts); sort the pairs with
+ * rfs_hit_keys: keys[ray_off[r]+k] = Gaussian id -- or, with cid (nullable:
+ * the exclusive scan of rfs_hits' used marks), its compact id among the
+ * Gaussians with a live hit, the same order in fewer key bits --
+ * slots[...] = r*hcap + k (ray_off = exclusive scan of counts); sort the pairs with
  * rfs_sort_pairs_u64 (stable: (ray, k) order within a Gaussian, the slot
  * order of the reference's bincount, grad.py:243-254);
  * rfs_gather_sorted: per sorted hit p its ray s_ray[p], w s_w[p], w T
  * s_wt[p] (complex64) and, if inv_slot is not NULL, inv_slot[slot] = p
- * (u32[R*hcap]);
+ * (u32[R*hcap]); with keys (nullable: a compact-id sort) the sorted keys are
+ * replaced by the Gaussian ids;
  * rfs_gauss_offsets: g_off (int32[N+1]) over the sorted keys.
  * Entry points taking (n_hits, h_dev) treat n_hits as the capacity and, when
  * h_dev (device u32) is given, process min(*h_dev, n_hits) hits -- the hit
  * index and the backward then need no host read of the hit count. */
-int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays, uint64_t* keys,
-                 uint32_t* slots, void* stream);
+int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays,
+                 const uint32_t* cid, uint64_t* keys, uint32_t* slots, void* stream);
 int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* h_dev, int hcap, const void* slab,
-                      uint32_t* s_ray,
-                      float* s_w, void* s_wt, uint32_t* inv_slot, void* stream);
+                      uint32_t* s_ray, float* s_w, void* s_wt, uint32_t* inv_slot, uint64_t* keys, void* stream);
 int rfs_gauss_offsets(const uint64_t* keys, int n_hits, const uint32_t* h_dev, int n, int* g_off, void* stream);
 
 
@@ -198,20 +204,22 @@ int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, cons
  * d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov (nullable); d_mean =
  * direct term + dm_dir (the bearing chain of rfs_grad_tx, nullable).
  * Scratch: acc64 f64[N*14], part_g i32[rfs_geom_part_elems(H)],
- * part_v f64[14*rfs_geom_part_elems(H)]. */
+ * part_v f64[14*rfs_geom_part_elems(H)].  stage (bit mask): 1 = the per-hit
+ * sums (K9a), 2 = the per-Gaussian chains (K9c) -- so only K9c has to wait
+ * for rfs_grad_tx's dm_dir when that runs on another stream. */
 size_t rfs_geom_part_elems(int n_hits);
 int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
                   const uint32_t* s_slot, const void* gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
-                  void* stream);
+                  int stage, void* stream);
 
 /* K9b: per-Gaussian TX-dependent terms: d_coeffs = conj(p_acc) conj(basis)
  * (grad.py:255) and the bearing chain of d_mean (grad.py:167-189) into dm_dir
  * (f32[N*3]), from P of rfs_bwd_gauss (g_off marks Gaussians without hits,
  * whose terms are zero).  accumulate = 1 adds a further TX chunk's terms.
- * Run before rfs_grad_geom, which adds dm_dir to d_mean. */
+ * Run before rfs_grad_geom's stage 2, which adds dm_dir to d_mean. */
 int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
                 const int* g_off, int include_direction_chain, int accumulate, float* dm_dir, void* d_coeffs,
                 void* stream);

@@ -21,7 +21,7 @@ namespace {
 template <int L>
 __global__ void __launch_bounds__(256) k_psi(int n, int nb, const float* __restrict__ means,
                                              const float2* __restrict__ coeffs, const float* __restrict__ tx,
-                                             const uint8_t* __restrict__ used, float2* __restrict__ psi) {
+                                             const uint32_t* __restrict__ used, float2* __restrict__ psi) {
     const int b = blockIdx.y * 64 + threadIdx.x;
     const int g = blockIdx.x * 4 + threadIdx.y;  // Gaussians on grid x (y is limited to 65535)
     if (b >= nb || g >= n) return;
@@ -137,26 +137,31 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
 }
 
 // ------------------------------------------- K8i by-Gaussian hit index
-// keys[c] = Gaussian id, vals[c] = slab slot r*hcap + k, c = ray_off[r] + k
+// keys[c] = Gaussian id (or its compact id cid[g] among the Gaussians with a
+// live hit: the same order with fewer key bits), vals[c] = slab slot
+// r*hcap + k, c = ray_off[r] + k
 __global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
-                           const uint32_t* __restrict__ ray_off, int hcap, int R, uint64_t* __restrict__ keys,
-                           uint32_t* __restrict__ slots) {
+                           const uint32_t* __restrict__ ray_off, int hcap, int R, const uint32_t* __restrict__ cid,
+                           uint64_t* __restrict__ keys, uint32_t* __restrict__ slots) {
     const int lane = threadIdx.x & 31;
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= R) return;
     const int cnt = min(counts[r], hcap);
     const uint32_t base = ray_off[r];
     for (int k = lane; k < cnt; k += 32) {
-        keys[base + k] = slab[(size_t)r * hcap + k].g;
+        const uint32_t g = slab[(size_t)r * hcap + k].g;
+        keys[base + k] = cid ? cid[g] : g;
         slots[base + k] = (uint32_t)((size_t)r * hcap + k);
     }
 }
 
-// per sorted hit p: its ray, w, w T; inverse map slot -> p (nullable)
+// per sorted hit p: its ray, w, w T; inverse map slot -> p (nullable); with
+// keys (compact-id sort), the keys are replaced by the Gaussian ids
 __global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h, const uint32_t* __restrict__ h_dev,
                                 int hcap,
                                 const RfsHit* __restrict__ slab, uint32_t* __restrict__ s_ray,
-                                float* __restrict__ s_w, float2* __restrict__ s_wt, uint32_t* __restrict__ inv_slot) {
+                                float* __restrict__ s_w, float2* __restrict__ s_wt, uint32_t* __restrict__ inv_slot,
+                                uint64_t* __restrict__ keys) {
     if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= h) return;
@@ -166,6 +171,7 @@ __global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h
     s_w[p] = hk.w;
     s_wt[p] = make_float2(hk.w * hk.t_re, hk.w * hk.t_im);
     if (inv_slot) inv_slot[s] = (uint32_t)p;
+    if (keys) keys[p] = hk.g;
 }
 
 // g_off[g] = lower_bound(g) over the sorted Gaussian keys, g in [0, n]: the
@@ -181,7 +187,7 @@ __global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, const 
 }
 
 template <int L>
-void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, const uint8_t* used,
+void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, const uint32_t* used,
                 float2* psi, cudaStream_t st) {
     dim3 grid(rfs_ceil_div(n, 4), rfs_ceil_div(nb, 64));
     k_psi<L><<<grid, dim3(64, 4), 0, st>>>(n, nb, means, coeffs, tx, used, psi);
@@ -191,7 +197,7 @@ void launch_psi(int n, int nb, const float* means, const float2* coeffs, const f
 
 extern "C" {
 
-int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const uint8_t* used,
+int rfs_psi(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const uint32_t* used,
             void* psi, void* stream) {
     if (n <= 0 || n_tx <= 0) return RFS_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -225,21 +231,21 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
     return RFS_OK;
 }
 
-int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays, uint64_t* keys,
-                 uint32_t* slots, void* stream) {
+int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays,
+                 const uint32_t* cid, uint64_t* keys, uint32_t* slots, void* stream) {
     if (n_rays <= 0) return RFS_OK;
     k_hit_keys<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-        (const RfsHit*)slab, counts, ray_off, hcap, n_rays, keys, slots);
+        (const RfsHit*)slab, counts, ray_off, hcap, n_rays, cid, keys, slots);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
 int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* h_dev, int hcap, const void* slab,
                       uint32_t* s_ray,
-                      float* s_w, void* s_wt, uint32_t* inv_slot, void* stream) {
+                      float* s_w, void* s_wt, uint32_t* inv_slot, uint64_t* keys, void* stream) {
     if (n_hits <= 0) return RFS_OK;
     k_gather_sorted<<<rfs_ceil_div(n_hits, 256), 256, 0, (cudaStream_t)stream>>>(
-        sorted_slots, n_hits, h_dev, hcap, (const RfsHit*)slab, s_ray, s_w, (float2*)s_wt, inv_slot);
+        sorted_slots, n_hits, h_dev, hcap, (const RfsHit*)slab, s_ray, s_w, (float2*)s_wt, inv_slot, keys);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

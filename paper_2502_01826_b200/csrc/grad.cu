@@ -256,9 +256,26 @@ __global__ void __launch_bounds__(128) k_geom_final(int n, const double* __restr
                                                    float* __restrict__ d_mean, float* __restrict__ d_quat,
                                                    float* __restrict__ d_log_scale, float* __restrict__ d_mag,
                                                    float* __restrict__ d_mag_raw, float* __restrict__ d_phase,
-                                                   float* __restrict__ d_cov, const float* __restrict__ dm_dir) {
+                                                   float* __restrict__ d_cov, const float* __restrict__ dm_dir,
+                                                   const int* __restrict__ g_off) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
+    if (g_off[g + 1] == g_off[g]) {  // no live hit (most Gaussians): every term is zero
+#pragma unroll
+        for (int i = 0; i < 3; ++i) d_mean[3 * g + i] = dm_dir ? dm_dir[3 * g + i] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) d_quat[4 * g + i] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) d_log_scale[3 * g + i] = 0.f;
+        d_mag[g] = 0.f;
+        d_mag_raw[g] = 0.f;
+        d_phase[g] = 0.f;
+        if (d_cov) {
+#pragma unroll
+            for (int i = 0; i < 9; ++i) d_cov[9 * g + i] = 0.f;
+        }
+        return;
+    }
     double a[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; ++i) a[i] = acc64[(size_t)g * NACC + i];
@@ -417,20 +434,22 @@ int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sort
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
-                  void* stream) {
+                  int stage, void* stream) {
     if (n <= 0) return RFS_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    RFS_CUDA_TRY(cudaMemsetAsync(acc64, 0, sizeof(double) * NACC * (size_t)n, st));
-    if (n_hits > 0) {
+    // acc64 rows of Gaussians with hits are all written by k_geom_seg / k_geom_fix;
+    // k_geom_final reads no other row (g_off), so no clearing pass
+    if ((stage & 1) && n_hits > 0) {
         k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
                                                                (const RfsGeom*)geom, dirs, g_off, rx[0], rx[1], rx[2],
                                                                ress_radius, acc64, part_g, part_v);
         k_geom_fix<<<rfs_ceil_div(rfs_ceil_div(n_hits, 32), 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, g_off, part_v,
                                                                               acc64);
     }
-    k_geom_final<<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, acc64, quats, log_scales, trans_mag_raw, d_mean, d_quat,
+    if (stage & 2)
+        k_geom_final<<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, acc64, quats, log_scales, trans_mag_raw, d_mean, d_quat,
                                                        d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov,
-                                                       dm_dir);
+                                                       dm_dir, g_off);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

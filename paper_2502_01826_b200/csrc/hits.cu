@@ -121,12 +121,13 @@ __device__ __forceinline__ bool terminated(double tre, double tim) {
 
 // Emit one hit in sorted order: terminate, record, advance T (_kernels.py:186-191).
 __device__ __forceinline__ void emit_hit(Ray& st, uint32_t g, float w, const RfsGeom* __restrict__ geom,
-                                         RfsHit* __restrict__ slab_ray, int hcap, uint8_t* __restrict__ used) {
+                                         RfsHit* __restrict__ slab_ray, int hcap, uint32_t* __restrict__ used,
+                                         int* __restrict__ stats) {
     if (terminated(st.tre, st.tim)) {
         st.done = true;
         return;
     }
-    if (used) used[g] = 1;  // Gaussian has a live hit: its psi row is needed
+    if (used) used[g] = 1u;  // Gaussian has a live hit: its psi row is needed (counted by k_count_used)
     if (st.live < hcap) {
         RfsHit h;
         h.g = g;
@@ -208,11 +209,11 @@ __global__ void __launch_bounds__(NT) k_hits(
     const float4* __restrict__ sph, const float4* __restrict__ whit, const RfsGeom* __restrict__ geom,
     const double* __restrict__ dirs, double rx0, double rx1, double rx2, double min_t, int n_az, int n_el,
     int tiles_u, int hcap, RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ slow_list,
-    int* __restrict__ stats, uint8_t* __restrict__ used) {
+    int* __restrict__ stats, uint32_t* __restrict__ used, int tile_lo) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HitsSmem<PCAP, NT, CH>& S = *reinterpret_cast<HitsSmem<PCAP, NT, CH>*>(smem_raw);
     constexpr int PARTS = 256 / NT;
-    const int tile = blockIdx.x / PARTS, part = blockIdx.x % PARTS;
+    const int tile = tile_lo + (int)blockIdx.x / PARTS, part = blockIdx.x % PARTS;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // each warp owns a 4 (u) x 8 (v) patch of the 16 x 16 tile
     const int q = part * (NT / 32) + wid, pu = q >> 1, pv = q & 1;
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(NT) k_hits(
     // emit every pending hit below `bound` (in (t_mid, g) order)
     auto emit_until = [&](double bound) {
         while (!st.done && head_t < bound) {
-            emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
+            emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used, stats);
             head = (head + 1) & (PCAP - 1);
             --npend;
             head_t = npend > 0 ? S.pt[head][tid] : DINF;
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(NT) k_hits(
     }
     // drain (also covers rays whose tile list ended with pending hits)
     while (!st.done && npend > 0) {
-        emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used);
+        emit_hit(st, S.pg[head][tid], S.pw[head][tid], geom, slab_ray, hcap, used, stats);
         head = (head + 1) & (PCAP - 1);
         --npend;
     }
@@ -399,7 +400,7 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
                             double rx2, double min_t, int n_az, int n_el, int tiles_u, int hcap,
                             RfsHit* __restrict__ slab, int* __restrict__ counts, double* __restrict__ pt,
                             uint32_t* __restrict__ pg, float* __restrict__ pw, int pcap, int* __restrict__ stats,
-                            uint8_t* __restrict__ used) {
+                            uint32_t* __restrict__ used) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_rays) return;
     const int r = rays[i];
@@ -426,7 +427,7 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
     for (int j = rg.x; j < rg.y && !st.done; ++j) {
         const double lbj = lb[j];
         while (npend > 0 && my_t[head] < lbj) {
-            emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap, used);
+            emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap, used, stats);
             ++head;
             --npend;
             if (st.done) break;
@@ -456,7 +457,7 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
         ++npend;
     }
     while (!st.done && npend > 0) {
-        emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap, used);
+        emit_hit(st, my_g[head], my_w[head], geom, slab_ray, hcap, used, stats);
         ++head;
         --npend;
     }
@@ -464,6 +465,15 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
     if (st.hcap_over) atomicAdd(&stats[1], 1);
     atomicMax(&stats[2], st.live);
     atomicAdd(&stats[3], min(st.live, hcap));
+}
+
+// stats[8] = number of Gaussians with a live hit (the by-Gaussian index sizes
+// its compact keys from it); stats[8] is zeroed by the caller
+__global__ void __launch_bounds__(256) k_count_used(const uint32_t* __restrict__ used, int n, int* __restrict__ stats) {
+    int c = 0;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) c += used[g] != 0u;
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&stats[8], c);
 }
 
 __global__ void k_max_range(const int2* __restrict__ ranges, int n_tiles, int* __restrict__ out) {
@@ -487,9 +497,9 @@ __global__ void k_ray_dirs(int n_az, int n_el, double* __restrict__ dirs) {
 }
 
 template <int PCAP, int NT, int CH>
-int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const double* lb, const void* sph,
+int launch_hits(int tile_lo, int tile_hi, const int* ranges, const uint32_t* vals, const double* lb, const void* sph,
                 const void* whit, const void* geom, const double* dirs, const double* rx, double min_t, int n_az,
-                int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used,
+                int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, uint32_t* used,
                 cudaStream_t st) {
     static bool attr = false;
     size_t smem = sizeof(HitsSmem<PCAP, NT, CH>);
@@ -502,9 +512,9 @@ int launch_hits(int n_tiles, const int* ranges, const uint32_t* vals, const doub
                                           (int)cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
-    k_hits<PCAP, NT, CH><<<n_tiles * (256 / NT), NT, smem, st>>>(
+    k_hits<PCAP, NT, CH><<<(tile_hi - tile_lo) * (256 / NT), NT, smem, st>>>(
         (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom, dirs, rx[0],
-        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used);
+        rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used, tile_lo);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -523,29 +533,35 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
 
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
-             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint8_t* used, int n, void* stream) {
+             int pcap, void* slab, int* counts, int* slow_list, int* stats, uint32_t* used, int n, int tile_lo,
+             int tile_hi, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (used && n > 0) RFS_CUDA_TRY(cudaMemsetAsync(used, 0, (size_t)n, st));
+    if (used && n > 0) RFS_CUDA_TRY(cudaMemsetAsync(used, 0, sizeof(uint32_t) * (size_t)n, st));
     const int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     const int R = n_az * n_el;
-    RFS_CUDA_TRY(cudaMemsetAsync(stats, 0, 8 * sizeof(int), st));
+    RFS_CUDA_TRY(cudaMemsetAsync(stats, 0, 16 * sizeof(int), st));
     RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)R, st));
     if (n_tiles <= 0) return RFS_OK;
-    int rc;
+    if (tile_hi < 0) tile_hi = n_tiles;  // default: every tile
+    if (tile_lo < 0 || tile_lo > tile_hi || tile_hi > n_tiles) return RFS_ERR_SHAPE;
     // 64-thread blocks: 7 per SM, so 68 of a 360x180 grid's 1104 blocks start
     // late; 128-thread blocks (all resident) measured no faster -- the kernel
     // is set by the longest warps' chains, not by the late starts
-    if (pcap <= 16)
-        rc = launch_hits<16, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
-    else if (pcap <= 32)
-        rc = launch_hits<32, 64, 32>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
-    else
-        rc = launch_hits<64, 32, 16>(n_tiles, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius, n_az, n_el,
-                                     tiles_u, hcap, slab, counts, slow_list, stats, used, st);
+    int rc = RFS_OK;
+    if (tile_hi > tile_lo) {
+        if (pcap <= 16)
+            rc = launch_hits<16, 64, 32>(tile_lo, tile_hi, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius,
+                                         n_az, n_el, tiles_u, hcap, slab, counts, slow_list, stats, used, st);
+        else if (pcap <= 32)
+            rc = launch_hits<32, 64, 32>(tile_lo, tile_hi, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius,
+                                         n_az, n_el, tiles_u, hcap, slab, counts, slow_list, stats, used, st);
+        else
+            rc = launch_hits<64, 32, 16>(tile_lo, tile_hi, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius,
+                                         n_az, n_el, tiles_u, hcap, slab, counts, slow_list, stats, used, st);
+    }
     if (rc != RFS_OK) return rc;
     k_max_range<<<rfs_ceil_div(n_tiles, 256), 256, 0, st>>>((const int2*)ranges, n_tiles, stats + 4);
+    if (used && n > 0) k_count_used<<<min(rfs_ceil_div(n, 256), 148 * 4), 256, 0, st>>>(used, n, stats);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -553,13 +569,17 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
 int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t* vals, const double* lb,
                   const void* sph, const void* whit, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, int n_az, int n_el, int hcap, void* slab, int* counts, double* pend_t,
-                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, uint8_t* used, void* stream) {
+                  uint32_t* pend_g, float* pend_w, int pcap, int* stats, uint32_t* used, int n, void* stream) {
     if (n_rays <= 0) return RFS_OK;
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     k_hits_slow<<<rfs_ceil_div(n_rays, 64), 64, 0, (cudaStream_t)stream>>>(
         rays, n_rays, (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom,
         dirs, rx[0], rx[1], rx[2], ress_radius, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, pend_t, pend_g,
         pend_w, pcap, stats, used);
+    if (used && n > 0) {  // the slow path marks more Gaussians: recount
+        RFS_CUDA_TRY(cudaMemsetAsync(stats + 8, 0, sizeof(int), (cudaStream_t)stream));
+        k_count_used<<<min(rfs_ceil_div(n, 256), 148 * 4), 256, 0, (cudaStream_t)stream>>>(used, n, stats);
+    }
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -13,6 +13,15 @@ After the all-reduce every rank holds identical gradients, so optimizer
 updates and densify / prune decisions (train.py:167-245) taken from them are
 identical on every rank without further communication.
 
+Strong scaling (`tile_step`, SURVEY.md §8(e) "Scaling risk" fallback): with
+few TX per rank the replicated TX-independent geometry -- above all the hit
+lists K6 -- dominates, so the ray space is sharded instead: each rank traces
+only the rays of a contiguous range of tiles (balanced by the tiles'
+incidence counts), composites all B TX for them, and the frames are summed
+over the ranks (disjoint supports: an all-reduce of S, which the loss needs
+whole); the backward of its own hits gives a partial gradient buffer, reduced
+as above (every gradient term is a sum over hits).
+
 The reduced payload is 44 fp32 per Gaussian: d_coeffs 32,
 d_mean 3, d_quat 4, d_log_scale 3, d_trans_mag 1, d_trans_phase 1.  The
 backward writes straight into `GradBuffer`, one persistent flat fp32 buffer
@@ -31,7 +40,7 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["shard_bounds", "shard_tx", "flatten_grads", "unflatten_grads", "allreduce_grads", "GradBuffer",
-           "dp_step", "GRAD_ORDER", "REDUCED_FLOATS"]
+           "dp_step", "GRAD_ORDER", "REDUCED_FLOATS", "tile_shards", "TileSharder", "tile_step"]
 
 # gradient buffer fields in the order they are packed by flatten_grads
 GRAD_ORDER = ("d_mean", "d_quat", "d_log_scale", "d_trans_mag", "d_trans_mag_raw", "d_trans_phase", "d_coeffs",
@@ -217,4 +226,87 @@ def dp_step(scene, txs_global, lam_global, include_direction_chain: bool = True,
     S = geo.S
     g = backward_reduced(scene, geo, tx, lam_global[a:b].contiguous(), gb, include_direction_chain, psi=geo.psi,
                          group=group)
+    return S, g
+
+
+def tile_shards(lengths, world: int) -> list:
+    """Contiguous tile ranges [(lo, hi)] for `world` ranks with balanced total
+    list length (the K6 cost is ~ the candidates its rays walk)."""
+    lengths = [max(int(x), 0) for x in lengths]
+    n = len(lengths)
+    total = sum(lengths) or 1
+    out, lo, acc = [], 0, 0
+    for r in range(world):
+        if r == world - 1:
+            out.append((lo, n))
+            break
+        target = total * (r + 1) / world
+        hi = lo
+        while hi < n and acc + lengths[hi] <= target:
+            acc += lengths[hi]
+            hi += 1
+        if hi < n and hi == lo and n - lo > world - 1 - r:  # at least one tile
+            acc += lengths[hi]
+            hi += 1
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+class TileSharder:
+    """The tile shard of each rank, balanced by the last step's tile list
+    lengths (an asynchronous 2 KB copy of the ranges, read at the next step);
+    equal tile counts until then.  Every rank computes the same (deterministic)
+    binning, hence the same shards."""
+
+    def __init__(self, world: int, rank: int):
+        self.world, self.rank = world, rank
+        self._pending = None
+        self._lengths = None
+
+    def bounds(self, n_tiles: int) -> tuple:
+        if self._pending is not None:
+            ev, host = self._pending
+            ev.synchronize()
+            self._lengths = (host[:, 1] - host[:, 0]).tolist()
+            self._pending = None
+        if self._lengths is None or len(self._lengths) != n_tiles:
+            return tile_shards([1] * n_tiles, self.world)[self.rank]
+        return tile_shards(self._lengths, self.world)[self.rank]
+
+    def update(self, geo) -> None:
+        host = torch.empty(tuple(geo.ranges.shape), dtype=geo.ranges.dtype).pin_memory()
+        host.copy_(geo.ranges, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pending = (ev, host)
+
+
+def tile_step(scene, tx, lamT, gb: GradBuffer, sharder: TileSharder, include_direction_chain: bool = True,
+              group=None, sort_backend: str = "hand", marks=None) -> tuple:
+    """One strong-scaling fwd+bwd step: every rank gets the WHOLE TX batch
+    `tx` [B, 3] and upstream lamT [R, B] (the loss kernel's layout), traces its
+    tile shard, all-reduces S (the full frames, as the loss needs them) and the
+    gradient buffer.  Returns (S [B, n_az, n_el], gradient dict)."""
+    from . import raster
+
+    world = _world(group)
+    n_tiles = ((scene.n_az + raster.TILE - 1) // raster.TILE) * ((scene.n_el + raster.TILE - 1) // raster.TILE)
+    tiles = sharder.bounds(n_tiles) if world > 1 else None
+    geo = raster.build_geometry(scene, sort_backend=sort_backend, marks=marks, psi_tx=tx, forward=True,
+                                index=True, tiles=tiles)
+    if world > 1:
+        sharder.update(geo)
+    S = geo.S
+    if world > 1:
+        s = _comm_stream(S.device)
+        s.wait_stream(torch.cuda.current_stream(S.device))
+        with torch.cuda.stream(s):  # the frames are summed while the backward runs
+            work = dist.all_reduce(torch.view_as_real(S), op=dist.ReduceOp.SUM, group=group, async_op=True)
+    g = backward_reduced(scene, geo, tx, None, gb, include_direction_chain, psi=geo.psi, lamT=lamT, group=group,
+                         marks=marks)
+    if world > 1:
+        work.wait()
+        torch.cuda.current_stream(S.device).wait_stream(s)
+        S.record_stream(s)
     return S, g

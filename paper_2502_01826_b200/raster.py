@@ -145,7 +145,7 @@ class Geometry:
     gidx: dict | None = None             # by-Gaussian hit index (built on first backward)
     psi: torch.Tensor | None = None      # psi of build_geometry(psi_tx=...)
     S: torch.Tensor | None = None        # forward of build_geometry(psi_tx=..., forward=True)
-    used: torch.Tensor | None = None     # u8 [N]: Gaussian has a live hit (psi rows needed)
+    used: torch.Tensor | None = None     # u32 [N]: Gaussian has a live hit (psi rows needed)
     after_result: object = None          # return value of build_geometry(after_forward=...)
 
     @property
@@ -162,12 +162,16 @@ class Geometry:
 
 
 # adaptive capacities, remembered across steps
-_CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {},
+_CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {}, "used_cap": {},
          # tile-key sort of the hand-written backend: "bucket" (per-tile buckets,
          # bucket.cu) or "radix" (global onesweep)
          "tile_sort": os.environ.get("RFS_TILE_SORT", "bucket"), "tile_max": {},
          # the early by-Gaussian index on the side stream (overlapping psi / K7 / loss)
-         "index_side": os.environ.get("RFS_INDEX_SIDE", "1") == "1"}
+         "index_side": os.environ.get("RFS_INDEX_SIDE", "1") == "1",
+         # psi of every Gaussian on the side stream at the start of the step
+         # (overlapping the geometry) for scenes up to this size; larger scenes
+         # compute only the rows of Gaussians with live hits, after K6
+         "psi_early_max": int(os.environ.get("RFS_PSI_EARLY_MAX", "0"))}
 _DIRS: dict = {}
 _SIDE: dict = {}
 
@@ -280,7 +284,8 @@ def _spin(ev: torch.cuda.Event) -> None:
 
 def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bool = False,
                    hcap: int | None = None, marks: list | None = None, psi_tx: torch.Tensor | None = None,
-                   index: bool = False, forward: bool = False, after_forward=None) -> Geometry:
+                   index: bool = False, forward: bool = False, after_forward=None,
+                   tiles: tuple | None = None) -> Geometry:
     """K1-K6: projection, binning, sort, ranges, emission bounds, hit lists.
 
     Two small device->host reads size the later buffers (M after the scan,
@@ -293,6 +298,9 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     `after_forward(S)` (optional) enqueues further work on S in the same
     window (e.g. the loss and the upstream transpose), result in
     geo.after_result.
+    `tiles` (optional (lo, hi)): trace only the rays of tiles [lo, hi) --
+    a rank's tile shard in the strong-scaling mode (parallel.TileSharder);
+    the other rays get no hits, so their S is exactly zero.
     `index=True` builds the by-Gaussian hit index for the backward.  `marks`
     (optional list) receives (phase, cuda.Event) pairs recorded after each
     phase on the current stream, for per-kernel timing in bench.py.
@@ -300,6 +308,24 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     scene.validate()
     lib = _native.load()
     dev = scene.means.device
+    t_lo, t_hi = (0, -1) if tiles is None else (int(tiles[0]), int(tiles[1]))
+    psi_ready = None
+    psi_early = None
+    psi_early_go = psi_tx is not None and 0 < scene.n <= _CAPS["psi_early_max"]
+
+    def start_psi_early():
+        # psi does not depend on the geometry: on the side stream, started once
+        # the dense K1-K4 kernels are queued, so it fills the SMs K6 leaves idle
+        nonlocal psi_early, psi_ready
+        side = _side_stream(dev)
+        psi_early = torch.empty((scene.n, int(psi_tx.shape[0])), dtype=torch.complex64, device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            compute_psi(scene, psi_tx, None, out=psi_early)
+            psi_ready = torch.cuda.Event()
+            psi_ready.record(side)
+        psi_early.record_stream(side)
+        psi_tx.record_stream(side)
     psi = None
     n, n_az, n_el = scene.n, scene.n_az, scene.n_el
     tiles_u = (n_az + TILE - 1) // TILE
@@ -383,17 +409,19 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     pc = _CAPS["pcap"]
     ray_counts = torch.empty(R, dtype=torch.int32, device=dev)
     slow = torch.empty(R, dtype=torch.int32, device=dev)
-    stats = torch.zeros(8, dtype=torch.int32, device=dev)
-    stats_h = _pinned(dev, "stats", 8)
+    stats = torch.zeros(16, dtype=torch.int32, device=dev)
+    stats_h = _pinned(dev, "stats", 16)
     S = None
     early = None
     redo_forward = False
-    used = torch.empty(nn, dtype=torch.uint8, device=dev)
+    used = torch.empty(nn, dtype=torch.int32, device=dev)
+    if psi_early_go:
+        start_psi_early()
     while True:
         slab = torch.empty(R * hc * 16, dtype=torch.uint8, device=dev)
         _native.call("rfs_hits", _ptr(ranges), n_tiles, _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit), _ptr(geom),
                      _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, pc, _ptr(slab), _ptr(ray_counts),
-                     _ptr(slow), _ptr(stats), _ptr(used), n, st)
+                     _ptr(slow), _ptr(stats), _ptr(used), n, t_lo, t_hi, st)
         ev_hits = torch.cuda.Event()
         ev_hits.record()
         _mark(marks, "hits")
@@ -402,24 +430,30 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             status_h.copy_(status, non_blocking=True)
         ev_s = torch.cuda.Event()
         ev_s.record()
-        if psi_tx is not None and psi is None:  # psi of the Gaussians with live hits only (K6 marks them)
-            psi = compute_psi(scene, psi_tx, used)
-            _mark(marks, "psi")
+        if psi_tx is not None and psi is None:
+            if psi_early is not None:
+                torch.cuda.current_stream(dev).wait_event(psi_ready)
+                psi = psi_early
+            else:  # psi of the Gaussians with live hits only (K6 marks them)
+                psi = compute_psi(scene, psi_tx, used)
+                _mark(marks, "psi")
         if forward and psi is not None and S is None:  # queued behind the statistics read
             S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el)
             _mark(marks, "forward")
             after = after_forward(S) if after_forward is not None else None
         h_cap = _CAPS["h_cap"].get((n_az, n_el, hc)) if index and sort_backend == "hand" else None
+        u_cap = _CAPS["used_cap"].get((n, n_az, n_el))
         early = None
-        if h_cap is not None:  # the by-Gaussian index, also behind the statistics read
+        if h_cap is not None and u_cap is not None:  # the by-Gaussian index, also behind the statistics read
             early = Geometry(n, n_az, n_el, tiles_u, tiles_v, -1, geom, rho32, dirs, ckeys, vals, ranges, hc, slab,
-                             ray_counts, [0] * 8, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
+                             ray_counts, [0] * 16, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
+            early.used = used
             if _CAPS["index_side"]:
                 # on the side stream, right behind K6: overlaps psi, the forward composite and the loss
                 side = _side_stream(dev)
                 side.wait_event(ev_hits)
                 with torch.cuda.stream(side):
-                    gauss_index(early, h_cap, _persistent)
+                    gauss_index(early, h_cap, _persistent, u_cap)
                     ready = torch.cuda.Event()
                     ready.record(side)
                 # the side stream reads these main-stream buffers: keep them alive
@@ -430,7 +464,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                 early.gidx["ready"] = ready
                 early.gidx["gen"] = _INDEX_GEN[0]
             else:
-                gauss_index(early, h_cap)
+                gauss_index(early, h_cap, used_cap=u_cap)
                 _mark(marks, "gauss_index")
         _spin(ev_s)  # read #2: hit-list statistics (and M when read #1 was skipped)
         s = stats_h.tolist()
@@ -466,9 +500,9 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             pw = torch.empty(nr * pcap, dtype=torch.float32, device=dev)
             _native.call("rfs_hits_slow", _ptr(slow), nr, _ptr(ranges), _ptr(vals), _ptr(lb), _ptr(sph), _ptr(whit),
                          _ptr(geom), _ptr(dirs), rx, float(scene.ress_radius), n_az, n_el, hc, _ptr(slab),
-                         _ptr(ray_counts), _ptr(pt), _ptr(pg), _ptr(pw), pcap, _ptr(stats), _ptr(used), st)
+                         _ptr(ray_counts), _ptr(pt), _ptr(pg), _ptr(pw), pcap, _ptr(stats), _ptr(used), n, st)
             s2 = stats.cpu().tolist()
-            s[1], s[2], s[3] = s2[1], s2[2], s2[3]
+            s[1], s[2], s[3], s[8] = s2[1], s2[2], s2[3], s2[8]
             redo_forward = True
         if s[1] > 0:
             join_early()
@@ -482,7 +516,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         _CAPS["tile_max"][(n, n_az, n_el)] = int(s[4])  # longest tile list (k_max_range)
     geo = Geometry(n, n_az, n_el, tiles_u, tiles_v, m, geom, rho32, dirs, ckeys[:max(m, 0)], vals[:max(m, 0)],
                    ranges, hc, slab, ray_counts, s, proj, sort_backend, tuple(scene.rx), float(scene.ress_radius))
-    if psi_tx is not None and redo_forward:  # the hit lists changed: new used set
+    if psi_tx is not None and redo_forward and psi_early is None:  # the hit lists changed: new used set
         psi = compute_psi(scene, psi_tx, used)
     geo.psi = psi
     geo.used = used
@@ -492,9 +526,13 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             after = after_forward(S) if after_forward is not None else None
         geo.S = S
         geo.after_result = after
+    if sort_backend == "hand":  # bound on the Gaussians with a live hit: the early index's key width
+        nu = int(s[8])
+        _CAPS["used_cap"][(n, n_az, n_el)] = min(max(n, 1), nu + nu // 4 + 256)
     if index:
         hh = int(s[3])
-        if early is not None and not redo_forward and hh <= h_cap:
+        if (early is not None and not redo_forward and hh <= h_cap
+                and int(s[8]) <= (1 << early.gidx["key_bits"])):
             geo.gidx = early.gidx
         else:
             gauss_index(geo)
@@ -511,12 +549,13 @@ def _check_tx(tx: torch.Tensor) -> torch.Tensor:
     return tx.to(dtype=torch.float32).contiguous()
 
 
-def compute_psi(scene: DeviceScene, tx: torch.Tensor, used: torch.Tensor | None = None) -> torch.Tensor:
-    """K5: psi [N, B] complex64; with `used` (u8 [N], Geometry.used) only the
+def compute_psi(scene: DeviceScene, tx: torch.Tensor, used: torch.Tensor | None = None,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """K5: psi [N, B] complex64; with `used` (u32 [N], Geometry.used) only the
     rows of Gaussians with live hits are computed -- the only rows K7 / K8c read."""
     tx = _check_tx(tx)
     b = int(tx.shape[0])
-    psi = torch.empty((scene.n, b), dtype=torch.complex64, device=scene.means.device)
+    psi = out if out is not None else torch.empty((scene.n, b), dtype=torch.complex64, device=scene.means.device)
     if scene.n and b:
         _native.call("rfs_psi", scene.n, b, scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs), _ptr(tx),
                      _ptr(used), _ptr(psi), _stream())
@@ -538,7 +577,7 @@ def forward(geo: Geometry, psi: torch.Tensor) -> torch.Tensor:
     return _forward_raw(geo.slab, geo.ray_counts, geo.hcap, psi, geo.n_az, geo.n_el)
 
 
-def gauss_index(geo: Geometry, h_cap: int | None = None, alloc=_fresh) -> None:
+def gauss_index(geo: Geometry, h_cap: int | None = None, alloc=_fresh, used_cap: int | None = None) -> None:
     """K8i: by-Gaussian index of the live hits (TX independent, cached on geo).
 
     Hits sorted by Gaussian id with a stable sort, so within a Gaussian they
@@ -547,6 +586,12 @@ def gauss_index(geo: Geometry, h_cap: int | None = None, alloc=_fresh) -> None:
     H stays on the device: `h_cap` (default: the exact H of the hit-list
     statistics) sizes the buffers and grids, every kernel reads min(H, h_cap)
     -- so build_geometry can enqueue this before it reads the statistics.
+    The sort keys are compact ids among the Gaussians with a live hit (an
+    exclusive scan of K6's used marks: the same order as the Gaussian ids,
+    with ceil(log2(used_cap)) bits -- at config 2 ~30k of 100k Gaussians are
+    hit, so 15 bits and two radix passes instead of three).  `used_cap`
+    (default: the exact count of the hit-list statistics) bounds that count;
+    build_geometry rebuilds the index if the real count exceeded it.
     """
     if geo.gidx is not None:
         return
@@ -555,31 +600,40 @@ def gauss_index(geo: Geometry, h_cap: int | None = None, alloc=_fresh) -> None:
     st = _stream()
     R = geo.n_rays
     cap = int(h_cap if h_cap is not None else geo.total_hits)
+    ucap = int(used_cap if used_cap is not None else geo.stats[8])
     ray_off = alloc("gi_ray_off", R, torch.int32, dev)
     tot = alloc("gi_tot", 1, torch.int32, dev)
-    temp = alloc("gi_rtemp", int(lib.rfs_scan_temp_elems(R)), torch.int32, dev)
+    temp = alloc("gi_rtemp", int(lib.rfs_scan_temp_elems(max(R, geo.n))), torch.int32, dev)
     _native.call("rfs_exclusive_scan_u32", _ptr(geo.ray_counts), R, _ptr(ray_off), _ptr(tot), _ptr(temp), st)
+    cid = None
+    if geo.used is not None and geo.n > 1:
+        cid = alloc("gi_cid", geo.n, torch.int32, dev)
+        n_used = alloc("gi_nused", 1, torch.int32, dev)
+        _native.call("rfs_exclusive_scan_u32", _ptr(geo.used), geo.n, _ptr(cid), _ptr(n_used), _ptr(temp), st)
+        bits = max(1, math.ceil(math.log2(max(ucap, 2))))
+    else:
+        bits = max(1, math.ceil(math.log2(max(geo.n, 2))))
     # hit keys land at ray_off[r] + k < H; positions >= cap are never read (H <= cap is checked)
     keys = alloc("gi_keys", max(R * geo.hcap, 1), torch.int64, dev)
     slots = alloc("gi_slots", max(R * geo.hcap, 1), torch.int32, dev)
-    _native.call("rfs_hit_keys", _ptr(geo.slab), _ptr(geo.ray_counts), _ptr(ray_off), geo.hcap, R, _ptr(keys),
-                 _ptr(slots), st)
-    bits = max(1, math.ceil(math.log2(max(geo.n, 2))))
+    _native.call("rfs_hit_keys", _ptr(geo.slab), _ptr(geo.ray_counts), _ptr(ray_off), geo.hcap, R, _ptr(cid),
+                 _ptr(keys), _ptr(slots), st)
     hd = tot.data_ptr()
     if cap > 1:
         if geo.sort_backend == "hand":
             keys, slots = sort_pairs(keys[:cap], slots[:cap], bits, "hand", hd, alloc)
         else:  # cub needs the exact count: only reached after the statistics read
             keys, slots = sort_pairs(keys[:cap], slots[:cap], bits, geo.sort_backend)
-    g_off = alloc("gi_goff", geo.n + 1, torch.int32, dev)
-    _native.call("rfs_gauss_offsets", _ptr(keys), cap, hd, geo.n, _ptr(g_off), st)
     s_ray = alloc("gi_s_ray", max(cap, 1), torch.int32, dev)
     s_w = alloc("gi_s_w", max(cap, 1), torch.float32, dev)
     s_wt = alloc("gi_s_wt", max(cap, 1), torch.complex64, dev)
+    # (compact-id keys are replaced by the Gaussian ids here, before the offsets)
     _native.call("rfs_gather_sorted", _ptr(slots), cap, hd, geo.hcap, _ptr(geo.slab), _ptr(s_ray), _ptr(s_w),
-                 _ptr(s_wt), None, st)
+                 _ptr(s_wt), None, _ptr(keys) if cid is not None else None, st)
+    g_off = alloc("gi_goff", geo.n + 1, torch.int32, dev)
+    _native.call("rfs_gauss_offsets", _ptr(keys), cap, hd, geo.n, _ptr(g_off), st)
     geo.gidx = {"h": cap, "h_dev": hd, "tot": tot, "sorted_g": keys, "g_off": g_off, "s_ray": s_ray, "s_w": s_w,
-                "s_wt": s_wt, "s_slot": slots}
+                "s_wt": s_wt, "s_slot": slots, "key_bits": bits if cid is not None else 64}
 
 
 def transpose_upstream(grad_S: torch.Tensor) -> torch.Tensor:
@@ -704,13 +758,16 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     acc64 = torch.empty((n, 14), dtype=torch.float64, device=dev)
     part_g = torch.empty(npart, dtype=torch.int32, device=dev)
     part_v = torch.empty((npart, 14), dtype=torch.float64, device=dev)
-    main.wait_stream(side)  # K9c adds K9b's bearing chain (dm_dir)
-    _native.call("rfs_grad_geom", n, h, gi["h_dev"], _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(gi["s_slot"]),
+    geom_args = [n, h, gi["h_dev"], _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(gi["s_slot"]),
                  _ptr(gs), _ptr(gi["g_off"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius),
                  _ptr(scene.quats), _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(acc64), _ptr(part_g),
                  _ptr(part_v), _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]),
-                 _ptr(out["d_trans_mag"]), _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]), _ptr(out["d_cov"]),
-                 _ptr(dm_dir), st)
+                 _ptr(out["d_trans_mag"]), _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]),
+                 _ptr(out["d_cov"]), _ptr(dm_dir)]
+    _native.call("rfs_grad_geom", *geom_args, 1, st)  # K9a: per-hit sums, alongside K9b
+    main.wait_stream(side)  # K9c adds K9b's bearing chain (dm_dir)
+    _native.call("rfs_grad_geom", *geom_args, 2, st)  # K9c
+    _native.launch_counter["kernels"] += 3  # k_geom_seg, k_geom_fix, k_geom_final
     _mark(marks, "grad_geom")
     return out
 

@@ -11,6 +11,6 @@ timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --sort cub >
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_hits|k_forward_v|k_bwd_gauss_v|k_bwd_pfix|k_bwd_rays|k_lam_transpose|k_grad_tx|k_geom|k_onesweep|k_psi|k_seg_sort|k_fill_stable|k_tile_count" -c 48 \
+    -k regex:"k_" -c 200 \
     -o gpurun_out/${TAG}_full python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
 echo done
