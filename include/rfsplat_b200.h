@@ -146,25 +146,29 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
                 void* stream);
 
 /* K8i: by-Gaussian index of the live hits (TX independent).
- * rfs_hit_keys: keys[ray_off[r]+k] = Gaussian id -- or, with cid (nullable:
- * the exclusive scan of rfs_hits' used marks), its compact id among the
- * Gaussians with a live hit, the same order in fewer key bits --
- * slots[...] = r*hcap + k (ray_off = exclusive scan of counts); sort the pairs with
- * rfs_sort_pairs_u64 (stable: (ray, k) order within a Gaussian, the slot
- * order of the reference's bincount, grad.py:243-254);
+ * rfs_used_list: order[cid[g]] = g for every g with used[g] (cid = the
+ * exclusive scan of rfs_hits' used marks: the compact id among the Gaussians
+ * with a live hit; entries at cid >= cap are dropped -- the caller checks
+ * the count and rebuilds).
+ * rfs_hit_keys: keys[ray_off[r]+k] = rank[g] (rank = cid, nullable: the
+ * Gaussian id), slots[...] = r*hcap + k (ray_off = exclusive scan of counts);
+ * sort the pairs with rfs_sort_pairs_u64 (stable: (ray, k) order within a
+ * Gaussian, the slot order of the reference's bincount, grad.py:243-254);
  * rfs_gather_sorted: per sorted hit p its ray s_ray[p], w s_w[p], w T
  * s_wt[p] (complex64) and, if inv_slot is not NULL, inv_slot[slot] = p
  * (u32[R*hcap]); with keys (nullable: a compact-id sort) the sorted keys are
  * replaced by the Gaussian ids;
- * rfs_gauss_offsets: g_off (int32[N+1]) over the sorted keys.
+ * rfs_gauss_ranges: g_rng (int32[2N]) = [first, end) of each Gaussian's run
+ * of sorted hits, (0, 0) for Gaussians without hits.
  * Entry points taking (n_hits, h_dev) treat n_hits as the capacity and, when
  * h_dev (device u32) is given, process min(*h_dev, n_hits) hits -- the hit
  * index and the backward then need no host read of the hit count. */
+int rfs_used_list(int n, const uint32_t* used, const uint32_t* cid, int cap, uint32_t* order, void* stream);
 int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays,
-                 const uint32_t* cid, uint64_t* keys, uint32_t* slots, void* stream);
+                 const uint32_t* rank, uint64_t* keys, uint32_t* slots, void* stream);
 int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* h_dev, int hcap, const void* slab,
                       uint32_t* s_ray, float* s_w, void* s_wt, uint32_t* inv_slot, uint64_t* keys, void* stream);
-int rfs_gauss_offsets(const uint64_t* keys, int n_hits, const uint32_t* h_dev, int n, int* g_off, void* stream);
+int rfs_gauss_ranges(const uint64_t* sorted_g, int n_hits, const uint32_t* h_dev, int n, int* g_rng, void* stream);
 
 
 /* K8: TX-batched backward over the shared hit lists, atomic-free and
@@ -189,7 +193,7 @@ int rfs_lam_transpose(const void* lam, int n_tx, int n_rays, void* lamT, void* s
 size_t rfs_bwd_part_elems(int n_hits, int n_tx);
 int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot,
                   int hcap,
-                  const void* s_wt, const int* g_off, const void* psi, const void* lamT, int accumulate, void* C,
+                  const void* s_wt, const int* g_rng, const void* psi, const void* lamT, int accumulate, void* C,
                   void* P, void* part, int* cnt, void* stream);
 int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32, const void* geom,
                  const void* C, void* gs, void* stream);
@@ -202,14 +206,15 @@ int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, cons
  * (grad.py:134-164) and d_trans_mag_raw = d|rho| sigma(1-sigma)
  * (train.py:161-162).  Writes d_mean (direct term), d_quat, d_log_scale,
  * d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov (nullable); d_mean =
- * direct term + dm_dir (the bearing chain of rfs_grad_tx, nullable).
+ * direct term + dm_dir (the bearing chain of rfs_grad_tx, nullable; read
+ * only for Gaussians with hits).
  * Scratch: acc64 f64[N*14], part_g i32[rfs_geom_part_elems(H)],
  * part_v f64[14*rfs_geom_part_elems(H)].  stage (bit mask): 1 = the per-hit
  * sums (K9a), 2 = the per-Gaussian chains (K9c) -- so only K9c has to wait
  * for rfs_grad_tx's dm_dir when that runs on another stream. */
 size_t rfs_geom_part_elems(int n_hits);
 int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
-                  const uint32_t* s_slot, const void* gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
+                  const uint32_t* s_slot, const void* gs, const int* g_rng, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
@@ -217,12 +222,16 @@ int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sort
 
 /* K9b: per-Gaussian TX-dependent terms: d_coeffs = conj(p_acc) conj(basis)
  * (grad.py:255) and the bearing chain of d_mean (grad.py:167-189) into dm_dir
- * (f32[N*3]), from P of rfs_bwd_gauss (g_off marks Gaussians without hits,
- * whose terms are zero).  accumulate = 1 adds a further TX chunk's terms.
- * Run before rfs_grad_geom's stage 2, which adds dm_dir to d_mean. */
-int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
-                const int* g_off, int include_direction_chain, int accumulate, float* dm_dir, void* d_coeffs,
-                void* stream);
+ * (f32[N*3]), from P of rfs_bwd_gauss, for the Gaussians with live hits:
+ * order[i], i < min(cap, *n_used) (rfs_used_list; n_used
+ * nullable); the d_coeffs rows of the other Gaussians (g_rng of
+ * rfs_gauss_ranges empty) are zeroed.  accumulate = 1 adds a further TX
+ * chunk's terms (and leaves the zero rows alone).  Run before rfs_grad_geom's
+ * stage 2, which adds dm_dir to d_mean. */
+int rfs_grad_tx(int cap, const uint32_t* n_used, const uint32_t* order, int n, const int* g_rng, int n_tx, int degree,
+                const float* means,
+                const void* coeffs, const float* tx, const void* P, int include_direction_chain, int accumulate,
+                float* dm_dir, void* d_coeffs, void* stream);
 
 /* Spectrum loss (loss.py:65-155) for n_frames frames [B][n_az*n_el], chained
  * into the rasterizer's upstream (upstream_to_ray, grad.py:104-120).  The

@@ -51,11 +51,12 @@ _SIGS = {
     "rfs_bwd_rays": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp]),
     "rfs_hit_keys": (i32, [vp, vp, vp, i32, i32, vp, vp, vp, vp]),
     "rfs_gather_sorted": (i32, [vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]),
-    "rfs_gauss_offsets": (i32, [vp, i32, vp, i32, vp, vp]),
+    "rfs_gauss_ranges": (i32, [vp, i32, vp, i32, vp, vp]),
+    "rfs_used_list": (i32, [i32, vp, vp, i32, vp, vp]),
     "rfs_geom_part_elems": (sz, [i32]),
     "rfs_grad_geom": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                             vp, vp, vp, vp, vp, i32, vp]),
-    "rfs_grad_tx": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
+    "rfs_grad_tx": (i32, [i32, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
     "rfs_loss_scratch_bytes": (sz, [i32, i32, i32]),
     "rfs_spectrum_loss": (i32, [i32, i32, i32, vp, vp, vp, f64, f64, vp, vp, vp, vp, vp, sz, vp]),
     "rfs_scalar_loss": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),
@@ -103,7 +104,7 @@ def load(require_cuda: bool = True):
 KERNELS_PER_CALL = {
     "rfs_project": 1, "rfs_exclusive_scan_u32": 1, "rfs_bin_fill": 1, "rfs_expand_keys": 1,
     "rfs_tile_ranges": 1, "rfs_lower_bounds": 1, "rfs_bin_bucket": 7, "rfs_hits": 3, "rfs_hits_slow": 1, "rfs_psi": 1,
-    "rfs_forward": 1, "rfs_lam_transpose": 1, "rfs_bwd_gauss": 1, "rfs_bwd_rays": 1, "rfs_hit_keys": 1, "rfs_gauss_offsets": 1, "rfs_grad_geom": 0,
+    "rfs_forward": 1, "rfs_lam_transpose": 1, "rfs_bwd_gauss": 1, "rfs_bwd_rays": 1, "rfs_hit_keys": 1, "rfs_gauss_ranges": 1, "rfs_used_list": 1, "rfs_grad_geom": 0,
     "rfs_grad_tx": 1, "rfs_gather_sorted": 1,
     "rfs_ray_dirs": 1, "rfs_spectrum_loss": 4, "rfs_sgd_step": 2, "rfs_scalar_loss": 1, "rfs_density_flags": 1,
     "rfs_density_apply": 1, "rfs_spectrum_dataset": 2, "rfs_scalar_dataset": 1,

@@ -77,7 +77,7 @@ __device__ __forceinline__ float reduce8(float (&v)[8], int lane) {
 template <int NJ>
 __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
     int h_tot, const uint32_t* __restrict__ h_dev, int nb, const uint64_t* __restrict__ sorted_g,
-    const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const int* __restrict__ g_off,
+    const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const int2* __restrict__ g_rng,
     const float2* __restrict__ psi, const float2* __restrict__ lamT, int accumulate, float2* __restrict__ C,
     float2* __restrict__ P, float2* __restrict__ part) {
     if (h_dev) h_tot = min(h_tot, (int)*h_dev);
@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
     int h = c0;
     while (h < c1) {
         const int g = (int)sh_g[wl][h - c0];
-        const int hs = g_off[g], he = g_off[g + 1];
+        const int2 rg = g_rng[g];
+        const int hs = rg.x, he = rg.y;
         const int send = min(he, c1);
         float2 ps[NJ], pa[NJ];
 #pragma unroll
@@ -170,30 +171,36 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
 
 // B a multiple of 64: lanes own TX pairs b = 2 lane + 64 j + {0, 1}, so a
 // lambda / psi / p_acc row is one 16-byte vector per lane and NP = B / 64
-// vectors per row.  Segments (runs of one Gaussian) are found from a ballot
-// mask of the staged chunk, chunk-straddling from the neighbouring keys; the
-// next segment's psi row is prefetched while the current one is reduced.
+// vectors per row.  Staging: per sorted hit one float4 (lambda-row offset of
+// its ray, slab slot, w T) in shared memory, read back with one broadcast
+// LDS.128 per hit; per hit then one wide IMAD, NP 16-byte lambda loads and
+// 16 NP FFMA (8 for C, 8 for p_acc).  Segments (runs of one Gaussian) are
+// found from a ballot mask of the staged chunk, chunk-straddling from the
+// neighbouring keys; the next segment's psi row is prefetched while the
+// current one is reduced.
 template <int NP>
 __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
     int h_tot, const uint32_t* __restrict__ h_dev, int nb, const uint64_t* __restrict__ sorted_g,
     const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const float4* __restrict__ psi,
     const float4* __restrict__ lamT, int accumulate, float2* __restrict__ C, float4* __restrict__ P,
-    float4* __restrict__ part, const int* __restrict__ g_off, int* __restrict__ cnt) {
+    float4* __restrict__ part, const int2* __restrict__ g_rng, int* __restrict__ cnt) {
     if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     __shared__ uint32_t sh_g[BG_WARPS][BG_CHUNK + 1];
-    __shared__ uint32_t sh_s[BG_WARPS][BG_CHUNK];
-    __shared__ float2 sh_wt[BG_WARPS][BG_CHUNK];
+    __shared__ float4 sh_e[BG_WARPS][BG_CHUNK];  // (lambda row offset, slot, w T re, w T im)
     __shared__ uint32_t sh_m[BG_WARPS][BG_CHUNK / 32];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int wglob = blockIdx.x * BG_WARPS + wl;
     const int c0 = wglob * BG_CHUNK;
     if (c0 >= h_tot) return;
     const int n = min(BG_CHUNK, h_tot - c0);
-    const int nq = nb >> 1;  // float4 per row
+    const uint32_t nq = (uint32_t)(nb >> 1);  // float4 per row
+    const float4* __restrict__ ll = lamT + lane;
+    asm("mov.b64 %0, %0;" : "+l"(ll));  // opaque: per-hit address = one wide IMAD on this base
     for (int i = lane; i < n; i += 32) {
         sh_g[wl][i] = (uint32_t)sorted_g[c0 + i];
-        sh_s[wl][i] = s_slot[c0 + i];
-        sh_wt[wl][i] = s_wt[c0 + i];
+        const uint32_t sl = s_slot[c0 + i];
+        const float2 wt = s_wt[c0 + i];
+        sh_e[wl][i] = make_float4(__uint_as_float((sl >> hshift) * nq), __uint_as_float(sl), wt.x, wt.y);
     }
     __syncwarp();
     const bool first_out = c0 > 0 && (uint32_t)sorted_g[c0 - 1] == sh_g[wl][0];
@@ -216,6 +223,31 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
             if (m) return min(32 * q + __ffs(m) - 1, n);
         }
         return n;
+    };
+    // per hit: conj(lam) psi summed over this lane's TX (cr, ci) and p_acc += conj(lam) w T
+    auto hit_terms = [&](const float4 (&a)[NP], const float4 (&q)[NP], float wr, float wi, float4 (&pa)[NP],
+                         float& cr, float& ci) {
+        cr = 0.f;
+        ci = 0.f;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            cr = fmaf(a[j].x, q[j].x, cr);
+            cr = fmaf(a[j].y, q[j].y, cr);
+            cr = fmaf(a[j].z, q[j].z, cr);
+            cr = fmaf(a[j].w, q[j].w, cr);
+            ci = fmaf(a[j].x, q[j].y, ci);
+            ci = fmaf(-a[j].y, q[j].x, ci);
+            ci = fmaf(a[j].z, q[j].w, ci);
+            ci = fmaf(-a[j].w, q[j].z, ci);
+            pa[j].x = fmaf(a[j].x, wr, pa[j].x);
+            pa[j].x = fmaf(a[j].y, wi, pa[j].x);
+            pa[j].y = fmaf(a[j].x, wi, pa[j].y);
+            pa[j].y = fmaf(-a[j].y, wr, pa[j].y);
+            pa[j].z = fmaf(a[j].z, wr, pa[j].z);
+            pa[j].z = fmaf(a[j].w, wi, pa[j].z);
+            pa[j].w = fmaf(a[j].z, wi, pa[j].w);
+            pa[j].w = fmaf(-a[j].w, wr, pa[j].w);
+        }
     };
     float4 ps[NP], pn[NP];
     {
@@ -242,60 +274,36 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
         // in a chunk are short, so padding them to BG_U would waste ~2x
         int i0 = s0;
         for (; i0 + BG_U <= e; i0 += BG_U) {
-            float4 l[BG_U][NP];
-            float2 wt[BG_U];
+            float4 l[BG_U][NP], eu[BG_U];
 #pragma unroll
             for (int u = 0; u < BG_U; ++u) {
-                const int i = i0 + u;
-                const uint32_t r = sh_s[wl][i] >> hshift;
-                wt[u] = sh_wt[wl][i];
+                eu[u] = sh_e[wl][i0 + u];
+                const float4* row = ll + __float_as_uint(eu[u].x);
 #pragma unroll
-                for (int j = 0; j < NP; ++j) l[u][j] = __ldg(&lamT[(size_t)r * nq + lane + 32 * j]);
+                for (int j = 0; j < NP; ++j) l[u][j] = __ldg(row + 32 * j);
             }
             float v[8];
 #pragma unroll
-            for (int u = 0; u < BG_U; ++u) {
-                float cr = 0.f, ci = 0.f;
-#pragma unroll
-                for (int j = 0; j < NP; ++j) {
-                    const float4 a = l[u][j], q = ps[j];
-                    // conj(lam) psi for the two TX of this lane
-                    cr += a.x * q.x + a.y * q.y + a.z * q.z + a.w * q.w;
-                    ci += a.x * q.y - a.y * q.x + a.z * q.w - a.w * q.z;
-                    // p_acc += conj(lam) w T
-                    pa[j].x += a.x * wt[u].x + a.y * wt[u].y;
-                    pa[j].y += a.x * wt[u].y - a.y * wt[u].x;
-                    pa[j].z += a.z * wt[u].x + a.w * wt[u].y;
-                    pa[j].w += a.z * wt[u].y - a.w * wt[u].x;
-                }
-                v[2 * u] = cr;
-                v[2 * u + 1] = ci;
-            }
+            for (int u = 0; u < BG_U; ++u) hit_terms(l[u], ps, eu[u].z, eu[u].w, pa, v[2 * u], v[2 * u + 1]);
             const float x = reduce8(v, lane);
             if ((lane & 3) == 0) {  // lanes 4i hold value i = 2u + component of hit i0 + u
                 const int i = lane >> 2, u = i >> 1;
-                float* cf = reinterpret_cast<float*>(C + sh_s[wl][i0 + u]) + (i & 1);
+                float* cf = reinterpret_cast<float*>(C + __float_as_uint(sh_e[wl][i0 + u].y)) + (i & 1);
                 *cf = accumulate ? *cf + x : x;
             }
         }
         for (; i0 < e; ++i0) {
-            const uint32_t r = sh_s[wl][i0] >> hshift;
-            const float2 w = sh_wt[wl][i0];
-            float cr = 0.f, ci = 0.f;
+            const float4 eu = sh_e[wl][i0];
+            const float4* row = ll + __float_as_uint(eu.x);
+            float4 l[NP];
 #pragma unroll
-            for (int j = 0; j < NP; ++j) {
-                const float4 a = __ldg(&lamT[(size_t)r * nq + lane + 32 * j]), q = ps[j];
-                cr += a.x * q.x + a.y * q.y + a.z * q.z + a.w * q.w;
-                ci += a.x * q.y - a.y * q.x + a.z * q.w - a.w * q.z;
-                pa[j].x += a.x * w.x + a.y * w.y;
-                pa[j].y += a.x * w.y - a.y * w.x;
-                pa[j].z += a.z * w.x + a.w * w.y;
-                pa[j].w += a.z * w.y - a.w * w.x;
-            }
+            for (int j = 0; j < NP; ++j) l[j] = __ldg(row + 32 * j);
+            float cr, ci;
+            hit_terms(l, ps, eu.z, eu.w, pa, cr, ci);
             cr = warp_sum(cr);
             ci = warp_sum(ci);
             if (lane == 0) {
-                float2* cp = C + sh_s[wl][i0];
+                float2* cp = C + __float_as_uint(eu.y);
                 *cp = accumulate ? make_float2(cp->x + cr, cp->y + ci) : make_float2(cr, ci);
             }
         }
@@ -321,7 +329,8 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
         if (k == 0 ? !first_out : !last_out) continue;
         const int gk = (int)sh_g[wl][k == 0 ? 0 : n - 1];
         if (k == 1 && first_out && gk == (int)sh_g[wl][0]) break;  // one Gaussian spans the chunk: counted once
-        const int w0 = g_off[gk] / BG_CHUNK, w1 = (g_off[gk + 1] - 1) / BG_CHUNK;
+        const int2 rg = g_rng[gk];
+        const int w0 = rg.x / BG_CHUNK, w1 = (rg.y - 1) / BG_CHUNK;
         int last = 0;
         if (lane == 0) last = atomicAdd(&cnt[gk], 1) == w1 - w0;
         last = __shfl_sync(0xffffffffu, last, 0);
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
 // Gaussian starts sums the chunk partials in chunk order (deterministic).
 __global__ void __launch_bounds__(256) k_bwd_pfix(int h_tot, const uint32_t* __restrict__ h_dev, int nb,
                                                   const uint64_t* __restrict__ sorted_g,
-                                                  const int* __restrict__ g_off, const float2* __restrict__ part,
+                                                  const int2* __restrict__ g_rng, const float2* __restrict__ part,
                                                   float2* __restrict__ P) {
     if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     const int lane = threadIdx.x & 31;
@@ -355,9 +364,9 @@ __global__ void __launch_bounds__(256) k_bwd_pfix(int h_tot, const uint32_t* __r
     if (c1 >= h_tot) return;
     const uint64_t g = sorted_g[c1 - 1];
     if (sorted_g[c1] != g) return;  // last segment ends inside the chunk
-    const int h0 = g_off[g];
-    if (h0 < c0) return;            // started in an earlier chunk, handled there
-    const int w1 = (g_off[g + 1] - 1) / BG_CHUNK;
+    const int2 rg = g_rng[g];
+    if (rg.x < c0) return;          // started in an earlier chunk, handled there
+    const int w1 = (rg.y - 1) / BG_CHUNK;
     // four chunk partials in flight per lane (fixed order: sequential in v)
     for (int b = lane; b < nb; b += 32) {
         float2 s = part[(size_t)(2 * w + 1) * nb + b];
@@ -481,7 +490,7 @@ size_t rfs_bwd_part_elems(int n_hits, int n_tx) {
 
 int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint64_t* sorted_g, const uint32_t* s_slot,
                   int hcap,
-                  const void* s_wt, const int* g_off, const void* psi, const void* lamT, int accumulate, void* C,
+                  const void* s_wt, const int* g_rng, const void* psi, const void* lamT, int accumulate, void* C,
                   void* P, void* part, int* cnt, void* stream) {
     if (n <= 0 || n_hits <= 0 || n_tx <= 0) return RFS_OK;
     if (n_tx > 32 * BG_MAXJ) return RFS_ERR_SHAPE;
@@ -496,7 +505,7 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
     k_bwd_gauss_v<NPV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,                   \
                                                        (const float2*)s_wt, (const float4*)psi,                  \
                                                        (const float4*)lamT, accumulate, (float2*)C, (float4*)P,  \
-                                                       (float4*)part, g_off, cnt)
+                                                       (float4*)part, (const int2*)g_rng, cnt)
         switch (n_tx / 64) {
             case 1: RFS_BV(1); break;
             case 2: RFS_BV(2); break;
@@ -509,14 +518,14 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
 #define RFS_BG(NJV)                                                                                              \
     k_bwd_gauss<NJV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,             \
                                                      (const float2*)s_wt,                                        \
-                                                     g_off, (const float2*)psi, (const float2*)lamT, accumulate, \
+                                                     (const int2*)g_rng, (const float2*)psi, (const float2*)lamT, accumulate, \
                                                      (float2*)C, (float2*)P, (float2*)part)
         if (nj == 1) RFS_BG(1);
         else if (nj == 2) RFS_BG(2);
         else if (nj <= 4) RFS_BG(4);
         else RFS_BG(8);
 #undef RFS_BG
-        k_bwd_pfix<<<rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, g_off,
+        k_bwd_pfix<<<rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, (const int2*)g_rng,
                                                                               (const float2*)part, (float2*)P);
     }
     RFS_LAUNCH_CHECK();

@@ -69,61 +69,104 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward(const RfsHit* __restrict
     }
 }
 
-// Even TX count: lanes own TX pairs (one 16-byte psi vector per hit), hit
-// records loaded lane-parallel and broadcast, four psi rows in flight.  A
-// block covers an FP_U x FP_V patch of rays (neighbouring rays cross mostly
-// the same Gaussians, so their psi rows are L1 hits).
-constexpr int FV_U = 4;
-constexpr int FP_U = 1, FP_V = 32, FP_RAYS = FP_U * FP_V;
+// Even TX count: lanes own TX pairs (one 16-byte psi vector per hit).  A
+// block covers a column of FP_V rays (neighbouring rays cross mostly the
+// same Gaussians, so their psi rows are L1 hits); warp w owns rays
+// v0 + w + 8 j, j < FV_RPW.  Per 32-hit chunk every lane loads one hit
+// record, forms w T and the hit's psi row offset once and parks them in a
+// per-warp shared-memory slot; the hit loop reads each record with one
+// broadcast LDS.128 and issues, per hit, one address IMAD, one 16-byte psi
+// load and 8 FFMA.  Latency is covered by software pipelining: the next
+// group of FV_U psi vectors is in flight while the current group is summed,
+// and the next chunk's (or next ray's) hit records while the current chunk
+// is composited.  psi row offsets are 32-bit float4 counts (N B / 2 < 2^32).
+#ifndef RFS_FV_U
+#define RFS_FV_U 4
+#endif
+constexpr int FV_U = RFS_FV_U;
+constexpr int FP_V = 32, FP_RAYS = FP_V;
+constexpr int FV_RPW = FP_RAYS / (CP_THREADS / 32);  // rays per warp
 __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restrict__ slab,
                                                           const int* __restrict__ counts, int hcap,
                                                           const float4* __restrict__ psi, int nb, int n_az, int n_el,
                                                           float2* __restrict__ S) {
     __shared__ float2 s_out[CP_BCH][FP_RAYS + 1];
+    __shared__ float4 s_hit[CP_THREADS / 32][32 + 2 * FV_U];  // (row offset bits, w T re, w T im, -)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pv_blocks = (n_el + FP_V - 1) / FP_V;
-    const int u0 = (blockIdx.x / pv_blocks) * FP_U, v0 = (blockIdx.x % pv_blocks) * FP_V;
+    const int u = blockIdx.x / pv_blocks, v0 = (blockIdx.x % pv_blocks) * FP_V;
     const int bc = blockIdx.y * CP_BCH;
     const int R = n_az * n_el;
-    const int nq = nb >> 1, q = (bc >> 1) + lane;  // this lane's float4 column
+    const uint32_t nq = (uint32_t)(nb >> 1);
     const bool on = 2 * lane + bc < nb;
-    for (int rl = wid; rl < FP_RAYS; rl += CP_THREADS / 32) {
-        const int u = u0 + rl / FP_V, v = v0 + rl % FP_V;
+    // this lane's float4 column; lanes past the batch re-read column 0 (never stored)
+    const float4* __restrict__ pl = psi + (on ? (bc >> 1) + lane : 0);
+    asm("mov.b64 %0, %0;" : "+l"(pl));  // opaque: per-hit address = one wide IMAD on this base
+    float4* sh = s_hit[wid];
+    if (lane < 2 * FV_U) sh[32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);  // padding: offset 0, w T = 0
+    int my_cnt = 0;  // lane j < FV_RPW: live hits of the warp's ray j
+    if (lane < FV_RPW) {
+        const int v = v0 + wid + (CP_THREADS / 32) * lane;
+        if (u < n_az && v < n_el) my_cnt = min(counts[u * n_el + v], hcap);
+    }
+    auto load_rec = [&](int j, int k, int cnt) -> float4 {  // staged form of hit k of ray j (zero past cnt)
+        float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < cnt) {
+            const RfsHit hl = slab[(size_t)(u * n_el + v0 + wid + (CP_THREADS / 32) * j) * hcap + k];
+            e = make_float4(__uint_as_float(hl.g * nq), hl.w * hl.t_re, hl.w * hl.t_im, 0.f);
+        }
+        return e;
+    };
+    float4 rec = load_rec(0, lane, __shfl_sync(0xffffffffu, my_cnt, 0));
+#pragma unroll 1
+    for (int j = 0; j < FV_RPW; ++j) {
+        const int cnt = __shfl_sync(0xffffffffu, my_cnt, j);
+        const int cnt_n = __shfl_sync(0xffffffffu, my_cnt, (j + 1) % FV_RPW);
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (u < n_az && v < n_el) {
-            const int r = u * n_el + v;
-            const int cnt = min(counts[r], hcap);
-            const RfsHit* h = slab + (size_t)r * hcap;
-            for (int kc = 0; kc < cnt; kc += 32) {
-                RfsHit hl;
-                if (kc + lane < cnt) {
-                    hl = h[kc + lane];
-                } else {
-                    hl.g = 0; hl.w = 0.f; hl.t_re = 0.f; hl.t_im = 0.f;
-                }
-                const float2 wtl = make_float2(hl.w * hl.t_re, hl.w * hl.t_im);
-                const int n_in = min(32, cnt - kc);
-                for (int i0 = 0; i0 < n_in; i0 += FV_U) {
-                    float4 pv[FV_U];
-                    float2 wt[FV_U];
+        if (cnt == 0 && j + 1 < FV_RPW) rec = load_rec(j + 1, lane, cnt_n);
+        for (int kc = 0; kc < cnt; kc += 32) {
+            __syncwarp();
+            sh[lane] = rec;
+            __syncwarp();
+            if (kc + 32 < cnt) rec = load_rec(j, kc + 32 + lane, cnt);
+            else if (j + 1 < FV_RPW) rec = load_rec(j + 1, lane, cnt_n);
+            const int n_in = min(32, cnt - kc);
+            // ping-pong register buffers (A: even groups, B: odd groups); entries
+            // past n_in read offset 0 with w T = 0
+            float4 ea[FV_U], pa[FV_U], eb[FV_U], pb[FV_U];
+            auto fetch = [&](float4(&e)[FV_U], float4(&p)[FV_U], int i0) {
 #pragma unroll
-                    for (int u = 0; u < FV_U; ++u) {
-                        const int i = i0 + u;  // lanes >= n_in carry w = 0, g = 0
-                        const uint32_t g = __shfl_sync(0xffffffffu, hl.g, i & 31);
-                        wt[u].x = __shfl_sync(0xffffffffu, wtl.x, i & 31);
-                        wt[u].y = __shfl_sync(0xffffffffu, wtl.y, i & 31);
-                        pv[u] = on ? __ldg(&psi[(size_t)g * nq + q]) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-#pragma unroll
-                    for (int u = 0; u < FV_U; ++u) {
-                        acc.x += wt[u].x * pv[u].x - wt[u].y * pv[u].y;
-                        acc.y += wt[u].x * pv[u].y + wt[u].y * pv[u].x;
-                        acc.z += wt[u].x * pv[u].z - wt[u].y * pv[u].w;
-                        acc.w += wt[u].x * pv[u].w + wt[u].y * pv[u].z;
-                    }
+                for (int k = 0; k < FV_U; ++k) {
+                    e[k] = sh[i0 + k];
+                    p[k] = __ldg(pl + __float_as_uint(e[k].x));
                 }
+            };
+            auto madd = [&](const float4(&e)[FV_U], const float4(&p)[FV_U]) {
+#pragma unroll
+                for (int k = 0; k < FV_U; ++k) {
+                    acc.x = fmaf(e[k].y, p[k].x, acc.x);
+                    acc.x = fmaf(-e[k].z, p[k].y, acc.x);
+                    acc.y = fmaf(e[k].y, p[k].y, acc.y);
+                    acc.y = fmaf(e[k].z, p[k].x, acc.y);
+                    acc.z = fmaf(e[k].y, p[k].z, acc.z);
+                    acc.z = fmaf(-e[k].z, p[k].w, acc.z);
+                    acc.w = fmaf(e[k].y, p[k].w, acc.w);
+                    acc.w = fmaf(e[k].z, p[k].z, acc.w);
+                }
+            };
+            fetch(ea, pa, 0);
+            for (int i0 = 0;;) {
+                fetch(eb, pb, i0 + FV_U);
+                madd(ea, pa);
+                i0 += FV_U;
+                if (i0 >= n_in) break;
+                fetch(ea, pa, i0 + FV_U);
+                madd(eb, pb);
+                i0 += FV_U;
+                if (i0 >= n_in) break;
             }
         }
+        const int rl = wid + (CP_THREADS / 32) * j;
         s_out[2 * lane][rl] = make_float2(acc.x, acc.y);
         s_out[2 * lane + 1][rl] = make_float2(acc.z, acc.w);
     }
@@ -131,17 +174,34 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
     const int nbc = min(CP_BCH, nb - bc);
     for (int i = threadIdx.x; i < nbc * FP_RAYS; i += CP_THREADS) {
         const int bl = i / FP_RAYS, rl = i % FP_RAYS;
-        const int u = u0 + rl / FP_V, v = v0 + rl % FP_V;
+        const int v = v0 + rl;
         if (u < n_az && v < n_el) S[(size_t)(bc + bl) * R + u * n_el + v] = s_out[bl][rl];
     }
 }
 
 // ------------------------------------------- K8i by-Gaussian hit index
-// keys[c] = Gaussian id (or its compact id cid[g] among the Gaussians with a
-// live hit: the same order with fewer key bits), vals[c] = slab slot
-// r*hcap + k, c = ray_off[r] + k
+// The hits are ordered by the compact id of their Gaussian among the
+// Gaussians with a live hit (cid, an exclusive scan of K6's used marks: the
+// Gaussian-id order in fewer key bits) and, stably, by (ray, k) within it --
+// the reference's bincount slot order, so every per-Gaussian sum keeps its
+// order.  (A spatial rank -- Gaussians sorted by the Morton code of their
+// projected centre -- was measured: the lambda-row gathers of K8c went from
+// 0.5 % to 4 % L1 hits, -4 us, while ranking cost +50 us.)
+
+// order[cid[g]] = g for the Gaussians with a live hit (entries at cid >= cap
+// are dropped: the caller checks the count and rebuilds)
+__global__ void k_used_list(int n, const uint32_t* __restrict__ used, const uint32_t* __restrict__ cid, int cap,
+                            uint32_t* __restrict__ order) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n || !used[g]) return;
+    const uint32_t c = cid[g];
+    if (c < (uint32_t)cap) order[c] = (uint32_t)g;
+}
+
+// keys[c] = rank[g] = cid[g] (or the Gaussian id when rank is NULL), vals[c] = slab
+// slot r*hcap + k, c = ray_off[r] + k
 __global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
-                           const uint32_t* __restrict__ ray_off, int hcap, int R, const uint32_t* __restrict__ cid,
+                           const uint32_t* __restrict__ ray_off, int hcap, int R, const uint32_t* __restrict__ rank,
                            uint64_t* __restrict__ keys, uint32_t* __restrict__ slots) {
     const int lane = threadIdx.x & 31;
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -150,7 +210,7 @@ __global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restric
     const uint32_t base = ray_off[r];
     for (int k = lane; k < cnt; k += 32) {
         const uint32_t g = slab[(size_t)r * hcap + k].g;
-        keys[base + k] = cid ? cid[g] : g;
+        keys[base + k] = rank ? rank[g] : g;
         slots[base + k] = (uint32_t)((size_t)r * hcap + k);
     }
 }
@@ -174,16 +234,16 @@ __global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h
     if (keys) keys[p] = hk.g;
 }
 
-// g_off[g] = lower_bound(g) over the sorted Gaussian keys, g in [0, n]: the
-// thread of sorted position p writes every g in (keys[p-1], keys[p]]
-__global__ void k_gauss_offsets(const uint64_t* __restrict__ keys, int h, const uint32_t* __restrict__ h_dev, int n,
-                                int* __restrict__ g_off) {
+// g_rng[g] = [first, end) of g's run of sorted hits ((0, 0) for a Gaussian
+// without hits: the array is cleared first); sorted_g = Gaussian id per hit
+__global__ void k_gauss_ranges(const uint64_t* __restrict__ sorted_g, int h, const uint32_t* __restrict__ h_dev,
+                               int2* __restrict__ g_rng) {
     if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p > h) return;
-    const long long prev = p > 0 ? (long long)keys[p - 1] : -1;
-    const long long cur = p < h ? min((long long)keys[p], (long long)n) : (long long)n;
-    for (long long g = prev + 1; g <= cur; ++g) g_off[g] = p;
+    if (p >= h) return;
+    const uint64_t g = sorted_g[p];
+    if (p == 0 || sorted_g[p - 1] != g) g_rng[g].x = p;
+    if (p == h - 1 || sorted_g[p + 1] != g) g_rng[g].y = p + 1;
 }
 
 template <int L>
@@ -221,7 +281,7 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
     if (n_rays <= 0 || n_tx <= 0) return RFS_OK;
     dim3 grid(rfs_ceil_div(n_rays, CP_RAYS), rfs_ceil_div(n_tx, CP_BCH));
     if (n_tx % 2 == 0) {
-        dim3 gv(rfs_ceil_div(n_az, FP_U) * rfs_ceil_div(n_el, FP_V), rfs_ceil_div(n_tx, CP_BCH));
+        dim3 gv(n_az * rfs_ceil_div(n_el, FP_V), rfs_ceil_div(n_tx, CP_BCH));
         k_forward_v<<<gv, CP_THREADS, 0, (cudaStream_t)stream>>>((const RfsHit*)slab, counts, hcap,
                                                                  (const float4*)psi, n_tx, n_az, n_el, (float2*)S);
     } else
@@ -231,11 +291,18 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
     return RFS_OK;
 }
 
+int rfs_used_list(int n, const uint32_t* used, const uint32_t* cid, int cap, uint32_t* order, void* stream) {
+    if (n <= 0) return RFS_OK;
+    k_used_list<<<rfs_ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(n, used, cid, cap, order);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
 int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays,
-                 const uint32_t* cid, uint64_t* keys, uint32_t* slots, void* stream) {
+                 const uint32_t* rank, uint64_t* keys, uint32_t* slots, void* stream) {
     if (n_rays <= 0) return RFS_OK;
     k_hit_keys<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-        (const RfsHit*)slab, counts, ray_off, hcap, n_rays, cid, keys, slots);
+        (const RfsHit*)slab, counts, ray_off, hcap, n_rays, rank, keys, slots);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -250,8 +317,12 @@ int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* 
     return RFS_OK;
 }
 
-int rfs_gauss_offsets(const uint64_t* keys, int n_hits, const uint32_t* h_dev, int n, int* g_off, void* stream) {
-    k_gauss_offsets<<<rfs_ceil_div(n_hits + 1, 256), 256, 0, (cudaStream_t)stream>>>(keys, n_hits, h_dev, n, g_off);
+int rfs_gauss_ranges(const uint64_t* sorted_g, int n_hits, const uint32_t* h_dev, int n, int* g_rng, void* stream) {
+    if (n <= 0) return RFS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    RFS_CUDA_TRY(cudaMemsetAsync(g_rng, 0, sizeof(int2) * (size_t)n, st));
+    if (n_hits > 0)
+        k_gauss_ranges<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(sorted_g, n_hits, h_dev, (int2*)g_rng);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

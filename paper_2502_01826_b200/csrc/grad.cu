@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) k_geom_seg(
     int h, const uint32_t* __restrict__ h_dev, const uint64_t* __restrict__ sorted_g, const uint32_t* __restrict__ s_ray,
     const float* __restrict__ s_w,
     const uint32_t* __restrict__ s_slot, const float4* __restrict__ gs, const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
-    const int* __restrict__ g_off, double rx0, double rx1, double rx2, double min_t, double* __restrict__ acc64,
+    const int2* __restrict__ g_rng, double rx0, double rx1, double rx2, double min_t, double* __restrict__ acc64,
     int* __restrict__ part_g, double* __restrict__ part_v) {
     if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(256) k_geom_seg(
         double sum = 0.0;
         for (int q = h_start; q < h_end; ++q) sum += sv[wl][q][i];
         const int gk = sg[wl][h_start];
-        const int h0 = g_off[gk], h1 = g_off[gk + 1];
+        const int2 rg = g_rng[gk];
+        const int h0 = rg.x, h1 = rg.y;
         if (h0 >= wb && h1 - 1 <= wb + 31) {  // whole segment inside this warp
             acc64[(size_t)gk * NACC + i] = sum;
             continue;
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(256) k_geom_seg(
 constexpr int FIX_SHORT = 4;
 __global__ void __launch_bounds__(256) k_geom_fix(int h, const uint32_t* __restrict__ h_dev,
                                                   const uint64_t* __restrict__ sorted_g,
-                                                  const int* __restrict__ g_off, const double* __restrict__ part_v,
+                                                  const int2* __restrict__ g_rng, const double* __restrict__ part_v,
                                                   double* __restrict__ acc64) {
     if (h_dev) h = min(h, (int)*h_dev);
     const int lane = threadIdx.x & 31;
@@ -168,8 +169,9 @@ __global__ void __launch_bounds__(256) k_geom_fix(int h, const uint32_t* __restr
         if (c1 < h) {
             g = (int)sorted_g[c1 - 1];
             // the last segment continues past this group and starts in it
-            mine = (int)sorted_g[c1] == g && g_off[g] >= c0;
-            if (mine) w1 = (g_off[g + 1] - 1) >> 5;
+            const int2 rg = g_rng[g];
+            mine = (int)sorted_g[c1] == g && rg.x >= c0;
+            if (mine) w1 = (rg.y - 1) >> 5;
         }
     }
     if (mine && w1 - w + 1 <= FIX_SHORT) {
@@ -257,12 +259,13 @@ __global__ void __launch_bounds__(128) k_geom_final(int n, const double* __restr
                                                    float* __restrict__ d_log_scale, float* __restrict__ d_mag,
                                                    float* __restrict__ d_mag_raw, float* __restrict__ d_phase,
                                                    float* __restrict__ d_cov, const float* __restrict__ dm_dir,
-                                                   const int* __restrict__ g_off) {
+                                                   const int2* __restrict__ g_rng) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
-    if (g_off[g + 1] == g_off[g]) {  // no live hit (most Gaussians): every term is zero
+    const int2 rg = g_rng[g];
+    if (rg.y == rg.x) {  // no live hit (most Gaussians): every term is zero (K9b skips them too)
 #pragma unroll
-        for (int i = 0; i < 3; ++i) d_mean[3 * g + i] = dm_dir ? dm_dir[3 * g + i] : 0.f;
+        for (int i = 0; i < 3; ++i) d_mean[3 * g + i] = 0.f;
 #pragma unroll
         for (int i = 0; i < 4; ++i) d_quat[4 * g + i] = 0.f;
 #pragma unroll
@@ -312,28 +315,40 @@ __device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
 
 // ------------------------------------------------------------------ K9b
 // NJ = TX blocks of 32 per lane (compile time: no dead predicated iterations).
-// Persistent warps walk Gaussians g, g + nwarps, ...; the next Gaussian's hit
-// range and p_acc row are requested while the current one is evaluated.
+// Persistent warps walk the Gaussians with live hits in the index's spatial
+// order (order[i], i < *n_used); the next Gaussian's p_acc row is requested
+// while the current one is evaluated.  Then (unless accumulating) the
+// d_coeffs rows of the Gaussians without hits (g_rng empty) are zeroed, so
+// d_coeffs is complete when this kernel ends (an all-reduce bucket may
+// start right behind it).
 template <int L, int NJ>
 __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
-    int n, int nb, const float* __restrict__ means, const float2* __restrict__ coeffs, const float* __restrict__ tx,
-    const float2* __restrict__ P, const int* __restrict__ g_off, int include_dir, int accumulate,
-    float* __restrict__ dm_dir, float2* __restrict__ d_coeffs) {
+    int cap, const uint32_t* __restrict__ n_used, const uint32_t* __restrict__ order, int n,
+    const int2* __restrict__ g_rng, int nb, const float* __restrict__ means, const float2* __restrict__ coeffs, const float* __restrict__ tx,
+    const float2* __restrict__ P, int include_dir, int accumulate, float* __restrict__ dm_dir,
+    float2* __restrict__ d_coeffs) {
     constexpr int K = Fle<L>::K;
     constexpr int NV = 2 * K;
     constexpr int NG = (NV + 31) / 32;
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * GB_THREADS) >> 5;
-    int g = (blockIdx.x * GB_THREADS + threadIdx.x) >> 5;
-    if (g >= n) return;
+    const int m = n_used ? min(cap, (int)*n_used) : cap;
+    if (!accumulate) {
+        for (int t = blockIdx.x * GB_THREADS + threadIdx.x; t < n; t += gridDim.x * GB_THREADS) {
+            const int2 rg = g_rng[t];
+            if (rg.y == rg.x)
+                for (int k = 0; k < K; ++k) d_coeffs[(size_t)t * K + k] = make_float2(0.f, 0.f);
+        }
+    }
+    int i = (blockIdx.x * GB_THREADS + threadIdx.x) >> 5;
+    if (i >= m) return;
     const int nj = (nb + 31) >> 5;
-    int h0 = g_off[g], h1 = g_off[g + 1];
+    int g = (int)order[i];
     for (;;) {
-        const int gn = g + nw;
-        int nh0 = 0, nh1 = 0;
-        if (gn < n) {
-            nh0 = g_off[gn];
-            nh1 = g_off[gn + 1];
+        const int in = i + nw;
+        int gn = 0;
+        if (in < m) {
+            gn = (int)order[in];
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
                 const int b = lane + 32 * j;
@@ -341,19 +356,14 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
             }
         }
         float* dcf = reinterpret_cast<float*>(d_coeffs + (size_t)g * K);
-        if (h1 <= h0) {  // Gaussian not hit (its p_acc row is not written by K8c): zero terms
-            if (!accumulate) {
-                for (int i = lane; i < NV; i += 32) dcf[i] = 0.f;
-                if (lane < 3) dm_dir[3 * g + lane] = 0.f;
-            }
-        } else {
+        if (g_rng[g].y > g_rng[g].x) {  // (always: a used Gaussian has hits)
         float vals[NG * 32];
-    #pragma unroll
-        for (int i = 0; i < NG * 32; ++i) vals[i] = 0.f;
+#pragma unroll
+        for (int q = 0; q < NG * 32; ++q) vals[q] = 0.f;
         float dm0 = 0.f, dm1 = 0.f, dm2 = 0.f;
         const float mxf = means[3 * g], myf = means[3 * g + 1], mzf = means[3 * g + 2];
         const float2* co = coeffs + (size_t)g * K;
-    #pragma unroll 1
+#pragma unroll 1
         for (int j = 0; j < NJ; ++j) {
             const int b = lane + 32 * j;
             if (j >= nj) break;
@@ -363,14 +373,14 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
             typename Fle<L>::Tables T;
             Fle<L>::tables(rx, ry, rz, T);
             float2 dpa = make_float2(0.f, 0.f), dpb = make_float2(0.f, 0.f);
-            Fle<L>::for_each(T, [&](int idx, int m, float2 bv, float2 dbv) {
+            Fle<L>::for_each(T, [&](int idx, int mm, float2 bv, float2 dbv) {
                 vals[2 * idx] += p.x * bv.x - p.y * bv.y;          // Re conj(P) conj(basis)
                 vals[2 * idx + 1] += -(p.x * bv.y + p.y * bv.x);   // Im
                 if (include_dir) {
                     const float2 cc = __ldg(&co[idx]);
                     const float2 cb = cmulf(cc, bv);
-                    dpa.x += -(float)m * cb.y;  // d psi / d alpha = sum c (i m) basis
-                    dpa.y += (float)m * cb.x;
+                    dpa.x += -(float)mm * cb.y;  // d psi / d alpha = sum c (i m) basis
+                    dpa.y += (float)mm * cb.x;
                     dpb = caddf(dpb, cmulf(cc, dbv));
                 }
             });
@@ -387,38 +397,38 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
                 }
             }
         }
-            float mine[NG];
+        float mine[NG];
 #pragma unroll
-            for (int q = 0; q < NG; ++q) mine[q] = transpose_reduce32(vals + 32 * q, lane);
-            dm0 = warp_sum(dm0);
-            dm1 = warp_sum(dm1);
-            dm2 = warp_sum(dm2);
+        for (int q = 0; q < NG; ++q) mine[q] = transpose_reduce32(vals + 32 * q, lane);
+        dm0 = warp_sum(dm0);
+        dm1 = warp_sum(dm1);
+        dm2 = warp_sum(dm2);
 #pragma unroll
-            for (int q = 0; q < NG; ++q) {
-                const int i = 32 * q + lane;
-                if (i < NV) dcf[i] = accumulate ? dcf[i] + mine[q] : mine[q];
-            }
-            if (lane == 0) {  // bearing chain of d_mean (grad.py:167-189); K9c adds the direct term
-                dm_dir[3 * g + 0] = accumulate ? dm_dir[3 * g + 0] + dm0 : dm0;
-                dm_dir[3 * g + 1] = accumulate ? dm_dir[3 * g + 1] + dm1 : dm1;
-                dm_dir[3 * g + 2] = accumulate ? dm_dir[3 * g + 2] + dm2 : dm2;
-            }
+        for (int q = 0; q < NG; ++q) {
+            const int t = 32 * q + lane;
+            if (t < NV) dcf[t] = accumulate ? dcf[t] + mine[q] : mine[q];
         }
-        if (gn >= n) break;
+        if (lane == 0) {  // bearing chain of d_mean (grad.py:167-189); K9c adds the direct term
+            dm_dir[3 * g + 0] = accumulate ? dm_dir[3 * g + 0] + dm0 : dm0;
+            dm_dir[3 * g + 1] = accumulate ? dm_dir[3 * g + 1] + dm1 : dm1;
+            dm_dir[3 * g + 2] = accumulate ? dm_dir[3 * g + 2] + dm2 : dm2;
+        }
+        }
+        if (in >= m) break;
+        i = in;
         g = gn;
-        h0 = nh0;
-        h1 = nh1;
     }
 }
 
 template <int L>
-void launch_tx(unsigned grid, cudaStream_t st, int n, int nb, const float* means, const float2* coeffs,
-               const float* tx, const float2* P, const int* g_off, int include_dir, int accumulate, float* dm_dir,
-               float2* d_coeffs) {
+void launch_tx(unsigned grid, cudaStream_t st, int cap, const uint32_t* n_used, const uint32_t* order, int n,
+               const int2* g_rng, int nb,
+               const float* means, const float2* coeffs, const float* tx, const float2* P, int include_dir,
+               int accumulate, float* dm_dir, float2* d_coeffs) {
     const int nj = (nb + 31) / 32;
 #define RFS_GT(NJV)                                                                                                \
-    k_grad_tx<L, NJV><<<grid, GB_THREADS, 0, st>>>(n, nb, means, coeffs, tx, P, g_off, include_dir, accumulate,   \
-                                                   dm_dir, d_coeffs)
+    k_grad_tx<L, NJV><<<grid, GB_THREADS, 0, st>>>(cap, n_used, order, n, g_rng, nb, means, coeffs, tx, P, include_dir,     \
+                                                   accumulate, dm_dir, d_coeffs)
     if (nj <= 2) RFS_GT(2); else RFS_GT(8);
 #undef RFS_GT
 }
@@ -430,41 +440,43 @@ extern "C" {
 size_t rfs_geom_part_elems(int n_hits) { return (size_t)2 * (size_t)((n_hits + 31) / 32 + 1); }
 
 int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
-                  const uint32_t* s_slot, const void* gs, const int* g_off, const void* geom, const double* dirs, const double* rx,
+                  const uint32_t* s_slot, const void* gs, const int* g_rng, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
                   int stage, void* stream) {
     if (n <= 0) return RFS_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    const int2* rg = (const int2*)g_rng;
     // acc64 rows of Gaussians with hits are all written by k_geom_seg / k_geom_fix;
-    // k_geom_final reads no other row (g_off), so no clearing pass
+    // k_geom_final reads no other row (g_rng), so no clearing pass
     if ((stage & 1) && n_hits > 0) {
         k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
-                                                               (const RfsGeom*)geom, dirs, g_off, rx[0], rx[1], rx[2],
+                                                               (const RfsGeom*)geom, dirs, rg, rx[0], rx[1], rx[2],
                                                                ress_radius, acc64, part_g, part_v);
-        k_geom_fix<<<rfs_ceil_div(rfs_ceil_div(n_hits, 32), 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, g_off, part_v,
+        k_geom_fix<<<rfs_ceil_div(rfs_ceil_div(n_hits, 32), 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, rg, part_v,
                                                                               acc64);
     }
     if (stage & 2)
         k_geom_final<<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, acc64, quats, log_scales, trans_mag_raw, d_mean, d_quat,
                                                        d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov,
-                                                       dm_dir, g_off);
+                                                       dm_dir, rg);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
-int rfs_grad_tx(int n, int n_tx, int degree, const float* means, const void* coeffs, const float* tx, const void* P,
-                const int* g_off, int include_direction_chain, int accumulate, float* dm_dir, void* d_coeffs,
-                void* stream) {
+int rfs_grad_tx(int cap, const uint32_t* n_used, const uint32_t* order, int n, const int* g_rng, int n_tx, int degree,
+                const float* means,
+                const void* coeffs, const float* tx, const void* P, int include_direction_chain, int accumulate,
+                float* dm_dir, void* d_coeffs, void* stream) {
     if (n <= 0) return RFS_OK;
     if (n_tx > 32 * GB_MAXJ) return RFS_ERR_SHAPE;
-    if (P == nullptr || g_off == nullptr) return RFS_ERR_CONTRACT;
+    if (P == nullptr || order == nullptr || g_rng == nullptr) return RFS_ERR_CONTRACT;
     cudaStream_t st = (cudaStream_t)stream;
     // persistent: 4 blocks of 4 warps per SM (128 registers per thread)
-    unsigned grid = (unsigned)std::min<long long>(rfs_ceil_div((long long)n * 32, GB_THREADS), 148LL * 4);
+    unsigned grid = (unsigned)std::min<long long>(rfs_ceil_div((long long)std::max(cap, 1) * 32, GB_THREADS), 148LL * 4);
 #define RFS_TX(LL)                                                                                                   \
-    launch_tx<LL>(grid, st, n, n_tx, means, (const float2*)coeffs, tx, (const float2*)P, g_off,                     \
+    launch_tx<LL>(grid, st, cap, n_used, order, n, (const int2*)g_rng, n_tx, means, (const float2*)coeffs, tx, (const float2*)P,           \
                   include_direction_chain, accumulate, dm_dir, (float2*)d_coeffs)
     switch (degree) {
         case 0: RFS_TX(0); break;

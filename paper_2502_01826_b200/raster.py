@@ -228,7 +228,8 @@ def _persistent(name: str, n: int, dtype, dev) -> torch.Tensor:
     return t[:n]
 
 
-def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand", m_dev_ptr: int | None = None, alloc=_fresh):
+def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand", m_dev_ptr: int | None = None, alloc=_fresh,
+               tag: str = ""):
     """K3: stable sort of u64 keys with u32 payload; returns sorted (keys, vals).
 
     With `m_dev_ptr` (device address of a u32 count; hand-written sort only)
@@ -240,13 +241,13 @@ def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand", m_dev_ptr: int 
     if m <= 1:
         return ckeys, vals
     end_bit = int(end_bit)
-    kalt = alloc("sort_kalt", m, ckeys.dtype, dev)
-    valt = alloc("sort_valt", m, vals.dtype, dev)
+    kalt = alloc(tag + "sort_kalt", m, ckeys.dtype, dev)
+    valt = alloc(tag + "sort_valt", m, vals.dtype, dev)
     lib = _native.load()
     res = _native.C.c_int(0)
     if backend == "hand":
         tb = int(lib.rfs_sort_temp_bytes(m, end_bit))
-        temp = alloc("sort_temp", max(tb, 16), torch.uint8, dev)
+        temp = alloc(tag + "sort_temp", max(tb, 16), torch.uint8, dev)
         _native.call("rfs_sort_pairs_u64", _ptr(ckeys), _ptr(vals), _ptr(kalt), _ptr(valt), m, end_bit,
                      _ptr(temp), tb, _native.C.byref(res), m_dev_ptr, _stream())
         _native.launch_counter["kernels"] += 2 + (end_bit + 7) // 8
@@ -532,7 +533,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     if index:
         hh = int(s[3])
         if (early is not None and not redo_forward and hh <= h_cap
-                and int(s[8]) <= (1 << early.gidx["key_bits"])):
+                and int(s[8]) <= early.gidx["u_cap"]):
             geo.gidx = early.gidx
         else:
             gauss_index(geo)
@@ -580,18 +581,19 @@ def forward(geo: Geometry, psi: torch.Tensor) -> torch.Tensor:
 def gauss_index(geo: Geometry, h_cap: int | None = None, alloc=_fresh, used_cap: int | None = None) -> None:
     """K8i: by-Gaussian index of the live hits (TX independent, cached on geo).
 
-    Hits sorted by Gaussian id with a stable sort, so within a Gaussian they
-    keep the (ray, k) order of the reference's bincount slots
-    (grad.py:222-254); per sorted hit: ray, slab slot, w, w T.  The hit count
-    H stays on the device: `h_cap` (default: the exact H of the hit-list
-    statistics) sizes the buffers and grids, every kernel reads min(H, h_cap)
-    -- so build_geometry can enqueue this before it reads the statistics.
-    The sort keys are compact ids among the Gaussians with a live hit (an
-    exclusive scan of K6's used marks: the same order as the Gaussian ids,
-    with ceil(log2(used_cap)) bits -- at config 2 ~30k of 100k Gaussians are
-    hit, so 15 bits and two radix passes instead of three).  `used_cap`
-    (default: the exact count of the hit-list statistics) bounds that count;
-    build_geometry rebuilds the index if the real count exceeded it.
+    Hits sorted by the compact id of their Gaussian among the Gaussians with
+    a live hit (K6's used marks) with a stable sort, so within a Gaussian
+    they keep the (ray, k) order of the reference's bincount slots
+    (grad.py:222-254) -- every per-Gaussian sum has the reference's order.
+    Per sorted hit: ray, slab slot, w, w T; per Gaussian its run [first,
+    end); the list of the Gaussians with hits (K9b walks only those).
+    The hit count H stays on the device: `h_cap` (default: the exact H of the
+    hit-list statistics) sizes the buffers and grids, every kernel reads
+    min(H, h_cap) -- so build_geometry can enqueue this before it reads the
+    statistics.  The compact id has ceil(log2(used_cap)) bits (at config 2 ~30k of
+    100k Gaussians are hit: 15 bits, two radix passes); `used_cap` (default:
+    the exact count of the hit-list statistics) bounds the number of used
+    Gaussians; build_geometry rebuilds the index if the real count exceeded it.
     """
     if geo.gidx is not None:
         return
@@ -600,23 +602,24 @@ def gauss_index(geo: Geometry, h_cap: int | None = None, alloc=_fresh, used_cap:
     st = _stream()
     R = geo.n_rays
     cap = int(h_cap if h_cap is not None else geo.total_hits)
-    ucap = int(used_cap if used_cap is not None else geo.stats[8])
+    ucap = max(int(used_cap if used_cap is not None else geo.stats[8]), 1)
     ray_off = alloc("gi_ray_off", R, torch.int32, dev)
     tot = alloc("gi_tot", 1, torch.int32, dev)
     temp = alloc("gi_rtemp", int(lib.rfs_scan_temp_elems(max(R, geo.n))), torch.int32, dev)
     _native.call("rfs_exclusive_scan_u32", _ptr(geo.ray_counts), R, _ptr(ray_off), _ptr(tot), _ptr(temp), st)
-    cid = None
-    if geo.used is not None and geo.n > 1:
-        cid = alloc("gi_cid", geo.n, torch.int32, dev)
-        n_used = alloc("gi_nused", 1, torch.int32, dev)
-        _native.call("rfs_exclusive_scan_u32", _ptr(geo.used), geo.n, _ptr(cid), _ptr(n_used), _ptr(temp), st)
-        bits = max(1, math.ceil(math.log2(max(ucap, 2))))
-    else:
-        bits = max(1, math.ceil(math.log2(max(geo.n, 2))))
+    # compact ids of the Gaussians with a live hit, and their list (K9b walks it)
+    cid = alloc("gi_cid", max(geo.n, 1), torch.int32, dev)
+    n_used = alloc("gi_nused", 1, torch.int32, dev)
+    _native.call("rfs_exclusive_scan_u32", _ptr(geo.used), geo.n, _ptr(cid), _ptr(n_used), _ptr(temp), st)
+    order = alloc("gi_order", ucap, torch.int32, dev)
+    _native.call("rfs_used_list", geo.n, _ptr(geo.used), _ptr(cid), ucap, _ptr(order), st)
+    nu = n_used.data_ptr()
+    rank = cid
+    bits = max(1, math.ceil(math.log2(max(ucap, 2))))
     # hit keys land at ray_off[r] + k < H; positions >= cap are never read (H <= cap is checked)
     keys = alloc("gi_keys", max(R * geo.hcap, 1), torch.int64, dev)
     slots = alloc("gi_slots", max(R * geo.hcap, 1), torch.int32, dev)
-    _native.call("rfs_hit_keys", _ptr(geo.slab), _ptr(geo.ray_counts), _ptr(ray_off), geo.hcap, R, _ptr(cid),
+    _native.call("rfs_hit_keys", _ptr(geo.slab), _ptr(geo.ray_counts), _ptr(ray_off), geo.hcap, R, _ptr(rank),
                  _ptr(keys), _ptr(slots), st)
     hd = tot.data_ptr()
     if cap > 1:
@@ -627,13 +630,14 @@ def gauss_index(geo: Geometry, h_cap: int | None = None, alloc=_fresh, used_cap:
     s_ray = alloc("gi_s_ray", max(cap, 1), torch.int32, dev)
     s_w = alloc("gi_s_w", max(cap, 1), torch.float32, dev)
     s_wt = alloc("gi_s_wt", max(cap, 1), torch.complex64, dev)
-    # (compact-id keys are replaced by the Gaussian ids here, before the offsets)
+    # (the rank keys are replaced by the Gaussian ids here, before the ranges)
     _native.call("rfs_gather_sorted", _ptr(slots), cap, hd, geo.hcap, _ptr(geo.slab), _ptr(s_ray), _ptr(s_w),
-                 _ptr(s_wt), None, _ptr(keys) if cid is not None else None, st)
-    g_off = alloc("gi_goff", geo.n + 1, torch.int32, dev)
-    _native.call("rfs_gauss_offsets", _ptr(keys), cap, hd, geo.n, _ptr(g_off), st)
-    geo.gidx = {"h": cap, "h_dev": hd, "tot": tot, "sorted_g": keys, "g_off": g_off, "s_ray": s_ray, "s_w": s_w,
-                "s_wt": s_wt, "s_slot": slots, "key_bits": bits if cid is not None else 64}
+                 _ptr(s_wt), None, _ptr(keys), st)
+    g_rng = alloc("gi_grng", 2 * max(geo.n, 1), torch.int32, dev)
+    _native.call("rfs_gauss_ranges", _ptr(keys), cap, hd, geo.n, _ptr(g_rng), st)
+    geo.gidx = {"h": cap, "h_dev": hd, "tot": tot, "sorted_g": keys, "g_rng": g_rng, "s_ray": s_ray, "s_w": s_w,
+                "s_wt": s_wt, "s_slot": slots, "key_bits": bits, "order": order, "u_cap": ucap,
+                "n_used": n_used, "n_used_dev": nu}  # (the tensors behind the device pointers stay referenced)
 
 
 def transpose_upstream(grad_S: torch.Tensor) -> torch.Tensor:
@@ -733,15 +737,17 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
         part = torch.empty(int(lib.rfs_bwd_part_elems(h, nbc)), dtype=torch.complex64, device=dev)
         pcnt = torch.empty(max(n, 1), dtype=torch.int32, device=dev)  # straddle counts (zeroed in C)
         _native.call("rfs_bwd_gauss", n, h, gi["h_dev"], nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_slot"]), geo.hcap,
-                     _ptr(gi["s_wt"]), _ptr(gi["g_off"]), _ptr(psic), _ptr(lamTc), int(c0 > 0), _ptr(C), _ptr(P),
+                     _ptr(gi["s_wt"]), _ptr(gi["g_rng"]), _ptr(psic), _ptr(lamTc), int(c0 > 0), _ptr(C), _ptr(P),
                      _ptr(part), _ptr(pcnt), st)
         _mark(marks, "bwd_gauss")
         # K9b on a second stream: it needs only P, so it overlaps the ray
         # recursion and the geometry sums below (K9c waits for it)
         side.wait_stream(main)
         with torch.cuda.stream(side):
-            _native.call("rfs_grad_tx", n, nbc, scene.fle_degree, _ptr(scene.means), _ptr(scene.coeffs),
-                         _ptr(txc), _ptr(P), _ptr(gi["g_off"]), int(bool(include_direction_chain)), int(c0 > 0),
+            _native.call("rfs_grad_tx", gi["u_cap"], gi["n_used_dev"], _ptr(gi["order"]), n, _ptr(gi["g_rng"]), nbc,
+                         scene.fle_degree,
+                         _ptr(scene.means), _ptr(scene.coeffs), _ptr(txc), _ptr(P), int(bool(include_direction_chain)),
+                         int(c0 > 0),
                          _ptr(dm_dir), _ptr(out["d_coeffs"]), side.cuda_stream)
         for t in (txc, P, dm_dir, out["d_coeffs"]):
             t.record_stream(side)
@@ -759,7 +765,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     part_g = torch.empty(npart, dtype=torch.int32, device=dev)
     part_v = torch.empty((npart, 14), dtype=torch.float64, device=dev)
     geom_args = [n, h, gi["h_dev"], _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(gi["s_slot"]),
-                 _ptr(gs), _ptr(gi["g_off"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius),
+                 _ptr(gs), _ptr(gi["g_rng"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius),
                  _ptr(scene.quats), _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), _ptr(acc64), _ptr(part_g),
                  _ptr(part_v), _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]),
                  _ptr(out["d_trans_mag"]), _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]),

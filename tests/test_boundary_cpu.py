@@ -32,7 +32,7 @@ def test_header_declares_the_kernel_abi():
     names = _declared()
     for n in ("rfs_project", "rfs_exclusive_scan_u32", "rfs_bin_fill", "rfs_sort_pairs_u64", "rfs_sort_pairs_u64_cub",
               "rfs_tile_ranges", "rfs_lower_bounds", "rfs_bin_bucket_temp_bytes", "rfs_bin_bucket", "rfs_hits", "rfs_psi", "rfs_forward", "rfs_lam_transpose", "rfs_bwd_gauss", "rfs_bwd_rays",
-              "rfs_hit_keys", "rfs_gather_sorted", "rfs_gauss_offsets", "rfs_grad_geom", "rfs_grad_tx"):
+              "rfs_hit_keys", "rfs_gather_sorted", "rfs_gauss_ranges", "rfs_used_list", "rfs_grad_geom", "rfs_grad_tx"):
         assert n in names
 
 
