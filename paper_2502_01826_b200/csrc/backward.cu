@@ -21,9 +21,8 @@
 //                        time.  Gaussians straddling chunks leave per-chunk
 //                        partial rows that
 //   K8f k_bwd_pfix       adds in chunk order.
-//   K8r k_bwd_rays       one warp per ray, lanes over its hits: the suffix
-//                        recursion as a warp scan of complex affine maps in
-//                        fp64, then GW_k = Re(T_k C_k) (_kernels.py:387-388),
+//   K8r k_bwd_rays       one thread per ray, hits back to front: the suffix
+//                        recursion in fp64, then GW_k = Re(T_k C_k) (_kernels.py:387-388),
 //                        d|rho|_k = Re(T_k e^{j phi} A_k), d(phase)_k =
 //                        -Im(T_k rho A_k) (_kernels.py:382-385), stored at
 //                        the hit's sorted position for K9a.
@@ -381,94 +380,42 @@ __global__ void __launch_bounds__(256) k_bwd_pfix(int h_tot, const uint32_t* __r
     }
 }
 
-// ------------------------------------------------------------ K8r ray scan
-struct Aff {  // x -> a x + c, complex fp64
-    double ar, ai, cr, ci;
-};
-
-__device__ __forceinline__ Aff compose(const Aff& f, const Aff& h) {  // f(h(x))
-    Aff o;
-    o.ar = f.ar * h.ar - f.ai * h.ai;
-    o.ai = f.ar * h.ai + f.ai * h.ar;
-    o.cr = f.ar * h.cr - f.ai * h.ci + f.cr;
-    o.ci = f.ar * h.ci + f.ai * h.cr + f.ci;
-    return o;
-}
-
+// ------------------------------------------------------------ K8r ray recursion
+// Thread per ray, hits walked back to front in fp64 (the reference's suffix
+// recursion, _kernels.py:522): A_{cnt-1} = 0, A_{k-1} = w_k C_k + rho_k A_k.
+// The loads of a hit do not depend on A, so they run ahead of the short
+// complex FMA chain; the 32 rays of a warp are neighbours (consecutive v),
+// so their rho gathers share L1 lines.
 // Precision: rho in fp64 from the geometry record (the reference's value),
 // and d(phase) -- a sum of strongly cancelling terms for Gaussians crossed by
 // many rays -- is stored as a float pair (hi, lo) for the fp64 sums of K9a.
-__global__ void __launch_bounds__(256) k_bwd_rays(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
+__global__ void __launch_bounds__(128) k_bwd_rays(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
                                                   int hcap, int R, const float4* __restrict__ rho32,
                                                   const RfsGeom* __restrict__ geom, const float2* __restrict__ C,
                                                   float4* __restrict__ gs) {
-    const int lane = threadIdx.x & 31;
-    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= R) return;
     const int cnt = min(counts[r], hcap);
-    if (cnt == 0) return;
-    // carried from the chunk above: A_{kc+32} and f_{kc+32} = (rho, w C) of hit kc+32
-    double Anr = 0.0, Ani = 0.0, Ur = 1.0, Ui = 0.0, Wr = 0.0, Wi = 0.0;
-    for (int kc = ((cnt - 1) >> 5) << 5; kc >= 0; kc -= 32) {
-        const int k = kc + lane;
-        const bool ok = k < cnt;
-        RfsHit hk;
-        const size_t pos = (size_t)r * hcap + k;
-        float2 ck = make_float2(0.f, 0.f);
-        if (ok) {
-            hk = slab[pos];
-            ck = C[pos];
-        } else {
-            hk.g = 0;
-            hk.w = 0.f;
-            hk.t_re = hk.t_im = 0.f;
-        }
-        const float4 rq = ok ? __ldg(&rho32[hk.g]) : make_float4(1.f, 0.f, 1.f, 0.f);
-        const double rr = ok ? __ldg(&geom[hk.g].rho_re) : 1.0, ri = ok ? __ldg(&geom[hk.g].rho_im) : 0.0;
+    const size_t base = (size_t)r * hcap;
+    double Ar = 0.0, Ai = 0.0;
+#pragma unroll 4
+    for (int k = cnt - 1; k >= 0; --k) {
+        const RfsHit hk = slab[base + k];
+        const float2 ck = C[base + k];
+        const float4 rq = __ldg(&rho32[hk.g]);
+        const double rr = __ldg(&geom[hk.g].rho_re), ri = __ldg(&geom[hk.g].rho_im);
         const double tr = hk.t_re, ti = hk.t_im;
-        // f_k(A) = w_k C_k + rho_k A; lane k holds F_k = f_{k+1} (identity past the end)
-        const double wc_r = (double)hk.w * (double)ck.x, wc_i = (double)hk.w * (double)ck.y;
-        Aff F;
-        {
-            const double nr = __shfl_down_sync(0xffffffffu, rr, 1);
-            const double ni = __shfl_down_sync(0xffffffffu, ri, 1);
-            const double ncr = __shfl_down_sync(0xffffffffu, wc_r, 1);
-            const double nci = __shfl_down_sync(0xffffffffu, wc_i, 1);
-            if (k + 1 >= cnt) {
-                F.ar = 1.0; F.ai = 0.0; F.cr = 0.0; F.ci = 0.0;
-            } else if (lane < 31) {
-                F.ar = nr; F.ai = ni; F.cr = ncr; F.ci = nci;
-            } else {
-                F.ar = Ur; F.ai = Ui; F.cr = Wr; F.ci = Wi;
-            }
-        }
-        // inclusive suffix scan: G_k = F_k o F_{k+1} o ... o F_{kc+31}
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            Aff H;
-            H.ar = __shfl_down_sync(0xffffffffu, F.ar, o);
-            H.ai = __shfl_down_sync(0xffffffffu, F.ai, o);
-            H.cr = __shfl_down_sync(0xffffffffu, F.cr, o);
-            H.ci = __shfl_down_sync(0xffffffffu, F.ci, o);
-            if (lane + o < 32) F = compose(F, H);
-        }
-        // A_k = G_k(A_{kc+32}) (A_cnt = 0 at the top)
-        const double Ar = F.ar * Anr - F.ai * Ani + F.cr;
-        const double Ai = F.ar * Ani + F.ai * Anr + F.ci;
-        if (ok) {
-            const double gw = tr * (double)ck.x - ti * (double)ck.y;     // Re(T C)          (_kernels.py:387-388)
-            const double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
-            const double dmag = tar * rq.z - tai * rq.w;                  // Re(T e^{jphi} A) (_kernels.py:382-383)
-            const double dph = -(tar * ri + tai * rr);                    // -Im(T rho A)     (_kernels.py:384-385)
-            const float dph_hi = (float)dph;
-            gs[pos] = make_float4((float)gw, (float)dmag, dph_hi, (float)(dph - (double)dph_hi));
-        }
-        Anr = __shfl_sync(0xffffffffu, Ar, 0);
-        Ani = __shfl_sync(0xffffffffu, Ai, 0);
-        Ur = __shfl_sync(0xffffffffu, rr, 0);
-        Ui = __shfl_sync(0xffffffffu, ri, 0);
-        Wr = __shfl_sync(0xffffffffu, wc_r, 0);
-        Wi = __shfl_sync(0xffffffffu, wc_i, 0);
+        const double gw = tr * (double)ck.x - ti * (double)ck.y;  // Re(T C)          (_kernels.py:387-388)
+        const double tar = tr * Ar - ti * Ai, tai = tr * Ai + ti * Ar;
+        const double dmag = tar * rq.z - tai * rq.w;             // Re(T e^{jphi} A) (_kernels.py:382-383)
+        const double dph = -(tar * ri + tai * rr);               // -Im(T rho A)     (_kernels.py:384-385)
+        const float dph_hi = (float)dph;
+        gs[base + k] = make_float4((float)gw, (float)dmag, dph_hi, (float)(dph - (double)dph_hi));
+        const double wcr = (double)hk.w * (double)ck.x, wci = (double)hk.w * (double)ck.y;
+        const double nr = wcr + (rr * Ar - ri * Ai);
+        const double ni = wci + (rr * Ai + ri * Ar);
+        Ar = nr;
+        Ai = ni;
     }
 }
 
@@ -535,7 +482,7 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
 int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32, const void* geom,
                  const void* C, void* gs, void* stream) {
     if (n_rays <= 0) return RFS_OK;
-    k_bwd_rays<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+    k_bwd_rays<<<rfs_ceil_div(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
         (const RfsHit*)slab, counts, hcap, n_rays, (const float4*)rho32, (const RfsGeom*)geom, (const float2*)C,
         (float4*)gs);
     RFS_LAUNCH_CHECK();
