@@ -40,6 +40,13 @@ __device__ __forceinline__ double power(const float2* __restrict__ S, const floa
     const float2 s = S[i];
     return (double)s.x * s.x + (double)s.y * s.y;
 }
+// the same rounded to fp32, for the window statistics (computed in fp32): the
+// correctly rounded fp32 of the fp64 power, so pred == gt gives SSIM = 1 exactly
+__device__ __forceinline__ float power_f(const float2* __restrict__ S, const float* __restrict__ pred, int i) {
+    if (pred) return __ldg(&pred[i]);
+    const float2 s = __ldg(&S[i]);
+    return (float)((double)s.x * s.x + (double)s.y * s.y);
+}
 
 // per-(frame, chunk) min / max of the ground truth (loss.py:108); the tile
 // kernels reduce a frame's RCH partials themselves
@@ -90,6 +97,7 @@ struct FwdSmem {
     float x[HU][HVP], y[HU][HVP];  // raw frames (0 in the padding)
     float h[5][HU][TVP];           // v-blurred x, y, xx, yy, xy of the centred frames
     double red[LT / 32];
+    float2 rng;                    // the frame's (min, max) of y
 };
 
 // The five window statistics in fp32 on frames centred by a per-tile constant
@@ -109,60 +117,71 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_fwd(const float2* __restrict__ S
     FwdSmem& M = *reinterpret_cast<FwdSmem*>(smem_raw);
     const int b = blockIdx.z, u0 = blockIdx.y * TU, v0 = blockIdx.x * TV;
     const size_t R = (size_t)n_az * n_el, fb = (size_t)b * R;
-    float lo = INFINITY, hi = -INFINITY;
-    for (int k = 0; k < RCH; ++k) {
-        const float2 rg = range[b * RCH + k];
-        lo = fminf(lo, rg.x);
-        hi = fmaxf(hi, rg.y);
-    }
-    const double D = fmax((double)hi - (double)lo, 1e-6);
-    const double c1 = (0.01 * D) * (0.01 * D), c2 = (0.03 * D) * (0.03 * D);
-    {   // halo load: row-major, every load of the thread in flight before the stores
-        constexpr int RS = LT / 64, NR = (HU + RS - 1) / RS;
-        const int hv = threadIdx.x & 63, v = v0 - LH + hv;
-        const bool vok = hv < HV && v >= 0 && v < n_el;
-        float xv[NR], yv[NR];
+    if (threadIdx.x < 32) {  // the frame's range: warp 0 folds the RCH = 32 chunk partials
+        static_assert(RCH == 32, "one partial per lane");
+        const float2 rg = range[b * RCH + threadIdx.x];
+        float lo = rg.x, hi = rg.y;
 #pragma unroll
-        for (int k = 0; k < NR; ++k) {
-            const int hu = (threadIdx.x >> 6) + k * RS, u = u0 - LH + hu;
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (threadIdx.x == 0) M.rng = make_float2(lo, hi);
+    }
+    {   // halo load: the HU x HV cells in row-major order over all threads, every
+        // load of the thread in flight before the stores; 32-bit frame offsets
+        constexpr int NH = (HU * HV + LT - 1) / LT;
+        const float2* Sb = S ? S + fb : nullptr;
+        const float* pb = pred ? pred + fb : nullptr;
+        const float* yb = gt + fb;
+        float xv[NH], yv[NH];
+#pragma unroll
+        for (int k = 0; k < NH; ++k) {
+            const int i = threadIdx.x + k * LT, hu = i / HV, hv = i - hu * HV;
+            const int u = u0 - LH + hu, v = v0 - LH + hv;
             xv[k] = yv[k] = 0.f;
-            if (vok && hu < HU && u >= 0 && u < n_az) {
-                const size_t r = fb + (size_t)u * n_el + v;
-                xv[k] = (float)power(S, pred, r);
-                yv[k] = gt[r];
+            if (hu < HU && u >= 0 && u < n_az && v >= 0 && v < n_el) {
+                const int off = u * n_el + v;
+                xv[k] = power_f(Sb, pb, off);
+                yv[k] = __ldg(&yb[off]);
             }
         }
 #pragma unroll
-        for (int k = 0; k < NR; ++k) {
-            const int hu = (threadIdx.x >> 6) + k * RS;
-            if (hv < HV && hu < HU) {
+        for (int k = 0; k < NH; ++k) {
+            const int i = threadIdx.x + k * LT, hu = i / HV, hv = i - hu * HV;
+            if (hu < HU) {
                 M.x[hu][hv] = xv[k];
                 M.y[hu][hv] = yv[k];
             }
         }
     }
     __syncthreads();
+    const double D = fmax((double)M.rng.y - (double)M.rng.x, 1e-6);
+    const double c1 = (0.01 * D) * (0.01 * D), c2 = (0.03 * D) * (0.03 * D);
     const float cx = M.x[LH][LH], cy = M.y[LH][LH];  // centre: the tile's first cell
     // correlate along v (axis 1): item = (segment, row), rows fastest -> conflict-free
     for (int it = threadIdx.x; it < (TV / SEG) * HU; it += LT) {
         const int sg = it / HU, hu = it - sg * HU, o0 = sg * SEG;
-        float wx[SEG + LW - 1], wy[SEG + LW - 1];
+        float wx[SEG + LW - 1], wy[SEG + LW - 1], wxx[SEG + LW - 1], wyy[SEG + LW - 1], wxy[SEG + LW - 1];
 #pragma unroll
-        for (int j = 0; j < SEG + LW - 1; ++j) {
+        for (int j = 0; j < SEG + LW - 1; ++j) {  // the products once per input, not once per tap
             wx[j] = M.x[hu][o0 + j] - cx;
             wy[j] = M.y[hu][o0 + j] - cy;
+            wxx[j] = wx[j] * wx[j];
+            wyy[j] = wy[j] * wy[j];
+            wxy[j] = wx[j] * wy[j];
         }
 #pragma unroll
         for (int o = 0; o < SEG; ++o) {
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
 #pragma unroll
             for (int t = 0; t < LW; ++t) {
-                const float w = c_winf[t], xv = wx[o + t], yv = wy[o + t];
-                a0 = fmaf(w, xv, a0);
-                a1 = fmaf(w, yv, a1);
-                a2 = fmaf(w, xv * xv, a2);
-                a3 = fmaf(w, yv * yv, a3);
-                a4 = fmaf(w, xv * yv, a4);
+                const float w = c_winf[t];
+                a0 = fmaf(w, wx[o + t], a0);
+                a1 = fmaf(w, wy[o + t], a1);
+                a2 = fmaf(w, wxx[o + t], a2);
+                a3 = fmaf(w, wyy[o + t], a3);
+                a4 = fmaf(w, wxy[o + t], a4);
             }
             M.h[0][hu][o0 + o] = a0; M.h[1][hu][o0 + o] = a1; M.h[2][hu][o0 + o] = a2;
             M.h[3][hu][o0 + o] = a3; M.h[4][hu][o0 + o] = a4;
@@ -249,25 +268,30 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S
     BwdSmem& M = *reinterpret_cast<BwdSmem*>(smem_raw);
     const int b = blockIdx.z, u0 = blockIdx.y * TU, v0 = blockIdx.x * TV;
     const size_t R = (size_t)n_az * n_el, fb = (size_t)b * R, plane = R * gridDim.z;
-    {   // halo load: row-major, every load of the thread in flight before the stores
-        constexpr int RS = LT / 64, NR = (HU + RS - 1) / RS;
-        const int hv = threadIdx.x & 63, v = v0 - LH + hv;
-        const bool vok = hv < HV && v >= 0 && v < n_el;
-        float mv[3][NR];
+    {   // halo load: the HU x HV cells in row-major order over all threads, every
+        // load of the thread in flight before the stores; 32-bit frame offsets
+        constexpr int NH = (HU * HV + LT - 1) / LT;
+        const float* m0 = maps + fb;
+        const float* m1 = m0 + plane;
+        const float* m2 = m1 + plane;
+        float mv[3][NH];
 #pragma unroll
-        for (int k = 0; k < NR; ++k) {
-            const int hu = (threadIdx.x >> 6) + k * RS, u = u0 - LH + hu;
-            const bool in = vok && hu < HU && u >= 0 && u < n_az;
-            const size_t r = fb + (size_t)u * n_el + v;
-#pragma unroll
-            for (int q = 0; q < 3; ++q) mv[q][k] = in ? maps[q * plane + r] : 0.f;
+        for (int k = 0; k < NH; ++k) {
+            const int i = threadIdx.x + k * LT, hu = i / HV, hv = i - hu * HV;
+            const int u = u0 - LH + hu, v = v0 - LH + hv;
+            const bool in = hu < HU && u >= 0 && u < n_az && v >= 0 && v < n_el;
+            const int off = u * n_el + v;
+            mv[0][k] = in ? __ldg(&m0[off]) : 0.f;
+            mv[1][k] = in ? __ldg(&m1[off]) : 0.f;
+            mv[2][k] = in ? __ldg(&m2[off]) : 0.f;
         }
 #pragma unroll
-        for (int k = 0; k < NR; ++k) {
-            const int hu = (threadIdx.x >> 6) + k * RS;
-            if (hv < HV && hu < HU) {
-#pragma unroll
-                for (int q = 0; q < 3; ++q) M.m[q][hu][hv] = mv[q][k];
+        for (int k = 0; k < NH; ++k) {
+            const int i = threadIdx.x + k * LT, hu = i / HV, hv = i - hu * HV;
+            if (hu < HU) {
+                M.m[0][hu][hv] = mv[0][k];
+                M.m[1][hu][hv] = mv[1][k];
+                M.m[2][hu][hv] = mv[2][k];
             }
         }
     }

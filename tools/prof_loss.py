@@ -12,6 +12,6 @@ torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(10):
-    loss.spectrum_loss_frames(S, gt)
+    loss.spectrum_loss_frames(S, gt, lam_layout="rays")
 e1.record(); torch.cuda.synchronize()
 print("loss ms", e0.elapsed_time(e1) / 10)
