@@ -358,6 +358,33 @@ def run_ours(args):
                "api": "api.train_step_host: TX + target power frames in, loss report out, spectrum loss on device",
                "loss": [round(float(x), 6) for x in reph[:, 0].tolist()[:2]]}
 
+        if world == 1:
+            # the reference-shaped drop-in call (render_complex_frame + backward_frame
+            # for the batch, render.py:282-289, grad.py:192-259): scene, TX and the
+            # upstream frames from pinned HOST buffers, frames and every gradient back
+            # to HOST buffers, each step (api.fwd_bwd_host) -- the PCIe copies dominate
+            hs = api.pinned_host_scene(scene)
+            lamh = lam.cpu().pin_memory()
+            outh = api.alloc_host_outputs(ds.n, (ds.fle_degree + 1) ** 2, B, 360, 180)
+            for _ in range(max(1, args.warmup)):
+                api.fwd_bwd_host(hs, txh, lamh, outh, scene.rx, scene.ress_radius, 360, 180, ds.fle_degree)
+            torch.cuda.synchronize()
+            gc.collect()
+            gc.disable()
+            es.record()
+            for _ in range(args.steps):
+                h2d_d, d2h_d = api.fwd_bwd_host(hs, txh, lamh, outh, scene.rx, scene.ress_radius, 360, 180,
+                                                ds.fle_degree)
+            ee.record()
+            torch.cuda.synchronize()
+            gc.enable()
+            td = es.elapsed_time(ee)
+            e2e["dropin"] = {"value": round(B * args.steps / (td / 1e3), 2), "unit": UNIT,
+                             "h2d_bytes_per_step": int(h2d_d), "d2h_bytes_per_step": int(d2h_d),
+                             "ms_per_step": round(td / args.steps, 4),
+                             "api": "api.fwd_bwd_host: scene + TX + upstream frames in, frames + all gradients out "
+                                    "(render_complex_frame + backward_frame for the batch, host buffers)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(scene, txs[: args.cpu_sample])

@@ -15,6 +15,9 @@ from .errors import NativeLibraryError, raise_for_status
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # RFS_LIB_PATH: an alternative build of the same library (A/B timing of kernel variants)
 LIB_PATH = os.environ.get("RFS_LIB_PATH") or os.path.join(_HERE, "lib", "librfsplat_b200.so")
+# RFS_NVTX=1: NVTX ranges named after the entry points around every call
+# (e.g. `ncu --nvtx --nvtx-include "rfs_hits/"`, or a timeline profiler)
+NVTX = os.environ.get("RFS_NVTX", "") == "1"
 _lock = threading.Lock()
 _lib = None
 
@@ -128,7 +131,14 @@ def call(name: str, *args) -> None:
         fn = getattr(load(), name)
         _FN[name] = fn
         _CUDA_OK = True
-    rc = fn(*args)
+    if NVTX:  # one NVTX range per entry point: its kernels group under the C-ABI name
+        import torch
+
+        torch.cuda.nvtx.range_push(name)
+        rc = fn(*args)
+        torch.cuda.nvtx.range_pop()
+    else:
+        rc = fn(*args)
     if rc:
         raise_for_status(int(rc), name)
     launch_counter["kernels"] += KERNELS_PER_CALL.get(name, 0)
