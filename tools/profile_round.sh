@@ -10,7 +10,7 @@ timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/${TAG}_bench.json
 timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --sort cub > gpurun_out/${TAG}_bench_cub.json 2>/dev/null
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_" -c 200 \
-    -o gpurun_out/${TAG}_full python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
+# one steady-state step only (cudaProfilerStart/Stop in tools/ncu_step.py): ~30 kernels
+timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on \
+    -o gpurun_out/${TAG}_full python tools/ncu_step.py > gpurun_out/${TAG}_ncu.log 2>&1
 echo done
