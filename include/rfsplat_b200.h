@@ -208,6 +208,9 @@ int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, cons
  * d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov (nullable); d_mean =
  * direct term + dm_dir (the bearing chain of rfs_grad_tx, nullable; read
  * only for Gaussians with hits).
+ * Stage 2 walks the Gaussians with live hits, order[i] for i < min(used_cap,
+ * *n_used) (rfs_used_list; n_used nullable), and zeroes every output row
+ * of the others.
  * Scratch: acc64 f64[N*14], part_g i32[rfs_geom_part_elems(H)],
  * part_v f64[14*rfs_geom_part_elems(H)].  stage (bit mask): 1 = the per-hit
  * sums (K9a), 2 = the per-Gaussian chains (K9c) -- so only K9c has to wait
@@ -216,6 +219,7 @@ size_t rfs_geom_part_elems(int n_hits);
 int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
                   const uint32_t* s_slot, const void* gs, const int* g_rng, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
+                  int used_cap, const uint32_t* n_used, const uint32_t* order,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
                   int stage, void* stream);

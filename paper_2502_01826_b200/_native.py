@@ -57,8 +57,8 @@ _SIGS = {
     "rfs_gauss_ranges": (i32, [vp, i32, vp, i32, vp, vp]),
     "rfs_used_list": (i32, [i32, vp, vp, i32, vp, vp]),
     "rfs_geom_part_elems": (sz, [i32]),
-    "rfs_grad_geom": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                            vp, vp, vp, vp, vp, i32, vp]),
+    "rfs_grad_geom": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, i32, vp, vp, vp, vp, vp,
+                            vp, vp, vp, vp, vp, vp, vp, vp, i32, vp]),
     "rfs_grad_tx": (i32, [i32, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
     "rfs_loss_scratch_bytes": (sz, [i32, i32, i32]),
     "rfs_spectrum_loss": (i32, [i32, i32, i32, vp, vp, vp, f64, f64, vp, vp, vp, vp, vp, sz, vp]),

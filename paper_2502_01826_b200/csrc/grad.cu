@@ -6,10 +6,9 @@
 //     each warp sums its runs of equal Gaussian id through shared memory
 //     (one lane per (run, value)).  Gaussians whose hits straddle warps
 //     leave per-warp partials that
-// K9a' k_geom_fix (thread per 32-hit group where such a Gaussian starts)
-//     adds in group order -- so every sum has a fixed order (the slot order
-//     of the reference's bincount, grad.py:243-254): deterministic.
-// K9c k_geom_final (thread per Gaussian, fp64): d_mean direct term, d_cov,
+//     K9c adds them in group order -- so every sum has a fixed order (the
+//     slot order of the reference's bincount, grad.py:243-254): deterministic.
+// K9c k_geom_final (lane per Gaussian with hits, fp64): d_mean direct term, d_cov,
 //     d|rho|, d(phase), chain_cov_to_shape (grad.py:134-164) and
 //     d_trans_mag_raw = d|rho| sigma (1 - sigma) (train.py:161-162).
 // K9b k_grad_tx (warp per Gaussian, lanes over TX; runs right after K8c):
@@ -147,67 +146,10 @@ __global__ void __launch_bounds__(256) k_geom_seg(
     }
 }
 
-// Gaussians whose hits straddle warps: thread per 32-hit group; the group
-// where such a Gaussian starts adds the group partials (slot 2w+1 of its own
-// group, slot 2v of the later ones).  Spans of up to FIX_SHORT groups (almost
-// all) are summed by that thread left to right; longer ones by the whole
-// warp, lane-strided over the groups plus a fixed butterfly.  Fixed orders:
-// deterministic.
+// Gaussians whose hits straddle warps: k_geom_final adds the group partials
+// (slot 2w+1 of the group where the Gaussian starts, slot 2v of the later
+// ones) in group order.
 constexpr int FIX_SHORT = 4;
-__global__ void __launch_bounds__(256) k_geom_fix(int h, const uint32_t* __restrict__ h_dev,
-                                                  const uint64_t* __restrict__ sorted_g,
-                                                  const int2* __restrict__ g_rng, const double* __restrict__ part_v,
-                                                  double* __restrict__ acc64) {
-    if (h_dev) h = min(h, (int)*h_dev);
-    const int lane = threadIdx.x & 31;
-    const int w = blockIdx.x * blockDim.x + threadIdx.x;  // group
-    const int c0 = w << 5;
-    bool mine = false;
-    int g = 0, w1 = 0;
-    if (c0 < h) {
-        const int c1 = min(c0 + 32, h);
-        if (c1 < h) {
-            g = (int)sorted_g[c1 - 1];
-            // the last segment continues past this group and starts in it
-            const int2 rg = g_rng[g];
-            mine = (int)sorted_g[c1] == g && rg.x >= c0;
-            if (mine) w1 = (rg.y - 1) >> 5;
-        }
-    }
-    if (mine && w1 - w + 1 <= FIX_SHORT) {
-        double s[NACC];
-#pragma unroll
-        for (int i = 0; i < NACC; ++i) s[i] = part_v[(size_t)(2 * w + 1) * NACC + i];
-        for (int v = w + 1; v <= w1; ++v) {
-#pragma unroll
-            for (int i = 0; i < NACC; ++i) s[i] += part_v[(size_t)(2 * v) * NACC + i];
-        }
-#pragma unroll
-        for (int i = 0; i < NACC; ++i) acc64[(size_t)g * NACC + i] = s[i];
-    }
-    unsigned longs = __ballot_sync(0xffffffffu, mine && w1 - w + 1 > FIX_SHORT);
-    while (longs) {
-        const int src = __ffs(longs) - 1;
-        longs &= longs - 1;
-        const int gw = __shfl_sync(0xffffffffu, w, src), gg = __shfl_sync(0xffffffffu, g, src),
-                  gw1 = __shfl_sync(0xffffffffu, w1, src);
-        double s[NACC];
-#pragma unroll
-        for (int i = 0; i < NACC; ++i) s[i] = 0.0;
-        for (int v = gw + lane; v <= gw1; v += 32) {
-            const size_t slot = v == gw ? (size_t)(2 * gw + 1) : (size_t)(2 * v);
-#pragma unroll
-            for (int i = 0; i < NACC; ++i) s[i] += part_v[slot * NACC + i];
-        }
-#pragma unroll
-        for (int i = 0; i < NACC; ++i) {
-            double t = s[i];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-            if (lane == 0) acc64[(size_t)gg * NACC + i] = t;
-        }
-    }
-}
 
 // chain_cov_to_shape for one Gaussian (grad.py:123-164), fp64.
 __device__ void cov_to_shape(const float* q4, const float* s3, const double* dcv, float* dq, float* ds) {
@@ -253,48 +195,103 @@ __device__ void cov_to_shape(const float* q4, const float* s3, const double* dcv
 }
 
 // ------------------------------------------------------------------ K9c
-__global__ void __launch_bounds__(128) k_geom_final(int n, const double* __restrict__ acc64, const float* __restrict__ quats,
-                                                   const float* __restrict__ log_scales, const float* __restrict__ raw,
-                                                   float* __restrict__ d_mean, float* __restrict__ d_quat,
-                                                   float* __restrict__ d_log_scale, float* __restrict__ d_mag,
-                                                   float* __restrict__ d_mag_raw, float* __restrict__ d_phase,
-                                                   float* __restrict__ d_cov, const float* __restrict__ dm_dir,
-                                                   const int2* __restrict__ g_rng) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    const int2 rg = g_rng[g];
-    if (rg.y == rg.x) {  // no live hit (most Gaussians): every term is zero (K9b skips them too)
+// Lane per Gaussian with live hits (order[i], i < min(cap, *n_used)): its 14
+// sums -- from acc64 when its hits lie in one 32-hit group, else the group
+// partials of k_geom_seg added in group order (spans of up to FIX_SHORT groups
+// by the lane, longer ones by the whole warp, lane-strided plus a fixed
+// butterfly: the straddle fix-up folded into this kernel) -- then the direct
+// d_mean term + K9b's bearing chain, d_cov, d|rho|, d(phase), d_trans_mag_raw
+// and chain_cov_to_shape in fp64.  A grid-stride loop then zeroes the rows of
+// the Gaussians without hits.  Every sum has a fixed order: deterministic.
+__global__ void __launch_bounds__(128) k_geom_final(
+    int cap, const uint32_t* __restrict__ n_used, const uint32_t* __restrict__ order, int n,
+    const double* __restrict__ acc64, const double* __restrict__ part_v, const float* __restrict__ quats,
+    const float* __restrict__ log_scales, const float* __restrict__ raw, float* __restrict__ d_mean,
+    float* __restrict__ d_quat, float* __restrict__ d_log_scale, float* __restrict__ d_mag,
+    float* __restrict__ d_mag_raw, float* __restrict__ d_phase, float* __restrict__ d_cov,
+    const float* __restrict__ dm_dir, const int2* __restrict__ g_rng) {
+    __shared__ double s_long[128 / 32][NACC];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int m = n_used ? min(cap, (int)*n_used) : cap;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (((i >> 5) << 5) < m) {  // warps with at least one used Gaussian
+        const bool on = i < m;
+        const int g = on ? (int)order[i] : 0;
+        const int2 rg = on ? g_rng[g] : make_int2(0, 1);
+        const int w0 = rg.x >> 5, w1 = (rg.y - 1) >> 5;
+        double a[NACC];
+        if (on && w0 == w1) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i) d_mean[3 * g + i] = 0.f;
+            for (int k = 0; k < NACC; ++k) a[k] = acc64[(size_t)g * NACC + k];
+        } else if (on && w1 - w0 + 1 <= FIX_SHORT) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) d_quat[4 * g + i] = 0.f;
+            for (int k = 0; k < NACC; ++k) a[k] = part_v[(size_t)(2 * w0 + 1) * NACC + k];
+            for (int v = w0 + 1; v <= w1; ++v) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i) d_log_scale[3 * g + i] = 0.f;
+                for (int k = 0; k < NACC; ++k) a[k] += part_v[(size_t)(2 * v) * NACC + k];
+            }
+        }
+        unsigned longs = __ballot_sync(0xffffffffu, on && w1 - w0 + 1 > FIX_SHORT);
+        while (longs) {
+            const int src = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const int gw = __shfl_sync(0xffffffffu, w0, src), gw1 = __shfl_sync(0xffffffffu, w1, src);
+            double t[NACC];
+#pragma unroll
+            for (int k = 0; k < NACC; ++k) t[k] = 0.0;
+            for (int v = gw + lane; v <= gw1; v += 32) {
+                const size_t slot = v == gw ? (size_t)(2 * gw + 1) : (size_t)(2 * v);
+#pragma unroll
+                for (int k = 0; k < NACC; ++k) t[k] += part_v[slot * NACC + k];
+            }
+#pragma unroll
+            for (int k = 0; k < NACC; ++k) {
+                double x = t[k];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                if (lane == 0) s_long[wl][k] = x;
+            }
+            __syncwarp();
+            if (lane == src) {
+#pragma unroll
+                for (int k = 0; k < NACC; ++k) a[k] = s_long[wl][k];
+            }
+            __syncwarp();
+        }
+        if (on) {
+            // direct term + the bearing chain of K9b (which ran before)
+            d_mean[3 * g + 0] = (float)a[0] + (dm_dir ? dm_dir[3 * g + 0] : 0.f);
+            d_mean[3 * g + 1] = (float)a[1] + (dm_dir ? dm_dir[3 * g + 1] : 0.f);
+            d_mean[3 * g + 2] = (float)a[2] + (dm_dir ? dm_dir[3 * g + 2] : 0.f);
+            d_mag[g] = (float)a[12];
+            const float sg = 1.f / (1.f + expf(-raw[g]));
+            d_mag_raw[g] = (float)a[12] * sg * (1.f - sg);
+            d_phase[g] = (float)a[13];
+            if (d_cov) {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) d_cov[9 * g + k] = (float)a[3 + k];
+            }
+            cov_to_shape(quats + 4 * g, log_scales + 3 * g, a + 3, d_quat + 4 * g, d_log_scale + 3 * g);
+        }
+    }
+    // Gaussians without live hits (most): every term is zero
+    for (int g = i; g < n; g += gridDim.x * blockDim.x) {
+        const int2 rg = g_rng[g];
+        if (rg.y != rg.x) continue;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) d_mean[3 * g + k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d_quat[4 * g + k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) d_log_scale[3 * g + k] = 0.f;
         d_mag[g] = 0.f;
         d_mag_raw[g] = 0.f;
         d_phase[g] = 0.f;
         if (d_cov) {
 #pragma unroll
-            for (int i = 0; i < 9; ++i) d_cov[9 * g + i] = 0.f;
+            for (int k = 0; k < 9; ++k) d_cov[9 * g + k] = 0.f;
         }
-        return;
     }
-    double a[NACC];
-#pragma unroll
-    for (int i = 0; i < NACC; ++i) a[i] = acc64[(size_t)g * NACC + i];
-    // direct term + the bearing chain of K9b (which ran before)
-    d_mean[3 * g + 0] = (float)a[0] + (dm_dir ? dm_dir[3 * g + 0] : 0.f);
-    d_mean[3 * g + 1] = (float)a[1] + (dm_dir ? dm_dir[3 * g + 1] : 0.f);
-    d_mean[3 * g + 2] = (float)a[2] + (dm_dir ? dm_dir[3 * g + 2] : 0.f);
-    d_mag[g] = (float)a[12];
-    const float sg = 1.f / (1.f + expf(-raw[g]));
-    d_mag_raw[g] = (float)a[12] * sg * (1.f - sg);
-    d_phase[g] = (float)a[13];
-    if (d_cov) {
-#pragma unroll
-        for (int i = 0; i < 9; ++i) d_cov[9 * g + i] = (float)a[3 + i];
-    }
-    cov_to_shape(quats + 4 * g, log_scales + 3 * g, a + 3, d_quat + 4 * g, d_log_scale + 3 * g);
 }
 
 // Sum of 32 per-lane values over the warp; afterwards lane l holds the total
@@ -442,25 +439,28 @@ size_t rfs_geom_part_elems(int n_hits) { return (size_t)2 * (size_t)((n_hits + 3
 int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sorted_g, const uint32_t* s_ray, const float* s_w,
                   const uint32_t* s_slot, const void* gs, const int* g_rng, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
+                  int used_cap, const uint32_t* n_used, const uint32_t* order,
                   double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
                   int stage, void* stream) {
     if (n <= 0) return RFS_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int2* rg = (const int2*)g_rng;
-    // acc64 rows of Gaussians with hits are all written by k_geom_seg / k_geom_fix;
-    // k_geom_final reads no other row (g_rng), so no clearing pass
-    if ((stage & 1) && n_hits > 0) {
+    // acc64 rows / part_v slots are all written by k_geom_seg before k_geom_final
+    // reads them (g_rng says which), so no clearing pass
+    if ((stage & 1) && n_hits > 0)
         k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
                                                                (const RfsGeom*)geom, dirs, rg, rx[0], rx[1], rx[2],
                                                                ress_radius, acc64, part_g, part_v);
-        k_geom_fix<<<rfs_ceil_div(rfs_ceil_div(n_hits, 32), 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, rg, part_v,
-                                                                              acc64);
+    if (stage & 2) {
+        if (order == nullptr) return RFS_ERR_CONTRACT;
+        const long long threads = std::max<long long>(used_cap, 1);
+        const unsigned grid = (unsigned)std::max<long long>(rfs_ceil_div(threads, 128),
+                                                            std::min<long long>(rfs_ceil_div(n, 128), 148LL * 8));
+        k_geom_final<<<grid, 128, 0, st>>>(used_cap, n_used, order, n, acc64, part_v, quats, log_scales, trans_mag_raw,
+                                          d_mean, d_quat, d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase,
+                                          d_cov, dm_dir, rg);
     }
-    if (stage & 2)
-        k_geom_final<<<rfs_ceil_div(n, 128), 128, 0, st>>>(n, acc64, quats, log_scales, trans_mag_raw, d_mean, d_quat,
-                                                       d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase, d_cov,
-                                                       dm_dir, rg);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
