@@ -369,18 +369,50 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
             const float rx = tx[3 * b] - mxf, ry = tx[3 * b + 1] - myf, rz = tx[3 * b + 2] - mzf;
             typename Fle<L>::Tables T;
             Fle<L>::tables(rx, ry, rz, T);
-            float2 dpa = make_float2(0.f, 0.f), dpb = make_float2(0.f, 0.f);
-            Fle<L>::for_each(T, [&](int idx, int mm, float2 bv, float2 dbv) {
-                vals[2 * idx] += p.x * bv.x - p.y * bv.y;          // Re conj(P) conj(basis)
-                vals[2 * idx + 1] += -(p.x * bv.y + p.y * bv.x);   // Im
-                if (include_dir) {
-                    const float2 cc = __ldg(&co[idx]);
-                    const float2 cb = cmulf(cc, bv);
-                    dpa.x += -(float)mm * cb.y;  // d psi / d alpha = sum c (i m) basis
-                    dpa.y += (float)mm * cb.x;
-                    dpb = caddf(dpb, cmulf(cc, dbv));
+            // grouped by order m: basis_lm = r_lm P_l^|m| E_m with E_m = e^{i m alpha}
+            // (E_-m = conj E_m), so per m one complex factor serves every l:
+            //   d_coeffs_lm += conj(p basis_lm) = r P_l^|m| conj(p E_m)
+            //   dpsi/dalpha = sum_m (i m) E_m sum_l c_lm r P_l^|m|,
+            //   dpsi/dbeta  = sum_m E_m sum_l c_lm r dP_l^|m|
+            float2 q[2 * L + 1], A[2 * L + 1], Bm[2 * L + 1];
+#pragma unroll
+            for (int m = -L; m <= L; ++m) {
+                const float2 e = m < 0 ? make_float2(T.em[-m].x, -T.em[-m].y) : T.em[m];
+                const float2 pe = cmulf(p, e);
+                q[m + L] = make_float2(pe.x, -pe.y);
+                A[m + L] = make_float2(0.f, 0.f);
+                Bm[m + L] = make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int l = 0; l <= L; ++l) {
+#pragma unroll
+                for (int m = -l; m <= l; ++m) {
+                    const int idx = l * l + l + m, ma = m < 0 ? -m : m;
+                    const float rt = Fle<L>::ratio(l, m);
+                    const float pv = rt * T.p[l][ma];
+                    vals[2 * idx] = fmaf(pv, q[m + L].x, vals[2 * idx]);
+                    vals[2 * idx + 1] = fmaf(pv, q[m + L].y, vals[2 * idx + 1]);
+                    if (include_dir) {
+                        const float2 cc = __ldg(&co[idx]);
+                        const float dv = rt * T.dp[l][ma];
+                        A[m + L].x = fmaf(cc.x, pv, A[m + L].x);
+                        A[m + L].y = fmaf(cc.y, pv, A[m + L].y);
+                        Bm[m + L].x = fmaf(cc.x, dv, Bm[m + L].x);
+                        Bm[m + L].y = fmaf(cc.y, dv, Bm[m + L].y);
+                    }
                 }
-            });
+            }
+            float2 dpa = make_float2(0.f, 0.f), dpb = make_float2(0.f, 0.f);
+            if (include_dir) {
+#pragma unroll
+                for (int m = -L; m <= L; ++m) {
+                    const float2 e = m < 0 ? make_float2(T.em[-m].x, -T.em[-m].y) : T.em[m];
+                    const float2 ea = cmulf(e, A[m + L]);
+                    dpa.x = fmaf(-(float)m, ea.y, dpa.x);  // (i m) E_m A_m
+                    dpa.y = fmaf((float)m, ea.x, dpa.y);
+                    dpb = caddf(dpb, cmulf(e, Bm[m + L]));
+                }
+            }
             if (include_dir) {
                 const float zeta2 = rx * rx + ry * ry + rz * rz;
                 const float rho2 = rx * rx + ry * ry;
