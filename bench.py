@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--deterministic", action="store_true", help="(no-op: the backward is always atomic-free and deterministic)")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--eager", action="store_true", help="time the eager step (no CUDA graph)")
     p.add_argument("--strong", action="store_true",
                    help="strong scaling: --batch TX in total, the ray space (tiles) sharded over the ranks, "
                         "frames and gradients all-reduced (parallel.tile_step); e.g. config 4: --gaussians 1000000")
@@ -273,6 +274,33 @@ def run_ours(args):
         for (_, a), (name, bb) in zip(marks[:-1], marks[1:]):
             phases.setdefault(name, []).append(a.elapsed_time(bb))
     launches = (_native.launch_counter["kernels"] - launches0) // args.steps
+    eager_ms = float(np.sum(per_step)) / args.steps
+    # The steady-state step as one CUDA graph (api.StepGraph: the same kernels,
+    # no host work between them, the hit statistics validated after the step).
+    # Single process only; `value` is the graph replay if every replay stayed
+    # within the capacities, else the eager steps above.
+    graph_info = None
+    if world == 1 and not args.strong and not args.eager:
+        sg = api.StepGraph(ds, tx, lamT, gb, True, args.sort)
+        for _ in range(args.warmup):
+            sg.replay()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        oks = []
+        for a, b_ in ev:
+            flush.fill_(1)  # evict L2 between steps (outside the timed events)
+            a.record()
+            sg.set_tx(tx)  # the step's TX batch into the graph's input buffer (device copy, timed)
+            sg.replay()
+            b_.record()
+        torch.cuda.synchronize()
+        oks.append(sg.ok())
+        g_ms = float(np.mean([a.elapsed_time(b_) for a, b_ in ev]))
+        graph_info = {"ms_per_step": round(g_ms, 4), "valid": all(oks), "eager_ms_per_step": round(eager_ms, 4)}
+        if all(oks):
+            per_step = [a.elapsed_time(b_) for a, b_ in ev]
+            launches = launches  # the same kernels per replay
+        del sg
     clk = clocks.stop()
     t_ms = float(np.sum(per_step))
     if world > 1:
@@ -340,14 +368,36 @@ def run_ours(args):
             dist.barrier()
         es = torch.cuda.Event(enable_timing=True)
         ee = torch.cuda.Event(enable_timing=True)
-        gc.collect()
-        gc.disable()
-        es.record()
-        for _ in range(args.steps):
-            _, h2d, d2h = api.train_step_host(ds, txh, gth, reph, sort_backend=args.sort, grads=gb)
-        ee.record()
-        torch.cuda.synchronize()
-        gc.enable()
+        e2e_step = "eager"
+        if world == 1 and not args.eager:
+            # the training step as one CUDA graph (api.TrainStepGraph): H2D of the
+            # TX batch and the measured frames, render, loss, backward, D2H of the
+            # loss report -- all graph nodes, replayed per step
+            tg = api.TrainStepGraph(ds, txh, gth, reph, gb, sort_backend=args.sort)
+            for _ in range(args.warmup):
+                tg.replay()
+            torch.cuda.synchronize()
+            gc.collect()
+            gc.disable()
+            es.record()
+            for _ in range(args.steps):
+                tg.replay()
+            ee.record()
+            torch.cuda.synchronize()
+            gc.enable()
+            h2d, d2h = tg.h2d, tg.d2h
+            if tg.ok():
+                e2e_step = "CUDA graph replay (api.TrainStepGraph)"
+            del tg
+        if e2e_step == "eager":
+            gc.collect()
+            gc.disable()
+            es.record()
+            for _ in range(args.steps):
+                _, h2d, d2h = api.train_step_host(ds, txh, gth, reph, sort_backend=args.sort, grads=gb)
+            ee.record()
+            torch.cuda.synchronize()
+            gc.enable()
         te = es.elapsed_time(ee)
         if world > 1:
             tt = torch.tensor([te], device=dev, dtype=torch.float64)
@@ -356,6 +406,7 @@ def run_ours(args):
         e2e = {"value": round(world * B * args.steps / (te / 1e3), 2), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(te / args.steps, 4),
                "api": "api.train_step_host: TX + target power frames in, loss report out, spectrum loss on device",
+               "step": e2e_step,
                "loss": [round(float(x), 6) for x in reph[:, 0].tolist()[:2]]}
 
         if world == 1:
@@ -407,7 +458,10 @@ def run_ours(args):
                        "sort": args.sort, "hit_stats": hit_stats,
                        "parallelism": (f"tile-sharded x{world} (rays split by tiles, frames + grads all-reduced)"
                                        if args.strong else f"dp{world} (TX-sharded, grads all-reduced)"),
-                       "l2": "flushed between steps (256 MB write)"},
+                       "l2": "flushed between steps (256 MB write)",
+                       "step": ("CUDA graph replay of the steady-state step (api.StepGraph); phase_ms / roofline "
+                                "from the eager steps" if graph_info and graph_info["valid"] else "eager"),
+                       "graph": graph_info},
             "roofline": rl, "kernels_roofline": roof, "phase_ms": {k: round(v, 4) for k, v in ph_ms.items()},
             "loss_ms": round(loss_ms, 4), "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clk,
         }

@@ -263,7 +263,7 @@ def fwd_bwd_host(host_scene: dict, tx_host: torch.Tensor, lam_host: torch.Tensor
 
 def fwd_bwd_device(ds: raster.DeviceScene, tx: torch.Tensor, lam: torch.Tensor | None = None,
                    include_direction_chain: bool = True, sort_backend: str = "hand", marks: list | None = None,
-                   lamT: torch.Tensor | None = None, grads=None, group=None) -> tuple:
+                   lamT: torch.Tensor | None = None, grads=None, group=None, deferred: dict | None = None) -> tuple:
     """The benched step (bench.py): render + backward of a device-resident
     scene for a TX batch [B, 3] under a fixed upstream.
 
@@ -276,6 +276,8 @@ def fwd_bwd_device(ds: raster.DeviceScene, tx: torch.Tensor, lam: torch.Tensor |
     `grads` (optional parallel.GradBuffer): the backward writes into it and,
     under torch.distributed with more than one rank, all-reduces it in two
     buckets overlapped with the epilogue (this rank's `tx` is its TX shard).
+    `deferred` (optional dict, see raster.build_geometry): the host-sync-free
+    steady-state form (StepGraph captures it).
     Returns (S [B, n_az, n_el], grads).
     """
     b = int(tx.shape[0])
@@ -283,7 +285,7 @@ def fwd_bwd_device(ds: raster.DeviceScene, tx: torch.Tensor, lam: torch.Tensor |
     if lamT is None and b <= raster.MAX_TX_PER_LAUNCH:
         early_t = lambda S: raster.transpose_upstream(lam)
     geo = raster.build_geometry(ds, sort_backend=sort_backend, marks=marks, psi_tx=tx, forward=True, index=True,
-                                after_forward=early_t)
+                                after_forward=early_t, deferred=deferred)
     lt = lamT if lamT is not None else geo.after_result
     if grads is not None:
         from . import parallel
@@ -293,6 +295,78 @@ def fwd_bwd_device(ds: raster.DeviceScene, tx: torch.Tensor, lam: torch.Tensor |
     else:
         g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=geo.psi, marks=marks, lamT=lt)
     return geo.S, g
+
+
+class StepGraph:
+    """The steady-state fwd+bwd step (fwd_bwd_device) captured as one CUDA graph.
+
+    The step has two host reads when run eagerly (the incidence count M and
+    the hit-list statistics); in the steady state every capacity they size is
+    known from earlier steps, so the captured form reads nothing back during
+    the step: the statistics land in pinned buffers and `ok()` validates them
+    afterwards (a False answer means the capacities were exceeded -- rerun the
+    step eagerly with `eager()`, which also grows them, and capture again).
+    Replays launch the ~30 kernels of the step (two streams) with no host
+    work in between.  Inputs: the static TX buffer `tx` [B, 3] (copy new
+    positions into it, `set_tx`) and the ray-major upstream `lamT`; outputs:
+    `S` and the gradient buffer `grads` (parallel.GradBuffer views).
+    Single process (the multi-rank all-reduce stays eager)."""
+
+    def __init__(self, ds: raster.DeviceScene, tx: torch.Tensor, lamT: torch.Tensor, grads,
+                 include_direction_chain: bool = True, sort_backend: str = "hand", warmup: int = 3):
+        self.ds, self.lamT, self.grads = ds, lamT, grads
+        self.tx = tx.to(torch.float32).contiguous().clone()
+        self.dc, self.sort_backend = include_direction_chain, sort_backend
+        for _ in range(max(1, warmup)):  # capacities, persistent buffers, kernel attributes
+            self.eager()
+        torch.cuda.synchronize()
+        self.deferred = {"stats": torch.zeros(16, dtype=torch.int32).pin_memory(),
+                         "status": torch.zeros(8, dtype=torch.int32).pin_memory()}
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.S, self.g = fwd_bwd_device(ds, self.tx, None, self.dc, sort_backend, lamT=lamT, grads=grads,
+                                            deferred=self.deferred)
+
+    def set_tx(self, tx: torch.Tensor) -> None:
+        self.tx.copy_(tx, non_blocking=True)
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    def ok(self) -> bool:
+        """After a synchronize: did the last replay stay within the capacities?"""
+        return raster.deferred_ok(self.deferred)
+
+    def eager(self):
+        return fwd_bwd_device(self.ds, self.tx, None, self.dc, self.sort_backend, lamT=self.lamT, grads=self.grads)
+
+
+class TrainStepGraph:
+    """train_step_host captured as one CUDA graph (see StepGraph): each replay
+    copies the TX positions and measured power frames from the given pinned
+    host buffers (fill them before replaying), renders, runs the spectrum loss
+    and the backward into `grads`, and copies the per-frame loss report into
+    `report_host` -- no host work inside the step.  `ok()` validates the
+    deferred statistics after a synchronize.  Single process."""
+
+    def __init__(self, ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torch.Tensor,
+                 report_host: torch.Tensor, grads, w_ssim: float = 0.2, w_fourier: float = 0.2,
+                 include_direction_chain: bool = True, sort_backend: str = "hand", warmup: int = 3):
+        args = (ds, tx_host, gt_host, report_host, w_ssim, w_fourier, include_direction_chain, sort_backend)
+        for _ in range(max(1, warmup)):
+            train_step_host(*args, grads=grads)
+        torch.cuda.synchronize()
+        self.deferred = {"stats": torch.zeros(16, dtype=torch.int32).pin_memory(),
+                         "status": torch.zeros(8, dtype=torch.int32).pin_memory()}
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.g, self.h2d, self.d2h = train_step_host(*args, grads=grads, deferred=self.deferred)
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    def ok(self) -> bool:
+        return raster.deferred_ok(self.deferred)
 
 
 _COPY: dict = {}
@@ -307,7 +381,8 @@ def _copy_stream(dev) -> torch.cuda.Stream:
 
 def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torch.Tensor, report_host: torch.Tensor,
                     w_ssim: float = 0.2, w_fourier: float = 0.2, include_direction_chain: bool = True,
-                    sort_backend: str = "hand", reduce_fn=None, grads=None, group=None) -> tuple:
+                    sort_backend: str = "hand", reduce_fn=None, grads=None, group=None,
+                    deferred: dict | None = None) -> tuple:
     """One training step of a device-resident scene on a TX batch from HOST buffers.
 
     The batched counterpart of the reference iteration (train.py:266-281,
@@ -320,6 +395,8 @@ def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torc
     the caller synchronizes.  `grads` (optional parallel.GradBuffer) receives
     the gradients, all-reduced over the ranks as in fwd_bwd_device;
     `reduce_fn(g)` (optional) is applied to a plain gradient dict instead.
+    `deferred` (optional dict, see raster.build_geometry): the host-sync-free
+    steady-state form (TrainStepGraph captures it).
     Returns (grads, h2d_bytes, d2h_bytes).
     """
     from . import loss as _loss
@@ -335,8 +412,8 @@ def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torc
         gt = gt_host.to(dev, non_blocking=True)
         gt_ready = torch.cuda.Event()
         gt_ready.record(cs)
-    tx.record_stream(main)
-    gt.record_stream(main)
+    raster._keep(tx, main)
+    raster._keep(gt, main)
     main.wait_event(tx_ready)
 
     def loss_and_upstream(S):  # queued behind the geometry's hit-statistics read
@@ -348,7 +425,7 @@ def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torc
         return rep, lam, None
 
     geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True, forward=True,
-                                after_forward=loss_and_upstream)
+                                after_forward=loss_and_upstream, deferred=deferred)
     rep, lam, lamT = geo.after_result
     if grads is not None:
         from . import parallel

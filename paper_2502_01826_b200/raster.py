@@ -276,6 +276,13 @@ def _pinned(dev, name: str, n: int) -> torch.Tensor:
     return t[:n]
 
 
+def _keep(t: torch.Tensor, stream) -> None:
+    """record_stream, except under CUDA-graph capture (the graph's private
+    memory pool keeps every buffer of the captured step alive)."""
+    if not torch.cuda.is_current_stream_capturing():
+        t.record_stream(stream)
+
+
 def _spin(ev: torch.cuda.Event) -> None:
     """Wait for an event by polling: a blocking wait sleeps and wakes tens of
     microseconds late, time in which the device would drain its queue."""
@@ -286,7 +293,7 @@ def _spin(ev: torch.cuda.Event) -> None:
 def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bool = False,
                    hcap: int | None = None, marks: list | None = None, psi_tx: torch.Tensor | None = None,
                    index: bool = False, forward: bool = False, after_forward=None,
-                   tiles: tuple | None = None) -> Geometry:
+                   tiles: tuple | None = None, deferred: dict | None = None) -> Geometry:
     """K1-K6: projection, binning, sort, ranges, emission bounds, hit lists.
 
     Two small device->host reads size the later buffers (M after the scan,
@@ -305,6 +312,13 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     `index=True` builds the by-Gaussian hit index for the backward.  `marks`
     (optional list) receives (phase, cuda.Event) pairs recorded after each
     phase on the current stream, for per-kernel timing in bench.py.
+    `deferred` (optional dict with pinned int32 tensors "stats" [16] and
+    "status" [8]): the steady-state, host-sync-free form used under CUDA-graph
+    capture (api.StepGraph) -- every capacity (M, hit slab, index, used
+    Gaussians) comes from earlier steps, nothing is read back during the call,
+    and the statistics / status words are copied into the given pinned buffers
+    for the caller to validate afterwards (deferred_ok); requires psi_tx,
+    index=True and known capacities.
     """
     scene.validate()
     lib = _native.load()
@@ -325,8 +339,9 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             compute_psi(scene, psi_tx, None, out=psi_early)
             psi_ready = torch.cuda.Event()
             psi_ready.record(side)
-        psi_early.record_stream(side)
-        psi_tx.record_stream(side)
+        _keep(psi_early, side)
+        _keep(psi_tx, side)
+        return psi_early, psi_ready
     psi = None
     n, n_az, n_el = scene.n, scene.n_az, scene.n_el
     tiles_u = (n_az + TILE - 1) // TILE
@@ -408,6 +423,8 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
 
     hc = 1 << max(0, math.ceil(math.log2(max(int(hcap or _CAPS["hcap"]), 1))))  # power of two: slot >> log2(hcap) = ray
     pc = _CAPS["pcap"]
+    if deferred is not None:
+        return _geometry_deferred(scene, deferred, locals())
     ray_counts = torch.empty(R, dtype=torch.int32, device=dev)
     slow = torch.empty(R, dtype=torch.int32, device=dev)
     stats = torch.zeros(16, dtype=torch.int32, device=dev)
@@ -459,8 +476,8 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
                     ready.record(side)
                 # the side stream reads these main-stream buffers: keep them alive
                 # (a geometry dropped without a backward) until it is done
-                slab.record_stream(side)
-                ray_counts.record_stream(side)
+                _keep(slab, side)
+                _keep(ray_counts, side)
                 _INDEX_GEN[0] += 1
                 early.gidx["ready"] = ready
                 early.gidx["gen"] = _INDEX_GEN[0]
@@ -542,6 +559,72 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
             key = (n_az, n_el, hc)
             _CAPS["h_cap"][key] = max(_CAPS["h_cap"].get(key, 0), hh + hh // 8 + 4096)
     return geo
+
+
+def _geometry_deferred(scene, deferred: dict, L: dict) -> Geometry:
+    """build_geometry's steady-state tail without host reads (see its
+    `deferred` argument): hit lists, psi (side stream), the forward composite
+    and the by-Gaussian index (side stream) on the known capacities; the
+    statistics / status words go to deferred["stats"] / ["status"]."""
+    n, n_az, n_el, dev = L["n"], L["n_az"], L["n_el"], L["dev"]
+    R, hc, pc, st = L["R"], L["hc"], L["pc"], L["st"]
+    h_cap = _CAPS["h_cap"].get((n_az, n_el, hc))
+    u_cap = _CAPS["used_cap"].get((n, n_az, n_el))
+    if L["m_cap"] is None or h_cap is None or u_cap is None or L["psi_tx"] is None or not L["index"]:
+        raise ValueError("deferred geometry needs psi_tx, index=True and capacities from earlier steps")
+    ray_counts = torch.empty(R, dtype=torch.int32, device=dev)
+    slow = torch.empty(R, dtype=torch.int32, device=dev)
+    stats = torch.zeros(16, dtype=torch.int32, device=dev)
+    used = torch.empty(L["nn"], dtype=torch.int32, device=dev)
+    psi, psi_ready = L["start_psi_early"]() if L["psi_early_go"] else (None, None)
+    slab = torch.empty(R * hc * 16, dtype=torch.uint8, device=dev)
+    _native.call("rfs_hits", _ptr(L["ranges"]), L["n_tiles"], _ptr(L["vals"]), _ptr(L["lb"]), _ptr(L["sph"]),
+                 _ptr(L["whit"]), _ptr(L["geom"]), _ptr(L["dirs"]), L["rx"], float(scene.ress_radius), n_az, n_el, hc,
+                 pc, _ptr(slab), _ptr(ray_counts), _ptr(slow), _ptr(stats), _ptr(used), n, L["t_lo"], L["t_hi"], st)
+    ev_hits = torch.cuda.Event()
+    ev_hits.record()
+    deferred["stats"].copy_(stats, non_blocking=True)
+    deferred["status"].copy_(L["status"], non_blocking=True)
+    marks = L["marks"]
+    _mark(marks, "hits")
+    if psi is None:
+        psi = compute_psi(scene, L["psi_tx"], used)
+    else:
+        torch.cuda.current_stream(dev).wait_event(psi_ready)
+    S = _forward_raw(slab, ray_counts, hc, psi, n_az, n_el) if L["forward"] else None
+    _mark(marks, "forward")
+    after = L["after_forward"](S) if (S is not None and L["after_forward"] is not None) else None
+    geo = Geometry(n, n_az, n_el, L["tiles_u"], L["tiles_v"], -1, L["geom"], L["rho32"], L["dirs"], L["ckeys"],
+                   L["vals"], L["ranges"], hc, slab, ray_counts, [], L["proj"], L["sort_backend"], tuple(scene.rx),
+                   float(scene.ress_radius))
+    geo.used = used
+    side = _side_stream(dev)
+    side.wait_event(ev_hits)
+    with torch.cuda.stream(side):
+        gauss_index(geo, h_cap, _persistent, u_cap)
+        ready = torch.cuda.Event()
+        ready.record(side)
+    _keep(slab, side)
+    _keep(ray_counts, side)
+    _INDEX_GEN[0] += 1
+    geo.gidx["ready"] = ready
+    geo.gidx["gen"] = _INDEX_GEN[0]
+    geo.psi, geo.S, geo.after_result = psi, S, after
+    deferred["caps"] = {"m_cap": L["m_cap"], "h_cap": h_cap, "u_cap": u_cap, "R": R}
+    return geo
+
+
+def deferred_ok(deferred: dict) -> bool:
+    """Validate a deferred geometry after its work completed (the caller
+    synchronized): no geometry error, M within the binning capacity, no ray on
+    the slow path, no hit-slab overflow, H and the used Gaussians within the
+    index capacities.  False means: redo the step eagerly (capacities grow)."""
+    st = deferred["stats"].tolist()
+    status = deferred["status"].tolist()
+    c = deferred["caps"]
+    m = int(status[1]) & 0xFFFFFFFF
+    return (int(status[0]) & (1 << 1)) == 0 and m <= c["m_cap"] and st[0] == 0 and st[1] == 0 \
+        and st[3] <= c["h_cap"] and st[8] <= c["u_cap"]
 
 
 def _check_tx(tx: torch.Tensor) -> torch.Tensor:
@@ -750,7 +833,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
                          int(c0 > 0),
                          _ptr(dm_dir), _ptr(out["d_coeffs"]), side.cuda_stream)
         for t in (txc, P, dm_dir, out["d_coeffs"]):
-            t.record_stream(side)
+            _keep(t, side)
     if on_coeffs is not None:  # d_coeffs is final once the side stream gets here
         ev = torch.cuda.Event()
         ev.record(side)
