@@ -33,6 +33,7 @@ namespace {
 // ------------------------------------------------------------ K8t transpose
 __global__ void __launch_bounds__(256) k_lam_transpose(const float2* __restrict__ lam, int nb, int R,
                                                        float2* __restrict__ lamT) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     __shared__ float2 t[32][33];
     const int r0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
     const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const int2* __restrict__ g_rng,
     const float2* __restrict__ psi, const float2* __restrict__ lamT, int accumulate, float2* __restrict__ C,
     float2* __restrict__ P, float2* __restrict__ part) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     __shared__ uint32_t sh_g[BG_WARPS][BG_CHUNK];
     __shared__ uint32_t sh_r[BG_WARPS][BG_CHUNK];
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
     const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const float4* __restrict__ psi,
     const float4* __restrict__ lamT, int accumulate, float2* __restrict__ C, float4* __restrict__ P,
     float4* __restrict__ part, const int2* __restrict__ g_rng, int* __restrict__ cnt) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     __shared__ uint32_t sh_g[BG_WARPS][BG_CHUNK + 1];
     __shared__ float4 sh_e[BG_WARPS][BG_CHUNK];  // (lambda row offset, slot, w T re, w T im)
@@ -354,6 +357,7 @@ __global__ void __launch_bounds__(256) k_bwd_pfix(int h_tot, const uint32_t* __r
                                                   const uint64_t* __restrict__ sorted_g,
                                                   const int2* __restrict__ g_rng, const float2* __restrict__ part,
                                                   float2* __restrict__ P) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -393,6 +397,7 @@ __global__ void __launch_bounds__(128) k_bwd_rays(const RfsHit* __restrict__ sla
                                                   int hcap, int R, const float4* __restrict__ rho32,
                                                   const RfsGeom* __restrict__ geom, const float2* __restrict__ C,
                                                   float4* __restrict__ gs) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= R) return;
     const int cnt = min(counts[r], hcap);
@@ -426,7 +431,7 @@ extern "C" {
 int rfs_lam_transpose(const void* lam, int n_tx, int n_rays, void* lamT, void* stream) {
     if (n_rays <= 0 || n_tx <= 0) return RFS_OK;
     dim3 grid(rfs_ceil_div(n_rays, 32), rfs_ceil_div(n_tx, 32));
-    k_lam_transpose<<<grid, 256, 0, (cudaStream_t)stream>>>((const float2*)lam, n_tx, n_rays, (float2*)lamT);
+    rfs_launch(k_lam_transpose, grid, 256, 0, (cudaStream_t)stream, (const float2*)lam, n_tx, n_rays, (float2*)lamT);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -449,7 +454,7 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
     if (n_tx % 64 == 0) {
         RFS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)n, st));
 #define RFS_BV(NPV)                                                                                              \
-    k_bwd_gauss_v<NPV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,                   \
+    rfs_launch(k_bwd_gauss_v<NPV>, grid, BG_WARPS * 32, 0, st, n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,                   \
                                                        (const float2*)s_wt, (const float4*)psi,                  \
                                                        (const float4*)lamT, accumulate, (float2*)C, (float4*)P,  \
                                                        (float4*)part, (const int2*)g_rng, cnt)
@@ -463,7 +468,7 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
     } else {
         const int nj = (n_tx + 31) / 32;
 #define RFS_BG(NJV)                                                                                              \
-    k_bwd_gauss<NJV><<<grid, BG_WARPS * 32, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,             \
+    rfs_launch(k_bwd_gauss<NJV>, grid, BG_WARPS * 32, 0, st, n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,             \
                                                      (const float2*)s_wt,                                        \
                                                      (const int2*)g_rng, (const float2*)psi, (const float2*)lamT, accumulate, \
                                                      (float2*)C, (float2*)P, (float2*)part)
@@ -472,7 +477,7 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
         else if (nj <= 4) RFS_BG(4);
         else RFS_BG(8);
 #undef RFS_BG
-        k_bwd_pfix<<<rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st>>>(n_hits, h_dev, n_tx, sorted_g, (const int2*)g_rng,
+        rfs_launch(k_bwd_pfix, rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st, n_hits, h_dev, n_tx, sorted_g, (const int2*)g_rng,
                                                                               (const float2*)part, (float2*)P);
     }
     RFS_LAUNCH_CHECK();
@@ -482,7 +487,7 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
 int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, const void* rho32, const void* geom,
                  const void* C, void* gs, void* stream) {
     if (n_rays <= 0) return RFS_OK;
-    k_bwd_rays<<<rfs_ceil_div(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
+    rfs_launch(k_bwd_rays, rfs_ceil_div(n_rays, 128), 128, 0, (cudaStream_t)stream, 
         (const RfsHit*)slab, counts, hcap, n_rays, (const float4*)rho32, (const RfsGeom*)geom, (const float2*)C,
         (float4*)gs);
     RFS_LAUNCH_CHECK();

@@ -77,6 +77,7 @@ __device__ __forceinline__ void block_hit_masks(const Rect& r, int tiles_u, int 
 // (shared-memory atomics: a count does not depend on the order)
 __global__ void __launch_bounds__(BK_BLK) k_tile_count(int n, const Rect* __restrict__ rects, int tiles_u,
                                                        int n_tiles, int nb, uint32_t* __restrict__ tab) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     __shared__ uint32_t h[BK_MAX_TILES];
     for (int t = threadIdx.x; t < n_tiles; t += BK_BLK) h[t] = 0;
     __syncthreads();
@@ -92,6 +93,7 @@ __global__ void __launch_bounds__(BK_BLK) k_tile_count(int n, const Rect* __rest
 // warp per tile: exclusive scan of its blocks' counts in place, total -> tot[t]
 __global__ void __launch_bounds__(128) k_tile_blockscan(int nb, int n_tiles, uint32_t* __restrict__ tab,
                                                         uint32_t* __restrict__ tot) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int t = (blockIdx.x * 128 + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (t >= n_tiles) return;
     uint32_t* row = tab + (size_t)t * nb;
@@ -116,6 +118,7 @@ __global__ void __launch_bounds__(BK_MAX_TILES) k_tile_offsets(int n_tiles, cons
                                                                uint32_t cap, int2* __restrict__ ranges,
                                                                uint32_t* __restrict__ off_out,
                                                                int* __restrict__ status) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     __shared__ uint32_t wsum[BK_MAX_TILES / 32];
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const uint32_t c = t < n_tiles ? tot[t] : 0u;
@@ -139,6 +142,7 @@ __global__ void __launch_bounds__(BK_BLK) k_fill_stable(int n, const Rect* __res
                                                         int nb, uint32_t cap, const uint32_t* __restrict__ tab,
                                                         const uint32_t* __restrict__ toff,
                                                         uint32_t* __restrict__ bcodes, uint32_t* __restrict__ bvals) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     constexpr int NW = BK_BLK / 32;
     __shared__ uint32_t hit[BK_MAX_TILES][NW];
     __shared__ uint32_t base[BK_MAX_TILES][NW];  // slot of warp w's first incidence in tile t
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(NT) k_seg_sort(const int2* __restrict__ ranges
                                                  uint32_t* __restrict__ altv, const RfsGeom* __restrict__ geom,
                                                  uint64_t* __restrict__ ckeys, uint32_t* __restrict__ vals,
                                                  double* __restrict__ lb) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     constexpr int NW = NT / 32, ITEMS = 8, ROUND = NT * ITEMS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -348,7 +353,7 @@ int launch_seg_sort(int n_tiles, const int* ranges, int lo, uint32_t* bcodes, ui
         RFS_CUDA_TRY(cudaFuncSetAttribute(k_seg_sort<CAP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    k_seg_sort<CAP, NT><<<n_tiles, NT, smem, st>>>((const int2*)ranges, lo, bcodes, bvals, altc, altv,
+    rfs_launch(k_seg_sort<CAP, NT>, n_tiles, NT, smem, st, (const int2*)ranges, lo, bcodes, bvals, altc, altv,
                                                    (const RfsGeom*)geom, ckeys, vals, lb);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
@@ -379,17 +384,17 @@ int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_a
     uint32_t* altc = toff + n_tiles;
     uint32_t* altv = altc + (cap > 0 ? cap : 0);
     if (n > 0) {
-        k_tile_count<<<nb, BK_BLK, 0, st>>>(n, (const Rect*)rects, tiles_u, n_tiles, nb, tab);
+        rfs_launch(k_tile_count, nb, BK_BLK, 0, st, n, (const Rect*)rects, tiles_u, n_tiles, nb, tab);
         RFS_LAUNCH_CHECK();
     } else {
         RFS_CUDA_TRY(cudaMemsetAsync(tab, 0, sizeof(uint32_t) * (size_t)n_tiles, st));
     }
-    k_tile_blockscan<<<rfs_ceil_div(n_tiles * 32, 128), 128, 0, st>>>(nb, n_tiles, tab, tot);
+    rfs_launch(k_tile_blockscan, rfs_ceil_div(n_tiles * 32, 128), 128, 0, st, nb, n_tiles, tab, tot);
     RFS_LAUNCH_CHECK();
-    k_tile_offsets<<<1, BK_MAX_TILES, 0, st>>>(n_tiles, tot, (uint32_t)cap, (int2*)ranges, toff, status);
+    rfs_launch(k_tile_offsets, 1, BK_MAX_TILES, 0, st, n_tiles, tot, (uint32_t)cap, (int2*)ranges, toff, status);
     RFS_LAUNCH_CHECK();
     if (n <= 0 || cap <= 0) return RFS_OK;
-    k_fill_stable<<<nb, BK_BLK, 0, st>>>(n, (const Rect*)rects, depth_code, tiles_u, n_tiles, nb, (uint32_t)cap, tab,
+    rfs_launch(k_fill_stable, nb, BK_BLK, 0, st, n, (const Rect*)rects, depth_code, tiles_u, n_tiles, nb, (uint32_t)cap, tab,
                                          toff, bcodes, bvals);
     RFS_LAUNCH_CHECK();
     int rc = launch_seg_sort<BK_SEG_SMALL, 512>(n_tiles, ranges, 0, bcodes, bvals, altc, altv, geom, ckeys, vals, lb,

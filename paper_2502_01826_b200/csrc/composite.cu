@@ -22,6 +22,7 @@ template <int L>
 __global__ void __launch_bounds__(256) k_psi(int n, int nb, const float* __restrict__ means,
                                              const float2* __restrict__ coeffs, const float* __restrict__ tx,
                                              const uint32_t* __restrict__ used, float2* __restrict__ psi) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int b = blockIdx.y * 64 + threadIdx.x;
     const int g = blockIdx.x * 4 + threadIdx.y;  // Gaussians on grid x (y is limited to 65535)
     if (b >= nb || g >= n) return;
@@ -40,6 +41,7 @@ constexpr int CP_BCH = 64;       // TX per block (lanes own b and b + 32)
 __global__ void __launch_bounds__(CP_THREADS) k_forward(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
                                                         int hcap, const float2* __restrict__ psi, int nb, int R,
                                                         float2* __restrict__ S) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     __shared__ float2 s_out[CP_BCH][CP_RAYS + 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int r0 = blockIdx.x * CP_RAYS, bc = blockIdx.y * CP_BCH;
@@ -90,6 +92,7 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
                                                           const int* __restrict__ counts, int hcap,
                                                           const float4* __restrict__ psi, int nb, int n_az, int n_el,
                                                           float2* __restrict__ S) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     __shared__ float2 s_out[CP_BCH][FP_RAYS + 1];
     __shared__ float4 s_hit[CP_THREADS / 32][32 + 2 * FV_U];  // (row offset bits, w T re, w T im, -)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -192,6 +195,7 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
 // are dropped: the caller checks the count and rebuilds)
 __global__ void k_used_list(int n, const uint32_t* __restrict__ used, const uint32_t* __restrict__ cid, int cap,
                             uint32_t* __restrict__ order) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n || !used[g]) return;
     const uint32_t c = cid[g];
@@ -203,6 +207,7 @@ __global__ void k_used_list(int n, const uint32_t* __restrict__ used, const uint
 __global__ void k_hit_keys(const RfsHit* __restrict__ slab, const int* __restrict__ counts,
                            const uint32_t* __restrict__ ray_off, int hcap, int R, const uint32_t* __restrict__ rank,
                            uint64_t* __restrict__ keys, uint32_t* __restrict__ slots) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int lane = threadIdx.x & 31;
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= R) return;
@@ -222,6 +227,7 @@ __global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h
                                 const RfsHit* __restrict__ slab, uint32_t* __restrict__ s_ray,
                                 float* __restrict__ s_w, float2* __restrict__ s_wt, uint32_t* __restrict__ inv_slot,
                                 uint64_t* __restrict__ keys) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= h) return;
@@ -238,6 +244,7 @@ __global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slots, int h
 // without hits: the array is cleared first); sorted_g = Gaussian id per hit
 __global__ void k_gauss_ranges(const uint64_t* __restrict__ sorted_g, int h, const uint32_t* __restrict__ h_dev,
                                int2* __restrict__ g_rng) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= h) return;
@@ -250,7 +257,7 @@ template <int L>
 void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, const uint32_t* used,
                 float2* psi, cudaStream_t st) {
     dim3 grid(rfs_ceil_div(n, 4), rfs_ceil_div(nb, 64));
-    k_psi<L><<<grid, dim3(64, 4), 0, st>>>(n, nb, means, coeffs, tx, used, psi);
+    rfs_launch(k_psi<L>, grid, dim3(64, 4), 0, st, n, nb, means, coeffs, tx, used, psi);
 }
 
 }  // namespace
@@ -282,10 +289,10 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
     dim3 grid(rfs_ceil_div(n_rays, CP_RAYS), rfs_ceil_div(n_tx, CP_BCH));
     if (n_tx % 2 == 0) {
         dim3 gv(n_az * rfs_ceil_div(n_el, FP_V), rfs_ceil_div(n_tx, CP_BCH));
-        k_forward_v<<<gv, CP_THREADS, 0, (cudaStream_t)stream>>>((const RfsHit*)slab, counts, hcap,
+        rfs_launch(k_forward_v, gv, CP_THREADS, 0, (cudaStream_t)stream, (const RfsHit*)slab, counts, hcap,
                                                                  (const float4*)psi, n_tx, n_az, n_el, (float2*)S);
     } else
-        k_forward<<<grid, CP_THREADS, 0, (cudaStream_t)stream>>>((const RfsHit*)slab, counts, hcap,
+        rfs_launch(k_forward, grid, CP_THREADS, 0, (cudaStream_t)stream, (const RfsHit*)slab, counts, hcap,
                                                                  (const float2*)psi, n_tx, n_rays, (float2*)S);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
@@ -293,7 +300,7 @@ int rfs_forward(const void* slab, const int* counts, int hcap, const void* psi, 
 
 int rfs_used_list(int n, const uint32_t* used, const uint32_t* cid, int cap, uint32_t* order, void* stream) {
     if (n <= 0) return RFS_OK;
-    k_used_list<<<rfs_ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(n, used, cid, cap, order);
+    rfs_launch(k_used_list, rfs_ceil_div(n, 256), 256, 0, (cudaStream_t)stream, n, used, cid, cap, order);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -301,7 +308,7 @@ int rfs_used_list(int n, const uint32_t* used, const uint32_t* cid, int cap, uin
 int rfs_hit_keys(const void* slab, const int* counts, const uint32_t* ray_off, int hcap, int n_rays,
                  const uint32_t* rank, uint64_t* keys, uint32_t* slots, void* stream) {
     if (n_rays <= 0) return RFS_OK;
-    k_hit_keys<<<rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+    rfs_launch(k_hit_keys, rfs_ceil_div((long long)n_rays * 32, 256), 256, 0, (cudaStream_t)stream, 
         (const RfsHit*)slab, counts, ray_off, hcap, n_rays, rank, keys, slots);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
@@ -311,7 +318,7 @@ int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* 
                       uint32_t* s_ray,
                       float* s_w, void* s_wt, uint32_t* inv_slot, uint64_t* keys, void* stream) {
     if (n_hits <= 0) return RFS_OK;
-    k_gather_sorted<<<rfs_ceil_div(n_hits, 256), 256, 0, (cudaStream_t)stream>>>(
+    rfs_launch(k_gather_sorted, rfs_ceil_div(n_hits, 256), 256, 0, (cudaStream_t)stream, 
         sorted_slots, n_hits, h_dev, hcap, (const RfsHit*)slab, s_ray, s_w, (float2*)s_wt, inv_slot, keys);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
@@ -322,7 +329,7 @@ int rfs_gauss_ranges(const uint64_t* sorted_g, int n_hits, const uint32_t* h_dev
     cudaStream_t st = (cudaStream_t)stream;
     RFS_CUDA_TRY(cudaMemsetAsync(g_rng, 0, sizeof(int2) * (size_t)n, st));
     if (n_hits > 0)
-        k_gauss_ranges<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(sorted_g, n_hits, h_dev, (int2*)g_rng);
+        rfs_launch(k_gauss_ranges, rfs_ceil_div(n_hits, 256), 256, 0, st, sorted_g, n_hits, h_dev, (int2*)g_rng);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

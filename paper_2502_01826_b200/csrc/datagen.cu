@@ -44,6 +44,7 @@ __device__ double path_len(const PathRec& p, const double* tx, const double* rx)
 __global__ void k_path_gain(int n_s, int n_p, const double* __restrict__ tx, const PathRec* __restrict__ paths,
                             double rx0, double rx1, double rx2, double f_c, int rolloff, int n_az, int n_el,
                             double2* __restrict__ gain, int2* __restrict__ cell, int* __restrict__ status) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_s * n_p) return;
     const int s = i / n_p, pi = i - s * n_p;
@@ -83,6 +84,7 @@ __global__ void k_path_gain(int n_s, int n_p, const double* __restrict__ tx, con
 __global__ void k_spectrum(int n_s, int n_p, int n_az, int n_el, double sigma_cells,
                            const double2* __restrict__ gain, const int2* __restrict__ cell,
                            float* __restrict__ power32, double* __restrict__ power64) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int R = n_az * n_el;
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int s = blockIdx.y;
@@ -119,6 +121,7 @@ __global__ void k_scalar(int n_s, int n_p, int n_sub, int mode, const double* __
                          const PathRec* __restrict__ paths, double rx0, double rx1, double rx2, double f_c,
                          double spacing, int rolloff, double* __restrict__ rssi, double2* __restrict__ csi,
                          int* __restrict__ status) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_s * n_sub) return;
     const int s = i / n_sub, k = i - s * n_sub;
@@ -162,12 +165,12 @@ int rfs_spectrum_dataset(int n_samples, const double* tx, int n_paths, const voi
     cudaStream_t st = (cudaStream_t)stream;
     RFS_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), st));
     const int np = n_samples * n_paths;
-    k_path_gain<<<rfs_ceil_div(np, 128), 128, 0, st>>>(n_samples, n_paths, tx, (const PathRec*)paths, rx[0], rx[1],
+    rfs_launch(k_path_gain, rfs_ceil_div(np, 128), 128, 0, st, n_samples, n_paths, tx, (const PathRec*)paths, rx[0], rx[1],
                                                        rx[2], f_c, rolloff, n_az, n_el, (double2*)gain, (int2*)cell,
                                                        status);
     const double sigma_cells = sigma_beam / (360.0 / (double)n_az);
     dim3 grid(rfs_ceil_div(n_az * n_el, 256), n_samples);
-    k_spectrum<<<grid, 256, 0, st>>>(n_samples, n_paths, n_az, n_el, sigma_cells, (const double2*)gain,
+    rfs_launch(k_spectrum, grid, 256, 0, st, n_samples, n_paths, n_az, n_el, sigma_cells, (const double2*)gain,
                                      (const int2*)cell, power32, power64);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
@@ -181,7 +184,7 @@ int rfs_scalar_dataset(int n_samples, const double* tx, int n_paths, const void*
     cudaStream_t st = (cudaStream_t)stream;
     RFS_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), st));
     const int ns = mode == 0 ? 1 : n_sub;
-    k_scalar<<<rfs_ceil_div(n_samples * ns, 128), 128, 0, st>>>(n_samples, n_paths, ns, mode, tx,
+    rfs_launch(k_scalar, rfs_ceil_div(n_samples * ns, 128), 128, 0, st, n_samples, n_paths, ns, mode, tx,
                                                                  (const PathRec*)paths, rx[0], rx[1], rx[2], f_c,
                                                                  spacing, rolloff, rssi, (double2*)csi, status);
     RFS_LAUNCH_CHECK();

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(256) k_geom_seg(
     const uint32_t* __restrict__ s_slot, const float4* __restrict__ gs, const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
     const int2* __restrict__ g_rng, double rx0, double rx1, double rx2, double min_t, double* __restrict__ acc64,
     int* __restrict__ part_g, double* __restrict__ part_v) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
@@ -210,6 +211,7 @@ __global__ void __launch_bounds__(128) k_geom_final(
     float* __restrict__ d_quat, float* __restrict__ d_log_scale, float* __restrict__ d_mag,
     float* __restrict__ d_mag_raw, float* __restrict__ d_phase, float* __restrict__ d_cov,
     const float* __restrict__ dm_dir, const int2* __restrict__ g_rng) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     __shared__ double s_long[128 / 32][NACC];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int m = n_used ? min(cap, (int)*n_used) : cap;
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
     const int2* __restrict__ g_rng, int nb, const float* __restrict__ means, const float2* __restrict__ coeffs, const float* __restrict__ tx,
     const float2* __restrict__ P, int include_dir, int accumulate, float* __restrict__ dm_dir,
     float2* __restrict__ d_coeffs) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     constexpr int K = Fle<L>::K;
     constexpr int NV = 2 * K;
     constexpr int NG = (NV + 31) / 32;
@@ -456,7 +459,7 @@ void launch_tx(unsigned grid, cudaStream_t st, int cap, const uint32_t* n_used, 
                int accumulate, float* dm_dir, float2* d_coeffs) {
     const int nj = (nb + 31) / 32;
 #define RFS_GT(NJV)                                                                                                \
-    k_grad_tx<L, NJV><<<grid, GB_THREADS, 0, st>>>(cap, n_used, order, n, g_rng, nb, means, coeffs, tx, P, include_dir,     \
+    rfs_launch(k_grad_tx<L, NJV>, grid, GB_THREADS, 0, st, cap, n_used, order, n, g_rng, nb, means, coeffs, tx, P, include_dir,     \
                                                    accumulate, dm_dir, d_coeffs)
     if (nj <= 2) RFS_GT(2); else RFS_GT(8);
 #undef RFS_GT
@@ -481,7 +484,7 @@ int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sort
     // acc64 rows / part_v slots are all written by k_geom_seg before k_geom_final
     // reads them (g_rng says which), so no clearing pass
     if ((stage & 1) && n_hits > 0)
-        k_geom_seg<<<rfs_ceil_div(n_hits, 256), 256, 0, st>>>(n_hits, h_dev, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
+        rfs_launch(k_geom_seg, rfs_ceil_div(n_hits, 256), 256, 0, st, n_hits, h_dev, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
                                                                (const RfsGeom*)geom, dirs, rg, rx[0], rx[1], rx[2],
                                                                ress_radius, acc64, part_g, part_v);
     if (stage & 2) {
@@ -489,7 +492,7 @@ int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sort
         const long long threads = std::max<long long>(used_cap, 1);
         const unsigned grid = (unsigned)std::max<long long>(rfs_ceil_div(threads, 128),
                                                             std::min<long long>(rfs_ceil_div(n, 128), 148LL * 8));
-        k_geom_final<<<grid, 128, 0, st>>>(used_cap, n_used, order, n, acc64, part_v, quats, log_scales, trans_mag_raw,
+        rfs_launch(k_geom_final, grid, 128, 0, st, used_cap, n_used, order, n, acc64, part_v, quats, log_scales, trans_mag_raw,
                                           d_mean, d_quat, d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase,
                                           d_cov, dm_dir, rg);
     }

@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(NT) k_hits(
     const double* __restrict__ dirs, double rx0, double rx1, double rx2, double min_t, int n_az, int n_el,
     int tiles_u, int hcap, RfsHit* __restrict__ slab, int* __restrict__ counts, int* __restrict__ slow_list,
     int* __restrict__ stats, uint32_t* __restrict__ used, int tile_lo) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HitsSmem<PCAP, NT, CH>& S = *reinterpret_cast<HitsSmem<PCAP, NT, CH>*>(smem_raw);
     constexpr int PARTS = 256 / NT;
@@ -401,6 +402,7 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
                             RfsHit* __restrict__ slab, int* __restrict__ counts, double* __restrict__ pt,
                             uint32_t* __restrict__ pg, float* __restrict__ pw, int pcap, int* __restrict__ stats,
                             uint32_t* __restrict__ used) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_rays) return;
     const int r = rays[i];
@@ -470,6 +472,7 @@ __global__ void k_hits_slow(const int* __restrict__ rays, int n_rays, const int2
 // stats[8] = number of Gaussians with a live hit (the by-Gaussian index sizes
 // its compact keys from it); stats[8] is zeroed by the caller
 __global__ void __launch_bounds__(256) k_count_used(const uint32_t* __restrict__ used, int n, int* __restrict__ stats) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     int c = 0;
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) c += used[g] != 0u;
     c = warp_sum(c);
@@ -477,6 +480,7 @@ __global__ void __launch_bounds__(256) k_count_used(const uint32_t* __restrict__
 }
 
 __global__ void k_max_range(const int2* __restrict__ ranges, int n_tiles, int* __restrict__ out) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < n_tiles) atomicMax(out, ranges[t].y - ranges[t].x);
 }
@@ -485,6 +489,7 @@ __global__ void k_max_range(const int2* __restrict__ ranges, int n_tiles, int* _
 // order as numpy (deg2rad(x) = x * (pi/180)); used only when the host does
 // not supply the table.
 __global__ void k_ray_dirs(int n_az, int n_el, double* __restrict__ dirs) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_az * n_el) return;
     int u = r / n_el, v = r % n_el;
@@ -512,7 +517,7 @@ int launch_hits(int tile_lo, int tile_hi, const int* ranges, const uint32_t* val
                                           (int)cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
-    k_hits<PCAP, NT, CH><<<(tile_hi - tile_lo) * (256 / NT), NT, smem, st>>>(
+    rfs_launch(k_hits<PCAP, NT, CH>, (tile_hi - tile_lo) * (256 / NT), NT, smem, st, 
         (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom, dirs, rx[0],
         rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used, tile_lo);
     RFS_LAUNCH_CHECK();
@@ -526,7 +531,7 @@ extern "C" {
 int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream) {
     int R = n_az * n_el;
     if (R <= 0) return RFS_OK;
-    k_ray_dirs<<<rfs_ceil_div(R, 256), 256, 0, (cudaStream_t)stream>>>(n_az, n_el, dirs);
+    rfs_launch(k_ray_dirs, rfs_ceil_div(R, 256), 256, 0, (cudaStream_t)stream, n_az, n_el, dirs);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -560,8 +565,8 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
                                          n_az, n_el, tiles_u, hcap, slab, counts, slow_list, stats, used, st);
     }
     if (rc != RFS_OK) return rc;
-    k_max_range<<<rfs_ceil_div(n_tiles, 256), 256, 0, st>>>((const int2*)ranges, n_tiles, stats + 4);
-    if (used && n > 0) k_count_used<<<min(rfs_ceil_div(n, 256), 148 * 4), 256, 0, st>>>(used, n, stats);
+    rfs_launch(k_max_range, rfs_ceil_div(n_tiles, 256), 256, 0, st, (const int2*)ranges, n_tiles, stats + 4);
+    if (used && n > 0) rfs_launch(k_count_used, min(rfs_ceil_div(n, 256), 148 * 4), 256, 0, st, used, n, stats);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
@@ -572,13 +577,13 @@ int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t
                   uint32_t* pend_g, float* pend_w, int pcap, int* stats, uint32_t* used, int n, void* stream) {
     if (n_rays <= 0) return RFS_OK;
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
-    k_hits_slow<<<rfs_ceil_div(n_rays, 64), 64, 0, (cudaStream_t)stream>>>(
+    rfs_launch(k_hits_slow, rfs_ceil_div(n_rays, 64), 64, 0, (cudaStream_t)stream, 
         rays, n_rays, (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom,
         dirs, rx[0], rx[1], rx[2], ress_radius, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, pend_t, pend_g,
         pend_w, pcap, stats, used);
     if (used && n > 0) {  // the slow path marks more Gaussians: recount
         RFS_CUDA_TRY(cudaMemsetAsync(stats + 8, 0, sizeof(int), (cudaStream_t)stream));
-        k_count_used<<<min(rfs_ceil_div(n, 256), 148 * 4), 256, 0, (cudaStream_t)stream>>>(used, n, stats);
+        rfs_launch(k_count_used, min(rfs_ceil_div(n, 256), 148 * 4), 256, 0, (cudaStream_t)stream, used, n, stats);
     }
     RFS_LAUNCH_CHECK();
     return RFS_OK;

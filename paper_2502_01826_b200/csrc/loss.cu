@@ -52,6 +52,7 @@ __device__ __forceinline__ float power_f(const float2* __restrict__ S, const flo
 // kernels reduce a frame's RCH partials themselves
 constexpr int RCH = 32;
 __global__ void __launch_bounds__(256) k_frame_range(const float* __restrict__ gt, int R, float2* __restrict__ range) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int b = blockIdx.y, c = blockIdx.x;
     const float* y = gt + (size_t)b * R;
     const int per = (R + RCH - 1) / RCH, i0 = c * per, i1 = min(R, i0 + per);
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_fwd(const float2* __restrict__ S
                                                  const float* __restrict__ gt,
                                                  const float2* __restrict__ range, int n_az, int n_el,
                                                  float* __restrict__ maps, double* __restrict__ part) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FwdSmem& M = *reinterpret_cast<FwdSmem*>(smem_raw);
     const int b = blockIdx.z, u0 = blockIdx.y * TU, v0 = blockIdx.x * TV;
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S
                                                  int n_az, int n_el, float w1, float ws, float wf,
                                                  float* __restrict__ grad, float2* __restrict__ lam,
                                                  float2* __restrict__ lamT) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdSmem& M = *reinterpret_cast<BwdSmem*>(smem_raw);
     const int b = blockIdx.z, u0 = blockIdx.y * TU, v0 = blockIdx.x * TV;
@@ -366,6 +369,7 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S
 // report[b] = {total, l1, ssim, fourier}; one warp per frame, fixed order
 __global__ void k_loss_final(const double* __restrict__ part, int nblk, int n_frames, double n_cells, double w1,
                              double ws, double wf, double* __restrict__ report) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int lane = threadIdx.x & 31;
     const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (b >= n_frames) return;
@@ -401,6 +405,7 @@ __global__ void k_loss_final(const double* __restrict__ part, int nblk, int n_fr
 __global__ void __launch_bounds__(256) k_scalar_loss(const float2* __restrict__ S, int R, int mode,
                                                      const float2* __restrict__ target, double* __restrict__ report,
                                                      float2* __restrict__ total_out, float2* __restrict__ lam) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int b = blockIdx.x;
     const float2* f = S + (size_t)b * R;
     double sr = 0.0, si = 0.0;
@@ -513,12 +518,12 @@ int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const flo
     p += (size_t)nblk * n_frames * 3 * sizeof(double);
     float2* range = (float2*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
     const double w1 = 1.0 - w_ssim - w_fourier;
-    k_frame_range<<<dim3(RCH, n_frames), 256, 0, st>>>(gt, (int)R, range);
-    k_ssim_fwd<<<grid, LT, sizeof(FwdSmem), st>>>((const float2*)S, pred, gt, range, n_az, n_el, maps, part);
-    k_ssim_bwd<<<grid, LT, sizeof(BwdSmem), st>>>((const float2*)S, pred, gt, maps, n_az, n_el, (float)w1,
+    rfs_launch(k_frame_range, dim3(RCH, n_frames), 256, 0, st, gt, (int)R, range);
+    rfs_launch(k_ssim_fwd, grid, LT, sizeof(FwdSmem), st, (const float2*)S, pred, gt, range, n_az, n_el, maps, part);
+    rfs_launch(k_ssim_bwd, grid, LT, sizeof(BwdSmem), st, (const float2*)S, pred, gt, maps, n_az, n_el, (float)w1,
                                                   (float)w_ssim, (float)w_fourier, grad, (float2*)lam,
                                                   (float2*)lamT);
-    k_loss_final<<<rfs_ceil_div((long long)n_frames * 32, 128), 128, 0, st>>>(part, nblk, n_frames, (double)R, w1,
+    rfs_launch(k_loss_final, rfs_ceil_div((long long)n_frames * 32, 128), 128, 0, st, part, nblk, n_frames, (double)R, w1,
                                                                                 w_ssim, w_fourier, report);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
@@ -528,7 +533,7 @@ int rfs_scalar_loss(int n_frames, int n_rays, int mode, const void* S, const voi
                     void* total, void* lam, void* stream) {
     if (n_frames <= 0 || n_rays <= 0) return RFS_OK;
     if (mode != 0 && mode != 1) return RFS_ERR_SHAPE;
-    k_scalar_loss<<<n_frames, 256, 0, (cudaStream_t)stream>>>((const float2*)S, n_rays, mode, (const float2*)target,
+    rfs_launch(k_scalar_loss, n_frames, 256, 0, (cudaStream_t)stream, (const float2*)S, n_rays, mode, (const float2*)target,
                                                               report, (float2*)total, (float2*)lam);
     RFS_LAUNCH_CHECK();
     return RFS_OK;

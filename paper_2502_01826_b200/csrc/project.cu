@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(256) k_project(
     RfsGeom* __restrict__ geom, float4* __restrict__ sph, float4* __restrict__ whit, uint32_t* __restrict__ code,
     Rect* __restrict__ rects, uint32_t* __restrict__ counts, float4* __restrict__ rho32,
     double* __restrict__ proj, int* __restrict__ err) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     double mx = (double)means[3 * g], my = (double)means[3 * g + 1], mz = (double)means[3 * g + 2];
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const uint32_t* _
                                                               uint32_t* __restrict__ out, uint32_t* __restrict__ total_out,
                                                               unsigned int* __restrict__ counter,
                                                               unsigned long long* __restrict__ status) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     __shared__ int tile_s;
     __shared__ uint32_t prefix_s;
     if (threadIdx.x == 0) tile_s = (int)atomicAdd(counter, 1u);
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_onepass(const uint32_t* _
 __global__ void __launch_bounds__(256) k_fill(int n, const Rect* __restrict__ rects, const uint32_t* __restrict__ code,
                                               const uint32_t* __restrict__ offs, int tiles_u, uint32_t cap,
                                               uint64_t* __restrict__ ckeys, uint32_t* __restrict__ vals) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     Rect r = rects[g];
@@ -370,6 +373,7 @@ __global__ void __launch_bounds__(256) k_fill(int n, const Rect* __restrict__ re
 // m_dev (nullable): the device-side count, clamped to m (then the capacity)
 __global__ void k_ranges(const uint64_t* __restrict__ ckeys, int m, const uint32_t* __restrict__ m_dev, int n_tiles,
                          int2* __restrict__ ranges) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (m_dev) m = min(m, (int)*m_dev);
     if (i > m) return;
@@ -383,6 +387,7 @@ __global__ void k_ranges(const uint64_t* __restrict__ ckeys, int m, const uint32
 
 // Restore reference keys (tile << 32 | code) for TileIndex.keys.
 __global__ void k_expand_keys(const uint64_t* __restrict__ ckeys, int m, uint64_t* __restrict__ keys) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     uint64_t c = ckeys[i];
@@ -399,6 +404,7 @@ __global__ void k_expand_keys(const uint64_t* __restrict__ ckeys, int m, uint64_
 constexpr int LB_THREADS = 1024;
 __global__ void __launch_bounds__(LB_THREADS) k_lower_bounds(const int2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                                                               const RfsGeom* __restrict__ geom, double* __restrict__ lb) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     constexpr int NW = LB_THREADS / 32;
     __shared__ double smin[NW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -440,7 +446,7 @@ int rfs_project(int n, const float* means, const float* quats, const float* log_
     if (n == 0) return RFS_OK;
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     cudaStream_t st = (cudaStream_t)stream;
-    k_project<<<rfs_ceil_div(n, 256), 256, 0, st>>>(
+    rfs_launch(k_project, rfs_ceil_div(n, 256), 256, 0, st, 
         n, means, quats, log_scales, trans_mag_raw, trans_phase, rx[0], rx[1], rx[2], ress_radius, n_az, n_el,
         tiles_u, (RfsGeom*)geom, (float4*)sph, (float4*)whit, depth_code, (Rect*)rects, counts, (float4*)rho32, proj_out, err_flags);
     RFS_LAUNCH_CHECK();
@@ -458,7 +464,7 @@ int rfs_exclusive_scan_u32(const uint32_t* in, int n, uint32_t* out, uint32_t* t
     }
     const int nb = rfs_ceil_div(n, SCAN_TILE);
     RFS_CUDA_TRY(cudaMemsetAsync(temp, 0, rfs_scan_temp_elems(n) * sizeof(uint32_t), st));
-    k_scan_onepass<<<nb, SCAN_THREADS, 0, st>>>(in, n, out, total, (unsigned int*)temp,
+    rfs_launch(k_scan_onepass, nb, SCAN_THREADS, 0, st, in, n, out, total, (unsigned int*)temp,
                                                 (unsigned long long*)(temp + 2));
     RFS_LAUNCH_CHECK();
     return RFS_OK;
@@ -468,28 +474,28 @@ int rfs_bin_fill(int n, const void* rects, const uint32_t* depth_code, const uin
                  uint64_t* ckeys, uint32_t* vals, void* stream) {
     if (n <= 0 || cap <= 0) return RFS_OK;
     int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
-    k_fill<<<rfs_ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(n, (const Rect*)rects, depth_code, offsets, tiles_u,
+    rfs_launch(k_fill, rfs_ceil_div(n, 256), 256, 0, (cudaStream_t)stream, n, (const Rect*)rects, depth_code, offsets, tiles_u,
                                                                     (uint32_t)cap, ckeys, vals);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
 int rfs_tile_ranges(const uint64_t* ckeys, int m, const uint32_t* m_dev, int n_tiles, int* ranges, void* stream) {
-    k_ranges<<<rfs_ceil_div(m + 1, 256), 256, 0, (cudaStream_t)stream>>>(ckeys, m, m_dev, n_tiles, (int2*)ranges);
+    rfs_launch(k_ranges, rfs_ceil_div(m + 1, 256), 256, 0, (cudaStream_t)stream, ckeys, m, m_dev, n_tiles, (int2*)ranges);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
 int rfs_expand_keys(const uint64_t* ckeys, int m, uint64_t* keys, void* stream) {
     if (m <= 0) return RFS_OK;
-    k_expand_keys<<<rfs_ceil_div(m, 256), 256, 0, (cudaStream_t)stream>>>(ckeys, m, keys);
+    rfs_launch(k_expand_keys, rfs_ceil_div(m, 256), 256, 0, (cudaStream_t)stream, ckeys, m, keys);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }
 
 int rfs_lower_bounds(const int* ranges, int n_tiles, const uint32_t* vals, const void* geom, double* lb, void* stream) {
     if (n_tiles <= 0) return RFS_OK;
-    k_lower_bounds<<<n_tiles, LB_THREADS, 0, (cudaStream_t)stream>>>((const int2*)ranges, vals, (const RfsGeom*)geom, lb);
+    rfs_launch(k_lower_bounds, n_tiles, LB_THREADS, 0, (cudaStream_t)stream, (const int2*)ranges, vals, (const RfsGeom*)geom, lb);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -45,6 +45,7 @@ template <int BITS>
 __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint64_t* __restrict__ keys, int m,
                                                       const uint32_t* __restrict__ m_dev, int passes,
                                                       uint32_t* __restrict__ hist) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     constexpr int RADIX = 1 << BITS;
     if (m_dev) m = min(m, (int)*m_dev);
     if ((long long)blockIdx.x * HIST_THREADS * HIST_ITEMS >= m) return;
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint64_t* __restric
 
 // exclusive scan of each pass's histogram (one block, one warp per pass)
 __global__ void k_hist_scan(uint32_t* __restrict__ hist, int passes, int radix) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (wid >= passes) return;
     uint32_t* h = hist + wid * radix;
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(const uint64_t* __restr
                                                         int shift, const uint32_t* __restrict__ digit_start,
                                                         uint32_t* __restrict__ lookback, int* __restrict__ tile_counter,
                                                         const uint32_t* __restrict__ m_dev) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     constexpr int RADIX = 1 << BITS, DPT = RADIX / RS_THREADS;
     static_assert(DPT >= 1, "at least one digit per thread");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -262,12 +265,12 @@ int run_sort(uint64_t* kin, uint32_t* vin, uint64_t* kout, uint32_t* vout, int m
                                           (int)(RS_MAX_PASSES * RADIX * sizeof(uint32_t))));
         attr_set = true;
     }
-    k_hist<BITS><<<rfs_ceil_div(m, HIST_THREADS * HIST_ITEMS), HIST_THREADS, passes * RADIX * sizeof(uint32_t), st>>>(
+    rfs_launch(k_hist<BITS>, rfs_ceil_div(m, HIST_THREADS * HIST_ITEMS), HIST_THREADS, passes * RADIX * sizeof(uint32_t), st, 
         kin, m, m_dev, passes, hist);
-    k_hist_scan<<<1, 32 * RS_MAX_PASSES, 0, st>>>(hist, passes, RADIX);
+    rfs_launch(k_hist_scan, 1, 32 * RS_MAX_PASSES, 0, st, hist, passes, RADIX);
     const int nt = num_tiles(m);
     for (int p = 0; p < passes; ++p) {
-        k_onesweep<BITS><<<nt, RS_THREADS, smem, st>>>(kin, vin, kout, vout, m, p * BITS, hist + p * RADIX,
+        rfs_launch(k_onesweep<BITS>, nt, RS_THREADS, smem, st, kin, vin, kout, vout, m, p * BITS, hist + p * RADIX,
                                                        lb + (size_t)p * nt * RADIX, ctr + p, m_dev);
         uint64_t* tk = kin; kin = kout; kout = tk;
         uint32_t* tv = vin; vin = vout; vout = tv;

@@ -9,6 +9,7 @@
 //   psi[N][B]       complex64 directional response, row = Gaussian (512 B @ B=64).
 #pragma once
 #include <cuda_runtime.h>
+#include <utility>
 #include <stdint.h>
 
 #define RFS_TILE 16
@@ -80,6 +81,32 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 static inline int rfs_ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---- programmatic dependent launch (Hopper/Blackwell) ----
+// Every kernel is launched with programmatic stream serialization: its CTAs
+// may be scheduled while the previous kernel in the stream drains (its tail
+// wave, its exit), and each kernel's first instruction is griddepcontrol.wait,
+// which returns once the previous grid has completed and its memory is
+// visible.  So dependent launches overlap the launch latency and the
+// predecessor's tail -- also between the nodes of a captured CUDA graph --
+// with unchanged semantics.
+__device__ __forceinline__ void rfs_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t rfs_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                     Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // K6 ray patches: warp q (0..7) of a 16 x 16 tile owns a 4 (u) x 8 (v) patch.
 // The patch cone (axis through the patch, half-angle covering its rays) as

@@ -66,6 +66,7 @@ __global__ void k_sgd_check(int n, int K, const float* __restrict__ d_mean, cons
                             const float* __restrict__ d_log_scale, const float* __restrict__ d_mag,
                             const float* __restrict__ d_phase, const float* __restrict__ d_coeffs,
                             long long* __restrict__ bad) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     // class order of _check_finite (train.py:133-142)
@@ -88,6 +89,7 @@ __global__ void k_sgd_update(int n, int K, float lr_mean, float lr_rot, float lr
                              float* __restrict__ grad_ema, float* __restrict__ last_dmean,
                              const long long* __restrict__ bad,
                              const long long* __restrict__ prior) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n || *bad != 0x7f7f7f7f7f7f7f7fLL) return;
     if (prior && *prior != 0x7f7f7f7f7f7f7f7fLL) return;  // an earlier step was bad: the scene stays as it was
@@ -124,6 +126,7 @@ __global__ void k_density_flags(int n, int mode, const float* __restrict__ grad_
                                 const float* __restrict__ log_scales, const float* __restrict__ raw, double thr_grad,
                                 double thr_radius, double thr_prune, uint32_t* __restrict__ keep,
                                 uint32_t* __restrict__ clone, uint32_t* __restrict__ split) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     uint32_t k = 1, c = 0, s = 0;
@@ -170,6 +173,7 @@ __global__ void k_density_apply(int n, int K, int mode, const uint32_t* __restri
                                 float* __restrict__ o_log_scales, float* __restrict__ o_raw,
                                 float* __restrict__ o_phase, float* __restrict__ o_coeffs,
                                 float* __restrict__ o_ema, float* __restrict__ o_last) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const uint32_t n_keep = totals[0], n_clone = totals[1];
@@ -228,9 +232,9 @@ int rfs_sgd_step(int n, int K, const float* lrs, float ema_decay, const float* d
     RFS_CUDA_TRY(cudaMemsetAsync(bad, 0x7f, sizeof(long long), st));  // sentinel 0x7f7f..7f = no bad row
     if (n <= 0) return RFS_OK;
     const int grid = rfs_ceil_div(n, 256);
-    k_sgd_check<<<grid, 256, 0, st>>>(n, K, d_mean, d_quat, d_log_scale, d_trans_mag, d_trans_phase,
+    rfs_launch(k_sgd_check, grid, 256, 0, st, n, K, d_mean, d_quat, d_log_scale, d_trans_mag, d_trans_phase,
                                       (const float*)d_coeffs, bad);
-    k_sgd_update<<<grid, 256, 0, st>>>(n, K, lrs[0], lrs[1], lrs[2], lrs[3], lrs[4], ema_decay, d_mean, d_quat,
+    rfs_launch(k_sgd_update, grid, 256, 0, st, n, K, lrs[0], lrs[1], lrs[2], lrs[3], lrs[4], ema_decay, d_mean, d_quat,
                                        d_log_scale, d_trans_mag, d_trans_phase, (const float*)d_coeffs, means, quats,
                                        log_scales, trans_mag_raw, trans_phase, (float*)coeffs, grad_ema, last_dmean,
                                        bad, prior);
@@ -243,7 +247,7 @@ int rfs_density_flags(int n, int mode, const float* grad_ema, const float* log_s
                       uint32_t* split, void* stream) {
     if (n <= 0) return RFS_OK;
     if (mode != 0 && mode != 1) return RFS_ERR_SHAPE;
-    k_density_flags<<<rfs_ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+    rfs_launch(k_density_flags, rfs_ceil_div(n, 256), 256, 0, (cudaStream_t)stream, 
         n, mode, grad_ema, log_scales, trans_mag_raw, thr_grad, thr_radius, thr_prune, keep, clone, split);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
@@ -257,7 +261,7 @@ int rfs_density_apply(int n, int K, int mode, const uint32_t* keep, const uint32
                       const float* last_dmean, float* o_means, float* o_quats, float* o_log_scales, float* o_raw,
                       float* o_phase, void* o_coeffs, float* o_ema, float* o_last, void* stream) {
     if (n <= 0) return RFS_OK;
-    k_density_apply<<<rfs_ceil_div(n, 128), 128, 0, (cudaStream_t)stream>>>(
+    rfs_launch(k_density_apply, rfs_ceil_div(n, 128), 128, 0, (cudaStream_t)stream, 
         n, K, mode, keep, clone, split, keep_off, clone_off, split_off, totals, step, log_split_factor, seed,
         iteration, means, quats, log_scales, trans_mag_raw, trans_phase, (const float*)coeffs, grad_ema, last_dmean,
         o_means, o_quats, o_log_scales, o_raw, o_phase, (float*)o_coeffs, o_ema, o_last);
