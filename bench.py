@@ -280,7 +280,7 @@ def run_ours(args):
     # Single process only; `value` is the graph replay if every replay stayed
     # within the capacities, else the eager steps above.
     graph_info = None
-    if world == 1 and not args.strong and not args.eager:
+    if world == 1 and not args.strong and not args.eager and args.sort == "hand":
         sg = api.StepGraph(ds, tx, lamT, gb, True, args.sort)
         for _ in range(args.warmup):
             sg.replay()
@@ -369,7 +369,7 @@ def run_ours(args):
         es = torch.cuda.Event(enable_timing=True)
         ee = torch.cuda.Event(enable_timing=True)
         e2e_step = "eager"
-        if world == 1 and not args.eager:
+        if world == 1 and not args.eager and args.sort == "hand":
             # the training step as one CUDA graph (api.TrainStepGraph): H2D of the
             # TX batch and the measured frames, render, loss, backward, D2H of the
             # loss report -- all graph nodes, replayed per step

@@ -570,8 +570,10 @@ def _geometry_deferred(scene, deferred: dict, L: dict) -> Geometry:
     R, hc, pc, st = L["R"], L["hc"], L["pc"], L["st"]
     h_cap = _CAPS["h_cap"].get((n_az, n_el, hc))
     u_cap = _CAPS["used_cap"].get((n, n_az, n_el))
-    if L["m_cap"] is None or h_cap is None or u_cap is None or L["psi_tx"] is None or not L["index"]:
-        raise ValueError("deferred geometry needs psi_tx, index=True and capacities from earlier steps")
+    if (L["m_cap"] is None or h_cap is None or u_cap is None or L["psi_tx"] is None or not L["index"]
+            or L["sort_backend"] != "hand"):
+        raise ValueError("deferred geometry needs the hand sort backend, psi_tx, index=True and capacities "
+                         "from earlier steps")
     ray_counts = torch.empty(R, dtype=torch.int32, device=dev)
     slow = torch.empty(R, dtype=torch.int32, device=dev)
     stats = torch.zeros(16, dtype=torch.int32, device=dev)
