@@ -21,6 +21,8 @@
 // sort, rfs_tile_ranges, rfs_lower_bounds).  Three k_seg_sort classes: lists
 // up to 4096 (512 threads) and 12288 (1024 threads) in shared memory, longer
 // ones with the same passes over global (L2-resident) ping-pong buffers.
+#include <cooperative_groups.h>
+
 #include "rfs_common.cuh"
 
 namespace {
@@ -28,7 +30,9 @@ namespace {
 constexpr int BK_MAX_TILES = 512;   // >= 23 x 12 (rfs_project caps the grid at 360 x 180)
 constexpr int BK_BLK = 256;         // Gaussians per fill block
 constexpr int BK_SEG_SMALL = 4096;  // tile lists sorted by 512-thread blocks
-constexpr int BK_SEG_MAX = 12288;   // longest tile list sorted in shared memory (1024 threads)
+constexpr int BK_SEG_MAX = 12288;   // longest tile list sorted in one block's shared memory (1024 threads)
+constexpr int BK_CL = 4;            // cluster of CTAs sorting one longer list in distributed shared memory
+constexpr int BK_SEG_CLUSTER = BK_CL * BK_SEG_MAX;  // longest tile list sorted by a cluster
 
 struct __align__(16) Rect {  // project.cu's splat rectangle
     short s1_lo, s1_hi, s2_hi, tv_lo, tv_hi, pad0, pad1, pad2;
@@ -344,6 +348,193 @@ __global__ void __launch_bounds__(NT) k_seg_sort(const int2* __restrict__ ranges
     }
 }
 
+// Tile lists of (BK_SEG_MAX, BK_CL * BK_SEG_MAX] entries (0.5M-1M-Gaussian
+// scenes): a thread-block cluster of BK_CL CTAs sorts one list in distributed
+// shared memory.  CTA c owns the contiguous slice [c S, (c + 1) S) of the
+// list (S = ceil(L / BK_CL) <= 12288, one round of 1024 x 12 items).  Per
+// 8-bit pass each CTA ranks its slice stably in registers (match_any +
+// per-warp counts, as k_seg_sort), scatters it locally into digit order, reads
+// the other CTAs' digit counts over DSMEM to find where digit d of its slice
+// starts in the whole list ((all digits < d) + (digit d of slices < c)), and
+// copies each digit run to the CTA(s) owning that range -- contiguous runs,
+// so the DSMEM stores coalesce; cluster barriers separate the passes.  The
+// emission bounds' suffix minimum crosses slices the same way.  Bitwise the
+// outputs of the single-block classes and of the radix path.
+__global__ void __launch_bounds__(1024) k_seg_sort_cluster(const int2* __restrict__ ranges, int lo,
+                                                           const uint32_t* __restrict__ bcodes,
+                                                           const uint32_t* __restrict__ bvals,
+                                                           const RfsGeom* __restrict__ geom,
+                                                           uint64_t* __restrict__ ckeys, uint32_t* __restrict__ vals,
+                                                           double* __restrict__ lb) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
+    namespace cg = cooperative_groups;
+    constexpr int NT = 1024, NW = NT / 32, ITEMS = 12, CAPL = BK_SEG_MAX;
+    static_assert(NT * ITEMS >= CAPL, "a slice is one round");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int tile = blockIdx.x / BK_CL, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int2 rg = ranges[tile];
+    const int L = rg.y - rg.x;
+    if (L <= lo || L > BK_CL * CAPL) return;  // another launch's class (uniform over the cluster)
+    const int S = (L + BK_CL - 1) / BK_CL;
+    const int s0 = rank * S, Ls = max(0, min(L, s0 + S) - s0);
+    uint32_t* k0 = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* v0 = k0 + CAPL;
+    uint32_t* k1 = v0 + CAPL;
+    uint32_t* v1 = k1 + CAPL;
+    __shared__ uint32_t cnt[256], loff[256], gbase[256], wsc[8];
+    __shared__ uint16_t wcnt[NW][256];
+    __shared__ double wmin[NW];
+    __shared__ double smin;
+    for (int i = tid; i < Ls; i += NT) {
+        k0[i] = bcodes[rg.x + s0 + i];
+        v0[i] = bvals[rg.x + s0 + i];
+    }
+    const unsigned lt = lanemask_lt();
+    uint32_t *sk = k0, *sv = v0, *dk = k1, *dv = v1;
+    __syncthreads();
+    for (int sh = 0; sh < 31; sh += 8) {
+        // 1. stable ranks of the slice in registers
+        for (int e = tid; e < NW * 256; e += NT) (&wcnt[0][0])[e] = 0;
+        __syncthreads();
+        uint32_t key[ITEMS], val[ITEMS], dig[ITEMS], rk[ITEMS];
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const int i = wid * 32 * ITEMS + j * 32 + lane;
+            const bool ok = i < Ls;
+            key[j] = ok ? sk[i] : 0u;
+            val[j] = ok ? sv[i] : 0u;
+            dig[j] = ok ? (key[j] >> sh) & 255u : 256u;
+            const unsigned peers = __match_any_sync(0xffffffffu, dig[j]);
+            const uint32_t cur = ok ? wcnt[wid][dig[j]] : 0u;
+            rk[j] = cur + __popc(peers & lt);
+            __syncwarp();
+            if (ok && (peers & lt) == 0) wcnt[wid][dig[j]] = (uint16_t)(cur + __popc(peers));
+            __syncwarp();
+        }
+        __syncthreads();
+        if (tid < 256) {  // per digit: exclusive scan over the warps, the slice count, its local start
+            uint32_t run = 0;
+#pragma unroll 4
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t x = wcnt[w][tid];
+                wcnt[w][tid] = (uint16_t)run;
+                run += x;
+            }
+            cnt[tid] = run;
+            loff[tid] = scan256_excl(run, wsc);
+        }
+        __syncthreads();
+        // 2. the slice in digit order, in place (every element is in registers)
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            if (dig[j] < 256u) {
+                const uint32_t dst = loff[dig[j]] + wcnt[wid][dig[j]] + rk[j];
+                sk[dst] = key[j];
+                sv[dst] = val[j];
+            }
+        }
+        cluster.sync();  // every slice's digit counts are final (and its digit-ordered copy)
+        // 3. where digit d of this slice starts in the whole list
+        if (tid < 256) {
+            uint32_t all = 0, before = 0;
+#pragma unroll
+            for (int c = 0; c < BK_CL; ++c) {
+                const uint32_t x = cluster.map_shared_rank(cnt, c)[tid];
+                all += x;
+                if (c < rank) before += x;
+            }
+            gbase[tid] = scan256_excl(all, wsc) + before;
+        }
+        __syncthreads();
+        // 4. digit runs to their owners: consecutive elements -> consecutive destinations
+        for (int i = tid; i < Ls; i += NT) {
+            const uint32_t k = sk[i], d = (k >> sh) & 255u;
+            const uint32_t dst = gbase[d] + ((uint32_t)i - loff[d]);
+            const int owner = (int)(dst / (uint32_t)S);
+            const uint32_t off = dst - (uint32_t)owner * (uint32_t)S;
+            cluster.map_shared_rank(dk, owner)[off] = k;
+            cluster.map_shared_rank(dv, owner)[off] = sv[i];
+        }
+        cluster.sync();  // every element of the pass has landed; counts read
+        uint32_t* t = sk;
+        sk = dk;
+        dk = t;
+        t = sv;
+        sv = dv;
+        dv = t;
+    }
+    // sorted compact keys (tile << 31 | depth code), Gaussian ids, lbv of this slice
+    const uint64_t th = (uint64_t)tile << 31;
+    double* sl = reinterpret_cast<double*>(dk);  // dk + dv: 8 B x CAPL
+    for (int i = tid; i < Ls; i += NT) {
+        const uint32_t g = sv[i];
+        ckeys[rg.x + s0 + i] = th | sk[i];
+        vals[rg.x + s0 + i] = g;
+        sl[i] = geom[g].lbv;
+    }
+    __syncthreads();
+    // lb[i] = min_{j >= i} lbv_j: runs within the slice as k_seg_sort, then
+    // the minimum of the later slices (DSMEM) folded in
+    const int E = (Ls + NT - 1) / NT;
+    const int i0 = tid * E, i1 = min(i0 + E, Ls);
+    double run = INFINITY;
+    for (int i = i1 - 1; i >= i0; --i) run = fmin(run, sl[i]);
+    double v = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = fmin(v, y);
+    }
+    if (lane == 0) wmin[wid] = v;
+    __syncthreads();
+    if (tid == 0) {
+        double m = INFINITY;
+        for (int w = 0; w < NW; ++w) m = fmin(m, wmin[w]);
+        smin = m;
+    }
+    cluster.sync();  // every slice's minimum is published
+    double later = INFINITY;
+    for (int c = rank + 1; c < BK_CL; ++c) later = fmin(later, *cluster.map_shared_rank(&smin, c));
+    double carry = __shfl_down_sync(0xffffffffu, v, 1);
+    if (lane == 31) carry = INFINITY;
+    for (int w = wid + 1; w < NW; ++w) carry = fmin(carry, wmin[w]);
+    carry = fmin(carry, later);
+    for (int i = i1 - 1; i >= i0; --i) {
+        carry = fmin(carry, sl[i]);
+        lb[rg.x + s0 + i] = carry;
+    }
+    cluster.sync();  // no CTA leaves while another may still read its shared memory
+}
+
+int launch_seg_sort_cluster(int n_tiles, const int* ranges, int lo, const uint32_t* bcodes, const uint32_t* bvals,
+                            const void* geom, uint64_t* ckeys, uint32_t* vals, double* lb, cudaStream_t st) {
+    static bool attr = false;
+    const size_t smem = (size_t)BK_SEG_MAX * 16;
+    if (!attr) {
+        RFS_CUDA_TRY(cudaFuncSetAttribute(k_seg_sort_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(n_tiles * BK_CL));
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[2];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = BK_CL;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 2;
+    RFS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_seg_sort_cluster, (const int2*)ranges, lo, bcodes, bvals,
+                                    (const RfsGeom*)geom, ckeys, vals, lb));
+    return RFS_OK;
+}
+
 template <int CAP, int NT>
 int launch_seg_sort(int n_tiles, const int* ranges, int lo, uint32_t* bcodes, uint32_t* bvals, uint32_t* altc,
                     uint32_t* altv, const void* geom, uint64_t* ckeys, uint32_t* vals, double* lb, cudaStream_t st) {
@@ -403,7 +594,9 @@ int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_a
     rc = launch_seg_sort<BK_SEG_MAX, 1024>(n_tiles, ranges, BK_SEG_SMALL, bcodes, bvals, altc, altv, geom, ckeys,
                                            vals, lb, st);
     if (rc != RFS_OK) return rc;
-    return launch_seg_sort<0, 1024>(n_tiles, ranges, BK_SEG_MAX, bcodes, bvals, altc, altv, geom, ckeys, vals, lb,
+    rc = launch_seg_sort_cluster(n_tiles, ranges, BK_SEG_MAX, bcodes, bvals, geom, ckeys, vals, lb, st);
+    if (rc != RFS_OK) return rc;
+    return launch_seg_sort<0, 1024>(n_tiles, ranges, BK_SEG_CLUSTER, bcodes, bvals, altc, altv, geom, ckeys, vals, lb,
                                     st);
 }
 

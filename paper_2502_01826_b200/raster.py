@@ -162,6 +162,12 @@ class Geometry:
 
 
 # adaptive capacities, remembered across steps
+# longest tile list the bucket path sorts in steady state: beyond one block's
+# shared memory (12288) the radix path is faster -- bucket.cu's 4-CTA cluster
+# class (DSMEM, up to 49152) and its global-memory class still serve the first
+# step of a scene (tile_max unknown); measured at 500k / 1M Gaussians:
+# bucket 382 / 761 us vs radix 270 / 477 us of binning
+BUCKET_MAX_LIST = 12288
 _CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {}, "used_cap": {},
          # tile-key sort of the hand-written backend: "bucket" (per-tile buckets,
          # bucket.cu) or "radix" (global onesweep)
@@ -404,10 +410,9 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
     # Read #1 (M) is skipped when a capacity from earlier steps is known: the
     # binning then runs on the device-side count and M is checked at read #2.
     m_cap = _CAPS.get("m_cap", {}).get((n, n_az, n_el)) if sort_backend == "hand" else None
-    # the buckets' global-memory class (tile lists > 12288) is correct but slower
-    # than the radix sort: scenes whose lists ran that long last time use the radix sort
+    # scenes whose tile lists ran longer than BUCKET_MAX_LIST last time use the radix sort
     bucket = (sort_backend == "hand" and _CAPS["tile_sort"] == "bucket"
-              and _CAPS["tile_max"].get((n, n_az, n_el), 0) <= 12288)
+              and _CAPS["tile_max"].get((n, n_az, n_el), 0) <= BUCKET_MAX_LIST)
     if m_cap is None:
         status_h.copy_(status, non_blocking=True)
         ev_m = torch.cuda.Event()

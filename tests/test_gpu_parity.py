@@ -283,7 +283,20 @@ def test_slow_path_bitwise_equals_ring_path():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("which", ["config1", "cube_", "special_", "hemi_", "bench20k", "bench100k", "bench500k"])
+def _cone_scene(n: int):
+    """n Gaussians within ~3 degrees of one direction: a few tile lists of ~n
+    entries (beyond the 4-CTA cluster class: the global-memory passes)."""
+    rng = np.random.default_rng(11)
+    s = bench_scene(rng, n, 360, 180)
+    d = rng.uniform(3.0, 15.0, n)
+    az = np.deg2rad(40.0 + rng.uniform(-1.5, 1.5, n))
+    el = np.deg2rad(-20.0 + rng.uniform(-1.5, 1.5, n))
+    s.means = np.stack([d * np.cos(el) * np.cos(az), d * np.cos(el) * np.sin(az), d * np.sin(el)], axis=1)
+    return round_to_f32(s)
+
+
+@pytest.mark.parametrize("which", ["config1", "cube_", "special_", "hemi_", "bench20k", "bench100k", "bench500k",
+                                   "bench1000k", "cone60k"])
 def test_bucket_binning_bitwise_equals_radix(which):
     """bucket.cu (per-tile buckets sorted in shared memory) must give bitwise
     the sorted keys, ids, ranges and emission bounds of the radix-sort path
@@ -294,8 +307,10 @@ def test_bucket_binning_bitwise_equals_radix(which):
         s = config1_scene()
     elif which.endswith("_"):
         s = scene_from(load("edge_scenes.npz"), which)
-    else:  # bench500k: tile lists beyond the shared-memory classes (global-memory passes)
-        n = {"bench20k": 20_000, "bench100k": 100_000, "bench500k": 500_000}[which]
+    elif which == "cone60k":
+        s = _cone_scene(60_000)
+    else:  # bench500k / 1000k: tile lists beyond one block (the 4-CTA cluster class)
+        n = {"bench20k": 20_000, "bench100k": 100_000, "bench500k": 500_000, "bench1000k": 1_000_000}[which]
         s = round_to_f32(bench_scene(np.random.default_rng(7), n, 360, 180))
     ds = raster.DeviceScene.from_host(s, "cuda")
     tx = torch.as_tensor(default_txs(2, seed=9), dtype=torch.float32, device="cuda")
@@ -314,9 +329,11 @@ def test_bucket_binning_bitwise_equals_radix(which):
         raster._CAPS.update(saved)
     for a, b in zip(out["radix"], out["bucket"]):
         np.testing.assert_array_equal(a, b)
-    if which == "bench500k":
-        rg = out["bucket"][2]
-        assert (rg[:, 1] - rg[:, 0]).max() > 12288
+    rg = out["bucket"][2]
+    if which in ("bench500k", "bench1000k"):
+        assert 12288 < (rg[:, 1] - rg[:, 0]).max() <= 4 * 12288  # the cluster class
+    if which == "cone60k":
+        assert (rg[:, 1] - rg[:, 0]).max() > 4 * 12288  # the global-memory class
 
 
 def _huge_gaussian_scene():
