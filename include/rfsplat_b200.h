@@ -251,7 +251,13 @@ int rfs_grad_tx(int cap, const uint32_t* n_used, const uint32_t* order, int n, c
 size_t rfs_loss_scratch_bytes(int n_frames, int n_az, int n_el);
 int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const float* pred, const float* gt,
                       double w_ssim, double w_fourier, double* report, float* grad, void* lam, void* lamT, void* scratch,
-                      size_t scratch_bytes, void* stream);
+                      size_t scratch_bytes, const void* gt_range, void* stream);
+/* The per-frame (min, max) partials of the ground truth (SSIM's dynamic range,
+ * loss.py:108): float2[rfs_frame_range_elems(B)]; rfs_spectrum_loss computes
+ * them itself when gt_range is NULL, or takes them precomputed -- e.g. on the
+ * copy stream right behind the frames' H2D copy, off the critical path. */
+size_t rfs_frame_range_elems(int n_frames);
+int rfs_frame_range(int n_frames, int n_az, int n_el, const float* gt, void* range, void* stream);
 
 /* Scalar (single-antenna) modes: total_b = sum_r S[b][r] (render_scalar,
  * render.py:301-307) and scalar_loss (loss.py:158-180) per frame; mode 0

@@ -61,7 +61,9 @@ _SIGS = {
                             vp, vp, vp, vp, vp, vp, vp, vp, i32, vp]),
     "rfs_grad_tx": (i32, [i32, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
     "rfs_loss_scratch_bytes": (sz, [i32, i32, i32]),
-    "rfs_spectrum_loss": (i32, [i32, i32, i32, vp, vp, vp, f64, f64, vp, vp, vp, vp, vp, sz, vp]),
+    "rfs_spectrum_loss": (i32, [i32, i32, i32, vp, vp, vp, f64, f64, vp, vp, vp, vp, vp, sz, vp, vp]),
+    "rfs_frame_range_elems": (sz, [i32]),
+    "rfs_frame_range": (i32, [i32, i32, i32, vp, vp, vp]),
     "rfs_scalar_loss": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),
     "rfs_sgd_step": (i32, [i32, i32, vp, C.c_float, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rfs_density_flags": (i32, [i32, i32, vp, vp, vp, f64, f64, f64, vp, vp, vp, vp]),
@@ -109,7 +111,7 @@ KERNELS_PER_CALL = {
     "rfs_tile_ranges": 1, "rfs_lower_bounds": 1, "rfs_bin_bucket": 7, "rfs_hits": 3, "rfs_hits_slow": 1, "rfs_psi": 1,
     "rfs_forward": 1, "rfs_lam_transpose": 1, "rfs_bwd_gauss": 1, "rfs_bwd_rays": 1, "rfs_hit_keys": 1, "rfs_gauss_ranges": 1, "rfs_used_list": 1, "rfs_grad_geom": 0,
     "rfs_grad_tx": 1, "rfs_gather_sorted": 1,
-    "rfs_ray_dirs": 1, "rfs_spectrum_loss": 4, "rfs_sgd_step": 2, "rfs_scalar_loss": 1, "rfs_density_flags": 1,
+    "rfs_ray_dirs": 1, "rfs_spectrum_loss": 4, "rfs_frame_range": 1, "rfs_sgd_step": 2, "rfs_scalar_loss": 1, "rfs_density_flags": 1,
     "rfs_density_apply": 1, "rfs_spectrum_dataset": 2, "rfs_scalar_dataset": 1,
 }
 launch_counter = {"kernels": 0}

@@ -410,18 +410,20 @@ def train_step_host(ds: raster.DeviceScene, tx_host: torch.Tensor, gt_host: torc
         tx_ready = torch.cuda.Event()
         tx_ready.record(cs)
         gt = gt_host.to(dev, non_blocking=True)
+        gt_rng = _loss.frame_range(gt)  # SSIM's dynamic range, off the critical path
         gt_ready = torch.cuda.Event()
         gt_ready.record(cs)
     raster._keep(tx, main)
     raster._keep(gt, main)
+    raster._keep(gt_rng, main)
     main.wait_event(tx_ready)
 
     def loss_and_upstream(S):  # queued behind the geometry's hit-statistics read
         main.wait_event(gt_ready)
         if S.shape[0] <= raster.MAX_TX_PER_LAUNCH:  # the loss writes the backward's ray-major layout
-            rep, lamT, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier, lam_layout="rays")
+            rep, lamT, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier, lam_layout="rays", gt_range=gt_rng)
             return rep, None, lamT
-        rep, lam, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier)
+        rep, lam, _ = _loss.spectrum_loss_frames(S, gt, w_ssim, w_fourier, gt_range=gt_rng)
         return rep, lam, None
 
     geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True, forward=True,

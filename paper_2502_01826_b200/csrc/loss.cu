@@ -498,9 +498,18 @@ size_t rfs_loss_scratch_bytes(int n_frames, int n_az, int n_el) {
            (size_t)n_frames * RCH * sizeof(float2) + 256;
 }
 
+size_t rfs_frame_range_elems(int n_frames) { return (size_t)(n_frames > 0 ? n_frames : 0) * RCH; }
+
+int rfs_frame_range(int n_frames, int n_az, int n_el, const float* gt, void* range, void* stream) {
+    if (n_frames <= 0 || n_az <= 0 || n_el <= 0) return RFS_OK;
+    rfs_launch(k_frame_range, dim3(RCH, n_frames), 256, 0, (cudaStream_t)stream, gt, n_az * n_el, (float2*)range);
+    RFS_LAUNCH_CHECK();
+    return RFS_OK;
+}
+
 int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const float* pred, const float* gt,
                       double w_ssim, double w_fourier, double* report, float* grad, void* lam, void* lamT, void* scratch,
-                      size_t scratch_bytes, void* stream) {
+                      size_t scratch_bytes, const void* gt_range, void* stream) {
     if (n_frames <= 0 || n_az <= 0 || n_el <= 0) return RFS_OK;
     if ((S == nullptr && pred == nullptr) || ((lam != nullptr || lamT != nullptr) && S == nullptr))
         return RFS_ERR_CONTRACT;
@@ -518,8 +527,12 @@ int rfs_spectrum_loss(int n_frames, int n_az, int n_el, const void* S, const flo
     p += (size_t)nblk * n_frames * 3 * sizeof(double);
     float2* range = (float2*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
     const double w1 = 1.0 - w_ssim - w_fourier;
-    rfs_launch(k_frame_range, dim3(RCH, n_frames), 256, 0, st, gt, (int)R, range);
-    rfs_launch(k_ssim_fwd, grid, LT, sizeof(FwdSmem), st, (const float2*)S, pred, gt, range, n_az, n_el, maps, part);
+    if (gt_range == nullptr)
+        rfs_launch(k_frame_range, dim3(RCH, n_frames), 256, 0, st, gt, (int)R, range);
+    else
+        range = (float2*)gt_range;  // precomputed (rfs_frame_range, e.g. right behind the frames' H2D copy)
+    rfs_launch(k_ssim_fwd, grid, LT, sizeof(FwdSmem), st, (const float2*)S, pred, gt, (const float2*)range, n_az, n_el,
+               maps, part);
     rfs_launch(k_ssim_bwd, grid, LT, sizeof(BwdSmem), st, (const float2*)S, pred, gt, maps, n_az, n_el, (float)w1,
                                                   (float)w_ssim, (float)w_fourier, grad, (float2*)lam,
                                                   (float2*)lamT);

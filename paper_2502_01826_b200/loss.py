@@ -40,9 +40,21 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+def frame_range(gt: torch.Tensor) -> torch.Tensor:
+    """Per-frame (min, max) partials of measured power frames gt [B, n_az, n_el]
+    (float32, on the device): SSIM's dynamic range (loss.py:108), computed
+    ahead of the loss, e.g. right behind the frames' H2D copy on its stream;
+    pass it to spectrum_loss_frames(gt_range=...)."""
+    b, n_az, n_el = (int(x) for x in gt.shape)
+    lib = _native.load()
+    out = torch.empty(2 * int(lib.rfs_frame_range_elems(b)), dtype=torch.float32, device=gt.device)
+    _native.call("rfs_frame_range", b, n_az, n_el, _ptr(gt), _ptr(out), torch.cuda.current_stream(gt.device).cuda_stream)
+    return out
+
+
 def spectrum_loss_frames(S: torch.Tensor | None, gt: torch.Tensor, w_ssim: float = 0.2, w_fourier: float = 0.2,
                          pred: torch.Tensor | None = None, want_lam: bool = True, want_grad: bool = False,
-                         lam_layout: str = "frames"):
+                         lam_layout: str = "frames", gt_range: torch.Tensor | None = None):
     """Loss of B frames on the device.
 
     S: complex64 [B, n_az, n_el] (the predicted power is |S|^2) or None with
@@ -51,7 +63,8 @@ def spectrum_loss_frames(S: torch.Tensor | None, gt: torch.Tensor, w_ssim: float
     lam or None, grad float32 [B, n_az, n_el] or None).  lam is complex64
     [B, n_az, n_el] (lam_layout "frames"), or [n_az*n_el, B] ("rays": the
     backward's layout, raster.backward(lamT=...), written directly by the
-    loss kernel -- no transpose pass).
+    loss kernel -- no transpose pass).  `gt_range` (optional): frame_range(gt),
+    precomputed.
     """
     if lam_layout not in ("frames", "rays"):
         raise ValueError("lam_layout must be 'frames' or 'rays'")
@@ -85,7 +98,7 @@ def spectrum_loss_frames(S: torch.Tensor | None, gt: torch.Tensor, w_ssim: float
     scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     _native.call("rfs_spectrum_loss", b, n_az, n_el, _ptr(S), _ptr(pred), _ptr(gt), float(w_ssim), float(w_fourier),
                  _ptr(report), _ptr(grad), None if rays else _ptr(lam), _ptr(lam) if rays else None, _ptr(scratch),
-                 nbytes, torch.cuda.current_stream(dev).cuda_stream)
+                 nbytes, _ptr(gt_range), torch.cuda.current_stream(dev).cuda_stream)
     return report, lam, grad
 
 
