@@ -152,22 +152,43 @@ __global__ void __launch_bounds__(256) k_geom_seg(
 // ones) in group order.
 constexpr int FIX_SHORT = 4;
 
-// chain_cov_to_shape for one Gaussian (grad.py:123-164), fp64.
-__device__ void cov_to_shape(const float* q4, const float* s3, const double* dcv, float* dq, float* ds) {
-    double q[4] = {q4[0], q4[1], q4[2], q4[3]};
-    double nrm = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-    double qu[4] = {q[0] / nrm, q[1] / nrm, q[2] / nrm, q[3] / nrm};
-    double n2 = sqrt(qu[0] * qu[0] + qu[1] * qu[1] + qu[2] * qu[2] + qu[3] * qu[3]);
+// chain_cov_to_shape for one Gaussian (grad.py:123-164), fp64, in closed
+// form: with D = diag(e^{2s}) and Sigma = R D R^T,
+//   d log_scale_a = 2 D_aa (R^T dSigma R)_aa,
+//   dq_k = <dSigma, dR_k D R^T + R D dR_k^T> = sum_ij (dR_k)_ij M_ij,
+//   M = (dSigma + dSigma^T) R D,
+// then projected through the quaternion normalisation (grad.py:160-164) --
+// the reference's triple loops (grad.py:134-158) regrouped, every array in
+// registers.
+__device__ __forceinline__ void cov_to_shape(const float* q4, const float* s3, const double* dcv, float* dq,
+                                             float* ds) {
+    const double q0 = q4[0], q1 = q4[1], q2 = q4[2], q3 = q4[3];
+    const double nrm = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    const double qu[4] = {q0 / nrm, q1 / nrm, q2 / nrm, q3 / nrm};
+    const double n2 = sqrt(qu[0] * qu[0] + qu[1] * qu[1] + qu[2] * qu[2] + qu[3] * qu[3]);
     double w = qu[0] / n2, x = qu[1] / n2, y = qu[2] / n2, z = qu[3] / n2;
-    double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
-                   2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
-                   2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
-    double dv[3] = {exp(2.0 * (double)s3[0]), exp(2.0 * (double)s3[1]), exp(2.0 * (double)s3[2])};
-#pragma unroll 1
+    const double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                         2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                         2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    const double dv[3] = {exp(2.0 * (double)s3[0]), exp(2.0 * (double)s3[1]), exp(2.0 * (double)s3[2])};
+    // T = dSigma R (for the scales), Ssym = dSigma + dSigma^T, M = Ssym R D
+    double T[9], M[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            double t = 0.0, m = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                t += dcv[3 * i + k] * R[3 * k + j];
+                m += (dcv[3 * i + k] + dcv[3 * k + i]) * R[3 * k + j];
+            }
+            T[3 * i + j] = t;
+            M[3 * i + j] = m * dv[j];
+        }
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
-        double s = 0.0;
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) s += R[3 * i + a] * dcv[3 * i + j] * R[3 * j + a];
+        const double s = R[a] * T[a] + R[3 + a] * T[3 + a] + R[6 + a] * T[6 + a];  // (R^T dSigma R)_aa
         ds[a] = (float)(2.0 * dv[a] * s);
     }
     w = qu[0]; x = qu[1]; y = qu[2]; z = qu[3];
@@ -177,22 +198,16 @@ __device__ void cov_to_shape(const float* q4, const float* s3, const double* dcv
                              {-4 * y, 2 * x, 2 * w, 2 * x, 0, 2 * z, -2 * w, 2 * z, -4 * y},
                              {-4 * z, -2 * w, 2 * x, 2 * w, -4 * z, 2 * y, 2 * x, 2 * y, 0}};
     double gq[4];
-#pragma unroll 1
-    for (int qi = 0; qi < 4; ++qi) {
-        double s = 0.0;
-        for (int i = 0; i < 3; ++i)
-            for (int k = 0; k < 3; ++k) {
-                double s1 = 0.0, s2 = 0.0;
-                for (int j = 0; j < 3; ++j) {
-                    s1 += dr[qi][3 * i + j] * dv[j] * R[3 * k + j];
-                    s2 += R[3 * i + j] * dv[j] * dr[qi][3 * k + j];
-                }
-                s += dcv[3 * i + k] * (s1 + s2);
-            }
-        gq[qi] = s;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double g = 0.0;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) g += dr[k][e] * M[e];
+        gq[k] = g;
     }
-    double dot = gq[0] * qu[0] + gq[1] * qu[1] + gq[2] * qu[2] + gq[3] * qu[3];
-    for (int qi = 0; qi < 4; ++qi) dq[qi] = (float)((gq[qi] - dot * qu[qi]) / nrm);
+    const double dot = gq[0] * qu[0] + gq[1] * qu[1] + gq[2] * qu[2] + gq[3] * qu[3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dq[k] = (float)((gq[k] - dot * qu[k]) / nrm);
 }
 
 // ------------------------------------------------------------------ K9c
