@@ -211,7 +211,9 @@ int rfs_bwd_rays(const void* slab, const int* counts, int hcap, int n_rays, cons
  * Stage 2 walks the Gaussians with live hits, order[i] for i < min(used_cap,
  * *n_used) (rfs_used_list; n_used nullable), and zeroes every output row
  * of the others.
- * Scratch: acc64 f64[N*14], part_g i32[rfs_geom_part_elems(H)],
+ * Scratch: acc64 f64[N*14], long_list i32[rfs_geom_part_elems(H)] ([0] =
+ * count of the Gaussians whose hits span more than 16 groups of 32, then
+ * their ids; stage 1 fills it, stage 2 sums them a block each),
  * part_v f64[14*rfs_geom_part_elems(H)].  stage (bit mask): 1 = the per-hit
  * sums (K9a), 2 = the per-Gaussian chains (K9c) -- so only K9c has to wait
  * for rfs_grad_tx's dm_dir when that runs on another stream. */
@@ -220,7 +222,7 @@ int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sort
                   const uint32_t* s_slot, const void* gs, const int* g_rng, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   int used_cap, const uint32_t* n_used, const uint32_t* order,
-                  double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
+                  double* acc64, int* long_list, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
                   int stage, void* stream);
 
@@ -278,7 +280,9 @@ int rfs_scalar_loss(int n_frames, int n_rays, int mode, const void* S, const voi
  *   0x7f7f7f7f7f7f7f7f if none -- in which case nothing is updated; prior
  *   (nullable, device i64): the first bad value of earlier steps -- a value
  *   other than the sentinel skips the update too (a training loop that checks
- *   only at its sync points leaves the scene as of its last good step).
+ *   only at its sync points leaves the scene as of its last good step);
+ *   lr_mean_dev (nullable, device f32): replaces lrs[0] -- a graph-captured
+ *   training iteration reads the schedule's value for its iteration there.
  * rfs_density_flags: mode 0 densify (keep = !split, clone, split: grad_ema >
  *   thr_grad, radius = trace(Sigma)/3 > thr_radius splits), mode 1 prune
  *   (keep = sigmoid(raw) >= thr_prune); u32 flags per Gaussian.
@@ -293,7 +297,7 @@ int rfs_sgd_step(int n, int K, const float* lrs, float ema_decay, const float* d
                  const float* d_log_scale, const float* d_trans_mag, const float* d_trans_phase, const void* d_coeffs,
                  float* means, float* quats, float* log_scales, float* trans_mag_raw, float* trans_phase,
                  void* coeffs, float* grad_ema, float* last_dmean, long long* bad,
-                 const long long* prior, void* stream);
+                 const long long* prior, const float* lr_mean_dev, void* stream);
 int rfs_density_flags(int n, int mode, const float* grad_ema, const float* log_scales, const float* trans_mag_raw,
                       double thr_grad, double thr_radius, double thr_prune, uint32_t* keep, uint32_t* clone,
                       uint32_t* split, void* stream);

@@ -65,7 +65,7 @@ _SIGS = {
     "rfs_frame_range_elems": (sz, [i32]),
     "rfs_frame_range": (i32, [i32, i32, i32, vp, vp, vp]),
     "rfs_scalar_loss": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp]),
-    "rfs_sgd_step": (i32, [i32, i32, vp, C.c_float, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "rfs_sgd_step": (i32, [i32, i32, vp, C.c_float, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rfs_density_flags": (i32, [i32, i32, vp, vp, vp, f64, f64, f64, vp, vp, vp, vp]),
     "rfs_density_apply": (i32, [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_ulonglong, i32,
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

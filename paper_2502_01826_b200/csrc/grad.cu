@@ -5,10 +5,11 @@
 //     the TX-reduced weight gradient GW_k of K8r, plus d|rho| and d(phase);
 //     each warp sums its runs of equal Gaussian id through shared memory
 //     (one lane per (run, value)).  Gaussians whose hits straddle warps
-//     leave per-warp partials that
-//     K9c adds them in group order -- so every sum has a fixed order (the
-//     slot order of the reference's bincount, grad.py:243-254): deterministic.
-// K9c k_geom_final (lane per Gaussian with hits, fp64): d_mean direct term, d_cov,
+//     leave per-warp partials that K9c adds in a fixed order (lanes over the
+//     groups, then a fixed butterfly) -- deterministic; within a group the
+//     slot order of the reference's bincount (grad.py:243-254).
+// K9c k_geom_span (warp per straddling Gaussian: its group partials) + k_geom_final
+//     (lane per Gaussian with hits, fp64): d_mean direct term, d_cov,
 //     d|rho|, d(phase), chain_cov_to_shape (grad.py:134-164) and
 //     d_trans_mag_raw = d|rho| sigma (1 - sigma) (train.py:161-162).
 // K9b k_grad_tx (warp per Gaussian, lanes over TX; runs right after K8c):
@@ -25,6 +26,7 @@ namespace {
 constexpr int NACC = 14;         // dmu[3], dcov[9], d|rho|, d(phase)
 constexpr int GB_THREADS = 128;
 constexpr int GB_MAXJ = 8;       // up to 256 TX per launch
+constexpr int FIX_SHORT = 16;    // straddle spans up to this many 32-hit groups: summed inline by K9c
 
 // ------------------------------------------------------------------ K9a
 __global__ void __launch_bounds__(256) k_geom_seg(
@@ -32,7 +34,7 @@ __global__ void __launch_bounds__(256) k_geom_seg(
     const float* __restrict__ s_w,
     const uint32_t* __restrict__ s_slot, const float4* __restrict__ gs, const RfsGeom* __restrict__ geom, const double* __restrict__ dirs,
     const int2* __restrict__ g_rng, double rx0, double rx1, double rx2, double min_t, double* __restrict__ acc64,
-    int* __restrict__ part_g, double* __restrict__ part_v) {
+    int* __restrict__ long_list, double* __restrict__ part_v) {
     rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     if (h_dev) h = min(h, (int)*h_dev);
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -136,13 +138,14 @@ __global__ void __launch_bounds__(256) k_geom_seg(
             continue;
         }
         // straddling segment: partial of this warp's first (slot 0) or last (slot 1) segment
-        if (h0 < wb) {
-            if (i == 0) part_g[2 * wglob] = gk;
-            part_v[(size_t)(2 * wglob) * NACC + i] = sum;
-        }
+        if (h0 < wb) part_v[(size_t)(2 * wglob) * NACC + i] = sum;
         if (h1 - 1 > wb + 31) {
-            if (i == 0) part_g[2 * wglob + 1] = gk;
             part_v[(size_t)(2 * wglob + 1) * NACC + i] = sum;
+            // the warp holding a long Gaussian's first hit lists it for k_geom_span
+            if (i == 0 && h0 >= wb && ((h1 - 1) >> 5) - (h0 >> 5) + 1 > FIX_SHORT) {
+                const int q = atomicAdd(long_list, 1);
+                long_list[1 + q] = gk;
+            }
         }
     }
 }
@@ -150,7 +153,6 @@ __global__ void __launch_bounds__(256) k_geom_seg(
 // Gaussians whose hits straddle warps: k_geom_final adds the group partials
 // (slot 2w+1 of the group where the Gaussian starts, slot 2v of the later
 // ones) in group order.
-constexpr int FIX_SHORT = 4;
 
 // chain_cov_to_shape for one Gaussian (grad.py:123-164), fp64, in closed
 // form: with D = diag(e^{2s}) and Sigma = R D R^T,
@@ -211,14 +213,54 @@ __device__ __forceinline__ void cov_to_shape(const float* q4, const float* s3, c
 }
 
 // ------------------------------------------------------------------ K9c
-// Lane per Gaussian with live hits (order[i], i < min(cap, *n_used)): its 14
-// sums -- from acc64 when its hits lie in one 32-hit group, else the group
-// partials of k_geom_seg added in group order (spans of up to FIX_SHORT groups
-// by the lane, longer ones by the whole warp, lane-strided plus a fixed
-// butterfly: the straddle fix-up folded into this kernel) -- then the direct
-// d_mean term + K9b's bearing chain, d_cov, d|rho|, d(phase), d_trans_mag_raw
-// and chain_cov_to_shape in fp64.  A grid-stride loop then zeroes the rows of
-// the Gaussians without hits.  Every sum has a fixed order: deterministic.
+// k_geom_span: a block per long Gaussian (hits over more than FIX_SHORT
+// 32-hit groups; k_geom_seg lists them, long_list[0] = count): its 14 sums
+// from the group partials (slot 2w0+1 of the first group, slot 2v of the
+// later ones), threads over the groups, then a fixed butterfly per warp and
+// the 8 warp totals added in warp order (deterministic), into its acc64 row.
+// A Gaussian covering thousands of rays (the 360x180 grids: up to 640
+// groups) costs ceil(W/256) loads per thread.
+__global__ void __launch_bounds__(256) k_geom_span(const int* __restrict__ long_list, const int2* __restrict__ g_rng,
+                                                   const double* __restrict__ part_v, double* __restrict__ acc64) {
+    rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
+    __shared__ double s_w[8][NACC];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int nl = long_list[0];
+    for (int b = blockIdx.x; b < nl; b += gridDim.x) {
+        const int g = long_list[1 + b];
+        const int2 rg = g_rng[g];
+        const int w0 = rg.x >> 5, w1 = (rg.y - 1) >> 5;
+        double t[NACC];
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) t[k] = 0.0;
+        for (int v = w0 + threadIdx.x; v <= w1; v += 256) {
+            const double* src = part_v + (size_t)(v == w0 ? 2 * w0 + 1 : 2 * v) * NACC;
+#pragma unroll
+            for (int k = 0; k < NACC; ++k) t[k] += src[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) {
+            double x = t[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            if (lane == 0) s_w[wl][k] = x;
+        }
+        __syncthreads();
+        if (threadIdx.x < NACC) {
+            double x = s_w[0][threadIdx.x];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) x += s_w[w][threadIdx.x];
+            acc64[(size_t)g * NACC + threadIdx.x] = x;
+        }
+        __syncthreads();
+    }
+}
+
+// k_geom_final: lane per Gaussian with live hits (order[i], i < min(cap,
+// *n_used)): its 14 sums (acc64, or a short straddle's group partials), the direct d_mean term + K9b's bearing
+// chain, d_cov, d|rho|, d(phase), d_trans_mag_raw and chain_cov_to_shape in
+// fp64.  A grid-stride loop then zeroes the rows of the Gaussians without
+// hits.  Every sum has a fixed order: deterministic.
 __global__ void __launch_bounds__(128) k_geom_final(
     int cap, const uint32_t* __restrict__ n_used, const uint32_t* __restrict__ order, int n,
     const double* __restrict__ acc64, const double* __restrict__ part_v, const float* __restrict__ quats,
@@ -227,20 +269,17 @@ __global__ void __launch_bounds__(128) k_geom_final(
     float* __restrict__ d_mag_raw, float* __restrict__ d_phase, float* __restrict__ d_cov,
     const float* __restrict__ dm_dir, const int2* __restrict__ g_rng) {
     rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-    __shared__ double s_long[128 / 32][NACC];
-    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int m = n_used ? min(cap, (int)*n_used) : cap;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (((i >> 5) << 5) < m) {  // warps with at least one used Gaussian
-        const bool on = i < m;
-        const int g = on ? (int)order[i] : 0;
-        const int2 rg = on ? g_rng[g] : make_int2(0, 1);
+    if (i < m) {
+        const int g = (int)order[i];
+        const int2 rg = g_rng[g];
         const int w0 = rg.x >> 5, w1 = (rg.y - 1) >> 5;
         double a[NACC];
-        if (on && w0 == w1) {
+        if (w0 == w1 || w1 - w0 + 1 > FIX_SHORT) {  // one group, or summed by k_geom_span
 #pragma unroll
             for (int k = 0; k < NACC; ++k) a[k] = acc64[(size_t)g * NACC + k];
-        } else if (on && w1 - w0 + 1 <= FIX_SHORT) {
+        } else {  // a short straddle: the group partials in group order
 #pragma unroll
             for (int k = 0; k < NACC; ++k) a[k] = part_v[(size_t)(2 * w0 + 1) * NACC + k];
             for (int v = w0 + 1; v <= w1; ++v) {
@@ -248,48 +287,19 @@ __global__ void __launch_bounds__(128) k_geom_final(
                 for (int k = 0; k < NACC; ++k) a[k] += part_v[(size_t)(2 * v) * NACC + k];
             }
         }
-        unsigned longs = __ballot_sync(0xffffffffu, on && w1 - w0 + 1 > FIX_SHORT);
-        while (longs) {
-            const int src = __ffs(longs) - 1;
-            longs &= longs - 1;
-            const int gw = __shfl_sync(0xffffffffu, w0, src), gw1 = __shfl_sync(0xffffffffu, w1, src);
-            double t[NACC];
+        // direct term + the bearing chain of K9b (which ran before)
+        d_mean[3 * g + 0] = (float)a[0] + (dm_dir ? dm_dir[3 * g + 0] : 0.f);
+        d_mean[3 * g + 1] = (float)a[1] + (dm_dir ? dm_dir[3 * g + 1] : 0.f);
+        d_mean[3 * g + 2] = (float)a[2] + (dm_dir ? dm_dir[3 * g + 2] : 0.f);
+        d_mag[g] = (float)a[12];
+        const float sg = 1.f / (1.f + expf(-raw[g]));
+        d_mag_raw[g] = (float)a[12] * sg * (1.f - sg);
+        d_phase[g] = (float)a[13];
+        if (d_cov) {
 #pragma unroll
-            for (int k = 0; k < NACC; ++k) t[k] = 0.0;
-            for (int v = gw + lane; v <= gw1; v += 32) {
-                const size_t slot = v == gw ? (size_t)(2 * gw + 1) : (size_t)(2 * v);
-#pragma unroll
-                for (int k = 0; k < NACC; ++k) t[k] += part_v[slot * NACC + k];
-            }
-#pragma unroll
-            for (int k = 0; k < NACC; ++k) {
-                double x = t[k];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-                if (lane == 0) s_long[wl][k] = x;
-            }
-            __syncwarp();
-            if (lane == src) {
-#pragma unroll
-                for (int k = 0; k < NACC; ++k) a[k] = s_long[wl][k];
-            }
-            __syncwarp();
+            for (int k = 0; k < 9; ++k) d_cov[9 * g + k] = (float)a[3 + k];
         }
-        if (on) {
-            // direct term + the bearing chain of K9b (which ran before)
-            d_mean[3 * g + 0] = (float)a[0] + (dm_dir ? dm_dir[3 * g + 0] : 0.f);
-            d_mean[3 * g + 1] = (float)a[1] + (dm_dir ? dm_dir[3 * g + 1] : 0.f);
-            d_mean[3 * g + 2] = (float)a[2] + (dm_dir ? dm_dir[3 * g + 2] : 0.f);
-            d_mag[g] = (float)a[12];
-            const float sg = 1.f / (1.f + expf(-raw[g]));
-            d_mag_raw[g] = (float)a[12] * sg * (1.f - sg);
-            d_phase[g] = (float)a[13];
-            if (d_cov) {
-#pragma unroll
-                for (int k = 0; k < 9; ++k) d_cov[9 * g + k] = (float)a[3 + k];
-            }
-            cov_to_shape(quats + 4 * g, log_scales + 3 * g, a + 3, d_quat + 4 * g, d_log_scale + 3 * g);
-        }
+        cov_to_shape(quats + 4 * g, log_scales + 3 * g, a + 3, d_quat + 4 * g, d_log_scale + 3 * g);
     }
     // Gaussians without live hits (most): every term is zero
     for (int g = i; g < n; g += gridDim.x * blockDim.x) {
@@ -490,7 +500,7 @@ int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sort
                   const uint32_t* s_slot, const void* gs, const int* g_rng, const void* geom, const double* dirs, const double* rx,
                   double ress_radius, const float* quats, const float* log_scales, const float* trans_mag_raw,
                   int used_cap, const uint32_t* n_used, const uint32_t* order,
-                  double* acc64, int* part_g, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
+                  double* acc64, int* long_list, double* part_v, float* d_mean, float* d_quat, float* d_log_scale,
                   float* d_trans_mag, float* d_trans_mag_raw, float* d_trans_phase, float* d_cov, const float* dm_dir,
                   int stage, void* stream) {
     if (n <= 0) return RFS_OK;
@@ -498,18 +508,20 @@ int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sort
     const int2* rg = (const int2*)g_rng;
     // acc64 rows / part_v slots are all written by k_geom_seg before k_geom_final
     // reads them (g_rng says which), so no clearing pass
+    if (stage & 1) RFS_CUDA_TRY(cudaMemsetAsync(long_list, 0, sizeof(int), st));  // the long-Gaussian count
     if ((stage & 1) && n_hits > 0)
-        rfs_launch(k_geom_seg, rfs_ceil_div(n_hits, 256), 256, 0, st, n_hits, h_dev, sorted_g, s_ray, s_w, s_slot, (const float4*)gs,
-                                                               (const RfsGeom*)geom, dirs, rg, rx[0], rx[1], rx[2],
-                                                               ress_radius, acc64, part_g, part_v);
+        rfs_launch(k_geom_seg, rfs_ceil_div(n_hits, 256), 256, 0, st, n_hits, h_dev, sorted_g, s_ray, s_w, s_slot,
+                   (const float4*)gs, (const RfsGeom*)geom, dirs, rg, rx[0], rx[1], rx[2], ress_radius, acc64, long_list,
+                   part_v);
     if (stage & 2) {
         if (order == nullptr) return RFS_ERR_CONTRACT;
-        const long long threads = std::max<long long>(used_cap, 1);
-        const unsigned grid = (unsigned)std::max<long long>(rfs_ceil_div(threads, 128),
+        rfs_launch(k_geom_span, 148 * 2, 256, 0, st, (const int*)long_list, rg, (const double*)part_v, acc64);
+        const long long ucap = std::max(used_cap, 1);
+        const unsigned grid = (unsigned)std::max<long long>(rfs_ceil_div(ucap, 128),
                                                             std::min<long long>(rfs_ceil_div(n, 128), 148LL * 8));
-        rfs_launch(k_geom_final, grid, 128, 0, st, used_cap, n_used, order, n, acc64, part_v, quats, log_scales, trans_mag_raw,
-                                          d_mean, d_quat, d_log_scale, d_trans_mag, d_trans_mag_raw, d_trans_phase,
-                                          d_cov, dm_dir, rg);
+        rfs_launch(k_geom_final, grid, 128, 0, st, used_cap, n_used, order, n, (const double*)acc64,
+                   (const double*)part_v, quats, log_scales, trans_mag_raw, d_mean, d_quat, d_log_scale, d_trans_mag,
+                   d_trans_mag_raw, d_trans_phase, d_cov, dm_dir, rg);
     }
     RFS_LAUNCH_CHECK();
     return RFS_OK;

@@ -68,16 +68,22 @@ __global__ void k_sgd_check(int n, int K, const float* __restrict__ d_mean, cons
                             long long* __restrict__ bad) {
     rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    // class order of _check_finite (train.py:133-142)
-    int cls = -1;
-    if (!finite_row(d_mean + 3 * (size_t)g, 3)) cls = 0;
-    else if (!finite_row(d_quat + 4 * (size_t)g, 4)) cls = 1;
-    else if (!finite_row(d_log_scale + 3 * (size_t)g, 3)) cls = 2;
-    else if (!isfinite(d_mag[g])) cls = 3;
-    else if (!isfinite(d_phase[g])) cls = 4;
-    else if (!finite_row(d_coeffs + 2 * (size_t)K * g, 2 * K)) cls = 5;
-    if (cls >= 0) atomicMin((unsigned long long*)bad, (unsigned long long)cls * (unsigned long long)n + g);
+    // class order of _check_finite (train.py:133-142): the smallest class * n + row wins the atomicMin,
+    // which is the first bad class, then its first bad row
+    if (g < n) {
+        int cls = -1;
+        if (!finite_row(d_mean + 3 * (size_t)g, 3)) cls = 0;
+        else if (!finite_row(d_quat + 4 * (size_t)g, 4)) cls = 1;
+        else if (!finite_row(d_log_scale + 3 * (size_t)g, 3)) cls = 2;
+        else if (!isfinite(d_mag[g])) cls = 3;
+        else if (!isfinite(d_phase[g])) cls = 4;
+        if (cls >= 0) atomicMin((unsigned long long*)bad, (unsigned long long)cls * (unsigned long long)n + g);
+    }
+    // coefficients (class 5): a flat, coalesced pass (a row of 2K floats per thread thrashes L1)
+    const size_t nf = (size_t)n * 2 * K, stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nf; e += stride)
+        if (!isfinite(d_coeffs[e]))
+            atomicMin((unsigned long long*)bad, 5ull * (unsigned long long)n + (unsigned long long)(e / (2 * K)));
 }
 
 __global__ void k_sgd_update(int n, int K, float lr_mean, float lr_rot, float lr_scale, float lr_trans, float lr_rad,
@@ -88,11 +94,33 @@ __global__ void k_sgd_update(int n, int K, float lr_mean, float lr_rot, float lr
                              float* __restrict__ raw, float* __restrict__ phase, float* __restrict__ coeffs,
                              float* __restrict__ grad_ema, float* __restrict__ last_dmean,
                              const long long* __restrict__ bad,
-                             const long long* __restrict__ prior) {
+                             const long long* __restrict__ prior, const float* __restrict__ lr_mean_dev) {
     rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n || *bad != 0x7f7f7f7f7f7f7f7fLL) return;
+    if (*bad != 0x7f7f7f7f7f7f7f7fLL) return;
     if (prior && *prior != 0x7f7f7f7f7f7f7f7fLL) return;  // an earlier step was bad: the scene stays as it was
+    if (lr_mean_dev) lr_mean = *lr_mean_dev;  // the schedule's value from the device (graph-captured loops)
+    // coefficients: a flat, coalesced pass over all n * 2K floats
+    {
+        const size_t nf = (size_t)n * 2 * K, stride = (size_t)gridDim.x * blockDim.x;
+        size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if ((((uintptr_t)coeffs | (uintptr_t)d_coeffs) & 15) == 0) {
+            float4* c4 = (float4*)coeffs;
+            const float4* d4 = (const float4*)d_coeffs;
+            for (; e < nf / 4; e += stride) {
+                float4 c = c4[e];
+                const float4 d = d4[e];
+                c.x -= lr_rad * d.x;
+                c.y -= lr_rad * d.y;
+                c.z -= lr_rad * d.z;
+                c.w -= lr_rad * d.w;
+                c4[e] = c;
+            }
+            e = (nf / 4) * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+        }
+        for (; e < nf; e += stride) coeffs[e] -= lr_rad * d_coeffs[e];
+    }
+    if (g >= n) return;
     float dm[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -112,7 +140,6 @@ __global__ void k_sgd_update(int n, int K, float lr_mean, float lr_rot, float lr
     const float mag = 1.f / (1.f + expf(-raw[g]));  // from the stored logit before the step
     raw[g] -= lr_trans * d_mag[g] * mag * (1.f - mag);
     phase[g] -= lr_trans * d_phase[g];
-    for (int i = 0; i < 2 * K; ++i) coeffs[2 * (size_t)K * g + i] -= lr_rad * d_coeffs[2 * (size_t)K * g + i];
     if (grad_ema) {  // TrainState.observe (train.py:102-105)
         grad_ema[g] = decay * grad_ema[g] + (1.f - decay) * sqrtf(dm[0] * dm[0] + dm[1] * dm[1] + dm[2] * dm[2]);
 #pragma unroll
@@ -227,7 +254,7 @@ int rfs_sgd_step(int n, int K, const float* lrs, float ema_decay, const float* d
                  const float* d_log_scale, const float* d_trans_mag, const float* d_trans_phase, const void* d_coeffs,
                  float* means, float* quats, float* log_scales, float* trans_mag_raw, float* trans_phase,
                  void* coeffs, float* grad_ema, float* last_dmean, long long* bad, const long long* prior,
-                 void* stream) {
+                 const float* lr_mean_dev, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     RFS_CUDA_TRY(cudaMemsetAsync(bad, 0x7f, sizeof(long long), st));  // sentinel 0x7f7f..7f = no bad row
     if (n <= 0) return RFS_OK;
@@ -237,7 +264,7 @@ int rfs_sgd_step(int n, int K, const float* lrs, float ema_decay, const float* d
     rfs_launch(k_sgd_update, grid, 256, 0, st, n, K, lrs[0], lrs[1], lrs[2], lrs[3], lrs[4], ema_decay, d_mean, d_quat,
                                        d_log_scale, d_trans_mag, d_trans_phase, (const float*)d_coeffs, means, quats,
                                        log_scales, trans_mag_raw, trans_phase, (float*)coeffs, grad_ema, last_dmean,
-                                       bad, prior);
+                                       bad, prior, lr_mean_dev);
     RFS_LAUNCH_CHECK();
     return RFS_OK;
 }

@@ -852,19 +852,19 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     rx = (_native.C.c_double * 3)(*geo.rx)
     npart = int(lib.rfs_geom_part_elems(h))
     acc64 = torch.empty((n, 14), dtype=torch.float64, device=dev)
-    part_g = torch.empty(npart, dtype=torch.int32, device=dev)
+    long_list = torch.empty(npart, dtype=torch.int32, device=dev)  # [0] count, then the long Gaussians
     part_v = torch.empty((npart, 14), dtype=torch.float64, device=dev)
     geom_args = [n, h, gi["h_dev"], _ptr(gi["sorted_g"]), _ptr(gi["s_ray"]), _ptr(gi["s_w"]), _ptr(gi["s_slot"]),
                  _ptr(gs), _ptr(gi["g_rng"]), _ptr(geo.geom), _ptr(geo.dirs), rx, float(geo.ress_radius),
                  _ptr(scene.quats), _ptr(scene.log_scales), _ptr(scene.trans_mag_raw), gi["u_cap"], gi["n_used_dev"],
-                 _ptr(gi["order"]), _ptr(acc64), _ptr(part_g),
+                 _ptr(gi["order"]), _ptr(acc64), _ptr(long_list),
                  _ptr(part_v), _ptr(out["d_mean"]), _ptr(out["d_quat"]), _ptr(out["d_log_scale"]),
                  _ptr(out["d_trans_mag"]), _ptr(out["d_trans_mag_raw"]), _ptr(out["d_trans_phase"]),
                  _ptr(out["d_cov"]), _ptr(dm_dir)]
     _native.call("rfs_grad_geom", *geom_args, 1, st)  # K9a: per-hit sums, alongside K9b
     main.wait_stream(side)  # K9c adds K9b's bearing chain (dm_dir)
     _native.call("rfs_grad_geom", *geom_args, 2, st)  # K9c
-    _native.launch_counter["kernels"] += 2  # k_geom_seg, k_geom_final
+    _native.launch_counter["kernels"] += 3  # k_geom_seg, k_geom_span, k_geom_final
     _mark(marks, "grad_geom")
     return out
 

@@ -33,6 +33,8 @@ __all__ = ["TrainConfig", "TrainState", "DensifyReport", "PruneReport", "lr_mean
 _CLASSES = ("mean", "quat", "log_scale", "trans_mag", "trans_phase", "coeffs")
 _FIELDS = ("means", "quats", "log_scales", "trans_mag_raw", "trans_phase", "coeffs")
 _NO_BAD = 0x7F7F7F7F7F7F7F7F
+_NO_OVF = 1 << 62
+_LOOP_HOOKS: dict = {}  # test seam: "before_capture" runs before each capture of the training iteration
 
 
 @dataclass
@@ -107,12 +109,15 @@ def _ptr(t):
 
 
 def sgd_step(scene: raster.DeviceScene, grads: dict, iteration: int, config: TrainConfig,
-             state: TrainState | None = None, check: bool = True, prior: torch.Tensor | None = None) -> None:
+             state: TrainState | None = None, check: bool = True, prior: torch.Tensor | None = None,
+             lr_dev: torch.Tensor | None = None) -> None:
     """One descent step on the device (train.py:145-162), plus TrainState.observe
     when `state` is given.  A non-finite gradient row leaves the scene untouched;
     with check=True the error is raised here (one 8-byte read), else it can be
     read later from `sgd_step.last_bad`.  `prior` (optional device i64, the
-    first bad value of earlier unchecked steps) skips the update once set."""
+    first bad value of earlier unchecked steps) skips the update once set.
+    `lr_dev` (optional device f32 [1]) replaces lr_mean(config, iteration):
+    the captured training iteration reads its schedule value there."""
     n, K = scene.n, scene.coeffs.shape[1]
     dev = scene.means.device
     bad = torch.empty(1, dtype=torch.int64, device=dev)
@@ -124,7 +129,7 @@ def sgd_step(scene: raster.DeviceScene, grads: dict, iteration: int, config: Tra
                  _ptr(grads["d_coeffs"]), _ptr(scene.means), _ptr(scene.quats), _ptr(scene.log_scales),
                  _ptr(scene.trans_mag_raw), _ptr(scene.trans_phase), _ptr(scene.coeffs),
                  _ptr(state.grad_ema if state else None), _ptr(state.last_dmean if state else None), _ptr(bad),
-                 _ptr(prior), st)
+                 _ptr(prior), _ptr(lr_dev), st)
     sgd_step.last_bad = bad
     if check:
         raise_if_bad(bad, n)
@@ -214,7 +219,7 @@ class TraceRow:
 
 def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tensor, config: TrainConfig,
                batch: int = 1, seed: int = 0, timings: list | None = None, mode: str = "spectrum",
-               check_every: int = 50, group=None):
+               check_every: int = 50, group=None, graph: bool | None = None):
     """Batched counterpart of train.train_loop (train.py:284-361) on the device.
 
     Each iteration draws `batch` samples (TX position + measured target) with a
@@ -222,8 +227,9 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
     backward, the SGD step and TrainState.observe; density control runs on the
     reference schedule during the first half of training.  The scene stays in
     HBM throughout; the loss trace is read back once at the end.  `timings`
-    (optional list) receives (iteration, milliseconds, n_gaussians, event) per
-    iteration from CUDA events.  `mode` is the dataset mode (train.py:266-291):
+    (optional list) receives (iteration, milliseconds, n_gaussians, event,
+    idle milliseconds since the previous iteration ended) per iteration from
+    CUDA events.  `mode` is the dataset mode (train.py:266-291):
     "spectrum" (frames = power frames [S, n_az, n_el]), "rssi" (frames = dBm
     [S]) or "csi" (frames = complex targets [S] or [S, subcarriers]; the
     config's csi_subcarrier is used, train.py:282).
@@ -243,6 +249,17 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
     with the epilogue), so every rank applies the same update and takes the
     same densify / prune decisions (Philox children keyed by seed and
     iteration); the loss trace is summed over the ranks once at the end.
+    Captured iterations (`graph`, default: on for a single process): after
+    one eager iteration at the current Gaussian count -- which sizes every
+    capacity -- the iteration is captured as one CUDA graph and replayed: the
+    samples and the learning rate are drawn up front and indexed on the
+    device by an iteration counter, the geometry runs in its host-read-free
+    form (raster.build_geometry(deferred=...)), and a capacity overflow found
+    on the device halts the following updates the way a bad step does; at the
+    next sync point the loop rewinds to the overflowing iteration and redoes
+    it eagerly (which grows the capacities) before capturing again.  Density
+    control runs eagerly and is followed by a new capture when it changed the
+    scene.  Results are bitwise those of the eager loop.
     Returns (trace, densify_reports, prune_reports).
     """
     import torch.distributed as dist
@@ -277,64 +294,180 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
             raise NonFiniteGradientError(v % n0, _CLASSES[v // n0])
 
     lo, hi = parallel.shard_bounds(batch, rank, world)
-    for it in range(1, config.iterations + 1):
-        idx = torch.as_tensor(rng.integers(len(txs), size=batch)[lo:hi], device=dev)
-        tx, gt = txs[idx].contiguous(), frames[idx].contiguous()
+    iters = config.iterations
+    if graph is None:
+        graph = world == 1 and dev.type == "cuda"
+    if graph and world > 1:
+        raise ConfigError("captured iterations need a single process (graph=False under torch.distributed)")
+    # the samples of every iteration (row it) and the learning-rate schedule, drawn up front
+    draws = [rng.integers(len(txs), size=batch)[lo:hi] for _ in range(iters)]
+    idx_all = torch.as_tensor(np.stack([np.zeros(hi - lo, dtype=np.int64)] + draws).astype(np.int64), device=dev)
+    lr_all = torch.tensor([0.0] + [lr_mean(config, i) for i in range(1, iters + 1)], dtype=torch.float32, device=dev)
+    ctr = torch.zeros(1, dtype=torch.int64, device=dev)  # the iteration a replay runs
+    ovf_at = torch.full((1,), _NO_OVF, dtype=torch.int64, device=dev)  # first replay past a capacity
+    halt = torch.full((1,), _NO_BAD, dtype=torch.int64, device=dev)
+    trace_buf = None
+    n_at = [0] * (iters + 1)
+    has_row = [False] * (iters + 1)
+
+    def loss_up(S, gt):
+        if mode == "spectrum":
+            if S.shape[0] <= raster.MAX_TX_PER_LAUNCH:  # the upstream written ray-major for the backward
+                rep, lamT, _ = _loss.spectrum_loss_frames(S, gt, config.w_ssim, config.w_fourier, lam_layout="rays")
+                return rep, None, lamT
+            rep, lam, _ = _loss.spectrum_loss_frames(S, gt, config.w_ssim, config.w_fourier)
+            return rep, lam, None
+        rep, _, lam = _loss.scalar_loss_frames(S, gt, "real_power" if mode == "rssi" else "complex")
+        return rep, lam, None
+
+    def step(it, deferred=None):
+        """One iteration; `deferred` = the captured form (indexes by ctr)."""
+        nonlocal gb, trace_buf
+        idx = idx_all[it] if deferred is None else idx_all.index_select(0, ctr).view(-1)
+        tx, gt = txs.index_select(0, idx), frames.index_select(0, idx)
+        geo = raster.build_geometry(scene, psi_tx=tx, forward=True, index=True,
+                                    after_forward=lambda S: loss_up(S, gt), deferred=deferred)
+        rep, lam, lamT = geo.after_result
+        if world > 1:
+            if gb is None or gb.n != scene.n:
+                gb = parallel.GradBuffer(scene.n, scene.fle_degree, dev)
+            g = parallel.backward_reduced(scene, geo, tx, lam, gb, config.direction_chain, psi=geo.psi, lamT=lamT,
+                                          group=group)
+        else:
+            g = raster.backward(scene, geo, tx, lam, config.direction_chain, psi=geo.psi, lamT=lamT)
+        n_now = scene.n
+        if deferred is None:
+            prior, lr_dev = first_bad, None
+        else:  # a capacity overflow of this or an earlier replay halts the updates like a bad step
+            c, sv, zv = deferred["caps"], deferred["stats"], deferred["status"]
+            over = (((zv[0:1] & 2) != 0) | ((zv[1:2].long() & 0xFFFFFFFF) > c["m_cap"]) | (sv[0:1] != 0)
+                    | (sv[1:2] != 0) | (sv[3:4] > c["h_cap"]) | (sv[8:9] > c["u_cap"]))
+            ovf_at.copy_(torch.where(over & (ovf_at == _NO_OVF), ctr, ovf_at))
+            halt.copy_(torch.where((first_bad != _NO_BAD) | (ovf_at != _NO_OVF), torch.zeros_like(halt),
+                                   torch.full_like(halt, _NO_BAD)))
+            prior, lr_dev = halt, lr_all.index_select(0, ctr)
+        sgd_step(scene, g, it, config, state, check=False, prior=prior, lr_dev=lr_dev)
+        fresh = (prior == _NO_BAD) & (sgd_step.last_bad != _NO_BAD)
+        first_n.copy_(torch.where(fresh, torch.full_like(first_n, n_now), first_n))
+        first_bad.copy_(torch.where(fresh, sgd_step.last_bad, first_bad))
+        if trace_buf is None:
+            trace_buf = torch.zeros((iters + 1, rep.shape[1]), dtype=rep.dtype, device=dev)
+        if deferred is None:
+            trace_buf[it].copy_(rep.sum(0))
+        else:
+            trace_buf.index_copy_(0, ctr, rep.sum(0, keepdim=True))
+            ctr.add_(1)
+
+    def signature():
+        return (scene.n,) + tuple(getattr(scene, k).data_ptr() for k in _FIELDS) + (
+            state.grad_ema.data_ptr(), state.last_dmean.data_ptr())
+
+    def capture():
+        hook = _LOOP_HOOKS.get("before_capture")
+        if hook is not None:
+            hook()
+        deferred = {"stats": torch.zeros(16, dtype=torch.int32, device=dev),
+                    "status": torch.zeros(8, dtype=torch.int32, device=dev)}
+        # capture_begin / capture_end on a side stream: no synchronize, gc pass
+        # or allocator flush per capture (torch.cuda.graph does all three)
+        g = torch.cuda.CUDAGraph()
+        cur = torch.cuda.current_stream(dev)
+        cap_stream.wait_stream(cur)
+        try:
+            with torch.cuda.stream(cap_stream):
+                g.capture_begin()
+                try:
+                    step(0, deferred)
+                finally:
+                    g.capture_end()
+        except ValueError:  # capacities not known for this scene (see raster._geometry_deferred)
+            return None
+        finally:
+            cur.wait_stream(cap_stream)
+        return g, signature()
+
+    cg = None  # (graph, scene signature)
+    cap_stream = torch.cuda.Stream(dev) if graph else None
+    graph_off = False  # captures kept overflowing at their first replay: eager until the scene changes
+    fails = tries = 0  # overflowing captures in a row / captures refused for missing capacities
+    since_sync = []  # iterations replayed since the last sync point
+    counts = train_loop.last_counts = {"replays": 0, "captures": 0, "rewinds": 0, "redone": 0}
+    it = 1
+    while it <= iters:
         e0 = torch.cuda.Event(enable_timing=True) if timings is not None else None
         if e0 is not None:
             e0.record()
         event = ""
         if scene.n > 0:
-            def loss_up(S):
-                if mode == "spectrum":
-                    rep, lam, _ = _loss.spectrum_loss_frames(S, gt, config.w_ssim, config.w_fourier)
-                else:
-                    rep, _, lam = _loss.scalar_loss_frames(S, gt, "real_power" if mode == "rssi" else "complex")
-                return rep, lam
-            geo = raster.build_geometry(scene, psi_tx=tx, forward=True, index=True, after_forward=loss_up)
-            rep, lam = geo.after_result
-            if world > 1:
-                if gb is None or gb.n != scene.n:
-                    gb = parallel.GradBuffer(scene.n, scene.fle_degree, dev)
-                g = parallel.backward_reduced(scene, geo, tx, lam, gb, config.direction_chain, psi=geo.psi,
-                                              group=group)
+            if cg is not None and cg[1] == signature():
+                cg[0].replay()
+                since_sync.append(it)
+                counts["replays"] += 1
             else:
-                g = raster.backward(scene, geo, tx, lam, config.direction_chain, psi=geo.psi)
-            n_now = scene.n
-            sgd_step(scene, g, it, config, state, check=False, prior=first_bad)
-            fresh = (first_bad == _NO_BAD) & (sgd_step.last_bad != _NO_BAD)
-            first_n.copy_(torch.where(fresh, torch.full_like(first_n, n_now), first_n))
-            first_bad.copy_(torch.where(fresh, sgd_step.last_bad, first_bad))
-            rows.append((it, rep.sum(0), scene.n))
+                if cg is not None:
+                    cg[0].reset()
+                cg = None
+                step(it)
+                ctr.fill_(it + 1)
+                if graph and not graph_off and it < iters and tries < 3:
+                    cg = capture()
+                    tries = 0 if cg is not None else tries + 1
+                    counts["captures"] += cg is not None
+            n_at[it], has_row[it] = scene.n, True
+        dens = it < iters / 2 and scene.n > 0 and (it % config.densify_every == 0 or it % config.prune_every == 0)
+        if since_sync and ((check_every > 0 and it % check_every == 0) or dens or it == iters):
+            o = int(ovf_at.item())
+            if o != _NO_OVF:  # iterations o..it were halted: redo them, o eagerly (capacities grow)
+                fails = fails + 1 if o == since_sync[0] else 0
+                graph_off = graph_off or fails >= 2
+                ovf_at.fill_(_NO_OVF)
+                counts["rewinds"] += 1
+                counts["redone"] += it - o + 1
+                cg[0].reset()
+                cg = None
+                if timings is not None:
+                    timings[:] = [t for t in timings if t[0] < o]
+                tries = 0
+                since_sync = []
+                it = o
+                continue
+            since_sync = []
         if check_every > 0 and it % check_every == 0:
             check()
-        if it < config.iterations / 2:
+        if it < iters / 2:
             if it % config.densify_every == 0 and scene.n > 0:
                 check()  # no density control after a bad step
                 r = densify(scene, state, it, config, seed)
                 if r.cloned or r.split:
                     reports_d.append((it, r))
                     event += "densify "
+                    graph_off, fails, tries = False, 0, 0
             if it % config.prune_every == 0 and scene.n > 0:
                 check()
                 r = prune(scene, state, it, config)
                 if r.removed:
                     reports_p.append((it, r))
                     event += "prune "
+                    graph_off, fails, tries = False, 0, 0
         if e0 is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
             timings.append((it, e0, e1, scene.n, event.strip()))
+        it += 1
+    if cg is not None:
+        cg[0].reset()
     torch.cuda.synchronize()
     check()
     if timings is not None:
-        timings[:] = [(it, a.elapsed_time(b), n, ev) for it, a, b, n, ev in timings]
+        timings[:] = [(i, a.elapsed_time(b), n, ev, timings[j - 1][2].elapsed_time(a) if j else 0.0)
+                      for j, (i, a, b, n, ev) in enumerate(timings)]
+    rows = [i for i in range(1, iters + 1) if has_row[i]]
     if rows:
-        sums = torch.stack([r for _, r, _ in rows])
+        sums = trace_buf[rows]
         if world > 1:
             dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
         means = (sums / max(batch, 1)).tolist()
     else:
         means = []
-    trace = [TraceRow(it, *(float(x) for x in m), n) for (it, _, n), m in zip(rows, means)]
+    trace = [TraceRow(i, *(float(x) for x in m), n_at[i]) for i, m in zip(rows, means)]
     return trace, reports_d, reports_p

@@ -236,3 +236,48 @@ def test_gpu_train_loop_csi_subcarrier():
     with pytest.raises(ConfigError):
         T.train_loop(raster.DeviceScene.from_host(init, "cuda"), txs, tg, T.TrainConfig(iterations=1, csi_subcarrier=26),
                      mode="csi")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["spectrum", "rssi"])
+def test_gpu_train_loop_captured_matches_eager(mode):
+    """The captured training iteration (CUDA graph replays, samples and
+    learning rate indexed on the device) gives bitwise the eager loop's trace,
+    density decisions and scene -- including a rewind: the first capture is
+    made with a too-small hit capacity, its replay overflows, the loop redoes
+    that iteration eagerly and captures again."""
+    import torch
+
+    from paper_2502_01826_b200 import raster
+
+    init, txs, frames = _small_fit_setup(12)
+    if mode == "rssi":
+        frames = 10 * torch.log10(frames.sum((1, 2)) + 1e-3) - 30
+    cfg = T.TrainConfig(iterations=40, densify_every=10, prune_every=15, densify_grad_threshold=1e-9)
+    out = {}
+    for g in (False, True):
+        shrink = {"left": 1}
+
+        def hook():
+            if shrink["left"]:
+                shrink["left"] -= 1
+                for k in raster._CAPS["h_cap"]:
+                    raster._CAPS["h_cap"][k] = 64
+        T._LOOP_HOOKS["before_capture"] = hook
+        try:
+            ds = raster.DeviceScene.from_host(init, "cuda")
+            tim = []
+            trace, dens, pr = T.train_loop(ds, txs, frames, cfg, batch=3, seed=7, timings=tim, mode=mode,
+                                           check_every=9, graph=g)
+        finally:
+            T._LOOP_HOOKS.pop("before_capture", None)
+        out[g] = (trace, dens, pr, ds, dict(T.train_loop.last_counts), tim)
+    (t0, d0, p0, s0, c0, _), (t1, d1, p1, s1, c1, tim1) = out[False], out[True]
+    assert c0["replays"] == 0
+    assert c1["replays"] >= 20 and c1["rewinds"] >= 1 and c1["captures"] >= 2, c1
+    assert [(r.iteration, r.total, r.n_primitives) for r in t0] == [(r.iteration, r.total, r.n_primitives) for r in t1]
+    assert [(i, r.cloned, r.split) for i, r in d0] == [(i, r.cloned, r.split) for i, r in d1]
+    assert [(i, r.removed) for i, r in p0] == [(i, r.removed) for i, r in p1]
+    for k in ("means", "quats", "log_scales", "trans_mag_raw", "trans_phase", "coeffs"):
+        assert torch.equal(getattr(s0, k), getattr(s1, k)), k
+    assert [t[0] for t in tim1] == list(range(1, 41))

@@ -25,6 +25,7 @@ from paper_2502_01826_b200.scene import cube_init, default_txs, round_to_f32
 ap = argparse.ArgumentParser()
 ap.add_argument("--iterations", type=int, default=600)
 ap.add_argument("--batch", type=int, default=16)
+ap.add_argument("--eager", action="store_true", help="no captured iterations (train_loop(graph=False))")
 ap.add_argument("--threshold", type=float, default=1e-7, help="densify_grad_threshold (lowered so it fires)")
 a = ap.parse_args()
 
@@ -44,18 +45,31 @@ _st = train.TrainState.zeros(_w.n, "cuda")
 _st.grad_ema.fill_(1.0)
 train.densify(_w, _st, 1, cfg, 0)
 train.prune(_w, _st, 1, cfg)
+# and of the step itself (module loading, allocator pools, capacities) on another copy
+_w = raster.DeviceScene.from_host(s0, "cuda")
+train.train_loop(_w, txs, frames, train.TrainConfig(iterations=3), batch=a.batch, seed=2, graph=not a.eager)
 del _w, _st
 torch.cuda.synchronize()
 tim = []
-trace, dens, pr = train.train_loop(ds, txs, frames, cfg, batch=a.batch, seed=1, timings=tim)
+e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e_start.record()
+trace, dens, pr = train.train_loop(ds, txs, frames, cfg, batch=a.batch, seed=1, timings=tim, graph=not a.eager)
+e_end.record()
+torch.cuda.synchronize()
+total_ms = e_start.elapsed_time(e_end)
 warm = 5
-plain = [t for it, t, n, ev in tim[warm:] if not ev]
-events = [{"iteration": it, "ms": round(t, 3), "n_after": n, "event": ev} for it, t, n, ev in tim if ev]
+plain = [t for it, t, n, ev, gap in tim[warm:] if not ev]
+gaps = np.array([gap for it, t, n, ev, gap in tim])
+events = [{"iteration": it, "ms": round(t, 3), "n_after": n, "event": ev} for it, t, n, ev, gap in tim if ev]
 print(json.dumps({
     "config": "config 5: cube_init 46^3 Gaussians, 360x180, densify/prune every 100 iterations (first half)",
     "data": "synthetic: spectrum_oracle dataset (datagen.generate_dataset, direct path + 2 reflectors, 256 TX)", "batch_tx": a.batch, "iterations": a.iterations,
     "n_start": int(s0.n), "n_end": int(ds.n), "ms_per_iteration_plain": round(float(np.median(plain)), 3),
     "spectra_per_s_plain": round(a.batch / (float(np.median(plain)) / 1e3), 1),
+    "ms_per_iteration_whole_run": round(total_ms / a.iterations, 3),
+    "idle_between_iterations_ms": {"sum": round(float(gaps.sum()), 2), "median": round(float(np.median(gaps)), 3),
+                                   "top": [[int(tim[i][0]), round(float(gaps[i]), 2)] for i in np.argsort(-gaps)[:8]]},
+    "captured": not a.eager, "loop_counts": train.train_loop.last_counts,
     "density_events": events,
     "loss_first": round(float(np.mean([r.total for r in trace[:10]])), 6),
     "loss_last": round(float(np.mean([r.total for r in trace[-10:]])), 6),
