@@ -226,32 +226,34 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
         }
         return n;
     };
-    // per hit: conj(lam) psi summed over this lane's TX (cr, ci) and p_acc += conj(lam) w T
-    auto hit_terms = [&](const float4 (&a)[NP], const float4 (&q)[NP], float wr, float wi, float4 (&pa)[NP],
-                         float& cr, float& ci) {
-        cr = 0.f;
-        ci = 0.f;
+    // per hit: conj(lam) psi summed over this lane's TX (cr, ci) and p_acc += conj(lam) w T,
+    // as paired fp32 FMAs (FFMA2) with a broadcast lambda component -- per
+    // component the same fused operations in the same order as the scalar
+    // form (negations folded into qn = (q.y, -q.x, q.w, -q.z), the segment's
+    // psi row, and (wi, -wr), the hit's), half the FMA instructions
+    auto hit_terms = [&](const float4 (&a)[NP], const float4 (&q)[NP], const float4 (&qn)[NP], float wr, float wi,
+                         float4 (&pa)[NP], float& cr, float& ci) {
+        float2 c = make_float2(0.f, 0.f);
+        const float2 w1 = make_float2(wr, wi), w2 = make_float2(wi, -wr);
 #pragma unroll
         for (int j = 0; j < NP; ++j) {
-            cr = fmaf(a[j].x, q[j].x, cr);
-            cr = fmaf(a[j].y, q[j].y, cr);
-            cr = fmaf(a[j].z, q[j].z, cr);
-            cr = fmaf(a[j].w, q[j].w, cr);
-            ci = fmaf(a[j].x, q[j].y, ci);
-            ci = fmaf(-a[j].y, q[j].x, ci);
-            ci = fmaf(a[j].z, q[j].w, ci);
-            ci = fmaf(-a[j].w, q[j].z, ci);
-            pa[j].x = fmaf(a[j].x, wr, pa[j].x);
-            pa[j].x = fmaf(a[j].y, wi, pa[j].x);
-            pa[j].y = fmaf(a[j].x, wi, pa[j].y);
-            pa[j].y = fmaf(-a[j].y, wr, pa[j].y);
-            pa[j].z = fmaf(a[j].z, wr, pa[j].z);
-            pa[j].z = fmaf(a[j].w, wi, pa[j].z);
-            pa[j].w = fmaf(a[j].z, wi, pa[j].w);
-            pa[j].w = fmaf(-a[j].w, wr, pa[j].w);
+            const float2 ax = make_float2(a[j].x, a[j].x), ay = make_float2(a[j].y, a[j].y);
+            const float2 az = make_float2(a[j].z, a[j].z), aw = make_float2(a[j].w, a[j].w);
+            c = __ffma2_rn(ax, make_float2(q[j].x, q[j].y), c);
+            c = __ffma2_rn(ay, make_float2(qn[j].x, qn[j].y), c);
+            c = __ffma2_rn(az, make_float2(q[j].z, q[j].w), c);
+            c = __ffma2_rn(aw, make_float2(qn[j].z, qn[j].w), c);
+            float2 p01 = make_float2(pa[j].x, pa[j].y), p23 = make_float2(pa[j].z, pa[j].w);
+            p01 = __ffma2_rn(ax, w1, p01);
+            p01 = __ffma2_rn(ay, w2, p01);
+            p23 = __ffma2_rn(az, w1, p23);
+            p23 = __ffma2_rn(aw, w2, p23);
+            pa[j] = make_float4(p01.x, p01.y, p23.x, p23.y);
         }
+        cr = c.x;
+        ci = c.y;
     };
-    float4 ps[NP], pn[NP];
+    float4 ps[NP], pn[NP], qn[NP];
     {
         const int g = (int)sh_g[wl][0];
 #pragma unroll
@@ -262,7 +264,10 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
         const int e = next_start(s0);
         const int g = (int)sh_g[wl][s0];
 #pragma unroll
-        for (int j = 0; j < NP; ++j) ps[j] = pn[j];
+        for (int j = 0; j < NP; ++j) {
+            ps[j] = pn[j];
+            qn[j] = make_float4(pn[j].y, -pn[j].x, pn[j].w, -pn[j].z);
+        }
         if (e < n) {
             const int gn = (int)sh_g[wl][e];
 #pragma unroll
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
             }
             float v[8];
 #pragma unroll
-            for (int u = 0; u < BG_U; ++u) hit_terms(l[u], ps, eu[u].z, eu[u].w, pa, v[2 * u], v[2 * u + 1]);
+            for (int u = 0; u < BG_U; ++u) hit_terms(l[u], ps, qn, eu[u].z, eu[u].w, pa, v[2 * u], v[2 * u + 1]);
             const float x = reduce8(v, lane);
             if ((lane & 3) == 0) {  // lanes 4i hold value i = 2u + component of hit i0 + u
                 const int i = lane >> 2, u = i >> 1;
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
 #pragma unroll
             for (int j = 0; j < NP; ++j) l[j] = __ldg(row + 32 * j);
             float cr, ci;
-            hit_terms(l, ps, eu.z, eu.w, pa, cr, ci);
+            hit_terms(l, ps, qn, eu.z, eu.w, pa, cr, ci);
             cr = warp_sum(cr);
             ci = warp_sum(ci);
             if (lane == 0) {

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward(const RfsHit* __restrict
 // record, forms w T and the hit's psi row offset once and parks them in a
 // per-warp shared-memory slot; the hit loop reads each record with one
 // broadcast LDS.128 and issues, per hit, one address IMAD, one 16-byte psi
-// load and 8 FFMA.  Latency is covered by software pipelining: the next
+// load and 4 FFMA2 (paired fp32 FMAs).  Latency is covered by software pipelining: the next
 // group of FV_U psi vectors is in flight while the current group is summed,
 // and the next chunk's (or next ray's) hit records while the current chunk
 // is composited.  psi row offsets are 32-bit float4 counts (N B / 2 < 2^32).
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
                                                           float2* __restrict__ S) {
     rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     __shared__ float2 s_out[CP_BCH][FP_RAYS + 1];
-    __shared__ float4 s_hit[CP_THREADS / 32][32 + 2 * FV_U];  // (row offset bits, w T re, w T im, -)
+    __shared__ float4 s_hit[CP_THREADS / 32][32 + 2 * FV_U];  // (row offset bits, w T re, -w T im, w T im)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pv_blocks = (n_el + FP_V - 1) / FP_V;
     const int u = blockIdx.x / pv_blocks, v0 = (blockIdx.x % pv_blocks) * FP_V;
@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
         float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
         if (k < cnt) {
             const RfsHit hl = slab[(size_t)(u * n_el + v0 + wid + (CP_THREADS / 32) * j) * hcap + k];
-            e = make_float4(__uint_as_float(hl.g * nq), hl.w * hl.t_re, hl.w * hl.t_im, 0.f);
+            const float wi = hl.w * hl.t_im;
+            e = make_float4(__uint_as_float(hl.g * nq), hl.w * hl.t_re, -wi, wi);
         }
         return e;
     };
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
     for (int j = 0; j < FV_RPW; ++j) {
         const int cnt = __shfl_sync(0xffffffffu, my_cnt, j);
         const int cnt_n = __shfl_sync(0xffffffffu, my_cnt, (j + 1) % FV_RPW);
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
         if (cnt == 0 && j + 1 < FV_RPW) rec = load_rec(j + 1, lane, cnt_n);
         for (int kc = 0; kc < cnt; kc += 32) {
             __syncwarp();
@@ -144,17 +145,16 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
                     p[k] = __ldg(pl + __float_as_uint(e[k].x));
                 }
             };
+            // acc += (w T) psi for the lane's two TX, as paired fp32 FMAs (FFMA2:
+            // the same fused operations per component, half the instructions)
             auto madd = [&](const float4(&e)[FV_U], const float4(&p)[FV_U]) {
 #pragma unroll
                 for (int k = 0; k < FV_U; ++k) {
-                    acc.x = fmaf(e[k].y, p[k].x, acc.x);
-                    acc.x = fmaf(-e[k].z, p[k].y, acc.x);
-                    acc.y = fmaf(e[k].y, p[k].y, acc.y);
-                    acc.y = fmaf(e[k].z, p[k].x, acc.y);
-                    acc.z = fmaf(e[k].y, p[k].z, acc.z);
-                    acc.z = fmaf(-e[k].z, p[k].w, acc.z);
-                    acc.w = fmaf(e[k].y, p[k].w, acc.w);
-                    acc.w = fmaf(e[k].z, p[k].z, acc.w);
+                    const float2 wr = make_float2(e[k].y, e[k].y), wi = make_float2(e[k].z, e[k].w);  // (-wi, wi)
+                    a01 = __ffma2_rn(wr, make_float2(p[k].x, p[k].y), a01);
+                    a01 = __ffma2_rn(wi, make_float2(p[k].y, p[k].x), a01);
+                    a23 = __ffma2_rn(wr, make_float2(p[k].z, p[k].w), a23);
+                    a23 = __ffma2_rn(wi, make_float2(p[k].w, p[k].z), a23);
                 }
             };
             fetch(ea, pa, 0);
@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restri
             }
         }
         const int rl = wid + (CP_THREADS / 32) * j;
-        s_out[2 * lane][rl] = make_float2(acc.x, acc.y);
-        s_out[2 * lane + 1][rl] = make_float2(acc.z, acc.w);
+        s_out[2 * lane][rl] = a01;
+        s_out[2 * lane + 1][rl] = a23;
     }
     __syncthreads();
     const int nbc = min(CP_BCH, nb - bc);

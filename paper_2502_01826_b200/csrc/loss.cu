@@ -94,9 +94,14 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return t;
 }
 
+// Pairs of statistics are interleaved (float2) so both blur passes run as
+// paired fp32 FMAs (FFMA2) on 8-byte shared-memory loads: per component the
+// same fused operations in the same order as the scalar form.
 struct FwdSmem {
-    float x[HU][HVP], y[HU][HVP];  // raw frames (0 in the padding)
-    float h[5][HU][TVP];           // v-blurred x, y, xx, yy, xy of the centred frames
+    float2 xy[HU][HVP];            // raw frames (x, y; 0 in the padding)
+    float2 h01[HU][TVP];           // v-blurred (x, y) of the centred frames
+    float2 h23[HU][TVP];           // v-blurred (xx, yy)
+    float h4[HU][TVP];             // v-blurred xy
     double red[LT / 32];
     float2 rng;                    // the frame's (min, max) of y
 };
@@ -151,42 +156,40 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_fwd(const float2* __restrict__ S
 #pragma unroll
         for (int k = 0; k < NH; ++k) {
             const int i = threadIdx.x + k * LT, hu = i / HV, hv = i - hu * HV;
-            if (hu < HU) {
-                M.x[hu][hv] = xv[k];
-                M.y[hu][hv] = yv[k];
-            }
+            if (hu < HU) M.xy[hu][hv] = make_float2(xv[k], yv[k]);
         }
     }
     __syncthreads();
     const double D = fmax((double)M.rng.y - (double)M.rng.x, 1e-6);
     const double c1 = (0.01 * D) * (0.01 * D), c2 = (0.03 * D) * (0.03 * D);
-    const float cx = M.x[LH][LH], cy = M.y[LH][LH];  // centre: the tile's first cell
+    const float2 cxy = M.xy[LH][LH];  // centre: the tile's first cell
+    const float cx = cxy.x, cy = cxy.y;
     // correlate along v (axis 1): item = (segment, row), rows fastest -> conflict-free
     for (int it = threadIdx.x; it < (TV / SEG) * HU; it += LT) {
         const int sg = it / HU, hu = it - sg * HU, o0 = sg * SEG;
-        float wx[SEG + LW - 1], wy[SEG + LW - 1], wxx[SEG + LW - 1], wyy[SEG + LW - 1], wxy[SEG + LW - 1];
+        float2 wd[SEG + LW - 1], wsq[SEG + LW - 1];
+        float wxy[SEG + LW - 1];
+        const float2 nc = make_float2(-cx, -cy);
 #pragma unroll
         for (int j = 0; j < SEG + LW - 1; ++j) {  // the products once per input, not once per tap
-            wx[j] = M.x[hu][o0 + j] - cx;
-            wy[j] = M.y[hu][o0 + j] - cy;
-            wxx[j] = wx[j] * wx[j];
-            wyy[j] = wy[j] * wy[j];
-            wxy[j] = wx[j] * wy[j];
+            wd[j] = __fadd2_rn(M.xy[hu][o0 + j], nc);  // (x - cx, y - cy)
+            wsq[j] = __fmul2_rn(wd[j], wd[j]);
+            wxy[j] = wd[j].x * wd[j].y;
         }
 #pragma unroll
         for (int o = 0; o < SEG; ++o) {
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+            float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+            float a4 = 0.f;
 #pragma unroll
             for (int t = 0; t < LW; ++t) {
                 const float w = c_winf[t];
-                a0 = fmaf(w, wx[o + t], a0);
-                a1 = fmaf(w, wy[o + t], a1);
-                a2 = fmaf(w, wxx[o + t], a2);
-                a3 = fmaf(w, wyy[o + t], a3);
+                a01 = __ffma2_rn(make_float2(w, w), wd[o + t], a01);
+                a23 = __ffma2_rn(make_float2(w, w), wsq[o + t], a23);
                 a4 = fmaf(w, wxy[o + t], a4);
             }
-            M.h[0][hu][o0 + o] = a0; M.h[1][hu][o0 + o] = a1; M.h[2][hu][o0 + o] = a2;
-            M.h[3][hu][o0 + o] = a3; M.h[4][hu][o0 + o] = a4;
+            M.h01[hu][o0 + o] = a01;
+            M.h23[hu][o0 + o] = a23;
+            M.h4[hu][o0 + o] = a4;
         }
     }
     __syncthreads();
@@ -206,17 +209,31 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_fwd(const float2* __restrict__ S
             }
         }
         float m[5][SEG];
+        {
+            float2 w01[SEG + LW - 1], w23[SEG + LW - 1];
+            float w4[SEG + LW - 1];
 #pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            float wv[SEG + LW - 1];
-#pragma unroll
-            for (int j = 0; j < SEG + LW - 1; ++j) wv[j] = M.h[k][o0 + j][ov];
+            for (int j = 0; j < SEG + LW - 1; ++j) {
+                w01[j] = M.h01[o0 + j][ov];
+                w23[j] = M.h23[o0 + j][ov];
+                w4[j] = M.h4[o0 + j][ov];
+            }
 #pragma unroll
             for (int o = 0; o < SEG; ++o) {
-                float a = 0.f;
+                float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+                float a4 = 0.f;
 #pragma unroll
-                for (int t = 0; t < LW; ++t) a = fmaf(c_winf[t], wv[o + t], a);
-                m[k][o] = a;
+                for (int t = 0; t < LW; ++t) {
+                    const float w = c_winf[t];
+                    a01 = __ffma2_rn(make_float2(w, w), w01[o + t], a01);
+                    a23 = __ffma2_rn(make_float2(w, w), w23[o + t], a23);
+                    a4 = fmaf(w, w4[o + t], a4);
+                }
+                m[0][o] = a01.x;
+                m[1][o] = a01.y;
+                m[2][o] = a23.x;
+                m[3][o] = a23.y;
+                m[4][o] = a4;
             }
         }
 #pragma unroll
@@ -257,8 +274,10 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_fwd(const float2* __restrict__ S
 }
 
 struct BwdSmem {
-    float m[3][HU][HVP];
-    float h[3][HU][TVP];
+    float2 m01[HU][HVP];  // (ds/dmu, ds/dv) maps, interleaved for FFMA2
+    float m2[HU][HVP];    // ds/dw
+    float2 h01[HU][TVP];
+    float h2[HU][TVP];
 };
 
 __global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S, const float* __restrict__ pred,
@@ -292,9 +311,8 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S
         for (int k = 0; k < NH; ++k) {
             const int i = threadIdx.x + k * LT, hu = i / HV, hv = i - hu * HV;
             if (hu < HU) {
-                M.m[0][hu][hv] = mv[0][k];
-                M.m[1][hu][hv] = mv[1][k];
-                M.m[2][hu][hv] = mv[2][k];
+                M.m01[hu][hv] = make_float2(mv[0][k], mv[1][k]);
+                M.m2[hu][hv] = mv[2][k];
             }
         }
     }
@@ -302,18 +320,25 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S
     // adjoint of the zero-padded correlation = the same correlation
     for (int it = threadIdx.x; it < (TV / SEG) * HU; it += LT) {
         const int sg = it / HU, hu = it - sg * HU, o0 = sg * SEG;
+        float2 w01[SEG + LW - 1];
+        float w2[SEG + LW - 1];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            float wv[SEG + LW - 1];
+        for (int j = 0; j < SEG + LW - 1; ++j) {
+            w01[j] = M.m01[hu][o0 + j];
+            w2[j] = M.m2[hu][o0 + j];
+        }
 #pragma unroll
-            for (int j = 0; j < SEG + LW - 1; ++j) wv[j] = M.m[k][hu][o0 + j];
+        for (int o = 0; o < SEG; ++o) {
+            float2 a01 = make_float2(0.f, 0.f);
+            float a2 = 0.f;
 #pragma unroll
-            for (int o = 0; o < SEG; ++o) {
-                float a = 0.f;
-#pragma unroll
-                for (int t = 0; t < LW; ++t) a = fmaf(c_winf[t], wv[o + t], a);
-                M.h[k][hu][o0 + o] = a;
+            for (int t = 0; t < LW; ++t) {
+                const float w = c_winf[t];
+                a01 = __ffma2_rn(make_float2(w, w), w01[o + t], a01);
+                a2 = fmaf(w, w2[o + t], a2);
             }
+            M.h01[hu][o0 + o] = a01;
+            M.h2[hu][o0 + o] = a2;
         }
     }
     __syncthreads();
@@ -335,17 +360,27 @@ __global__ void __launch_bounds__(LT, 5) k_ssim_bwd(const float2* __restrict__ S
         }
     }
     float a[3][SEG];
+    {
+        float2 w01[SEG + LW - 1];
+        float w2[SEG + LW - 1];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        float wv[SEG + LW - 1];
-#pragma unroll
-        for (int j = 0; j < SEG + LW - 1; ++j) wv[j] = M.h[k][o0 + j][ov];
+        for (int j = 0; j < SEG + LW - 1; ++j) {
+            w01[j] = M.h01[o0 + j][ov];
+            w2[j] = M.h2[o0 + j][ov];
+        }
 #pragma unroll
         for (int o = 0; o < SEG; ++o) {
-            float acc = 0.f;
+            float2 a01 = make_float2(0.f, 0.f);
+            float a2 = 0.f;
 #pragma unroll
-            for (int t = 0; t < LW; ++t) acc = fmaf(c_winf[t], wv[o + t], acc);
-            a[k][o] = acc;
+            for (int t = 0; t < LW; ++t) {
+                const float w = c_winf[t];
+                a01 = __ffma2_rn(make_float2(w, w), w01[o + t], a01);
+                a2 = fmaf(w, w2[o + t], a2);
+            }
+            a[0][o] = a01.x;
+            a[1][o] = a01.y;
+            a[2][o] = a2;
         }
     }
 #pragma unroll
