@@ -236,25 +236,50 @@ def fwd_bwd_host(host_scene: dict, tx_host: torch.Tensor, lam_host: torch.Tensor
     The drop-in for a caller holding the scene and upstream frames on the
     host, i.e. render_complex_frame + backward_frame of the reference
     (render.py:282-289, grad.py:192-259) for a TX batch.  Copies are
-    stream-ordered (non_blocking); the caller synchronizes.  `reduce_fn`
+    stream-ordered (non_blocking) with respect to the current stream; the caller
+    synchronizes.  Inside, the upstream frames travel on a copy stream while the
+    geometry and the forward run, and the frames come back on another while
+    the backward runs.  `reduce_fn`
     (optional) all-reduces the device gradient dict before the D2H copy.
     Returns (h2d_bytes, d2h_bytes).
     """
     dev = torch.device("cuda", torch.cuda.current_device())
+    main = torch.cuda.current_stream(dev)
     d = {k: host_scene[k].to(dev, non_blocking=True) for k in SCENE_FIELDS}
     ds = raster.DeviceScene(d["means"], d["quats"], d["log_scales"], d["trans_mag_raw"], d["trans_phase"],
                             d["coeffs"], tuple(float(x) for x in rx), float(ress_radius), n_az, n_el, fle_degree)
     tx = tx_host.to(dev, non_blocking=True)
-    lam = lam_host.to(dev, non_blocking=True)
+    # the upstream frames (the largest input) on the H2D copy stream, overlapping
+    # the TX-independent geometry and the forward; the backward waits for them
+    lam = torch.empty(tuple(lam_host.shape), dtype=lam_host.dtype, device=dev)
+    up = _copy_stream(dev)
+    up.wait_stream(main)
+    with torch.cuda.stream(up):
+        lam.copy_(lam_host, non_blocking=True)
+        lam_ready = torch.cuda.Event()
+        lam_ready.record(up)
+    lam.record_stream(up)
     geo = raster.build_geometry(ds, sort_backend=sort_backend, psi_tx=tx, index=True, forward=True)
     psi = geo.psi
     S = raster.forward(geo, psi)
+    # the frames back on the D2H copy stream while the backward runs (the other
+    # copy engine: the two directions overlap too)
+    down = _copy_stream_d2h(dev)
+    down.wait_stream(main)
+    with torch.cuda.stream(down):
+        out["S"].copy_(S, non_blocking=True)
+    S.record_stream(down)
+    main.wait_event(lam_ready)
     g = raster.backward(ds, geo, tx, lam, include_direction_chain, psi=psi)
     if reduce_fn is not None:
         reduce_fn(g)
-    out["S"].copy_(S, non_blocking=True)
+    down.wait_stream(main)
+    with torch.cuda.stream(down):
+        for k in OUT_GRADS:
+            out[k].copy_(g[k], non_blocking=True)
     for k in OUT_GRADS:
-        out[k].copy_(g[k], non_blocking=True)
+        g[k].record_stream(down)
+    main.wait_stream(down)  # stream-ordered for the caller, as before
     h2d = sum(host_scene[k].numel() * host_scene[k].element_size() for k in SCENE_FIELDS)
     h2d += tx_host.numel() * tx_host.element_size() + lam_host.numel() * lam_host.element_size()
     d2h = sum(out[k].numel() * out[k].element_size() for k in ("S",) + OUT_GRADS)
@@ -374,6 +399,13 @@ _COPY: dict = {}
 
 def _copy_stream(dev) -> torch.cuda.Stream:
     k = str(dev)
+    if k not in _COPY:
+        _COPY[k] = torch.cuda.Stream(device=dev)
+    return _COPY[k]
+
+
+def _copy_stream_d2h(dev) -> torch.cuda.Stream:
+    k = "d2h:" + str(dev)
     if k not in _COPY:
         _COPY[k] = torch.cuda.Stream(device=dev)
     return _COPY[k]
