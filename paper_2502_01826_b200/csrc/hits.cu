@@ -15,8 +15,10 @@
 // lb[i] = min_{j>=i} (depth_j - r3_j) precedes every hit the remaining
 // candidates can produce: it is final and is emitted, and a ray stops
 // scanning as soon as it terminates.  Pending (t_mid, g, w) entries live in a
-// per-thread ring in shared memory; a ray that overflows it is redone by
-// k_hits_slow with a global buffer sized to its tile (exact, rarely taken).
+// per-thread ring in shared memory; a full ring keeps the PCAP smallest and
+// remembers the smallest hit it dropped -- a ray that terminates before that
+// hit is due is exact as is, one that would need it is redone by k_hits_slow
+// with a global buffer sized to its tile (exact, rarely taken).
 //   Per warp (a 4 x 8 ray patch), chunks of CH candidates: stage the fp32
 //   filter data in warp-private shared memory and have the bulk-copy engine
 //   bring the fp64 records of the cone-relevant ones (cp.async.bulk, one per
@@ -240,6 +242,11 @@ __global__ void __launch_bounds__(NT) k_hits(
     int head = 0, npend = 0, max_pend = 0;
     int n_sph = 0, n_wh = 0;
     double head_t = DINF;
+    // a full ring keeps the PCAP smallest (t_mid, g) pending hits: the evicted
+    // or refused ones are represented by their minimum (ev_t, ev_g); the ray
+    // only fails (-> slow path) if it would have to emit that hit
+    double ev_t = DINF;
+    uint32_t ev_g = 0xffffffffu;
     const int2 rg = ranges[tile];
     const int c_lo = rg.x, c_hi = rg.y;
     WarpStage<CH>& W = S.ws[wid];
@@ -281,6 +288,10 @@ __global__ void __launch_bounds__(NT) k_hits(
             head = (head + 1) & (PCAP - 1);
             --npend;
             head_t = npend > 0 ? S.pt[head][tid] : DINF;
+        }
+        if (!st.done && ev_t < bound) {  // a dropped hit is due: redo the ray on the slow path
+            pend_over = true;
+            st.done = true;
         }
     };
 
@@ -338,10 +349,20 @@ __global__ void __launch_bounds__(NT) k_hits(
                 double t_mid;
                 float w;
                 if (!exact_hit_s(W.gd[j], st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid, w)) continue;
-                if (npend == PCAP) {
-                    pend_over = true;
-                    st.done = true;
-                    break;
+                if (ev_t < t_mid || (ev_t == t_mid && ev_g < g)) continue;  // after a dropped hit: dropped too
+                if (npend == PCAP) {  // full: keep the PCAP smallest, remember the smallest dropped
+                    const int tl = (head + PCAP - 1) & (PCAP - 1);
+                    const double tt = S.pt[tl][tid];
+                    const uint32_t tg = S.pg[tl][tid];
+                    if (tt > t_mid || (tt == t_mid && tg > g)) {
+                        ev_t = tt;  // the tail is the largest pending entry, and below every earlier drop
+                        ev_g = tg;
+                        --npend;
+                    } else {
+                        ev_t = t_mid;
+                        ev_g = g;
+                        continue;
+                    }
                 }
                 int k = npend;
                 int ps = (head + k - 1) & (PCAP - 1);
@@ -376,6 +397,7 @@ __global__ void __launch_bounds__(NT) k_hits(
         head = (head + 1) & (PCAP - 1);
         --npend;
     }
+    if (!st.done && ev_t < DINF) pend_over = true;  // it needed a dropped hit
     if (!valid) return;
     atomicMax(&stats[5], max_pend);
     atomicAdd(&stats[6], n_sph);

@@ -274,12 +274,48 @@ def test_slow_path_bitwise_equals_ring_path():
             out[pc] = (g.S.cpu().numpy(), g.ray_counts.cpu().numpy(), g.stats[0])
     finally:
         raster._CAPS.update(saved)
-    assert out[16][2] > out[64][2]  # the small ring overflowed on more rays (slow path taken)
+    assert out[16][2] > 0 and out[16][2] >= out[64][2]  # the small ring was not enough (slow path taken)
     np.testing.assert_array_equal(out[16][0], out[64][0])
     np.testing.assert_array_equal(out[16][1], out[64][1])
     ref = oracle.render_complex_frame(s, default_txs(2, seed=3)[0])
     P, Pr = np.abs(out[64][0][0]) ** 2, np.abs(ref) ** 2
     assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= 1e-4
+
+
+@pytest.mark.gpu
+def test_full_ring_keeps_smallest_pending_hits():
+    """Config-5 geometry (cube_init at 360x180, the receiver inside the cloud),
+    opaque Gaussians: rays hold up to 22 pending hits but terminate after 7
+    emitted ones.  A full 16-entry ring keeps the 16 smallest (t_mid, g) and
+    remembers the smallest dropped hit, so every ray finishes in the ring (no
+    slow path): bitwise the hit lists and frames of a 64-entry ring, and the
+    oracle's live counts."""
+    import torch
+
+    from paper_2502_01826_b200 import raster
+    from paper_2502_01826_b200.scene import cube_init
+
+    s = cube_init([-15] * 3, [15] * 3, 0.65, 360, 180)
+    s.trans_mag_raw[:] = -2.0
+    s = round_to_f32(s)
+    ds = raster.DeviceScene.from_host(s, "cuda")
+    tx = torch.as_tensor(default_txs(2, seed=3), dtype=torch.float32, device="cuda")
+    saved = dict(raster._CAPS)
+    try:
+        out = {}
+        for pc in (16, 64):
+            raster._CAPS["pcap"] = pc
+            g = raster.build_geometry(ds, psi_tx=tx, forward=True)
+            out[pc] = (g.S.cpu().numpy(), *_hit_lists(g), list(g.stats))
+    finally:
+        raster._CAPS.update(saved)
+    st16, st64 = out[16][3], out[64][3]
+    assert st16[5] == 16 and st64[5] > 16  # the small rings filled up
+    assert st16[0] == 0, st16  # ... without sending a ray to the slow path
+    for i in range(3):
+        np.testing.assert_array_equal(out[16][i], out[64][i])
+    oc = oracle.OracleContext(s)
+    np.testing.assert_array_equal(out[16][1], oc.live_counts().ravel())
 
 
 @pytest.mark.gpu

@@ -67,6 +67,8 @@ print(json.dumps({
     "n_start": int(s0.n), "n_end": int(ds.n), "ms_per_iteration_plain": round(float(np.median(plain)), 3),
     "spectra_per_s_plain": round(a.batch / (float(np.median(plain)) / 1e3), 1),
     "ms_per_iteration_whole_run": round(total_ms / a.iterations, 3),
+    "ms_median_by_50": [round(float(np.median([t for it, t, n, ev, gap in tim if b <= it < b + 50] or [0])), 3)
+                        for b in range(1, a.iterations + 1, 50)],
     "idle_between_iterations_ms": {"sum": round(float(gaps.sum()), 2), "median": round(float(np.median(gaps)), 3),
                                    "top": [[int(tim[i][0]), round(float(gaps[i]), 2)] for i in np.argsort(-gaps)[:8]]},
     "captured": not a.eager, "loop_counts": train.train_loop.last_counts,

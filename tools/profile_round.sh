@@ -13,4 +13,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 # one steady-state step only (cudaProfilerStart/Stop in tools/ncu_step.py): ~30 kernels
 timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -o gpurun_out/${TAG}_full python tools/ncu_step.py > gpurun_out/${TAG}_ncu.log 2>&1
+# config 5: one training iteration's launch list and the 400-iteration timing (captured iterations)
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/${TAG}_c5_launches.csv python tools/bench_density.py --iterations 8 --eager > /dev/null 2>&1
+python tools/launch_list.py gpurun_out/${TAG}_c5_launches.csv > gpurun_out/${TAG}_c5_launches.txt 2>&1
+timeout 600 python tools/bench_density.py --iterations 600 > gpurun_out/${TAG}_density.json 2> gpurun_out/${TAG}_density.err
 echo done
