@@ -20,6 +20,7 @@ split, the children's attributes and count), SURVEY.md §7 H8.
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -391,7 +392,7 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
     graph_off = False  # captures kept overflowing at their first replay: eager until the scene changes
     fails = tries = 0  # overflowing captures in a row / captures refused for missing capacities
     since_sync = []  # iterations replayed since the last sync point
-    counts = train_loop.last_counts = {"replays": 0, "captures": 0, "rewinds": 0, "redone": 0}
+    counts = train_loop.last_counts = {"replays": 0, "captures": 0, "rewinds": 0, "redone": 0, "capture_ms": 0.0}
     it = 1
     while it <= iters:
         e0 = torch.cuda.Event(enable_timing=True) if timings is not None else None
@@ -410,7 +411,9 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
                 step(it)
                 ctr.fill_(it + 1)
                 if graph and not graph_off and it < iters and tries < 3:
+                    t_cap = time.perf_counter()
                     cg = capture()
+                    counts["capture_ms"] += (time.perf_counter() - t_cap) * 1e3
                     tries = 0 if cg is not None else tries + 1
                     counts["captures"] += cg is not None
             n_at[it], has_row[it] = scene.n, True
