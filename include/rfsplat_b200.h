@@ -119,10 +119,13 @@ int rfs_ray_dirs(int n_az, int n_el, double* dirs, void* stream);
  * used (nullable u32[n], zeroed here): 1 for every Gaussian with a live hit.
  * The exact streaming re-sort with early termination (hits.cu); pcap
  * selects the pending ring (<= 16 -> 16 entries per ray, <= 32 -> 32, else
- * 64); stats[5] = the largest pending set, stats[6] / [7] = fp32 sphere /
+ * 64), and pcap | RFS_PCAP_EVICT makes a full ring keep its smallest hits
+ * (a ray then needs the slow path only if it must emit a dropped hit);
+ * stats[5] = the largest pending set, stats[6] / [7] = fp32 sphere /
  * whitened-ellipsoid passes (diagnostics).  Only the rays of tiles
  * [tile_lo, tile_hi) are traced (tile_hi < 0: all tiles); the others get no
  * hits -- the tile shard of a rank in the strong-scaling mode. */
+#define RFS_PCAP_EVICT 0x10000
 int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double* lb, const void* sph, const void* whit,
              const void* geom, const double* dirs, const double* rx, double ress_radius, int n_az, int n_el, int hcap,
              int pcap, void* slab, int* counts, int* slow_list, int* stats, uint32_t* used, int n, int tile_lo,

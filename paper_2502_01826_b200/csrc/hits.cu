@@ -204,8 +204,10 @@ struct HitsSmem {
     WarpStage<CH> ws[NT / 32];
 };
 
-// Streaming K6 (dense scenes): see the file comment.
-template <int PCAP, int NT, int CH>
+// Streaming K6 (dense scenes): see the file comment.  EVICT: a full ring keeps
+// its PCAP smallest hits (else the ray goes to the slow path at once) --
+// switched on by the host once a scene sends many rays to the slow path.
+template <int PCAP, int NT, int CH, bool EVICT>
 __global__ void __launch_bounds__(NT) k_hits(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ vals, const double* __restrict__ lb,
     const float4* __restrict__ sph, const float4* __restrict__ whit, const RfsGeom* __restrict__ geom,
@@ -289,9 +291,11 @@ __global__ void __launch_bounds__(NT) k_hits(
             --npend;
             head_t = npend > 0 ? S.pt[head][tid] : DINF;
         }
-        if (!st.done && ev_t < bound) {  // a dropped hit is due: redo the ray on the slow path
-            pend_over = true;
-            st.done = true;
+        if constexpr (EVICT) {
+            if (!st.done && ev_t < bound) {  // a dropped hit is due: redo the ray on the slow path
+                pend_over = true;
+                st.done = true;
+            }
         }
     };
 
@@ -349,20 +353,26 @@ __global__ void __launch_bounds__(NT) k_hits(
                 double t_mid;
                 float w;
                 if (!exact_hit_s(W.gd[j], st.dx, st.dy, st.dz, uf, vf, naz, rx0, rx1, rx2, min_t, t_mid, w)) continue;
-                if (ev_t < t_mid || (ev_t == t_mid && ev_g < g)) continue;  // after a dropped hit: dropped too
-                if (npend == PCAP) {  // full: keep the PCAP smallest, remember the smallest dropped
-                    const int tl = (head + PCAP - 1) & (PCAP - 1);
-                    const double tt = S.pt[tl][tid];
-                    const uint32_t tg = S.pg[tl][tid];
-                    if (tt > t_mid || (tt == t_mid && tg > g)) {
-                        ev_t = tt;  // the tail is the largest pending entry, and below every earlier drop
-                        ev_g = tg;
-                        --npend;
-                    } else {
-                        ev_t = t_mid;
-                        ev_g = g;
-                        continue;
+                if constexpr (EVICT) {
+                    if (ev_t < t_mid || (ev_t == t_mid && ev_g < g)) continue;  // after a dropped hit: dropped too
+                    if (npend == PCAP) {  // full: keep the PCAP smallest, remember the smallest dropped
+                        const int tl = (head + PCAP - 1) & (PCAP - 1);
+                        const double tt = S.pt[tl][tid];
+                        const uint32_t tg = S.pg[tl][tid];
+                        if (tt > t_mid || (tt == t_mid && tg > g)) {
+                            ev_t = tt;  // the tail is the largest pending entry, and below every earlier drop
+                            ev_g = tg;
+                            --npend;
+                        } else {
+                            ev_t = t_mid;
+                            ev_g = g;
+                            continue;
+                        }
                     }
+                } else if (npend == PCAP) {
+                    pend_over = true;
+                    st.done = true;
+                    break;
                 }
                 int k = npend;
                 int ps = (head + k - 1) & (PCAP - 1);
@@ -397,7 +407,9 @@ __global__ void __launch_bounds__(NT) k_hits(
         head = (head + 1) & (PCAP - 1);
         --npend;
     }
-    if (!st.done && ev_t < DINF) pend_over = true;  // it needed a dropped hit
+    if constexpr (EVICT) {
+        if (!st.done && ev_t < DINF) pend_over = true;  // it needed a dropped hit
+    }
     if (!valid) return;
     atomicMax(&stats[5], max_pend);
     atomicAdd(&stats[6], n_sph);
@@ -523,7 +535,7 @@ __global__ void k_ray_dirs(int n_az, int n_el, double* __restrict__ dirs) {
     dirs[3 * r + 2] = sin(be);
 }
 
-template <int PCAP, int NT, int CH>
+template <int PCAP, int NT, int CH, bool EVICT>
 int launch_hits(int tile_lo, int tile_hi, const int* ranges, const uint32_t* vals, const double* lb, const void* sph,
                 const void* whit, const void* geom, const double* dirs, const double* rx, double min_t, int n_az,
                 int n_el, int tiles_u, int hcap, void* slab, int* counts, int* slow_list, int* stats, uint32_t* used,
@@ -532,14 +544,14 @@ int launch_hits(int tile_lo, int tile_hi, const int* ranges, const uint32_t* val
     size_t smem = sizeof(HitsSmem<PCAP, NT, CH>);
     if (!attr) {
         RFS_CUDA_TRY(
-            cudaFuncSetAttribute(k_hits<PCAP, NT, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cudaFuncSetAttribute(k_hits<PCAP, NT, CH, EVICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         // the whole grid must be resident at once (a late-starting tile extends
         // the kernel): ask for the largest shared-memory carveout
-        RFS_CUDA_TRY(cudaFuncSetAttribute(k_hits<PCAP, NT, CH>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        RFS_CUDA_TRY(cudaFuncSetAttribute(k_hits<PCAP, NT, CH, EVICT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                           (int)cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
-    rfs_launch(k_hits<PCAP, NT, CH>, (tile_hi - tile_lo) * (256 / NT), NT, smem, st, 
+    rfs_launch(k_hits<PCAP, NT, CH, EVICT>, (tile_hi - tile_lo) * (256 / NT), NT, smem, st, 
         (const int2*)ranges, vals, lb, (const float4*)sph, (const float4*)whit, (const RfsGeom*)geom, dirs, rx[0],
         rx[1], rx[2], min_t, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, slow_list, stats, used, tile_lo);
     RFS_LAUNCH_CHECK();
@@ -576,15 +588,15 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
     // is set by the longest warps' chains, not by the late starts
     int rc = RFS_OK;
     if (tile_hi > tile_lo) {
-        if (pcap <= 16)
-            rc = launch_hits<16, 64, 32>(tile_lo, tile_hi, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius,
-                                         n_az, n_el, tiles_u, hcap, slab, counts, slow_list, stats, used, st);
-        else if (pcap <= 32)
-            rc = launch_hits<32, 64, 32>(tile_lo, tile_hi, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius,
-                                         n_az, n_el, tiles_u, hcap, slab, counts, slow_list, stats, used, st);
-        else
-            rc = launch_hits<64, 32, 16>(tile_lo, tile_hi, ranges, vals, lb, sph, whit, geom, dirs, rx, ress_radius,
-                                         n_az, n_el, tiles_u, hcap, slab, counts, slow_list, stats, used, st);
+#define RFS_LH(P, T, C, E) launch_hits<P, T, C, E>(tile_lo, tile_hi, ranges, vals, lb, sph, whit, geom, dirs, rx, \
+                                                  ress_radius, n_az, n_el, tiles_u, hcap, slab, counts, slow_list, \
+                                                  stats, used, st)
+        const bool evict = (pcap & RFS_PCAP_EVICT) != 0;
+        const int pc = pcap & ~RFS_PCAP_EVICT;
+        if (pc <= 16) rc = evict ? RFS_LH(16, 64, 32, true) : RFS_LH(16, 64, 32, false);
+        else if (pc <= 32) rc = evict ? RFS_LH(32, 64, 32, true) : RFS_LH(32, 64, 32, false);
+        else rc = evict ? RFS_LH(64, 32, 16, true) : RFS_LH(64, 32, 16, false);
+#undef RFS_LH
     }
     if (rc != RFS_OK) return rc;
     rfs_launch(k_max_range, rfs_ceil_div(n_tiles, 256), 256, 0, st, (const int2*)ranges, n_tiles, stats + 4);

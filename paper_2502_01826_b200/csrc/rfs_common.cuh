@@ -13,6 +13,9 @@
 #include <stdint.h>
 
 #define RFS_TILE 16
+#ifndef RFS_PCAP_EVICT
+#define RFS_PCAP_EVICT 0x10000  // rfs_hits: pcap flag, as include/rfsplat_b200.h defines it
+#endif
 #define RFS_TERM_EPS2 1e-12   // _kernels.py:20
 #define RFS_TANGENT_EPS 1e-10 // _kernels.py:22
 #define RFS_PI 3.141592653589793

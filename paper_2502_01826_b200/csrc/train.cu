@@ -81,9 +81,22 @@ __global__ void k_sgd_check(int n, int K, const float* __restrict__ d_mean, cons
     }
     // coefficients (class 5): a flat, coalesced pass (a row of 2K floats per thread thrashes L1)
     const size_t nf = (size_t)n * 2 * K, stride = (size_t)gridDim.x * blockDim.x;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nf; e += stride)
-        if (!isfinite(d_coeffs[e]))
-            atomicMin((unsigned long long*)bad, 5ull * (unsigned long long)n + (unsigned long long)(e / (2 * K)));
+    size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    auto flag = [&](size_t i) {
+        atomicMin((unsigned long long*)bad, 5ull * (unsigned long long)n + (unsigned long long)(i / (2 * K)));
+    };
+    if (((uintptr_t)d_coeffs & 15) == 0) {  // 16-byte loads, then the tail
+        const float4* d4 = (const float4*)d_coeffs;
+        for (; e < nf / 4; e += stride) {
+            const float4 d = d4[e];
+            if (!(isfinite(d.x) && isfinite(d.y) && isfinite(d.z) && isfinite(d.w)))
+                for (int k = 0; k < 4; ++k)
+                    if (!isfinite(d_coeffs[4 * e + k])) flag(4 * e + k);
+        }
+        e = (nf / 4) * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    }
+    for (; e < nf; e += stride)
+        if (!isfinite(d_coeffs[e])) flag(e);
 }
 
 __global__ void k_sgd_update(int n, int K, float lr_mean, float lr_rot, float lr_scale, float lr_trans, float lr_rad,

@@ -168,7 +168,11 @@ class Geometry:
 # step of a scene (tile_max unknown); measured at 500k / 1M Gaussians:
 # bucket 382 / 761 us vs radix 270 / 477 us of binning
 BUCKET_MAX_LIST = 12288
+RFS_PCAP_EVICT = 0x10000  # include/rfsplat_b200.h
 _CAPS = {"hcap": 64, "pcap": 16, "m_cap": {}, "h_cap": {}, "used_cap": {},
+         # K6: a full pending ring keeps its smallest hits (RFS_PCAP_EVICT); turned
+         # on the first time a scene sends more than 0.1 % of the rays to the slow path
+         "ring_evict": False,
          # tile-key sort of the hand-written backend: "bucket" (per-tile buckets,
          # bucket.cu) or "radix" (global onesweep)
          "tile_sort": os.environ.get("RFS_TILE_SORT", "bucket"), "tile_max": {},
@@ -427,7 +431,7 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         ckeys, vals, ranges, lb = bin_tiles(m_cap, True, bucket)
 
     hc = 1 << max(0, math.ceil(math.log2(max(int(hcap or _CAPS["hcap"]), 1))))  # power of two: slot >> log2(hcap) = ray
-    pc = _CAPS["pcap"]
+    pc = _CAPS["pcap"] | (RFS_PCAP_EVICT if _CAPS["ring_evict"] else 0)
     if deferred is not None:
         return _geometry_deferred(scene, deferred, locals())
     ray_counts = torch.empty(R, dtype=torch.int32, device=dev)
@@ -513,8 +517,11 @@ def build_geometry(scene: DeviceScene, sort_backend: str = "hand", want_proj: bo
         if s[0] > 0:
             # rays whose pending ring overflowed: exact slow path, and a larger
             # ring for the next steps if it happens often
-            if s[0] > R // 1000 and pc < 64:
-                _CAPS["pcap"] = 2 * pc
+            if s[0] > R // 1000:  # keep the smallest hits of a full ring first, then grow it
+                if not _CAPS["ring_evict"]:
+                    _CAPS["ring_evict"] = True
+                elif _CAPS["pcap"] < 64:
+                    _CAPS["pcap"] = 2 * _CAPS["pcap"]
             join_early()
             pcap = max(int(s[4]), 1)
             nr = int(s[0])

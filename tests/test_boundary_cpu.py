@@ -102,3 +102,13 @@ def test_errors_are_the_reference_classes_when_installed():
     env = dict(os.environ, PYTHONPATH=os.pathsep.join(["/root/reference/pkg/src", REPO]),
                NUMBA_CACHE_DIR="/tmp/nb")
     subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+
+
+def test_pcap_evict_flag_matches_header():
+    """rfs_hits' ring flag: the header's value is the one the kernels and raster.py use."""
+    from paper_2502_01826_b200 import raster
+
+    hdr = re.search(r"#define RFS_PCAP_EVICT (0x[0-9a-fA-F]+)", open(HEADER).read())
+    common = re.search(r"#define RFS_PCAP_EVICT (0x[0-9a-fA-F]+)",
+                       open(os.path.join(REPO, "paper_2502_01826_b200", "csrc", "rfs_common.cuh")).read())
+    assert hdr and common and int(hdr.group(1), 16) == int(common.group(1), 16) == raster.RFS_PCAP_EVICT

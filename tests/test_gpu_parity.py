@@ -305,15 +305,21 @@ def test_full_ring_keeps_smallest_pending_hits():
         out = {}
         for pc in (16, 64):
             raster._CAPS["pcap"] = pc
+            raster._CAPS["ring_evict"] = True
             g = raster.build_geometry(ds, psi_tx=tx, forward=True)
             out[pc] = (g.S.cpu().numpy(), *_hit_lists(g), list(g.stats))
+        raster._CAPS["pcap"], raster._CAPS["ring_evict"] = 16, False  # without: the ring overflows
+        g = raster.build_geometry(ds, psi_tx=tx, forward=True)
+        out["plain"] = (g.S.cpu().numpy(), *_hit_lists(g), list(g.stats))
     finally:
         raster._CAPS.update(saved)
     st16, st64 = out[16][3], out[64][3]
     assert st16[5] == 16 and st64[5] > 16  # the small rings filled up
     assert st16[0] == 0, st16  # ... without sending a ray to the slow path
+    assert out["plain"][3][0] > 0.1 * 64800  # (a ring that does not keep them: the slow path)
     for i in range(3):
         np.testing.assert_array_equal(out[16][i], out[64][i])
+        np.testing.assert_array_equal(out["plain"][i], out[64][i])
     oc = oracle.OracleContext(s)
     np.testing.assert_array_equal(out[16][1], oc.live_counts().ravel())
 
