@@ -107,12 +107,12 @@ def load(require_cuda: bool = True):
 
 # kernels launched per entry-point call (sort: 2 + passes, added by raster.sort_pairs)
 KERNELS_PER_CALL = {
-    "rfs_project": 1, "rfs_exclusive_scan_u32": 1, "rfs_bin_fill": 1, "rfs_expand_keys": 1,
-    "rfs_tile_ranges": 1, "rfs_lower_bounds": 1, "rfs_bin_bucket": 7, "rfs_hits": 3, "rfs_hits_slow": 1, "rfs_psi": 1,
-    "rfs_forward": 1, "rfs_lam_transpose": 1, "rfs_bwd_gauss": 1, "rfs_bwd_rays": 1, "rfs_hit_keys": 1, "rfs_gauss_ranges": 1, "rfs_used_list": 1, "rfs_grad_geom": 0,
+    "rfs_project": 1, "rfs_exclusive_scan_u32": 2, "rfs_bin_fill": 1, "rfs_expand_keys": 1,
+    "rfs_tile_ranges": 1, "rfs_lower_bounds": 1, "rfs_bin_bucket": 8, "rfs_hits": 6, "rfs_hits_slow": 3, "rfs_psi": 1,
+    "rfs_forward": 1, "rfs_lam_transpose": 1, "rfs_bwd_gauss": 2, "rfs_bwd_rays": 1, "rfs_hit_keys": 1, "rfs_gauss_ranges": 2, "rfs_used_list": 1, "rfs_grad_geom": 0,
     "rfs_grad_tx": 1, "rfs_gather_sorted": 1,
-    "rfs_ray_dirs": 1, "rfs_spectrum_loss": 4, "rfs_frame_range": 1, "rfs_sgd_step": 2, "rfs_scalar_loss": 1, "rfs_density_flags": 1,
-    "rfs_density_apply": 1, "rfs_spectrum_dataset": 2, "rfs_scalar_dataset": 1,
+    "rfs_ray_dirs": 1, "rfs_spectrum_loss": 4, "rfs_frame_range": 1, "rfs_sgd_step": 3, "rfs_scalar_loss": 1, "rfs_density_flags": 1,
+    "rfs_density_apply": 1, "rfs_spectrum_dataset": 3, "rfs_scalar_dataset": 2,
 }
 launch_counter = {"kernels": 0}
 

@@ -457,7 +457,7 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
     const int nwarps = rfs_ceil_div(n_hits, BG_CHUNK);
     const unsigned grid = (unsigned)rfs_ceil_div(nwarps, BG_WARPS);
     if (n_tx % 64 == 0) {
-        RFS_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)n, st));
+        RFS_CUDA_TRY(rfs_fill_u32(cnt, 0u, (size_t)n, st));
 #define RFS_BV(NPV)                                                                                              \
     rfs_launch(k_bwd_gauss_v<NPV>, grid, BG_WARPS * 32, 0, st, n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,                   \
                                                        (const float2*)s_wt, (const float4*)psi,                  \

@@ -578,7 +578,7 @@ int rfs_bin_bucket(int n, const void* rects, const uint32_t* depth_code, int n_a
         rfs_launch(k_tile_count, nb, BK_BLK, 0, st, n, (const Rect*)rects, tiles_u, n_tiles, nb, tab);
         RFS_LAUNCH_CHECK();
     } else {
-        RFS_CUDA_TRY(cudaMemsetAsync(tab, 0, sizeof(uint32_t) * (size_t)n_tiles, st));
+        RFS_CUDA_TRY(rfs_fill_u32(tab, 0u, (size_t)n_tiles, st));
     }
     rfs_launch(k_tile_blockscan, rfs_ceil_div(n_tiles * 32, 128), 128, 0, st, nb, n_tiles, tab, tot);
     RFS_LAUNCH_CHECK();

@@ -327,7 +327,7 @@ int rfs_gather_sorted(const uint32_t* sorted_slots, int n_hits, const uint32_t* 
 int rfs_gauss_ranges(const uint64_t* sorted_g, int n_hits, const uint32_t* h_dev, int n, int* g_rng, void* stream) {
     if (n <= 0) return RFS_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    RFS_CUDA_TRY(cudaMemsetAsync(g_rng, 0, sizeof(int2) * (size_t)n, st));
+    RFS_CUDA_TRY(rfs_fill_u32(g_rng, 0u, 2 * (size_t)n, st));
     if (n_hits > 0)
         rfs_launch(k_gauss_ranges, rfs_ceil_div(n_hits, 256), 256, 0, st, sorted_g, n_hits, h_dev, (int2*)g_rng);
     RFS_LAUNCH_CHECK();

@@ -163,7 +163,7 @@ int rfs_spectrum_dataset(int n_samples, const double* tx, int n_paths, const voi
     if (n_samples <= 0) return RFS_OK;
     if (n_paths <= 0 || n_az <= 0 || n_el <= 0) return RFS_ERR_SHAPE;
     cudaStream_t st = (cudaStream_t)stream;
-    RFS_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), st));
+    RFS_CUDA_TRY(rfs_fill_u32(status, 0u, 1, st));
     const int np = n_samples * n_paths;
     rfs_launch(k_path_gain, rfs_ceil_div(np, 128), 128, 0, st, n_samples, n_paths, tx, (const PathRec*)paths, rx[0], rx[1],
                                                        rx[2], f_c, rolloff, n_az, n_el, (double2*)gain, (int2*)cell,
@@ -182,7 +182,7 @@ int rfs_scalar_dataset(int n_samples, const double* tx, int n_paths, const void*
     if (n_samples <= 0) return RFS_OK;
     if (n_paths <= 0 || (mode != 0 && mode != 1) || (mode == 1 && n_sub <= 0)) return RFS_ERR_SHAPE;
     cudaStream_t st = (cudaStream_t)stream;
-    RFS_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), st));
+    RFS_CUDA_TRY(rfs_fill_u32(status, 0u, 1, st));
     const int ns = mode == 0 ? 1 : n_sub;
     rfs_launch(k_scalar, rfs_ceil_div(n_samples * ns, 128), 128, 0, st, n_samples, n_paths, ns, mode, tx,
                                                                  (const PathRec*)paths, rx[0], rx[1], rx[2], f_c,

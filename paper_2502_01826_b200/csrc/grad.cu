@@ -508,7 +508,7 @@ int rfs_grad_geom(int n, int n_hits, const uint32_t* h_dev, const uint64_t* sort
     const int2* rg = (const int2*)g_rng;
     // acc64 rows / part_v slots are all written by k_geom_seg before k_geom_final
     // reads them (g_rng says which), so no clearing pass
-    if (stage & 1) RFS_CUDA_TRY(cudaMemsetAsync(long_list, 0, sizeof(int), st));  // the long-Gaussian count
+    if (stage & 1) RFS_CUDA_TRY(rfs_fill_u32(long_list, 0u, 1, st));  // the long-Gaussian count
     if ((stage & 1) && n_hits > 0)
         rfs_launch(k_geom_seg, rfs_ceil_div(n_hits, 256), 256, 0, st, n_hits, h_dev, sorted_g, s_ray, s_w, s_slot,
                    (const float4*)gs, (const RfsGeom*)geom, dirs, rg, rx[0], rx[1], rx[2], ress_radius, acc64, long_list,

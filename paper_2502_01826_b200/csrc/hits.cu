@@ -575,11 +575,11 @@ int rfs_hits(const int* ranges, int n_tiles, const uint32_t* vals, const double*
              int pcap, void* slab, int* counts, int* slow_list, int* stats, uint32_t* used, int n, int tile_lo,
              int tile_hi, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (used && n > 0) RFS_CUDA_TRY(cudaMemsetAsync(used, 0, sizeof(uint32_t) * (size_t)n, st));
+    if (used && n > 0) RFS_CUDA_TRY(rfs_fill_u32(used, 0u, (size_t)n, st));
     const int tiles_u = (n_az + RFS_TILE - 1) / RFS_TILE;
     const int R = n_az * n_el;
-    RFS_CUDA_TRY(cudaMemsetAsync(stats, 0, 16 * sizeof(int), st));
-    RFS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * (size_t)R, st));
+    RFS_CUDA_TRY(rfs_fill_u32(stats, 0u, 16, st));
+    RFS_CUDA_TRY(rfs_fill_u32(counts, 0u, (size_t)R, st));
     if (n_tiles <= 0) return RFS_OK;
     if (tile_hi < 0) tile_hi = n_tiles;  // default: every tile
     if (tile_lo < 0 || tile_lo > tile_hi || tile_hi > n_tiles) return RFS_ERR_SHAPE;
@@ -616,7 +616,7 @@ int rfs_hits_slow(const int* rays, int n_rays, const int* ranges, const uint32_t
         dirs, rx[0], rx[1], rx[2], ress_radius, n_az, n_el, tiles_u, hcap, (RfsHit*)slab, counts, pend_t, pend_g,
         pend_w, pcap, stats, used);
     if (used && n > 0) {  // the slow path marks more Gaussians: recount
-        RFS_CUDA_TRY(cudaMemsetAsync(stats + 8, 0, sizeof(int), (cudaStream_t)stream));
+        RFS_CUDA_TRY(rfs_fill_u32(stats + 8, 0u, 1, (cudaStream_t)stream));
         rfs_launch(k_count_used, min(rfs_ceil_div(n, 256), 148 * 4), 256, 0, (cudaStream_t)stream, used, n, stats);
     }
     RFS_LAUNCH_CHECK();

@@ -459,11 +459,11 @@ size_t rfs_scan_temp_elems(int n) { return 2 + 2 * ((size_t)rfs_ceil_div(n > 0 ?
 int rfs_exclusive_scan_u32(const uint32_t* in, int n, uint32_t* out, uint32_t* total, uint32_t* temp, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n <= 0) {
-        RFS_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(uint32_t), st));
+        RFS_CUDA_TRY(rfs_fill_u32(total, 0u, 1, st));
         return RFS_OK;
     }
     const int nb = rfs_ceil_div(n, SCAN_TILE);
-    RFS_CUDA_TRY(cudaMemsetAsync(temp, 0, rfs_scan_temp_elems(n) * sizeof(uint32_t), st));
+    RFS_CUDA_TRY(rfs_fill_u32(temp, 0u, rfs_scan_temp_elems(n), st));
     rfs_launch(k_scan_onepass, nb, SCAN_THREADS, 0, st, in, n, out, total, (unsigned int*)temp,
                                                 (unsigned long long*)(temp + 2));
     RFS_LAUNCH_CHECK();

@@ -310,7 +310,7 @@ int rfs_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint3
     uint32_t* hist = (uint32_t*)t;
     int* ctr = (int*)(t + (size_t)RS_MAX_PASSES * RS_MAX_RADIX * sizeof(uint32_t));
     uint32_t* lb = (uint32_t*)((unsigned char*)ctr + 64 * sizeof(int));
-    RFS_CUDA_TRY(cudaMemsetAsync(temp, 0, rfs_sort_temp_bytes(m, end_bit), st));
+    RFS_CUDA_TRY(rfs_fill_u32(temp, 0u, rfs_sort_temp_bytes(m, end_bit) / 4, st));
     int rc;
     switch (bits_for(end_bit)) {
         case 8: rc = run_sort<8>(keys, vals, keys_alt, vals_alt, m, passes, hist, lb, ctr, m_dev, st); break;

@@ -111,6 +111,23 @@ static inline cudaError_t rfs_launch(void (*kernel)(KArgs...), dim3 grid, dim3 b
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Fill n 32-bit words with v on the SMs.  Used instead of cudaMemsetAsync on
+// the step path: a memset node can go through a copy engine, where it waits
+// behind a concurrent bulk H2D copy (the training step's frames) and stalls
+// the stream; a kernel also keeps the programmatic-launch chain unbroken.
+namespace {
+__global__ void __launch_bounds__(256) k_fill_u32(uint32_t* __restrict__ p, uint32_t v, size_t n) {
+    rfs_pdl_wait();
+    for (size_t i = (size_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (size_t)gridDim.x * 256) p[i] = v;
+}
+}  // namespace
+static inline cudaError_t rfs_fill_u32(void* p, uint32_t v, size_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const size_t blocks = (n + 255) / 256;
+    return rfs_launch(k_fill_u32, dim3((unsigned)(blocks < 148 * 8 ? blocks : 148 * 8)), dim3(256), 0, st,
+                      (uint32_t*)p, v, n);
+}
+
 // K6 ray patches: warp q (0..7) of a 16 x 16 tile owns a 4 (u) x 8 (v) patch.
 // The patch cone (axis through the patch, half-angle covering its rays) as
 // k_hits computes it; called by a full warp.  ca = (cx, cy, cz, th_p),

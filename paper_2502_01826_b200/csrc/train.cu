@@ -269,7 +269,7 @@ int rfs_sgd_step(int n, int K, const float* lrs, float ema_decay, const float* d
                  void* coeffs, float* grad_ema, float* last_dmean, long long* bad, const long long* prior,
                  const float* lr_mean_dev, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    RFS_CUDA_TRY(cudaMemsetAsync(bad, 0x7f, sizeof(long long), st));  // sentinel 0x7f7f..7f = no bad row
+    RFS_CUDA_TRY(rfs_fill_u32(bad, 0x7f7f7f7fu, 2, st));  // sentinel 0x7f7f..7f = no bad row
     if (n <= 0) return RFS_OK;
     const int grid = rfs_ceil_div(n, 256);
     rfs_launch(k_sgd_check, grid, 256, 0, st, n, K, d_mean, d_quat, d_log_scale, d_trans_mag, d_trans_phase,

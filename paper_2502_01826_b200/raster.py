@@ -260,7 +260,7 @@ def sort_pairs(ckeys, vals, end_bit: int, backend: str = "hand", m_dev_ptr: int 
         temp = alloc(tag + "sort_temp", max(tb, 16), torch.uint8, dev)
         _native.call("rfs_sort_pairs_u64", _ptr(ckeys), _ptr(vals), _ptr(kalt), _ptr(valt), m, end_bit,
                      _ptr(temp), tb, _native.C.byref(res), m_dev_ptr, _stream())
-        _native.launch_counter["kernels"] += 2 + (end_bit + 7) // 8
+        _native.launch_counter["kernels"] += 3 + (end_bit + 7) // 8
     elif backend == "cub":
         if m_dev_ptr is not None:
             raise ValueError("the cub backend needs a host-side count")
@@ -871,7 +871,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
     _native.call("rfs_grad_geom", *geom_args, 1, st)  # K9a: per-hit sums, alongside K9b
     main.wait_stream(side)  # K9c adds K9b's bearing chain (dm_dir)
     _native.call("rfs_grad_geom", *geom_args, 2, st)  # K9c
-    _native.launch_counter["kernels"] += 3  # k_geom_seg, k_geom_span, k_geom_final
+    _native.launch_counter["kernels"] += 4  # fill, k_geom_seg, k_geom_span, k_geom_final
     _mark(marks, "grad_geom")
     return out
 
