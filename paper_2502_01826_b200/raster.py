@@ -597,8 +597,6 @@ def _geometry_deferred(scene, deferred: dict, L: dict) -> Geometry:
                  pc, _ptr(slab), _ptr(ray_counts), _ptr(slow), _ptr(stats), _ptr(used), n, L["t_lo"], L["t_hi"], st)
     ev_hits = torch.cuda.Event()
     ev_hits.record()
-    deferred["stats"].copy_(stats, non_blocking=True)
-    deferred["status"].copy_(L["status"], non_blocking=True)
     marks = L["marks"]
     _mark(marks, "hits")
     if psi is None:
@@ -618,7 +616,13 @@ def _geometry_deferred(scene, deferred: dict, L: dict) -> Geometry:
         gauss_index(geo, h_cap, _persistent, u_cap)
         ready = torch.cuda.Event()
         ready.record(side)
+        # the statistics for the validation after the step: off the main stream
+        # (psi and the composite do not wait for the copies), behind the index;
+        # the step joins the side stream before its last kernel
+        deferred["stats"].copy_(stats, non_blocking=True)
+        deferred["status"].copy_(L["status"], non_blocking=True)
     _keep(slab, side)
+    _keep(stats, side)
     _keep(ray_counts, side)
     _INDEX_GEN[0] += 1
     geo.gidx["ready"] = ready
