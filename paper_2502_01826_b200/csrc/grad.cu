@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
             }
         }
         float* dcf = reinterpret_cast<float*>(d_coeffs + (size_t)g * K);
-        if (g_rng[g].y > g_rng[g].x) {  // (always: a used Gaussian has hits)
+        {  // (a used Gaussian always has hits; no branch, so the shuffles below stay warp-converged)
         float vals[NG * 32];
 #pragma unroll
         for (int q = 0; q < NG * 32; ++q) vals[q] = 0.f;
@@ -418,15 +418,16 @@ __global__ void __launch_bounds__(GB_THREADS) k_grad_tx(
                     const int idx = l * l + l + m, ma = m < 0 ? -m : m;
                     const float rt = Fle<L>::ratio(l, m);
                     const float pv = rt * T.p[l][ma];
-                    vals[2 * idx] = fmaf(pv, q[m + L].x, vals[2 * idx]);
-                    vals[2 * idx + 1] = fmaf(pv, q[m + L].y, vals[2 * idx + 1]);
+                    // paired fp32 FMAs (FFMA2), the scalar form's operations
+                    const float2 v2 = __ffma2_rn(make_float2(pv, pv), q[m + L],
+                                                 make_float2(vals[2 * idx], vals[2 * idx + 1]));
+                    vals[2 * idx] = v2.x;
+                    vals[2 * idx + 1] = v2.y;
                     if (include_dir) {
                         const float2 cc = __ldg(&co[idx]);
                         const float dv = rt * T.dp[l][ma];
-                        A[m + L].x = fmaf(cc.x, pv, A[m + L].x);
-                        A[m + L].y = fmaf(cc.y, pv, A[m + L].y);
-                        Bm[m + L].x = fmaf(cc.x, dv, Bm[m + L].x);
-                        Bm[m + L].y = fmaf(cc.y, dv, Bm[m + L].y);
+                        A[m + L] = __ffma2_rn(cc, make_float2(pv, pv), A[m + L]);
+                        Bm[m + L] = __ffma2_rn(cc, make_float2(dv, dv), Bm[m + L]);
                     }
                 }
             }

@@ -1,5 +1,5 @@
 """Kernel timeline of the e2e training step (api.TrainStepGraph replays at
-config 2) from torch.profiler: per-stream busy time, the critical-path gaps
+config 2; MODE=step: the benched api.StepGraph) from torch.profiler: per-stream busy time, the critical-path gaps
 and the order of the kernels of one replay."""
 import json
 import os
@@ -25,7 +25,11 @@ txh = torch.as_tensor(txs, dtype=torch.float32).pin_memory()
 gth = gt.cpu().pin_memory()
 reph = torch.empty((B, 4), dtype=torch.float64).pin_memory()
 gb = parallel.GradBuffer(ds.n, ds.fle_degree, "cuda")
-tg = api.TrainStepGraph(ds, txh, gth, reph, gb)
+if os.environ.get("MODE", "train") == "step":  # the benched `value` step (api.StepGraph)
+    lamT = raster.transpose_upstream((geo.S * 1e-3).to(torch.complex64).contiguous())
+    tg = api.StepGraph(ds, tx, lamT, gb)
+else:
+    tg = api.TrainStepGraph(ds, txh, gth, reph, gb)
 for _ in range(5):
     tg.replay()
 torch.cuda.synchronize()
