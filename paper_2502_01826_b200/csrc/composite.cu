@@ -15,22 +15,30 @@
 namespace {
 
 // ------------------------------------------------------------------ K5: psi
-// block (64 TX, 4 Gaussians); a Gaussian's coefficient row is an L1 broadcast
-// used (nullable): Gaussians with at least one live hit (marked by K6); the
-// rows of the others are never read by K7 / K8c and are left unwritten.
+// A warp per group of 32 consecutive Gaussians: one coalesced load of their
+// `used` marks (nullable: all), then, Gaussian by Gaussian (warp-uniform),
+// lanes over the TX.  Only ~30 % of the Gaussians have live hits at config 2;
+// a thread per (Gaussian, TX) spent most of its blocks on an early exit.  The
+// rows of unused Gaussians are never read by K7 / K8c and are left unwritten.
 template <int L>
 __global__ void __launch_bounds__(256) k_psi(int n, int nb, const float* __restrict__ means,
                                              const float2* __restrict__ coeffs, const float* __restrict__ tx,
                                              const uint32_t* __restrict__ used, float2* __restrict__ psi) {
     rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-    const int b = blockIdx.y * 64 + threadIdx.x;
-    const int g = blockIdx.x * 4 + threadIdx.y;  // Gaussians on grid x (y is limited to 65535)
-    if (b >= nb || g >= n) return;
-    if (used && !used[g]) return;
-    float rx = tx[3 * b] - means[3 * g];
-    float ry = tx[3 * b + 1] - means[3 * g + 1];
-    float rz = tx[3 * b + 2] - means[3 * g + 2];
-    psi[(size_t)g * nb + b] = Fle<L>::psi(rx, ry, rz, coeffs + (size_t)g * Fle<L>::K);
+    const int lane = threadIdx.x & 31;
+    const int g0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+    if (g0 >= n) return;
+    const int g_l = g0 + lane;
+    unsigned todo = __ballot_sync(0xffffffffu, g_l < n && (!used || used[g_l] != 0u));
+    while (todo) {
+        const int g = g0 + __ffs(todo) - 1;
+        todo &= todo - 1;
+        const float mx = means[3 * g], my = means[3 * g + 1], mz = means[3 * g + 2];
+        const float2* c = coeffs + (size_t)g * Fle<L>::K;
+#pragma unroll 2
+        for (int b = lane; b < nb; b += 32)
+            psi[(size_t)g * nb + b] = Fle<L>::psi(tx[3 * b] - mx, tx[3 * b + 1] - my, tx[3 * b + 2] - mz, c);
+    }
 }
 
 // --------------------------------------------------------------- K7 forward
@@ -256,8 +264,7 @@ __global__ void k_gauss_ranges(const uint64_t* __restrict__ sorted_g, int h, con
 template <int L>
 void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, const uint32_t* used,
                 float2* psi, cudaStream_t st) {
-    dim3 grid(rfs_ceil_div(n, 4), rfs_ceil_div(nb, 64));
-    rfs_launch(k_psi<L>, grid, dim3(64, 4), 0, st, n, nb, means, coeffs, tx, used, psi);
+    rfs_launch(k_psi<L>, rfs_ceil_div(n, 256), 256, 0, st, n, nb, means, coeffs, tx, used, psi);
 }
 
 }  // namespace

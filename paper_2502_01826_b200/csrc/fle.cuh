@@ -100,8 +100,13 @@ struct Fle {
     __device__ static __forceinline__ float2 psi(float rx, float ry, float rz, const float2* __restrict__ c) {
         Tables T;
         tables(rx, ry, rz, T);
+        // acc += c_k b_k as paired fp32 FMAs (FFMA2): (re, im) += c.x (b.x, b.y) + c.y (-b.y, b.x)
         float2 acc = make_float2(0.f, 0.f);
-        for_each(T, [&](int idx, int, float2 b, float2) { acc = caddf(acc, cmulf(__ldg(&c[idx]), b)); });
+        for_each(T, [&](int idx, int, float2 b, float2) {
+            const float2 ck = __ldg(&c[idx]);
+            acc = __ffma2_rn(make_float2(ck.x, ck.x), b, acc);
+            acc = __ffma2_rn(make_float2(ck.y, ck.y), make_float2(-b.y, b.x), acc);
+        });
         return acc;
     }
 };
