@@ -179,8 +179,11 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
 // found from a ballot mask of the staged chunk, chunk-straddling from the
 // neighbouring keys; the next segment's psi row is prefetched while the
 // current one is reduced.
+#ifndef RFS_BG_MINB
+#define RFS_BG_MINB 8
+#endif
 template <int NP>
-__global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss_v(
+__global__ void __launch_bounds__(BG_WARPS * 32, RFS_BG_MINB) k_bwd_gauss_v(
     int h_tot, const uint32_t* __restrict__ h_dev, int nb, const uint64_t* __restrict__ sorted_g,
     const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const float4* __restrict__ psi,
     const float4* __restrict__ lamT, int accumulate, float2* __restrict__ C, float4* __restrict__ P,
