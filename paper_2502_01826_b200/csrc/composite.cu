@@ -96,7 +96,10 @@ __global__ void __launch_bounds__(CP_THREADS) k_forward(const RfsHit* __restrict
 constexpr int FV_U = RFS_FV_U;
 constexpr int FP_V = 32, FP_RAYS = FP_V;
 constexpr int FV_RPW = FP_RAYS / (CP_THREADS / 32);  // rays per warp
-__global__ void __launch_bounds__(CP_THREADS) k_forward_v(const RfsHit* __restrict__ slab,
+#ifndef RFS_FV_MINB
+#define RFS_FV_MINB 5  // 48 registers (a small spill): 5 blocks per SM measured fastest (51 vs 53 us at 1..4)
+#endif
+__global__ void __launch_bounds__(CP_THREADS, RFS_FV_MINB) k_forward_v(const RfsHit* __restrict__ slab,
                                                           const int* __restrict__ counts, int hcap,
                                                           const float4* __restrict__ psi, int nb, int n_az, int n_el,
                                                           float2* __restrict__ S) {

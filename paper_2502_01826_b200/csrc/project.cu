@@ -58,7 +58,10 @@ __device__ Rect splat_rect(double cu, double cv, double radius, int n_az, int n_
 // K1: one thread per Gaussian.  prepare_context's shape part (render.py:220-227,
 // scene.py:118-161), project_scene (splat.py:212-268) and the count pass of
 // expand_tile_rects (_kernels.py:532-541), all fp64.
-__global__ void __launch_bounds__(256) k_project(
+#ifndef RFS_PJ_MINB
+#define RFS_PJ_MINB 3  // 80 registers (spills a little): one wave of the grid, 20 -> 17 us
+#endif
+__global__ void __launch_bounds__(256, RFS_PJ_MINB) k_project(
     int n, const float* __restrict__ means, const float* __restrict__ quats,
     const float* __restrict__ log_scales, const float* __restrict__ raw, const float* __restrict__ phase,
     double rx0, double rx1, double rx2, double ress, int n_az, int n_el, int tiles_u,
