@@ -15,21 +15,24 @@
 namespace {
 
 // ------------------------------------------------------------------ K5: psi
-// A warp per group of 32 consecutive Gaussians: one coalesced load of their
+// A warp per group of PSI_G consecutive Gaussians: one coalesced load of their
 // `used` marks (nullable: all), then, Gaussian by Gaussian (warp-uniform),
 // lanes over the TX.  Only ~30 % of the Gaussians have live hits at config 2;
 // a thread per (Gaussian, TX) spent most of its blocks on an early exit.  The
 // rows of unused Gaussians are never read by K7 / K8c and are left unwritten.
+#ifndef PSI_G
+#define PSI_G 8  // Gaussians per warp: 8 -> 26 us, 16 -> 31, 32 -> 35 (more warps in flight)
+#endif
 template <int L>
 __global__ void __launch_bounds__(256) k_psi(int n, int nb, const float* __restrict__ means,
                                              const float2* __restrict__ coeffs, const float* __restrict__ tx,
                                              const uint32_t* __restrict__ used, float2* __restrict__ psi) {
     rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     const int lane = threadIdx.x & 31;
-    const int g0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+    const int g0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * PSI_G;
     if (g0 >= n) return;
     const int g_l = g0 + lane;
-    unsigned todo = __ballot_sync(0xffffffffu, g_l < n && (!used || used[g_l] != 0u));
+    unsigned todo = __ballot_sync(0xffffffffu, lane < PSI_G && g_l < n && (!used || used[g_l] != 0u));
     while (todo) {
         const int g = g0 + __ffs(todo) - 1;
         todo &= todo - 1;
@@ -267,7 +270,7 @@ __global__ void k_gauss_ranges(const uint64_t* __restrict__ sorted_g, int h, con
 template <int L>
 void launch_psi(int n, int nb, const float* means, const float2* coeffs, const float* tx, const uint32_t* used,
                 float2* psi, cudaStream_t st) {
-    rfs_launch(k_psi<L>, rfs_ceil_div(n, 256), 256, 0, st, n, nb, means, coeffs, tx, used, psi);
+    rfs_launch(k_psi<L>, rfs_ceil_div(n, 8 * PSI_G), 256, 0, st, n, nb, means, coeffs, tx, used, psi);
 }
 
 }  // namespace
