@@ -205,6 +205,14 @@ def run_ours(args):
                  "sphere_pass": geo.stats[6], "whitened_pass": geo.stats[7], "slow_rays": geo.stats[0]}
     R = geo.n_rays
     n_used = int(geo.used[: ds.n].sum().item())  # Gaussians with a live hit (rows K7 / K8 touch)
+
+    def hit_stats_after():
+        """K6 statistics of a geometry built after the timed steps, with the ring
+        size / eviction mode they ran with (the first geometry above starts cold)."""
+        g = raster.build_geometry(ds, sort_backend=args.sort)
+        return {"max_live": g.stats[2], "max_tile_list": g.stats[4], "max_pending": g.stats[5],
+                "sphere_pass": g.stats[6], "whitened_pass": g.stats[7], "slow_rays": g.stats[0],
+                "ring": raster._CAPS["pcap"], "ring_keeps_smallest": bool(raster._CAPS["ring_evict"])}
     del S0, P0
     # spectrum loss alone (not part of `value`, SURVEY.md §8(d)): timed separately
     from paper_2502_01826_b200 import loss as _loss
@@ -455,7 +463,7 @@ def run_ours(args):
                        "used_gaussians": n_used,
                        "upstream": "fixed synthetic lambda, given to the backward in the loss kernel's "
                                    "ray-major output layout (made once, outside the timed steps)",
-                       "sort": args.sort, "hit_stats": hit_stats,
+                       "sort": args.sort, "hit_stats": hit_stats_after(),
                        "parallelism": (f"tile-sharded x{world} (rays split by tiles, frames + grads all-reduced)"
                                        if args.strong else f"dp{world} (TX-sharded, grads all-reduced)"),
                        "l2": "flushed between steps (256 MB write)",
