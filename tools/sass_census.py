@@ -2,9 +2,9 @@
 under paper_2502_01826_b200/lib): per kernel, instruction count and the
 opcodes that show how the data moves (UBLKCP = cp.async.bulk, LDGSTS =
 cp.async, SYNCS = mbarrier, UTMALDG = TMA tensor load, LDS/STS, SHFL) and what
-computes (FFMA, DFMA/DMUL/DADD, MUFU).
+computes (FFMA, FFMA2 = paired fp32 FMA, DFMA/DMUL/DADD, MUFU).
 
-    python tools/sass_census.py > profiles/r2_sass_census.txt
+    python tools/sass_census.py > profiles/r2u_sass_census.txt
 """
 import collections
 import glob
@@ -13,7 +13,7 @@ import re
 import subprocess
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KEYS = ["UBLKCP", "LDGSTS", "SYNCS", "UTMALDG", "LDG", "STG", "LDS", "STS", "SHFL", "ATOMG", "RED", "FFMA", "FMUL",
+KEYS = ["UBLKCP", "LDGSTS", "SYNCS", "UTMALDG", "LDG", "STG", "LDS", "STS", "SHFL", "ATOMG", "RED", "FFMA", "FFMA2", "FMUL", "FMUL2",
         "DFMA", "DMUL", "DADD", "MUFU", "BAR", "WARPSYNC"]
 
 
