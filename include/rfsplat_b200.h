@@ -184,7 +184,7 @@ int rfs_gauss_ranges(const uint64_t* sorted_g, int n_hits, const uint32_t* h_dev
  *   conj(lam_b[ray]) psi[g][b] (complex64[R*hcap]; accumulate = 1 adds a
  *   further TX chunk) and P[g][b] = p_acc (complex64[N*B]; rows of Gaussians
  *   without hits are left unwritten).  part: complex64[rfs_bwd_part_elems(H,
- *   B)] and cnt (i32[N]) scratch.  B a multiple of 64 takes the 16-byte-vector
+ *   B)] and cnt (i32[N + 1]) scratch.  B a multiple of 64 takes the 16-byte-vector
  *   path, whose chunks complete straddling Gaussians themselves (last chunk
  *   to finish sums the partials in chunk order).
  * rfs_bwd_rays: per ray the suffix recursion A_k = w_{k+1} C_{k+1} +

@@ -20,7 +20,7 @@
 //                        lambda rows of its rays are gathered four hits at a
 //                        time.  Gaussians straddling chunks leave per-chunk
 //                        partial rows that
-//   K8f k_bwd_pfix       adds in chunk order.
+//   K8f k_bwd_pfix       adds (a block per straddling Gaussian, fixed order).
 //   K8r k_bwd_rays       one thread per ray, hits back to front: the suffix
 //                        recursion in fp64, then GW_k = Re(T_k C_k) (_kernels.py:387-388),
 //                        d|rho|_k = Re(T_k e^{j phi} A_k), d(phase)_k =
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
     int h_tot, const uint32_t* __restrict__ h_dev, int nb, const uint64_t* __restrict__ sorted_g,
     const uint32_t* __restrict__ s_slot, int hshift, const float2* __restrict__ s_wt, const int2* __restrict__ g_rng,
     const float2* __restrict__ psi, const float2* __restrict__ lamT, int accumulate, float2* __restrict__ C,
-    float2* __restrict__ P, float2* __restrict__ part) {
+    float2* __restrict__ P, float2* __restrict__ part, int* __restrict__ strad) {
     rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
     if (h_dev) h_tot = min(h_tot, (int)*h_dev);
     __shared__ uint32_t sh_g[BG_WARPS][BG_CHUNK];
@@ -165,6 +165,10 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_bwd_gauss(
                 const int b = lane + 32 * j;
                 if (b < nb) d2[b] = pa[j];
             }
+        }
+        if (lane == 0 && hs >= c0 && he > c1) {  // g starts here and straddles: list it for k_bwd_pfix
+            const int q = atomicAdd(strad, 1);
+            strad[1 + q] = g;
         }
         h = send;
     }
@@ -359,36 +363,39 @@ __global__ void __launch_bounds__(BG_WARPS * 32, RFS_BG_MINB) k_bwd_gauss_v(
     }
 }
 
-// Gaussians whose hits straddle chunks: the warp of the chunk where such a
-// Gaussian starts sums the chunk partials in chunk order (deterministic).
-__global__ void __launch_bounds__(256) k_bwd_pfix(int h_tot, const uint32_t* __restrict__ h_dev, int nb,
-                                                  const uint64_t* __restrict__ sorted_g,
+// Gaussians whose hits straddle chunks (listed by k_bwd_gauss, strad[0] =
+// count): a block per Gaussian sums its chunk partials (slot 2w0+1 of the
+// first chunk, slot 2v of the later ones).  Threads = (TX b, phase): phase p
+// adds the chunks w0 + p, w0 + p + PH, ... in order, then the PH phase sums
+// are added in phase order -- a fixed order (deterministic) with chains of
+// W / PH partials instead of W (a Gaussian crossed by thousands of rays at
+// 360x180 spans ~160 chunks).
+__global__ void __launch_bounds__(256) k_bwd_pfix(int nb, const int* __restrict__ strad,
                                                   const int2* __restrict__ g_rng, const float2* __restrict__ part,
                                                   float2* __restrict__ P) {
     rfs_pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-    if (h_dev) h_tot = min(h_tot, (int)*h_dev);
-    const int lane = threadIdx.x & 31;
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int c0 = w * BG_CHUNK;
-    if (c0 >= h_tot) return;
-    const int c1 = min(c0 + BG_CHUNK, h_tot);
-    if (c1 >= h_tot) return;
-    const uint64_t g = sorted_g[c1 - 1];
-    if (sorted_g[c1] != g) return;  // last segment ends inside the chunk
-    const int2 rg = g_rng[g];
-    if (rg.x < c0) return;          // started in an earlier chunk, handled there
-    const int w1 = (rg.y - 1) / BG_CHUNK;
-    // four chunk partials in flight per lane (fixed order: sequential in v)
-    for (int b = lane; b < nb; b += 32) {
-        float2 s = part[(size_t)(2 * w + 1) * nb + b];
-        int v = w + 1;
-        for (; v + 3 <= w1; v += 4) {
-            const float2 a0 = part[(size_t)(2 * v) * nb + b], a1 = part[(size_t)(2 * v + 2) * nb + b];
-            const float2 a2 = part[(size_t)(2 * v + 4) * nb + b], a3 = part[(size_t)(2 * v + 6) * nb + b];
-            s = caddf(caddf(caddf(caddf(s, a0), a1), a2), a3);
+    __shared__ float2 s_ph[256];
+    const int ph_n = max(1, 256 / nb);  // phases (nb <= 256)
+    const int t = threadIdx.x, b = t % nb, ph = t / nb;
+    const bool act = ph < ph_n;
+    const int nl = strad[0];
+    for (int i = blockIdx.x; i < nl; i += gridDim.x) {
+        const int g = strad[1 + i];
+        const int2 rg = g_rng[g];
+        const int w0 = rg.x / BG_CHUNK, w1 = (rg.y - 1) / BG_CHUNK;
+        float2 acc = make_float2(0.f, 0.f);
+        if (act) {
+            for (int v = w0 + ph; v <= w1; v += ph_n)
+                acc = caddf(acc, part[(size_t)(v == w0 ? 2 * w0 + 1 : 2 * v) * nb + b]);
+            s_ph[t] = acc;
         }
-        for (; v <= w1; ++v) s = caddf(s, part[(size_t)(2 * v) * nb + b]);
-        P[(size_t)g * nb + b] = s;
+        __syncthreads();
+        if (t < nb) {
+            float2 sum = s_ph[t];
+            for (int p = 1; p < ph_n; ++p) sum = caddf(sum, s_ph[p * nb + t]);
+            P[(size_t)g * nb + t] = sum;
+        }
+        __syncthreads();
     }
 }
 
@@ -475,18 +482,19 @@ int rfs_bwd_gauss(int n, int n_hits, const uint32_t* h_dev, int n_tx, const uint
 #undef RFS_BV
     } else {
         const int nj = (n_tx + 31) / 32;
+        RFS_CUDA_TRY(rfs_fill_u32(cnt, 0u, 1, st));  // the straddler list's count
 #define RFS_BG(NJV)                                                                                              \
     rfs_launch(k_bwd_gauss<NJV>, grid, BG_WARPS * 32, 0, st, n_hits, h_dev, n_tx, sorted_g, s_slot, hshift,             \
                                                      (const float2*)s_wt,                                        \
                                                      (const int2*)g_rng, (const float2*)psi, (const float2*)lamT, accumulate, \
-                                                     (float2*)C, (float2*)P, (float2*)part)
+                                                     (float2*)C, (float2*)P, (float2*)part, cnt)
         if (nj == 1) RFS_BG(1);
         else if (nj == 2) RFS_BG(2);
         else if (nj <= 4) RFS_BG(4);
         else RFS_BG(8);
 #undef RFS_BG
-        rfs_launch(k_bwd_pfix, rfs_ceil_div((long long)nwarps * 32, 256), 256, 0, st, n_hits, h_dev, n_tx, sorted_g, (const int2*)g_rng,
-                                                                              (const float2*)part, (float2*)P);
+        rfs_launch(k_bwd_pfix, 148 * 4, 256, 0, st, n_tx, (const int*)cnt, (const int2*)g_rng, (const float2*)part,
+                   (float2*)P);
     }
     RFS_LAUNCH_CHECK();
     return RFS_OK;

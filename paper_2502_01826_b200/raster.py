@@ -839,7 +839,7 @@ def backward(scene: DeviceScene, geo: Geometry, tx: torch.Tensor, grad_S: torch.
             _native.call("rfs_lam_transpose", _ptr(grad_S[c0:c1]), nbc, R, _ptr(lamTc), st)
         P = torch.empty((n, nbc), dtype=torch.complex64, device=dev)
         part = torch.empty(int(lib.rfs_bwd_part_elems(h, nbc)), dtype=torch.complex64, device=dev)
-        pcnt = torch.empty(max(n, 1), dtype=torch.int32, device=dev)  # straddle counts (zeroed in C)
+        pcnt = torch.empty(n + 1, dtype=torch.int32, device=dev)  # straddle counts / list (zeroed in C)
         _native.call("rfs_bwd_gauss", n, h, gi["h_dev"], nbc, _ptr(gi["sorted_g"]), _ptr(gi["s_slot"]), geo.hcap,
                      _ptr(gi["s_wt"]), _ptr(gi["g_rng"]), _ptr(psic), _ptr(lamTc), int(c0 > 0), _ptr(C), _ptr(P),
                      _ptr(part), _ptr(pcnt), st)

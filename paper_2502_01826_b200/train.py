@@ -220,7 +220,7 @@ class TraceRow:
 
 def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tensor, config: TrainConfig,
                batch: int = 1, seed: int = 0, timings: list | None = None, mode: str = "spectrum",
-               check_every: int = 50, group=None, graph: bool | None = None):
+               check_every: int = 50, group=None, graph: bool = False):
     """Batched counterpart of train.train_loop (train.py:284-361) on the device.
 
     Each iteration draws `batch` samples (TX position + measured target) with a
@@ -250,7 +250,9 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
     with the epilogue), so every rank applies the same update and takes the
     same densify / prune decisions (Philox children keyed by seed and
     iteration); the loss trace is summed over the ranks once at the end.
-    Captured iterations (`graph`, default: on for a single process): after
+    Captured iterations (`graph=True`, single process; for host-bound loops --
+    small grids or batches -- since each capture costs milliseconds and a
+    device-bound loop such as config 5 gains nothing from it): after
     one eager iteration at the current Gaussian count -- which sizes every
     capacity -- the iteration is captured as one CUDA graph and replayed: the
     samples and the learning rate are drawn up front and indexed on the
@@ -296,8 +298,6 @@ def train_loop(scene: raster.DeviceScene, txs: torch.Tensor, frames: torch.Tenso
 
     lo, hi = parallel.shard_bounds(batch, rank, world)
     iters = config.iterations
-    if graph is None:
-        graph = world == 1 and dev.type == "cuda"
     if graph and world > 1:
         raise ConfigError("captured iterations need a single process (graph=False under torch.distributed)")
     # the samples of every iteration (row it) and the learning-rate schedule, drawn up front

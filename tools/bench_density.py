@@ -25,7 +25,8 @@ from paper_2502_01826_b200.scene import cube_init, default_txs, round_to_f32
 ap = argparse.ArgumentParser()
 ap.add_argument("--iterations", type=int, default=600)
 ap.add_argument("--batch", type=int, default=16)
-ap.add_argument("--eager", action="store_true", help="no captured iterations (train_loop(graph=False))")
+ap.add_argument("--eager", action="store_true", help="no captured iterations (train_loop(graph=False), the default)")
+ap.add_argument("--graph", action="store_true", help="captured iterations (train_loop(graph=True))")
 ap.add_argument("--threshold", type=float, default=1e-7, help="densify_grad_threshold (lowered so it fires)")
 a = ap.parse_args()
 
@@ -47,13 +48,13 @@ train.densify(_w, _st, 1, cfg, 0)
 train.prune(_w, _st, 1, cfg)
 # and of the step itself (module loading, allocator pools, capacities) on another copy
 _w = raster.DeviceScene.from_host(s0, "cuda")
-train.train_loop(_w, txs, frames, train.TrainConfig(iterations=3), batch=a.batch, seed=2, graph=not a.eager)
+train.train_loop(_w, txs, frames, train.TrainConfig(iterations=3), batch=a.batch, seed=2, graph=a.graph and not a.eager)
 del _w, _st
 torch.cuda.synchronize()
 tim = []
 e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e_start.record()
-trace, dens, pr = train.train_loop(ds, txs, frames, cfg, batch=a.batch, seed=1, timings=tim, graph=not a.eager)
+trace, dens, pr = train.train_loop(ds, txs, frames, cfg, batch=a.batch, seed=1, timings=tim, graph=a.graph and not a.eager)
 e_end.record()
 torch.cuda.synchronize()
 total_ms = e_start.elapsed_time(e_end)
@@ -71,7 +72,7 @@ print(json.dumps({
                         for b in range(1, a.iterations + 1, 50)],
     "idle_between_iterations_ms": {"sum": round(float(gaps.sum()), 2), "median": round(float(np.median(gaps)), 3),
                                    "top": [[int(tim[i][0]), round(float(gaps[i]), 2)] for i in np.argsort(-gaps)[:8]]},
-    "captured": not a.eager, "loop_counts": train.train_loop.last_counts,
+    "captured": a.graph and not a.eager, "loop_counts": train.train_loop.last_counts,
     "density_events": events,
     "loss_first": round(float(np.mean([r.total for r in trace[:10]])), 6),
     "loss_last": round(float(np.mean([r.total for r in trace[-10:]])), 6),
