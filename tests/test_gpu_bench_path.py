@@ -122,10 +122,12 @@ def test_bench_step_config2_vs_oracle(B):
     _check(s, default_txs(B, seed=1))
 
 
-@pytest.mark.parametrize("B", [64, 128])
+@pytest.mark.parametrize("B", [16, 64, 128])
 def test_bench_step_straddling_gaussian_vs_oracle(B):
     """A Gaussian around the receiver: ~R hits on one Gaussian, spread over
-    hundreds of backward chunks, completed by the last-arriving chunk."""
+    hundreds of backward chunks, completed by the last-arriving chunk (B a
+    multiple of 64) or listed and summed by k_bwd_pfix (B = 16, the generic
+    kernel of small training batches); K9c's span kernel sums its groups."""
     s = _scene(20_000, 17, "huge")
     _check(s, default_txs(B, seed=4))
 
